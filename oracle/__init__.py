@@ -1,0 +1,390 @@
+"""CPU oracle for the SPUMA pressure path -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s cpu_baseline /
+``--impl reference`` legs may import this package.  The product
+(``paper_2512_22215_b200``) never imports it and shares no code with it; the
+only common dependency is the seeded input module ``gen``.
+
+This is a thin ctypes marshalling layer over ``oracle/oracle.c`` (plain
+single-threaded C, fp64, ``-O2 -ffp-contract=off``).  All arithmetic of the
+method lives in oracle.c; see its header for the paper citations per function
+(O1..O7) and DESIGN.md §3 for the readings.  Parity unpinned: normFactor (Q1)
+and loop/convergence semantics (Q2/Q3) are pinned only by special cases.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+from dataclasses import dataclass
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+import gen
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "liboracle.so")
+_SRC = os.path.join(_HERE, "oracle.c")
+_lock = threading.Lock()
+_lib = None
+
+ZERO_GRADIENT, FIXED_VALUE, EMPTY, PROCESSOR = gen.ZERO_GRADIENT, gen.FIXED_VALUE, gen.EMPTY, gen.PROCESSOR
+
+
+def build(force: bool = False) -> str:
+    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC):
+        tmp = _SO + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
+                               "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _SO)
+    return _SO
+
+
+class Controls(ctypes.Structure):
+    """SolverControls: tolerance, relTol, maxIter, minIter."""
+    _fields_ = [("tolerance", ctypes.c_double), ("rel_tol", ctypes.c_double),
+                ("max_iter", ctypes.c_int), ("min_iter", ctypes.c_int)]
+
+
+class Perf(ctypes.Structure):
+    _fields_ = [("initial_residual", ctypes.c_double), ("final_residual", ctypes.c_double),
+                ("n_iterations", ctypes.c_int), ("converged", ctypes.c_int), ("singular", ctypes.c_int)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class _Domain(ctypes.Structure):
+    _fields_ = [("n_cells", ctypes.c_int), ("n_faces", ctypes.c_int),
+                ("owner", ctypes.c_void_p), ("neighbour", ctypes.c_void_p),
+                ("diag", ctypes.c_void_p), ("upper", ctypes.c_void_p), ("source", ctypes.c_void_p),
+                ("psi", ctypes.c_void_p), ("n_iface", ctypes.c_int), ("iface_cells", ctypes.c_void_p),
+                ("iface_coeffs", ctypes.c_void_p), ("iface_src_domain", ctypes.c_void_p),
+                ("iface_src_cell", ctypes.c_void_p)]
+
+
+def _L():
+    global _lib
+    with _lock:
+        if _lib is None:
+            build()
+            lib = ctypes.CDLL(_SO)
+            vp, ci, cd = ctypes.c_void_p, ctypes.c_int, ctypes.c_double
+            lib.or_check_addressing.argtypes = [ci, ci, vp, vp]
+            lib.or_check_addressing.restype = ci
+            lib.or_owner_start.argtypes = [ci, ci, vp, vp]
+            lib.or_losort.argtypes = [ci, ci, vp, vp, vp]
+            lib.or_rcm.argtypes = [ci, ci, vp, vp, vp]
+            lib.or_rcm.restype = ci
+            lib.or_renumber_faces.argtypes = [ci, vp, vp, vp, vp, vp, vp, vp]
+            lib.or_geometry.argtypes = [ci] + [vp] * 8
+            lib.or_boundary_delta.argtypes = [ci] + [vp] * 6
+            lib.or_processor_geometry.argtypes = [ci] + [vp] * 9
+            lib.or_assemble.argtypes = [ci, ci] + [vp] * 6 + [ci] + [vp] * 8 + [ci, cd] + [vp] * 4
+            lib.or_amul.argtypes = [ci, ci] + [vp] * 6 + [ci] + [vp] * 4
+            lib.or_sumA.argtypes = [ci, ci] + [vp] * 5 + [ci] + [vp] * 3
+            lib.or_pcg.argtypes = [ci, ctypes.POINTER(_Domain), ctypes.POINTER(Controls), ctypes.POINTER(Perf)]
+            lib.or_pcg.restype = ci
+            lib.or_dense_from_ldu.argtypes = [ci, ci] + [vp] * 6
+            lib.or_dense_matvec.argtypes = [ci, vp, vp, vp]
+            lib.or_dense_solve.argtypes = [ci, vp, vp, vp]
+            lib.or_dense_solve.restype = ci
+            _lib = lib
+    return _lib
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data
+
+
+def _i32(a):
+    return np.ascontiguousarray(a, dtype=np.int32)
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+# --------------------------------------------------------------------------- O1
+def check_addressing(n_cells: int, owner, neighbour) -> int:
+    owner, neighbour = _i32(owner), _i32(neighbour)
+    return _L().or_check_addressing(n_cells, owner.shape[0], _p(owner), _p(neighbour))
+
+
+def owner_start(n_cells: int, owner) -> np.ndarray:
+    owner = _i32(owner)
+    out = np.empty(n_cells + 1, np.int32)
+    _L().or_owner_start(n_cells, owner.shape[0], _p(owner), _p(out))
+    return out
+
+
+def losort(n_cells: int, neighbour):
+    neighbour = _i32(neighbour)
+    lo = np.empty(neighbour.shape[0], np.int32)
+    ls = np.empty(n_cells + 1, np.int32)
+    _L().or_losort(n_cells, neighbour.shape[0], _p(neighbour), _p(lo), _p(ls))
+    return lo, ls
+
+
+# --------------------------------------------------------------------------- O2
+def rcm(n_cells: int, owner, neighbour) -> np.ndarray:
+    owner, neighbour = _i32(owner), _i32(neighbour)
+    perm = np.empty(n_cells, np.int32)
+    if _L().or_rcm(n_cells, owner.shape[0], _p(owner), _p(neighbour), _p(perm)):
+        raise MemoryError("or_rcm")
+    return perm
+
+
+def renumber_faces(perm, owner, neighbour):
+    perm, owner, neighbour = _i32(perm), _i32(owner), _i32(neighbour)
+    F = owner.shape[0]
+    o, n, fm = np.empty(F, np.int32), np.empty(F, np.int32), np.empty(F, np.int32)
+    fl = np.empty(F, np.int8)
+    _L().or_renumber_faces(F, _p(perm), _p(owner), _p(neighbour), _p(o), _p(n), _p(fm), _p(fl))
+    return o, n, fm, fl
+
+
+def renumber_mesh(mesh: gen.Mesh, perm) -> gen.Mesh:
+    """Apply O2's face re-keying to a whole mesh (cells moved by perm[old] = new)."""
+    o, n, fm, fl = renumber_faces(perm, mesh.owner, mesh.neighbour)
+    sgn = np.where(fl.astype(bool), -1.0, 1.0)[:, None]
+    inv = np.empty(mesh.n_cells, np.int64)
+    inv[perm] = np.arange(mesh.n_cells)
+    from dataclasses import replace
+    patches = [replace(p, face_cells=_i32(np.asarray(perm)[p.face_cells])) for p in mesh.patches]
+    return gen.Mesh(mesh.n_cells, o, n, np.ascontiguousarray(mesh.Sf[fm] * sgn), mesh.magSf[fm].copy(),
+                    mesh.Cf[fm].copy(), mesh.C[inv].copy(), mesh.V[inv].copy(), patches,
+                    gid=None if mesh.gid is None else mesh.gid[inv].copy(),
+                    gface=None if mesh.gface is None else mesh.gface[fm].copy(), dims=mesh.dims)
+
+
+# --------------------------------------------------------------------------- O3
+@dataclass
+class Geometry:
+    delta: np.ndarray  # [F]
+    weights: np.ndarray  # [F]
+    bdelta: np.ndarray  # [Fb] concatenated over patches (processor: global orientation)
+    bweight: np.ndarray  # [Fb] processor faces only (else 0)
+
+
+def geometry(mesh: gen.Mesh) -> Geometry:
+    lib = _L()
+    F = mesh.n_faces
+    delta, w = np.empty(F), np.empty(F)
+    Sf, magSf, C, Cf = _f64(mesh.Sf), _f64(mesh.magSf), _f64(mesh.C), _f64(mesh.Cf)
+    own, nbr = _i32(mesh.owner), _i32(mesh.neighbour)
+    lib.or_geometry(F, _p(own), _p(nbr), _p(Sf), _p(magSf), _p(C), _p(Cf), _p(delta), _p(w))
+    bd, bw = [], []
+    for p in mesh.patches:
+        n = p.n_faces
+        d, ww = np.zeros(n), np.zeros(n)
+        fc, pS, pm, pC = _i32(p.face_cells), _f64(p.Sf), _f64(p.magSf), _f64(p.Cf)
+        if p.kind == PROCESSOR:
+            nC, io = _f64(p.neighbour_C), np.ascontiguousarray(p.is_owner, dtype=np.int8)
+            lib.or_processor_geometry(n, _p(fc), _p(pS), _p(pm), _p(pC), _p(C), _p(nC), _p(io), _p(d), _p(ww))
+        elif p.kind != EMPTY:
+            lib.or_boundary_delta(n, _p(fc), _p(pS), _p(pm), _p(pC), _p(C), _p(d))
+        bd.append(d)
+        bw.append(ww)
+    cat = lambda xs: np.concatenate(xs) if xs else np.zeros(0)
+    return Geometry(delta, w, cat(bd), cat(bw))
+
+
+# --------------------------------------------------------------------------- O4
+@dataclass
+class LduSystem:
+    diag: np.ndarray
+    upper: np.ndarray  # lower == upper
+    source: np.ndarray
+    iface: List[np.ndarray]  # per processor patch (patch order), true entries A[P][remote]
+
+
+def _bcat(mesh, attr, dtype, default=0):
+    xs = []
+    for p in mesh.patches:
+        v = getattr(p, attr) if not callable(attr) else attr(p)
+        xs.append(np.full(p.n_faces, default, dtype) if v is None else np.asarray(v, dtype))
+    return np.ascontiguousarray(np.concatenate(xs) if xs else np.zeros(0, dtype), dtype=dtype)
+
+
+def assemble(mesh: gen.Mesh, gamma=None, ref_cell: int = -1, ref_value: float = 0.0, source=None,
+             geo: Optional[Geometry] = None, gamma_remote: Optional[Sequence[np.ndarray]] = None) -> LduSystem:
+    """fvm::laplacian(gamma, p) + setReference + boundary coefficients (O4).
+
+    gamma_remote: per processor patch, gamma of the remote cells (the gamma halo)."""
+    lib = _L()
+    geo = geo or geometry(mesh)
+    N, F = mesh.n_cells, mesh.n_faces
+    diag, upper = np.empty(N), np.empty(F)
+    src = np.zeros(N) if source is None else _f64(source).copy()
+    bkind = _i32(np.concatenate([np.full(p.n_faces, p.kind, np.int32) for p in mesh.patches]) if mesh.patches else np.zeros(0))
+    bcells = _bcat(mesh, "face_cells", np.int32)
+    bmag = _bcat(mesh, "magSf", np.float64)
+    bval = _bcat(mesh, "value", np.float64)
+    bown = _bcat(mesh, "is_owner", np.int8)
+    gr = []
+    k = 0
+    for p in mesh.patches:
+        if p.kind == PROCESSOR and gamma_remote is not None:
+            gr.append(np.asarray(gamma_remote[k], np.float64))
+            k += 1
+        else:
+            gr.append(np.zeros(p.n_faces))
+    bgr = _f64(np.concatenate(gr) if gr else np.zeros(0))
+    iface_all = np.zeros(bkind.shape[0])
+    g = None if gamma is None else _f64(gamma)
+    own, nbr, mag = _i32(mesh.owner), _i32(mesh.neighbour), _f64(mesh.magSf)
+    lib.or_assemble(N, F, _p(own), _p(nbr), _p(mag), _p(geo.delta),
+                    _p(geo.weights), _p(g), bkind.shape[0], _p(bkind), _p(bcells), _p(bmag), _p(geo.bdelta),
+                    _p(geo.bweight), _p(bval), _p(bgr), _p(bown), int(ref_cell), float(ref_value),
+                    _p(diag), _p(upper), _p(src), _p(iface_all))
+    iface, off = [], 0
+    for p in mesh.patches:
+        if p.kind == PROCESSOR:
+            iface.append(iface_all[off:off + p.n_faces].copy())
+        off += p.n_faces
+    return LduSystem(diag, upper, src, iface)
+
+
+def processor_patches(mesh: gen.Mesh):
+    return [p for p in mesh.patches if p.kind == PROCESSOR]
+
+
+# --------------------------------------------------------------------------- O5
+def amul(mesh: gen.Mesh, diag, upper, x, lower=None, iface=None, x_remote=None) -> np.ndarray:
+    lib = _L()
+    N = mesh.n_cells
+    y = np.empty(N)
+    lower = upper if lower is None else lower
+    ic, ico, xr = _iface_arrays(mesh, iface, x_remote)
+    a = [_i32(mesh.owner), _i32(mesh.neighbour), _f64(diag), _f64(lower), _f64(upper), _f64(x)]
+    lib.or_amul(N, mesh.n_faces, *[_p(v) for v in a], ic.shape[0], _p(ic), _p(ico), _p(xr), _p(y))
+    return y
+
+
+def sumA(mesh: gen.Mesh, diag, upper, lower=None, iface=None) -> np.ndarray:
+    lib = _L()
+    y = np.empty(mesh.n_cells)
+    lower = upper if lower is None else lower
+    ic, ico, _ = _iface_arrays(mesh, iface, None)
+    a = [_i32(mesh.owner), _i32(mesh.neighbour), _f64(diag), _f64(lower), _f64(upper)]
+    lib.or_sumA(mesh.n_cells, mesh.n_faces, *[_p(v) for v in a], ic.shape[0], _p(ic), _p(ico), _p(y))
+    return y
+
+
+def _iface_arrays(mesh, iface, x_remote):
+    pp = processor_patches(mesh)
+    if not pp or iface is None:
+        return np.zeros(0, np.int32), np.zeros(0), np.zeros(0)
+    ic = _i32(np.concatenate([p.face_cells for p in pp]))
+    ico = _f64(np.concatenate(iface))
+    xr = np.zeros(ic.shape[0]) if x_remote is None else _f64(np.concatenate(x_remote))
+    return ic, ico, xr
+
+
+# --------------------------------------------------------------------------- O6 / O8
+def controls(tolerance=1e-6, rel_tol=0.0, max_iter=5000, min_iter=0) -> Controls:
+    return Controls(tolerance, rel_tol, max_iter, min_iter)
+
+
+def pcg(mesh: gen.Mesh, sys: LduSystem, psi0=None, ctl: Optional[Controls] = None):
+    """Single-domain PCG + diagonal preconditioner. Returns (psi, perf dict)."""
+    psi, perf = pcg_decomposed([mesh], [sys], None if psi0 is None else [psi0], ctl)
+    return psi[0], perf
+
+
+def pcg_decomposed(meshes: Sequence[gen.Mesh], systems: Sequence[LduSystem], psi0=None,
+                   ctl: Optional[Controls] = None):
+    """O8: PCG over P sub-domains run sequentially; x_remote copied between
+    domains before every Amul; global sums in rank order."""
+    ctl = ctl or controls()
+    P = len(meshes)
+    keep = []
+    doms = (_Domain * P)()
+    psis = []
+    # gid -> (domain, local) lookup for interface sources
+    lut = {}
+    if P > 1:
+        for r, m in enumerate(meshes):
+            for loc, g in enumerate(m.gid):
+                lut[int(g)] = (r, loc)
+    for r, (m, s) in enumerate(zip(meshes, systems)):
+        psi = np.zeros(m.n_cells) if psi0 is None else _f64(psi0[r]).copy()
+        psis.append(psi)
+        pp = processor_patches(m)
+        if pp:
+            ic = _i32(np.concatenate([p.face_cells for p in pp]))
+            ico = _f64(np.concatenate(s.iface))
+            src = [lut[int(g)] for p in pp for g in p.neighbour_gid]
+            sd = _i32([a for a, _ in src])
+            sc = _i32([b for _, b in src])
+        else:
+            ic, ico, sd, sc = np.zeros(0, np.int32), np.zeros(0), np.zeros(0, np.int32), np.zeros(0, np.int32)
+        arrs = [_i32(m.owner), _i32(m.neighbour), _f64(s.diag), _f64(s.upper), _f64(s.source), ic, ico, sd, sc]
+        keep.append(arrs)
+        d = doms[r]
+        d.n_cells, d.n_faces = m.n_cells, m.n_faces
+        d.owner, d.neighbour, d.diag, d.upper, d.source = [_p(a) for a in arrs[:5]]
+        d.psi = _p(psi)
+        d.n_iface = ic.shape[0]
+        d.iface_cells, d.iface_coeffs, d.iface_src_domain, d.iface_src_cell = [_p(a) for a in arrs[5:]]
+    perf = Perf()
+    rc = _L().or_pcg(P, doms, ctypes.byref(ctl), ctypes.byref(perf))
+    if rc:
+        raise MemoryError("or_pcg")
+    return psis, perf.as_dict()
+
+
+def gamma_halo(meshes: Sequence[gen.Mesh], gammas: Sequence[np.ndarray]):
+    """Per domain, per processor patch: gamma of the remote cells (test plumbing)."""
+    lut = {}
+    for r, m in enumerate(meshes):
+        for loc, g in enumerate(m.gid):
+            lut[int(g)] = (r, loc)
+    out = []
+    for m in meshes:
+        out.append([np.array([gammas[lut[int(g)][0]][lut[int(g)][1]] for g in p.neighbour_gid])
+                    for p in processor_patches(m)])
+    return out
+
+
+# --------------------------------------------------------------------------- O7
+def dense_from_ldu(mesh_or_n, owner=None, neighbour=None, diag=None, upper=None, lower=None) -> np.ndarray:
+    if isinstance(mesh_or_n, gen.Mesh):
+        n, owner, neighbour = mesh_or_n.n_cells, mesh_or_n.owner, mesh_or_n.neighbour
+    else:
+        n = int(mesh_or_n)
+    lower = upper if lower is None else lower
+    A = np.empty((n, n))
+    owner, neighbour = _i32(owner), _i32(neighbour)
+    d, lo, up = _f64(diag), _f64(lower), _f64(upper)
+    _L().or_dense_from_ldu(n, owner.shape[0], _p(owner), _p(neighbour), _p(d), _p(lo), _p(up), _p(A))
+    return A
+
+
+def dense_matvec(A, x) -> np.ndarray:
+    A = _f64(A)
+    y = np.empty(A.shape[0])
+    x = _f64(x)
+    _L().or_dense_matvec(A.shape[0], _p(A), _p(x), _p(y))
+    return y
+
+
+def dense_solve(A, b) -> np.ndarray:
+    A = _f64(A)
+    x = np.empty(A.shape[0])
+    b = _f64(b)
+    if _L().or_dense_solve(A.shape[0], _p(A), _p(b), _p(x)):
+        raise np.linalg.LinAlgError("singular")
+    return x
+
+
+# --------------------------------------------------------------------------- convenience
+def solve_case(mesh: gen.Mesh, gamma=None, b=None, ref_cell: int = 0, ref_value: float = 0.0,
+               ctl: Optional[Controls] = None, psi0=None):
+    """Assembly (O3, O4) + PCG (O6) of one case; returns (psi, perf, system)."""
+    sys = assemble(mesh, gamma, ref_cell, ref_value, b)
+    psi, perf = pcg(mesh, sys, psi0, ctl)
+    return psi, perf, sys

@@ -1,0 +1,607 @@
+/*
+ * oracle/oracle.c -- the CPU ORACLE for the SPUMA pressure path (arXiv 2512.22215).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load or call this code.
+ * The product (paper_2512_22215_b200, libspuma) never links, imports or
+ * executes it, and this file shares no code, header, table or helper with it.
+ *
+ * Plain, slow, single-threaded, fp64, built with -O2 -ffp-contract=off (no FMA
+ * contraction, round-to-nearest-even).  Every function follows the OpenFOAM
+ * definitions the paper relies on ("SPUMA ... reproduces OpenFOAM-v2412",
+ * PAPER.md P:371) in their plain face-loop form; readings where the
+ * paper is silent are DESIGN.md §3 (Q1..Q16).
+ *
+ *   O1 addressing   or_check_addressing, or_owner_start, or_losort       P:82-83 (lduAddressing)
+ *   O2 renumbering  or_rcm, or_renumber_faces                            BASELINE.json "renumbered cells"; reading Q12
+ *   O3 geometry     or_geometry, or_boundary_delta, or_processor_geometry P:1133-1146 ("Gauss linear corrected", linear)
+ *   O4 assembly     or_assemble                                           P:736 "P assembly", P:520 negSumDiag
+ *   O5 Amul         or_amul, or_sumA                                      P:506 "SpMVM (Amul + Tmul)", P:519 sumA
+ *   O6 PCG          or_pcg (P >= 1 domains, O8 when P > 1)                P:961, P:1033-1041 (pcgDiag)
+ *   O7 dense        or_dense_from_ldu, or_dense_matvec, or_dense_solve    brute force for N <= 64
+ *
+ * Pins (tests/test_oracle_*.py, -m "not gpu"): SPEC chain examples,
+ * closed-form Poisson eigenmodes (Dirichlet / Neumann) and linear exactness,
+ * dense brute force, symmetry / zero-row-sum / Sigma diag invariants,
+ * decomposition invariance, A-norm monotonicity.
+ * Parity unpinned: the normFactor formula (Q1) and the convergence/loop
+ * semantics (Q2, Q3) are pinned only by special cases (init residual = 1 for
+ * psi0 = 0; exact start; minIter), not by any number the paper prints -- the
+ * paper prints no PCG iteration count, residual or matrix value for this path.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ------------------------------------------------------------------------- */
+/* O1 addressing ("the mesh data structure reflects the sparsity     */
+/* pattern of the matrix"; SPEC S:275-281 invariants)                         */
+/* ------------------------------------------------------------------------- */
+
+/* 0 = valid; 2 = addressing violation (index range, owner >= neighbour, order) */
+int or_check_addressing(int n_cells, int n_faces, const int* owner, const int* neighbour)
+{
+    for (int f = 0; f < n_faces; ++f) {
+        if (owner[f] < 0 || owner[f] >= n_cells || neighbour[f] < 0 || neighbour[f] >= n_cells) return 2;
+        if (!(owner[f] < neighbour[f])) return 2;
+        if (f > 0) {
+            if (owner[f] < owner[f - 1]) return 2;
+            if (owner[f] == owner[f - 1] && neighbour[f] < neighbour[f - 1]) return 2;
+        }
+    }
+    return 0;
+}
+
+/* ownerStart[c] = number of faces with owner < c (faces sorted by owner) */
+void or_owner_start(int n_cells, int n_faces, const int* owner, int* owner_start)
+{
+    for (int c = 0; c <= n_cells; ++c) {
+        int lo = 0, hi = n_faces; /* first face with owner >= c */
+        while (lo < hi) {
+            int mid = lo + (hi - lo) / 2;
+            if (owner[mid] < c) lo = mid + 1;
+            else hi = mid;
+        }
+        owner_start[c] = lo;
+    }
+}
+
+typedef struct { int key; int face; } or_pair;
+static int or_pair_cmp(const void* a, const void* b)
+{
+    const or_pair* x = (const or_pair*)a;
+    const or_pair* y = (const or_pair*)b;
+    if (x->key != y->key) return x->key < y->key ? -1 : 1;
+    return x->face < y->face ? -1 : (x->face > y->face);
+}
+
+/* losort = faces sorted by neighbour, ties by face index; losortStart[c] = #faces with neighbour < c */
+void or_losort(int n_cells, int n_faces, const int* neighbour, int* losort, int* losort_start)
+{
+    or_pair* p = (or_pair*)malloc(sizeof(or_pair) * (size_t)(n_faces > 0 ? n_faces : 1));
+    for (int f = 0; f < n_faces; ++f) {
+        p[f].key = neighbour[f];
+        p[f].face = f;
+    }
+    qsort(p, (size_t)n_faces, sizeof(or_pair), or_pair_cmp);
+    for (int k = 0; k < n_faces; ++k) losort[k] = p[k].face;
+    for (int c = 0; c <= n_cells; ++c) {
+        int lo = 0, hi = n_faces;
+        while (lo < hi) {
+            int mid = lo + (hi - lo) / 2;
+            if (p[mid].key < c) lo = mid + 1;
+            else hi = mid;
+        }
+        losort_start[c] = lo;
+    }
+    free(p);
+}
+
+/* ------------------------------------------------------------------------- */
+/* O2 reverse Cuthill-McKee with fixed tie-breaks (reading Q12)              */
+/* ------------------------------------------------------------------------- */
+
+static const int* or_rcm_deg;
+static int or_deg_cmp(const void* a, const void* b)
+{
+    int x = *(const int*)a, y = *(const int*)b;
+    if (or_rcm_deg[x] != or_rcm_deg[y]) return or_rcm_deg[x] < or_rcm_deg[y] ? -1 : 1;
+    return x < y ? -1 : (x > y);
+}
+
+/*
+ * perm[old] = new.  Graph = cells with internal faces as edges; deg(c) = number
+ * of internal faces of c.  Start at the unvisited cell of minimum degree (ties:
+ * smallest index), BFS with a FIFO queue; a dequeued cell enqueues its
+ * unvisited neighbours sorted by (deg, index).  Restart per component.
+ * Visit order k -> new[c_k] = N-1-k.
+ */
+int or_rcm(int n_cells, int n_faces, const int* owner, const int* neighbour, int* perm)
+{
+    int* deg = (int*)calloc((size_t)n_cells + 1, sizeof(int));
+    int* start = (int*)calloc((size_t)n_cells + 2, sizeof(int));
+    int* adj = (int*)malloc(sizeof(int) * (size_t)(2 * n_faces + 1));
+    int* fill = (int*)calloc((size_t)n_cells + 1, sizeof(int));
+    char* seen = (char*)calloc((size_t)n_cells + 1, 1);
+    int* queue = (int*)malloc(sizeof(int) * (size_t)(n_cells + 1));
+    int* cand = (int*)malloc(sizeof(int) * (size_t)(2 * n_faces + 1));
+    if (!deg || !start || !adj || !fill || !seen || !queue || !cand) return 6;
+    for (int f = 0; f < n_faces; ++f) {
+        deg[owner[f]]++;
+        deg[neighbour[f]]++;
+    }
+    for (int c = 0; c < n_cells; ++c) start[c + 1] = start[c] + deg[c];
+    for (int f = 0; f < n_faces; ++f) {
+        adj[start[owner[f]] + fill[owner[f]]++] = neighbour[f];
+        adj[start[neighbour[f]] + fill[neighbour[f]]++] = owner[f];
+    }
+    or_rcm_deg = deg;
+    int k = 0;
+    while (k < n_cells) {
+        int s = -1;
+        for (int c = 0; c < n_cells; ++c)
+            if (!seen[c] && (s < 0 || deg[c] < deg[s])) s = c;
+        int head = k, tail = k;
+        queue[tail++] = s;
+        seen[s] = 1;
+        while (head < tail) {
+            int c = queue[head++];
+            int nc = 0;
+            for (int e = start[c]; e < start[c + 1]; ++e) {
+                int d = adj[e];
+                if (!seen[d]) {
+                    seen[d] = 1; /* marks duplicates (several faces to one cell) once */
+                    cand[nc++] = d;
+                }
+            }
+            qsort(cand, (size_t)nc, sizeof(int), or_deg_cmp);
+            for (int i = 0; i < nc; ++i) queue[tail++] = cand[i];
+        }
+        k = tail;
+    }
+    for (int i = 0; i < n_cells; ++i) perm[queue[i]] = n_cells - 1 - i;
+    free(deg);
+    free(start);
+    free(adj);
+    free(fill);
+    free(seen);
+    free(queue);
+    free(cand);
+    return 0;
+}
+
+typedef struct { int o, n, f; } or_triple;
+static int or_triple_cmp(const void* a, const void* b)
+{
+    const or_triple* x = (const or_triple*)a;
+    const or_triple* y = (const or_triple*)b;
+    if (x->o != y->o) return x->o < y->o ? -1 : 1;
+    if (x->n != y->n) return x->n < y->n ? -1 : 1;
+    return x->f < y->f ? -1 : (x->f > y->f);
+}
+
+/*
+ * Re-key faces under perm[old] = new: (a, b) = (new[P], new[N]); owner = min,
+ * neighbour = max; flip[g] = 1 iff the pair swapped (Sf must be negated);
+ * faces re-sorted by (owner, neighbour), ties by old face index.
+ * face_map[new face] = old face.
+ */
+void or_renumber_faces(int n_faces, const int* perm, const int* owner, const int* neighbour, int* owner_out,
+                       int* neighbour_out, int* face_map, signed char* flip)
+{
+    or_triple* t = (or_triple*)malloc(sizeof(or_triple) * (size_t)(n_faces > 0 ? n_faces : 1));
+    for (int f = 0; f < n_faces; ++f) {
+        int a = perm[owner[f]], b = perm[neighbour[f]];
+        t[f].o = a < b ? a : b;
+        t[f].n = a < b ? b : a;
+        t[f].f = f;
+    }
+    qsort(t, (size_t)n_faces, sizeof(or_triple), or_triple_cmp);
+    for (int g = 0; g < n_faces; ++g) {
+        owner_out[g] = t[g].o;
+        neighbour_out[g] = t[g].n;
+        face_map[g] = t[g].f;
+        flip[g] = (signed char)(perm[owner[t[g].f]] > perm[neighbour[t[g].f]]);
+    }
+    free(t);
+}
+
+/* ------------------------------------------------------------------------- */
+/* O3 geometry: [OF] surfaceInterpolation::makeNonOrthDeltaCoeffs (the       */
+/* "stabilised form for bad meshes") and makeWeights; "Gauss linear          */
+/* corrected" laplacian, "linear" interpolation.  Reading Q6.  */
+/* ------------------------------------------------------------------------- */
+
+static void or_face_geometry(const double* CP, const double* CN, const double* S, double magS, const double* Cf,
+                             double* delta, double* weight)
+{
+    double d[3], nh[3];
+    for (int k = 0; k < 3; ++k) d[k] = CN[k] - CP[k];
+    for (int k = 0; k < 3; ++k) nh[k] = S[k] / magS;
+    double nd = nh[0] * d[0] + nh[1] * d[1] + nh[2] * d[2];
+    double magd = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+    double lim = 0.05 * magd;
+    *delta = 1.0 / (nd > lim ? nd : lim);
+
+    double eo[3], en[3];
+    for (int k = 0; k < 3; ++k) {
+        eo[k] = Cf[k] - CP[k];
+        en[k] = CN[k] - Cf[k];
+    }
+    double SfdOwn = fabs(S[0] * eo[0] + S[1] * eo[1] + S[2] * eo[2]);
+    double SfdNei = fabs(S[0] * en[0] + S[1] * en[1] + S[2] * en[2]);
+    double den = SfdOwn + SfdNei;
+    *weight = den > 1e-150 ? SfdNei / den : 0.5;
+}
+
+void or_geometry(int n_faces, const int* owner, const int* neighbour, const double* Sf, const double* magSf,
+                 const double* C, const double* Cf, double* delta, double* weights)
+{
+    for (int f = 0; f < n_faces; ++f)
+        or_face_geometry(C + 3 * owner[f], C + 3 * neighbour[f], Sf + 3 * f, magSf[f], Cf + 3 * f, delta + f,
+                         weights + f);
+}
+
+/* non-coupled patch face of cell P: delta_b = 1 / (nhat . (Cf - C_P)) */
+void or_boundary_delta(int n, const int* face_cells, const double* Sf, const double* magSf, const double* Cf,
+                       const double* C, double* delta)
+{
+    for (int i = 0; i < n; ++i) {
+        const double* cp = C + 3 * face_cells[i];
+        double nh[3], e[3];
+        for (int k = 0; k < 3; ++k) {
+            nh[k] = Sf[3 * i + k] / magSf[i];
+            e[k] = Cf[3 * i + k] - cp[k];
+        }
+        delta[i] = 1.0 / (nh[0] * e[0] + nh[1] * e[1] + nh[2] * e[2]);
+    }
+}
+
+/* processor face, evaluated in the GLOBAL orientation (reading O3 / Q9) */
+void or_processor_geometry(int n, const int* face_cells, const double* Sf_out, const double* magSf,
+                           const double* Cf, const double* C, const double* neighbour_C, const signed char* is_owner,
+                           double* delta, double* weights)
+{
+    for (int i = 0; i < n; ++i) {
+        double S[3];
+        const double *CP, *CN;
+        if (is_owner[i]) {
+            for (int k = 0; k < 3; ++k) S[k] = Sf_out[3 * i + k];
+            CP = C + 3 * face_cells[i];
+            CN = neighbour_C + 3 * i;
+        } else {
+            for (int k = 0; k < 3; ++k) S[k] = -Sf_out[3 * i + k];
+            CP = neighbour_C + 3 * i;
+            CN = C + 3 * face_cells[i];
+        }
+        or_face_geometry(CP, CN, S, magSf[i], Cf + 3 * i, delta + i, weights + i);
+    }
+}
+
+/* ------------------------------------------------------------------------- */
+/* O4 assembly of fvm::laplacian(gamma, p): [OF] gaussLaplacianScheme::      */
+/* fvmLaplacianUncorrected, lduMatrix::negSumDiag, fvMatrix::        */
+/* setReference (P:1083-1084 pRefCell/pRefValue), addBoundaryDiag,           */
+/* addBoundarySource.  Readings Q6, Q7, Q9, Q15.                             */
+/* ------------------------------------------------------------------------- */
+
+enum { OR_ZERO_GRADIENT = 0, OR_FIXED_VALUE = 1, OR_EMPTY = 2, OR_PROCESSOR = 3 };
+
+/*
+ * Boundary faces are given concatenated in patch order; per face:
+ *   bkind     patch kind
+ *   bcells    local owner cell
+ *   bmagSf    |S_b|
+ *   bdelta    delta_b (non-coupled) or delta_f in global orientation (processor)
+ *   bweight   processor only: global-orientation weight w
+ *   bvalue    fixedValue only: p_b
+ *   bgamma_r  processor only: gamma of the remote cell
+ *   bis_owner processor only: 1 if the local cell is the global owner
+ * iface receives, for processor faces only (in boundary order), the true matrix
+ * entry A[P][remote] = delta_f (gamma_f |S_f|)  (reading Q9); other slots untouched.
+ */
+void or_assemble(int n_cells, int n_faces, const int* owner, const int* neighbour, const double* magSf,
+                 const double* delta, const double* weights, const double* gamma, int n_bfaces, const int* bkind,
+                 const int* bcells, const double* bmagSf, const double* bdelta, const double* bweight,
+                 const double* bvalue, const double* bgamma_r, const signed char* bis_owner, int ref_cell,
+                 double ref_value, double* diag, double* upper, double* source, double* iface)
+{
+    /* 1-2: face coefficients, upper = deltaCoeffs * (gamma_f * magSf); lower aliases upper */
+    for (int f = 0; f < n_faces; ++f) {
+        double gf = 1.0;
+        if (gamma) gf = weights[f] * (gamma[owner[f]] - gamma[neighbour[f]]) + gamma[neighbour[f]];
+        upper[f] = delta[f] * (gf * magSf[f]);
+    }
+    /* 3: negSumDiag, face order: Diag[l] -= Lower; Diag[u] -= Upper */
+    for (int c = 0; c < n_cells; ++c) diag[c] = 0.0;
+    for (int f = 0; f < n_faces; ++f) {
+        diag[owner[f]] -= upper[f]; /* lower == upper */
+        diag[neighbour[f]] -= upper[f];
+    }
+    /* 4: setReference before any boundary coefficient */
+    if (ref_cell >= 0 && ref_cell < n_cells) {
+        source[ref_cell] += diag[ref_cell] * ref_value;
+        diag[ref_cell] += diag[ref_cell];
+    }
+    /* 5: boundary coefficients in (patch, face) order */
+    for (int i = 0; i < n_bfaces; ++i) {
+        int P = bcells[i];
+        double gP = gamma ? gamma[P] : 1.0;
+        if (bkind[i] == OR_FIXED_VALUE) {
+            double gms = gP * bmagSf[i];
+            diag[P] += gms * (-bdelta[i]);                   /* internalCoeffs = pGamma * (-delta)       */
+            source[P] += (-gms) * (bdelta[i] * bvalue[i]);  /* boundaryCoeffs = -pGamma * (delta * p_b) */
+        } else if (bkind[i] == OR_PROCESSOR) {
+            double gf = 1.0;
+            if (gamma) {
+                double gO = bis_owner[i] ? gP : bgamma_r[i];
+                double gN = bis_owner[i] ? bgamma_r[i] : gP;
+                gf = bweight[i] * (gO - gN) + gN;
+            }
+            double gms = gf * bmagSf[i];
+            diag[P] += gms * (-bdelta[i]);
+            iface[i] = bdelta[i] * gms;
+        }
+    }
+}
+
+/* ------------------------------------------------------------------------- */
+/* O5 Amul and sumA: plain face-loop   */
+/* scatter, then processor interfaces in order.                              */
+/* ------------------------------------------------------------------------- */
+
+void or_amul(int n_cells, int n_faces, const int* owner, const int* neighbour, const double* diag,
+             const double* lower, const double* upper, const double* x, int n_iface, const int* iface_cells,
+             const double* iface_coeffs, const double* x_remote, double* y)
+{
+    for (int c = 0; c < n_cells; ++c) y[c] = diag[c] * x[c];
+    for (int f = 0; f < n_faces; ++f) {
+        y[neighbour[f]] += lower[f] * x[owner[f]];
+        y[owner[f]] += upper[f] * x[neighbour[f]];
+    }
+    for (int i = 0; i < n_iface; ++i) y[iface_cells[i]] += iface_coeffs[i] * x_remote[i];
+}
+
+void or_sumA(int n_cells, int n_faces, const int* owner, const int* neighbour, const double* diag,
+             const double* lower, const double* upper, int n_iface, const int* iface_cells, const double* iface_coeffs,
+             double* sumA)
+{
+    for (int c = 0; c < n_cells; ++c) sumA[c] = diag[c];
+    for (int f = 0; f < n_faces; ++f) {
+        sumA[owner[f]] += lower[f];
+        sumA[neighbour[f]] += upper[f];
+    }
+    for (int i = 0; i < n_iface; ++i) sumA[iface_cells[i]] += iface_coeffs[i];
+}
+
+/* ------------------------------------------------------------------------- */
+/* O6 PCG + diagonal preconditioner ([OF] PCG::scalarSolve,                  */
+/* lduMatrix::solver::normFactor, SolverPerformance::checkConvergence /      */
+/* checkSingularity; controls P:1033-1041).  Readings Q1-Q5, Q11.            */
+/* P > 1 domains = O8 decomposed oracle: x_remote copied between domains     */
+/* before each Amul, global sums = per-domain sums added in rank order.      */
+/* ------------------------------------------------------------------------- */
+
+typedef struct {
+    int n_cells, n_faces;
+    const int* owner;
+    const int* neighbour;
+    const double* diag;
+    const double* upper; /* symmetric: lower == upper */
+    const double* source;
+    double* psi;
+    int n_iface;
+    const int* iface_cells;
+    const double* iface_coeffs;
+    const int* iface_src_domain; /* x_remote[i] = x of domain iface_src_domain[i] ... */
+    const int* iface_src_cell;   /* ... at its local cell iface_src_cell[i]           */
+} or_domain;
+
+typedef struct { double tolerance, rel_tol; int max_iter, min_iter; } or_controls;
+typedef struct { double initial_residual, final_residual; int n_iterations, converged, singular; } or_perf;
+
+typedef struct { double *wA, *rA, *pA, *rD, *xr, *sumA; } or_work;
+
+static int or_conv(double r, double init, const or_controls* c)
+{
+    return (r < c->tolerance) || (c->rel_tol > 1e-20 && r < c->rel_tol * init);
+}
+
+static void or_dom_amul(int nd, or_domain* D, or_work* W, double* const* x, double* const* y)
+{
+    for (int p = 0; p < nd; ++p)
+        for (int i = 0; i < D[p].n_iface; ++i) W[p].xr[i] = x[D[p].iface_src_domain[i]][D[p].iface_src_cell[i]];
+    for (int p = 0; p < nd; ++p)
+        or_amul(D[p].n_cells, D[p].n_faces, D[p].owner, D[p].neighbour, D[p].diag, D[p].upper, D[p].upper, x[p],
+                D[p].n_iface, D[p].iface_cells, D[p].iface_coeffs, W[p].xr, y[p]);
+}
+
+int or_pcg(int nd, or_domain* D, const or_controls* ctl, or_perf* perf)
+{
+    or_work* W = (or_work*)calloc((size_t)nd, sizeof(or_work));
+    double** X = (double**)malloc(sizeof(double*) * (size_t)nd);
+    double** Y = (double**)malloc(sizeof(double*) * (size_t)nd);
+    for (int p = 0; p < nd; ++p) {
+        size_t n = (size_t)D[p].n_cells + 1;
+        W[p].wA = (double*)calloc(n, sizeof(double));
+        W[p].rA = (double*)calloc(n, sizeof(double));
+        W[p].pA = (double*)calloc(n, sizeof(double));
+        W[p].rD = (double*)calloc(n, sizeof(double));
+        W[p].sumA = (double*)calloc(n, sizeof(double));
+        W[p].xr = (double*)calloc((size_t)D[p].n_iface + 1, sizeof(double));
+        if (!W[p].wA || !W[p].rA || !W[p].pA || !W[p].rD || !W[p].sumA || !W[p].xr) return 6;
+    }
+    perf->n_iterations = 0;
+    perf->converged = 0;
+    perf->singular = 0;
+
+    /* wA = A psi ; rA = source - wA */
+    for (int p = 0; p < nd; ++p) { X[p] = D[p].psi; Y[p] = W[p].wA; }
+    or_dom_amul(nd, D, W, X, Y);
+    for (int p = 0; p < nd; ++p)
+        for (int c = 0; c < D[p].n_cells; ++c) W[p].rA[c] = D[p].source[c] - W[p].wA[c];
+
+    /* normFactor = gSum(|wA - xRef| + |source - xRef|) + small, xRef = sumA * gAverage(psi) */
+    double spsi = 0.0, ncell = 0.0;
+    for (int p = 0; p < nd; ++p) {
+        double s = 0.0;
+        for (int c = 0; c < D[p].n_cells; ++c) s += D[p].psi[c];
+        spsi += s;
+        ncell += (double)D[p].n_cells;
+    }
+    double xbar = spsi / ncell;
+    double normFactor = 0.0;
+    for (int p = 0; p < nd; ++p) {
+        or_sumA(D[p].n_cells, D[p].n_faces, D[p].owner, D[p].neighbour, D[p].diag, D[p].upper, D[p].upper,
+                D[p].n_iface, D[p].iface_cells, D[p].iface_coeffs, W[p].sumA);
+        double s = 0.0;
+        for (int c = 0; c < D[p].n_cells; ++c) {
+            double xref = W[p].sumA[c] * xbar;
+            s += fabs(W[p].wA[c] - xref) + fabs(D[p].source[c] - xref);
+        }
+        normFactor += s;
+    }
+    normFactor += 1e-20;
+
+    double smag = 0.0;
+    for (int p = 0; p < nd; ++p) {
+        double s = 0.0;
+        for (int c = 0; c < D[p].n_cells; ++c) s += fabs(W[p].rA[c]);
+        smag += s;
+    }
+    perf->initial_residual = smag / normFactor;
+    perf->final_residual = perf->initial_residual;
+
+    for (int p = 0; p < nd; ++p)
+        for (int c = 0; c < D[p].n_cells; ++c) W[p].rD[c] = 1.0 / D[p].diag[c];
+
+    double wArA = 1e20, wArAold;
+    if (ctl->min_iter > 0 || !or_conv(perf->final_residual, perf->initial_residual, ctl)) {
+        do {
+            wArAold = wArA;
+            /* precondition wA = rD rA ; wArA = gSumProd(wA, rA) */
+            wArA = 0.0;
+            for (int p = 0; p < nd; ++p) {
+                double s = 0.0;
+                for (int c = 0; c < D[p].n_cells; ++c) {
+                    W[p].wA[c] = W[p].rD[c] * W[p].rA[c];
+                    s += W[p].wA[c] * W[p].rA[c];
+                }
+                wArA += s;
+            }
+            /* update search direction */
+            if (perf->n_iterations == 0) {
+                for (int p = 0; p < nd; ++p)
+                    for (int c = 0; c < D[p].n_cells; ++c) W[p].pA[c] = W[p].wA[c];
+            } else {
+                double beta = wArA / wArAold;
+                for (int p = 0; p < nd; ++p)
+                    for (int c = 0; c < D[p].n_cells; ++c) W[p].pA[c] = W[p].wA[c] + beta * W[p].pA[c];
+            }
+            /* wA = A pA ; wApA = gSumProd(wA, pA) */
+            for (int p = 0; p < nd; ++p) { X[p] = W[p].pA; Y[p] = W[p].wA; }
+            or_dom_amul(nd, D, W, X, Y);
+            double wApA = 0.0;
+            for (int p = 0; p < nd; ++p) {
+                double s = 0.0;
+                for (int c = 0; c < D[p].n_cells; ++c) s += W[p].wA[c] * W[p].pA[c];
+                wApA += s;
+            }
+            if (fabs(wApA) / normFactor < 1e-300) { /* checkSingularity: vSmall */
+                perf->singular = 1;
+                break;
+            }
+            double alpha = wArA / wApA;
+            smag = 0.0;
+            for (int p = 0; p < nd; ++p) {
+                double s = 0.0;
+                for (int c = 0; c < D[p].n_cells; ++c) {
+                    D[p].psi[c] += alpha * W[p].pA[c];
+                    W[p].rA[c] -= alpha * W[p].wA[c];
+                }
+                for (int c = 0; c < D[p].n_cells; ++c) s += fabs(W[p].rA[c]);
+                smag += s;
+            }
+            perf->final_residual = smag / normFactor;
+        } while ((++perf->n_iterations < ctl->max_iter && !or_conv(perf->final_residual, perf->initial_residual, ctl)) ||
+                 perf->n_iterations < ctl->min_iter);
+    }
+    perf->converged = or_conv(perf->final_residual, perf->initial_residual, ctl);
+
+    for (int p = 0; p < nd; ++p) {
+        free(W[p].wA);
+        free(W[p].rA);
+        free(W[p].pA);
+        free(W[p].rD);
+        free(W[p].sumA);
+        free(W[p].xr);
+    }
+    free(W);
+    free(X);
+    free(Y);
+    return 0;
+}
+
+/* ------------------------------------------------------------------------- */
+/* O7 dense brute force (N <= 64): entries (P,N) = upper, (N,P) = lower       */
+/* ------------------------------------------------------------------------- */
+
+void or_dense_from_ldu(int n, int n_faces, const int* owner, const int* neighbour, const double* diag,
+                       const double* lower, const double* upper, double* A)
+{
+    for (int i = 0; i < n * n; ++i) A[i] = 0.0;
+    for (int c = 0; c < n; ++c) A[c * n + c] = diag[c];
+    for (int f = 0; f < n_faces; ++f) {
+        A[owner[f] * n + neighbour[f]] += upper[f];
+        A[neighbour[f] * n + owner[f]] += lower[f];
+    }
+}
+
+void or_dense_matvec(int n, const double* A, const double* x, double* y)
+{
+    for (int i = 0; i < n; ++i) {
+        long double s = 0.0L;
+        for (int j = 0; j < n; ++j) s += (long double)A[i * n + j] * (long double)x[j];
+        y[i] = (double)s;
+    }
+}
+
+/* Gaussian elimination with partial pivoting in long double; 0 ok, 1 singular */
+int or_dense_solve(int n, const double* A, const double* b, double* x)
+{
+    long double* M = (long double*)malloc(sizeof(long double) * (size_t)n * (size_t)(n + 1));
+    for (int i = 0; i < n; ++i) {
+        for (int j = 0; j < n; ++j) M[i * (n + 1) + j] = A[i * n + j];
+        M[i * (n + 1) + n] = b[i];
+    }
+    for (int k = 0; k < n; ++k) {
+        int piv = k;
+        for (int i = k + 1; i < n; ++i)
+            if (fabsl(M[i * (n + 1) + k]) > fabsl(M[piv * (n + 1) + k])) piv = i;
+        if (M[piv * (n + 1) + k] == 0.0L) {
+            free(M);
+            return 1;
+        }
+        if (piv != k)
+            for (int j = 0; j <= n; ++j) {
+                long double t = M[k * (n + 1) + j];
+                M[k * (n + 1) + j] = M[piv * (n + 1) + j];
+                M[piv * (n + 1) + j] = t;
+            }
+        for (int i = k + 1; i < n; ++i) {
+            long double m = M[i * (n + 1) + k] / M[k * (n + 1) + k];
+            for (int j = k; j <= n; ++j) M[i * (n + 1) + j] -= m * M[k * (n + 1) + j];
+        }
+    }
+    long double* xs = (long double*)malloc(sizeof(long double) * (size_t)(n > 0 ? n : 1));
+    for (int i = n - 1; i >= 0; --i) {
+        long double s = M[i * (n + 1) + n];
+        for (int j = i + 1; j < n; ++j) s -= M[i * (n + 1) + j] * xs[j];
+        xs[i] = s / M[i * (n + 1) + i];
+    }
+    for (int i = 0; i < n; ++i) x[i] = (double)xs[i];
+    free(xs);
+    free(M);
+    return 0;
+}

@@ -1,0 +1,47 @@
+"""Case builders for tests (inputs only; no method arithmetic)."""
+import numpy as np
+
+import gen
+
+
+def small_random_mesh(nx=5, ny=5, nz=2, jitter=0.3, seed=11, permute=True):
+    """A perturbed, randomly permuted hex mesh (<= ~50 cells) for brute-force pins."""
+    m = gen.box(nx, ny, nz, (1.0, 1.0, 0.5), jitter=jitter, seed=seed)
+    if permute:
+        m = gen.permute(m, seed=seed + 100)
+    return m
+
+
+def dirichlet_box(nx, ny, nz, L=(1.0, 1.0, 1.0), walls=("xmin", "xmax", "ymin", "ymax", "zmin", "zmax"), empty=()):
+    m = gen.box(nx, ny, nz, L)
+    for p in m.patches:
+        if p.name in empty:
+            m = gen.set_kind(m, p.name, gen.EMPTY)
+        elif p.name in walls:
+            m = gen.set_kind(m, p.name, gen.FIXED_VALUE, np.zeros(p.n_faces))
+    return m
+
+
+def dense_ldu(n, owner, neighbour, diag, upper, lower=None):
+    """Dense matrix straight from the lduMatrix definition: numpy, independent of oracle.c."""
+    lower = upper if lower is None else lower
+    A = np.zeros((n, n))
+    A[np.arange(n), np.arange(n)] = diag
+    np.add.at(A, (np.asarray(owner), np.asarray(neighbour)), upper)
+    np.add.at(A, (np.asarray(neighbour), np.asarray(owner)), lower)
+    return A
+
+
+def lattice_modes(dims, ks, kind):
+    """Separable sin (Dirichlet) / cos (Neumann) modes on a lattice, cell id i + nx(j + ny k)."""
+    u = np.ones(1)
+    for n, k in zip(dims, ks):  # x fastest -> build with kron in reverse
+        i = np.arange(n)
+        f = np.sin(np.pi * k * (i + 0.5) / n) if kind == "sin" else np.cos(np.pi * k * (i + 0.5) / n)
+        u = np.kron(f, u)
+    return u
+
+
+def eigenvalue(dims, ks, coefs):
+    """lambda = -sum_d coef_d 4 sin^2(pi k_d / (2 n_d)) (ghost-mirror identity)."""
+    return -sum(c * 4.0 * np.sin(np.pi * k / (2.0 * n)) ** 2 for n, k, c in zip(dims, ks, coefs))

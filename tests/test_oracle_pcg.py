@@ -1,0 +1,203 @@
+"""Pins for oracle O6 (PCG + diagonal preconditioner).
+
+Controls: PAPER.md P:961, P:1033-1041 (pcgDiag); algorithm [OF] PCG::scalarSolve
+per readings Q1-Q5.  The paper prints no iteration count or
+residual for this path, so the pins are closed forms,
+dense brute force (P6), special cases (P7), A-norm monotonicity (P9) and the
+SPEC examples."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import gen
+import oracle as O
+from cases import dense_ldu, dirichlet_box, eigenvalue, lattice_modes, small_random_mesh
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+# --------------------------------------------------------------- P3 Dirichlet eigenmodes
+@pytest.mark.parametrize("tol,bound,iters", [(1e-6, 1e-6, None), (1e-9, 1e-9, None), (1e-12, 1e-12, None)])
+def test_p3_dirichlet_2d_sin_mode(tol, bound, iters):
+    n = 20
+    m = dirichlet_box(n, n, 1, (1.0, 1.0, 0.1), walls=("xmin", "xmax", "ymin", "ymax"), empty=("zmin", "zmax"))
+    s = O.assemble(m, None, -1)
+    u = lattice_modes((n, n), (3, 5), "sin")
+    lam = eigenvalue((n, n), (3, 5), (0.1, 0.1))  # coef = gamma |S| / h = (h dz) / h = dz
+    # the assembled matrix has u as an eigenvector (ghost-mirror identity)
+    assert np.max(np.abs(O.amul(m, s.diag, s.upper, u) - lam * u)) < 1e-14
+    psi, perf = O.pcg(m, O.LduSystem(s.diag, s.upper, lam * u, []), None, O.controls(tol, 0.0, 1000, 0))
+    assert perf["converged"] == 1 and perf["singular"] == 0
+    assert perf["final_residual"] < tol
+    assert rel(psi, u) < bound
+
+
+def test_p3_dirichlet_1d_and_3d():
+    n = 40
+    m = dirichlet_box(n, 1, 1, (1.0, 0.1, 0.1), walls=("xmin", "xmax"), empty=("ymin", "ymax", "zmin", "zmax"))
+    s = O.assemble(m, None, -1)
+    u = lattice_modes((n,), (7,), "sin")
+    lam = eigenvalue((n,), (7,), (0.01 * n,))  # |S| = 0.1 * 0.1, h = 1/n -> coef = |S|/h = 0.01 n
+    assert np.max(np.abs(O.amul(m, s.diag, s.upper, u) - lam * u)) < 1e-12
+    psi, perf = O.pcg(m, O.LduSystem(s.diag, s.upper, lam * u, []), None, O.controls(1e-12))
+    assert rel(psi, u) < 1e-11
+    n = 8
+    m = dirichlet_box(n, n, n)
+    s = O.assemble(m, None, -1)
+    ks = (1, 2, 3)
+    u = lattice_modes((n, n, n), ks, "sin")
+    lam = eigenvalue((n, n, n), ks, (1.0 / n,) * 3)  # |S| = h^2, coef = h
+    assert np.max(np.abs(O.amul(m, s.diag, s.upper, u) - lam * u)) < 1e-14
+    psi, perf = O.pcg(m, O.LduSystem(s.diag, s.upper, lam * u, []), None, O.controls(1e-12))
+    assert perf["converged"] and rel(psi, u) < 1e-11
+
+
+# --------------------------------------------------------------- P4 Neumann eigenmodes
+def test_p4_neumann_cos_mode_modulo_mean():
+    nx, ny = 16, 12
+    m = gen.box(nx, ny, 1, (1.0, 0.75, 0.1))
+    m = gen.set_kind(gen.set_kind(m, "zmin", gen.EMPTY), "zmax", gen.EMPTY)
+    s = O.assemble(m, None, -1)  # no reference: singular, consistent RHS
+    u = lattice_modes((nx, ny), (2, 3), "cos")
+    lam = eigenvalue((nx, ny), (2, 3), (0.1, 0.1))  # |S| = h dz, coef = dz (square cells)
+    assert np.max(np.abs(O.amul(m, s.diag, s.upper, u) - lam * u)) < 1e-14
+    psi, perf = O.pcg(m, O.LduSystem(s.diag, s.upper, lam * u, []), None, O.controls(1e-12))
+    assert perf["converged"]
+    assert rel(psi - psi.mean(), u - u.mean()) < 1e-10
+
+
+# --------------------------------------------------------------- P5 linear exactness
+def test_p5_linear_solution_is_exact():
+    n = 16
+    m = gen.box(n, n, 1, (1.0, 1.0, 0.0625))
+    m = gen.set_kind(m, "xmin", gen.FIXED_VALUE, np.zeros(n))
+    m = gen.set_kind(m, "xmax", gen.FIXED_VALUE, np.ones(n))
+    m = gen.set_kind(gen.set_kind(m, "zmin", gen.EMPTY), "zmax", gen.EMPTY)
+    s = O.assemble(m, None, -1)
+    xc = m.C[:, 0].copy()
+    assert np.all(O.amul(m, s.diag, s.upper, xc) - s.source == 0.0)
+    psi, perf = O.pcg(m, s, None, O.controls(1e-12))
+    assert perf["converged"] and np.max(np.abs(psi - xc)) < 1e-12
+
+
+# --------------------------------------------------------------- P6 dense brute force
+@pytest.mark.parametrize("seed", range(4))
+def test_p6_dense_brute_force(seed):
+    m = small_random_mesh(seed=seed)
+    assert m.n_cells <= 64
+    gamma = gen.gamma_lognormal(m)
+    b = gen.rhs(m)
+    if seed % 2:
+        m = gen.set_kind(m, "xmax", gen.FIXED_VALUE, np.linspace(0, 1, m.patches[1].n_faces))
+        s = O.assemble(m, gamma, -1, source=b)
+    else:
+        s = O.assemble(m, gamma, 0, 0.0, source=b)
+    A = dense_ldu(m.n_cells, m.owner, m.neighbour, s.diag, s.upper)
+    x_np = np.linalg.solve(A, s.source)
+    x_or = O.dense_solve(A, s.source)
+    assert rel(x_or, x_np) < 1e-12
+    psi, perf = O.pcg(m, s, None, O.controls(1e-14, 0.0, 1000, 0))
+    assert perf["converged"]
+    assert rel(psi, x_np) < 1e-10
+    assert perf["n_iterations"] <= m.n_cells + 10
+
+
+# --------------------------------------------------------------- P7 special cases
+def test_p7_identity_one_iteration():
+    g = json.load(open(os.path.join(GOLD, "spec_pcg_examples.json")))["identity"]
+    n = g["n"]
+    m = gen.Mesh(n, np.zeros(0, np.int32), np.zeros(0, np.int32), np.zeros((0, 3)), np.zeros(0), np.zeros((0, 3)),
+                 np.zeros((n, 3)), np.ones(n))
+    b = np.array(g["b"])
+    psi, perf = O.pcg(m, O.LduSystem(np.ones(n), np.zeros(0), b, []), None, O.controls(1e-9))
+    assert perf["n_iterations"] == g["max_iterations"] and perf["converged"]
+    assert np.array_equal(psi, b)
+
+
+def test_p7_exact_start_and_min_iter():
+    n = 5
+    m = gen.box(n, n, n, (float(n),) * 3)
+    s = O.assemble(m, None, 0, 0.0)
+    rng = np.random.default_rng(1)
+    x = rng.integers(-5, 6, m.n_cells).astype(float)
+    b = O.amul(m, s.diag, s.upper, x)  # integer arithmetic: exact
+    sysb = O.LduSystem(s.diag, s.upper, b, [])
+    psi, perf = O.pcg(m, sysb, x, O.controls(1e-9, 0.0, 100, 0))
+    assert perf["n_iterations"] == 0 and perf["initial_residual"] == 0.0 and perf["converged"]
+    assert np.array_equal(psi, x)
+    # minIter = 1 with a zero residual: the first iteration meets wApA = 0 -> singular, no update (Q3/Q4)
+    psi, perf = O.pcg(m, sysb, x, O.controls(1e-9, 0.0, 100, 1))
+    assert perf["singular"] == 1 and perf["n_iterations"] == 0 and np.array_equal(psi, x)
+    # round-off-level residual: minIter = 1 forces exactly one iteration
+    mm = small_random_mesh(seed=2)
+    ss = O.assemble(mm, gen.gamma_lognormal(mm), 0, 0.0, source=gen.rhs(mm))
+    xs = np.linalg.solve(dense_ldu(mm.n_cells, mm.owner, mm.neighbour, ss.diag, ss.upper), ss.source)
+    psi, perf = O.pcg(mm, ss, xs, O.controls(1e-6, 0.0, 100, 1))
+    assert perf["n_iterations"] == 1 and perf["converged"] and perf["initial_residual"] < 1e-12
+    psi, perf = O.pcg(mm, ss, xs, O.controls(1e-6, 0.0, 100, 0))
+    assert perf["n_iterations"] == 0
+
+
+def test_initial_residual_is_one_for_zero_start():
+    """Q1: psi0 = 0 -> xRef = 0, normFactor = sum|b| + 1e-20, initial residual = 1."""
+    m = small_random_mesh(seed=5)
+    s = O.assemble(m, gen.gamma_lognormal(m), 0, 0.0, source=gen.rhs(m) * 1e3)
+    _, perf = O.pcg(m, s, None, O.controls(1e-6))
+    assert perf["initial_residual"] == 1.0
+
+
+def test_normfactor_for_constant_start_on_neumann_matrix():
+    """Q1: psi0 = c with zero row sums: A psi0 = sumA c (both ~0) -> initial residual = sum|b|/sum|b| ~ 1."""
+    n = 4
+    m = gen.box(n, n, n, (float(n),) * 3)
+    s = O.assemble(m, None, -1, source=np.linspace(-1, 1, 64))
+    _, perf = O.pcg(m, s, np.full(64, 3.0), O.controls(1e-6, 0.0, 1, 1))
+    assert perf["initial_residual"] == 1.0
+
+
+# --------------------------------------------------------------- P9 A-norm monotonicity
+def test_p9_error_a_norm_non_increasing():
+    m = small_random_mesh(seed=7)
+    s = O.assemble(m, gen.gamma_lognormal(m), 0, 0.0, source=gen.rhs(m))
+    A = dense_ldu(m.n_cells, m.owner, m.neighbour, s.diag, s.upper)
+    xs = np.linalg.solve(A, s.source)
+    norms = []
+    for k in range(1, 30):
+        psi, perf = O.pcg(m, s, None, O.controls(0.0, 0.0, k, k))
+        e = xs - psi
+        norms.append(float(e @ (-A) @ e))  # -A is SPD for the Laplacian
+    assert all(b <= a * (1 + 1e-10) + 1e-28 for a, b in zip(norms, norms[1:]))
+    assert norms[-1] < 1e-6 * norms[0]
+
+
+# --------------------------------------------------------------- SPEC / paper controls
+def test_spec_poisson1d():
+    g = json.load(open(os.path.join(GOLD, "spec_pcg_examples.json")))["poisson1d"]
+    n = g["n"]
+    own = np.arange(n - 1, dtype=np.int32)
+    m = gen.Mesh(n, own, own + 1, np.zeros((n - 1, 3)), np.ones(n - 1), np.zeros((n - 1, 3)), np.zeros((n, 3)), np.ones(n))
+    diag = np.full(n, g["diag"])
+    up = np.full(n - 1, g["offdiag"])
+    b = np.ones(n)
+    psi, perf = O.pcg(m, O.LduSystem(diag, up, b, []), None, O.controls(g["tolerance"], 0.0, 1000, 0))
+    x = np.linalg.solve(dense_ldu(n, m.owner, m.neighbour, diag, up), b)
+    assert rel(psi, x) < g["dense_rel_err"]
+    assert perf["n_iterations"] <= g["max_iterations"]
+
+
+def test_paper_pcgdiag_controls_on_cavity():
+    c = json.load(open(os.path.join(GOLD, "pcgdiag_controls.json")))
+    m = gen.cavity2d(20)
+    psi, perf, s = O.solve_case(m, gen.gamma_lognormal(m), gen.rhs(m), 0, 0.0,
+                                O.controls(c["tolerance"], c["relTol"], c["maxIter"], c["minIter"]))
+    assert perf["converged"] and perf["n_iterations"] >= c["minIter"]
+    assert perf["final_residual"] < c["tolerance"] or perf["final_residual"] < c["relTol"] * perf["initial_residual"]
+    # the residual the solver reports is the normalised L1 residual of the returned psi (Q1)
+    r = s.source - O.amul(m, s.diag, s.upper, psi)
+    assert np.sum(np.abs(r)) / np.sum(np.abs(s.source)) == pytest.approx(perf["final_residual"], rel=1e-6)
