@@ -1,0 +1,39 @@
+"""Mutation sanity check for the oracle pins: each plausible mistake (dropped term, wrong sign,
+wrong index, transposed operand) injected into oracle.c must fail at least one -m "not gpu" test.
+Restores oracle.c at the end.  Run: python scripts/oracle_mutation_check.py"""
+import subprocess, sys
+import os
+os.chdir(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+src = open('oracle/oracle.c').read()
+muts = [
+ ("diag[neighbour[f]] -= upper[f];", "/*dropped*/"),
+ ("source[P] += (-gms) * (bdelta[i] * bvalue[i]);", "source[P] += (gms) * (bdelta[i] * bvalue[i]);"),
+ ("diag[ref_cell] += diag[ref_cell];", ";"),
+ ("*weight = den > 1e-150 ? SfdNei / den : 0.5;", "*weight = den > 1e-150 ? SfdOwn / den : 0.5;"),
+ ("double beta = wArA / wArAold;", "double beta = wArAold / wArA;"),
+ ("W[p].rA[c] -= alpha * W[p].wA[c];", "W[p].rA[c] += alpha * W[p].wA[c];"),
+ ("s += fabs(W[p].wA[c] - xref) + fabs(D[p].source[c] - xref);", "s += fabs(W[p].wA[c] - xref);"),
+ ("y[iface_cells[i]] += iface_coeffs[i] * x_remote[i];", "y[iface_cells[i]] += iface_coeffs[i] * x[iface_cells[i]];"),
+ ("perm[queue[i]] = n_cells - 1 - i;", "perm[queue[i]] = i;"),
+ ("return x->face < y->face ? -1 : (x->face > y->face);", "return x->face > y->face ? -1 : (x->face < y->face);"),
+ ("for (int k = 0; k < 3; ++k) S[k] = -Sf_out[3 * i + k];", "for (int k = 0; k < 3; ++k) S[k] = Sf_out[3 * i + k];"),
+ ("double lim = 0.05 * magd;", "double lim = 0.5 * magd;"),
+ ("return (r < c->tolerance) || (c->rel_tol > 1e-20 && r < c->rel_tol * init);", "return (r < c->tolerance);"),
+
+ ("diag[P] += gms * (-bdelta[i]);                   /* internalCoeffs", "diag[P] += gms * (-0.5*bdelta[i]);                   /* internalCoeffs"),
+ ("gf = weights[f] * (gamma[owner[f]] - gamma[neighbour[f]]) + gamma[neighbour[f]];", "gf = weights[f] * (gamma[neighbour[f]] - gamma[owner[f]]) + gamma[owner[f]];"),
+ ("if (fabs(wApA) / normFactor < 1e-300) {", "if (fabs(wApA) / normFactor < -1.0) {"),
+ ("for (int c = 0; c < D[p].n_cells; ++c) W[p].rD[c] = 1.0 / D[p].diag[c];", "for (int c = 0; c < D[p].n_cells; ++c) W[p].rD[c] = 1.0;"),
+ ("delta[i] = 1.0 / (nh[0] * e[0] + nh[1] * e[1] + nh[2] * e[2]);", "delta[i] = 1.0 / (nh[0] * e[0] + nh[1] * e[1] + nh[2] * e[2]) / 2;"),
+]
+res = []
+for a, b in muts:
+    assert a in src, a
+    open('oracle/oracle.c', 'w').write(src.replace(a, b))
+    r = subprocess.run([sys.executable, '-m', 'pytest', 'tests', '-x', '-q', '-m', 'not gpu'], capture_output=True, text=True)
+    caught = r.returncode != 0
+    line = [l for l in r.stdout.splitlines() if l.startswith('FAILED')][:1]
+    res.append((caught, a[:60], line))
+    print(caught, a[:70], line, flush=True)
+open('oracle/oracle.c', 'w').write(src)
+print('ALL CAUGHT' if all(c for c, *_ in res) else 'SOME MISSED')

@@ -201,3 +201,64 @@ def test_paper_pcgdiag_controls_on_cavity():
     # the residual the solver reports is the normalised L1 residual of the returned psi (Q1)
     r = s.source - O.amul(m, s.diag, s.upper, psi)
     assert np.sum(np.abs(r)) / np.sum(np.abs(s.source)) == pytest.approx(perf["final_residual"], rel=1e-6)
+
+
+def test_jacobi_preconditioner_solves_diagonal_matrix_in_one_iteration():
+    """diag-only A with distinct entries: diagonal-preconditioned CG is exact after 1 step
+    (plain CG would need one step per distinct eigenvalue)."""
+    n = 5
+    m = gen.Mesh(n, np.zeros(0, np.int32), np.zeros(0, np.int32), np.zeros((0, 3)), np.zeros(0), np.zeros((0, 3)),
+                 np.zeros((n, 3)), np.ones(n))
+    d = np.array([-1.0, -2.0, -4.0, -8.0, -16.0])
+    b = np.array([1.0, 3.0, -2.0, 0.5, 8.0])
+    psi, perf = O.pcg(m, O.LduSystem(d, np.zeros(0), b, []), None, O.controls(1e-12))
+    assert perf["n_iterations"] == 1 and np.array_equal(psi, b / d)
+
+
+def _textbook_pcg(A, b, k):
+    """Textbook Jacobi-preconditioned CG (Hestenes-Stiefel), dense numpy, x0 = 0: k-th iterate."""
+    Minv = 1.0 / np.diag(A)
+    x = np.zeros_like(b)
+    r = b.copy()
+    z = Minv * r
+    p = z.copy()
+    rz = r @ z
+    for _ in range(k):
+        Ap = A @ p
+        a = rz / (p @ Ap)
+        x = x + a * p
+        r = r - a * Ap
+        z = Minv * r
+        rz_new = r @ z
+        p = z + (rz_new / rz) * p
+        rz = rz_new
+    return x
+
+
+@pytest.mark.parametrize("seed", [0, 3])
+def test_iterates_match_textbook_pcg(seed):
+    """Every iterate (not just the limit) equals the textbook Jacobi-PCG iterate:
+    pins alpha, beta, the preconditioner and the update order."""
+    m = small_random_mesh(seed=seed)
+    s = O.assemble(m, gen.gamma_lognormal(m), 0, 0.0, source=gen.rhs(m))
+    A = dense_ldu(m.n_cells, m.owner, m.neighbour, s.diag, s.upper)
+    for k in (1, 2, 3, 5, 8, 12):
+        psi, perf = O.pcg(m, s, None, O.controls(0.0, 0.0, k, k))
+        ref = _textbook_pcg(A, s.source, k)
+        assert perf["n_iterations"] == k
+        assert rel(psi, ref) < 1e-10
+
+
+def test_rel_tol_stops_at_first_iteration_below_it():
+    """Q2/Q3: converged = r < tol || (relTol > 1e-20 && r < relTol * init); the loop stops at the
+    first iteration that meets it."""
+    m = gen.cavity2d(20)
+    gamma, b = gen.gamma_lognormal(m), gen.rhs(m)
+    psi, perf, s = O.solve_case(m, gamma, b, 0, 0.0, O.controls(1e-9, 1e-3, 3000, 0))
+    n = perf["n_iterations"]
+    assert perf["final_residual"] < 1e-3 * perf["initial_residual"] and perf["final_residual"] >= 1e-9
+    _, p2, _ = O.solve_case(m, gamma, b, 0, 0.0, O.controls(1e-9, 1e-3, n - 1, 0))
+    assert p2["n_iterations"] == n - 1 and not p2["converged"]
+    assert p2["final_residual"] >= 1e-3 * p2["initial_residual"]
+    _, p3, _ = O.solve_case(m, gamma, b, 0, 0.0, O.controls(1e-9, 0.0, 3000, 0))
+    assert p3["n_iterations"] > n and p3["final_residual"] < 1e-9
