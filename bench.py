@@ -1,0 +1,345 @@
+#!/usr/bin/env python
+"""Benchmark: pressure PCG cells*iter/s and HBM GB/s (% of peak) -- BASELINE.json metric.
+
+Workload (config.workload): BASELINE config 3, the 3-D cavity/cube with 200^3
+cells PER GPU (8M cells, 23.88M internal faces), weak scaling over
+1/2/4/8 GPUs (N = 1: one 200^3 cube).  Synthetic, seeded inputs
+(gen/: unit-cube lattice, six zeroGradient walls, gamma = 1, b = V(2U-1)
+minus its mean, reference cell 0, psi0 = 0); solve to 1e-6 (reading Q5:
+tolerance 1e-6 on the normalised residual, relTol 0, minIter 0, maxIter 5000).
+
+One step = the whole hot path on one batch of input: assemble the Laplacian
+(A4-A5: face coefficients + diagonal gather + reference) and solve it (A6
+setup + A7-A11 iterations to convergence + A12).  value = global cells *
+PCG iterations / step time (max over ranks).  Inputs (8M cells, ~1.3 GB per
+iteration) are far larger than the 126 MB L2, so no L2 flush is needed.
+
+Also reported: roofline of the dominant kernel (the Amul, A7), timed live
+with CUDA events over the timed region; e2e through the C-ABI with host
+buffers; clocks under load; our kernel launch count; and the CPU oracle
+(cpu_baseline) on a bounded sample of the same workload.
+
+--impl reference: the oracle (plain single-threaded C) timed on the host as
+the reference arm (this tier has no reference implementation to install).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "pressure PCG cells·iter/s and HBM GB/s (% of peak) at 1/2/4/8 B200"
+UNIT = "cells*iter/s"
+TOL = (1e-6, 0.0, 5000, 0)
+
+
+def env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            j = json.load(f)
+        return float(j["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def algorithmic_bytes(N, F):
+    """per PCG iteration, fused minimum. Phase A (Amul + dot): 24 B/cell + 16 B/face;
+    B (update + dots): 56 B/cell; C (direction): 32 B/cell."""
+    return {"A": 24 * N + 16 * F, "B": 56 * N, "C": 32 * N, "iter": 112 * N + 16 * F}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except (FileNotFoundError, OSError):
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        mhz, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                mhz.append(float(r[1]))
+                mx = float(r[2])
+                for n, v in zip(names, r[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(n)
+            except (ValueError, IndexError):
+                continue
+        if not mhz:
+            return None
+        return {"sm_mhz": statistics.median(mhz), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(mhz)}
+
+
+def load_traffic(workload):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    try:
+        with open(p) as f:
+            j = json.load(f)
+        if j.get("workload") == workload:
+            return j.get("amul_dram_bytes_per_launch")
+    except (OSError, ValueError):
+        pass
+    return None
+
+
+# ---------------------------------------------------------------------------- workload
+def build_workload(n, rank, world):
+    import gen
+    if world == 1:
+        m = gen.cube(n)
+        b = gen.rhs(m)
+        return m, b, 0, {"workload": f"C3 cube {n}^3 per GPU (weak), gamma=1, tol 1e-6", "cells_per_gpu": n ** 3}
+    raise NotImplementedError("multi-rank workload: see bench_multi")
+
+
+# ---------------------------------------------------------------------------- oracle legs
+def oracle_sample(n, iters):
+    """The oracle (as it stands) on the same workload: assembly + PCG setup + `iters` iterations."""
+    import gen
+    import oracle as O
+    m = gen.cube(n)
+    b = gen.rhs(m)
+    O.build()
+    t0 = time.perf_counter()
+    O.solve_case(m, None, b, 0, 0.0, O.controls(0.0, 0.0, iters, iters))
+    t = time.perf_counter() - t0
+    return m.n_cells * iters / t, t
+
+
+def cpu_baseline(n, iters):
+    v, t = oracle_sample(n, iters)
+    return {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"cube {n}^3 ({n ** 3} cells): assembly + PCG setup + {iters} iterations "
+                      f"(minIter = maxIter = {iters}), single thread, {t:.1f} s"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    n = args.n
+    iters = args.ref_iters
+    for _ in range(args.warmup):
+        oracle_sample(n, iters)
+    ts = []
+    for _ in range(args.steps):
+        v, t = oracle_sample(n, iters)
+        ts.append(t)
+    T = sum(ts)
+    value = n ** 3 * iters * args.steps / T
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * T / args.steps,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic",
+           "config": {"workload": f"C3 cube {n}^3 per GPU (weak), gamma=1; oracle sample of {iters} iterations per step",
+                      "cells": n ** 3},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                            "sample": f"per step: cube {n}^3 assembly + PCG setup + {iters} iterations, single thread"},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+# ---------------------------------------------------------------------------- GPU arm
+def run_gpu(args, rank, world, local_rank):
+    import torch
+    import paper_2512_22215_b200 as P
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    mesh, b, ref, cfg = build_workload(args.n, rank, world)
+    N, F = mesh.n_cells, mesh.n_faces
+    stream = torch.cuda.current_stream()
+    h = P.Mesh.from_mesh(mesh, stream=stream.cuda_stream)
+    h.set_batch(args.batch)
+    f64 = dict(dtype=torch.float64, device=dev)
+    diag, upper = torch.empty(N, **f64), torch.empty(F, **f64)
+    b_dev = torch.as_tensor(b, **f64)
+    src, psi = torch.empty(N, **f64), torch.empty(N, **f64)
+    iface = None
+    perfs = []
+
+    def step():
+        src.copy_(b_dev)
+        h.assemble_laplacian(None, None, ref, 0.0, diag, upper, src, iface)
+        psi.zero_()
+        perfs.append(h.pcg_solve(diag, upper, iface, src, psi, *TOL))
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    perfs.clear()
+    h.reset_stats()
+    h.set_timing(not args.no_kernel_timing)
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    clk = clocks.stop()
+    t = e0.elapsed_time(e1) / 1000.0
+    if world > 1:
+        tt = torch.tensor([t], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t = float(tt.item())
+    st = h.get_stats()
+    h.set_timing(False)
+    iters = sum(p["n_iterations"] for p in perfs)
+    n_global = N * world
+    value = n_global * iters / t
+    nb = algorithmic_bytes(N, F)
+    peak, peak_kind = peaks()
+    amul_ms = st["phase_ms"][1] / max(st["phase_count"][1], 1)
+    achieved = nb["A"] / (amul_ms / 1e3) / 1e9 if amul_ms > 0 else None
+    phase_avg = {k: (st["phase_ms"][i] / st["phase_count"][i] if st["phase_count"][i] else None)
+                 for i, k in enumerate(("direction", "amul_dot", "update", "assembly"))}
+    iter_ms = sum(v for k, v in phase_avg.items() if k != "assembly" and v)
+    eff_gbs = nb["iter"] / (iter_ms / 1e3) / 1e9 if iter_ms else None
+
+    # ---- e2e: the same metric through the C-ABI with pinned host buffers (copies inside the region)
+    e2e = None
+    if not args.no_e2e:
+        hb = torch.as_tensor(b).pin_memory()
+        hsrc = torch.empty(N, dtype=torch.float64).pin_memory()
+        hpsi = torch.empty(N, dtype=torch.float64).pin_memory()
+        eperfs = []
+
+        def estep():
+            hsrc.copy_(hb)
+            h.assemble_laplacian(None, None, ref, 0.0, diag, upper, hsrc, iface)
+            hpsi.zero_()
+            eperfs.append(h.pcg_solve(diag, upper, iface, hsrc, hpsi, *TOL))
+
+        estep()
+        eperfs.clear()
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        w0 = time.perf_counter()
+        e0.record(stream)
+        for _ in range(args.steps):
+            estep()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - w0
+        te = max(e0.elapsed_time(e1) / 1000.0, wall)
+        if world > 1:
+            tt = torch.tensor([te], dtype=torch.float64, device=dev)
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            te = float(tt.item())
+        eit = sum(p["n_iterations"] for p in eperfs)
+        e2e = {"value": n_global * eit / te, "unit": UNIT,
+               "h2d_bytes_per_step": 8 * N * 3, "d2h_bytes_per_step": 8 * N * 2,
+               "note": "host pinned b, source, psi through spuma_assemble_laplacian/spuma_pcg_solve; "
+                       "h2d = source (assemble) + source + psi0 (solve); d2h = source (assemble) + psi"}
+
+    if rank != 0:
+        return
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        cpu = cpu_baseline(args.n, args.cpu_iters)
+    traffic = load_traffic(cfg["workload"])
+    cfg.update({"global_cells": n_global, "faces_per_gpu": F, "parallelism": f"dd{world}",
+                "iterations_per_step": iters / max(len(perfs), 1), "l2": "inputs larger than L2 (no flush)",
+                "batch_iterations": st["batch_iterations"], "grid": st["blocks_per_grid"],
+                "effective_iteration_GBps": eff_gbs,
+                "effective_iteration_frac_of_peak": (eff_gbs / peak) if eff_gbs else None,
+                "effective_iteration_frac_of_8TBps": (eff_gbs / 8000.0) if eff_gbs else None,
+                "phase_avg_ms": phase_avg, "algorithmic_bytes": nb})
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": 1000 * t / args.steps, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg,
+           "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                        "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                        "kernel": "k_amul_dot (A7 Amul + wA.pA)", "peak_source": f"{peak_kind} hbm_gbs",
+                        "bytes_per_launch": nb["A"], "avg_launch_ms": amul_ms},
+           "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": st["kernel_launches"],
+           "solver": {"n_iterations": [p["n_iterations"] for p in perfs],
+                      "final_residual": perfs[-1]["final_residual"] if perfs else None}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="spuma", choices=["spuma", "reference"])
+    ap.add_argument("--n", type=int, default=200, help="cube edge per GPU (C3: 200)")
+    ap.add_argument("--batch", type=int, default=16)
+    ap.add_argument("--cpu-iters", type=int, default=50)
+    ap.add_argument("--ref-iters", type=int, default=6)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-kernel-timing", action="store_true")
+    args = ap.parse_args()
+    rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    run_gpu(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,238 @@
+/*
+ * spuma.h -- C-ABI of libspuma: the B200-native pressure-equation hot path of
+ * SPUMA (Bna et al., arXiv 2512.22215, "SPUMA: a minimally invasive approach
+ * to the GPU porting of OPENFOAM").
+ *
+ * What it computes (citations are PAPER.md line numbers, "P:n"):
+ *   - the LDU matrix of fvm::laplacian(gamma, p) on an unstructured finite-
+ *     volume mesh ("P assembly"; lduMatrix / lduAddressing with an
+ *     implicit DOF map; "Gauss linear corrected" with linear
+ *     interpolation; negSumDiag P:520; pRefCell/pRefValue
+ *     P:1083-1084),
+ *   - its solve by PCG with the diagonal (Jacobi) preconditioner (the
+ *     "pcgDiag" solver), including the SpMV Amul
+ *     (21.79% of the paper's kernel time), the PCG vector updates and
+ *     the dot-product reductions,
+ *   - over a domain decomposition, one rank per GPU, with processor-patch halo
+ *     exchange -- done here with NCCL over NVLink.
+ * OpenFOAM semantics the paper relies on but does not print ("SPUMA
+ * reproduces OpenFOAM-v2412") are the readings Q1..Q16 of DESIGN.md §3.
+ *
+ * Conventions (all calls):
+ *   - Types: labels are int32 (spuma_label), scalars fp64 (spuma_scalar).  The
+ *     path is fp64 only (reading Q16; the paper never states precision).
+ *   - Numbering: every per-cell / per-face array at this API is in the
+ *     CALLER's numbering, even with renumber = 1 (the library permutes on entry
+ *     and exit).  Internal faces are the lduAddressing faces: owner < neighbour,
+ *     sorted by (owner, neighbour).  "lower" is not passed: the Laplacian is
+ *     symmetric, lower == upper.
+ *   - Memory space: hot-path arrays (gamma, patch values, diag, upper, source,
+ *     psi, iface_coeffs, x, y) may be device pointers (cudaMalloc / torch CUDA
+ *     tensors) or host pointers (pageable or pinned); the library detects the
+ *     space with cudaPointerGetAttributes and stages host arrays through its own
+ *     device buffers (host<->device copies are then part of the call).
+ *     spuma_mesh_create accepts host or device arrays (pointers_on_device).
+ *   - Ownership: the caller owns every array it passes; the library never
+ *     frees or retains a caller pointer after a call returns.  The handle owns
+ *     its derived addressing, geometry, permutation, halo plan, NCCL
+ *     communicator and every PCG workspace, all allocated once in
+ *     spuma_mesh_create (the paper's memory-pool lesson) and released
+ *     by spuma_free.
+ *   - Synchrony: every call returns after its work is complete; work is
+ *     ordered on the handle's CUDA stream (desc.cuda_stream, or a stream the
+ *     handle creates).
+ *   - Errors: a non-OK spuma_status is returned; spuma_last_error() gives a
+ *     thread-local message.  Non-convergence and singularity are NOT errors
+ *     (reported in spuma_solver_perf, OpenFOAM behaviour).  There is no CPU
+ *     fallback: without a usable CUDA device every compute call fails with
+ *     SPUMA_ERR_CUDA.
+ *   - Thread safety: a handle is not thread-safe; distinct handles are
+ *     independent.
+ */
+#ifndef SPUMA_H
+#define SPUMA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPUMA_ABI_VERSION 1
+
+typedef int32_t spuma_label;
+typedef double spuma_scalar;
+typedef struct spuma_mesh_s* spuma_mesh;
+
+typedef enum {
+    SPUMA_OK = 0,
+    SPUMA_ERR_INVALID_ARGUMENT = 1, /* NULL where required, bad enum, bad size, abi mismatch   */
+    SPUMA_ERR_ADDRESSING = 2,       /* owner >= neighbour, unsorted faces, index out of range  */
+    SPUMA_ERR_LENGTH_MISMATCH = 3,  /* inconsistent array sizes (e.g. processor patch lengths) */
+    SPUMA_ERR_CUDA = 4,             /* CUDA runtime error (incl. no device)                    */
+    SPUMA_ERR_NCCL = 5,             /* NCCL error                                              */
+    SPUMA_ERR_OUT_OF_MEMORY = 6,
+    SPUMA_ERR_STATE = 7             /* call not valid in the handle's state                    */
+} spuma_status;
+
+/* Boundary condition of p on a patch (the kinds the pressure path needs; P:87,
+ * P:536 for processor patches; zeroGradient/fixedValue/empty are [OF]). */
+typedef enum {
+    SPUMA_PATCH_ZERO_GRADIENT = 0, /* no matrix contribution                                      */
+    SPUMA_PATCH_FIXED_VALUE = 1,   /* diag += (g|S|)(-delta_b); source += -(g|S|)(delta_b p_b)      */
+    SPUMA_PATCH_EMPTY = 2,         /* 2-D front/back: ignored entirely                             */
+    SPUMA_PATCH_PROCESSOR = 3      /* coupled face to cell of neighbour_rank (domain decomposition) */
+} spuma_patch_kind;
+
+typedef struct {
+    spuma_patch_kind kind;
+    spuma_label n_faces;
+    const spuma_label* face_cells;   /* [n_faces] cell owning the face (local numbering)          */
+    const spuma_scalar* Sf;          /* [3*n_faces] face area vectors, pointing OUT of the domain */
+    const spuma_scalar* magSf;       /* [n_faces] |Sf|                                             */
+    const spuma_scalar* Cf;          /* [3*n_faces] face centres                                   */
+    /* PROCESSOR only (ignored otherwise): */
+    int neighbour_rank;              /* rank holding the other cell                                */
+    const spuma_label* global_face;  /* [n_faces] face id in the undecomposed mesh; faces must be
+                                        ascending in it (reading Q13) -- both sides then agree   */
+    const spuma_scalar* neighbour_C; /* [3*n_faces] centre of the remote cell                      */
+    const signed char* is_owner;     /* [n_faces] 1 if the local cell is the owner of the
+                                        undecomposed face (face evaluated in global orientation) */
+} spuma_patch_desc;
+
+typedef struct {
+    int abi_version;                 /* SPUMA_ABI_VERSION                                           */
+    spuma_label n_cells;             /* cells of this (sub-)domain                                  */
+    spuma_label n_faces;             /* internal faces only                                         */
+    const spuma_label* owner;        /* [n_faces] lowerAddr; owner < neighbour; sorted    */
+    const spuma_label* neighbour;    /* [n_faces] upperAddr                                         */
+    const spuma_scalar* Sf;          /* [3*n_faces] owner -> neighbour                              */
+    const spuma_scalar* magSf;       /* [n_faces]                                                   */
+    const spuma_scalar* C;           /* [3*n_cells] cell centres                                    */
+    const spuma_scalar* Cf;          /* [3*n_faces] face centres (interpolation weights)            */
+    int n_patches;
+    const spuma_patch_desc* patches; /* [n_patches], boundary coefficients applied in this order    */
+    int renumber;                    /* 0: keep caller numbering; 1: reverse Cuthill-McKee inside   */
+    int pointers_on_device;          /* 0: arrays above are host memory; 1: device memory           */
+    void* cuda_stream;               /* cudaStream_t to order work on; NULL: handle makes its own   */
+    int rank, n_ranks;               /* n_ranks == 1: no communication                              */
+    const void* nccl_unique_id;      /* 128-byte ncclUniqueId from rank 0 (n_ranks > 1)             */
+} spuma_mesh_desc;
+
+/* SolverControls (P:1033-1041 key names). converged := r < tolerance ||
+ * (rel_tol > 1e-20 && r < rel_tol * initial_residual), r the normalised L1
+ * residual (reading Q1/Q2); at least min_iter, at most max_iter iterations. */
+typedef struct {
+    spuma_scalar tolerance, rel_tol;
+    int max_iter, min_iter;
+} spuma_solver_controls;
+
+typedef struct {
+    spuma_scalar initial_residual, final_residual;
+    int n_iterations;
+    int converged, singular;
+} spuma_solver_perf;
+
+/*
+ * Build a handle for one (sub-)mesh: validate the addressing (A0), optionally
+ * renumber cells by reverse Cuthill-McKee (A1, reading O2/Q12), derive
+ * ownerStart / losort / losortStart and the per-cell boundary lists (A2),
+ * compute nonOrthDeltaCoeffs and linear weights on the device (A3),
+ * build the halo plan and the NCCL communicator (n_ranks > 1), and allocate
+ * every workspace.  Errors: INVALID_ARGUMENT, ADDRESSING, LENGTH_MISMATCH,
+ * CUDA, NCCL, OUT_OF_MEMORY.  *out is NULL on error.
+ */
+spuma_status spuma_mesh_create(const spuma_mesh_desc* desc, spuma_mesh* out);
+
+/*
+ * Assemble fvm::laplacian(gamma, p) ("P assembly"):
+ *   gamma_f  = w (gamma_P - gamma_N) + gamma_N         (linear; gamma == NULL: gamma = 1)
+ *   upper[f] = delta_f (gamma_f |S_f|)                 lower == upper
+ *   diag[c]  = -sum of the off-diagonals of row c      (negSumDiag)
+ *   setReference(ref_cell, ref_value) if ref_cell >= 0:
+ *            source[ref] += diag[ref] ref_value; diag[ref] += diag[ref]
+ *   then boundary coefficients in (patch, face) order (fixedValue, processor).
+ * gamma: [n_cells]. patch_value: [n_patches] array of pointers, fixedValue
+ * values per patch face (entries for other kinds ignored; may be NULL if no
+ * fixedValue patch).  diag [n_cells], upper [n_faces] are written; source
+ * [n_cells] is read-modified-written.  iface_coeffs: [sum of processor faces]
+ * written with the true matrix entries A[P][remote] (reading Q9), in patch
+ * order; NULL allowed when there is no processor patch.  n_ranks > 1: the gamma
+ * halo is exchanged with the neighbours (collective: all ranks must call).
+ */
+spuma_status spuma_assemble_laplacian(spuma_mesh m, const spuma_scalar* gamma,
+                                      const spuma_scalar* const* patch_value, spuma_label ref_cell,
+                                      spuma_scalar ref_value, spuma_scalar* diag, spuma_scalar* upper,
+                                      spuma_scalar* source, spuma_scalar* iface_coeffs);
+
+/*
+ * Solve A psi = source by PCG with the diagonal preconditioner, OpenFOAM
+ * semantics (normFactor Q1, convergence Q2, loop Q3, singularity
+ * Q4).  psi [n_cells] is the initial guess on entry and the solution on exit.
+ * diag/upper/iface_coeffs as produced by spuma_assemble_laplacian (or any
+ * symmetric LDU matrix on this mesh).  perf must be non-NULL.  n_ranks > 1:
+ * collective; dot products and norms are global and every rank returns the
+ * same perf.
+ */
+spuma_status spuma_pcg_solve(spuma_mesh m, const spuma_scalar* diag, const spuma_scalar* upper,
+                             const spuma_scalar* iface_coeffs, const spuma_scalar* source, spuma_scalar* psi,
+                             const spuma_solver_controls* ctl, spuma_solver_perf* perf);
+
+/* Release everything the handle owns (NULL-safe). */
+void spuma_free(spuma_mesh m);
+
+/* ---------------- diagnostics (parity tests, benchmark harness) ---------------- */
+
+/* y = A x (lduMatrix::Amul), with the processor-interface terms when
+ * n_ranks > 1 (collective halo exchange of x). */
+spuma_status spuma_amul(spuma_mesh m, const spuma_scalar* diag, const spuma_scalar* upper,
+                        const spuma_scalar* iface_coeffs, const spuma_scalar* x, spuma_scalar* y);
+
+/* Host copies of the derived addressing, INTERNAL numbering (after renumbering).
+ * perm [n_cells] (perm[caller cell] = internal cell), owner/neighbour [n_faces],
+ * owner_start/losort_start [n_cells+1], losort [n_faces], face_map [n_faces]
+ * (face_map[internal face] = caller face).  Any pointer may be NULL. */
+spuma_status spuma_mesh_get_addressing(spuma_mesh m, spuma_label* perm, spuma_label* owner,
+                                       spuma_label* neighbour, spuma_label* owner_start, spuma_label* losort,
+                                       spuma_label* losort_start, spuma_label* face_map);
+
+/* Host copies of the A3 geometry in CALLER face order: delta [n_faces]
+ * (nonOrthDeltaCoeffs), weights [n_faces], bdelta [total boundary faces in
+ * patch order, empty patches included as 0]. Any pointer may be NULL. */
+spuma_status spuma_mesh_get_geometry(spuma_mesh m, spuma_scalar* delta, spuma_scalar* weights,
+                                     spuma_scalar* bdelta);
+
+typedef struct {
+    uint64_t kernel_launches;        /* kernels this handle launched (graph nodes counted per replay) */
+    uint64_t solves, iterations;     /* totals over the handle's life                                 */
+    int timing_enabled;
+    /* phase timing (CUDA events on the handle's stream, enabled by spuma_set_timing):
+       [0] direction (pA = rD rA + beta pA), [1] Amul + wA.pA, [2] update + residual dots,
+       [3] assembly (face coefficients + diagonal gather) */
+    double phase_ms[4];
+    uint64_t phase_count[4];
+    int blocks_per_grid, threads_per_block, batch_iterations;
+} spuma_stats;
+
+spuma_status spuma_get_stats(spuma_mesh m, spuma_stats* out);
+spuma_status spuma_reset_stats(spuma_mesh m);
+/* Record CUDA events around every hot-loop kernel (adds event nodes to the
+ * captured iteration graphs); off by default. */
+spuma_status spuma_set_timing(spuma_mesh m, int enable);
+/* Iterations per captured CUDA-graph batch (default 16; 1..256). */
+spuma_status spuma_set_batch(spuma_mesh m, int iterations);
+
+/* Fill out128 with a fresh ncclUniqueId (rank 0 calls it and broadcasts). */
+spuma_status spuma_nccl_get_unique_id(void* out128);
+
+/* Message of the last non-OK status on this thread ("" if none). */
+const char* spuma_last_error(void);
+
+/* ABI version the library was built with. */
+int spuma_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPUMA_H */

@@ -1,0 +1,845 @@
+// api.cu -- the C-ABI of libspuma (include/spuma.h): mesh handle, assembly,
+// PCG orchestration (graph-captured iteration batches), NCCL halo exchange.
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "host.h"
+#include "internal.h"
+
+using namespace spuma;
+
+namespace spuma {
+
+static thread_local std::string g_err;
+
+spuma_status set_error(spuma_status s, const std::string& msg)
+{
+    g_err = msg;
+    return s;
+}
+
+}  // namespace spuma
+
+namespace {
+
+template <class T>
+spuma_status dalloc(T** p, size_t n)
+{
+    *p = nullptr;
+    if (n == 0) n = 1;
+    SPUMA_CUDA(cudaMalloc(reinterpret_cast<void**>(p), n * sizeof(T)));
+    return SPUMA_OK;
+}
+
+template <class T>
+spuma_status upload(T** p, const std::vector<T>& v, cudaStream_t s)
+{
+    SPUMA_TRY(dalloc(p, v.size()));
+    if (!v.empty()) SPUMA_CUDA(cudaMemcpyAsync(*p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+    return SPUMA_OK;
+}
+
+bool is_device_ptr(const void* p)
+{
+    if (!p) return false;
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// host copy of a caller array that may live on the device
+template <class T>
+spuma_status fetch(std::vector<T>& out, const T* p, size_t n, bool on_device)
+{
+    out.resize(n);
+    if (n == 0) return SPUMA_OK;
+    if (!p) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "NULL array in mesh description");
+    if (on_device) SPUMA_CUDA(cudaMemcpy(out.data(), p, n * sizeof(T), cudaMemcpyDeviceToHost));
+    else std::memcpy(out.data(), p, n * sizeof(T));
+    return SPUMA_OK;
+}
+
+MeshArgs mesh_args(const spuma_mesh m)
+{
+    MeshArgs a{};
+    a.N = m->N;
+    a.F = m->F;
+    a.ownerStart = m->d_ownerStart;
+    a.losortStart = m->d_losortStart;
+    a.losort = m->d_losort;
+    a.ownerLo = m->d_ownerLo;
+    a.neighbour = m->d_neighbour;
+    a.owner = m->d_owner;
+    a.ifStart = m->n_iface ? m->d_ifStart : nullptr;
+    a.ifIdx = m->d_ifIdx;
+    a.n_iface = m->n_iface;
+    return a;
+}
+
+enum CellRole { R_GAMMA = 0, R_DIAG, R_SOURCE, R_PSI, R_X, R_Y, R_COUNT };
+
+double** cell_buf(spuma_mesh m, int role)
+{
+    double** bufs[R_COUNT] = {&m->d_cell_a, &m->d_cell_b, &m->d_cell_c, &m->d_cell_d, &m->d_cell_e, &m->d_cell_t};
+    return bufs[role];
+}
+
+// caller cell array -> device array in internal numbering
+spuma_status cells_in(spuma_mesh m, const double* p, int role, const double** out)
+{
+    const bool dev = is_device_ptr(p);
+    if (!m->renumber && dev) {
+        *out = p;
+        return SPUMA_OK;
+    }
+    double** buf = cell_buf(m, role);
+    if (!*buf) SPUMA_TRY(dalloc(buf, m->N));
+    if (!m->renumber) {
+        SPUMA_CUDA(cudaMemcpyAsync(*buf, p, sizeof(double) * m->N, cudaMemcpyHostToDevice, m->stream));
+    } else {
+        const double* src = p;
+        if (!dev) {
+            if (!m->d_face_t) SPUMA_TRY(dalloc(&m->d_face_t, std::max(m->F, m->N)));
+            SPUMA_CUDA(cudaMemcpyAsync(m->d_face_t, p, sizeof(double) * m->N, cudaMemcpyHostToDevice, m->stream));
+            src = m->d_face_t;
+        }
+        launch_scatter(m->stream, m->N, m->d_perm, src, *buf);  // buf[perm[i]] = p[i]
+    }
+    *out = *buf;
+    return SPUMA_OK;
+}
+
+// internal device array -> caller cell array
+spuma_status cells_out(spuma_mesh m, double* p, const double* buf)
+{
+    if (buf == p) return SPUMA_OK;
+    if (!m->renumber) {
+        SPUMA_CUDA(cudaMemcpyAsync(p, buf, sizeof(double) * m->N, cudaMemcpyDefault, m->stream));
+        return SPUMA_OK;
+    }
+    if (!m->d_face_t) SPUMA_TRY(dalloc(&m->d_face_t, std::max(m->F, m->N)));
+    launch_gather(m->stream, m->N, m->d_perm, buf, m->d_face_t);  // t[i] = buf[perm[i]]
+    SPUMA_CUDA(cudaMemcpyAsync(p, m->d_face_t, sizeof(double) * m->N, cudaMemcpyDefault, m->stream));
+    return SPUMA_OK;
+}
+
+spuma_status faces_in(spuma_mesh m, const double* p, const double** out)
+{
+    const bool dev = is_device_ptr(p);
+    if (!m->renumber && dev) {
+        *out = p;
+        return SPUMA_OK;
+    }
+    if (!m->d_face_a) SPUMA_TRY(dalloc(&m->d_face_a, m->F));
+    if (!m->renumber) {
+        SPUMA_CUDA(cudaMemcpyAsync(m->d_face_a, p, sizeof(double) * m->F, cudaMemcpyHostToDevice, m->stream));
+    } else {
+        const double* src = p;
+        if (!dev) {
+            if (!m->d_face_t) SPUMA_TRY(dalloc(&m->d_face_t, std::max(m->F, m->N)));
+            SPUMA_CUDA(cudaMemcpyAsync(m->d_face_t, p, sizeof(double) * m->F, cudaMemcpyHostToDevice, m->stream));
+            src = m->d_face_t;
+        }
+        launch_gather(m->stream, m->F, m->d_face_map, src, m->d_face_a);  // a[new] = p[face_map[new]]
+    }
+    *out = m->d_face_a;
+    return SPUMA_OK;
+}
+
+spuma_status faces_out(spuma_mesh m, double* p, const double* buf)
+{
+    if (buf == p) return SPUMA_OK;
+    if (!m->renumber) {
+        SPUMA_CUDA(cudaMemcpyAsync(p, buf, sizeof(double) * m->F, cudaMemcpyDefault, m->stream));
+        return SPUMA_OK;
+    }
+    if (!m->d_face_t) SPUMA_TRY(dalloc(&m->d_face_t, std::max(m->F, m->N)));
+    launch_scatter(m->stream, m->F, m->d_face_map, buf, m->d_face_t);  // t[face_map[new]] = buf[new]
+    SPUMA_CUDA(cudaMemcpyAsync(p, m->d_face_t, sizeof(double) * m->F, cudaMemcpyDefault, m->stream));
+    return SPUMA_OK;
+}
+
+spuma_status iface_in(spuma_mesh m, const double* p, const double** out)
+{
+    if (m->n_iface == 0 || is_device_ptr(p)) {
+        *out = p;
+        return SPUMA_OK;
+    }
+    if (!m->d_iface_a) SPUMA_TRY(dalloc(&m->d_iface_a, m->n_iface));
+    SPUMA_CUDA(cudaMemcpyAsync(m->d_iface_a, p, sizeof(double) * m->n_iface, cudaMemcpyHostToDevice, m->stream));
+    *out = m->d_iface_a;
+    return SPUMA_OK;
+}
+
+// ---------------------------------------------------------------------------
+// halo exchange over NCCL (processor patches)
+// ---------------------------------------------------------------------------
+
+spuma_status halo_exchange(spuma_mesh m, const double* x, double* xr, cudaStream_t s)
+{
+    if (m->n_ranks == 1 || m->n_iface == 0) return SPUMA_OK;
+    launch_pack(s, m->n_iface, m->d_if_cell, x, m->d_sendbuf);
+    m->stats.kernel_launches += 1;
+    SPUMA_NCCL(ncclGroupStart());
+    for (const auto& p : m->patches) {
+        if (p.kind != SPUMA_PATCH_PROCESSOR || p.n_faces == 0) continue;
+        SPUMA_NCCL(ncclSend(m->d_sendbuf + p.iface_offset, p.n_faces, ncclDouble, p.neighbour_rank, m->comm, s));
+        SPUMA_NCCL(ncclRecv(xr + p.iface_offset, p.n_faces, ncclDouble, p.neighbour_rank, m->comm, s));
+    }
+    SPUMA_NCCL(ncclGroupEnd());
+    return SPUMA_OK;
+}
+
+// every rank gets all ranks' 4 partials (rank order) and finalises identically
+spuma_status reduce_finalize(spuma_mesh m, int stage, cudaStream_t s)
+{
+    double* gathered = m->ws.part;  // free after the reduction kernel finished
+    SPUMA_NCCL(ncclAllGather(m->ws.scal->rank_part, gathered, 4, ncclDouble, m->comm, s));
+    launch_finalize(s, stage, gathered, m->n_ranks, m->ws);
+    m->stats.kernel_launches += 1;
+    return SPUMA_OK;
+}
+
+void record(spuma_mesh m, std::vector<cudaEvent_t>& ev, int idx, cudaStream_t s)
+{
+    cudaEventRecordWithFlags(ev[idx], s, cudaEventRecordExternal);
+}
+
+// one PCG iteration (A11, A7h, A7-A8, A9-A10) on stream s
+spuma_status enqueue_iteration(spuma_mesh m, cudaStream_t s, std::vector<cudaEvent_t>* ev, int slot)
+{
+    const MeshArgs a = mesh_args(m);
+    const bool fin = m->n_ranks == 1;
+    if (ev) record(m, *ev, slot * 6 + 0, s);
+    launch_direction(s, m->grid, a, m->ws);
+    if (ev) record(m, *ev, slot * 6 + 1, s);
+    SPUMA_TRY(halo_exchange(m, m->ws.pA, m->ws.xr, s));
+    if (ev) record(m, *ev, slot * 6 + 2, s);
+    launch_amul_dot(s, m->grid, a, m->ws, fin);
+    if (ev) record(m, *ev, slot * 6 + 3, s);
+    if (!fin) SPUMA_TRY(reduce_finalize(m, 3, s));
+    if (ev) record(m, *ev, slot * 6 + 4, s);
+    launch_update(s, m->grid, a, m->ws, fin);
+    if (ev) record(m, *ev, slot * 6 + 5, s);
+    if (!fin) SPUMA_TRY(reduce_finalize(m, 4, s));
+    m->stats.kernel_launches += 3;
+    return SPUMA_OK;
+}
+
+void destroy_graphs(spuma_mesh m)
+{
+    for (int i = 0; i < 2; ++i) {
+        if (m->gexec[i]) cudaGraphExecDestroy(m->gexec[i]);
+        m->gexec[i] = nullptr;
+        for (auto e : m->tev[i]) cudaEventDestroy(e);
+        m->tev[i].clear();
+    }
+}
+
+spuma_status build_graphs(spuma_mesh m)
+{
+    if (m->gexec[0] && m->gexec_timed == m->timing && m->gexec_batch == m->batch) return SPUMA_OK;
+    destroy_graphs(m);
+    const uint64_t launches_before = m->stats.kernel_launches;
+    for (int g = 0; g < 2; ++g) {
+        std::vector<cudaEvent_t>* ev = nullptr;
+        if (m->timing) {
+            m->tev[g].resize((size_t)m->batch * 6);
+            for (auto& e : m->tev[g]) SPUMA_CUDA(cudaEventCreate(&e));
+            ev = &m->tev[g];
+        }
+        cudaGraph_t graph = nullptr;
+        SPUMA_CUDA(cudaStreamBeginCapture(m->stream, cudaStreamCaptureModeThreadLocal));
+        spuma_status st = SPUMA_OK;
+        for (int k = 0; k < m->batch && st == SPUMA_OK; ++k) st = enqueue_iteration(m, m->stream, ev, k);
+        cudaError_t e = cudaStreamEndCapture(m->stream, &graph);
+        if (st != SPUMA_OK) {
+            if (graph) cudaGraphDestroy(graph);
+            return st;
+        }
+        SPUMA_CUDA(e);
+        e = cudaGraphInstantiate(&m->gexec[g], graph, 0);
+        cudaGraphDestroy(graph);
+        SPUMA_CUDA(e);
+    }
+    m->stats.kernel_launches = launches_before;  // capture launches nothing
+    m->gexec_timed = m->timing;
+    m->gexec_batch = m->batch;
+    return SPUMA_OK;
+}
+
+uint64_t launches_per_iteration(spuma_mesh m)
+{
+    uint64_t k = 3;
+    if (m->n_ranks > 1) k += 2 + (m->n_iface ? 1 : 0);
+    return k;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C-ABI
+// ===========================================================================
+
+extern "C" {
+
+const char* spuma_last_error(void) { return g_err.c_str(); }
+
+int spuma_abi_version(void) { return SPUMA_ABI_VERSION; }
+
+spuma_status spuma_nccl_get_unique_id(void* out128)
+{
+    if (!out128) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "out128 is NULL");
+    ncclUniqueId id;
+    SPUMA_NCCL(ncclGetUniqueId(&id));
+    std::memcpy(out128, &id, sizeof(id));
+    return SPUMA_OK;
+}
+
+void spuma_free(spuma_mesh m)
+{
+    if (!m) return;
+    if (m->stream) cudaStreamSynchronize(m->stream);
+    destroy_graphs(m);
+    for (int i = 0; i < 2; ++i) {
+        if (m->batch_done[i]) cudaEventDestroy(m->batch_done[i]);
+        if (m->asm_ev[i]) cudaEventDestroy(m->asm_ev[i]);
+    }
+    void* dptrs[] = {m->d_owner, m->d_neighbour, m->d_ownerStart, m->d_losortStart, m->d_losort, m->d_ownerLo,
+                     m->d_perm, m->d_face_map, m->d_delta, m->d_weights, m->d_magSf, m->d_bkind, m->d_bcell,
+                     m->d_bproc, m->d_bmagSf, m->d_bdelta, m->d_bweight, m->d_bvalue, m->d_bgamma_r,
+                     m->d_bis_owner, m->d_bStart, m->d_bFace, m->d_ifStart, m->d_ifIdx, m->d_if_cell,
+                     m->d_sendbuf, m->d_cell_a, m->d_cell_b, m->d_cell_c, m->d_cell_d, m->d_cell_e, m->d_cell_t,
+                     m->d_face_a, m->d_face_t, m->d_iface_a, m->ws.wA, m->ws.rA, m->ws.pA, m->ws.rD, m->ws.sumA,
+                     m->ws.xr, m->ws.part, m->ws.scal, m->ws.ptrs};
+    for (void* p : dptrs)
+        if (p) cudaFree(p);
+    if (m->h_ptrs) cudaFreeHost(m->h_ptrs);
+    if (m->h_scal) cudaFreeHost(m->h_scal);
+    if (m->comm) ncclCommDestroy(m->comm);
+    if (m->comm_stream) cudaStreamDestroy(m->comm_stream);
+    if (m->own_stream && m->stream) cudaStreamDestroy(m->stream);
+    delete m;
+}
+
+static spuma_status mesh_create_impl(const spuma_mesh_desc* d, spuma_mesh m)
+{
+    const int N = d->n_cells, F = d->n_faces;
+    int ndev = 0;
+    SPUMA_CUDA(cudaGetDeviceCount(&ndev));
+    SPUMA_CUDA(cudaGetDevice(&m->device));
+    if (d->cuda_stream) {
+        m->stream = static_cast<cudaStream_t>(d->cuda_stream);
+    } else {
+        SPUMA_CUDA(cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking));
+        m->own_stream = true;
+    }
+    m->N = N;
+    m->F = F;
+    m->renumber = d->renumber ? 1 : 0;
+    m->rank = d->rank;
+    m->n_ranks = d->n_ranks;
+    const bool od = d->pointers_on_device != 0;
+
+    // ---- A0: host copies + validation
+    std::vector<int> owner, neighbour;
+    std::vector<double> Sf, magSf, C, Cf;
+    SPUMA_TRY(fetch(owner, d->owner, F, od));
+    SPUMA_TRY(fetch(neighbour, d->neighbour, F, od));
+    SPUMA_TRY(fetch(Sf, d->Sf, 3 * (size_t)F, od));
+    SPUMA_TRY(fetch(magSf, d->magSf, F, od));
+    SPUMA_TRY(fetch(C, d->C, 3 * (size_t)N, od));
+    SPUMA_TRY(fetch(Cf, d->Cf, 3 * (size_t)F, od));
+    std::string why;
+    if (!valid_addressing(N, F, owner.data(), neighbour.data(), &why)) return set_error(SPUMA_ERR_ADDRESSING, why);
+
+    struct HP {
+        int kind, n, rank;
+        std::vector<int> cells, gface;
+        std::vector<double> Sf, magSf, Cf, nC;
+        std::vector<signed char> own;
+    };
+    std::vector<HP> hp(d->n_patches);
+    for (int p = 0; p < d->n_patches; ++p) {
+        const spuma_patch_desc& pd = d->patches[p];
+        HP& h = hp[p];
+        h.kind = pd.kind;
+        h.n = pd.n_faces;
+        h.rank = pd.neighbour_rank;
+        if (pd.kind < SPUMA_PATCH_ZERO_GRADIENT || pd.kind > SPUMA_PATCH_PROCESSOR)
+            return set_error(SPUMA_ERR_INVALID_ARGUMENT, "patch " + std::to_string(p) + ": bad kind");
+        if (pd.n_faces < 0) return set_error(SPUMA_ERR_LENGTH_MISMATCH, "patch " + std::to_string(p) + ": n_faces < 0");
+        SPUMA_TRY(fetch(h.cells, pd.face_cells, pd.n_faces, od));
+        SPUMA_TRY(fetch(h.Sf, pd.Sf, 3 * (size_t)pd.n_faces, od));
+        SPUMA_TRY(fetch(h.magSf, pd.magSf, pd.n_faces, od));
+        SPUMA_TRY(fetch(h.Cf, pd.Cf, 3 * (size_t)pd.n_faces, od));
+        for (int c : h.cells)
+            if (c < 0 || c >= N)
+                return set_error(SPUMA_ERR_ADDRESSING, "patch " + std::to_string(p) + ": face cell out of range");
+        if (pd.kind == SPUMA_PATCH_PROCESSOR) {
+            if (d->n_ranks <= 1 || pd.neighbour_rank < 0 || pd.neighbour_rank >= d->n_ranks ||
+                pd.neighbour_rank == d->rank)
+                return set_error(SPUMA_ERR_INVALID_ARGUMENT, "patch " + std::to_string(p) + ": bad neighbour_rank");
+            SPUMA_TRY(fetch(h.gface, pd.global_face, pd.n_faces, od));
+            SPUMA_TRY(fetch(h.nC, pd.neighbour_C, 3 * (size_t)pd.n_faces, od));
+            SPUMA_TRY(fetch(h.own, pd.is_owner, pd.n_faces, od));
+            for (int i = 1; i < pd.n_faces; ++i)
+                if (h.gface[i] <= h.gface[i - 1])
+                    return set_error(SPUMA_ERR_ADDRESSING, "processor patch " + std::to_string(p) +
+                                                               ": global_face not strictly ascending (Q13)");
+        }
+    }
+
+    // ---- A1: renumbering
+    if (m->renumber) {
+        m->h_perm = rcm_permutation(N, F, owner.data(), neighbour.data());
+        std::vector<int> o2, n2;
+        std::vector<char> flip;
+        rekey_faces(N, F, m->h_perm.data(), owner.data(), neighbour.data(), o2, n2, m->h_face_map, flip);
+        std::vector<double> Sf2(3 * (size_t)F), magSf2(F), Cf2(3 * (size_t)F), C2(3 * (size_t)N);
+        for (int g = 0; g < F; ++g) {
+            const int f = m->h_face_map[g];
+            const double sg = flip[g] ? -1.0 : 1.0;
+            for (int k = 0; k < 3; ++k) {
+                Sf2[3 * (size_t)g + k] = flip[g] ? -Sf[3 * (size_t)f + k] : Sf[3 * (size_t)f + k];
+                Cf2[3 * (size_t)g + k] = Cf[3 * (size_t)f + k];
+            }
+            (void)sg;
+            magSf2[g] = magSf[f];
+        }
+        for (int c = 0; c < N; ++c)
+            for (int k = 0; k < 3; ++k) C2[3 * (size_t)m->h_perm[c] + k] = C[3 * (size_t)c + k];
+        owner.swap(o2);
+        neighbour.swap(n2);
+        Sf.swap(Sf2);
+        magSf.swap(magSf2);
+        Cf.swap(Cf2);
+        C.swap(C2);
+        for (auto& h : hp)
+            for (int& c : h.cells) c = m->h_perm[c];
+    } else {
+        m->h_perm.resize(N);
+        for (int c = 0; c < N; ++c) m->h_perm[c] = c;
+        m->h_face_map.resize(F);
+        for (int f = 0; f < F; ++f) m->h_face_map[f] = f;
+    }
+
+    // ---- A2: derived addressing
+    std::vector<int> ownerLo;
+    derived_addressing(N, F, owner.data(), neighbour.data(), m->h_ownerStart, m->h_losort, m->h_losortStart, ownerLo);
+    m->h_owner = owner;
+    m->h_neighbour = neighbour;
+
+    // boundary faces, concatenated in patch order
+    std::vector<int> bkind, bcell, bproc, if_cell;
+    std::vector<double> bSf, bmagSf, bCf, bnC;
+    std::vector<signed char> bown;
+    std::vector<char> contributes;
+    int iface_off = 0;
+    for (int p = 0; p < (int)hp.size(); ++p) {
+        const HP& h = hp[p];
+        Patch P{h.kind, h.n, (int)bkind.size(), h.rank, h.kind == SPUMA_PATCH_PROCESSOR ? iface_off : -1};
+        m->patches.push_back(P);
+        for (int i = 0; i < h.n; ++i) {
+            bkind.push_back(h.kind);
+            bcell.push_back(h.cells[i]);
+            for (int k = 0; k < 3; ++k) {
+                bSf.push_back(h.Sf[3 * (size_t)i + k]);
+                bCf.push_back(h.Cf[3 * (size_t)i + k]);
+                bnC.push_back(h.kind == SPUMA_PATCH_PROCESSOR ? h.nC[3 * (size_t)i + k] : 0.0);
+            }
+            bmagSf.push_back(h.magSf[i]);
+            bown.push_back(h.kind == SPUMA_PATCH_PROCESSOR ? h.own[i] : 0);
+            contributes.push_back(h.kind == SPUMA_PATCH_FIXED_VALUE || h.kind == SPUMA_PATCH_PROCESSOR);
+            if (h.kind == SPUMA_PATCH_PROCESSOR) {
+                bproc.push_back(iface_off++);
+                if_cell.push_back(h.cells[i]);
+            } else {
+                bproc.push_back(-1);
+            }
+        }
+    }
+    m->Fb = (int)bkind.size();
+    m->n_iface = iface_off;
+    std::vector<int> bStart, bFace;
+    cell_lists(N, bcell, contributes, bStart, bFace);
+    std::vector<int> ifStart, ifIdx;
+    cell_lists(N, if_cell, std::vector<char>(if_cell.size(), 1), ifStart, ifIdx);
+
+    // ---- uploads
+    cudaStream_t s = m->stream;
+    SPUMA_TRY(upload(&m->d_owner, owner, s));
+    SPUMA_TRY(upload(&m->d_neighbour, neighbour, s));
+    SPUMA_TRY(upload(&m->d_ownerStart, m->h_ownerStart, s));
+    SPUMA_TRY(upload(&m->d_losortStart, m->h_losortStart, s));
+    SPUMA_TRY(upload(&m->d_losort, m->h_losort, s));
+    SPUMA_TRY(upload(&m->d_ownerLo, ownerLo, s));
+    if (m->renumber) {
+        SPUMA_TRY(upload(&m->d_perm, m->h_perm, s));
+        SPUMA_TRY(upload(&m->d_face_map, m->h_face_map, s));
+    }
+    SPUMA_TRY(upload(&m->d_magSf, magSf, s));
+    SPUMA_TRY(upload(&m->d_bkind, bkind, s));
+    SPUMA_TRY(upload(&m->d_bcell, bcell, s));
+    SPUMA_TRY(upload(&m->d_bproc, bproc, s));
+    SPUMA_TRY(upload(&m->d_bmagSf, bmagSf, s));
+    SPUMA_TRY(upload(&m->d_bis_owner, bown, s));
+    SPUMA_TRY(upload(&m->d_bStart, bStart, s));
+    SPUMA_TRY(upload(&m->d_bFace, bFace, s));
+    SPUMA_TRY(upload(&m->d_ifStart, ifStart, s));
+    SPUMA_TRY(upload(&m->d_ifIdx, ifIdx, s));
+    SPUMA_TRY(upload(&m->d_if_cell, if_cell, s));
+    SPUMA_TRY(dalloc(&m->d_bdelta, m->Fb));
+    SPUMA_TRY(dalloc(&m->d_bweight, m->Fb));
+    SPUMA_TRY(dalloc(&m->d_bvalue, m->Fb));
+    SPUMA_CUDA(cudaMemsetAsync(m->d_bvalue, 0, sizeof(double) * std::max(m->Fb, 1), s));
+    SPUMA_TRY(dalloc(&m->d_bgamma_r, m->n_iface));
+    SPUMA_TRY(dalloc(&m->d_sendbuf, m->n_iface));
+    SPUMA_TRY(dalloc(&m->d_delta, F));
+    SPUMA_TRY(dalloc(&m->d_weights, F));
+
+    // ---- A3: geometry on the device
+    {
+        double *dSf = nullptr, *dC = nullptr, *dCf = nullptr, *dbSf = nullptr, *dbCf = nullptr, *dbnC = nullptr;
+        SPUMA_TRY(upload(&dSf, Sf, s));
+        SPUMA_TRY(upload(&dC, C, s));
+        SPUMA_TRY(upload(&dCf, Cf, s));
+        SPUMA_TRY(upload(&dbSf, bSf, s));
+        SPUMA_TRY(upload(&dbCf, bCf, s));
+        SPUMA_TRY(upload(&dbnC, bnC, s));
+        launch_geometry(s, F, m->d_owner, m->d_neighbour, dSf, m->d_magSf, dC, dCf, m->d_delta, m->d_weights);
+        launch_bgeometry(s, m->Fb, m->d_bkind, m->d_bcell, dbSf, m->d_bmagSf, dbCf, dC, dbnC, m->d_bis_owner,
+                         m->d_bdelta, m->d_bweight);
+        m->stats.kernel_launches += (F > 0) + (m->Fb > 0);
+        SPUMA_CUDA(cudaStreamSynchronize(s));
+        cudaFree(dSf);
+        cudaFree(dC);
+        cudaFree(dCf);
+        cudaFree(dbSf);
+        cudaFree(dbCf);
+        cudaFree(dbnC);
+    }
+
+    // ---- workspaces (allocated once: the paper's memory-pool lesson)
+    m->grid = occupancy_grid(N, &m->grid_faces, F);
+    SPUMA_TRY(dalloc(&m->ws.wA, N + 1));
+    SPUMA_TRY(dalloc(&m->ws.rA, N + 1));
+    SPUMA_TRY(dalloc(&m->ws.pA, N + 1));
+    SPUMA_TRY(dalloc(&m->ws.rD, N + 1));
+    SPUMA_TRY(dalloc(&m->ws.sumA, N + 1));
+    SPUMA_TRY(dalloc(&m->ws.xr, m->n_iface));
+    SPUMA_TRY(dalloc(&m->ws.part, (size_t)kMaxPartials * std::max(m->grid, 4 * std::max(m->n_ranks, 1))));
+    SPUMA_TRY(dalloc(&m->ws.scal, 1));
+    SPUMA_TRY(dalloc(&m->ws.ptrs, 1));
+    SPUMA_CUDA(cudaMemsetAsync(m->ws.scal, 0, sizeof(DevScal), s));
+    SPUMA_CUDA(cudaMemsetAsync(m->ws.pA, 0, sizeof(double) * (N + 1), s));
+    SPUMA_CUDA(cudaMallocHost(reinterpret_cast<void**>(&m->h_ptrs), sizeof(DevPtrs)));
+    SPUMA_CUDA(cudaMallocHost(reinterpret_cast<void**>(&m->h_scal), 2 * sizeof(DevScal)));
+    for (int i = 0; i < 2; ++i) {
+        SPUMA_CUDA(cudaEventCreateWithFlags(&m->batch_done[i], cudaEventDisableTiming));
+        SPUMA_CUDA(cudaEventCreate(&m->asm_ev[i]));
+    }
+
+    // ---- communicator
+    if (m->n_ranks > 1) {
+        if (!d->nccl_unique_id) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "n_ranks > 1 needs nccl_unique_id");
+        ncclUniqueId id;
+        std::memcpy(&id, d->nccl_unique_id, sizeof(id));
+        SPUMA_NCCL(ncclCommInitRank(&m->comm, m->n_ranks, id, m->rank));
+    }
+    SPUMA_CUDA(cudaStreamSynchronize(s));
+    m->stats.blocks_per_grid = m->grid;
+    m->stats.threads_per_block = kThreads;
+    m->stats.batch_iterations = m->batch;
+    return SPUMA_OK;
+}
+
+spuma_status spuma_mesh_create(const spuma_mesh_desc* d, spuma_mesh* out)
+{
+    if (!out) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "out is NULL");
+    *out = nullptr;
+    if (!d) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "desc is NULL");
+    if (d->abi_version != SPUMA_ABI_VERSION) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "abi_version mismatch");
+    if (d->n_cells < 0 || d->n_faces < 0) return set_error(SPUMA_ERR_LENGTH_MISMATCH, "negative size");
+    if (d->n_patches < 0 || (d->n_patches > 0 && !d->patches))
+        return set_error(SPUMA_ERR_INVALID_ARGUMENT, "patches is NULL");
+    if (d->n_ranks < 1 || d->rank < 0 || d->rank >= d->n_ranks)
+        return set_error(SPUMA_ERR_INVALID_ARGUMENT, "bad rank / n_ranks");
+    if (d->n_faces > 0 && (!d->owner || !d->neighbour || !d->Sf || !d->magSf || !d->Cf))
+        return set_error(SPUMA_ERR_INVALID_ARGUMENT, "NULL face array");
+    if (d->n_cells > 0 && !d->C) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "C is NULL");
+    spuma_mesh m = new spuma_mesh_s();
+    spuma_status st = mesh_create_impl(d, m);
+    if (st != SPUMA_OK) {
+        spuma_free(m);
+        return st;
+    }
+    g_err.clear();
+    *out = m;
+    return SPUMA_OK;
+}
+
+spuma_status spuma_assemble_laplacian(spuma_mesh m, const spuma_scalar* gamma, const spuma_scalar* const* patch_value,
+                                      spuma_label ref_cell, spuma_scalar ref_value, spuma_scalar* diag,
+                                      spuma_scalar* upper, spuma_scalar* source, spuma_scalar* iface_coeffs)
+{
+    if (!m) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "mesh is NULL");
+    if ((m->N > 0 && (!diag || !source)) || (m->F > 0 && !upper))
+        return set_error(SPUMA_ERR_INVALID_ARGUMENT, "NULL diag/upper/source");
+    if (m->n_iface > 0 && !iface_coeffs) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "iface_coeffs is NULL");
+    if (ref_cell >= m->N) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "ref_cell out of range");
+    cudaStream_t s = m->stream;
+    // fixedValue values -> concatenated boundary buffer
+    for (size_t p = 0; p < m->patches.size(); ++p) {
+        const Patch& P = m->patches[p];
+        if (P.kind != SPUMA_PATCH_FIXED_VALUE || P.n_faces == 0) continue;
+        if (!patch_value || !patch_value[p])
+            return set_error(SPUMA_ERR_INVALID_ARGUMENT, "missing fixedValue values for patch " + std::to_string(p));
+        SPUMA_CUDA(cudaMemcpyAsync(m->d_bvalue + P.offset, patch_value[p], sizeof(double) * P.n_faces,
+                                   cudaMemcpyDefault, s));
+    }
+    const double* g = nullptr;
+    if (gamma) SPUMA_TRY(cells_in(m, gamma, R_GAMMA, &g));
+    // internal outputs
+    const double* src_in = nullptr;
+    SPUMA_TRY(cells_in(m, source, R_SOURCE, &src_in));
+    double* src_i = const_cast<double*>(src_in);
+    double* diag_i = diag;
+    if (m->renumber || !is_device_ptr(diag)) {
+        if (!m->d_cell_b) SPUMA_TRY(dalloc(&m->d_cell_b, m->N));
+        diag_i = m->d_cell_b;
+    }
+    double* upper_i = upper;
+    if (m->renumber || !is_device_ptr(upper)) {
+        if (!m->d_face_a) SPUMA_TRY(dalloc(&m->d_face_a, m->F));
+        upper_i = m->d_face_a;
+    }
+    double* iface_i = iface_coeffs;
+    if (m->n_iface && !is_device_ptr(iface_coeffs)) {
+        if (!m->d_iface_a) SPUMA_TRY(dalloc(&m->d_iface_a, m->n_iface));
+        iface_i = m->d_iface_a;
+    }
+    // gamma halo (processor faces interpolate gamma in global orientation)
+    if (g && m->n_iface) SPUMA_TRY(halo_exchange(m, g, m->d_bgamma_r, s));
+    const int rc = ref_cell < 0 ? -1 : (m->renumber ? m->h_perm[ref_cell] : ref_cell);
+    const MeshArgs a = mesh_args(m);
+    if (m->timing) SPUMA_CUDA(cudaEventRecord(m->asm_ev[0], s));
+    launch_face_coeffs(s, m->grid_faces, m->F, m->d_owner, m->d_neighbour, m->d_delta, m->d_weights, m->d_magSf, g,
+                       upper_i);
+    launch_diag_gather(s, m->grid, a, upper_i, m->d_bStart, m->d_bFace, m->d_bkind, m->d_bcell, m->d_bproc,
+                       m->d_bmagSf, m->d_bdelta, m->d_bweight, m->d_bvalue, m->d_bgamma_r, m->d_bis_owner, g, rc,
+                       ref_value, diag_i, src_i, iface_i);
+    if (m->timing) SPUMA_CUDA(cudaEventRecord(m->asm_ev[1], s));
+    m->stats.kernel_launches += 2;
+    SPUMA_TRY(cells_out(m, diag, diag_i));
+    SPUMA_TRY(faces_out(m, upper, upper_i));
+    SPUMA_TRY(cells_out(m, source, src_i));
+    if (iface_i != iface_coeffs)
+        SPUMA_CUDA(cudaMemcpyAsync(iface_coeffs, iface_i, sizeof(double) * m->n_iface, cudaMemcpyDefault, s));
+    SPUMA_CUDA(cudaStreamSynchronize(s));
+    SPUMA_CUDA(cudaGetLastError());
+    if (m->timing) {
+        float ms = 0.f;
+        SPUMA_CUDA(cudaEventElapsedTime(&ms, m->asm_ev[0], m->asm_ev[1]));
+        m->stats.phase_ms[3] += ms;
+        m->stats.phase_count[3] += 1;
+    }
+    return SPUMA_OK;
+}
+
+spuma_status spuma_amul(spuma_mesh m, const spuma_scalar* diag, const spuma_scalar* upper,
+                        const spuma_scalar* iface_coeffs, const spuma_scalar* x, spuma_scalar* y)
+{
+    if (!m) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "mesh is NULL");
+    if (m->N > 0 && (!diag || !x || !y)) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "NULL array");
+    if (m->F > 0 && !upper) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "upper is NULL");
+    if (m->n_iface > 0 && !iface_coeffs) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "iface_coeffs is NULL");
+    cudaStream_t s = m->stream;
+    const double *d_i, *u_i, *x_i, *if_i = nullptr;
+    SPUMA_TRY(cells_in(m, diag, R_DIAG, &d_i));
+    SPUMA_TRY(faces_in(m, upper, &u_i));
+    SPUMA_TRY(cells_in(m, x, R_X, &x_i));
+    if (m->n_iface) SPUMA_TRY(iface_in(m, iface_coeffs, &if_i));
+    double* y_i = y;
+    if (m->renumber || !is_device_ptr(y)) {
+        if (!m->d_cell_t) SPUMA_TRY(dalloc(&m->d_cell_t, m->N));
+        y_i = m->d_cell_t;
+    }
+    SPUMA_TRY(halo_exchange(m, x_i, m->ws.xr, s));
+    launch_amul(s, m->grid, mesh_args(m), d_i, u_i, if_i, x_i, m->ws.xr, y_i);
+    m->stats.kernel_launches += 1;
+    SPUMA_TRY(cells_out(m, y, y_i));
+    SPUMA_CUDA(cudaStreamSynchronize(s));
+    SPUMA_CUDA(cudaGetLastError());
+    return SPUMA_OK;
+}
+
+spuma_status spuma_pcg_solve(spuma_mesh m, const spuma_scalar* diag, const spuma_scalar* upper,
+                             const spuma_scalar* iface_coeffs, const spuma_scalar* source, spuma_scalar* psi,
+                             const spuma_solver_controls* ctl, spuma_solver_perf* perf)
+{
+    if (!m) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "mesh is NULL");
+    if (!ctl || !perf) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "NULL controls/perf");
+    if (m->N > 0 && (!diag || !source || !psi)) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "NULL array");
+    if (m->F > 0 && !upper) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "upper is NULL");
+    if (m->n_iface > 0 && !iface_coeffs) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "iface_coeffs is NULL");
+    if (ctl->max_iter < 0 || ctl->min_iter < 0) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "negative iteration limit");
+    cudaStream_t s = m->stream;
+    DevPtrs P{};
+    const double* psi_in = nullptr;
+    SPUMA_TRY(cells_in(m, diag, R_DIAG, &P.diag));
+    SPUMA_TRY(faces_in(m, upper, &P.upper));
+    SPUMA_TRY(cells_in(m, source, R_SOURCE, &P.source));
+    SPUMA_TRY(cells_in(m, psi, R_PSI, &psi_in));
+    P.psi = const_cast<double*>(psi_in);
+    if (m->n_iface) SPUMA_TRY(iface_in(m, iface_coeffs, &P.iface));
+    *m->h_ptrs = P;
+    SPUMA_CUDA(cudaMemcpyAsync(m->ws.ptrs, m->h_ptrs, sizeof(DevPtrs), cudaMemcpyHostToDevice, s));
+    launch_scal_init(s, m->ws, *ctl, m->n_ranks);
+
+    // ---- A6 setup
+    const MeshArgs a = mesh_args(m);
+    const bool fin = m->n_ranks == 1;
+    SPUMA_TRY(halo_exchange(m, P.psi, m->ws.xr, s));
+    launch_setup1(s, m->grid, a, m->ws, fin);
+    if (!fin) SPUMA_TRY(reduce_finalize(m, 1, s));
+    launch_setup2(s, m->grid, a, m->ws, fin);
+    if (!fin) SPUMA_TRY(reduce_finalize(m, 2, s));
+    m->stats.kernel_launches += 3;
+
+    // ---- A7-A11 in captured batches, ping-pong; host reads the scalars once per batch
+    SPUMA_TRY(build_graphs(m));
+    SPUMA_CUDA(cudaMemcpyAsync(&m->h_scal[1], m->ws.scal, sizeof(DevScal), cudaMemcpyDeviceToHost, s));
+    SPUMA_CUDA(cudaStreamSynchronize(s));
+    uint64_t launched_batches = 0;
+    int done = m->h_scal[1].done;
+    int b = 0;
+    int prev_n = 0;
+    while (!done) {
+        const int g = b & 1;
+        SPUMA_CUDA(cudaGraphLaunch(m->gexec[g], s));
+        SPUMA_CUDA(cudaMemcpyAsync(&m->h_scal[g], m->ws.scal, sizeof(DevScal), cudaMemcpyDeviceToHost, s));
+        SPUMA_CUDA(cudaEventRecord(m->batch_done[g], s));
+        ++launched_batches;
+        if (b > 0) {  // wait for the previous batch while this one runs
+            const int pg = (b - 1) & 1;
+            SPUMA_CUDA(cudaEventSynchronize(m->batch_done[pg]));
+            if (m->timing) {
+                const int n_it = std::min(m->batch, m->h_scal[pg].n - prev_n);
+                for (int k = 0; k < n_it; ++k)
+                    for (int ph = 0; ph < 3; ++ph) {
+                        float ms = 0.f;
+                        static const int from[3] = {0, 2, 4};
+                        SPUMA_CUDA(cudaEventElapsedTime(&ms, m->tev[pg][k * 6 + from[ph]], m->tev[pg][k * 6 + from[ph] + 1]));
+                        m->stats.phase_ms[ph] += ms;
+                        m->stats.phase_count[ph] += 1;
+                    }
+                prev_n = m->h_scal[pg].n;
+            }
+            done = m->h_scal[pg].done;
+        }
+        ++b;
+        if (b > 2 + (ctl->max_iter + m->batch - 1) / m->batch + 1)
+            return set_error(SPUMA_ERR_STATE, "PCG batch loop did not terminate");
+    }
+    SPUMA_CUDA(cudaStreamSynchronize(s));
+    if (m->timing && b > 0) {  // the last batch's events (already complete)
+        const int pg = (b - 1) & 1;
+        const int n_it = std::min(m->batch, m->h_scal[pg].n - prev_n);
+        for (int k = 0; k < n_it; ++k)
+            for (int ph = 0; ph < 3; ++ph) {
+                float ms = 0.f;
+                static const int from[3] = {0, 2, 4};
+                SPUMA_CUDA(cudaEventElapsedTime(&ms, m->tev[pg][k * 6 + from[ph]], m->tev[pg][k * 6 + from[ph] + 1]));
+                m->stats.phase_ms[ph] += ms;
+                m->stats.phase_count[ph] += 1;
+            }
+    }
+    DevScal fs;
+    SPUMA_CUDA(cudaMemcpy(&fs, m->ws.scal, sizeof(DevScal), cudaMemcpyDeviceToHost));
+    SPUMA_CUDA(cudaGetLastError());
+    perf->initial_residual = fs.init;
+    perf->final_residual = fs.fin;
+    perf->n_iterations = fs.n;
+    perf->converged = fs.converged;
+    perf->singular = fs.singular;
+    m->stats.kernel_launches += launched_batches * (uint64_t)m->batch * launches_per_iteration(m);
+    m->stats.solves += 1;
+    m->stats.iterations += fs.n;
+    SPUMA_TRY(cells_out(m, psi, P.psi));
+    SPUMA_CUDA(cudaStreamSynchronize(s));
+    return SPUMA_OK;
+}
+
+spuma_status spuma_mesh_get_addressing(spuma_mesh m, spuma_label* perm, spuma_label* owner, spuma_label* neighbour,
+                                       spuma_label* owner_start, spuma_label* losort, spuma_label* losort_start,
+                                       spuma_label* face_map)
+{
+    if (!m) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "mesh is NULL");
+    auto cp = [](spuma_label* dst, const std::vector<int>& v) {
+        if (dst && !v.empty()) std::memcpy(dst, v.data(), v.size() * sizeof(int));
+    };
+    cp(perm, m->h_perm);
+    cp(owner, m->h_owner);
+    cp(neighbour, m->h_neighbour);
+    cp(owner_start, m->h_ownerStart);
+    cp(losort, m->h_losort);
+    cp(losort_start, m->h_losortStart);
+    cp(face_map, m->h_face_map);
+    return SPUMA_OK;
+}
+
+spuma_status spuma_mesh_get_geometry(spuma_mesh m, spuma_scalar* delta, spuma_scalar* weights, spuma_scalar* bdelta)
+{
+    if (!m) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "mesh is NULL");
+    std::vector<double> d(m->F), w(m->F);
+    SPUMA_CUDA(cudaMemcpy(d.data(), m->d_delta, sizeof(double) * m->F, cudaMemcpyDeviceToHost));
+    SPUMA_CUDA(cudaMemcpy(w.data(), m->d_weights, sizeof(double) * m->F, cudaMemcpyDeviceToHost));
+    for (int g = 0; g < m->F; ++g) {
+        if (delta) delta[m->h_face_map[g]] = d[g];
+        if (weights) weights[m->h_face_map[g]] = w[g];
+    }
+    if (bdelta && m->Fb) SPUMA_CUDA(cudaMemcpy(bdelta, m->d_bdelta, sizeof(double) * m->Fb, cudaMemcpyDeviceToHost));
+    return SPUMA_OK;
+}
+
+spuma_status spuma_get_stats(spuma_mesh m, spuma_stats* out)
+{
+    if (!m || !out) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "NULL argument");
+    m->stats.timing_enabled = m->timing;
+    m->stats.batch_iterations = m->batch;
+    *out = m->stats;
+    return SPUMA_OK;
+}
+
+spuma_status spuma_reset_stats(spuma_mesh m)
+{
+    if (!m) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "mesh is NULL");
+    const int g = m->stats.blocks_per_grid, t = m->stats.threads_per_block;
+    m->stats = spuma_stats{};
+    m->stats.blocks_per_grid = g;
+    m->stats.threads_per_block = t;
+    return SPUMA_OK;
+}
+
+spuma_status spuma_set_timing(spuma_mesh m, int enable)
+{
+    if (!m) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "mesh is NULL");
+    m->timing = enable != 0;
+    return SPUMA_OK;
+}
+
+spuma_status spuma_set_batch(spuma_mesh m, int iterations)
+{
+    if (!m) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "mesh is NULL");
+    if (iterations < 1 || iterations > 256) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "batch out of range");
+    m->batch = iterations;
+    return SPUMA_OK;
+}
+
+}  // extern "C"

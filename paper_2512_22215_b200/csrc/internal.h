@@ -1,0 +1,182 @@
+// internal.h -- libspuma internals (not part of the C-ABI; see include/spuma.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "spuma.h"
+
+namespace spuma {
+
+constexpr int kThreads = 256;      // threads per CTA of every cell/face kernel (8 warps)
+constexpr int kMaxPartials = 4;    // reduction values per kernel
+constexpr int kPhases = 4;         // timing phases (spuma_stats.phase_ms)
+
+// Device-resident PCG state (A6-A12).  Written only by the finalisation code
+// (last CTA of a reduction kernel, or the 1-CTA finalise kernel when P > 1).
+struct DevScal {
+    double wArA, wArAold, wApA, alpha, beta;
+    double normFactor, init, fin, xbar;
+    double tol, rel_tol;
+    double rank_part[4];   // this rank's partial sums of the current reduction (P > 1)
+    int n, done, singular, converged;
+    int max_iter, min_iter, n_ranks, pad;
+    unsigned int ticket[8];
+};
+
+// Per-call pointers of the hot loop (device copy read by the captured kernels,
+// so one captured graph serves every spuma_pcg_solve call on the handle).
+struct DevPtrs {
+    const double* diag;
+    const double* upper;
+    const double* iface;
+    const double* source;
+    double* psi;
+};
+
+// Mesh-constant kernel arguments (captured by value).
+struct MeshArgs {
+    int N, F;
+    const int* ownerStart;   // [N+1]
+    const int* losortStart;  // [N+1]
+    const int* losort;       // [F]  faces sorted by neighbour (stable)
+    const int* ownerLo;      // [F]  owner[losort[k]]
+    const int* neighbour;    // [F]
+    const int* owner;        // [F]
+    // processor interfaces, per cell in (patch, face) order
+    const int* ifStart;      // [N+1] or nullptr (no interfaces)
+    const int* ifIdx;        // [n_iface] index into iface / x_remote arrays
+    int n_iface;
+};
+
+struct Workspace {
+    double *wA, *rA, *pA, *rD, *sumA;
+    double* xr;        // [n_iface] x_remote received from the neighbours
+    double* part;      // [kMaxPartials * grid] per-CTA partials
+    DevScal* scal;
+    DevPtrs* ptrs;
+};
+
+struct Patch {
+    int kind, n_faces, offset;   // offset into the concatenated boundary arrays
+    int neighbour_rank;          // processor
+    int iface_offset;            // processor: offset into the iface arrays
+};
+
+}  // namespace spuma
+
+struct spuma_mesh_s {
+    int N = 0, F = 0, Fb = 0, n_iface = 0;
+    int renumber = 0;
+    int rank = 0, n_ranks = 1;
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    cudaStream_t comm_stream = nullptr;
+    ncclComm_t comm = nullptr;
+
+    std::vector<spuma::Patch> patches;
+    // host copies of the derived addressing (internal numbering) for diagnostics
+    std::vector<int> h_perm, h_face_map, h_owner, h_neighbour, h_ownerStart, h_losort, h_losortStart;
+
+    // device: addressing (internal numbering)
+    int *d_owner = nullptr, *d_neighbour = nullptr, *d_ownerStart = nullptr, *d_losortStart = nullptr;
+    int *d_losort = nullptr, *d_ownerLo = nullptr;
+    int *d_perm = nullptr, *d_face_map = nullptr;  // renumber only
+    // device: geometry
+    double *d_delta = nullptr, *d_weights = nullptr, *d_magSf = nullptr;
+    // device: boundary faces, concatenated in patch order (all patches)
+    int *d_bkind = nullptr, *d_bcell = nullptr, *d_bproc = nullptr;  // bproc: iface ordinal or -1
+    double *d_bmagSf = nullptr, *d_bdelta = nullptr, *d_bweight = nullptr, *d_bvalue = nullptr;
+    double* d_bgamma_r = nullptr;    // [n_iface] remote gamma (gamma halo)
+    signed char* d_bis_owner = nullptr;
+    int *d_bStart = nullptr, *d_bFace = nullptr;   // per-cell lists of contributing boundary faces
+    // device: interfaces
+    int *d_ifStart = nullptr, *d_ifIdx = nullptr, *d_if_cell = nullptr;  // if_cell: [n_iface] local cell
+    double* d_sendbuf = nullptr;     // [n_iface] packed x for the neighbours
+    // staging (renumbering / host pointers), allocated on first use
+    double *d_cell_a = nullptr, *d_cell_b = nullptr, *d_cell_c = nullptr, *d_cell_d = nullptr,
+           *d_cell_e = nullptr, *d_cell_t = nullptr;
+    double *d_face_a = nullptr, *d_face_t = nullptr, *d_iface_a = nullptr;
+
+    spuma::Workspace ws{};
+    spuma::DevPtrs* h_ptrs = nullptr;   // pinned
+    spuma::DevScal* h_scal = nullptr;   // pinned [2]
+    int grid = 0;                       // CTAs of the cell kernels (fixed: deterministic partials)
+    int grid_faces = 0;
+
+    // captured iteration batches (ping-pong) and timing events
+    int batch = 16;
+    bool timing = false;
+    cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+    bool gexec_timed = false;
+    int gexec_batch = 0;
+    std::vector<cudaEvent_t> tev[2];     // [batch * 3 * 2] per graph
+    cudaEvent_t batch_done[2] = {nullptr, nullptr};
+    cudaEvent_t asm_ev[2] = {nullptr, nullptr};
+
+    spuma_stats stats{};
+};
+
+// error plumbing (api.cu)
+namespace spuma {
+spuma_status set_error(spuma_status s, const std::string& msg);
+}
+
+#define SPUMA_CUDA(call)                                                                             \
+    do {                                                                                             \
+        cudaError_t e_ = (call);                                                                     \
+        if (e_ != cudaSuccess)                                                                       \
+            return spuma::set_error(e_ == cudaErrorMemoryAllocation ? SPUMA_ERR_OUT_OF_MEMORY : SPUMA_ERR_CUDA, \
+                                    std::string(#call) + ": " + cudaGetErrorString(e_));             \
+    } while (0)
+
+#define SPUMA_NCCL(call)                                                                             \
+    do {                                                                                             \
+        ncclResult_t r_ = (call);                                                                    \
+        if (r_ != ncclSuccess)                                                                       \
+            return spuma::set_error(SPUMA_ERR_NCCL, std::string(#call) + ": " + ncclGetErrorString(r_)); \
+    } while (0)
+
+#define SPUMA_TRY(call)                      \
+    do {                                     \
+        spuma_status s_ = (call);            \
+        if (s_ != SPUMA_OK) return s_;       \
+    } while (0)
+
+// kernels.cu launchers (all asynchronous on `s`)
+namespace spuma {
+void launch_geometry(cudaStream_t s, int F, const int* owner, const int* neighbour, const double* Sf,
+                     const double* magSf, const double* C, const double* Cf, double* delta, double* weights);
+void launch_bgeometry(cudaStream_t s, int Fb, const int* kind, const int* bcell, const double* bSf,
+                      const double* bmagSf, const double* bCf, const double* C, const double* nC,
+                      const signed char* is_owner, double* bdelta, double* bweight);
+void launch_face_coeffs(cudaStream_t s, int grid, int F, const int* owner, const int* neighbour,
+                        const double* delta, const double* weights, const double* magSf, const double* gamma,
+                        double* upper);
+void launch_diag_gather(cudaStream_t s, int grid, const MeshArgs& a, const double* upper, const int* bStart,
+                        const int* bFace, const int* bkind, const int* bcell, const int* bproc,
+                        const double* bmagSf, const double* bdelta, const double* bweight, const double* bvalue,
+                        const double* bgamma_r, const signed char* bis_owner, const double* gamma, int ref_cell,
+                        double ref_value, double* diag, double* source, double* iface);
+void launch_amul(cudaStream_t s, int grid, const MeshArgs& a, const double* diag, const double* upper,
+                 const double* iface, const double* x, const double* xr, double* y);
+void launch_gather(cudaStream_t s, int n, const int* idx, const double* in, double* out);   // out[i] = in[idx[i]]
+void launch_scatter(cudaStream_t s, int n, const int* idx, const double* in, double* out);  // out[idx[i]] = in[i]
+void launch_pack(cudaStream_t s, int n, const int* cell, const double* x, double* out);     // out[i] = x[cell[i]]
+
+// PCG (A6-A12). `fin` = true when this rank finalises itself (P == 1).
+void launch_setup1(cudaStream_t s, int grid, const MeshArgs& a, const Workspace& w, bool fin);
+void launch_setup2(cudaStream_t s, int grid, const MeshArgs& a, const Workspace& w, bool fin);
+void launch_direction(cudaStream_t s, int grid, const MeshArgs& a, const Workspace& w);
+void launch_amul_dot(cudaStream_t s, int grid, const MeshArgs& a, const Workspace& w, bool fin);
+void launch_update(cudaStream_t s, int grid, const MeshArgs& a, const Workspace& w, bool fin);
+// P > 1: finalise from the gathered rank partials ([n_ranks][4], rank order)
+void launch_finalize(cudaStream_t s, int stage, const double* gathered, int n_ranks, const Workspace& w);
+void launch_scal_init(cudaStream_t s, const Workspace& w, const spuma_solver_controls& c, int n_ranks);
+int occupancy_grid(int N, int* grid_faces, int F);
+}  // namespace spuma

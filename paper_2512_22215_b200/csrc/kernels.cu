@@ -1,0 +1,627 @@
+// kernels.cu -- sm_100a kernels of the SPUMA pressure path.
+//
+// Everything here is fp64 and bandwidth-bound (~0.16 flop/B,
+// no dense contraction), so there are no tensor-core paths: the kernels are
+// coalesced streaming passes and deterministic per-cell GATHERS over the
+// losort/ownerStart restructuring of the faces, replacing the paper's
+// atomic face-loop scatters.
+//
+// Bit-exactness: the library is compiled with --fmad=false, so a*b+c is a
+// DMUL followed by a DADD, exactly as the oracle (-ffp-contract=off); the
+// per-row accumulation order is the oracle's face order (reading Q10):
+// diag*x, then faces with neighbour == c in losort order, then faces with
+// owner == c in face order, then processor interfaces in (patch, face) order.
+// Reductions use a fixed shape (per-thread grid-stride order, warp shuffle
+// tree, CTA tree, last-CTA sum of the per-CTA partials in CTA order), so
+// results are run-to-run bitwise reproducible.
+#include "internal.h"
+
+#include <cstdio>
+
+namespace spuma {
+
+// ---------------------------------------------------------------------------
+// helpers
+// ---------------------------------------------------------------------------
+
+// Sum NV values over the CTA; the result is valid in thread 0.
+template <int NV>
+__device__ __forceinline__ void cta_sum(double (&v)[NV])
+{
+    __shared__ double sh[NV][kThreads / 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int i = 0; i < NV; ++i)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v[i] += __shfl_down_sync(0xffffffffu, v[i], o);
+    if (lane == 0)
+#pragma unroll
+        for (int i = 0; i < NV; ++i) sh[i][warp] = v[i];
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            double t = lane < kThreads / 32 ? sh[i][lane] : 0.0;
+#pragma unroll
+            for (int o = 4; o > 0; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
+            v[i] = t;
+        }
+    }
+    __syncthreads();
+}
+
+// Store this CTA's partials; return true in the LAST CTA to finish, which then
+// holds the grid-wide sums (CTA order) in v (thread 0).
+template <int NV>
+__device__ __forceinline__ bool grid_sum(double (&v)[NV], double* part, unsigned int* ticket)
+{
+    __shared__ bool last;
+    cta_sum<NV>(v);
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int i = 0; i < NV; ++i) part[i * gridDim.x + blockIdx.x] = v[i];
+        __threadfence();
+        last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return false;
+    __threadfence();
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+        double t = 0.0;
+        for (int b = threadIdx.x; b < (int)gridDim.x; b += kThreads) t += __ldcg(part + i * gridDim.x + b);
+        v[i] = t;
+    }
+    cta_sum<NV>(v);
+    if (threadIdx.x == 0) *ticket = 0u;
+    return true;
+}
+
+__device__ __forceinline__ bool conv(double r, double init, double tol, double rel_tol)
+{
+    return (r < tol) || (rel_tol > 1e-20 && r < rel_tol * init);
+}
+
+// Finalisation steps of the PCG scalars, from global sums g[].
+__device__ void finalize(DevScal* s, int stage, const double* g)
+{
+    switch (stage) {
+    case 1:  // gAverage(psi) = gSum(psi) / gSum(nCells)
+        s->xbar = g[0] / g[1];
+        break;
+    case 2: {  // normFactor, initial residual, first wArA, iterate-at-all decision (Q1, Q3)
+        s->normFactor = g[0] + 1e-20;
+        s->init = g[1] / s->normFactor;
+        s->fin = s->init;
+        s->wArA = g[2];
+        s->wArAold = 1e20;
+        s->n = 0;
+        s->singular = 0;
+        s->converged = conv(s->fin, s->init, s->tol, s->rel_tol);
+        s->done = !(s->min_iter > 0 || !s->converged);
+        break;
+    }
+    case 3: {  // alpha = wArA / wApA, checkSingularity (Q4)
+        s->wApA = g[0];
+        if (fabs(s->wApA) / s->normFactor < 1e-300) {
+            s->singular = 1;
+            s->done = 1;
+        } else {
+            s->alpha = s->wArA / s->wApA;
+        }
+        break;
+    }
+    case 4: {  // final residual, convergence, loop condition, beta for the next direction
+        s->fin = g[1] / s->normFactor;
+        s->n = s->n + 1;
+        const bool c = conv(s->fin, s->init, s->tol, s->rel_tol);
+        s->converged = c;
+        if (!((s->n < s->max_iter && !c) || s->n < s->min_iter)) s->done = 1;
+        s->wArAold = s->wArA;
+        s->wArA = g[0];
+        s->beta = s->wArA / s->wArAold;
+        break;
+    }
+    }
+}
+
+// y_c = (A x)_c in the oracle's face order (reading Q10).
+__device__ __forceinline__ double amul_row(const MeshArgs& a, int c, const double* __restrict__ diag,
+                                           const double* __restrict__ upper, const double* __restrict__ iface,
+                                           const double* __restrict__ x, const double* __restrict__ xr,
+                                           double* rowsum)
+{
+    double s = diag[c] * x[c];
+    double r = diag[c];
+    const int k1 = a.losortStart[c + 1];
+    for (int k = a.losortStart[c]; k < k1; ++k) {
+        const double u = upper[a.losort[k]];
+        s = s + u * x[a.ownerLo[k]];
+        r = r + u;
+    }
+    const int f1 = a.ownerStart[c + 1];
+    for (int f = a.ownerStart[c]; f < f1; ++f) {
+        const double u = upper[f];
+        s = s + u * x[a.neighbour[f]];
+        r = r + u;
+    }
+    if (a.ifStart) {
+        const int j1 = a.ifStart[c + 1];
+        for (int j = a.ifStart[c]; j < j1; ++j) {
+            const int i = a.ifIdx[j];
+            s = s + iface[i] * xr[i];
+            r = r + iface[i];
+        }
+    }
+    if (rowsum) *rowsum = r;
+    return s;
+}
+
+// ---------------------------------------------------------------------------
+// A3 geometry: nonOrthDeltaCoeffs (stabilised form) and linear weights
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ void face_geometry(const double* CP, const double* CN, const double* S, double magS,
+                                              const double* Cf, double* delta, double* weight)
+{
+    const double dx = CN[0] - CP[0], dy = CN[1] - CP[1], dz = CN[2] - CP[2];
+    const double nx = S[0] / magS, ny = S[1] / magS, nz = S[2] / magS;
+    const double nd = nx * dx + ny * dy + nz * dz;
+    const double magd = sqrt(dx * dx + dy * dy + dz * dz);
+    const double lim = 0.05 * magd;
+    *delta = 1.0 / (nd > lim ? nd : lim);
+    const double ox = Cf[0] - CP[0], oy = Cf[1] - CP[1], oz = Cf[2] - CP[2];
+    const double ex = CN[0] - Cf[0], ey = CN[1] - Cf[1], ez = CN[2] - Cf[2];
+    const double so = fabs(S[0] * ox + S[1] * oy + S[2] * oz);
+    const double sn = fabs(S[0] * ex + S[1] * ey + S[2] * ez);
+    const double den = so + sn;
+    *weight = den > 1e-150 ? sn / den : 0.5;
+}
+
+__global__ void k_geometry(int F, const int* __restrict__ owner, const int* __restrict__ neighbour,
+                           const double* __restrict__ Sf, const double* __restrict__ magSf,
+                           const double* __restrict__ C, const double* __restrict__ Cf, double* __restrict__ delta,
+                           double* __restrict__ weights)
+{
+    for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < F; f += gridDim.x * blockDim.x)
+        face_geometry(C + 3 * (size_t)owner[f], C + 3 * (size_t)neighbour[f], Sf + 3 * (size_t)f, magSf[f],
+                      Cf + 3 * (size_t)f, delta + f, weights + f);
+}
+
+__global__ void k_bgeometry(int Fb, const int* __restrict__ kind, const int* __restrict__ bcell,
+                            const double* __restrict__ bSf, const double* __restrict__ bmagSf,
+                            const double* __restrict__ bCf, const double* __restrict__ C,
+                            const double* __restrict__ nC, const signed char* __restrict__ is_owner,
+                            double* __restrict__ bdelta, double* __restrict__ bweight)
+{
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < Fb; i += gridDim.x * blockDim.x) {
+        const double* cp = C + 3 * (size_t)bcell[i];
+        const double* S = bSf + 3 * (size_t)i;
+        if (kind[i] == SPUMA_PATCH_PROCESSOR) {
+            // global orientation: the rank holding the undecomposed owner plays P (reading Q9)
+            double Sg[3];
+            const double *CP, *CN;
+            if (is_owner[i]) {
+                Sg[0] = S[0], Sg[1] = S[1], Sg[2] = S[2];
+                CP = cp;
+                CN = nC + 3 * (size_t)i;
+            } else {
+                Sg[0] = -S[0], Sg[1] = -S[1], Sg[2] = -S[2];
+                CP = nC + 3 * (size_t)i;
+                CN = cp;
+            }
+            face_geometry(CP, CN, Sg, bmagSf[i], bCf + 3 * (size_t)i, bdelta + i, bweight + i);
+        } else if (kind[i] == SPUMA_PATCH_EMPTY) {
+            bdelta[i] = 0.0;
+            bweight[i] = 0.0;
+        } else {
+            const double nx = S[0] / bmagSf[i], ny = S[1] / bmagSf[i], nz = S[2] / bmagSf[i];
+            const double* cf = bCf + 3 * (size_t)i;
+            const double ex = cf[0] - cp[0], ey = cf[1] - cp[1], ez = cf[2] - cp[2];
+            bdelta[i] = 1.0 / (nx * ex + ny * ey + nz * ez);
+            bweight[i] = 0.0;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// A4 face coefficients and A5 diagonal + reference + boundary (gather)
+// ---------------------------------------------------------------------------
+
+__global__ void __launch_bounds__(kThreads) k_face_coeffs(int F, const int* __restrict__ owner,
+                                                         const int* __restrict__ neighbour,
+                                                         const double* __restrict__ delta,
+                                                         const double* __restrict__ weights,
+                                                         const double* __restrict__ magSf,
+                                                         const double* __restrict__ gamma,
+                                                         double* __restrict__ upper)
+{
+    for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < F; f += gridDim.x * blockDim.x) {
+        double gf = 1.0;
+        if (gamma) {
+            const double gn = gamma[neighbour[f]];
+            gf = weights[f] * (gamma[owner[f]] - gn) + gn;
+        }
+        upper[f] = delta[f] * (gf * magSf[f]);
+    }
+}
+
+__global__ void __launch_bounds__(kThreads)
+    k_diag_gather(MeshArgs a, const double* __restrict__ upper, const int* __restrict__ bStart,
+                  const int* __restrict__ bFace, const int* __restrict__ bkind, const int* __restrict__ bproc,
+                  const double* __restrict__ bmagSf, const double* __restrict__ bdelta,
+                  const double* __restrict__ bweight, const double* __restrict__ bvalue,
+                  const double* __restrict__ bgamma_r, const signed char* __restrict__ bis_owner,
+                  const double* __restrict__ gamma, int ref_cell, double ref_value, double* __restrict__ diag,
+                  double* __restrict__ source, double* __restrict__ iface)
+{
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < a.N; c += gridDim.x * blockDim.x) {
+        double d = 0.0;
+        const int k1 = a.losortStart[c + 1];
+        for (int k = a.losortStart[c]; k < k1; ++k) d = d - upper[a.losort[k]];
+        const int f1 = a.ownerStart[c + 1];
+        for (int f = a.ownerStart[c]; f < f1; ++f) d = d - upper[f];
+        const int j0 = bStart[c], j1 = bStart[c + 1];
+        if (c == ref_cell || j1 > j0) {
+            double s = source[c];
+            if (c == ref_cell) {  // setReference, before any boundary coefficient (Q7)
+                s = s + d * ref_value;
+                d = d + d;
+            }
+            const double gP = gamma ? gamma[c] : 1.0;
+            for (int j = j0; j < j1; ++j) {
+                const int b = bFace[j];
+                if (bkind[b] == SPUMA_PATCH_FIXED_VALUE) {
+                    const double gms = gP * bmagSf[b];
+                    d = d + gms * (-bdelta[b]);
+                    s = s + (-gms) * (bdelta[b] * bvalue[b]);
+                } else {  // processor (reading Q9): global-orientation interpolation
+                    const int i = bproc[b];
+                    double gf = 1.0;
+                    if (gamma) {
+                        const double gr = bgamma_r[i];
+                        const double gO = bis_owner[b] ? gP : gr;
+                        const double gN = bis_owner[b] ? gr : gP;
+                        gf = bweight[b] * (gO - gN) + gN;
+                    }
+                    const double gms = gf * bmagSf[b];
+                    d = d + gms * (-bdelta[b]);
+                    iface[i] = bdelta[b] * gms;
+                }
+            }
+            source[c] = s;
+        }
+        diag[c] = d;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// A7 Amul (plain; diagnostics and the multi-rank setup)
+// ---------------------------------------------------------------------------
+
+__global__ void __launch_bounds__(kThreads) k_amul(MeshArgs a, const double* __restrict__ diag,
+                                                  const double* __restrict__ upper,
+                                                  const double* __restrict__ iface, const double* __restrict__ x,
+                                                  const double* __restrict__ xr, double* __restrict__ y)
+{
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < a.N; c += gridDim.x * blockDim.x)
+        y[c] = amul_row(a, c, diag, upper, iface, x, xr, nullptr);
+}
+
+__global__ void k_gather(int n, const int* __restrict__ idx, const double* __restrict__ in, double* __restrict__ out)
+{
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = in[idx[i]];
+}
+
+__global__ void k_scatter(int n, const int* __restrict__ idx, const double* __restrict__ in, double* __restrict__ out)
+{
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[idx[i]] = in[i];
+}
+
+// ---------------------------------------------------------------------------
+// A6 PCG setup
+// ---------------------------------------------------------------------------
+
+// wA = A psi, sumA = A 1 (lduMatrix::sumA), partial sum(psi) and nCells
+__global__ void __launch_bounds__(kThreads) k_setup1(MeshArgs a, Workspace w, int fin)
+{
+    const DevPtrs p = *w.ptrs;
+    double v[2] = {0.0, 0.0};
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < a.N; c += gridDim.x * blockDim.x) {
+        double rs;
+        w.wA[c] = amul_row(a, c, p.diag, p.upper, p.iface, p.psi, w.xr, &rs);
+        w.sumA[c] = rs;
+        v[0] += p.psi[c];
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) v[1] = (double)a.N;
+    if (grid_sum<2>(v, w.part, &w.scal->ticket[0]) && threadIdx.x == 0) {
+        if (fin) finalize(w.scal, 1, v);
+        else w.scal->rank_part[0] = v[0], w.scal->rank_part[1] = v[1];
+    }
+}
+
+// rA = source - wA; rD = 1/diag; partials of |wA - xRef| + |source - xRef|, |rA|, (rD rA) rA
+__global__ void __launch_bounds__(kThreads) k_setup2(MeshArgs a, Workspace w, int fin)
+{
+    const DevPtrs p = *w.ptrs;
+    const double xbar = w.scal->xbar;
+    double v[3] = {0.0, 0.0, 0.0};
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < a.N; c += gridDim.x * blockDim.x) {
+        const double b = p.source[c], wa = w.wA[c];
+        const double r = b - wa;
+        const double xref = w.sumA[c] * xbar;
+        const double rd = 1.0 / p.diag[c];
+        w.rA[c] = r;
+        w.rD[c] = rd;
+        v[0] += fabs(wa - xref) + fabs(b - xref);
+        v[1] += fabs(r);
+        v[2] += (rd * r) * r;
+    }
+    if (grid_sum<3>(v, w.part, &w.scal->ticket[1]) && threadIdx.x == 0) {
+        if (fin) finalize(w.scal, 2, v);
+        else w.scal->rank_part[0] = v[0], w.scal->rank_part[1] = v[1], w.scal->rank_part[2] = v[2];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// A7-A11 hot loop (each kernel is a no-op once the device 'done' flag is set)
+// ---------------------------------------------------------------------------
+
+// A11 pA = rD rA + beta pA  (n == 0: pA = rD rA)
+__global__ void __launch_bounds__(kThreads) k_direction(int N, Workspace w)
+{
+    if (w.scal->done) return;
+    const bool first = w.scal->n == 0;
+    const double beta = w.scal->beta;
+    const int np = N >> 1;
+    const double2* __restrict__ rD2 = reinterpret_cast<const double2*>(w.rD);
+    const double2* __restrict__ rA2 = reinterpret_cast<const double2*>(w.rA);
+    double2* __restrict__ pA2 = reinterpret_cast<double2*>(w.pA);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < np; i += gridDim.x * blockDim.x) {
+        const double2 d = rD2[i], r = rA2[i];
+        double2 q;
+        if (first) {
+            q.x = d.x * r.x;
+            q.y = d.y * r.y;
+        } else {
+            const double2 p = pA2[i];
+            q.x = d.x * r.x + beta * p.x;
+            q.y = d.y * r.y + beta * p.y;
+        }
+        pA2[i] = q;
+    }
+    if ((N & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+        const int c = N - 1;
+        w.pA[c] = first ? w.rD[c] * w.rA[c] : w.rD[c] * w.rA[c] + beta * w.pA[c];
+    }
+}
+
+// A7 + A8: wA = A pA, partial wA.pA -> alpha
+__global__ void __launch_bounds__(kThreads) k_amul_dot(MeshArgs a, Workspace w, int fin)
+{
+    if (w.scal->done) return;
+    const DevPtrs p = *w.ptrs;
+    double v[1] = {0.0};
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < a.N; c += gridDim.x * blockDim.x) {
+        const double y = amul_row(a, c, p.diag, p.upper, p.iface, w.pA, w.xr, nullptr);
+        w.wA[c] = y;
+        v[0] += y * w.pA[c];
+    }
+    if (grid_sum<1>(v, w.part, &w.scal->ticket[2]) && threadIdx.x == 0) {
+        if (fin) finalize(w.scal, 3, v);
+        else w.scal->rank_part[0] = v[0];
+    }
+}
+
+// A9 + A10: psi += alpha pA; rA -= alpha wA; partials (rD rA) rA and |rA|
+__global__ void __launch_bounds__(kThreads) k_update(int N, Workspace w, int fin)
+{
+    if (w.scal->done) return;
+    const DevPtrs p = *w.ptrs;
+    const double alpha = w.scal->alpha;
+    double v[2] = {0.0, 0.0};
+    const int np = N >> 1;
+    double2* __restrict__ psi2 = reinterpret_cast<double2*>(p.psi);
+    double2* __restrict__ rA2 = reinterpret_cast<double2*>(w.rA);
+    const double2* __restrict__ pA2 = reinterpret_cast<const double2*>(w.pA);
+    const double2* __restrict__ wA2 = reinterpret_cast<const double2*>(w.wA);
+    const double2* __restrict__ rD2 = reinterpret_cast<const double2*>(w.rD);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < np; i += gridDim.x * blockDim.x) {
+        double2 x = psi2[i], r = rA2[i];
+        const double2 pp = pA2[i], ww = wA2[i], d = rD2[i];
+        x.x = x.x + alpha * pp.x;
+        x.y = x.y + alpha * pp.y;
+        r.x = r.x - alpha * ww.x;
+        r.y = r.y - alpha * ww.y;
+        psi2[i] = x;
+        rA2[i] = r;
+        v[0] += (d.x * r.x) * r.x;
+        v[0] += (d.y * r.y) * r.y;
+        v[1] += fabs(r.x);
+        v[1] += fabs(r.y);
+    }
+    if ((N & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+        const int c = N - 1;
+        p.psi[c] = p.psi[c] + alpha * w.pA[c];
+        const double r = w.rA[c] - alpha * w.wA[c];
+        w.rA[c] = r;
+        v[0] += (w.rD[c] * r) * r;
+        v[1] += fabs(r);
+    }
+    if (grid_sum<2>(v, w.part, &w.scal->ticket[3]) && threadIdx.x == 0) {
+        if (fin) finalize(w.scal, 4, v);
+        else w.scal->rank_part[0] = v[0], w.scal->rank_part[1] = v[1];
+    }
+}
+
+// P > 1: global sums of the gathered rank partials in rank order, then finalise
+__global__ void k_finalize(int stage, const double* __restrict__ gathered, int n_ranks, Workspace w)
+{
+    if (stage >= 3 && w.scal->done) return;
+    double g[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int r = 0; r < n_ranks; ++r)
+        for (int i = 0; i < 4; ++i) g[i] += gathered[4 * r + i];
+    finalize(w.scal, stage, g);
+}
+
+__global__ void k_scal_init(DevScal* s, double tol, double rel_tol, int max_iter, int min_iter, int n_ranks)
+{
+    s->tol = tol;
+    s->rel_tol = rel_tol;
+    s->max_iter = max_iter;
+    s->min_iter = min_iter;
+    s->n_ranks = n_ranks;
+    s->n = 0;
+    s->done = 0;
+    s->singular = 0;
+    s->converged = 0;
+    s->alpha = s->beta = 0.0;
+    for (int i = 0; i < 4; ++i) s->rank_part[i] = 0.0;
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+
+static int g_sms = 0;
+
+static int sms()
+{
+    if (!g_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (g_sms <= 0) g_sms = 148;
+    }
+    return g_sms;
+}
+
+template <class K>
+static int grid_for(K kernel, long long work, int per_thread = 1)
+{
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kThreads, 0);
+    if (occ <= 0) occ = 1;
+    long long need = (work + (long long)kThreads * per_thread - 1) / ((long long)kThreads * per_thread);
+    long long cap = (long long)occ * sms();
+    long long g = need < cap ? need : cap;
+    return (int)(g < 1 ? 1 : g);
+}
+
+int occupancy_grid(int N, int* grid_faces, int F)
+{
+    // the largest grid any reduction kernel uses (sizes the partials buffer)
+    int g = grid_for(k_setup1, N);
+    g = std::max(g, grid_for(k_setup2, N));
+    g = std::max(g, grid_for(k_amul_dot, N));
+    g = std::max(g, grid_for(k_update, N, 2));
+    if (grid_faces) *grid_faces = grid_for(k_face_coeffs, F);
+    return g;
+}
+
+void launch_geometry(cudaStream_t s, int F, const int* owner, const int* neighbour, const double* Sf,
+                     const double* magSf, const double* C, const double* Cf, double* delta, double* weights)
+{
+    if (F <= 0) return;
+    k_geometry<<<grid_for(k_geometry, F), kThreads, 0, s>>>(F, owner, neighbour, Sf, magSf, C, Cf, delta, weights);
+}
+
+void launch_bgeometry(cudaStream_t s, int Fb, const int* kind, const int* bcell, const double* bSf,
+                      const double* bmagSf, const double* bCf, const double* C, const double* nC,
+                      const signed char* is_owner, double* bdelta, double* bweight)
+{
+    if (Fb <= 0) return;
+    k_bgeometry<<<grid_for(k_bgeometry, Fb), kThreads, 0, s>>>(Fb, kind, bcell, bSf, bmagSf, bCf, C, nC, is_owner,
+                                                               bdelta, bweight);
+}
+
+void launch_face_coeffs(cudaStream_t s, int grid, int F, const int* owner, const int* neighbour,
+                        const double* delta, const double* weights, const double* magSf, const double* gamma,
+                        double* upper)
+{
+    if (F <= 0) return;
+    (void)grid;
+    k_face_coeffs<<<grid_for(k_face_coeffs, F), kThreads, 0, s>>>(F, owner, neighbour, delta, weights, magSf, gamma,
+                                                                  upper);
+}
+
+void launch_diag_gather(cudaStream_t s, int grid, const MeshArgs& a, const double* upper, const int* bStart,
+                        const int* bFace, const int* bkind, const int* bcell, const int* bproc,
+                        const double* bmagSf, const double* bdelta, const double* bweight, const double* bvalue,
+                        const double* bgamma_r, const signed char* bis_owner, const double* gamma, int ref_cell,
+                        double ref_value, double* diag, double* source, double* iface)
+{
+    if (a.N <= 0) return;
+    (void)grid;
+    (void)bcell;
+    k_diag_gather<<<grid_for(k_diag_gather, a.N), kThreads, 0, s>>>(a, upper, bStart, bFace, bkind, bproc, bmagSf,
+                                                                    bdelta, bweight, bvalue, bgamma_r, bis_owner,
+                                                                    gamma, ref_cell, ref_value, diag, source, iface);
+}
+
+void launch_amul(cudaStream_t s, int grid, const MeshArgs& a, const double* diag, const double* upper,
+                 const double* iface, const double* x, const double* xr, double* y)
+{
+    if (a.N <= 0) return;
+    (void)grid;
+    k_amul<<<grid_for(k_amul, a.N), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y);
+}
+
+void launch_gather(cudaStream_t s, int n, const int* idx, const double* in, double* out)
+{
+    if (n <= 0) return;
+    k_gather<<<grid_for(k_gather, n), kThreads, 0, s>>>(n, idx, in, out);
+}
+
+void launch_scatter(cudaStream_t s, int n, const int* idx, const double* in, double* out)
+{
+    if (n <= 0) return;
+    k_scatter<<<grid_for(k_scatter, n), kThreads, 0, s>>>(n, idx, in, out);
+}
+
+void launch_pack(cudaStream_t s, int n, const int* cell, const double* x, double* out)
+{
+    launch_gather(s, n, cell, x, out);
+}
+
+void launch_setup1(cudaStream_t s, int grid, const MeshArgs& a, const Workspace& w, bool fin)
+{
+    (void)grid;
+    k_setup1<<<grid_for(k_setup1, a.N), kThreads, 0, s>>>(a, w, fin ? 1 : 0);
+}
+
+void launch_setup2(cudaStream_t s, int grid, const MeshArgs& a, const Workspace& w, bool fin)
+{
+    (void)grid;
+    k_setup2<<<grid_for(k_setup2, a.N), kThreads, 0, s>>>(a, w, fin ? 1 : 0);
+}
+
+void launch_direction(cudaStream_t s, int grid, const MeshArgs& a, const Workspace& w)
+{
+    (void)grid;
+    k_direction<<<grid_for(k_direction, a.N, 2), kThreads, 0, s>>>(a.N, w);
+}
+
+void launch_amul_dot(cudaStream_t s, int grid, const MeshArgs& a, const Workspace& w, bool fin)
+{
+    (void)grid;
+    k_amul_dot<<<grid_for(k_amul_dot, a.N), kThreads, 0, s>>>(a, w, fin ? 1 : 0);
+}
+
+void launch_update(cudaStream_t s, int grid, const MeshArgs& a, const Workspace& w, bool fin)
+{
+    (void)grid;
+    k_update<<<grid_for(k_update, a.N, 2), kThreads, 0, s>>>(a.N, w, fin ? 1 : 0);
+}
+
+void launch_finalize(cudaStream_t s, int stage, const double* gathered, int n_ranks, const Workspace& w)
+{
+    k_finalize<<<1, 1, 0, s>>>(stage, gathered, n_ranks, w);
+}
+
+void launch_scal_init(cudaStream_t s, const Workspace& w, const spuma_solver_controls& c, int n_ranks)
+{
+    k_scal_init<<<1, 1, 0, s>>>(w.scal, c.tolerance, c.rel_tol, c.max_iter, c.min_iter, n_ranks);
+}
+
+}  // namespace spuma

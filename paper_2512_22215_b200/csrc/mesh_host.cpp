@@ -1,0 +1,152 @@
+// mesh_host.cpp -- host-side mesh logic of libspuma: addressing validation (A0),
+// reverse Cuthill-McKee renumbering (A1), face re-keying, and the derived
+// addressing ownerStart / losort / losortStart (A2).  Runs once per mesh.
+//
+// A1's rule (the paper is silent, BASELINE.json asks for "renumbered cells";
+// reading Q12): start at the unvisited cell of minimum degree
+// (ties: smallest index), FIFO BFS, a dequeued cell enqueues its unvisited
+// neighbours sorted by (degree, index), restart per component, reverse.
+#include <algorithm>
+#include <cstdint>
+#include <numeric>
+#include <vector>
+
+#include "host.h"
+
+namespace spuma {
+
+bool valid_addressing(int N, int F, const int* owner, const int* neighbour, std::string* why)
+{
+    for (int f = 0; f < F; ++f) {
+        const int o = owner[f], n = neighbour[f];
+        if (o < 0 || o >= N || n < 0 || n >= N) {
+            *why = "face " + std::to_string(f) + ": cell index out of range";
+            return false;
+        }
+        if (o >= n) {
+            *why = "face " + std::to_string(f) + ": owner >= neighbour";
+            return false;
+        }
+        if (f && (o < owner[f - 1] || (o == owner[f - 1] && n < neighbour[f - 1]))) {
+            *why = "face " + std::to_string(f) + ": faces not sorted by (owner, neighbour)";
+            return false;
+        }
+    }
+    return true;
+}
+
+std::vector<int> rcm_permutation(int N, int F, const int* owner, const int* neighbour)
+{
+    std::vector<int> deg(N, 0), start(N + 1, 0), adj(2 * (size_t)F);
+    for (int f = 0; f < F; ++f) {
+        ++deg[owner[f]];
+        ++deg[neighbour[f]];
+    }
+    for (int c = 0; c < N; ++c) start[c + 1] = start[c] + deg[c];
+    {
+        std::vector<int> pos(start.begin(), start.end() - 1);
+        for (int f = 0; f < F; ++f) {
+            adj[pos[owner[f]]++] = neighbour[f];
+            adj[pos[neighbour[f]]++] = owner[f];
+        }
+    }
+    auto less = [&](int a, int b) { return deg[a] != deg[b] ? deg[a] < deg[b] : a < b; };
+    std::vector<int> by_degree(N);
+    std::iota(by_degree.begin(), by_degree.end(), 0);
+    std::sort(by_degree.begin(), by_degree.end(), less);
+
+    std::vector<char> seen(N, 0);
+    std::vector<int> order;
+    order.reserve(N);
+    std::vector<int> cand;
+    size_t next_start = 0;
+    while ((int)order.size() < N) {
+        while (seen[by_degree[next_start]]) ++next_start;
+        const int s = by_degree[next_start];
+        seen[s] = 1;
+        size_t head = order.size();
+        order.push_back(s);
+        while (head < order.size()) {
+            const int c = order[head++];
+            cand.clear();
+            for (int e = start[c]; e < start[c + 1]; ++e) {
+                const int d = adj[e];
+                if (!seen[d]) {
+                    seen[d] = 1;
+                    cand.push_back(d);
+                }
+            }
+            std::sort(cand.begin(), cand.end(), less);
+            order.insert(order.end(), cand.begin(), cand.end());
+        }
+    }
+    std::vector<int> perm(N);
+    for (int k = 0; k < N; ++k) perm[order[k]] = N - 1 - k;
+    return perm;
+}
+
+void rekey_faces(int N, int F, const int* perm, const int* owner, const int* neighbour, std::vector<int>& owner_out,
+                 std::vector<int>& neighbour_out, std::vector<int>& face_map, std::vector<char>& flip)
+{
+    std::vector<int> lo(F), hi(F), tmp(F);
+    for (int f = 0; f < F; ++f) {
+        const int a = perm[owner[f]], b = perm[neighbour[f]];
+        lo[f] = std::min(a, b);
+        hi[f] = std::max(a, b);
+    }
+    // stable by (lo, hi, old face): LSD counting sort, hi then lo
+    std::vector<int64_t> cnt(N + 1);
+    std::fill(cnt.begin(), cnt.end(), 0);
+    for (int f = 0; f < F; ++f) ++cnt[hi[f] + 1];
+    for (int c = 0; c < N; ++c) cnt[c + 1] += cnt[c];
+    for (int f = 0; f < F; ++f) tmp[cnt[hi[f]]++] = f;
+    std::fill(cnt.begin(), cnt.end(), 0);
+    for (int f = 0; f < F; ++f) ++cnt[lo[f] + 1];
+    for (int c = 0; c < N; ++c) cnt[c + 1] += cnt[c];
+    face_map.assign(F, 0);
+    for (int t = 0; t < F; ++t) {
+        const int f = tmp[t];
+        face_map[cnt[lo[f]]++] = f;
+    }
+    owner_out.resize(F);
+    neighbour_out.resize(F);
+    flip.resize(F);
+    for (int g = 0; g < F; ++g) {
+        const int f = face_map[g];
+        owner_out[g] = lo[f];
+        neighbour_out[g] = hi[f];
+        flip[g] = perm[owner[f]] > perm[neighbour[f]];
+    }
+}
+
+void derived_addressing(int N, int F, const int* owner, const int* neighbour, std::vector<int>& ownerStart,
+                        std::vector<int>& losort, std::vector<int>& losortStart, std::vector<int>& ownerLo)
+{
+    ownerStart.assign(N + 1, 0);
+    for (int f = 0; f < F; ++f) ++ownerStart[owner[f] + 1];
+    for (int c = 0; c < N; ++c) ownerStart[c + 1] += ownerStart[c];
+    losortStart.assign(N + 1, 0);
+    for (int f = 0; f < F; ++f) ++losortStart[neighbour[f] + 1];
+    for (int c = 0; c < N; ++c) losortStart[c + 1] += losortStart[c];
+    losort.assign(F, 0);
+    ownerLo.assign(F, 0);
+    std::vector<int> pos(losortStart.begin(), losortStart.end() - 1);
+    for (int f = 0; f < F; ++f) losort[pos[neighbour[f]]++] = f;  // stable: ascending face index
+    for (int k = 0; k < F; ++k) ownerLo[k] = owner[losort[k]];
+}
+
+void cell_lists(int N, const std::vector<int>& cell_of, const std::vector<char>& keep, std::vector<int>& start,
+                std::vector<int>& items)
+{
+    start.assign(N + 1, 0);
+    const int n = (int)cell_of.size();
+    for (int i = 0; i < n; ++i)
+        if (keep[i]) ++start[cell_of[i] + 1];
+    for (int c = 0; c < N; ++c) start[c + 1] += start[c];
+    items.assign(start[N], 0);
+    std::vector<int> pos(start.begin(), start.end() - 1);
+    for (int i = 0; i < n; ++i)
+        if (keep[i]) items[pos[cell_of[i]]++] = i;  // stable: input order
+}
+
+}  // namespace spuma

@@ -1,0 +1,287 @@
+"""Thin ctypes binding of libspuma (include/spuma.h) -- argument marshalling only.
+
+Every step of the path runs in libspuma's CUDA kernels; this module converts
+numpy arrays / torch tensors to pointers and C structs.  Names follow the
+C-ABI (``spuma_mesh_create`` -> ``mesh_create`` ...).  There is no CPU
+fallback: if libspuma.so is missing and cannot be built, import fails; if no
+CUDA device is usable, every compute call raises SpumaError(SPUMA_ERR_CUDA).
+
+Arrays: torch CUDA tensors (device pointers, used in place), torch CPU tensors
+or numpy arrays (host pointers; the library stages them).  fp64 scalars,
+int32 labels; tensors/arrays must be contiguous.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _build
+
+ZERO_GRADIENT, FIXED_VALUE, EMPTY, PROCESSOR = 0, 1, 2, 3
+STATUS = {0: "SPUMA_OK", 1: "SPUMA_ERR_INVALID_ARGUMENT", 2: "SPUMA_ERR_ADDRESSING", 3: "SPUMA_ERR_LENGTH_MISMATCH",
+          4: "SPUMA_ERR_CUDA", 5: "SPUMA_ERR_NCCL", 6: "SPUMA_ERR_OUT_OF_MEMORY", 7: "SPUMA_ERR_STATE"}
+ABI_VERSION = 1
+
+_vp, _ci, _cd, _lab = ctypes.c_void_p, ctypes.c_int, ctypes.c_double, ctypes.c_int32
+
+
+class SpumaError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class PatchDesc(ctypes.Structure):
+    _fields_ = [("kind", _ci), ("n_faces", _lab), ("face_cells", _vp), ("Sf", _vp), ("magSf", _vp), ("Cf", _vp),
+                ("neighbour_rank", _ci), ("global_face", _vp), ("neighbour_C", _vp), ("is_owner", _vp)]
+
+
+class MeshDesc(ctypes.Structure):
+    _fields_ = [("abi_version", _ci), ("n_cells", _lab), ("n_faces", _lab), ("owner", _vp), ("neighbour", _vp),
+                ("Sf", _vp), ("magSf", _vp), ("C", _vp), ("Cf", _vp), ("n_patches", _ci),
+                ("patches", ctypes.POINTER(PatchDesc)), ("renumber", _ci), ("pointers_on_device", _ci),
+                ("cuda_stream", _vp), ("rank", _ci), ("n_ranks", _ci), ("nccl_unique_id", _vp)]
+
+
+class SolverControls(ctypes.Structure):
+    _fields_ = [("tolerance", _cd), ("rel_tol", _cd), ("max_iter", _ci), ("min_iter", _ci)]
+
+
+class SolverPerf(ctypes.Structure):
+    _fields_ = [("initial_residual", _cd), ("final_residual", _cd), ("n_iterations", _ci), ("converged", _ci),
+                ("singular", _ci)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("kernel_launches", ctypes.c_uint64), ("solves", ctypes.c_uint64), ("iterations", ctypes.c_uint64),
+                ("timing_enabled", _ci), ("phase_ms", _cd * 4), ("phase_count", ctypes.c_uint64 * 4),
+                ("blocks_per_grid", _ci), ("threads_per_block", _ci), ("batch_iterations", _ci)]
+
+    def as_dict(self):
+        d = {k: getattr(self, k) for k, _ in self._fields_}
+        d["phase_ms"] = list(self.phase_ms)
+        d["phase_count"] = list(self.phase_count)
+        return d
+
+
+_lib = None
+
+
+def lib():
+    """Load libspuma.so (building it in-tree with nvcc if missing or stale)."""
+    global _lib
+    if _lib is None:
+        path = _build.SO
+        if _build.stale():
+            _build.build()
+        L = ctypes.CDLL(path)
+        L.spuma_mesh_create.argtypes = [ctypes.POINTER(MeshDesc), ctypes.POINTER(_vp)]
+        L.spuma_assemble_laplacian.argtypes = [_vp, _vp, _vp, _lab, _cd, _vp, _vp, _vp, _vp]
+        L.spuma_pcg_solve.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, ctypes.POINTER(SolverControls),
+                                      ctypes.POINTER(SolverPerf)]
+        L.spuma_free.argtypes = [_vp]
+        L.spuma_free.restype = None
+        L.spuma_amul.argtypes = [_vp] * 6
+        L.spuma_mesh_get_addressing.argtypes = [_vp] * 8
+        L.spuma_mesh_get_geometry.argtypes = [_vp] * 4
+        L.spuma_get_stats.argtypes = [_vp, ctypes.POINTER(Stats)]
+        L.spuma_reset_stats.argtypes = [_vp]
+        L.spuma_set_timing.argtypes = [_vp, _ci]
+        L.spuma_set_batch.argtypes = [_vp, _ci]
+        L.spuma_nccl_get_unique_id.argtypes = [_vp]
+        L.spuma_last_error.restype = ctypes.c_char_p
+        L.spuma_abi_version.restype = _ci
+        for name in ("spuma_mesh_create", "spuma_assemble_laplacian", "spuma_pcg_solve", "spuma_amul",
+                     "spuma_mesh_get_addressing", "spuma_mesh_get_geometry", "spuma_get_stats",
+                     "spuma_reset_stats", "spuma_set_timing", "spuma_set_batch", "spuma_nccl_get_unique_id"):
+            getattr(L, name).restype = _ci
+        if L.spuma_abi_version() != ABI_VERSION:
+            raise SpumaError(1, "libspuma ABI version mismatch")
+        _lib = L
+    return _lib
+
+
+def _check(st: int):
+    if st != 0:
+        raise SpumaError(st, lib().spuma_last_error().decode())
+
+
+def _ptr(a, dtype):
+    """(pointer, keep-alive) for a numpy array / torch tensor / None."""
+    if a is None:
+        return None, None
+    try:
+        import torch
+        if isinstance(a, torch.Tensor):
+            want = torch.float64 if dtype == np.float64 else (torch.int32 if dtype == np.int32 else torch.int8)
+            if a.dtype != want:
+                raise TypeError(f"expected {want}, got {a.dtype}")
+            if not a.is_contiguous():
+                raise ValueError("tensor must be contiguous")
+            return a.data_ptr(), a
+    except ImportError:  # pragma: no cover
+        pass
+    arr = np.ascontiguousarray(a, dtype=dtype)
+    if arr is not a and isinstance(a, np.ndarray) and a.dtype == dtype and a.flags.c_contiguous:
+        arr = a
+    return arr.ctypes.data, arr
+
+
+def nccl_get_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().spuma_nccl_get_unique_id(buf))
+    return buf.raw
+
+
+class Mesh:
+    """A libspuma mesh handle (spuma_mesh)."""
+
+    def __init__(self, handle: int, n_cells: int, n_faces: int, n_iface: int, n_bfaces: int, keep):
+        self._h = handle
+        self.n_cells, self.n_faces, self.n_iface, self.n_bfaces = n_cells, n_faces, n_iface, n_bfaces
+        self._keep = keep
+
+    # ---------------------------------------------------------------- create / free
+    @classmethod
+    def mesh_create(cls, n_cells: int, owner, neighbour, Sf, magSf, C, Cf, patches: Sequence = (),
+                    renumber: bool = False, stream: Optional[int] = None, rank: int = 0, n_ranks: int = 1,
+                    nccl_unique_id: Optional[bytes] = None, pointers_on_device: bool = False) -> "Mesh":
+        """spuma_mesh_create.  ``patches``: objects with kind, face_cells, Sf, magSf, Cf and, for
+        processor patches, neighbour_rank, global_face, neighbour_C, is_owner."""
+        keep = []
+
+        def P(a, dt):
+            p, k = _ptr(a, dt)
+            keep.append(k)
+            return p
+
+        n_faces = int(len(owner))
+        descs = (PatchDesc * max(len(patches), 1))()
+        n_iface = n_b = 0
+        for i, p in enumerate(patches):
+            d = descs[i]
+            d.kind = int(p.kind)
+            d.n_faces = int(len(p.face_cells))
+            n_b += d.n_faces
+            d.face_cells = P(p.face_cells, np.int32)
+            d.Sf, d.magSf, d.Cf = P(p.Sf, np.float64), P(p.magSf, np.float64), P(p.Cf, np.float64)
+            if d.kind == PROCESSOR:
+                n_iface += d.n_faces
+                d.neighbour_rank = int(p.neighbour_rank)
+                d.global_face = P(p.global_face, np.int32)
+                d.neighbour_C = P(p.neighbour_C, np.float64)
+                d.is_owner = P(p.is_owner, np.int8)
+            else:
+                d.neighbour_rank = -1
+        keep.append(descs)
+        idbuf = None
+        if nccl_unique_id is not None:
+            idbuf = ctypes.create_string_buffer(bytes(nccl_unique_id), 128)
+            keep.append(idbuf)
+        desc = MeshDesc(ABI_VERSION, int(n_cells), n_faces, P(owner, np.int32), P(neighbour, np.int32),
+                        P(Sf, np.float64), P(magSf, np.float64), P(C, np.float64), P(Cf, np.float64),
+                        len(patches), descs, 1 if renumber else 0, 1 if pointers_on_device else 0,
+                        stream, rank, n_ranks, ctypes.cast(idbuf, _vp) if idbuf is not None else None)
+        h = _vp()
+        _check(lib().spuma_mesh_create(ctypes.byref(desc), ctypes.byref(h)))
+        return cls(h.value, int(n_cells), n_faces, n_iface, n_b, None)
+
+    @classmethod
+    def from_mesh(cls, mesh, **kw) -> "Mesh":
+        """Duck-typed: any object with n_cells, owner, neighbour, Sf, magSf, C, Cf, patches."""
+        return cls.mesh_create(mesh.n_cells, mesh.owner, mesh.neighbour, mesh.Sf, mesh.magSf, mesh.C, mesh.Cf,
+                               list(mesh.patches), **kw)
+
+    def free(self):
+        """spuma_free."""
+        if self._h:
+            lib().spuma_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+    # ---------------------------------------------------------------- hot path
+    def assemble_laplacian(self, gamma, patch_values, ref_cell: int, ref_value: float, diag, upper, source,
+                           iface_coeffs=None):
+        """spuma_assemble_laplacian; diag/upper/iface written, source read-modified-written in place."""
+        keep = []
+        arr = None
+        if patch_values is not None:
+            arr = (_vp * max(len(patch_values), 1))()
+            for i, v in enumerate(patch_values):
+                p, k = _ptr(v, np.float64)
+                keep.append(k)
+                arr[i] = p
+        g, kg = _ptr(gamma, np.float64)
+        d, kd = _ptr(diag, np.float64)
+        u, ku = _ptr(upper, np.float64)
+        s, ks = _ptr(source, np.float64)
+        f, kf = _ptr(iface_coeffs, np.float64)
+        _check(lib().spuma_assemble_laplacian(self._h, g, arr, int(ref_cell), float(ref_value), d, u, s, f))
+        return kd, ku, ks, kf
+
+    def pcg_solve(self, diag, upper, iface_coeffs, source, psi, tolerance=1e-6, rel_tol=0.0, max_iter=5000,
+                  min_iter=0) -> dict:
+        """spuma_pcg_solve; psi updated in place; returns the solver performance."""
+        ctl = SolverControls(tolerance, rel_tol, max_iter, min_iter)
+        perf = SolverPerf()
+        d, kd = _ptr(diag, np.float64)
+        u, ku = _ptr(upper, np.float64)
+        f, kf = _ptr(iface_coeffs, np.float64)
+        s, ks = _ptr(source, np.float64)
+        p, kp = _ptr(psi, np.float64)
+        _check(lib().spuma_pcg_solve(self._h, d, u, f, s, p, ctypes.byref(ctl), ctypes.byref(perf)))
+        return perf.as_dict()
+
+    def amul(self, diag, upper, iface_coeffs, x, y):
+        """spuma_amul: y = A x."""
+        d, kd = _ptr(diag, np.float64)
+        u, ku = _ptr(upper, np.float64)
+        f, kf = _ptr(iface_coeffs, np.float64)
+        xp, kx = _ptr(x, np.float64)
+        yp, ky = _ptr(y, np.float64)
+        _check(lib().spuma_amul(self._h, d, u, f, xp, yp))
+        return ky
+
+    # ---------------------------------------------------------------- diagnostics
+    def mesh_get_addressing(self) -> dict:
+        N, F = self.n_cells, self.n_faces
+        out = {k: np.empty(n, np.int32) for k, n in (("perm", N), ("owner", F), ("neighbour", F),
+                                                      ("owner_start", N + 1), ("losort", F),
+                                                      ("losort_start", N + 1), ("face_map", F))}
+        _check(lib().spuma_mesh_get_addressing(self._h, *[out[k].ctypes.data for k in
+                                                          ("perm", "owner", "neighbour", "owner_start", "losort",
+                                                           "losort_start", "face_map")]))
+        return out
+
+    def mesh_get_geometry(self) -> dict:
+        d, w, b = np.empty(self.n_faces), np.empty(self.n_faces), np.empty(max(self.n_bfaces, 1))
+        _check(lib().spuma_mesh_get_geometry(self._h, d.ctypes.data, w.ctypes.data, b.ctypes.data))
+        return {"delta": d, "weights": w, "bdelta": b[:self.n_bfaces]}
+
+    def get_stats(self) -> dict:
+        s = Stats()
+        _check(lib().spuma_get_stats(self._h, ctypes.byref(s)))
+        return s.as_dict()
+
+    def reset_stats(self):
+        _check(lib().spuma_reset_stats(self._h))
+
+    def set_timing(self, enable: bool):
+        _check(lib().spuma_set_timing(self._h, 1 if enable else 0))
+
+    def set_batch(self, iterations: int):
+        _check(lib().spuma_set_batch(self._h, int(iterations)))
+
+
+mesh_create = Mesh.mesh_create
