@@ -136,12 +136,24 @@ def load_traffic(workload):
 
 # ---------------------------------------------------------------------------- workload
 def build_workload(n, rank, world):
+    """C3: one n^3 block per rank of the global (n px, n py, n pz) cube (px,py,pz) = 1/2x1x1/2x2x1/2x2x2."""
     import gen
+    wl = f"C3 cube {n}^3 per GPU (weak), gamma=1, tol 1e-6"
     if world == 1:
         m = gen.cube(n)
         b = gen.rhs(m)
-        return m, b, 0, {"workload": f"C3 cube {n}^3 per GPU (weak), gamma=1, tol 1e-6", "cells_per_gpu": n ** 3}
-    raise NotImplementedError("multi-rank workload: see bench_multi")
+        return m, b, 0, {"workload": wl, "cells_per_gpu": n ** 3}
+    import torch
+    import torch.distributed as dist
+    nproc = gen.nproc_for(world)
+    m = gen.weak_block(n, nproc, rank)
+    # b = V (2U - 1) keyed by global cell id, minus the GLOBAL mean (all-reduced)
+    b = m.V * (2.0 * gen.uniform(gen.SEED_RHS, 0, m.gid) - 1.0)
+    t = torch.tensor([b.sum(), float(m.n_cells)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t)
+    b = b - float(t[0] / t[1])
+    ref = 0 if rank == 0 else -1  # global cell 0 lives on rank 0, local cell 0
+    return m, b, ref, {"workload": wl, "cells_per_gpu": n ** 3, "blocks": list(nproc)}
 
 
 # ---------------------------------------------------------------------------- oracle legs
@@ -203,13 +215,18 @@ def run_gpu(args, rank, world, local_rank):
     mesh, b, ref, cfg = build_workload(args.n, rank, world)
     N, F = mesh.n_cells, mesh.n_faces
     stream = torch.cuda.current_stream()
-    h = P.Mesh.from_mesh(mesh, stream=stream.cuda_stream)
+    uid = None
+    if world > 1:
+        obj = [P.nccl_get_unique_id() if rank == 0 else None]
+        torch.distributed.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    h = P.Mesh.from_mesh(mesh, stream=stream.cuda_stream, rank=rank, n_ranks=world, nccl_unique_id=uid)
     h.set_batch(args.batch)
     f64 = dict(dtype=torch.float64, device=dev)
     diag, upper = torch.empty(N, **f64), torch.empty(F, **f64)
     b_dev = torch.as_tensor(b, **f64)
     src, psi = torch.empty(N, **f64), torch.empty(N, **f64)
-    iface = None
+    iface = torch.empty(h.n_iface, **f64) if h.n_iface else None
     perfs = []
 
     def step():

@@ -65,6 +65,9 @@ def _L():
             lib.gen_gamma_lognormal.argtypes = [ctypes.c_int64, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p]
             lib.gen_rhs.argtypes = [ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p]
             lib.gen_uniform_fill.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]
+            lib.gen_hex_window.restype = ctypes.c_int
+            lib.gen_hex_window.argtypes = ([ctypes.c_int] * 3 + [ctypes.c_double] * 4 + [ctypes.c_uint64] +
+                                           [ctypes.c_int] * 6 + [ctypes.c_void_p] * 15)
             _lib = lib
     return _lib
 
@@ -353,13 +356,94 @@ def split_cell_field(x: np.ndarray, part: np.ndarray, nparts: Optional[int] = No
     return [np.ascontiguousarray(x[part == r]) for r in range(P)]
 
 
-def weak_block(n: int, nproc=(1, 1, 1), rank: int = 0) -> Mesh:
-    """C3: rank ``rank``'s n^3 block of the global (n px, n py, n pz) cube with h = 1/n.
+def lattice_block(gdims, L, lo, dims, rank_of, jitter: float = 0.0, seed: int = SEED_JITTER,
+                  names=("xmin", "xmax", "ymin", "ymax", "zmin", "zmax")) -> Mesh:
+    """One rank's window ``lo + [0, dims)`` of the global lattice ``gdims`` on box ``L``.
 
-    Built directly from the global lattice and decomposed, so ids/values are
-    those of the undecomposed mesh."""
+    Generated directly (no global mesh in memory): vertex coordinates use the
+    global formula, so geometry is bitwise that of ``box(*gdims, L)`` and both
+    sides of a cut agree.  Patches: the six walls (empty where the side is a
+    cut), then one processor patch per cut side, to ``rank_of(side)``, in
+    ascending neighbour rank (the ``decompose`` convention).  ``gface`` and
+    ``gid`` are the undecomposed ids.  V of cut-side cells accumulates its
+    faces in another order than ``box`` (inputs only; b is keyed by gid)."""
+    lib = _L()
+    NX, NY, NZ = gdims
+    nx, ny, nz = dims
+    nN = np.zeros(1, np.int64)
+    nF = np.zeros(1, np.int64)
+    ps = np.zeros(6, np.int64)
+    lib.gen_hex_counts(nx, ny, nz, _p(nN), _p(nF), _p(ps))
+    N, F, Fb = int(nN[0]), int(nF[0]), int(ps.sum())
+    owner, nbr = np.empty(F, np.int32), np.empty(F, np.int32)
+    Sf, magSf, Cf = np.empty((F, 3)), np.empty(F), np.empty((F, 3))
+    C, V, gid = np.empty((N, 3)), np.empty(N), np.empty(N, np.int32)
+    bc, bSf, bm, bCf = np.empty(Fb, np.int32), np.empty((Fb, 3)), np.empty(Fb), np.empty((Fb, 3))
+    bnC, bng, bgf = np.empty((Fb, 3)), np.empty(Fb, np.int32), np.empty(Fb, np.int32)
+    lib.gen_hex_window(NX, NY, NZ, float(L[0]), float(L[1]), float(L[2]), float(jitter), seed, lo[0], lo[1], lo[2],
+                       nx, ny, nz, _p(owner), _p(nbr), _p(Sf), _p(magSf), _p(Cf), _p(C), _p(V), _p(gid), _p(bc),
+                       _p(bSf), _p(bm), _p(bCf), _p(bnC), _p(bng), _p(bgf))
+    walls, procs = [], []
+    off = 0
+    for k in range(6):
+        n = int(ps[k])
+        sl = slice(off, off + n)
+        off += n
+        cut = n > 0 and bng[sl][0] >= 0
+        if not cut:
+            walls.append(Patch(names[k], ZERO_GRADIENT, bc[sl].copy(), bSf[sl].copy(), bm[sl].copy(), bCf[sl].copy()))
+            continue
+        walls.append(Patch(names[k], ZERO_GRADIENT, np.zeros(0, np.int32), np.zeros((0, 3)), np.zeros(0), np.zeros((0, 3))))
+        q = int(rank_of(k))
+        procs.append((q, Patch("", PROCESSOR, bc[sl].copy(), bSf[sl].copy(), bm[sl].copy(), bCf[sl].copy(),
+                               neighbour_rank=q, global_face=bgf[sl].copy(), neighbour_C=bnC[sl].copy(),
+                               is_owner=np.full(n, 1 if k % 2 == 1 else 0, np.int8),
+                               neighbour_gid=bng[sl].copy())))
+    procs.sort(key=lambda t: t[0])
+    me = None
+    patches = walls + [replace(p, name=f"procBoundary{me}to{q}") for q, p in procs]
+    # undecomposed face ids of the internal faces
+    gi = gid[owner]
+    ax = np.where(nbr - owner == 1, 0, np.where(nbr - owner == nx, 1, 2))
+    gface = _lattice_face_ids(gdims, gi, ax)
+    return Mesh(N, owner, nbr, Sf, magSf, Cf, C, V, patches, gid=gid, gface=gface, dims=tuple(gdims))
+
+
+def _lattice_face_ids(gdims, cell, axis):
+    """Face id in the undecomposed lattice of the face along ``axis`` owned by global cell ``cell``."""
+    NX, NY, NZ = (np.int64(v) for v in gdims)
+    c = cell.astype(np.int64)
+    i, j, k = c % NX, (c // NX) % NY, c // (NX * NY)
+    cx = (j + NY * k) * (NX - 1) + np.minimum(i, NX - 1)
+    cy = k * NX * (NY - 1) + np.where(j < NY - 1, j * NX + i, (NY - 1) * NX)
+    cz = np.where(k < NZ - 1, c, NX * NY * (NZ - 1))
+    fid = cx + cy + cz + ((axis >= 1) & (i < NX - 1)) + ((axis >= 2) & (j < NY - 1))
+    return fid.astype(np.int32)
+
+
+def block_grid(nproc):
+    """Rank of block (bx, by, bz) = bx + px (by + py bz) (matches ``block_parts``)."""
     px, py, pz = nproc
-    g = box(n * px, n * py, n * pz, (float(px), float(py), float(pz)))
+    return lambda bx, by, bz: bx + px * (by + py * bz)
+
+
+def weak_block(n: int, nproc=(1, 1, 1), rank: int = 0) -> Mesh:
+    """BASELINE config 3: rank ``rank``'s n^3 block of the global (n px, n py, n pz) unit-spaced
+    cube (h = 1/n), generated directly from the global lattice."""
+    px, py, pz = nproc
     if px * py * pz == 1:
-        return g
-    return decompose(g, block_parts(g, nproc), px * py * pz)[rank]
+        return cube(n)
+    bx, by, bz = rank % px, (rank // px) % py, rank // (px * py)
+    R = block_grid(nproc)
+    nb = {0: (bx - 1, by, bz), 1: (bx + 1, by, bz), 2: (bx, by - 1, bz), 3: (bx, by + 1, bz),
+          4: (bx, by, bz - 1), 5: (bx, by, bz + 1)}
+    m = lattice_block((n * px, n * py, n * pz), (float(px), float(py), float(pz)), (n * bx, n * by, n * bz),
+                      (n, n, n), lambda side: R(*nb[side]))
+    m.patches = [replace(p, name=f"procBoundary{rank}to{p.neighbour_rank}") if p.kind == PROCESSOR else p
+                 for p in m.patches]
+    return m
+
+
+def nproc_for(world: int):
+    """Block layout of BASELINE config 3: 1 -> (1,1,1), 2 -> (2,1,1), 4 -> (2,2,1), 8 -> (2,2,2)."""
+    return {1: (1, 1, 1), 2: (2, 1, 1), 4: (2, 2, 1), 8: (2, 2, 2)}.get(world) or (world, 1, 1)

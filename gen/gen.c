@@ -304,3 +304,164 @@ void gen_rhs(int64_t n, const int32_t* gid, const double* V, uint64_t seed, doub
     double mean = n > 0 ? s / (double)n : 0.0;
     for (int64_t c = 0; c < n; ++c) b[c] -= mean;
 }
+
+/* ------------------------------------------------------------------------- */
+/* window of a global lattice (one rank's block of a decomposed lattice)     */
+/* ------------------------------------------------------------------------- */
+
+typedef struct {
+    int NX, NY, NZ;
+    double Lx, Ly, Lz, jitter;
+    uint64_t seed;
+} glat;
+
+static void gvtx(const glat* g, int i, int j, int k, double* x)
+{
+    int64_t id = (int64_t)i + (int64_t)(g->NX + 1) * ((int64_t)j + (int64_t)(g->NY + 1) * k);
+    x[0] = g->Lx * i / g->NX;
+    x[1] = g->Ly * j / g->NY;
+    x[2] = g->Lz * k / g->NZ;
+    if (g->jitter > 0.0) {
+        if (i > 0 && i < g->NX) x[0] += (2.0 * gen_uniform(g->seed, 0, (uint64_t)id) - 1.0) * g->jitter * (g->Lx / g->NX);
+        if (j > 0 && j < g->NY) x[1] += (2.0 * gen_uniform(g->seed, 1, (uint64_t)id) - 1.0) * g->jitter * (g->Ly / g->NY);
+        if (k > 0 && k < g->NZ) x[2] += (2.0 * gen_uniform(g->seed, 2, (uint64_t)id) - 1.0) * g->jitter * (g->Lz / g->NZ);
+    }
+}
+
+static void gquad(const glat* g, int axis, int i, int j, int k, double sign, double* Sf, double* Cf, double* m)
+{
+    double v[4][3];
+    if (axis == 0) {
+        gvtx(g, i, j, k, v[0]); gvtx(g, i, j + 1, k, v[1]); gvtx(g, i, j + 1, k + 1, v[2]); gvtx(g, i, j, k + 1, v[3]);
+    } else if (axis == 1) {
+        gvtx(g, i, j, k, v[0]); gvtx(g, i, j, k + 1, v[1]); gvtx(g, i + 1, j, k + 1, v[2]); gvtx(g, i + 1, j, k, v[3]);
+    } else {
+        gvtx(g, i, j, k, v[0]); gvtx(g, i + 1, j, k, v[1]); gvtx(g, i + 1, j + 1, k, v[2]); gvtx(g, i, j + 1, k, v[3]);
+    }
+    quad(v[0], v[1], v[2], v[3], sign, Sf, Cf, m);
+}
+
+static void gcentre(const glat* g, int i, int j, int k, double* C)
+{
+    double v[8][3];
+    int n = 0;
+    for (int dk = 0; dk < 2; ++dk)
+        for (int dj = 0; dj < 2; ++dj)
+            for (int di = 0; di < 2; ++di) gvtx(g, i + di, j + dj, k + dk, v[n++]);
+    for (int d = 0; d < 3; ++d) {
+        double s = 0.0;
+        for (int q = 0; q < 8; ++q) s += v[q][d];
+        C[d] = 0.125 * s;
+    }
+}
+
+/* global face id of the face of cell (i,j,k) along axis (owner side) in the
+ * undecomposed lattice: faces owned by earlier cells + earlier axes of this cell */
+static int64_t gface_id(const glat* g, int i, int j, int k, int axis)
+{
+    const int64_t NX = g->NX, NY = g->NY, NZ = g->NZ;
+    const int64_t c = (int64_t)i + NX * ((int64_t)j + NY * k);
+    int64_t cx = ((int64_t)j + NY * k) * (NX - 1) + (i < NX - 1 ? i : NX - 1);
+    int64_t cy = (int64_t)k * NX * (NY - 1) + (j < NY - 1 ? (int64_t)j * NX + i : (NY - 1) * NX);
+    int64_t cz = k < NZ - 1 ? c : NX * NY * (NZ - 1);
+    int64_t id = cx + cy + cz;
+    if (axis >= 1 && i < NX - 1) id += 1;
+    if (axis >= 2 && j < NY - 1) id += 1;
+    return id;
+}
+
+void gen_window_counts(int nx, int ny, int nz, int64_t* n_cells, int64_t* n_faces, int64_t* side_sizes)
+{
+    gen_hex_counts(nx, ny, nz, n_cells, n_faces, side_sizes);
+}
+
+/*
+ * Cells [i0, i0+nx) x [j0, j0+ny) x [k0, k0+nz) of the global lattice NX x NY x NZ
+ * on [0,Lx]x[0,Ly]x[0,Lz].  Local cell id = li + nx (lj + ny lk).  Internal faces
+ * (both cells inside) in local (owner, neighbour) order.  The 6 sides of the window
+ * (xmin, xmax, ymin, ymax, zmin, zmax; cells in local id order) are returned as
+ * boundary faces with outward Sf; for each, if the side is interior to the global
+ * lattice, also the centre of the cell across (bnC), its global id (bngid) and
+ * the global face id (bgface); else bngid = -1.
+ * gid[c] = global cell id.  Vertex coordinates use the global formula, so both
+ * sides of a cut agree bitwise.
+ */
+int gen_hex_window(int NX, int NY, int NZ, double Lx, double Ly, double Lz, double jitter, uint64_t seed,
+                   int i0, int j0, int k0, int nx, int ny, int nz, int32_t* owner, int32_t* neighbour, double* Sf,
+                   double* magSf, double* Cf, double* C, double* V, int32_t* gid, int32_t* bcells, double* bSf,
+                   double* bmagSf, double* bCf, double* bnC, int32_t* bngid, int32_t* bgface)
+{
+    glat g = {NX, NY, NZ, Lx, Ly, Lz, jitter, seed};
+    const int64_t N = (int64_t)nx * ny * nz;
+    for (int k = 0; k < nz; ++k)
+        for (int j = 0; j < ny; ++j)
+            for (int i = 0; i < nx; ++i) {
+                int64_t c = (int64_t)i + (int64_t)nx * ((int64_t)j + (int64_t)ny * k);
+                gcentre(&g, i0 + i, j0 + j, k0 + k, C + 3 * c);
+                gid[c] = (int32_t)((int64_t)(i0 + i) + (int64_t)NX * ((int64_t)(j0 + j) + (int64_t)NY * (k0 + k)));
+                V[c] = 0.0;
+            }
+    int64_t f = 0;
+    for (int k = 0; k < nz; ++k)
+        for (int j = 0; j < ny; ++j)
+            for (int i = 0; i < nx; ++i) {
+                int64_t c = (int64_t)i + (int64_t)nx * ((int64_t)j + (int64_t)ny * k);
+                const int I = i0 + i, J = j0 + j, K = k0 + k;
+                if (i < nx - 1) {
+                    owner[f] = (int32_t)c; neighbour[f] = (int32_t)(c + 1);
+                    gquad(&g, 0, I + 1, J, K, 1.0, Sf + 3 * f, Cf + 3 * f, magSf + f); ++f;
+                }
+                if (j < ny - 1) {
+                    owner[f] = (int32_t)c; neighbour[f] = (int32_t)(c + nx);
+                    gquad(&g, 1, I, J + 1, K, 1.0, Sf + 3 * f, Cf + 3 * f, magSf + f); ++f;
+                }
+                if (k < nz - 1) {
+                    owner[f] = (int32_t)c; neighbour[f] = (int32_t)(c + (int64_t)nx * ny);
+                    gquad(&g, 2, I, J, K + 1, 1.0, Sf + 3 * f, Cf + 3 * f, magSf + f); ++f;
+                }
+            }
+    const int64_t F = f;
+    for (f = 0; f < F; ++f) {
+        double cs = Cf[3 * f] * Sf[3 * f] + Cf[3 * f + 1] * Sf[3 * f + 1] + Cf[3 * f + 2] * Sf[3 * f + 2];
+        V[owner[f]] += cs;
+        V[neighbour[f]] -= cs;
+    }
+    int64_t b = 0;
+    for (int axis = 0; axis < 3; ++axis)
+        for (int side = 0; side < 2; ++side) {
+            const int na = axis == 0 ? nx : (axis == 1 ? ny : nz);
+            const int la = side ? na - 1 : 0; /* local index along axis of the side's cells */
+            for (int k = 0; k < nz; ++k)
+                for (int j = 0; j < ny; ++j)
+                    for (int i = 0; i < nx; ++i) {
+                        const int li = axis == 0 ? la : i, lj = axis == 1 ? la : j, lk = axis == 2 ? la : k;
+                        if ((axis == 0 && i != 0) || (axis == 1 && j != 0) || (axis == 2 && k != 0)) continue;
+                        const int64_t c = (int64_t)li + (int64_t)nx * ((int64_t)lj + (int64_t)ny * lk);
+                        const int I = i0 + li, J = j0 + lj, K = k0 + lk;
+                        /* vertex plane of the face along the axis */
+                        int pi = I, pj = J, pk = K;
+                        if (side) { if (axis == 0) pi++; else if (axis == 1) pj++; else pk++; }
+                        bcells[b] = (int32_t)c;
+                        gquad(&g, axis, pi, pj, pk, side ? 1.0 : -1.0, bSf + 3 * b, bCf + 3 * b, bmagSf + b);
+                        V[c] += bCf[3 * b] * bSf[3 * b] + bCf[3 * b + 1] * bSf[3 * b + 1] + bCf[3 * b + 2] * bSf[3 * b + 2];
+                        int RI = I, RJ = J, RK = K; /* cell across */
+                        int inside;
+                        if (axis == 0) { RI += side ? 1 : -1; inside = RI >= 0 && RI < NX; }
+                        else if (axis == 1) { RJ += side ? 1 : -1; inside = RJ >= 0 && RJ < NY; }
+                        else { RK += side ? 1 : -1; inside = RK >= 0 && RK < NZ; }
+                        if (inside) {
+                            gcentre(&g, RI, RJ, RK, bnC + 3 * b);
+                            bngid[b] = (int32_t)((int64_t)RI + (int64_t)NX * ((int64_t)RJ + (int64_t)NY * RK));
+                            /* the global owner is the smaller id: the + side's local cell, the - side's remote cell */
+                            bgface[b] = side ? (int32_t)gface_id(&g, I, J, K, axis) : (int32_t)gface_id(&g, RI, RJ, RK, axis);
+                        } else {
+                            bnC[3 * b] = bnC[3 * b + 1] = bnC[3 * b + 2] = 0.0;
+                            bngid[b] = -1;
+                            bgface[b] = -1;
+                        }
+                        ++b;
+                    }
+        }
+    for (int64_t c = 0; c < N; ++c) V[c] = V[c] / 3.0;
+    return 0;
+}
