@@ -158,6 +158,121 @@ __device__ __forceinline__ double amul_row(const MeshArgs& a, int c, const doubl
 }
 
 // ---------------------------------------------------------------------------
+// A7 tiled Amul: a CTA owns a tile of kThreads consecutive cells.  Phase 1
+// computes every face product of the tile cooperatively -- the tile's
+// owner-side faces [ownerStart[c0], ownerStart[c1]) and neighbour-side entries
+// [losortStart[c0], losortStart[c1]) are CONTIGUOUS ranges, so the coefficient
+// and index loads are fully coalesced and independent (kUnroll in flight per
+// thread) and only x[column] / upper[losort[k]] are gathers (L1/L2 hits on a
+// renumbered mesh).  Phase 2: each thread sums its row from shared memory in
+// the oracle's order (Q10), so the result is bitwise that of amul_row().
+// ---------------------------------------------------------------------------
+
+constexpr int kTileCap = 1024;  // face products per side held in shared memory per tile
+constexpr int kUnroll = 4;      // faces in flight per thread per side (4 * 256 = kTileCap)
+
+struct TileSmem {
+    double prodN[kTileCap];  // neighbour side, losort order
+    double prodO[kTileCap];  // owner side, face order
+    int os[kThreads + 1];
+    int ls[kThreads + 1];
+};
+
+// Products of one side of the tile: prod[k - k0] = coef[k] * x[col[k]], with
+// coef[k] = upper[k] (owner side) or upper[losort[k]] (neighbour side).
+template <bool INDIRECT>
+__device__ __forceinline__ void tile_products(int k0, int k1, const int* __restrict__ coef_idx,
+                                              const int* __restrict__ col, const double* __restrict__ upper,
+                                              const double* __restrict__ x, double* __restrict__ prod)
+{
+    for (int base = k0 + (int)threadIdx.x; base < k1; base += kThreads * kUnroll) {
+        int cidx[kUnroll];
+        double u[kUnroll];
+#pragma unroll
+        for (int r = 0; r < kUnroll; ++r) {
+            const int k = base + r * kThreads;
+            cidx[r] = k < k1 ? __ldg(col + k) : 0;
+            if (!INDIRECT) u[r] = k < k1 ? __ldg(upper + k) : 0.0;
+        }
+        if (INDIRECT) {
+            int fi[kUnroll];
+#pragma unroll
+            for (int r = 0; r < kUnroll; ++r) {
+                const int k = base + r * kThreads;
+                fi[r] = k < k1 ? __ldg(coef_idx + k) : 0;
+            }
+#pragma unroll
+            for (int r = 0; r < kUnroll; ++r) u[r] = __ldg(upper + fi[r]);
+        }
+        double xv[kUnroll];
+#pragma unroll
+        for (int r = 0; r < kUnroll; ++r) xv[r] = __ldg(x + cidx[r]);
+#pragma unroll
+        for (int r = 0; r < kUnroll; ++r) {
+            const int k = base + r * kThreads;
+            if (k < k1) prod[k - k0] = u[r] * xv[r];
+        }
+    }
+}
+
+// y = A x over the whole mesh, tiles grid-strided over CTAs; returns this thread's sum of y*x.
+template <bool DOT>
+__device__ __forceinline__ double amul_tiles(const MeshArgs& a, const double* __restrict__ diag,
+                                             const double* __restrict__ upper, const double* __restrict__ iface,
+                                             const double* __restrict__ x, const double* __restrict__ xr,
+                                             double* __restrict__ y, TileSmem& sm)
+{
+    double acc = 0.0;
+    const int n_tiles = (a.N + kThreads - 1) / kThreads;
+    const int t = threadIdx.x;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        const int c0 = tile * kThreads;
+        const int n = min(kThreads, a.N - c0);
+        const int c = c0 + t;
+        if (t <= n) {
+            sm.os[t] = __ldg(a.ownerStart + c0 + t);
+            sm.ls[t] = __ldg(a.losortStart + c0 + t);
+        }
+        double dx = 0.0, xc = 0.0;
+        if (t < n) {
+            xc = __ldg(x + c);
+            dx = __ldg(diag + c) * xc;
+        }
+        __syncthreads();
+        const int f0 = sm.os[0], f1 = sm.os[n], k0 = sm.ls[0], k1 = sm.ls[n];
+        const bool staged = (f1 - f0) <= kTileCap && (k1 - k0) <= kTileCap;
+        if (staged) {
+            tile_products<true>(k0, k1, a.losort, a.ownerLo, upper, x, sm.prodN);
+            tile_products<false>(f0, f1, nullptr, a.neighbour, upper, x, sm.prodO);
+        }
+        __syncthreads();
+        if (t < n) {
+            double s;
+            if (staged) {
+                s = dx;
+                const int ke = sm.ls[t + 1];
+                for (int k = sm.ls[t]; k < ke; ++k) s = s + sm.prodN[k - k0];
+                const int fe = sm.os[t + 1];
+                for (int f = sm.os[t]; f < fe; ++f) s = s + sm.prodO[f - f0];
+                if (a.ifStart) {
+                    const int j1 = a.ifStart[c + 1];
+                    for (int j = a.ifStart[c]; j < j1; ++j) {
+                        const int i = a.ifIdx[j];
+                        s = s + iface[i] * xr[i];
+                    }
+                }
+            } else {
+                s = amul_row(a, c, diag, upper, iface, x, xr, nullptr);
+            }
+            y[c] = s;
+            if (DOT) acc += s * xc;
+        }
+        __syncthreads();  // smem reused by the next tile
+    }
+    return acc;
+}
+
+// ---------------------------------------------------------------------------
 // A3 geometry: nonOrthDeltaCoeffs (stabilised form) and linear weights
 // ---------------------------------------------------------------------------
 
@@ -304,8 +419,8 @@ __global__ void __launch_bounds__(kThreads) k_amul(MeshArgs a, const double* __r
                                                   const double* __restrict__ iface, const double* __restrict__ x,
                                                   const double* __restrict__ xr, double* __restrict__ y)
 {
-    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < a.N; c += gridDim.x * blockDim.x)
-        y[c] = amul_row(a, c, diag, upper, iface, x, xr, nullptr);
+    __shared__ TileSmem sm;
+    amul_tiles<false>(a, diag, upper, iface, x, xr, y, sm);
 }
 
 __global__ void k_gather(int n, const int* __restrict__ idx, const double* __restrict__ in, double* __restrict__ out)
@@ -400,13 +515,10 @@ __global__ void __launch_bounds__(kThreads) k_direction(int N, Workspace w)
 __global__ void __launch_bounds__(kThreads) k_amul_dot(MeshArgs a, Workspace w, int fin)
 {
     if (w.scal->done) return;
+    __shared__ TileSmem sm;
     const DevPtrs p = *w.ptrs;
-    double v[1] = {0.0};
-    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < a.N; c += gridDim.x * blockDim.x) {
-        const double y = amul_row(a, c, p.diag, p.upper, p.iface, w.pA, w.xr, nullptr);
-        w.wA[c] = y;
-        v[0] += y * w.pA[c];
-    }
+    double v[1];
+    v[0] = amul_tiles<true>(a, p.diag, p.upper, p.iface, w.pA, w.xr, w.wA, sm);
     if (grid_sum<1>(v, w.part, &w.scal->ticket[2]) && threadIdx.x == 0) {
         if (fin) finalize(w.scal, 3, v);
         else w.scal->rank_part[0] = v[0];
@@ -565,6 +677,7 @@ void launch_amul(cudaStream_t s, int grid, const MeshArgs& a, const double* diag
     if (a.N <= 0) return;
     (void)grid;
     k_amul<<<grid_for(k_amul, a.N), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y);
+
 }
 
 void launch_gather(cudaStream_t s, int n, const int* idx, const double* in, double* out)
