@@ -229,9 +229,13 @@ __device__ __forceinline__ double amul_tiles(const MeshArgs& a, const double* __
         const int c0 = tile * kThreads;
         const int n = min(kThreads, a.N - c0);
         const int c = c0 + t;
-        if (t <= n) {
+        if (t < n) {
             sm.os[t] = __ldg(a.ownerStart + c0 + t);
             sm.ls[t] = __ldg(a.losortStart + c0 + t);
+        }
+        if (t == 0) {  // row extent end of the tile (n may equal kThreads)
+            sm.os[n] = __ldg(a.ownerStart + c0 + n);
+            sm.ls[n] = __ldg(a.losortStart + c0 + n);
         }
         double dx = 0.0, xc = 0.0;
         if (t < n) {
