@@ -223,6 +223,12 @@ spuma_status spuma_set_timing(spuma_mesh m, int enable);
 /* Iterations per captured CUDA-graph batch (default 16; 1..256). */
 spuma_status spuma_set_batch(spuma_mesh m, int iterations);
 
+/* Tuning options.  SPUMA_OPT_AMUL_VARIANT selects the A7 kernel (all variants are
+ * bitwise identical): 0 per-row, 1 CTA tile, 2 unrolled per-row, 3 TMA
+ * producer/consumer pipeline (cp.async.bulk + mbarrier).  Errors: INVALID_ARGUMENT. */
+typedef enum { SPUMA_OPT_AMUL_VARIANT = 0 } spuma_option;
+spuma_status spuma_set_option(spuma_mesh m, int option, int value);
+
 /* Fill out128 with a fresh ncclUniqueId (rank 0 calls it and broadcasts). */
 spuma_status spuma_nccl_get_unique_id(void* out128);
 

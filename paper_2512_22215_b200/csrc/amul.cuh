@@ -1,0 +1,262 @@
+// amul.cuh -- A7 Amul variants (included by kernels.cu).  All variants compute
+// y_c = diag_c x_c + sum_{nbr(c)} upper x + sum_{own(c)} upper x (+ interfaces)
+// in the oracle's order (reading Q10) with separate DMUL/DADD (--fmad=false),
+// so every variant is bitwise identical to amul_row() and to the oracle.
+//
+//   0  per-row:   one thread per cell, grid-stride (amul_row)
+//   1  tile:      CTA-cooperative products in shared memory, then ordered row sums
+//   2  unrolled:  one thread per cell, up to 4 faces per side loaded as one batch
+//   3  tma:       warp-specialised pipeline -- a producer warp streams each tile's
+//                 contiguous ranges (upper/neighbour of the owner side,
+//                 losort/ownerLo of the neighbour side, ownerStart/losortStart,
+//                 x, diag) into shared-memory stages with cp.async.bulk (TMA)
+//                 completing on mbarriers; consumer warps gather x[column] and
+//                 upper[losort] (L2), stage the products and sum rows in order.
+#pragma once
+
+namespace spuma {
+
+// ---------------------------------------------------------------------------- variant 2
+__device__ __forceinline__ double amul_row_unrolled(const MeshArgs& a, int c, const double* __restrict__ diag,
+                                                    const double* __restrict__ upper,
+                                                    const double* __restrict__ iface,
+                                                    const double* __restrict__ x, const double* __restrict__ xr)
+{
+    const int k0 = __ldg(a.losortStart + c), k1 = __ldg(a.losortStart + c + 1);
+    const int f0 = __ldg(a.ownerStart + c), f1 = __ldg(a.ownerStart + c + 1);
+    const double d = __ldg(diag + c), xc = __ldg(x + c);
+    if (k1 - k0 > 4 || f1 - f0 > 4) return amul_row(a, c, diag, upper, iface, x, xr, nullptr);
+    int fi[4], cn[4], co[4];
+    double uo[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const bool vn = k0 + r < k1, vo = f0 + r < f1;
+        fi[r] = vn ? __ldg(a.losort + k0 + r) : 0;
+        cn[r] = vn ? __ldg(a.ownerLo + k0 + r) : c;
+        co[r] = vo ? __ldg(a.neighbour + f0 + r) : c;
+        uo[r] = vo ? __ldg(upper + f0 + r) : 0.0;
+    }
+    double un[4], xn[4], xo[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        un[r] = k0 + r < k1 ? __ldg(upper + fi[r]) : 0.0;
+        xn[r] = __ldg(x + cn[r]);
+        xo[r] = __ldg(x + co[r]);
+    }
+    double s = d * xc;
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+        if (k0 + r < k1) s = s + un[r] * xn[r];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+        if (f0 + r < f1) s = s + uo[r] * xo[r];
+    if (a.ifStart) {
+        const int j1 = a.ifStart[c + 1];
+        for (int j = a.ifStart[c]; j < j1; ++j) {
+            const int i = a.ifIdx[j];
+            s = s + iface[i] * xr[i];
+        }
+    }
+    return s;
+}
+
+// ---------------------------------------------------------------------------- variant 3 (TMA)
+namespace tma {
+
+constexpr int kCells = 128;          // cells per tile == consumer threads
+constexpr int kCons = kCells;        // consumer threads
+constexpr int kBlock = kCons + 32;   // + one producer warp
+constexpr int kCap = 448;            // faces per side per stage (3.5 per cell)
+constexpr int kStages = 3;
+
+struct Meta {
+    int c0, n, f0, f1, k0, k1;
+    int offU, offN, offK, staged;
+};
+
+struct Stage {
+    alignas(16) double up[kCap + 2];     // upper[a0 .. a1)           owner side
+    alignas(16) double xx[kCells];       // x[c0 .. c0+n)
+    alignas(16) double dg[kCells];       // diag[c0 .. c0+n)
+    alignas(16) int nb[kCap + 4];        // neighbour[b0 .. b1)       owner side
+    alignas(16) int lo[kCap + 4];        // losort[q0 .. q1)          neighbour side
+    alignas(16) int ol[kCap + 4];        // ownerLo[q0 .. q1)
+    alignas(16) int os[kCells + 4];      // ownerStart[c0 .. c0+n]
+    alignas(16) int ls[kCells + 4];      // losortStart[c0 .. c0+n]
+    Meta meta;
+};
+
+struct Smem {
+    Stage st[kStages];
+    alignas(16) double prodN[kCap];
+    alignas(16) double prodO[kCap];
+    alignas(8) unsigned long long full[kStages];
+    alignas(8) unsigned long long empty[kStages];
+};
+
+__device__ __forceinline__ uint32_t s32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void bar_init(unsigned long long* b, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void bar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void bar_arrive(unsigned long long* b)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s32(b)) : "memory");
+}
+__device__ __forceinline__ void bar_arrive_tx(unsigned long long* b, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bar_wait(unsigned long long* b, uint32_t parity)
+{
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(s32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* b)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     s32(dst)),
+                 "l"(src), "r"(bytes), "r"(s32(b))
+                 : "memory");
+}
+__device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kCons) : "memory"); }
+
+// Lengths (elements) the windows may not exceed: internal arrays are padded by
+// 8 elements; caller arrays (upper, diag, and x in the diagnostic Amul) are not.
+struct Bounds {
+    long long upper_len, x_len, diag_len;
+};
+
+template <bool DOT>
+__device__ double amul_tma(const MeshArgs& a, const double* __restrict__ diag, const double* __restrict__ upper,
+                           const double* __restrict__ iface, const double* __restrict__ x,
+                           const double* __restrict__ xr, double* __restrict__ y, Bounds bd, Smem& sm)
+{
+    const int tid = threadIdx.x;
+    const int n_tiles = (a.N + kCells - 1) / kCells;
+    if (tid == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            bar_init(&sm.full[s], 1);
+            bar_init(&sm.empty[s], 1);
+        }
+        bar_fence_init();
+    }
+    __syncthreads();
+    double acc = 0.0;
+    if (tid >= kCons) {
+        // ------------------------------------------------------------ producer warp
+        if (tid == kCons) {
+            int i = 0;
+            int tile = blockIdx.x;
+            int nf0 = 0, nf1 = 0, nk0 = 0, nk1 = 0;
+            if (tile < n_tiles) {
+                const int c0 = tile * kCells, n = min(kCells, a.N - c0);
+                nf0 = __ldg(a.ownerStart + c0);
+                nf1 = __ldg(a.ownerStart + c0 + n);
+                nk0 = __ldg(a.losortStart + c0);
+                nk1 = __ldg(a.losortStart + c0 + n);
+            }
+            for (; tile < n_tiles; ++i, tile += gridDim.x) {
+                const int s = i % kStages, u = i / kStages;
+                const int c0 = tile * kCells, n = min(kCells, a.N - c0);
+                const int f0 = nf0, f1 = nf1, k0 = nk0, k1 = nk1;
+                // prefetch the next tile's extents before blocking on the stage
+                const int nt = tile + gridDim.x;
+                if (nt < n_tiles) {
+                    const int d0 = nt * kCells, dn = min(kCells, a.N - d0);
+                    nf0 = __ldg(a.ownerStart + d0);
+                    nf1 = __ldg(a.ownerStart + d0 + dn);
+                    nk0 = __ldg(a.losortStart + d0);
+                    nk1 = __ldg(a.losortStart + d0 + dn);
+                }
+                if (u > 0) bar_wait(&sm.empty[s], (u - 1) & 1);
+                Stage& st = sm.st[s];
+                const long long a0 = f0 & ~1, a1 = (f1 + 1) & ~1;      // upper (double) window
+                const long long b0 = f0 & ~3, b1 = (f1 + 3) & ~3;      // neighbour (int) window
+                const long long q0 = k0 & ~3, q1 = (k1 + 3) & ~3;      // losort / ownerLo windows
+                const long long x1 = (c0 + n + 1) & ~1;                // x / diag windows [c0, x1)
+                const long long o1 = (c0 + n + 1 + 3) & ~3;            // ownerStart / losortStart [c0, o1)
+                const bool staged = (f1 - f0) <= kCap && (k1 - k0) <= kCap && a1 <= bd.upper_len &&
+                                    x1 <= bd.x_len && x1 <= bd.diag_len;
+                st.meta = Meta{c0, n, f0, f1, k0, k1, (int)(f0 - a0), (int)(f0 - b0), (int)(k0 - q0), staged ? 1 : 0};
+                if (!staged) {
+                    bar_arrive(&sm.full[s]);
+                    continue;
+                }
+                const uint32_t bu = (uint32_t)((a1 - a0) * 8), bn = (uint32_t)((b1 - b0) * 4);
+                const uint32_t bq = (uint32_t)((q1 - q0) * 4), bx = (uint32_t)((x1 - c0) * 8);
+                const uint32_t bo = (uint32_t)((o1 - c0) * 4);
+                bar_arrive_tx(&sm.full[s], bu + bn + 2 * bq + 2 * bx + 2 * bo);
+                if (bu) bulk_g2s(st.up, upper + a0, bu, &sm.full[s]);
+                if (bn) bulk_g2s(st.nb, a.neighbour + b0, bn, &sm.full[s]);
+                if (bq) {
+                    bulk_g2s(st.lo, a.losort + q0, bq, &sm.full[s]);
+                    bulk_g2s(st.ol, a.ownerLo + q0, bq, &sm.full[s]);
+                }
+                bulk_g2s(st.xx, x + c0, bx, &sm.full[s]);
+                bulk_g2s(st.dg, diag + c0, bx, &sm.full[s]);
+                bulk_g2s(st.os, a.ownerStart + c0, bo, &sm.full[s]);
+                bulk_g2s(st.ls, a.losortStart + c0, bo, &sm.full[s]);
+            }
+        }
+    } else {
+        // ------------------------------------------------------------ consumer warps
+        int i = 0;
+        for (int tile = blockIdx.x; tile < n_tiles; ++i, tile += gridDim.x) {
+            const int s = i % kStages, u = i / kStages;
+            bar_wait(&sm.full[s], u & 1);
+            Stage& st = sm.st[s];
+            const Meta m = st.meta;
+            const int c = m.c0 + tid;
+            if (m.staged) {
+                // products: gathers are independent -> all in flight at once
+                const int no = m.f1 - m.f0, nn = m.k1 - m.k0;
+#pragma unroll 4
+                for (int j = tid; j < nn; j += kCons) {
+                    const int f = st.lo[m.offK + j];
+                    const int col = st.ol[m.offK + j];
+                    sm.prodN[j] = __ldg(upper + f) * __ldg(x + col);
+                }
+#pragma unroll 4
+                for (int j = tid; j < no; j += kCons) sm.prodO[j] = st.up[m.offU + j] * __ldg(x + st.nb[m.offN + j]);
+                consumers_sync();
+                if (tid < m.n) {
+                    const double xc = st.xx[tid];
+                    double r = st.dg[tid] * xc;
+                    const int ke = st.ls[tid + 1] - m.k0;
+                    for (int k = st.ls[tid] - m.k0; k < ke; ++k) r = r + sm.prodN[k];
+                    const int fe = st.os[tid + 1] - m.f0;
+                    for (int f = st.os[tid] - m.f0; f < fe; ++f) r = r + sm.prodO[f];
+                    if (a.ifStart) {
+                        const int j1 = a.ifStart[c + 1];
+                        for (int j = a.ifStart[c]; j < j1; ++j) {
+                            const int q = a.ifIdx[j];
+                            r = r + iface[q] * xr[q];
+                        }
+                    }
+                    y[c] = r;
+                    if (DOT) acc += r * xc;
+                }
+            } else if (tid < m.n) {
+                const double r = amul_row(a, c, diag, upper, iface, x, xr, nullptr);
+                y[c] = r;
+                if (DOT) acc += r * x[c];
+            }
+            consumers_sync();  // stage s and the product buffers are free
+            if (tid == 0) bar_arrive(&sm.empty[s]);
+        }
+    }
+    return acc;
+}
+
+}  // namespace tma
+}  // namespace spuma

@@ -24,12 +24,13 @@ spuma_status set_error(spuma_status s, const std::string& msg)
 
 namespace {
 
+// every internal array carries kPad zeroed elements past its end (TMA windows)
 template <class T>
 spuma_status dalloc(T** p, size_t n)
 {
     *p = nullptr;
-    if (n == 0) n = 1;
-    SPUMA_CUDA(cudaMalloc(reinterpret_cast<void**>(p), n * sizeof(T)));
+    SPUMA_CUDA(cudaMalloc(reinterpret_cast<void**>(p), (n + kPad) * sizeof(T)));
+    SPUMA_CUDA(cudaMemset(*p, 0, (n + kPad) * sizeof(T)));
     return SPUMA_OK;
 }
 
@@ -220,7 +221,7 @@ spuma_status enqueue_iteration(spuma_mesh m, cudaStream_t s, std::vector<cudaEve
     if (ev) record(m, *ev, slot * 6 + 1, s);
     SPUMA_TRY(halo_exchange(m, m->ws.pA, m->ws.xr, s));
     if (ev) record(m, *ev, slot * 6 + 2, s);
-    launch_amul_dot(s, m->grid, a, m->ws, fin);
+    launch_amul_dot(s, m->amul_variant, a, m->ws, fin);
     if (ev) record(m, *ev, slot * 6 + 3, s);
     if (!fin) SPUMA_TRY(reduce_finalize(m, 3, s));
     if (ev) record(m, *ev, slot * 6 + 4, s);
@@ -687,7 +688,8 @@ spuma_status spuma_amul(spuma_mesh m, const spuma_scalar* diag, const spuma_scal
         y_i = m->d_cell_t;
     }
     SPUMA_TRY(halo_exchange(m, x_i, m->ws.xr, s));
-    launch_amul(s, m->grid, mesh_args(m), d_i, u_i, if_i, x_i, m->ws.xr, y_i);
+    launch_amul(s, m->amul_variant, mesh_args(m), d_i, u_i, if_i, x_i, m->ws.xr, y_i,
+                (x_i == x) ? (long long)m->N : (long long)m->N + kPad);
     m->stats.kernel_launches += 1;
     SPUMA_TRY(cells_out(m, y, y_i));
     SPUMA_CUDA(cudaStreamSynchronize(s));
@@ -829,6 +831,19 @@ spuma_status spuma_set_timing(spuma_mesh m, int enable)
     if (!m) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "mesh is NULL");
     m->timing = enable != 0;
     return SPUMA_OK;
+}
+
+spuma_status spuma_set_option(spuma_mesh m, int option, int value)
+{
+    if (!m) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "mesh is NULL");
+    switch (option) {
+    case SPUMA_OPT_AMUL_VARIANT:
+        if (value < 0 || value > 3) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "amul variant must be 0..3");
+        if (value != m->amul_variant) destroy_graphs(m);
+        m->amul_variant = value;
+        return SPUMA_OK;
+    default: return set_error(SPUMA_ERR_INVALID_ARGUMENT, "unknown option");
+    }
 }
 
 spuma_status spuma_set_batch(spuma_mesh m, int iterations)

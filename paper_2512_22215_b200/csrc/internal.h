@@ -111,6 +111,7 @@ struct spuma_mesh_s {
 
     // captured iteration batches (ping-pong) and timing events
     int batch = 16;
+    int amul_variant = 0;
     bool timing = false;
     cudaGraphExec_t gexec[2] = {nullptr, nullptr};
     bool gexec_timed = false;
@@ -163,8 +164,8 @@ void launch_diag_gather(cudaStream_t s, int grid, const MeshArgs& a, const doubl
                         const double* bmagSf, const double* bdelta, const double* bweight, const double* bvalue,
                         const double* bgamma_r, const signed char* bis_owner, const double* gamma, int ref_cell,
                         double ref_value, double* diag, double* source, double* iface);
-void launch_amul(cudaStream_t s, int grid, const MeshArgs& a, const double* diag, const double* upper,
-                 const double* iface, const double* x, const double* xr, double* y);
+void launch_amul(cudaStream_t s, int variant, const MeshArgs& a, const double* diag, const double* upper,
+                 const double* iface, const double* x, const double* xr, double* y, long long x_len);
 void launch_gather(cudaStream_t s, int n, const int* idx, const double* in, double* out);   // out[i] = in[idx[i]]
 void launch_scatter(cudaStream_t s, int n, const int* idx, const double* in, double* out);  // out[idx[i]] = in[i]
 void launch_pack(cudaStream_t s, int n, const int* cell, const double* x, double* out);     // out[i] = x[cell[i]]
@@ -173,7 +174,8 @@ void launch_pack(cudaStream_t s, int n, const int* cell, const double* x, double
 void launch_setup1(cudaStream_t s, int grid, const MeshArgs& a, const Workspace& w, bool fin);
 void launch_setup2(cudaStream_t s, int grid, const MeshArgs& a, const Workspace& w, bool fin);
 void launch_direction(cudaStream_t s, int grid, const MeshArgs& a, const Workspace& w);
-void launch_amul_dot(cudaStream_t s, int grid, const MeshArgs& a, const Workspace& w, bool fin);
+void launch_amul_dot(cudaStream_t s, int variant, const MeshArgs& a, const Workspace& w, bool fin);
+constexpr int kPad = 8;  // padding elements on internal arrays (16-byte TMA windows may overrun by <= 3)
 void launch_update(cudaStream_t s, int grid, const MeshArgs& a, const Workspace& w, bool fin);
 // P > 1: finalise from the gathered rank partials ([n_ranks][4], rank order)
 void launch_finalize(cudaStream_t s, int stage, const double* gathered, int n_ranks, const Workspace& w);

@@ -39,9 +39,10 @@ __device__ __forceinline__ void cta_sum(double (&v)[NV])
         for (int i = 0; i < NV; ++i) sh[i][warp] = v[i];
     __syncthreads();
     if (warp == 0) {
+        const int nw = blockDim.x >> 5;  // <= kThreads / 32
 #pragma unroll
         for (int i = 0; i < NV; ++i) {
-            double t = lane < kThreads / 32 ? sh[i][lane] : 0.0;
+            double t = lane < nw ? sh[i][lane] : 0.0;
 #pragma unroll
             for (int o = 4; o > 0; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
             v[i] = t;
@@ -69,7 +70,7 @@ __device__ __forceinline__ bool grid_sum(double (&v)[NV], double* part, unsigned
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
         double t = 0.0;
-        for (int b = threadIdx.x; b < (int)gridDim.x; b += kThreads) t += __ldcg(part + i * gridDim.x + b);
+        for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) t += __ldcg(part + i * gridDim.x + b);
         v[i] = t;
     }
     cta_sum<NV>(v);
@@ -276,6 +277,10 @@ __device__ __forceinline__ double amul_tiles(const MeshArgs& a, const double* __
     return acc;
 }
 
+}  // namespace spuma
+#include "amul.cuh"
+namespace spuma {
+
 // ---------------------------------------------------------------------------
 // A3 geometry: nonOrthDeltaCoeffs (stabilised form) and linear weights
 // ---------------------------------------------------------------------------
@@ -418,13 +423,23 @@ __global__ void __launch_bounds__(kThreads)
 // A7 Amul (plain; diagnostics and the multi-rank setup)
 // ---------------------------------------------------------------------------
 
-__global__ void __launch_bounds__(kThreads) k_amul(MeshArgs a, const double* __restrict__ diag,
-                                                  const double* __restrict__ upper,
-                                                  const double* __restrict__ iface, const double* __restrict__ x,
-                                                  const double* __restrict__ xr, double* __restrict__ y)
+template <int V>
+__global__ void __launch_bounds__(V == 3 ? tma::kBlock : kThreads)
+    k_amul(MeshArgs a, const double* __restrict__ diag, const double* __restrict__ upper,
+           const double* __restrict__ iface, const double* __restrict__ x, const double* __restrict__ xr,
+           double* __restrict__ y, tma::Bounds bd)
 {
-    __shared__ TileSmem sm;
-    amul_tiles<false>(a, diag, upper, iface, x, xr, y, sm);
+    if constexpr (V == 1) {
+        __shared__ TileSmem sm;
+        amul_tiles<false>(a, diag, upper, iface, x, xr, y, sm);
+    } else if constexpr (V == 3) {
+        __shared__ tma::Smem sm;
+        tma::amul_tma<false>(a, diag, upper, iface, x, xr, y, bd, sm);
+    } else {
+        for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < a.N; c += gridDim.x * blockDim.x)
+            y[c] = V == 2 ? amul_row_unrolled(a, c, diag, upper, iface, x, xr)
+                          : amul_row(a, c, diag, upper, iface, x, xr, nullptr);
+    }
 }
 
 __global__ void k_gather(int n, const int* __restrict__ idx, const double* __restrict__ in, double* __restrict__ out)
@@ -516,13 +531,27 @@ __global__ void __launch_bounds__(kThreads) k_direction(int N, Workspace w)
 }
 
 // A7 + A8: wA = A pA, partial wA.pA -> alpha
-__global__ void __launch_bounds__(kThreads) k_amul_dot(MeshArgs a, Workspace w, int fin)
+template <int V>
+__global__ void __launch_bounds__(V == 3 ? tma::kBlock : kThreads) k_amul_dot(MeshArgs a, Workspace w, int fin)
 {
     if (w.scal->done) return;
-    __shared__ TileSmem sm;
     const DevPtrs p = *w.ptrs;
-    double v[1];
-    v[0] = amul_tiles<true>(a, p.diag, p.upper, p.iface, w.pA, w.xr, w.wA, sm);
+    double v[1] = {0.0};
+    if constexpr (V == 1) {
+        __shared__ TileSmem sm;
+        v[0] = amul_tiles<true>(a, p.diag, p.upper, p.iface, w.pA, w.xr, w.wA, sm);
+    } else if constexpr (V == 3) {
+        __shared__ tma::Smem sm;
+        const tma::Bounds bd{a.F, (long long)a.N + 8, a.N};
+        v[0] = tma::amul_tma<true>(a, p.diag, p.upper, p.iface, w.pA, w.xr, w.wA, bd, sm);
+    } else {
+        for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < a.N; c += gridDim.x * blockDim.x) {
+            const double y = V == 2 ? amul_row_unrolled(a, c, p.diag, p.upper, p.iface, w.pA, w.xr)
+                                    : amul_row(a, c, p.diag, p.upper, p.iface, w.pA, w.xr, nullptr);
+            w.wA[c] = y;
+            v[0] += y * w.pA[c];
+        }
+    }
     if (grid_sum<1>(v, w.part, &w.scal->ticket[2]) && threadIdx.x == 0) {
         if (fin) finalize(w.scal, 3, v);
         else w.scal->rank_part[0] = v[0];
@@ -613,12 +642,12 @@ static int sms()
 }
 
 template <class K>
-static int grid_for(K kernel, long long work, int per_thread = 1)
+static int grid_for(K kernel, long long work, int per_thread = 1, int block = kThreads)
 {
     int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, block, 0);
     if (occ <= 0) occ = 1;
-    long long need = (work + (long long)kThreads * per_thread - 1) / ((long long)kThreads * per_thread);
+    long long need = (work + (long long)block * per_thread - 1) / ((long long)block * per_thread);
     long long cap = (long long)occ * sms();
     long long g = need < cap ? need : cap;
     return (int)(g < 1 ? 1 : g);
@@ -629,7 +658,10 @@ int occupancy_grid(int N, int* grid_faces, int F)
     // the largest grid any reduction kernel uses (sizes the partials buffer)
     int g = grid_for(k_setup1, N);
     g = std::max(g, grid_for(k_setup2, N));
-    g = std::max(g, grid_for(k_amul_dot, N));
+    g = std::max(g, grid_for(k_amul_dot<0>, N));
+    g = std::max(g, grid_for(k_amul_dot<1>, N));
+    g = std::max(g, grid_for(k_amul_dot<2>, N));
+    g = std::max(g, grid_for(k_amul_dot<3>, N, 1, tma::kBlock));
     g = std::max(g, grid_for(k_update, N, 2));
     if (grid_faces) *grid_faces = grid_for(k_face_coeffs, F);
     return g;
@@ -675,13 +707,20 @@ void launch_diag_gather(cudaStream_t s, int grid, const MeshArgs& a, const doubl
                                                                     gamma, ref_cell, ref_value, diag, source, iface);
 }
 
-void launch_amul(cudaStream_t s, int grid, const MeshArgs& a, const double* diag, const double* upper,
-                 const double* iface, const double* x, const double* xr, double* y)
+void launch_amul(cudaStream_t s, int variant, const MeshArgs& a, const double* diag, const double* upper,
+                 const double* iface, const double* x, const double* xr, double* y, long long x_len)
 {
     if (a.N <= 0) return;
-    (void)grid;
-    k_amul<<<grid_for(k_amul, a.N), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y);
-
+    const tma::Bounds bd{a.F, x_len, a.N};
+    switch (variant) {
+    case 1: k_amul<1><<<grid_for(k_amul<1>, a.N), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd); break;
+    case 2: k_amul<2><<<grid_for(k_amul<2>, a.N), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd); break;
+    case 3:
+        k_amul<3><<<grid_for(k_amul<3>, a.N, tma::kCells, tma::kBlock), tma::kBlock, 0, s>>>(a, diag, upper, iface,
+                                                                                            x, xr, y, bd);
+        break;
+    default: k_amul<0><<<grid_for(k_amul<0>, a.N), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd); break;
+    }
 }
 
 void launch_gather(cudaStream_t s, int n, const int* idx, const double* in, double* out)
@@ -719,10 +758,17 @@ void launch_direction(cudaStream_t s, int grid, const MeshArgs& a, const Workspa
     k_direction<<<grid_for(k_direction, a.N, 2), kThreads, 0, s>>>(a.N, w);
 }
 
-void launch_amul_dot(cudaStream_t s, int grid, const MeshArgs& a, const Workspace& w, bool fin)
+void launch_amul_dot(cudaStream_t s, int variant, const MeshArgs& a, const Workspace& w, bool fin)
 {
-    (void)grid;
-    k_amul_dot<<<grid_for(k_amul_dot, a.N), kThreads, 0, s>>>(a, w, fin ? 1 : 0);
+    const int f = fin ? 1 : 0;
+    switch (variant) {
+    case 1: k_amul_dot<1><<<grid_for(k_amul_dot<1>, a.N), kThreads, 0, s>>>(a, w, f); break;
+    case 2: k_amul_dot<2><<<grid_for(k_amul_dot<2>, a.N), kThreads, 0, s>>>(a, w, f); break;
+    case 3:
+        k_amul_dot<3><<<grid_for(k_amul_dot<3>, a.N, tma::kCells, tma::kBlock), tma::kBlock, 0, s>>>(a, w, f);
+        break;
+    default: k_amul_dot<0><<<grid_for(k_amul_dot<0>, a.N), kThreads, 0, s>>>(a, w, f); break;
+    }
 }
 
 void launch_update(cudaStream_t s, int grid, const MeshArgs& a, const Workspace& w, bool fin)

@@ -24,6 +24,8 @@ ZERO_GRADIENT, FIXED_VALUE, EMPTY, PROCESSOR = 0, 1, 2, 3
 STATUS = {0: "SPUMA_OK", 1: "SPUMA_ERR_INVALID_ARGUMENT", 2: "SPUMA_ERR_ADDRESSING", 3: "SPUMA_ERR_LENGTH_MISMATCH",
           4: "SPUMA_ERR_CUDA", 5: "SPUMA_ERR_NCCL", 6: "SPUMA_ERR_OUT_OF_MEMORY", 7: "SPUMA_ERR_STATE"}
 ABI_VERSION = 1
+OPT_AMUL_VARIANT = 0
+AMUL_VARIANTS = (0, 1, 2, 3)
 
 _vp, _ci, _cd, _lab = ctypes.c_void_p, ctypes.c_int, ctypes.c_double, ctypes.c_int32
 
@@ -94,12 +96,14 @@ def lib():
         L.spuma_reset_stats.argtypes = [_vp]
         L.spuma_set_timing.argtypes = [_vp, _ci]
         L.spuma_set_batch.argtypes = [_vp, _ci]
+        L.spuma_set_option.argtypes = [_vp, _ci, _ci]
         L.spuma_nccl_get_unique_id.argtypes = [_vp]
         L.spuma_last_error.restype = ctypes.c_char_p
         L.spuma_abi_version.restype = _ci
         for name in ("spuma_mesh_create", "spuma_assemble_laplacian", "spuma_pcg_solve", "spuma_amul",
                      "spuma_mesh_get_addressing", "spuma_mesh_get_geometry", "spuma_get_stats",
-                     "spuma_reset_stats", "spuma_set_timing", "spuma_set_batch", "spuma_nccl_get_unique_id"):
+                     "spuma_reset_stats", "spuma_set_timing", "spuma_set_batch", "spuma_nccl_get_unique_id",
+                     "spuma_set_option"):
             getattr(L, name).restype = _ci
         if L.spuma_abi_version() != ABI_VERSION:
             raise SpumaError(1, "libspuma ABI version mismatch")
@@ -282,6 +286,10 @@ class Mesh:
 
     def set_batch(self, iterations: int):
         _check(lib().spuma_set_batch(self._h, int(iterations)))
+
+    def set_option(self, option: int, value: int):
+        """spuma_set_option (OPT_AMUL_VARIANT: 0 per-row, 1 tile, 2 unrolled, 3 TMA pipeline)."""
+        _check(lib().spuma_set_option(self._h, int(option), int(value)))
 
 
 mesh_create = Mesh.mesh_create

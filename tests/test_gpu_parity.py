@@ -135,14 +135,19 @@ def test_assembly_parity(name, mesh, renumber, with_gamma):
 
 
 # ------------------------------------------------------------------ A7 Amul
+VARIANTS = list(P.spuma.AMUL_VARIANTS)
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
 @pytest.mark.parametrize("renumber", [False, True])
 @pytest.mark.parametrize("name,mesh", CASES, ids=[c[0] for c in CASES])
-def test_amul_bit_exact(name, mesh, renumber):
+def test_amul_bit_exact(name, mesh, renumber, variant):
     rng = np.random.default_rng(5)
     diag = rng.uniform(-4, -1, mesh.n_cells)
     upper = rng.uniform(0.1, 1, mesh.n_faces)
     x = rng.standard_normal(mesh.n_cells)
     h = P.Mesh.from_mesh(mesh, renumber=renumber)
+    h.set_option(P.spuma.OPT_AMUL_VARIANT, variant)
     y = torch.empty(mesh.n_cells, dtype=torch.float64, device="cuda")
     h.amul(dev(diag), dev(upper), None, dev(x), y)
     ref = O.amul(mesh, diag, upper, x) if not renumber else None
@@ -318,12 +323,14 @@ def _star_mesh(n):
     return gen.Mesh(n, owner, nbr, Sf, np.ones(F), 0.5 * (C[owner] + C[nbr]), C, np.ones(n), [])
 
 
+@pytest.mark.parametrize("variant", VARIANTS)
 @pytest.mark.parametrize("n", [300, 3000])
-def test_amul_bit_exact_overflowing_tiles(n):
+def test_amul_bit_exact_overflowing_tiles(n, variant):
     m = _star_mesh(n)
     rng = np.random.default_rng(n)
     diag, upper, x = rng.uniform(-4, -1, n), rng.uniform(0.1, 1, m.n_faces), rng.standard_normal(n)
     h = P.Mesh.from_mesh(m)
+    h.set_option(P.spuma.OPT_AMUL_VARIANT, variant)
     y = torch.empty(n, dtype=torch.float64, device="cuda")
     h.amul(dev(diag), dev(upper), None, dev(x), y)
     assert np.array_equal(y.cpu().numpy(), O.amul(m, diag, upper, x))
@@ -334,7 +341,23 @@ def test_amul_bit_exact_full_size_8M():
     m = gen.cube(200)
     s = O.assemble(m, None, 0, 0.0)
     x = np.sin(np.arange(m.n_cells) * 1e-3)
+    ref = O.amul(m, s.diag, s.upper, x)
     h = P.Mesh.from_mesh(m)
     y = torch.empty(m.n_cells, dtype=torch.float64, device="cuda")
-    h.amul(dev(s.diag), dev(s.upper), None, dev(x), y)
-    assert np.array_equal(y.cpu().numpy(), O.amul(m, s.diag, s.upper, x))
+    for v in VARIANTS:
+        h.set_option(P.spuma.OPT_AMUL_VARIANT, v)
+        y.zero_()
+        h.amul(dev(s.diag), dev(s.upper), None, dev(x), y)
+        assert np.array_equal(y.cpu().numpy(), ref), v
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_pcg_all_amul_variants_identical(variant):
+    """Every A7 variant gives the bitwise-same PCG trajectory (same products, same row order, same reductions)."""
+    m = gen.permute(gen.perturbed(12, 0.2), seed=3)
+    g, b = gen.gamma_lognormal(m), gen.rhs(m)
+    psi0, p0, _, _ = gpu_solve_case(m, g, b, 0)
+    h = P.Mesh.from_mesh(m)
+    h.set_option(P.spuma.OPT_AMUL_VARIANT, variant)
+    psi, p, _, _ = gpu_solve_case(m, g, b, 0, handle=h)
+    assert p == p0 and np.array_equal(psi, psi0)
