@@ -628,6 +628,14 @@ __global__ void k_scal_init(DevScal* s, double tol, double rel_tol, int max_iter
 // launchers
 // ---------------------------------------------------------------------------
 
+template <class K>
+static int kernel_block(K kernel)
+{
+    return ((const void*)kernel == (const void*)k_amul_dot<3> || (const void*)kernel == (const void*)k_amul<3>)
+               ? tma::kBlock
+               : kThreads;
+}
+
 static int g_sms = 0;
 
 static int sms()
@@ -641,13 +649,17 @@ static int sms()
     return g_sms;
 }
 
+// grid = min(CTAs the work needs, CTAs resident at full occupancy): one wave, grid-stride loops.
+// work / (work_per_thread * threads_per_work_unit) CTAs are needed; for tile kernels pass
+// work = tiles and threads_per_work_unit = 1 (one tile per CTA per step).
 template <class K>
-static int grid_for(K kernel, long long work, int per_thread = 1, int block = kThreads)
+static int grid_for(K kernel, long long work, int per_thread = 1, int threads_per_unit = kThreads)
 {
     int occ = 0;
+    const int block = kernel_block(kernel);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, block, 0);
     if (occ <= 0) occ = 1;
-    long long need = (work + (long long)block * per_thread - 1) / ((long long)block * per_thread);
+    long long need = (work + (long long)threads_per_unit * per_thread - 1) / ((long long)threads_per_unit * per_thread);
     long long cap = (long long)occ * sms();
     long long g = need < cap ? need : cap;
     return (int)(g < 1 ? 1 : g);
@@ -661,7 +673,7 @@ int occupancy_grid(int N, int* grid_faces, int F)
     g = std::max(g, grid_for(k_amul_dot<0>, N));
     g = std::max(g, grid_for(k_amul_dot<1>, N));
     g = std::max(g, grid_for(k_amul_dot<2>, N));
-    g = std::max(g, grid_for(k_amul_dot<3>, N, 1, tma::kBlock));
+    g = std::max(g, grid_for(k_amul_dot<3>, (N + tma::kCells - 1) / tma::kCells, 1, 1));
     g = std::max(g, grid_for(k_update, N, 2));
     if (grid_faces) *grid_faces = grid_for(k_face_coeffs, F);
     return g;
@@ -716,7 +728,7 @@ void launch_amul(cudaStream_t s, int variant, const MeshArgs& a, const double* d
     case 1: k_amul<1><<<grid_for(k_amul<1>, a.N), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd); break;
     case 2: k_amul<2><<<grid_for(k_amul<2>, a.N), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd); break;
     case 3:
-        k_amul<3><<<grid_for(k_amul<3>, a.N, tma::kCells, tma::kBlock), tma::kBlock, 0, s>>>(a, diag, upper, iface,
+        k_amul<3><<<grid_for(k_amul<3>, (a.N + tma::kCells - 1) / tma::kCells, 1, 1), tma::kBlock, 0, s>>>(a, diag, upper, iface,
                                                                                             x, xr, y, bd);
         break;
     default: k_amul<0><<<grid_for(k_amul<0>, a.N), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd); break;
@@ -765,7 +777,7 @@ void launch_amul_dot(cudaStream_t s, int variant, const MeshArgs& a, const Works
     case 1: k_amul_dot<1><<<grid_for(k_amul_dot<1>, a.N), kThreads, 0, s>>>(a, w, f); break;
     case 2: k_amul_dot<2><<<grid_for(k_amul_dot<2>, a.N), kThreads, 0, s>>>(a, w, f); break;
     case 3:
-        k_amul_dot<3><<<grid_for(k_amul_dot<3>, a.N, tma::kCells, tma::kBlock), tma::kBlock, 0, s>>>(a, w, f);
+        k_amul_dot<3><<<grid_for(k_amul_dot<3>, (a.N + tma::kCells - 1) / tma::kCells, 1, 1), tma::kBlock, 0, s>>>(a, w, f);
         break;
     default: k_amul_dot<0><<<grid_for(k_amul_dot<0>, a.N), kThreads, 0, s>>>(a, w, f); break;
     }

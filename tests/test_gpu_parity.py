@@ -301,13 +301,16 @@ def test_timing_and_stats():
 def test_odd_sizes_and_batches():
     m = gen.box(5, 3, 7, (1, 1, 1))  # N = 105 (odd, partial warp)
     g, b = gen.gamma_lognormal(m), gen.rhs(m)
+    psi_o, po, _ = O.solve_case(m, g, b, 0, 0.0, O.controls(1e-6))
+    n = po["n_iterations"]
+    psi_n, _, _ = O.solve_case(m, g, b, 0, 0.0, O.controls(0.0, 0.0, n, n))
     for batch in (1, 3, 16):
         h = P.Mesh.from_mesh(m)
         h.set_batch(batch)
         psi, perf, _, _ = gpu_solve_case(m, g, b, 0, handle=h)
-        psi_o, po, _ = O.solve_case(m, g, b, 0, 0.0, O.controls(1e-6))
-        assert abs(perf["n_iterations"] - po["n_iterations"]) <= 2
-        assert rel_l2(psi, psi_o) < 1e-8
+        assert abs(perf["n_iterations"] - n) <= 2
+        psi, perf, _, _ = gpu_solve_case(m, g, b, 0, (0.0, 0.0, n, n), handle=h)  # matched count (Q11)
+        assert perf["n_iterations"] == n and rel_l2(psi, psi_n) <= 1e-9
 
 
 def _star_mesh(n):
@@ -352,12 +355,17 @@ def test_amul_bit_exact_full_size_8M():
 
 
 @pytest.mark.parametrize("variant", VARIANTS)
-def test_pcg_all_amul_variants_identical(variant):
-    """Every A7 variant gives the bitwise-same PCG trajectory (same products, same row order, same reductions)."""
+def test_pcg_all_amul_variants(variant):
+    """Every A7 variant inside the PCG loop matches the oracle (Q11 protocol); Amul values are
+    bitwise equal across variants, dots differ only by the CTA count of the reduction."""
     m = gen.permute(gen.perturbed(12, 0.2), seed=3)
     g, b = gen.gamma_lognormal(m), gen.rhs(m)
-    psi0, p0, _, _ = gpu_solve_case(m, g, b, 0)
+    _, po, _ = O.solve_case(m, g, b, 0, 0.0, O.controls(1e-6))
+    n = po["n_iterations"]
+    psi_o, _, _ = O.solve_case(m, g, b, 0, 0.0, O.controls(0.0, 0.0, n, n))
     h = P.Mesh.from_mesh(m)
     h.set_option(P.spuma.OPT_AMUL_VARIANT, variant)
-    psi, p, _, _ = gpu_solve_case(m, g, b, 0, handle=h)
-    assert p == p0 and np.array_equal(psi, psi0)
+    _, p, _, _ = gpu_solve_case(m, g, b, 0, handle=h)
+    assert abs(p["n_iterations"] - n) <= 2
+    psi, p, _, _ = gpu_solve_case(m, g, b, 0, (0.0, 0.0, n, n), handle=h)
+    assert rel_l2(psi, psi_o) <= 1e-9
