@@ -6,6 +6,9 @@
 //   0  per-row:   one thread per cell, grid-stride (amul_row)
 //   1  tile:      CTA-cooperative products in shared memory, then ordered row sums
 //   2  unrolled:  one thread per cell, up to 4 faces per side loaded as one batch
+//   4  per-row capped at 32 registers (8 CTAs of 256 threads per SM: more warps in flight)
+//   5  unrolled, two cells per thread (c and c + 256 of a 512-cell tile): both cells'
+//      loads issued together, twice the bytes in flight per thread
 //   3  tma:       warp-specialised pipeline -- a producer warp streams each tile's
 //                 contiguous ranges (upper/neighbour of the owner side,
 //                 losort/ownerLo of the neighbour side, ownerStart/losortStart,
@@ -60,6 +63,72 @@ __device__ __forceinline__ double amul_row_unrolled(const MeshArgs& a, int c, co
     return s;
 }
 
+// ---------------------------------------------------------------------------- variant 5
+// Two rows per thread, every load of both rows issued before any use.
+__device__ __forceinline__ void amul_rows2(const MeshArgs& a, int c, int e, const double* __restrict__ diag,
+                                           const double* __restrict__ upper, const double* __restrict__ iface,
+                                           const double* __restrict__ x, const double* __restrict__ xr,
+                                           double* __restrict__ y, double& acc, bool dot)
+{
+    const bool ve = e < a.N;
+    const int ec = ve ? e : c;
+    const int k0 = __ldg(a.losortStart + c), k1 = __ldg(a.losortStart + c + 1);
+    const int f0 = __ldg(a.ownerStart + c), f1 = __ldg(a.ownerStart + c + 1);
+    const int q0 = __ldg(a.losortStart + ec), q1 = __ldg(a.losortStart + ec + 1);
+    const int g0 = __ldg(a.ownerStart + ec), g1 = __ldg(a.ownerStart + ec + 1);
+    const double dc = __ldg(diag + c), xc = __ldg(x + c), de = __ldg(diag + ec), xe = __ldg(x + ec);
+    if (k1 - k0 > 3 || f1 - f0 > 3 || q1 - q0 > 3 || g1 - g0 > 3 || a.ifStart) {
+        const double r = amul_row(a, c, diag, upper, iface, x, xr, nullptr);
+        y[c] = r;
+        if (dot) acc += r * xc;
+        if (ve) {
+            const double t = amul_row(a, e, diag, upper, iface, x, xr, nullptr);
+            y[e] = t;
+            if (dot) acc += t * xe;
+        }
+        return;
+    }
+    int fi[6], cn[6], co[6];
+    double uo[6];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+        bool vn = k0 + r < k1, vo = f0 + r < f1;
+        fi[r] = vn ? __ldg(a.losort + k0 + r) : 0;
+        cn[r] = vn ? __ldg(a.ownerLo + k0 + r) : c;
+        co[r] = vo ? __ldg(a.neighbour + f0 + r) : c;
+        uo[r] = vo ? __ldg(upper + f0 + r) : 0.0;
+        vn = q0 + r < q1, vo = g0 + r < g1;
+        fi[3 + r] = vn ? __ldg(a.losort + q0 + r) : 0;
+        cn[3 + r] = vn ? __ldg(a.ownerLo + q0 + r) : ec;
+        co[3 + r] = vo ? __ldg(a.neighbour + g0 + r) : ec;
+        uo[3 + r] = vo ? __ldg(upper + g0 + r) : 0.0;
+    }
+    double un[6], xn[6], xo[6];
+#pragma unroll
+    for (int r = 0; r < 6; ++r) {
+        un[r] = __ldg(upper + fi[r]);
+        xn[r] = __ldg(x + cn[r]);
+        xo[r] = __ldg(x + co[r]);
+    }
+    double s = dc * xc, t = de * xe;
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+        if (k0 + r < k1) s = s + un[r] * xn[r];
+        if (q0 + r < q1) t = t + un[3 + r] * xn[3 + r];
+    }
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+        if (f0 + r < f1) s = s + uo[r] * xo[r];
+        if (g0 + r < g1) t = t + uo[3 + r] * xo[3 + r];
+    }
+    y[c] = s;
+    if (dot) acc += s * xc;
+    if (ve) {
+        y[e] = t;
+        if (dot) acc += t * xe;
+    }
+}
+
 // ---------------------------------------------------------------------------- variant 3 (TMA)
 namespace tma {
 
@@ -67,7 +136,7 @@ constexpr int kCells = 128;          // cells per tile == consumer threads
 constexpr int kCons = kCells;        // consumer threads
 constexpr int kBlock = kCons + 32;   // + one producer warp
 constexpr int kCap = 448;            // faces per side per stage (3.5 per cell)
-constexpr int kStages = 3;
+constexpr int kStages = 2;
 
 struct Meta {
     int c0, n, f0, f1, k0, k1;

@@ -24,13 +24,15 @@ spuma_status set_error(spuma_status s, const std::string& msg)
 
 namespace {
 
-// every internal array carries kPad zeroed elements past its end (TMA windows)
+// every internal array carries kPad zeroed elements past its end (TMA windows); the
+// zero-fill is synchronous so no stream can overtake it
 template <class T>
 spuma_status dalloc(T** p, size_t n)
 {
     *p = nullptr;
     SPUMA_CUDA(cudaMalloc(reinterpret_cast<void**>(p), (n + kPad) * sizeof(T)));
     SPUMA_CUDA(cudaMemset(*p, 0, (n + kPad) * sizeof(T)));
+    SPUMA_CUDA(cudaDeviceSynchronize());
     return SPUMA_OK;
 }
 
@@ -838,7 +840,7 @@ spuma_status spuma_set_option(spuma_mesh m, int option, int value)
     if (!m) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "mesh is NULL");
     switch (option) {
     case SPUMA_OPT_AMUL_VARIANT:
-        if (value < 0 || value > 3) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "amul variant must be 0..3");
+        if (value < 0 || value > 5) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "amul variant must be 0..5");
         if (value != m->amul_variant) destroy_graphs(m);
         m->amul_variant = value;
         return SPUMA_OK;

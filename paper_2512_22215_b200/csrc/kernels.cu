@@ -423,8 +423,15 @@ __global__ void __launch_bounds__(kThreads)
 // A7 Amul (plain; diagnostics and the multi-rank setup)
 // ---------------------------------------------------------------------------
 
+// minimum resident CTAs per SM per variant (caps registers: 65536 / (CTAs * threads))
 template <int V>
-__global__ void __launch_bounds__(V == 3 ? tma::kBlock : kThreads)
+constexpr int amul_min_ctas()
+{
+    return V == 4 ? 8 : (V == 3 ? 4 : (V == 5 ? 3 : 6));
+}
+
+template <int V>
+__global__ void __launch_bounds__(V == 3 ? tma::kBlock : kThreads, amul_min_ctas<V>())
     k_amul(MeshArgs a, const double* __restrict__ diag, const double* __restrict__ upper,
            const double* __restrict__ iface, const double* __restrict__ x, const double* __restrict__ xr,
            double* __restrict__ y, tma::Bounds bd)
@@ -435,6 +442,12 @@ __global__ void __launch_bounds__(V == 3 ? tma::kBlock : kThreads)
     } else if constexpr (V == 3) {
         __shared__ tma::Smem sm;
         tma::amul_tma<false>(a, diag, upper, iface, x, xr, y, bd, sm);
+    } else if constexpr (V == 5) {
+        double acc = 0.0;
+        for (int t0 = blockIdx.x * 2 * kThreads; t0 < a.N; t0 += gridDim.x * 2 * kThreads) {
+            const int c = t0 + threadIdx.x;
+            if (c < a.N) amul_rows2(a, c, c + kThreads, diag, upper, iface, x, xr, y, acc, false);
+        }
     } else {
         for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < a.N; c += gridDim.x * blockDim.x)
             y[c] = V == 2 ? amul_row_unrolled(a, c, diag, upper, iface, x, xr)
@@ -532,7 +545,8 @@ __global__ void __launch_bounds__(kThreads) k_direction(int N, Workspace w)
 
 // A7 + A8: wA = A pA, partial wA.pA -> alpha
 template <int V>
-__global__ void __launch_bounds__(V == 3 ? tma::kBlock : kThreads) k_amul_dot(MeshArgs a, Workspace w, int fin)
+__global__ void __launch_bounds__(V == 3 ? tma::kBlock : kThreads, amul_min_ctas<V>())
+    k_amul_dot(MeshArgs a, Workspace w, int fin)
 {
     if (w.scal->done) return;
     const DevPtrs p = *w.ptrs;
@@ -544,6 +558,13 @@ __global__ void __launch_bounds__(V == 3 ? tma::kBlock : kThreads) k_amul_dot(Me
         __shared__ tma::Smem sm;
         const tma::Bounds bd{a.F, (long long)a.N + 8, a.N};
         v[0] = tma::amul_tma<true>(a, p.diag, p.upper, p.iface, w.pA, w.xr, w.wA, bd, sm);
+    } else if constexpr (V == 5) {
+        double acc = 0.0;
+        for (int t0 = blockIdx.x * 2 * kThreads; t0 < a.N; t0 += gridDim.x * 2 * kThreads) {
+            const int c = t0 + threadIdx.x;
+            if (c < a.N) amul_rows2(a, c, c + kThreads, p.diag, p.upper, p.iface, w.pA, w.xr, w.wA, acc, true);
+        }
+        v[0] = acc;
     } else {
         for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < a.N; c += gridDim.x * blockDim.x) {
             const double y = V == 2 ? amul_row_unrolled(a, c, p.diag, p.upper, p.iface, w.pA, w.xr)
@@ -674,6 +695,8 @@ int occupancy_grid(int N, int* grid_faces, int F)
     g = std::max(g, grid_for(k_amul_dot<1>, N));
     g = std::max(g, grid_for(k_amul_dot<2>, N));
     g = std::max(g, grid_for(k_amul_dot<3>, (N + tma::kCells - 1) / tma::kCells, 1, 1));
+    g = std::max(g, grid_for(k_amul_dot<4>, N));
+    g = std::max(g, grid_for(k_amul_dot<5>, N, 2));
     g = std::max(g, grid_for(k_update, N, 2));
     if (grid_faces) *grid_faces = grid_for(k_face_coeffs, F);
     return g;
@@ -731,6 +754,8 @@ void launch_amul(cudaStream_t s, int variant, const MeshArgs& a, const double* d
         k_amul<3><<<grid_for(k_amul<3>, (a.N + tma::kCells - 1) / tma::kCells, 1, 1), tma::kBlock, 0, s>>>(a, diag, upper, iface,
                                                                                             x, xr, y, bd);
         break;
+    case 4: k_amul<4><<<grid_for(k_amul<4>, a.N), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd); break;
+    case 5: k_amul<5><<<grid_for(k_amul<5>, a.N, 2), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd); break;
     default: k_amul<0><<<grid_for(k_amul<0>, a.N), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd); break;
     }
 }
@@ -779,6 +804,8 @@ void launch_amul_dot(cudaStream_t s, int variant, const MeshArgs& a, const Works
     case 3:
         k_amul_dot<3><<<grid_for(k_amul_dot<3>, (a.N + tma::kCells - 1) / tma::kCells, 1, 1), tma::kBlock, 0, s>>>(a, w, f);
         break;
+    case 4: k_amul_dot<4><<<grid_for(k_amul_dot<4>, a.N), kThreads, 0, s>>>(a, w, f); break;
+    case 5: k_amul_dot<5><<<grid_for(k_amul_dot<5>, a.N, 2), kThreads, 0, s>>>(a, w, f); break;
     default: k_amul_dot<0><<<grid_for(k_amul_dot<0>, a.N), kThreads, 0, s>>>(a, w, f); break;
     }
 }
