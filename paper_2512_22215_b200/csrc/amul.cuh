@@ -9,6 +9,8 @@
 //   4  per-row capped at 32 registers (8 CTAs of 256 threads per SM: more warps in flight)
 //   5  unrolled, two cells per thread (c and c + 256 of a 512-cell tile): both cells'
 //      loads issued together, twice the bytes in flight per thread
+//   6  SELL-C:    chunk-of-32 slot layout, packed neighbour side, one row per thread
+//   7  SELL-C:    two rows per thread (chunks k and k+1 of a 64-cell warp tile)
 //   3  tma:       warp-specialised pipeline -- a producer warp streams each tile's
 //                 contiguous ranges (upper/neighbour of the owner side,
 //                 losort/ownerLo of the neighbour side, ownerStart/losortStart,
@@ -129,6 +131,98 @@ __device__ __forceinline__ void amul_rows2(const MeshArgs& a, int c, int e, cons
     }
 }
 
+// ---------------------------------------------------------------------------- variants 6, 7 (SELL-C)
+// Rows read from the SELL-C slots (host.h build_sell): the neighbour side is one packed
+// int32 per entry (owner column << 5 | position of the face in the owner's range), so
+// neither losort nor losortStart is streamed: DRAM bytes ~ 16 per face (upper 8, two
+// 4-byte slots) + 28 per cell (ownerStart, diag, x, y).  Coefficient of a neighbour-side
+// entry = upper[ownerStart[column] + position] (L2 hit: the owner's row streamed it).
+// When every chunk has the same widths (hex meshes) the slot bases are arithmetic and
+// the per-chunk meta load drops out of the dependency chain.
+template <int R>
+__device__ __forceinline__ void amul_rows_sell(const MeshArgs& a, int c, int wn_u, int wo_u,
+                                               const double* __restrict__ diag, const double* __restrict__ upper,
+                                               const double* __restrict__ iface, const double* __restrict__ x,
+                                               const double* __restrict__ xr, double* __restrict__ y, double& acc,
+                                               bool dot)
+{
+    constexpr int W = 3;  // fast-path slot width per side
+    const int l = c & 31;
+    int cc[R], nbase[R], obase[R], wn[R], wo[R], osc[R];
+    double dg[R], xc[R];
+    bool ok = true;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        cc[r] = min(c + 32 * r, a.N - 1);
+        const int k = cc[r] >> 5;
+        if (wn_u >= 0) {
+            nbase[r] = k * 32 * wn_u;
+            obase[r] = k * 32 * wo_u;
+            wn[r] = wn_u;
+            wo[r] = wo_u;
+        } else {
+            const int4 m = __ldg(a.sell_meta + k);
+            nbase[r] = m.x, obase[r] = m.y, wn[r] = m.z, wo[r] = m.w;
+        }
+        ok = ok && wn[r] <= W && wo[r] <= W;
+        osc[r] = __ldg(a.ownerStart + cc[r]);
+        dg[r] = __ldg(diag + cc[r]);
+        xc[r] = __ldg(x + cc[r]);
+    }
+    if (!ok || a.ifStart) {
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+            if (c + 32 * r < a.N) {
+                const double v = amul_row(a, cc[r], diag, upper, iface, x, xr, nullptr);
+                y[cc[r]] = v;
+                if (dot) acc += v * xc[r];
+            }
+        return;
+    }
+    unsigned pk[R][W];
+    int nb[R][W];
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+            pk[r][j] = j < wn[r] ? __ldg(a.sell_n + nbase[r] + 32 * j + l) : 0xFFFFFFFFu;
+            nb[r][j] = j < wo[r] ? __ldg(a.sell_o + obase[r] + 32 * j + l) : -1;
+        }
+    int oc[R][W];
+    double xn[R][W], xo[R][W], uo[R][W];
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+            const bool vn = pk[r][j] != 0xFFFFFFFFu, vo = nb[r][j] >= 0;
+            const int col = vn ? (int)(pk[r][j] >> 5) : cc[r];
+            oc[r][j] = vn ? __ldg(a.ownerStart + col) : 0;
+            xn[r][j] = __ldg(x + col);
+            xo[r][j] = __ldg(x + (vo ? nb[r][j] : cc[r]));
+            uo[r][j] = vo ? __ldg(upper + osc[r] + j) : 0.0;
+        }
+    double un[R][W];
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int j = 0; j < W; ++j)
+            un[r][j] = pk[r][j] != 0xFFFFFFFFu ? __ldg(upper + oc[r][j] + (int)(pk[r][j] & 31u)) : 0.0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        double s = dg[r] * xc[r];
+#pragma unroll
+        for (int j = 0; j < W; ++j)
+            if (pk[r][j] != 0xFFFFFFFFu) s = s + un[r][j] * xn[r][j];
+#pragma unroll
+        for (int j = 0; j < W; ++j)
+            if (nb[r][j] >= 0) s = s + uo[r][j] * xo[r][j];
+        if (c + 32 * r < a.N) {
+            y[cc[r]] = s;
+            if (dot) acc += s * xc[r];
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------- variant 3 (TMA)
 namespace tma {
 
@@ -203,6 +297,7 @@ __device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;
 // 8 elements; caller arrays (upper, diag, and x in the diagnostic Amul) are not.
 struct Bounds {
     long long upper_len, x_len, diag_len;
+    int sell_wn, sell_wo;  // uniform SELL widths, or -1 (per-chunk meta)
 };
 
 template <bool DOT>

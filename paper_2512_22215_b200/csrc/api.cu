@@ -81,6 +81,9 @@ MeshArgs mesh_args(const spuma_mesh m)
     a.ifStart = m->n_iface ? m->d_ifStart : nullptr;
     a.ifIdx = m->d_ifIdx;
     a.n_iface = m->n_iface;
+    a.sell_meta = reinterpret_cast<const int4*>(m->d_sell_meta);
+    a.sell_n = m->d_sell_n;
+    a.sell_o = m->d_sell_o;
     return a;
 }
 
@@ -223,7 +226,7 @@ spuma_status enqueue_iteration(spuma_mesh m, cudaStream_t s, std::vector<cudaEve
     if (ev) record(m, *ev, slot * 6 + 1, s);
     SPUMA_TRY(halo_exchange(m, m->ws.pA, m->ws.xr, s));
     if (ev) record(m, *ev, slot * 6 + 2, s);
-    launch_amul_dot(s, m->amul_variant, a, m->ws, fin);
+    launch_amul_dot(s, m->amul_variant, a, m->ws, fin, m->sell_wn, m->sell_wo);
     if (ev) record(m, *ev, slot * 6 + 3, s);
     if (!fin) SPUMA_TRY(reduce_finalize(m, 3, s));
     if (ev) record(m, *ev, slot * 6 + 4, s);
@@ -329,7 +332,8 @@ void spuma_free(spuma_mesh m)
         if (m->batch_done[i]) cudaEventDestroy(m->batch_done[i]);
         if (m->asm_ev[i]) cudaEventDestroy(m->asm_ev[i]);
     }
-    void* dptrs[] = {m->d_owner, m->d_neighbour, m->d_ownerStart, m->d_losortStart, m->d_losort, m->d_ownerLo,
+    void* dptrs[] = {m->d_sell_meta, m->d_sell_n, m->d_sell_o,
+                     m->d_owner, m->d_neighbour, m->d_ownerStart, m->d_losortStart, m->d_losort, m->d_ownerLo,
                      m->d_perm, m->d_face_map, m->d_delta, m->d_weights, m->d_magSf, m->d_bkind, m->d_bcell,
                      m->d_bproc, m->d_bmagSf, m->d_bdelta, m->d_bweight, m->d_bvalue, m->d_bgamma_r,
                      m->d_bis_owner, m->d_bStart, m->d_bFace, m->d_ifStart, m->d_ifIdx, m->d_if_cell,
@@ -498,6 +502,16 @@ static spuma_status mesh_create_impl(const spuma_mesh_desc* d, spuma_mesh m)
     SPUMA_TRY(upload(&m->d_losortStart, m->h_losortStart, s));
     SPUMA_TRY(upload(&m->d_losort, m->h_losort, s));
     SPUMA_TRY(upload(&m->d_ownerLo, ownerLo, s));
+    {
+        const SellHost sell = build_sell(N, m->h_ownerStart, m->h_losortStart, m->h_losort, ownerLo, neighbour);
+        if (sell.ok) {
+            m->sell_wn = sell.uniform_wn;
+            m->sell_wo = sell.uniform_wo;
+            SPUMA_TRY(upload(&m->d_sell_meta, sell.meta, s));
+            SPUMA_TRY(upload(&m->d_sell_n, sell.nslot, s));
+            SPUMA_TRY(upload(&m->d_sell_o, sell.oslot, s));
+        }
+    }
     if (m->renumber) {
         SPUMA_TRY(upload(&m->d_perm, m->h_perm, s));
         SPUMA_TRY(upload(&m->d_face_map, m->h_face_map, s));
@@ -691,7 +705,7 @@ spuma_status spuma_amul(spuma_mesh m, const spuma_scalar* diag, const spuma_scal
     }
     SPUMA_TRY(halo_exchange(m, x_i, m->ws.xr, s));
     launch_amul(s, m->amul_variant, mesh_args(m), d_i, u_i, if_i, x_i, m->ws.xr, y_i,
-                (x_i == x) ? (long long)m->N : (long long)m->N + kPad);
+                (x_i == x) ? (long long)m->N : (long long)m->N + kPad, m->sell_wn, m->sell_wo);
     m->stats.kernel_launches += 1;
     SPUMA_TRY(cells_out(m, y, y_i));
     SPUMA_CUDA(cudaStreamSynchronize(s));
@@ -840,7 +854,7 @@ spuma_status spuma_set_option(spuma_mesh m, int option, int value)
     if (!m) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "mesh is NULL");
     switch (option) {
     case SPUMA_OPT_AMUL_VARIANT:
-        if (value < 0 || value > 5) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "amul variant must be 0..5");
+        if (value < 0 || value > 7) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "amul variant must be 0..7");
         if (value != m->amul_variant) destroy_graphs(m);
         m->amul_variant = value;
         return SPUMA_OK;

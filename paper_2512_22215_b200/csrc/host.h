@@ -10,6 +10,21 @@ void rekey_faces(int N, int F, const int* perm, const int* owner, const int* nei
                  std::vector<int>& neighbour_out, std::vector<int>& face_map, std::vector<char>& flip);
 void derived_addressing(int N, int F, const int* owner, const int* neighbour, std::vector<int>& ownerStart,
                         std::vector<int>& losort, std::vector<int>& losortStart, std::vector<int>& ownerLo);
+// SELL-C (C = 32) layout of the Amul rows (variant 6/7).  Per chunk of 32 cells:
+// meta = {nbase, obase, wn, wo}; neighbour-side slot j of lane l at nslot[nbase + 32 j + l]
+// = (ownerLo << 5) | (face - ownerStart[ownerLo]) in losort order, 0xFFFFFFFF = empty;
+// owner-side slot j at oslot[obase + 32 j + l] = neighbour[ownerStart[c] + j], -1 = empty.
+struct SellHost {
+    std::vector<int> meta;          // [4 * chunks]
+    std::vector<unsigned> nslot;
+    std::vector<int> oslot;
+    bool ok = false;                // false: a column >= 2^27 - 1 or a position >= 31 (not encodable)
+    int uniform_wn = -1, uniform_wo = -1;  // >= 0: every chunk has these widths (bases = 32 k w)
+};
+SellHost build_sell(int N, const std::vector<int>& ownerStart, const std::vector<int>& losortStart,
+                    const std::vector<int>& losort, const std::vector<int>& ownerLo,
+                    const std::vector<int>& neighbour);
+
 // per-cell lists of the items i with keep[i], in input order
 void cell_lists(int N, const std::vector<int>& cell_of, const std::vector<char>& keep, std::vector<int>& start,
                 std::vector<int>& items);

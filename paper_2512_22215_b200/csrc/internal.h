@@ -51,6 +51,10 @@ struct MeshArgs {
     const int* ifStart;      // [N+1] or nullptr (no interfaces)
     const int* ifIdx;        // [n_iface] index into iface / x_remote arrays
     int n_iface;
+    // SELL-C layout (variants 6/7; see host.h build_sell), nullptr if not encodable
+    const int4* sell_meta;   // [chunks] {nbase, obase, wn, wo}
+    const unsigned* sell_n;  // neighbour-side slots (owner column << 5 | position in the owner's faces)
+    const int* sell_o;       // owner-side slots (neighbour column)
 };
 
 struct Workspace {
@@ -87,6 +91,10 @@ struct spuma_mesh_s {
     int *d_owner = nullptr, *d_neighbour = nullptr, *d_ownerStart = nullptr, *d_losortStart = nullptr;
     int *d_losort = nullptr, *d_ownerLo = nullptr;
     int *d_perm = nullptr, *d_face_map = nullptr;  // renumber only
+    int* d_sell_meta = nullptr;
+    int sell_wn = -1, sell_wo = -1;  // uniform chunk widths (ELL-like) or -1
+    unsigned* d_sell_n = nullptr;
+    int* d_sell_o = nullptr;
     // device: geometry
     double *d_delta = nullptr, *d_weights = nullptr, *d_magSf = nullptr;
     // device: boundary faces, concatenated in patch order (all patches)
@@ -165,7 +173,8 @@ void launch_diag_gather(cudaStream_t s, int grid, const MeshArgs& a, const doubl
                         const double* bgamma_r, const signed char* bis_owner, const double* gamma, int ref_cell,
                         double ref_value, double* diag, double* source, double* iface);
 void launch_amul(cudaStream_t s, int variant, const MeshArgs& a, const double* diag, const double* upper,
-                 const double* iface, const double* x, const double* xr, double* y, long long x_len);
+                 const double* iface, const double* x, const double* xr, double* y, long long x_len, int sell_wn,
+                 int sell_wo);
 void launch_gather(cudaStream_t s, int n, const int* idx, const double* in, double* out);   // out[i] = in[idx[i]]
 void launch_scatter(cudaStream_t s, int n, const int* idx, const double* in, double* out);  // out[idx[i]] = in[i]
 void launch_pack(cudaStream_t s, int n, const int* cell, const double* x, double* out);     // out[i] = x[cell[i]]
@@ -174,7 +183,8 @@ void launch_pack(cudaStream_t s, int n, const int* cell, const double* x, double
 void launch_setup1(cudaStream_t s, int grid, const MeshArgs& a, const Workspace& w, bool fin);
 void launch_setup2(cudaStream_t s, int grid, const MeshArgs& a, const Workspace& w, bool fin);
 void launch_direction(cudaStream_t s, int grid, const MeshArgs& a, const Workspace& w);
-void launch_amul_dot(cudaStream_t s, int variant, const MeshArgs& a, const Workspace& w, bool fin);
+void launch_amul_dot(cudaStream_t s, int variant, const MeshArgs& a, const Workspace& w, bool fin, int sell_wn,
+                     int sell_wo);
 constexpr int kPad = 8;  // padding elements on internal arrays (16-byte TMA windows may overrun by <= 3)
 void launch_update(cudaStream_t s, int grid, const MeshArgs& a, const Workspace& w, bool fin);
 // P > 1: finalise from the gathered rank partials ([n_ranks][4], rank order)

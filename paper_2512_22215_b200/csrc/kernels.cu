@@ -427,7 +427,7 @@ __global__ void __launch_bounds__(kThreads)
 template <int V>
 constexpr int amul_min_ctas()
 {
-    return V == 4 ? 8 : (V == 3 ? 4 : (V == 5 ? 3 : 6));
+    return V == 4 ? 8 : (V == 3 ? 4 : ((V == 5 || V == 7) ? 3 : (V == 6 ? 5 : 6)));
 }
 
 template <int V>
@@ -448,6 +448,12 @@ __global__ void __launch_bounds__(V == 3 ? tma::kBlock : kThreads, amul_min_ctas
             const int c = t0 + threadIdx.x;
             if (c < a.N) amul_rows2(a, c, c + kThreads, diag, upper, iface, x, xr, y, acc, false);
         }
+    } else if constexpr (V == 6 || V == 7) {
+        constexpr int R = V == 7 ? 2 : 1;
+        double acc = 0.0;
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        for (int t0 = (blockIdx.x * (kThreads / 32) + warp) * 32 * R; t0 < a.N; t0 += gridDim.x * kThreads * R)
+            amul_rows_sell<R>(a, t0 + lane, bd.sell_wn, bd.sell_wo, diag, upper, iface, x, xr, y, acc, false);
     } else {
         for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < a.N; c += gridDim.x * blockDim.x)
             y[c] = V == 2 ? amul_row_unrolled(a, c, diag, upper, iface, x, xr)
@@ -546,7 +552,7 @@ __global__ void __launch_bounds__(kThreads) k_direction(int N, Workspace w)
 // A7 + A8: wA = A pA, partial wA.pA -> alpha
 template <int V>
 __global__ void __launch_bounds__(V == 3 ? tma::kBlock : kThreads, amul_min_ctas<V>())
-    k_amul_dot(MeshArgs a, Workspace w, int fin)
+    k_amul_dot(MeshArgs a, Workspace w, int fin, int sell_wn, int sell_wo)
 {
     if (w.scal->done) return;
     const DevPtrs p = *w.ptrs;
@@ -556,7 +562,7 @@ __global__ void __launch_bounds__(V == 3 ? tma::kBlock : kThreads, amul_min_ctas
         v[0] = amul_tiles<true>(a, p.diag, p.upper, p.iface, w.pA, w.xr, w.wA, sm);
     } else if constexpr (V == 3) {
         __shared__ tma::Smem sm;
-        const tma::Bounds bd{a.F, (long long)a.N + 8, a.N};
+        const tma::Bounds bd{a.F, (long long)a.N + 8, a.N, sell_wn, sell_wo};
         v[0] = tma::amul_tma<true>(a, p.diag, p.upper, p.iface, w.pA, w.xr, w.wA, bd, sm);
     } else if constexpr (V == 5) {
         double acc = 0.0;
@@ -564,6 +570,13 @@ __global__ void __launch_bounds__(V == 3 ? tma::kBlock : kThreads, amul_min_ctas
             const int c = t0 + threadIdx.x;
             if (c < a.N) amul_rows2(a, c, c + kThreads, p.diag, p.upper, p.iface, w.pA, w.xr, w.wA, acc, true);
         }
+        v[0] = acc;
+    } else if constexpr (V == 6 || V == 7) {
+        constexpr int R = V == 7 ? 2 : 1;
+        double acc = 0.0;
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        for (int t0 = (blockIdx.x * (kThreads / 32) + warp) * 32 * R; t0 < a.N; t0 += gridDim.x * kThreads * R)
+            amul_rows_sell<R>(a, t0 + lane, sell_wn, sell_wo, p.diag, p.upper, p.iface, w.pA, w.xr, w.wA, acc, true);
         v[0] = acc;
     } else {
         for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < a.N; c += gridDim.x * blockDim.x) {
@@ -697,6 +710,8 @@ int occupancy_grid(int N, int* grid_faces, int F)
     g = std::max(g, grid_for(k_amul_dot<3>, (N + tma::kCells - 1) / tma::kCells, 1, 1));
     g = std::max(g, grid_for(k_amul_dot<4>, N));
     g = std::max(g, grid_for(k_amul_dot<5>, N, 2));
+    g = std::max(g, grid_for(k_amul_dot<6>, N));
+    g = std::max(g, grid_for(k_amul_dot<7>, N, 2));
     g = std::max(g, grid_for(k_update, N, 2));
     if (grid_faces) *grid_faces = grid_for(k_face_coeffs, F);
     return g;
@@ -743,10 +758,12 @@ void launch_diag_gather(cudaStream_t s, int grid, const MeshArgs& a, const doubl
 }
 
 void launch_amul(cudaStream_t s, int variant, const MeshArgs& a, const double* diag, const double* upper,
-                 const double* iface, const double* x, const double* xr, double* y, long long x_len)
+                 const double* iface, const double* x, const double* xr, double* y, long long x_len, int sell_wn,
+                 int sell_wo)
 {
     if (a.N <= 0) return;
-    const tma::Bounds bd{a.F, x_len, a.N};
+    if ((variant == 6 || variant == 7) && !a.sell_n) variant = 5;
+    const tma::Bounds bd{a.F, x_len, a.N, sell_wn, sell_wo};
     switch (variant) {
     case 1: k_amul<1><<<grid_for(k_amul<1>, a.N), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd); break;
     case 2: k_amul<2><<<grid_for(k_amul<2>, a.N), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd); break;
@@ -756,6 +773,8 @@ void launch_amul(cudaStream_t s, int variant, const MeshArgs& a, const double* d
         break;
     case 4: k_amul<4><<<grid_for(k_amul<4>, a.N), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd); break;
     case 5: k_amul<5><<<grid_for(k_amul<5>, a.N, 2), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd); break;
+    case 6: k_amul<6><<<grid_for(k_amul<6>, a.N), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd); break;
+    case 7: k_amul<7><<<grid_for(k_amul<7>, a.N, 2), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd); break;
     default: k_amul<0><<<grid_for(k_amul<0>, a.N), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd); break;
     }
 }
@@ -795,18 +814,22 @@ void launch_direction(cudaStream_t s, int grid, const MeshArgs& a, const Workspa
     k_direction<<<grid_for(k_direction, a.N, 2), kThreads, 0, s>>>(a.N, w);
 }
 
-void launch_amul_dot(cudaStream_t s, int variant, const MeshArgs& a, const Workspace& w, bool fin)
+void launch_amul_dot(cudaStream_t s, int variant, const MeshArgs& a, const Workspace& w, bool fin, int sell_wn,
+                     int sell_wo)
 {
     const int f = fin ? 1 : 0;
+    if ((variant == 6 || variant == 7) && !a.sell_n) variant = 5;  // layout not encodable on this mesh
     switch (variant) {
-    case 1: k_amul_dot<1><<<grid_for(k_amul_dot<1>, a.N), kThreads, 0, s>>>(a, w, f); break;
-    case 2: k_amul_dot<2><<<grid_for(k_amul_dot<2>, a.N), kThreads, 0, s>>>(a, w, f); break;
+    case 1: k_amul_dot<1><<<grid_for(k_amul_dot<1>, a.N), kThreads, 0, s>>>(a, w, f, sell_wn, sell_wo); break;
+    case 2: k_amul_dot<2><<<grid_for(k_amul_dot<2>, a.N), kThreads, 0, s>>>(a, w, f, sell_wn, sell_wo); break;
     case 3:
-        k_amul_dot<3><<<grid_for(k_amul_dot<3>, (a.N + tma::kCells - 1) / tma::kCells, 1, 1), tma::kBlock, 0, s>>>(a, w, f);
+        k_amul_dot<3><<<grid_for(k_amul_dot<3>, (a.N + tma::kCells - 1) / tma::kCells, 1, 1), tma::kBlock, 0, s>>>(a, w, f, sell_wn, sell_wo);
         break;
-    case 4: k_amul_dot<4><<<grid_for(k_amul_dot<4>, a.N), kThreads, 0, s>>>(a, w, f); break;
-    case 5: k_amul_dot<5><<<grid_for(k_amul_dot<5>, a.N, 2), kThreads, 0, s>>>(a, w, f); break;
-    default: k_amul_dot<0><<<grid_for(k_amul_dot<0>, a.N), kThreads, 0, s>>>(a, w, f); break;
+    case 4: k_amul_dot<4><<<grid_for(k_amul_dot<4>, a.N), kThreads, 0, s>>>(a, w, f, sell_wn, sell_wo); break;
+    case 5: k_amul_dot<5><<<grid_for(k_amul_dot<5>, a.N, 2), kThreads, 0, s>>>(a, w, f, sell_wn, sell_wo); break;
+    case 6: k_amul_dot<6><<<grid_for(k_amul_dot<6>, a.N), kThreads, 0, s>>>(a, w, f, sell_wn, sell_wo); break;
+    case 7: k_amul_dot<7><<<grid_for(k_amul_dot<7>, a.N, 2), kThreads, 0, s>>>(a, w, f, sell_wn, sell_wo); break;
+    default: k_amul_dot<0><<<grid_for(k_amul_dot<0>, a.N), kThreads, 0, s>>>(a, w, f, sell_wn, sell_wo); break;
     }
 }
 

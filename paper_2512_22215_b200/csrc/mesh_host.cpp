@@ -149,4 +149,61 @@ void cell_lists(int N, const std::vector<int>& cell_of, const std::vector<char>&
         if (keep[i]) items[pos[cell_of[i]]++] = i;  // stable: input order
 }
 
+SellHost build_sell(int N, const std::vector<int>& ownerStart, const std::vector<int>& losortStart,
+                    const std::vector<int>& losort, const std::vector<int>& ownerLo,
+                    const std::vector<int>& neighbour)
+{
+    SellHost S;
+    const int chunks = (N + 31) / 32;
+    S.meta.assign(4 * (size_t)chunks, 0);
+    std::vector<int> cwn(chunks), cwo(chunks);
+    size_t sell_slots = 0;
+    int gwn = 0, gwo = 0;
+    for (int k = 0; k < chunks; ++k) {
+        int wn = 0, wo = 0;
+        for (int c = 32 * k; c < std::min(N, 32 * k + 32); ++c) {
+            wn = std::max(wn, losortStart[c + 1] - losortStart[c]);
+            wo = std::max(wo, ownerStart[c + 1] - ownerStart[c]);
+        }
+        cwn[k] = wn;
+        cwo[k] = wo;
+        gwn = std::max(gwn, wn);
+        gwo = std::max(gwo, wo);
+        sell_slots += 32 * (size_t)(wn + wo);
+    }
+    // ELL-like uniform widths when they pad by <= 10 %: slot bases become arithmetic
+    const bool uniform = 32 * (size_t)chunks * (gwn + gwo) * 10 <= sell_slots * 11;
+    if (uniform) {
+        S.uniform_wn = gwn;
+        S.uniform_wo = gwo;
+    }
+    size_t nb = 0, ob = 0;
+    for (int k = 0; k < chunks; ++k) {
+        const int wn = uniform ? gwn : cwn[k], wo = uniform ? gwo : cwo[k];
+        S.meta[4 * k + 0] = (int)std::min(nb, (size_t)INT32_MAX);
+        S.meta[4 * k + 1] = (int)std::min(ob, (size_t)INT32_MAX);
+        S.meta[4 * k + 2] = wn;
+        S.meta[4 * k + 3] = wo;
+        nb += 32 * (size_t)wn;
+        ob += 32 * (size_t)wo;
+    }
+    if (nb >= (1ull << 31) || ob >= (1ull << 31)) return S;
+    S.nslot.assign(nb, 0xFFFFFFFFu);
+    S.oslot.assign(ob, -1);
+    for (int c = 0; c < N; ++c) {
+        const int k = c >> 5, l = c & 31;
+        const int nbase = S.meta[4 * k], obase = S.meta[4 * k + 1];
+        for (int q = losortStart[c], j = 0; q < losortStart[c + 1]; ++q, ++j) {
+            const int o = ownerLo[q];
+            const int pos = losort[q] - ownerStart[o];
+            if (o >= (1 << 27) - 1 || pos >= 31) return S;
+            S.nslot[nbase + 32 * (size_t)j + l] = ((unsigned)o << 5) | (unsigned)pos;
+        }
+        for (int f = ownerStart[c], j = 0; f < ownerStart[c + 1]; ++f, ++j)
+            S.oslot[obase + 32 * (size_t)j + l] = neighbour[f];
+    }
+    S.ok = true;
+    return S;
+}
+
 }  // namespace spuma
