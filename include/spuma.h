@@ -227,7 +227,9 @@ spuma_status spuma_set_batch(spuma_mesh m, int iterations);
  * bitwise identical): 0 per-row, 1 CTA tile, 2 unrolled per-row, 3 TMA
  * producer/consumer pipeline (cp.async.bulk + mbarrier), 4 per-row at 8 CTAs/SM,
  * 5 unrolled two rows per thread, 6/7 SELL-C-32 slot layout with packed neighbour
- * side (one / two rows per thread).  Errors: INVALID_ARGUMENT. */
+ * side (one / two rows per thread), 8/9 ELL with a per-solve owner-slot ordered
+ * coefficient copy (no row extents streamed; one / two rows per thread).
+ * Errors: INVALID_ARGUMENT. */
 typedef enum { SPUMA_OPT_AMUL_VARIANT = 0 } spuma_option;
 spuma_status spuma_set_option(spuma_mesh m, int option, int value);
 

@@ -11,6 +11,8 @@
 //      loads issued together, twice the bytes in flight per thread
 //   6  SELL-C:    chunk-of-32 slot layout, packed neighbour side, one row per thread
 //   7  SELL-C:    two rows per thread (chunks k and k+1 of a 64-cell warp tile)
+//   8  ELL:       uniform-width SELL + per-solve owner-slot coefficient copy, 1 row/thread
+//   9  ELL:       same, two rows per thread
 //   3  tma:       warp-specialised pipeline -- a producer warp streams each tile's
 //                 contiguous ranges (upper/neighbour of the owner side,
 //                 losort/ownerLo of the neighbour side, ownerStart/losortStart,
@@ -207,6 +209,80 @@ __device__ __forceinline__ void amul_rows_sell(const MeshArgs& a, int c, int wn_
 #pragma unroll
         for (int j = 0; j < W; ++j)
             un[r][j] = pk[r][j] != 0xFFFFFFFFu ? __ldg(upper + oc[r][j] + (int)(pk[r][j] & 31u)) : 0.0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        double s = dg[r] * xc[r];
+#pragma unroll
+        for (int j = 0; j < W; ++j)
+            if (pk[r][j] != 0xFFFFFFFFu) s = s + un[r][j] * xn[r][j];
+#pragma unroll
+        for (int j = 0; j < W; ++j)
+            if (nb[r][j] >= 0) s = s + uo[r][j] * xo[r][j];
+        if (c + 32 * r < a.N) {
+            y[cc[r]] = s;
+            if (dot) acc += s * xc[r];
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------- variants 8, 9 (ELL + coefficient copy)
+// Uniform-width SELL (ELL) layout plus a per-solve copy of the coefficients in owner-side
+// slot order, upper_s[32 wo k + 32 j + l] = upper[ownerStart[c] + j] (c = 32 k + l).  The
+// owner side then streams (upper_s, neighbour slot) and the neighbour side finds its
+// coefficient at upper_s[32 wo (col >> 5) + 32 pos + (col & 31)] -- an L2 hit of the
+// owner's chunk -- so no row extent is loaded at all: two dependent levels, DRAM bytes
+// ~ 16 per face + 24 per cell (the algorithmic minimum of SURVEY §8(d)).
+template <int R>
+__device__ __forceinline__ void amul_rows_ell(const MeshArgs& a, int c, int wn, int wo,
+                                              const double* __restrict__ diag, const double* __restrict__ upper,
+                                              const double* __restrict__ upper_s, const double* __restrict__ iface,
+                                              const double* __restrict__ x, const double* __restrict__ xr,
+                                              double* __restrict__ y, double& acc, bool dot)
+{
+    constexpr int W = 3;
+    const int l = c & 31;
+    if (wn > W || wo > W || a.ifStart) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int cr = c + 32 * r;
+            if (cr < a.N) {
+                const double v = amul_row(a, cr, diag, upper, iface, x, xr, nullptr);
+                y[cr] = v;
+                if (dot) acc += v * x[cr];
+            }
+        }
+        return;
+    }
+    int cc[R];
+    double dg[R], xc[R];
+    unsigned pk[R][W];
+    int nb[R][W];
+    double uo[R][W];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        cc[r] = min(c + 32 * r, a.N - 1);
+        const int k = cc[r] >> 5;
+        dg[r] = __ldg(diag + cc[r]);
+        xc[r] = __ldg(x + cc[r]);
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+            pk[r][j] = j < wn ? __ldg(a.sell_n + (size_t)32 * wn * k + 32 * j + l) : 0xFFFFFFFFu;
+            nb[r][j] = j < wo ? __ldg(a.sell_o + (size_t)32 * wo * k + 32 * j + l) : -1;
+            uo[r][j] = j < wo ? __ldg(upper_s + (size_t)32 * wo * k + 32 * j + l) : 0.0;
+        }
+    }
+    double un[R][W], xn[R][W], xo[R][W];
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+            const bool vn = pk[r][j] != 0xFFFFFFFFu;
+            const int col = vn ? (int)(pk[r][j] >> 5) : cc[r];
+            const int pos = (int)(pk[r][j] & 31u);
+            un[r][j] = vn ? __ldg(upper_s + (size_t)32 * wo * (col >> 5) + 32 * pos + (col & 31)) : 0.0;
+            xn[r][j] = __ldg(x + col);
+            xo[r][j] = __ldg(x + (nb[r][j] >= 0 ? nb[r][j] : cc[r]));
+        }
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         double s = dg[r] * xc[r];

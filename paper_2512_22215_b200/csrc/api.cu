@@ -84,6 +84,9 @@ MeshArgs mesh_args(const spuma_mesh m)
     a.sell_meta = reinterpret_cast<const int4*>(m->d_sell_meta);
     a.sell_n = m->d_sell_n;
     a.sell_o = m->d_sell_o;
+    a.ell_wn = m->sell_wn;
+    a.ell_wo = m->sell_wo;
+    a.upper_s = m->d_upper_s;
     return a;
 }
 
@@ -332,7 +335,7 @@ void spuma_free(spuma_mesh m)
         if (m->batch_done[i]) cudaEventDestroy(m->batch_done[i]);
         if (m->asm_ev[i]) cudaEventDestroy(m->asm_ev[i]);
     }
-    void* dptrs[] = {m->d_sell_meta, m->d_sell_n, m->d_sell_o,
+    void* dptrs[] = {m->d_sell_meta, m->d_sell_n, m->d_sell_o, m->d_upper_s,
                      m->d_owner, m->d_neighbour, m->d_ownerStart, m->d_losortStart, m->d_losort, m->d_ownerLo,
                      m->d_perm, m->d_face_map, m->d_delta, m->d_weights, m->d_magSf, m->d_bkind, m->d_bcell,
                      m->d_bproc, m->d_bmagSf, m->d_bdelta, m->d_bweight, m->d_bvalue, m->d_bgamma_r,
@@ -507,6 +510,7 @@ static spuma_status mesh_create_impl(const spuma_mesh_desc* d, spuma_mesh m)
         if (sell.ok) {
             m->sell_wn = sell.uniform_wn;
             m->sell_wo = sell.uniform_wo;
+            if (m->sell_wo >= 0) SPUMA_TRY(dalloc(&m->d_upper_s, (size_t)32 * m->sell_wo * ((N + 31) / 32)));
             SPUMA_TRY(upload(&m->d_sell_meta, sell.meta, s));
             SPUMA_TRY(upload(&m->d_sell_n, sell.nslot, s));
             SPUMA_TRY(upload(&m->d_sell_o, sell.oslot, s));
@@ -704,6 +708,10 @@ spuma_status spuma_amul(spuma_mesh m, const spuma_scalar* diag, const spuma_scal
         y_i = m->d_cell_t;
     }
     SPUMA_TRY(halo_exchange(m, x_i, m->ws.xr, s));
+    if (amul_uses_ell(m->amul_variant) && m->d_upper_s) {
+        launch_ell_coeffs(s, mesh_args(m), u_i, m->d_upper_s);
+        m->stats.kernel_launches += 1;
+    }
     launch_amul(s, m->amul_variant, mesh_args(m), d_i, u_i, if_i, x_i, m->ws.xr, y_i,
                 (x_i == x) ? (long long)m->N : (long long)m->N + kPad, m->sell_wn, m->sell_wo);
     m->stats.kernel_launches += 1;
@@ -738,6 +746,10 @@ spuma_status spuma_pcg_solve(spuma_mesh m, const spuma_scalar* diag, const spuma
 
     // ---- A6 setup
     const MeshArgs a = mesh_args(m);
+    if (amul_uses_ell(m->amul_variant) && m->d_upper_s) {
+        launch_ell_coeffs(s, a, P.upper, m->d_upper_s);
+        m->stats.kernel_launches += 1;
+    }
     const bool fin = m->n_ranks == 1;
     SPUMA_TRY(halo_exchange(m, P.psi, m->ws.xr, s));
     launch_setup1(s, m->grid, a, m->ws, fin);
@@ -854,7 +866,7 @@ spuma_status spuma_set_option(spuma_mesh m, int option, int value)
     if (!m) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "mesh is NULL");
     switch (option) {
     case SPUMA_OPT_AMUL_VARIANT:
-        if (value < 0 || value > 7) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "amul variant must be 0..7");
+        if (value < 0 || value > 9) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "amul variant must be 0..9");
         if (value != m->amul_variant) destroy_graphs(m);
         m->amul_variant = value;
         return SPUMA_OK;

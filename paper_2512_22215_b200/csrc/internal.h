@@ -55,6 +55,8 @@ struct MeshArgs {
     const int4* sell_meta;   // [chunks] {nbase, obase, wn, wo}
     const unsigned* sell_n;  // neighbour-side slots (owner column << 5 | position in the owner's faces)
     const int* sell_o;       // owner-side slots (neighbour column)
+    int ell_wn, ell_wo;      // uniform chunk widths (ELL) or -1
+    const double* upper_s;   // owner-slot ordered coefficient copy (variants 8/9), refreshed per call
 };
 
 struct Workspace {
@@ -93,6 +95,7 @@ struct spuma_mesh_s {
     int *d_perm = nullptr, *d_face_map = nullptr;  // renumber only
     int* d_sell_meta = nullptr;
     int sell_wn = -1, sell_wo = -1;  // uniform chunk widths (ELL-like) or -1
+    double* d_upper_s = nullptr;     // [32 * sell_wo * chunks] (uniform layout only)
     unsigned* d_sell_n = nullptr;
     int* d_sell_o = nullptr;
     // device: geometry
@@ -176,6 +179,8 @@ void launch_amul(cudaStream_t s, int variant, const MeshArgs& a, const double* d
                  const double* iface, const double* x, const double* xr, double* y, long long x_len, int sell_wn,
                  int sell_wo);
 void launch_gather(cudaStream_t s, int n, const int* idx, const double* in, double* out);   // out[i] = in[idx[i]]
+void launch_ell_coeffs(cudaStream_t s, const MeshArgs& a, const double* upper, double* upper_s);
+bool amul_uses_ell(int variant);
 void launch_scatter(cudaStream_t s, int n, const int* idx, const double* in, double* out);  // out[idx[i]] = in[i]
 void launch_pack(cudaStream_t s, int n, const int* cell, const double* x, double* out);     // out[i] = x[cell[i]]
 

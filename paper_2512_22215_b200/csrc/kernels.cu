@@ -427,7 +427,7 @@ __global__ void __launch_bounds__(kThreads)
 template <int V>
 constexpr int amul_min_ctas()
 {
-    return V == 4 ? 8 : (V == 3 ? 4 : ((V == 5 || V == 7) ? 3 : (V == 6 ? 5 : 6)));
+    return V == 4 ? 8 : (V == 3 ? 4 : ((V == 5 || V == 7 || V == 9) ? 3 : ((V == 6 || V == 8) ? 5 : 6)));
 }
 
 template <int V>
@@ -454,6 +454,12 @@ __global__ void __launch_bounds__(V == 3 ? tma::kBlock : kThreads, amul_min_ctas
         const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
         for (int t0 = (blockIdx.x * (kThreads / 32) + warp) * 32 * R; t0 < a.N; t0 += gridDim.x * kThreads * R)
             amul_rows_sell<R>(a, t0 + lane, bd.sell_wn, bd.sell_wo, diag, upper, iface, x, xr, y, acc, false);
+    } else if constexpr (V == 8 || V == 9) {
+        constexpr int R = V == 9 ? 2 : 1;
+        double acc = 0.0;
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        for (int t0 = (blockIdx.x * (kThreads / 32) + warp) * 32 * R; t0 < a.N; t0 += gridDim.x * kThreads * R)
+            amul_rows_ell<R>(a, t0 + lane, a.ell_wn, a.ell_wo, diag, upper, a.upper_s, iface, x, xr, y, acc, false);
     } else {
         for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < a.N; c += gridDim.x * blockDim.x)
             y[c] = V == 2 ? amul_row_unrolled(a, c, diag, upper, iface, x, xr)
@@ -577,6 +583,14 @@ __global__ void __launch_bounds__(V == 3 ? tma::kBlock : kThreads, amul_min_ctas
         const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
         for (int t0 = (blockIdx.x * (kThreads / 32) + warp) * 32 * R; t0 < a.N; t0 += gridDim.x * kThreads * R)
             amul_rows_sell<R>(a, t0 + lane, sell_wn, sell_wo, p.diag, p.upper, p.iface, w.pA, w.xr, w.wA, acc, true);
+        v[0] = acc;
+    } else if constexpr (V == 8 || V == 9) {
+        constexpr int R = V == 9 ? 2 : 1;
+        double acc = 0.0;
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        for (int t0 = (blockIdx.x * (kThreads / 32) + warp) * 32 * R; t0 < a.N; t0 += gridDim.x * kThreads * R)
+            amul_rows_ell<R>(a, t0 + lane, a.ell_wn, a.ell_wo, p.diag, p.upper, a.upper_s, p.iface, w.pA, w.xr, w.wA,
+                             acc, true);
         v[0] = acc;
     } else {
         for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < a.N; c += gridDim.x * blockDim.x) {
@@ -712,6 +726,8 @@ int occupancy_grid(int N, int* grid_faces, int F)
     g = std::max(g, grid_for(k_amul_dot<5>, N, 2));
     g = std::max(g, grid_for(k_amul_dot<6>, N));
     g = std::max(g, grid_for(k_amul_dot<7>, N, 2));
+    g = std::max(g, grid_for(k_amul_dot<8>, N));
+    g = std::max(g, grid_for(k_amul_dot<9>, N, 2));
     g = std::max(g, grid_for(k_update, N, 2));
     if (grid_faces) *grid_faces = grid_for(k_face_coeffs, F);
     return g;
@@ -762,6 +778,7 @@ void launch_amul(cudaStream_t s, int variant, const MeshArgs& a, const double* d
                  int sell_wo)
 {
     if (a.N <= 0) return;
+    if ((variant == 8 || variant == 9) && !a.upper_s) variant -= 2;
     if ((variant == 6 || variant == 7) && !a.sell_n) variant = 5;
     const tma::Bounds bd{a.F, x_len, a.N, sell_wn, sell_wo};
     switch (variant) {
@@ -775,8 +792,28 @@ void launch_amul(cudaStream_t s, int variant, const MeshArgs& a, const double* d
     case 5: k_amul<5><<<grid_for(k_amul<5>, a.N, 2), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd); break;
     case 6: k_amul<6><<<grid_for(k_amul<6>, a.N), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd); break;
     case 7: k_amul<7><<<grid_for(k_amul<7>, a.N, 2), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd); break;
+    case 8: k_amul<8><<<grid_for(k_amul<8>, a.N), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd); break;
+    case 9: k_amul<9><<<grid_for(k_amul<9>, a.N, 2), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd); break;
     default: k_amul<0><<<grid_for(k_amul<0>, a.N), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd); break;
     }
+}
+
+// owner-slot ordered coefficient copy for variants 8/9 (once per solve / Amul call)
+__global__ void k_ell_coeffs(MeshArgs a, const double* __restrict__ upper, double* __restrict__ upper_s)
+{
+    for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < a.F; f += gridDim.x * blockDim.x) {
+        const int o = a.owner[f];
+        const int j = f - a.ownerStart[o];
+        upper_s[(size_t)32 * a.ell_wo * (o >> 5) + 32 * j + (o & 31)] = upper[f];
+    }
+}
+
+bool amul_uses_ell(int variant) { return variant == 8 || variant == 9; }
+
+void launch_ell_coeffs(cudaStream_t s, const MeshArgs& a, const double* upper, double* upper_s)
+{
+    if (a.F <= 0 || !upper_s) return;
+    k_ell_coeffs<<<grid_for(k_ell_coeffs, a.F), kThreads, 0, s>>>(a, upper, upper_s);
 }
 
 void launch_gather(cudaStream_t s, int n, const int* idx, const double* in, double* out)
@@ -818,7 +855,8 @@ void launch_amul_dot(cudaStream_t s, int variant, const MeshArgs& a, const Works
                      int sell_wo)
 {
     const int f = fin ? 1 : 0;
-    if ((variant == 6 || variant == 7) && !a.sell_n) variant = 5;  // layout not encodable on this mesh
+    if ((variant == 8 || variant == 9) && !a.upper_s) variant -= 2;  // no uniform-width layout: SELL
+    if ((variant == 6 || variant == 7) && !a.sell_n) variant = 5;    // layout not encodable on this mesh
     switch (variant) {
     case 1: k_amul_dot<1><<<grid_for(k_amul_dot<1>, a.N), kThreads, 0, s>>>(a, w, f, sell_wn, sell_wo); break;
     case 2: k_amul_dot<2><<<grid_for(k_amul_dot<2>, a.N), kThreads, 0, s>>>(a, w, f, sell_wn, sell_wo); break;
@@ -829,6 +867,8 @@ void launch_amul_dot(cudaStream_t s, int variant, const MeshArgs& a, const Works
     case 5: k_amul_dot<5><<<grid_for(k_amul_dot<5>, a.N, 2), kThreads, 0, s>>>(a, w, f, sell_wn, sell_wo); break;
     case 6: k_amul_dot<6><<<grid_for(k_amul_dot<6>, a.N), kThreads, 0, s>>>(a, w, f, sell_wn, sell_wo); break;
     case 7: k_amul_dot<7><<<grid_for(k_amul_dot<7>, a.N, 2), kThreads, 0, s>>>(a, w, f, sell_wn, sell_wo); break;
+    case 8: k_amul_dot<8><<<grid_for(k_amul_dot<8>, a.N), kThreads, 0, s>>>(a, w, f, sell_wn, sell_wo); break;
+    case 9: k_amul_dot<9><<<grid_for(k_amul_dot<9>, a.N, 2), kThreads, 0, s>>>(a, w, f, sell_wn, sell_wo); break;
     default: k_amul_dot<0><<<grid_for(k_amul_dot<0>, a.N), kThreads, 0, s>>>(a, w, f, sell_wn, sell_wo); break;
     }
 }

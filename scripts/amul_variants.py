@@ -28,7 +28,7 @@ diag, upper, src = torch.empty(N, **f64), torch.empty(F, **f64), torch.as_tensor
 h.assemble_laplacian(None, None, 0, 0.0, diag, upper, src, None)
 ref = None
 out = {}
-for v in [int(x) for x in os.environ.get("VARIANTS", "0,2,5,6,7,3").split(",")]:
+for v in [int(x) for x in os.environ.get("VARIANTS", "0,5,6,7,8,9").split(",")]:
     h.set_option(P.spuma.OPT_AMUL_VARIANT, v)
     psi = torch.zeros(N, **f64)
     h.pcg_solve(diag, upper, None, src, psi, 1e-6, 0.0, 5000, 0)  # warm-up / graph capture
