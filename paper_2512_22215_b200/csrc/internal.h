@@ -122,7 +122,7 @@ struct spuma_mesh_s {
 
     // captured iteration batches (ping-pong) and timing events
     int batch = 16;
-    int amul_variant = 0;
+    int amul_variant = 8;  // ELL + coefficient copy (falls back to 6 -> 5 when the mesh is not uniform)
     bool timing = false;
     cudaGraphExec_t gexec[2] = {nullptr, nullptr};
     bool gexec_timed = false;
