@@ -345,8 +345,8 @@ def main():
     ap.add_argument("--impl", default="spuma", choices=["spuma", "reference"])
     ap.add_argument("--n", type=int, default=200, help="cube edge per GPU (C3: 200)")
     ap.add_argument("--batch", type=int, default=16)
-    ap.add_argument("--cpu-iters", type=int, default=50)
-    ap.add_argument("--ref-iters", type=int, default=6)
+    ap.add_argument("--cpu-iters", type=int, default=150)
+    ap.add_argument("--ref-iters", type=int, default=20)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-kernel-timing", action="store_true")

@@ -60,7 +60,7 @@ def report(path, tag):
             for key in KEYS:
                 if key in h:
                     lines.append(f"{key:60s} {r[h.index(key)]:>20s} {units[h.index(key)]}")
-        name = k.split("::")[-1]
+        name = k.replace("void ", "").split("::")[-1].replace("<", "_").replace(">", "").strip()
         open(os.path.join(PROF, f"{tag}_ncu_{name}.txt"), "w").write("\n".join(lines) + "\n")
         print("\n".join(lines))
         if name.startswith("k_amul"):
