@@ -233,6 +233,24 @@ spuma_status spuma_set_batch(spuma_mesh m, int iterations);
 typedef enum { SPUMA_OPT_AMUL_VARIANT = 0 } spuma_option;
 spuma_status spuma_set_option(spuma_mesh m, int option, int value);
 
+/* External communication, used when n_ranks > 1 and desc.nccl_unique_id == NULL
+ * (a host transport instead of NCCL -- e.g. several ranks sharing one GPU in tests).
+ * Must be set before the first collective call.  Buffers are host memory; both
+ * callbacks are collective across ranks and return 0 on success (else the calling
+ * spuma_* function fails with SPUMA_ERR_NCCL).  The device path is unchanged except
+ * that the iteration batches are launched directly (host callbacks are not capturable).
+ *   exchange:  for i < n_peers send send[offsets[i] .. +counts[i]) to rank peers[i] and
+ *              receive counts[i] doubles from it into recv[offsets[i] ..) (processor-patch
+ *              halo, faces in ascending undecomposed face id on both sides, Q13)
+ *   allgather: n doubles from every rank into recv[n * rank ..), rank order */
+typedef struct {
+    void* ctx;
+    int (*exchange)(void* ctx, int n_peers, const int* peers, const int* offsets, const int* counts,
+                    const double* send, double* recv);
+    int (*allgather)(void* ctx, const double* send, double* recv, int n);
+} spuma_comm_callbacks;
+spuma_status spuma_set_comm_callbacks(spuma_mesh m, const spuma_comm_callbacks* cb);
+
 /* Fill out128 with a fresh ncclUniqueId (rank 0 calls it and broadcasts). */
 spuma_status spuma_nccl_get_unique_id(void* out128);
 

@@ -23,6 +23,21 @@
 
 namespace spuma {
 
+// Processor-interface terms of row c (after its internal faces, reading Q10); rows
+// without interfaces are skipped with one bit of a per-cell mask (1 bit / cell).
+__device__ __forceinline__ double add_iface(const MeshArgs& a, int c, double s, const double* __restrict__ iface,
+                                            const double* __restrict__ xr)
+{
+    if (a.ifMask && ((__ldg(a.ifMask + (c >> 5)) >> (c & 31)) & 1u)) {
+        const int j1 = a.ifStart[c + 1];
+        for (int j = a.ifStart[c]; j < j1; ++j) {
+            const int i = a.ifIdx[j];
+            s = s + iface[i] * xr[i];
+        }
+    }
+    return s;
+}
+
 // ---------------------------------------------------------------------------- variant 2
 __device__ __forceinline__ double amul_row_unrolled(const MeshArgs& a, int c, const double* __restrict__ diag,
                                                     const double* __restrict__ upper,
@@ -171,7 +186,7 @@ __device__ __forceinline__ void amul_rows_sell(const MeshArgs& a, int c, int wn_
         dg[r] = __ldg(diag + cc[r]);
         xc[r] = __ldg(x + cc[r]);
     }
-    if (!ok || a.ifStart) {
+    if (!ok) {
 #pragma unroll
         for (int r = 0; r < R; ++r)
             if (c + 32 * r < a.N) {
@@ -218,6 +233,7 @@ __device__ __forceinline__ void amul_rows_sell(const MeshArgs& a, int c, int wn_
 #pragma unroll
         for (int j = 0; j < W; ++j)
             if (nb[r][j] >= 0) s = s + uo[r][j] * xo[r][j];
+        s = add_iface(a, cc[r], s, iface, xr);
         if (c + 32 * r < a.N) {
             y[cc[r]] = s;
             if (dot) acc += s * xc[r];
@@ -241,7 +257,7 @@ __device__ __forceinline__ void amul_rows_ell(const MeshArgs& a, int c, int wn, 
 {
     constexpr int W = 3;
     const int l = c & 31;
-    if (wn > W || wo > W || a.ifStart) {
+    if (wn > W || wo > W) {
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             const int cr = c + 32 * r;
@@ -292,6 +308,7 @@ __device__ __forceinline__ void amul_rows_ell(const MeshArgs& a, int c, int wn, 
 #pragma unroll
         for (int j = 0; j < W; ++j)
             if (nb[r][j] >= 0) s = s + uo[r][j] * xo[r][j];
+        s = add_iface(a, cc[r], s, iface, xr);
         if (c + 32 * r < a.N) {
             y[cc[r]] = s;
             if (dot) acc += s * xc[r];

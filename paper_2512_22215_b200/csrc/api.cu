@@ -80,6 +80,7 @@ MeshArgs mesh_args(const spuma_mesh m)
     a.owner = m->d_owner;
     a.ifStart = m->n_iface ? m->d_ifStart : nullptr;
     a.ifIdx = m->d_ifIdx;
+    a.ifMask = m->n_iface ? m->d_ifMask : nullptr;
     a.n_iface = m->n_iface;
     a.sell_meta = reinterpret_cast<const int4*>(m->d_sell_meta);
     a.sell_n = m->d_sell_n;
@@ -191,7 +192,23 @@ spuma_status iface_in(spuma_mesh m, const double* p, const double** out)
 
 spuma_status halo_exchange(spuma_mesh m, const double* x, double* xr, cudaStream_t s)
 {
-    if (m->n_ranks == 1 || m->n_iface == 0) return SPUMA_OK;
+    if (m->n_ranks == 1) return SPUMA_OK;
+    if (m->external_comm) {
+        if (!m->cb.exchange) return set_error(SPUMA_ERR_STATE, "external comm: callbacks not set");
+        if (m->n_iface) {
+            launch_pack(s, m->n_iface, m->d_if_cell, x, m->d_sendbuf);
+            m->stats.kernel_launches += 1;
+            SPUMA_CUDA(cudaMemcpyAsync(m->h_send, m->d_sendbuf, sizeof(double) * m->n_iface, cudaMemcpyDeviceToHost, s));
+        }
+        SPUMA_CUDA(cudaStreamSynchronize(s));
+        if (m->cb.exchange(m->cb.ctx, (int)m->cb_peers.size(), m->cb_peers.data(), m->cb_offsets.data(),
+                           m->cb_counts.data(), m->h_send, m->h_recv) != 0)
+            return set_error(SPUMA_ERR_NCCL, "external comm: exchange callback failed");
+        if (m->n_iface)
+            SPUMA_CUDA(cudaMemcpyAsync(xr, m->h_recv, sizeof(double) * m->n_iface, cudaMemcpyHostToDevice, s));
+        return SPUMA_OK;
+    }
+    if (m->n_iface == 0) return SPUMA_OK;
     launch_pack(s, m->n_iface, m->d_if_cell, x, m->d_sendbuf);
     m->stats.kernel_launches += 1;
     SPUMA_NCCL(ncclGroupStart());
@@ -208,6 +225,17 @@ spuma_status halo_exchange(spuma_mesh m, const double* x, double* xr, cudaStream
 spuma_status reduce_finalize(spuma_mesh m, int stage, cudaStream_t s)
 {
     double* gathered = m->ws.part;  // free after the reduction kernel finished
+    if (m->external_comm) {
+        if (!m->cb.allgather) return set_error(SPUMA_ERR_STATE, "external comm: callbacks not set");
+        SPUMA_CUDA(cudaMemcpyAsync(m->h_part, m->ws.scal->rank_part, 4 * sizeof(double), cudaMemcpyDeviceToHost, s));
+        SPUMA_CUDA(cudaStreamSynchronize(s));
+        if (m->cb.allgather(m->cb.ctx, m->h_part, m->h_part + 4, 4) != 0)
+            return set_error(SPUMA_ERR_NCCL, "external comm: allgather callback failed");
+        SPUMA_CUDA(cudaMemcpyAsync(gathered, m->h_part + 4, 4 * sizeof(double) * m->n_ranks, cudaMemcpyHostToDevice, s));
+        launch_finalize(s, stage, gathered, m->n_ranks, m->ws);
+        m->stats.kernel_launches += 1;
+        return SPUMA_OK;
+    }
     SPUMA_NCCL(ncclAllGather(m->ws.scal->rank_part, gathered, 4, ncclDouble, m->comm, s));
     launch_finalize(s, stage, gathered, m->n_ranks, m->ws);
     m->stats.kernel_launches += 1;
@@ -339,13 +367,16 @@ void spuma_free(spuma_mesh m)
                      m->d_owner, m->d_neighbour, m->d_ownerStart, m->d_losortStart, m->d_losort, m->d_ownerLo,
                      m->d_perm, m->d_face_map, m->d_delta, m->d_weights, m->d_magSf, m->d_bkind, m->d_bcell,
                      m->d_bproc, m->d_bmagSf, m->d_bdelta, m->d_bweight, m->d_bvalue, m->d_bgamma_r,
-                     m->d_bis_owner, m->d_bStart, m->d_bFace, m->d_ifStart, m->d_ifIdx, m->d_if_cell,
+                     m->d_bis_owner, m->d_bStart, m->d_bFace, m->d_ifStart, m->d_ifIdx, m->d_if_cell, m->d_ifMask,
                      m->d_sendbuf, m->d_cell_a, m->d_cell_b, m->d_cell_c, m->d_cell_d, m->d_cell_e, m->d_cell_t,
                      m->d_face_a, m->d_face_t, m->d_iface_a, m->ws.wA, m->ws.rA, m->ws.pA, m->ws.rD, m->ws.sumA,
                      m->ws.xr, m->ws.part, m->ws.scal, m->ws.ptrs};
     for (void* p : dptrs)
         if (p) cudaFree(p);
     if (m->h_ptrs) cudaFreeHost(m->h_ptrs);
+    if (m->h_send) cudaFreeHost(m->h_send);
+    if (m->h_recv) cudaFreeHost(m->h_recv);
+    if (m->h_part) cudaFreeHost(m->h_part);
     if (m->h_scal) cudaFreeHost(m->h_scal);
     if (m->comm) ncclCommDestroy(m->comm);
     if (m->comm_stream) cudaStreamDestroy(m->comm_stream);
@@ -531,6 +562,11 @@ static spuma_status mesh_create_impl(const spuma_mesh_desc* d, spuma_mesh m)
     SPUMA_TRY(upload(&m->d_ifStart, ifStart, s));
     SPUMA_TRY(upload(&m->d_ifIdx, ifIdx, s));
     SPUMA_TRY(upload(&m->d_if_cell, if_cell, s));
+    {
+        std::vector<unsigned> mask((N + 31) / 32 + 1, 0u);
+        for (int c : if_cell) mask[c >> 5] |= 1u << (c & 31);
+        SPUMA_TRY(upload(&m->d_ifMask, mask, s));
+    }
     SPUMA_TRY(dalloc(&m->d_bdelta, m->Fb));
     SPUMA_TRY(dalloc(&m->d_bweight, m->Fb));
     SPUMA_TRY(dalloc(&m->d_bvalue, m->Fb));
@@ -584,10 +620,22 @@ static spuma_status mesh_create_impl(const spuma_mesh_desc* d, spuma_mesh m)
 
     // ---- communicator
     if (m->n_ranks > 1) {
-        if (!d->nccl_unique_id) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "n_ranks > 1 needs nccl_unique_id");
-        ncclUniqueId id;
-        std::memcpy(&id, d->nccl_unique_id, sizeof(id));
-        SPUMA_NCCL(ncclCommInitRank(&m->comm, m->n_ranks, id, m->rank));
+        for (const auto& P : m->patches)
+            if (P.kind == SPUMA_PATCH_PROCESSOR && P.n_faces > 0) {
+                m->cb_peers.push_back(P.neighbour_rank);
+                m->cb_offsets.push_back(P.iface_offset);
+                m->cb_counts.push_back(P.n_faces);
+            }
+        if (!d->nccl_unique_id) {
+            m->external_comm = true;
+            SPUMA_CUDA(cudaMallocHost(reinterpret_cast<void**>(&m->h_send), sizeof(double) * (m->n_iface + 1)));
+            SPUMA_CUDA(cudaMallocHost(reinterpret_cast<void**>(&m->h_recv), sizeof(double) * (m->n_iface + 1)));
+            SPUMA_CUDA(cudaMallocHost(reinterpret_cast<void**>(&m->h_part), sizeof(double) * 4 * (m->n_ranks + 1)));
+        } else {
+            ncclUniqueId id;
+            std::memcpy(&id, d->nccl_unique_id, sizeof(id));
+            SPUMA_NCCL(ncclCommInitRank(&m->comm, m->n_ranks, id, m->rank));
+        }
     }
     SPUMA_CUDA(cudaStreamSynchronize(s));
     m->stats.blocks_per_grid = m->grid;
@@ -758,6 +806,17 @@ spuma_status spuma_pcg_solve(spuma_mesh m, const spuma_scalar* diag, const spuma
     if (!fin) SPUMA_TRY(reduce_finalize(m, 2, s));
     m->stats.kernel_launches += 3;
 
+    if (m->external_comm) {  // host callbacks cannot be captured: iterate with direct launches
+        SPUMA_CUDA(cudaMemcpyAsync(&m->h_scal[0], m->ws.scal, sizeof(DevScal), cudaMemcpyDeviceToHost, s));
+        SPUMA_CUDA(cudaStreamSynchronize(s));
+        int it = 0;
+        while (!m->h_scal[0].done) {
+            SPUMA_TRY(enqueue_iteration(m, s, nullptr, 0));
+            SPUMA_CUDA(cudaMemcpyAsync(&m->h_scal[0], m->ws.scal, sizeof(DevScal), cudaMemcpyDeviceToHost, s));
+            SPUMA_CUDA(cudaStreamSynchronize(s));
+            if (++it > ctl->max_iter + 1) return set_error(SPUMA_ERR_STATE, "PCG loop did not terminate");
+        }
+    } else {
     // ---- A7-A11 in captured batches, ping-pong; host reads the scalars once per batch
     SPUMA_TRY(build_graphs(m));
     SPUMA_CUDA(cudaMemcpyAsync(&m->h_scal[1], m->ws.scal, sizeof(DevScal), cudaMemcpyDeviceToHost, s));
@@ -787,6 +846,8 @@ spuma_status spuma_pcg_solve(spuma_mesh m, const spuma_scalar* diag, const spuma
     }
     SPUMA_CUDA(cudaStreamSynchronize(s));
     if (m->timing && b > 0) SPUMA_TRY(account_timing(m, (b - 1) & 1, m->h_scal[(b - 1) & 1].n - prev_n));
+    m->stats.kernel_launches += launched_batches * (uint64_t)m->batch * launches_per_iteration(m);
+    }
     DevScal fs;
     SPUMA_CUDA(cudaMemcpy(&fs, m->ws.scal, sizeof(DevScal), cudaMemcpyDeviceToHost));
     SPUMA_CUDA(cudaGetLastError());
@@ -795,7 +856,6 @@ spuma_status spuma_pcg_solve(spuma_mesh m, const spuma_scalar* diag, const spuma
     perf->n_iterations = fs.n;
     perf->converged = fs.converged;
     perf->singular = fs.singular;
-    m->stats.kernel_launches += launched_batches * (uint64_t)m->batch * launches_per_iteration(m);
     m->stats.solves += 1;
     m->stats.iterations += fs.n;
     SPUMA_TRY(cells_out(m, psi, P.psi));
@@ -872,6 +932,14 @@ spuma_status spuma_set_option(spuma_mesh m, int option, int value)
         return SPUMA_OK;
     default: return set_error(SPUMA_ERR_INVALID_ARGUMENT, "unknown option");
     }
+}
+
+spuma_status spuma_set_comm_callbacks(spuma_mesh m, const spuma_comm_callbacks* cb)
+{
+    if (!m || !cb || !cb->exchange || !cb->allgather) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "NULL callbacks");
+    if (!m->external_comm) return set_error(SPUMA_ERR_STATE, "handle uses NCCL (or n_ranks == 1)");
+    m->cb = *cb;
+    return SPUMA_OK;
 }
 
 spuma_status spuma_set_batch(spuma_mesh m, int iterations)

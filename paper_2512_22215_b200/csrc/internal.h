@@ -50,6 +50,7 @@ struct MeshArgs {
     // processor interfaces, per cell in (patch, face) order
     const int* ifStart;      // [N+1] or nullptr (no interfaces)
     const int* ifIdx;        // [n_iface] index into iface / x_remote arrays
+    const unsigned* ifMask;  // [ceil(N/32)] bit c: cell c has interface faces (nullptr: none)
     int n_iface;
     // SELL-C layout (variants 6/7; see host.h build_sell), nullptr if not encodable
     const int4* sell_meta;   // [chunks] {nbase, obase, wn, wo}
@@ -84,6 +85,10 @@ struct spuma_mesh_s {
     bool own_stream = false;
     cudaStream_t comm_stream = nullptr;
     ncclComm_t comm = nullptr;
+    bool external_comm = false;          // n_ranks > 1 without an NCCL id: host callbacks
+    spuma_comm_callbacks cb{};
+    double *h_send = nullptr, *h_recv = nullptr, *h_part = nullptr;  // pinned (external comm)
+    std::vector<int> cb_peers, cb_offsets, cb_counts;
 
     std::vector<spuma::Patch> patches;
     // host copies of the derived addressing (internal numbering) for diagnostics
@@ -108,6 +113,7 @@ struct spuma_mesh_s {
     int *d_bStart = nullptr, *d_bFace = nullptr;   // per-cell lists of contributing boundary faces
     // device: interfaces
     int *d_ifStart = nullptr, *d_ifIdx = nullptr, *d_if_cell = nullptr;  // if_cell: [n_iface] local cell
+    unsigned* d_ifMask = nullptr;
     double* d_sendbuf = nullptr;     // [n_iface] packed x for the neighbours
     // staging (renumbering / host pointers), allocated on first use
     double *d_cell_a = nullptr, *d_cell_b = nullptr, *d_cell_c = nullptr, *d_cell_d = nullptr,

@@ -60,6 +60,17 @@ class SolverPerf(ctypes.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+EXCHANGE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_int),
+                               ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
+                               ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double))
+ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(ctypes.c_double),
+                                ctypes.POINTER(ctypes.c_double), ctypes.c_int)
+
+
+class CommCallbacks(ctypes.Structure):
+    _fields_ = [("ctx", _vp), ("exchange", EXCHANGE_FN), ("allgather", ALLGATHER_FN)]
+
+
 class Stats(ctypes.Structure):
     _fields_ = [("kernel_launches", ctypes.c_uint64), ("solves", ctypes.c_uint64), ("iterations", ctypes.c_uint64),
                 ("timing_enabled", _ci), ("phase_ms", _cd * 4), ("phase_count", ctypes.c_uint64 * 4),
@@ -98,12 +109,13 @@ def lib():
         L.spuma_set_batch.argtypes = [_vp, _ci]
         L.spuma_set_option.argtypes = [_vp, _ci, _ci]
         L.spuma_nccl_get_unique_id.argtypes = [_vp]
+        L.spuma_set_comm_callbacks.argtypes = [_vp, ctypes.POINTER(CommCallbacks)]
         L.spuma_last_error.restype = ctypes.c_char_p
         L.spuma_abi_version.restype = _ci
         for name in ("spuma_mesh_create", "spuma_assemble_laplacian", "spuma_pcg_solve", "spuma_amul",
                      "spuma_mesh_get_addressing", "spuma_mesh_get_geometry", "spuma_get_stats",
                      "spuma_reset_stats", "spuma_set_timing", "spuma_set_batch", "spuma_nccl_get_unique_id",
-                     "spuma_set_option"):
+                     "spuma_set_option", "spuma_set_comm_callbacks"):
             getattr(L, name).restype = _ci
         if L.spuma_abi_version() != ABI_VERSION:
             raise SpumaError(1, "libspuma ABI version mismatch")
@@ -194,7 +206,9 @@ class Mesh:
                         stream, rank, n_ranks, ctypes.cast(idbuf, _vp) if idbuf is not None else None)
         h = _vp()
         _check(lib().spuma_mesh_create(ctypes.byref(desc), ctypes.byref(h)))
-        return cls(h.value, int(n_cells), n_faces, n_iface, n_b, None)
+        obj = cls(h.value, int(n_cells), n_faces, n_iface, n_b, None)
+        obj.rank, obj.n_ranks = int(rank), int(n_ranks)
+        return obj
 
     @classmethod
     def from_mesh(cls, mesh, **kw) -> "Mesh":
@@ -286,6 +300,40 @@ class Mesh:
 
     def set_batch(self, iterations: int):
         _check(lib().spuma_set_batch(self._h, int(iterations)))
+
+    def set_comm_callbacks(self, exchange, allgather):
+        """spuma_set_comm_callbacks (external-comm mode: n_ranks > 1 without an NCCL id).
+
+        exchange(peers, offsets, counts, send, recv) and allgather(send, recv) receive numpy views
+        of the library's host buffers and must fill recv; they run inside the spuma_* call."""
+        def _ex(ctx, n, peers, offs, counts, send, recv):
+            try:
+                pe = [peers[i] for i in range(n)]
+                of = [offs[i] for i in range(n)]
+                co = [counts[i] for i in range(n)]
+                tot = max([o + c for o, c in zip(of, co)] + [0])
+                sv = np.ctypeslib.as_array(send, shape=(max(tot, 1),))
+                rv = np.ctypeslib.as_array(recv, shape=(max(tot, 1),))
+                exchange(pe, of, co, sv, rv)
+                return 0
+            except Exception:  # pragma: no cover - reported as SPUMA_ERR_NCCL
+                import traceback
+                traceback.print_exc()
+                return 1
+
+        def _ag(ctx, send, recv, n):
+            try:
+                allgather(np.ctypeslib.as_array(send, shape=(n,)),
+                          np.ctypeslib.as_array(recv, shape=(n * self.n_ranks,)))
+                return 0
+            except Exception:  # pragma: no cover
+                import traceback
+                traceback.print_exc()
+                return 1
+
+        cb = CommCallbacks(None, EXCHANGE_FN(_ex), ALLGATHER_FN(_ag))
+        self._cb = cb  # keep the trampolines alive with the handle
+        _check(lib().spuma_set_comm_callbacks(self._h, ctypes.byref(cb)))
 
     def set_option(self, option: int, value: int):
         """spuma_set_option (OPT_AMUL_VARIANT: 0 per-row, 1 tile, 2 unrolled, 3 TMA pipeline)."""

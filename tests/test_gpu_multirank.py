@@ -1,0 +1,138 @@
+"""Multi-rank path of libspuma on ONE GPU: P processes share cuda:0, each with its own
+sub-mesh handle (n_ranks = P), communicating through the external-comm callbacks over
+torch.distributed gloo (NCCL cannot put two ranks on one device).  Everything on the
+device is the multi-rank code the NCCL build runs: gamma halo + processor coefficients
+in global orientation (Q9), per-cell interface masks in the Amul, rank partials
+finalised from the rank-ordered all-gather.
+
+Checked against the decomposed oracle (O8, same sub-meshes): coefficients and
+interface coefficients bitwise, PCG iterations +-2 and solution 1e-9 at matched counts
+(Q11); and against the undecomposed oracle (P8)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+import torch.distributed as dist  # noqa: E402
+import torch.multiprocessing as mp  # noqa: E402
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _callbacks(rank):
+    def exchange(peers, offsets, counts, send, recv):
+        reqs = []
+        for p, o, c in zip(peers, offsets, counts):
+            reqs.append(dist.isend(torch.from_numpy(np.array(send[o:o + c])), p))
+        bufs = []
+        for p, o, c in zip(peers, offsets, counts):
+            b = torch.empty(c, dtype=torch.float64)
+            reqs.append(dist.irecv(b, p))
+            bufs.append((o, c, b))
+        for r in reqs:
+            r.wait()
+        for o, c, b in bufs:
+            recv[o:o + c] = b.numpy()
+
+    def allgather(send, recv):
+        out = [torch.empty(send.shape[0], dtype=torch.float64) for _ in range(dist.get_world_size())]
+        dist.all_gather(out, torch.from_numpy(np.array(send)))
+        recv[:] = torch.cat(out).numpy()
+
+    return exchange, allgather
+
+
+def _case(P, how):
+    import gen
+    m = gen.permute(gen.perturbed(10, 0.2), seed=6)
+    gamma, b = gen.gamma_lognormal(m), gen.rhs(m)
+    part = gen.rcb_parts(m, P) if how == "rcb" else gen.block_parts(m, (P, 1, 1))
+    return m, gamma, b, part
+
+
+def _worker(rank, P, how, port, q):
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=P)
+        import gen
+        import oracle as O
+        import paper_2512_22215_b200 as S
+        torch.cuda.set_device(0)
+        m, gamma, b, part = _case(P, how)
+        subs = gen.decompose(m, part, P)
+        gs, bs = gen.split_cell_field(gamma, part, P), gen.split_cell_field(b, part, P)
+        halo = O.gamma_halo(subs, gs)
+        ref_local = [int(np.nonzero(sm.gid == 0)[0][0]) if (sm.gid == 0).any() else -1 for sm in subs]
+        systems = [O.assemble(sm, gs[r], ref_local[r], 0.0, source=bs[r], gamma_remote=halo[r])
+                   for r, sm in enumerate(subs)]
+        me = subs[rank]
+        h = S.Mesh.from_mesh(me, rank=rank, n_ranks=P)
+        h.set_comm_callbacks(*_callbacks(rank))
+        f64 = dict(dtype=torch.float64, device="cuda")
+        diag, upper = torch.empty(me.n_cells, **f64), torch.empty(me.n_faces, **f64)
+        src = torch.as_tensor(bs[rank], **f64)
+        iface = torch.empty(max(h.n_iface, 1), **f64)
+        h.assemble_laplacian(torch.as_tensor(gs[rank], **f64), None, ref_local[rank], 0.0, diag, upper, src, iface)
+        s = systems[rank]
+        assert np.array_equal(upper.cpu().numpy(), s.upper)
+        assert np.array_equal(diag.cpu().numpy(), s.diag)
+        assert np.array_equal(src.cpu().numpy(), s.source)
+        oi = np.concatenate(s.iface) if s.iface else np.zeros(0)
+        assert np.array_equal(iface.cpu().numpy()[:oi.shape[0]], oi)
+        # Amul with the halo
+        x = np.cos(np.arange(m.n_cells) * 0.37)
+        xs = gen.split_cell_field(x, part, P)
+        y = torch.empty(me.n_cells, **f64)
+        h.amul(diag, upper, iface, torch.as_tensor(xs[rank], **f64), y)
+        xh = O.gamma_halo(subs, xs)[rank]
+        assert np.array_equal(y.cpu().numpy(), O.amul(me, s.diag, s.upper, xs[rank], iface=s.iface, x_remote=xh))
+        # PCG vs the decomposed oracle (Q11) and every rank agrees on perf
+        psi = torch.zeros(me.n_cells, **f64)
+        perf = h.pcg_solve(diag, upper, iface, src, psi, 1e-9, 0.0, 3000, 0)
+        psis_o, po = O.pcg_decomposed(subs, systems, None, O.controls(1e-9, 0.0, 3000, 0))
+        assert abs(perf["n_iterations"] - po["n_iterations"]) <= 2, (perf, po)
+        n = min(perf["n_iterations"], po["n_iterations"])
+        psi.zero_()
+        perf_n = h.pcg_solve(diag, upper, iface, src, psi, 0.0, 0.0, n, n)
+        psis_o, _ = O.pcg_decomposed(subs, systems, None, O.controls(0.0, 0.0, n, n))
+        loc = psi.cpu().numpy()
+        num = np.array([np.sum((loc - psis_o[rank]) ** 2), np.sum(psis_o[rank] ** 2)])
+        tot = [torch.empty(2, dtype=torch.float64) for _ in range(P)]
+        dist.all_gather(tot, torch.from_numpy(num))
+        err = np.sqrt(sum(t[0].item() for t in tot) / sum(t[1].item() for t in tot))
+        assert err <= 1e-9, err
+        allp = [None] * P
+        dist.all_gather_object(allp, perf)
+        assert all(p == allp[0] for p in allp)  # identical decisions on every rank
+        h.free()
+        q.put((rank, "ok"))
+    except BaseException:
+        import traceback
+        q.put((rank, traceback.format_exc()))
+    finally:
+        if dist.is_initialized():
+            dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("P,how", [(2, "block"), (3, "rcb"), (4, "rcb")])
+def test_multirank_on_one_gpu_matches_decomposed_oracle(P, how):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    ps = [ctx.Process(target=_worker, args=(r, P, how, port, q)) for r in range(P)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=600) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+    bad = {r: m for r, m in res.items() if m != "ok"}
+    assert not bad, bad
