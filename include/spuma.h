@@ -230,7 +230,12 @@ spuma_status spuma_set_batch(spuma_mesh m, int iterations);
  * side (one / two rows per thread), 8/9 ELL with a per-solve owner-slot ordered
  * coefficient copy (no row extents streamed; one / two rows per thread).
  * Errors: INVALID_ARGUMENT. */
-typedef enum { SPUMA_OPT_AMUL_VARIANT = 0 } spuma_option;
+typedef enum {
+    SPUMA_OPT_AMUL_VARIANT = 0,
+    /* meshes with at most this many cells (single rank) are solved by one single-CTA
+     * kernel launch (latency path, BASELINE config 1); default 8192; 0 disables */
+    SPUMA_OPT_SMALL_SOLVE_MAX_CELLS = 1
+} spuma_option;
 spuma_status spuma_set_option(spuma_mesh m, int option, int value);
 
 /* External communication, used when n_ranks > 1 and desc.nccl_unique_id == NULL

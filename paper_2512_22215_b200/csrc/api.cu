@@ -792,6 +792,27 @@ spuma_status spuma_pcg_solve(spuma_mesh m, const spuma_scalar* diag, const spuma
     SPUMA_CUDA(cudaMemcpyAsync(m->ws.ptrs, m->h_ptrs, sizeof(DevPtrs), cudaMemcpyHostToDevice, s));
     launch_scal_init(s, m->ws, *ctl, m->n_ranks);
 
+    // ---- small meshes: the whole solve in one single-CTA launch (latency path)
+    if (m->n_ranks == 1 && m->N <= m->small_max_cells && !m->timing) {
+        launch_pcg_single(s, mesh_args(m), m->ws);
+        m->stats.kernel_launches += 2;
+        DevScal fs;
+        SPUMA_CUDA(cudaMemcpyAsync(m->h_scal, m->ws.scal, sizeof(DevScal), cudaMemcpyDeviceToHost, s));
+        SPUMA_CUDA(cudaStreamSynchronize(s));
+        fs = m->h_scal[0];
+        SPUMA_CUDA(cudaGetLastError());
+        perf->initial_residual = fs.init;
+        perf->final_residual = fs.fin;
+        perf->n_iterations = fs.n;
+        perf->converged = fs.converged;
+        perf->singular = fs.singular;
+        m->stats.solves += 1;
+        m->stats.iterations += fs.n;
+        SPUMA_TRY(cells_out(m, psi, P.psi));
+        SPUMA_CUDA(cudaStreamSynchronize(s));
+        return SPUMA_OK;
+    }
+
     // ---- A6 setup
     const MeshArgs a = mesh_args(m);
     if (amul_uses_ell(m->amul_variant) && m->d_upper_s) {
@@ -925,6 +946,10 @@ spuma_status spuma_set_option(spuma_mesh m, int option, int value)
 {
     if (!m) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "mesh is NULL");
     switch (option) {
+    case SPUMA_OPT_SMALL_SOLVE_MAX_CELLS:
+        if (value < 0) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "small-solve threshold must be >= 0");
+        m->small_max_cells = value;
+        return SPUMA_OK;
     case SPUMA_OPT_AMUL_VARIANT:
         if (value < 0 || value > 9) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "amul variant must be 0..9");
         if (value != m->amul_variant) destroy_graphs(m);

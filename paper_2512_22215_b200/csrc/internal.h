@@ -128,6 +128,7 @@ struct spuma_mesh_s {
 
     // captured iteration batches (ping-pong) and timing events
     int batch = 16;
+    int small_max_cells = 8192;  // single-CTA solve at or below this many cells (1 rank)
     int amul_variant = 8;  // ELL + coefficient copy (falls back to 6 -> 5 when the mesh is not uniform)
     bool timing = false;
     cudaGraphExec_t gexec[2] = {nullptr, nullptr};
@@ -201,5 +202,6 @@ void launch_update(cudaStream_t s, int grid, const MeshArgs& a, const Workspace&
 // P > 1: finalise from the gathered rank partials ([n_ranks][4], rank order)
 void launch_finalize(cudaStream_t s, int stage, const double* gathered, int n_ranks, const Workspace& w);
 void launch_scal_init(cudaStream_t s, const Workspace& w, const spuma_solver_controls& c, int n_ranks);
+void launch_pcg_single(cudaStream_t s, const MeshArgs& a, const Workspace& w);  // whole solve, 1 CTA
 int occupancy_grid(int N, int* grid_faces, int F);
 }  // namespace spuma

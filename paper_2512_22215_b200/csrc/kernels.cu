@@ -647,6 +647,112 @@ __global__ void __launch_bounds__(kThreads) k_update(int N, Workspace w, int fin
     }
 }
 
+// ---------------------------------------------------------------------------
+// Small meshes (BASELINE config 1, 400 cells): the whole solve (A6-A12) in ONE
+// CTA of 1024 threads -- phases separated by __syncthreads() instead of kernel
+// launches, so an iteration costs a few CTA barriers instead of 3 launches.
+// Same row order (bitwise Amul) and the same finalisation code.
+// ---------------------------------------------------------------------------
+
+constexpr int kSmallThreads = 1024;
+
+template <int NV>
+__device__ __forceinline__ void cta_sum_1024(double (&v)[NV])
+{
+    __shared__ double sh[NV][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int i = 0; i < NV; ++i)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v[i] += __shfl_down_sync(0xffffffffu, v[i], o);
+    if (lane == 0)
+#pragma unroll
+        for (int i = 0; i < NV; ++i) sh[i][warp] = v[i];
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            double t = lane < nw ? sh[i][lane] : 0.0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
+            v[i] = t;
+        }
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(kSmallThreads) k_pcg_single(MeshArgs a, Workspace w)
+{
+    const DevPtrs p = *w.ptrs;
+    DevScal* sc = w.scal;
+    const int N = a.N, t = threadIdx.x;
+    {  // A6: wA = A psi, sumA, gAverage(psi)
+        double v[2] = {0.0, 0.0};
+        for (int c = t; c < N; c += kSmallThreads) {
+            double rs;
+            w.wA[c] = amul_row(a, c, p.diag, p.upper, p.iface, p.psi, w.xr, &rs);
+            w.sumA[c] = rs;
+            v[0] += p.psi[c];
+        }
+        if (t == 0) v[1] = (double)N;
+        cta_sum_1024<2>(v);
+        if (t == 0) finalize(sc, 1, v);
+        __syncthreads();
+    }
+    {  // A6: residual, normFactor, rD, first wArA
+        const double xbar = sc->xbar;
+        double v[3] = {0.0, 0.0, 0.0};
+        for (int c = t; c < N; c += kSmallThreads) {
+            const double b = p.source[c], wa = w.wA[c];
+            const double r = b - wa;
+            const double xref = w.sumA[c] * xbar;
+            const double rd = 1.0 / p.diag[c];
+            w.rA[c] = r;
+            w.rD[c] = rd;
+            v[0] += fabs(wa - xref) + fabs(b - xref);
+            v[1] += fabs(r);
+            v[2] += (rd * r) * r;
+        }
+        cta_sum_1024<3>(v);
+        if (t == 0) finalize(sc, 2, v);
+        __syncthreads();
+    }
+    while (!sc->done) {
+        const bool first = sc->n == 0;
+        const double beta = sc->beta;
+        for (int c = t; c < N; c += kSmallThreads)  // A11
+            w.pA[c] = first ? w.rD[c] * w.rA[c] : w.rD[c] * w.rA[c] + beta * w.pA[c];
+        __syncthreads();
+        double v[2] = {0.0, 0.0};
+        for (int c = t; c < N; c += kSmallThreads) {  // A7
+            const double y = amul_row(a, c, p.diag, p.upper, p.iface, w.pA, w.xr, nullptr);
+            w.wA[c] = y;
+            v[0] += y * w.pA[c];
+        }
+        cta_sum_1024<1>(reinterpret_cast<double(&)[1]>(v[0]));
+        if (t == 0) finalize(sc, 3, v);  // A8
+        __syncthreads();
+        if (sc->done) break;
+        const double alpha = sc->alpha;
+        v[0] = v[1] = 0.0;
+        for (int c = t; c < N; c += kSmallThreads) {  // A9
+            p.psi[c] = p.psi[c] + alpha * w.pA[c];
+            const double r = w.rA[c] - alpha * w.wA[c];
+            w.rA[c] = r;
+            v[0] += (w.rD[c] * r) * r;
+            v[1] += fabs(r);
+        }
+        cta_sum_1024<2>(v);
+        if (t == 0) finalize(sc, 4, v);  // A10
+        __syncthreads();
+    }
+}
+
+void launch_pcg_single(cudaStream_t s, const MeshArgs& a, const Workspace& w)
+{
+    k_pcg_single<<<1, kSmallThreads, 0, s>>>(a, w);
+}
+
 // P > 1: global sums of the gathered rank partials in rank order, then finalise
 __global__ void k_finalize(int stage, const double* __restrict__ gathered, int n_ranks, Workspace w)
 {

@@ -306,6 +306,7 @@ def test_odd_sizes_and_batches():
     psi_n, _, _ = O.solve_case(m, g, b, 0, 0.0, O.controls(0.0, 0.0, n, n))
     for batch in (1, 3, 16):
         h = P.Mesh.from_mesh(m)
+        h.set_option(P.spuma.OPT_SMALL_SOLVE_MAX_CELLS, 0)  # graph-batched path
         h.set_batch(batch)
         psi, perf, _, _ = gpu_solve_case(m, g, b, 0, handle=h)
         assert abs(perf["n_iterations"] - n) <= 2
@@ -369,3 +370,22 @@ def test_pcg_all_amul_variants(variant):
     assert abs(p["n_iterations"] - n) <= 2
     psi, p, _, _ = gpu_solve_case(m, g, b, 0, (0.0, 0.0, n, n), handle=h)
     assert rel_l2(psi, psi_o) <= 1e-9
+
+
+@pytest.mark.parametrize("name,mesh", CASES, ids=[c[0] for c in CASES])
+def test_small_single_cta_path_and_graph_path(name, mesh):
+    """Meshes <= 8192 cells take the single-CTA solve; both paths match the oracle (Q11)."""
+    g, b = gen.gamma_lognormal(mesh), gen.rhs(mesh)
+    _, po, _ = O.solve_case(mesh, g, b, 0, 0.0, O.controls(1e-6))
+    n = po["n_iterations"]
+    psi_o, _, _ = O.solve_case(mesh, g, b, 0, 0.0, O.controls(0.0, 0.0, n, n))
+    for thr in (8192, 0):
+        h = P.Mesh.from_mesh(mesh)
+        h.set_option(P.spuma.OPT_SMALL_SOLVE_MAX_CELLS, thr)
+        _, p, _, _ = gpu_solve_case(mesh, g, b, 0, handle=h)
+        assert abs(p["n_iterations"] - n) <= 2 and p["converged"]
+        psi, p, _, _ = gpu_solve_case(mesh, g, b, 0, (0.0, 0.0, n, n), handle=h)
+        assert p["n_iterations"] == n and rel_l2(psi, psi_o) <= 1e-9
+        st = h.get_stats()
+        if thr:
+            assert st["kernel_launches"] < 20  # one solve = a handful of launches
