@@ -234,7 +234,9 @@ typedef enum {
     SPUMA_OPT_AMUL_VARIANT = 0,
     /* meshes with at most this many cells (single rank) are solved by one single-CTA
      * kernel launch (latency path, BASELINE config 1); default 8192; 0 disables */
-    SPUMA_OPT_SMALL_SOLVE_MAX_CELLS = 1
+    SPUMA_OPT_SMALL_SOLVE_MAX_CELLS = 1,
+    /* programmatic dependent launch of the hot-loop kernels (1 = on, default; process-wide) */
+    SPUMA_OPT_PDL = 2
 } spuma_option;
 spuma_status spuma_set_option(spuma_mesh m, int option, int value);
 

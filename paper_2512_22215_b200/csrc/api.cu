@@ -946,6 +946,10 @@ spuma_status spuma_set_option(spuma_mesh m, int option, int value)
 {
     if (!m) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "mesh is NULL");
     switch (option) {
+    case SPUMA_OPT_PDL:
+        if (g_use_pdl != (value != 0)) destroy_graphs(m);
+        g_use_pdl = value != 0;
+        return SPUMA_OK;
     case SPUMA_OPT_SMALL_SOLVE_MAX_CELLS:
         if (value < 0) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "small-solve threshold must be >= 0");
         m->small_max_cells = value;

@@ -204,4 +204,5 @@ void launch_finalize(cudaStream_t s, int stage, const double* gathered, int n_ra
 void launch_scal_init(cudaStream_t s, const Workspace& w, const spuma_solver_controls& c, int n_ranks);
 void launch_pcg_single(cudaStream_t s, const MeshArgs& a, const Workspace& w);  // whole solve, 1 CTA
 int occupancy_grid(int N, int* grid_faces, int F);
+extern bool g_use_pdl;  // programmatic dependent launch of the hot-loop kernels (process-wide)
 }  // namespace spuma

@@ -78,6 +78,13 @@ __device__ __forceinline__ bool grid_sum(double (&v)[NV], double* part, unsigned
     return true;
 }
 
+// Programmatic dependent launch (sm_90+): a hot-loop kernel launched with the PDL
+// attribute may start while its predecessor drains; it must wait before reading the
+// predecessor's results, and lets its own successor launch once its main loop is done.
+// Both are no-ops for a normal launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ bool conv(double r, double init, double tol, double rel_tol)
 {
     return (r < tol) || (rel_tol > 1e-20 && r < rel_tol * init);
@@ -529,6 +536,7 @@ __global__ void __launch_bounds__(kThreads) k_setup2(MeshArgs a, Workspace w, in
 // A11 pA = rD rA + beta pA  (n == 0: pA = rD rA)
 __global__ void __launch_bounds__(kThreads) k_direction(int N, Workspace w)
 {
+    pdl_wait();
     if (w.scal->done) return;
     const bool first = w.scal->n == 0;
     const double beta = w.scal->beta;
@@ -553,6 +561,7 @@ __global__ void __launch_bounds__(kThreads) k_direction(int N, Workspace w)
         const int c = N - 1;
         w.pA[c] = first ? w.rD[c] * w.rA[c] : w.rD[c] * w.rA[c] + beta * w.pA[c];
     }
+    pdl_trigger();
 }
 
 // A7 + A8: wA = A pA, partial wA.pA -> alpha
@@ -560,6 +569,7 @@ template <int V>
 __global__ void __launch_bounds__(V == 3 ? tma::kBlock : kThreads, amul_min_ctas<V>())
     k_amul_dot(MeshArgs a, Workspace w, int fin, int sell_wn, int sell_wo)
 {
+    pdl_wait();
     if (w.scal->done) return;
     const DevPtrs p = *w.ptrs;
     double v[1] = {0.0};
@@ -600,6 +610,7 @@ __global__ void __launch_bounds__(V == 3 ? tma::kBlock : kThreads, amul_min_ctas
             v[0] += y * w.pA[c];
         }
     }
+    pdl_trigger();
     if (grid_sum<1>(v, w.part, &w.scal->ticket[2]) && threadIdx.x == 0) {
         if (fin) finalize(w.scal, 3, v);
         else w.scal->rank_part[0] = v[0];
@@ -609,6 +620,7 @@ __global__ void __launch_bounds__(V == 3 ? tma::kBlock : kThreads, amul_min_ctas
 // A9 + A10: psi += alpha pA; rA -= alpha wA; partials (rD rA) rA and |rA|
 __global__ void __launch_bounds__(kThreads) k_update(int N, Workspace w, int fin)
 {
+    pdl_wait();
     if (w.scal->done) return;
     const DevPtrs p = *w.ptrs;
     const double alpha = w.scal->alpha;
@@ -641,6 +653,7 @@ __global__ void __launch_bounds__(kThreads) k_update(int N, Workspace w, int fin
         v[0] += (w.rD[c] * r) * r;
         v[1] += fabs(r);
     }
+    pdl_trigger();
     if (grid_sum<2>(v, w.part, &w.scal->ticket[3]) && threadIdx.x == 0) {
         if (fin) finalize(w.scal, 4, v);
         else w.scal->rank_part[0] = v[0], w.scal->rank_part[1] = v[1];
@@ -788,6 +801,25 @@ static int kernel_block(K kernel)
     return ((const void*)kernel == (const void*)k_amul_dot<3> || (const void*)kernel == (const void*)k_amul<3>)
                ? tma::kBlock
                : kThreads;
+}
+
+bool g_use_pdl = true;
+
+// launch with the programmatic-stream-serialization attribute when PDL is on
+template <typename... KArgs, typename... Args>
+static void launch_hot(void (*kernel)(KArgs...), int grid, int block, cudaStream_t s, Args... args)
+{
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = g_use_pdl ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, kernel, args...);
 }
 
 static int g_sms = 0;
@@ -954,7 +986,7 @@ void launch_setup2(cudaStream_t s, int grid, const MeshArgs& a, const Workspace&
 void launch_direction(cudaStream_t s, int grid, const MeshArgs& a, const Workspace& w)
 {
     (void)grid;
-    k_direction<<<grid_for(k_direction, a.N, 2), kThreads, 0, s>>>(a.N, w);
+    launch_hot(k_direction, grid_for(k_direction, a.N, 2), kThreads, s, a.N, w);
 }
 
 void launch_amul_dot(cudaStream_t s, int variant, const MeshArgs& a, const Workspace& w, bool fin, int sell_wn,
@@ -970,19 +1002,19 @@ void launch_amul_dot(cudaStream_t s, int variant, const MeshArgs& a, const Works
         k_amul_dot<3><<<grid_for(k_amul_dot<3>, (a.N + tma::kCells - 1) / tma::kCells, 1, 1), tma::kBlock, 0, s>>>(a, w, f, sell_wn, sell_wo);
         break;
     case 4: k_amul_dot<4><<<grid_for(k_amul_dot<4>, a.N), kThreads, 0, s>>>(a, w, f, sell_wn, sell_wo); break;
-    case 5: k_amul_dot<5><<<grid_for(k_amul_dot<5>, a.N, 2), kThreads, 0, s>>>(a, w, f, sell_wn, sell_wo); break;
-    case 6: k_amul_dot<6><<<grid_for(k_amul_dot<6>, a.N), kThreads, 0, s>>>(a, w, f, sell_wn, sell_wo); break;
-    case 7: k_amul_dot<7><<<grid_for(k_amul_dot<7>, a.N, 2), kThreads, 0, s>>>(a, w, f, sell_wn, sell_wo); break;
-    case 8: k_amul_dot<8><<<grid_for(k_amul_dot<8>, a.N), kThreads, 0, s>>>(a, w, f, sell_wn, sell_wo); break;
-    case 9: k_amul_dot<9><<<grid_for(k_amul_dot<9>, a.N, 2), kThreads, 0, s>>>(a, w, f, sell_wn, sell_wo); break;
-    default: k_amul_dot<0><<<grid_for(k_amul_dot<0>, a.N), kThreads, 0, s>>>(a, w, f, sell_wn, sell_wo); break;
+    case 5: launch_hot(k_amul_dot<5>, grid_for(k_amul_dot<5>, a.N, 2), kThreads, s, a, w, f, sell_wn, sell_wo); break;
+    case 6: launch_hot(k_amul_dot<6>, grid_for(k_amul_dot<6>, a.N), kThreads, s, a, w, f, sell_wn, sell_wo); break;
+    case 7: launch_hot(k_amul_dot<7>, grid_for(k_amul_dot<7>, a.N, 2), kThreads, s, a, w, f, sell_wn, sell_wo); break;
+    case 8: launch_hot(k_amul_dot<8>, grid_for(k_amul_dot<8>, a.N), kThreads, s, a, w, f, sell_wn, sell_wo); break;
+    case 9: launch_hot(k_amul_dot<9>, grid_for(k_amul_dot<9>, a.N, 2), kThreads, s, a, w, f, sell_wn, sell_wo); break;
+    default: launch_hot(k_amul_dot<0>, grid_for(k_amul_dot<0>, a.N), kThreads, s, a, w, f, sell_wn, sell_wo); break;
     }
 }
 
 void launch_update(cudaStream_t s, int grid, const MeshArgs& a, const Workspace& w, bool fin)
 {
     (void)grid;
-    k_update<<<grid_for(k_update, a.N, 2), kThreads, 0, s>>>(a.N, w, fin ? 1 : 0);
+    launch_hot(k_update, grid_for(k_update, a.N, 2), kThreads, s, a.N, w, fin ? 1 : 0);
 }
 
 void launch_finalize(cudaStream_t s, int stage, const double* gathered, int n_ranks, const Workspace& w)

@@ -30,6 +30,7 @@ ref = None
 out = {}
 for v in [int(x) for x in os.environ.get("VARIANTS", "0,5,6,7,8,9").split(",")]:
     h.set_option(P.spuma.OPT_AMUL_VARIANT, v)
+    h.set_option(P.spuma.OPT_PDL, int(os.environ.get("PDL", "1")))
     psi = torch.zeros(N, **f64)
     h.pcg_solve(diag, upper, None, src, psi, 1e-6, 0.0, 5000, 0)  # warm-up / graph capture
     h.reset_stats()
@@ -57,4 +58,5 @@ for v in [int(x) for x in os.environ.get("VARIANTS", "0,5,6,7,8,9").split(",")]:
               "amul_alg_GBps": (24 * N + 16 * F) / (ph[1] / 1e3) / 1e9,
               "cells_iter_per_s": N * perf2["n_iterations"] / t_untimed,
               "bitwise_equal_v0": bool(np.array_equal(r, ref))}
+    out[v]["pdl"] = int(os.environ.get("PDL", "1"))
     print(v, json.dumps(out[v]), flush=True)
