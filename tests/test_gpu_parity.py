@@ -389,3 +389,53 @@ def test_small_single_cta_path_and_graph_path(name, mesh):
         st = h.get_stats()
         if thr:
             assert st["kernel_launches"] < 20  # one solve = a handful of launches
+
+
+def _empty_mesh(n):
+    return gen.Mesh(n, np.zeros(0, np.int32), np.zeros(0, np.int32), np.zeros((0, 3)), np.zeros(0),
+                    np.zeros((0, 3)), np.zeros((n, 3)), np.ones(n), [])
+
+
+@pytest.mark.parametrize("small", [8192, 0])
+def test_degenerate_meshes(small):
+    # no cells: nothing to solve; reported converged with zero residual, as the oracle
+    m = _empty_mesh(0)
+    h = P.Mesh.from_mesh(m)
+    h.set_option(P.spuma.OPT_SMALL_SOLVE_MAX_CELLS, small)
+    z = torch.zeros(0, dtype=torch.float64, device="cuda")
+    perf = h.pcg_solve(z, z, None, z, z, 1e-6)
+    _, po = O.pcg(m, O.LduSystem(np.zeros(0), np.zeros(0), np.zeros(0), []), None, O.controls(1e-6))
+    assert perf["n_iterations"] == po["n_iterations"] == 0 and perf["converged"] == po["converged"] == 1
+    # one cell, no faces, reference cell: diag doubled, psi = b / (2 d)
+    m = _empty_mesh(1)
+    m = gen.Mesh(1, m.owner, m.neighbour, m.Sf, m.magSf, m.Cf, m.C, m.V,
+                 [gen.Patch("wall", gen.FIXED_VALUE, np.zeros(1, np.int32), np.array([[1.0, 0, 0]]), np.ones(1),
+                            np.array([[0.5, 0, 0]]), value=np.array([2.0]))])
+    m.C[0] = [0.0, 0.0, 0.0]
+    h = P.Mesh.from_mesh(m)
+    h.set_option(P.spuma.OPT_SMALL_SOLVE_MAX_CELLS, small)
+    diag, upper, src, _ = gpu_assemble(h, m, None, 0, 0.0, np.array([3.0]))
+    s = O.assemble(m, None, 0, 0.0, source=np.array([3.0]))
+    assert np.array_equal(diag.cpu().numpy(), s.diag) and np.array_equal(src.cpu().numpy(), s.source)
+    psi = torch.zeros(1, dtype=torch.float64, device="cuda")
+    perf = h.pcg_solve(diag, upper, None, src, psi, 1e-12)
+    assert perf["n_iterations"] == 1 and psi.item() == pytest.approx(s.source[0] / s.diag[0], rel=1e-15)
+
+
+def test_disconnected_components_renumbered():
+    """Two disconnected blocks: RCM restarts per component (Q12); both paths still bit-exact."""
+    a = gen.box(3, 2, 1, (1, 1, 1))
+    b = gen.box(2, 2, 2, (1, 1, 1))
+    n = a.n_cells + b.n_cells
+    owner = np.concatenate([a.owner, b.owner + a.n_cells]).astype(np.int32)
+    nbr = np.concatenate([a.neighbour, b.neighbour + a.n_cells]).astype(np.int32)
+    m = gen.Mesh(n, owner, nbr, np.concatenate([a.Sf, b.Sf]), np.concatenate([a.magSf, b.magSf]),
+                 np.concatenate([a.Cf, b.Cf]), np.concatenate([a.C, b.C + 5.0]), np.concatenate([a.V, b.V]), [])
+    h = P.Mesh.from_mesh(m, renumber=True)
+    ad = h.mesh_get_addressing()
+    assert np.array_equal(ad["perm"], O.rcm(n, owner, nbr))
+    rng = np.random.default_rng(0)
+    diag, upper, x = rng.uniform(-3, -1, n), rng.uniform(0.1, 1, m.n_faces), rng.standard_normal(n)
+    y = torch.empty(n, dtype=torch.float64, device="cuda")
+    h.amul(dev(diag), dev(upper), None, dev(x), y)
+    assert np.array_equal(y.cpu().numpy(), O.amul(m, diag, upper, x))
