@@ -156,7 +156,7 @@ __device__ __forceinline__ void amul_rows2(const MeshArgs& a, int c, int e, cons
 // entry = upper[ownerStart[column] + position] (L2 hit: the owner's row streamed it).
 // When every chunk has the same widths (hex meshes) the slot bases are arithmetic and
 // the per-chunk meta load drops out of the dependency chain.
-template <int R>
+template <int R, bool IF = false>
 __device__ __forceinline__ void amul_rows_sell(const MeshArgs& a, int c, int wn_u, int wo_u,
                                                const double* __restrict__ diag, const double* __restrict__ upper,
                                                const double* __restrict__ iface, const double* __restrict__ x,
@@ -233,7 +233,7 @@ __device__ __forceinline__ void amul_rows_sell(const MeshArgs& a, int c, int wn_
 #pragma unroll
         for (int j = 0; j < W; ++j)
             if (nb[r][j] >= 0) s = s + uo[r][j] * xo[r][j];
-        s = add_iface(a, cc[r], s, iface, xr);
+        if constexpr (IF) s = add_iface(a, cc[r], s, iface, xr);
         if (c + 32 * r < a.N) {
             y[cc[r]] = s;
             if (dot) acc += s * xc[r];
@@ -248,7 +248,7 @@ __device__ __forceinline__ void amul_rows_sell(const MeshArgs& a, int c, int wn_
 // coefficient at upper_s[32 wo (col >> 5) + 32 pos + (col & 31)] -- an L2 hit of the
 // owner's chunk -- so no row extent is loaded at all: two dependent levels, DRAM bytes
 // ~ 16 per face + 24 per cell (the algorithmic minimum of SURVEY §8(d)).
-template <int R>
+template <int R, bool IF = false>
 __device__ __forceinline__ void amul_rows_ell(const MeshArgs& a, int c, int wn, int wo,
                                               const double* __restrict__ diag, const double* __restrict__ upper,
                                               const double* __restrict__ upper_s, const double* __restrict__ iface,
@@ -308,7 +308,7 @@ __device__ __forceinline__ void amul_rows_ell(const MeshArgs& a, int c, int wn, 
 #pragma unroll
         for (int j = 0; j < W; ++j)
             if (nb[r][j] >= 0) s = s + uo[r][j] * xo[r][j];
-        s = add_iface(a, cc[r], s, iface, xr);
+        if constexpr (IF) s = add_iface(a, cc[r], s, iface, xr);
         if (c + 32 * r < a.N) {
             y[cc[r]] = s;
             if (dot) acc += s * xc[r];

@@ -460,13 +460,13 @@ __global__ void __launch_bounds__(V == 3 ? tma::kBlock : kThreads, amul_min_ctas
         double acc = 0.0;
         const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
         for (int t0 = (blockIdx.x * (kThreads / 32) + warp) * 32 * R; t0 < a.N; t0 += gridDim.x * kThreads * R)
-            amul_rows_sell<R>(a, t0 + lane, bd.sell_wn, bd.sell_wo, diag, upper, iface, x, xr, y, acc, false);
+            (a.ifMask ? amul_rows_sell<R, true>(a, t0 + lane, bd.sell_wn, bd.sell_wo, diag, upper, iface, x, xr, y, acc, false) : amul_rows_sell<R, false>(a, t0 + lane, bd.sell_wn, bd.sell_wo, diag, upper, iface, x, xr, y, acc, false));
     } else if constexpr (V == 8 || V == 9) {
         constexpr int R = V == 9 ? 2 : 1;
         double acc = 0.0;
         const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
         for (int t0 = (blockIdx.x * (kThreads / 32) + warp) * 32 * R; t0 < a.N; t0 += gridDim.x * kThreads * R)
-            amul_rows_ell<R>(a, t0 + lane, a.ell_wn, a.ell_wo, diag, upper, a.upper_s, iface, x, xr, y, acc, false);
+            (a.ifMask ? amul_rows_ell<R, true>(a, t0 + lane, a.ell_wn, a.ell_wo, diag, upper, a.upper_s, iface, x, xr, y, acc, false) : amul_rows_ell<R, false>(a, t0 + lane, a.ell_wn, a.ell_wo, diag, upper, a.upper_s, iface, x, xr, y, acc, false));
     } else {
         for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < a.N; c += gridDim.x * blockDim.x)
             y[c] = V == 2 ? amul_row_unrolled(a, c, diag, upper, iface, x, xr)
@@ -592,15 +592,16 @@ __global__ void __launch_bounds__(V == 3 ? tma::kBlock : kThreads, amul_min_ctas
         double acc = 0.0;
         const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
         for (int t0 = (blockIdx.x * (kThreads / 32) + warp) * 32 * R; t0 < a.N; t0 += gridDim.x * kThreads * R)
-            amul_rows_sell<R>(a, t0 + lane, sell_wn, sell_wo, p.diag, p.upper, p.iface, w.pA, w.xr, w.wA, acc, true);
+            (a.ifMask ? amul_rows_sell<R, true>(a, t0 + lane, sell_wn, sell_wo, p.diag, p.upper, p.iface, w.pA, w.xr, w.wA, acc, true) : amul_rows_sell<R, false>(a, t0 + lane, sell_wn, sell_wo, p.diag, p.upper, p.iface, w.pA, w.xr, w.wA, acc, true));
         v[0] = acc;
     } else if constexpr (V == 8 || V == 9) {
         constexpr int R = V == 9 ? 2 : 1;
         double acc = 0.0;
         const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
         for (int t0 = (blockIdx.x * (kThreads / 32) + warp) * 32 * R; t0 < a.N; t0 += gridDim.x * kThreads * R)
-            amul_rows_ell<R>(a, t0 + lane, a.ell_wn, a.ell_wo, p.diag, p.upper, a.upper_s, p.iface, w.pA, w.xr, w.wA,
-                             acc, true);
+            (a.ifMask ? amul_rows_ell<R, true>(a, t0 + lane, a.ell_wn, a.ell_wo, p.diag, p.upper, a.upper_s, p.iface, w.pA, w.xr, w.wA,
+                             acc, true) : amul_rows_ell<R, false>(a, t0 + lane, a.ell_wn, a.ell_wo, p.diag, p.upper, a.upper_s, p.iface, w.pA, w.xr, w.wA,
+                             acc, true));
         v[0] = acc;
     } else {
         for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < a.N; c += gridDim.x * blockDim.x) {

@@ -438,4 +438,8 @@ def test_disconnected_components_renumbered():
     diag, upper, x = rng.uniform(-3, -1, n), rng.uniform(0.1, 1, m.n_faces), rng.standard_normal(n)
     y = torch.empty(n, dtype=torch.float64, device="cuda")
     h.amul(dev(diag), dev(upper), None, dev(x), y)
-    assert np.array_equal(y.cpu().numpy(), O.amul(m, diag, upper, x))
+    perm = ad["perm"]
+    rm = O.renumber_mesh(m, perm)
+    fm = O.renumber_faces(perm, owner, nbr)[2]
+    ref = O.amul(rm, gen.permute_cell_field(diag, perm), upper[fm], gen.permute_cell_field(x, perm))[perm]
+    assert np.array_equal(y.cpu().numpy(), ref)
