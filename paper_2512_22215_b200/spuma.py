@@ -92,8 +92,8 @@ def lib():
     """Load libspuma.so (building it in-tree with nvcc if missing or stale)."""
     global _lib
     if _lib is None:
-        path = _build.SO
-        if _build.stale():
+        path = os.environ.get("SPUMA_LIBRARY", _build.SO)  # override: an alternative in-tree build (A/B)
+        if path == _build.SO and _build.stale():
             _build.build()
         L = ctypes.CDLL(path)
         L.spuma_mesh_create.argtypes = [ctypes.POINTER(MeshDesc), ctypes.POINTER(_vp)]

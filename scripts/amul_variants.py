@@ -30,7 +30,10 @@ ref = None
 out = {}
 for v in [int(x) for x in os.environ.get("VARIANTS", "0,5,6,7,8,9").split(",")]:
     h.set_option(P.spuma.OPT_AMUL_VARIANT, v)
-    h.set_option(P.spuma.OPT_PDL, int(os.environ.get("PDL", "1")))
+    try:
+        h.set_option(P.spuma.OPT_PDL, int(os.environ.get("PDL", "1")))
+    except P.SpumaError:  # older library without the option (A/B runs)
+        pass
     psi = torch.zeros(N, **f64)
     h.pcg_solve(diag, upper, None, src, psi, 1e-6, 0.0, 5000, 0)  # warm-up / graph capture
     h.reset_stats()
