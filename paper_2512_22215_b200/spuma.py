@@ -111,14 +111,16 @@ def lib():
         L.spuma_set_batch.argtypes = [_vp, _ci]
         L.spuma_set_option.argtypes = [_vp, _ci, _ci]
         L.spuma_nccl_get_unique_id.argtypes = [_vp]
-        L.spuma_set_comm_callbacks.argtypes = [_vp, ctypes.POINTER(CommCallbacks)]
+        if hasattr(L, "spuma_set_comm_callbacks"):  # absent only in older A/B builds
+            L.spuma_set_comm_callbacks.argtypes = [_vp, ctypes.POINTER(CommCallbacks)]
         L.spuma_last_error.restype = ctypes.c_char_p
         L.spuma_abi_version.restype = _ci
         for name in ("spuma_mesh_create", "spuma_assemble_laplacian", "spuma_pcg_solve", "spuma_amul",
                      "spuma_mesh_get_addressing", "spuma_mesh_get_geometry", "spuma_get_stats",
                      "spuma_reset_stats", "spuma_set_timing", "spuma_set_batch", "spuma_nccl_get_unique_id",
                      "spuma_set_option", "spuma_set_comm_callbacks"):
-            getattr(L, name).restype = _ci
+            if hasattr(L, name):
+                getattr(L, name).restype = _ci
         if L.spuma_abi_version() != ABI_VERSION:
             raise SpumaError(1, "libspuma ABI version mismatch")
         _lib = L
