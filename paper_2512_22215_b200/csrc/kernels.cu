@@ -18,6 +18,8 @@
 
 #include <cstdio>
 
+
+
 namespace spuma {
 
 // ---------------------------------------------------------------------------
@@ -82,8 +84,13 @@ __device__ __forceinline__ bool grid_sum(double (&v)[NV], double* part, unsigned
 // attribute may start while its predecessor drains; it must wait before reading the
 // predecessor's results, and lets its own successor launch once its main loop is done.
 // Both are no-ops for a normal launch.
+#ifndef SPUMA_NO_PDL_INSTR
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+#else
+__device__ __forceinline__ void pdl_wait() {}
+__device__ __forceinline__ void pdl_trigger() {}
+#endif
 
 __device__ __forceinline__ bool conv(double r, double init, double tol, double rel_tol)
 {
@@ -437,7 +444,7 @@ constexpr int amul_min_ctas()
     return V == 4 ? 8 : (V == 3 ? 4 : ((V == 5 || V == 7 || V == 9) ? 3 : ((V == 6 || V == 8) ? 5 : 6)));
 }
 
-template <int V>
+template <int V, bool IF = false>
 __global__ void __launch_bounds__(V == 3 ? tma::kBlock : kThreads, amul_min_ctas<V>())
     k_amul(MeshArgs a, const double* __restrict__ diag, const double* __restrict__ upper,
            const double* __restrict__ iface, const double* __restrict__ x, const double* __restrict__ xr,
@@ -460,13 +467,13 @@ __global__ void __launch_bounds__(V == 3 ? tma::kBlock : kThreads, amul_min_ctas
         double acc = 0.0;
         const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
         for (int t0 = (blockIdx.x * (kThreads / 32) + warp) * 32 * R; t0 < a.N; t0 += gridDim.x * kThreads * R)
-            (a.ifMask ? amul_rows_sell<R, true>(a, t0 + lane, bd.sell_wn, bd.sell_wo, diag, upper, iface, x, xr, y, acc, false) : amul_rows_sell<R, false>(a, t0 + lane, bd.sell_wn, bd.sell_wo, diag, upper, iface, x, xr, y, acc, false));
+            amul_rows_sell<R, IF>(a, t0 + lane, bd.sell_wn, bd.sell_wo, diag, upper, iface, x, xr, y, acc, false);
     } else if constexpr (V == 8 || V == 9) {
         constexpr int R = V == 9 ? 2 : 1;
         double acc = 0.0;
         const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
         for (int t0 = (blockIdx.x * (kThreads / 32) + warp) * 32 * R; t0 < a.N; t0 += gridDim.x * kThreads * R)
-            (a.ifMask ? amul_rows_ell<R, true>(a, t0 + lane, a.ell_wn, a.ell_wo, diag, upper, a.upper_s, iface, x, xr, y, acc, false) : amul_rows_ell<R, false>(a, t0 + lane, a.ell_wn, a.ell_wo, diag, upper, a.upper_s, iface, x, xr, y, acc, false));
+            amul_rows_ell<R, IF>(a, t0 + lane, a.ell_wn, a.ell_wo, diag, upper, a.upper_s, iface, x, xr, y, acc, false);
     } else {
         for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < a.N; c += gridDim.x * blockDim.x)
             y[c] = V == 2 ? amul_row_unrolled(a, c, diag, upper, iface, x, xr)
@@ -565,7 +572,7 @@ __global__ void __launch_bounds__(kThreads) k_direction(int N, Workspace w)
 }
 
 // A7 + A8: wA = A pA, partial wA.pA -> alpha
-template <int V>
+template <int V, bool IF = false>
 __global__ void __launch_bounds__(V == 3 ? tma::kBlock : kThreads, amul_min_ctas<V>())
     k_amul_dot(MeshArgs a, Workspace w, int fin, int sell_wn, int sell_wo)
 {
@@ -592,16 +599,15 @@ __global__ void __launch_bounds__(V == 3 ? tma::kBlock : kThreads, amul_min_ctas
         double acc = 0.0;
         const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
         for (int t0 = (blockIdx.x * (kThreads / 32) + warp) * 32 * R; t0 < a.N; t0 += gridDim.x * kThreads * R)
-            (a.ifMask ? amul_rows_sell<R, true>(a, t0 + lane, sell_wn, sell_wo, p.diag, p.upper, p.iface, w.pA, w.xr, w.wA, acc, true) : amul_rows_sell<R, false>(a, t0 + lane, sell_wn, sell_wo, p.diag, p.upper, p.iface, w.pA, w.xr, w.wA, acc, true));
+            amul_rows_sell<R, IF>(a, t0 + lane, sell_wn, sell_wo, p.diag, p.upper, p.iface, w.pA, w.xr, w.wA, acc, true);
         v[0] = acc;
     } else if constexpr (V == 8 || V == 9) {
         constexpr int R = V == 9 ? 2 : 1;
         double acc = 0.0;
         const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
         for (int t0 = (blockIdx.x * (kThreads / 32) + warp) * 32 * R; t0 < a.N; t0 += gridDim.x * kThreads * R)
-            (a.ifMask ? amul_rows_ell<R, true>(a, t0 + lane, a.ell_wn, a.ell_wo, p.diag, p.upper, a.upper_s, p.iface, w.pA, w.xr, w.wA,
-                             acc, true) : amul_rows_ell<R, false>(a, t0 + lane, a.ell_wn, a.ell_wo, p.diag, p.upper, a.upper_s, p.iface, w.pA, w.xr, w.wA,
-                             acc, true));
+            amul_rows_ell<R, IF>(a, t0 + lane, a.ell_wn, a.ell_wo, p.diag, p.upper, a.upper_s, p.iface, w.pA, w.xr, w.wA,
+                             acc, true);
         v[0] = acc;
     } else {
         for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < a.N; c += gridDim.x * blockDim.x) {
@@ -867,6 +873,10 @@ int occupancy_grid(int N, int* grid_faces, int F)
     g = std::max(g, grid_for(k_amul_dot<7>, N, 2));
     g = std::max(g, grid_for(k_amul_dot<8>, N));
     g = std::max(g, grid_for(k_amul_dot<9>, N, 2));
+    g = std::max(g, grid_for(k_amul_dot<6, true>, N));
+    g = std::max(g, grid_for(k_amul_dot<7, true>, N, 2));
+    g = std::max(g, grid_for(k_amul_dot<8, true>, N));
+    g = std::max(g, grid_for(k_amul_dot<9, true>, N, 2));
     g = std::max(g, grid_for(k_update, N, 2));
     if (grid_faces) *grid_faces = grid_for(k_face_coeffs, F);
     return g;
@@ -929,10 +939,22 @@ void launch_amul(cudaStream_t s, int variant, const MeshArgs& a, const double* d
         break;
     case 4: k_amul<4><<<grid_for(k_amul<4>, a.N), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd); break;
     case 5: k_amul<5><<<grid_for(k_amul<5>, a.N, 2), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd); break;
-    case 6: k_amul<6><<<grid_for(k_amul<6>, a.N), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd); break;
-    case 7: k_amul<7><<<grid_for(k_amul<7>, a.N, 2), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd); break;
-    case 8: k_amul<8><<<grid_for(k_amul<8>, a.N), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd); break;
-    case 9: k_amul<9><<<grid_for(k_amul<9>, a.N, 2), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd); break;
+    case 6:
+        if (a.ifMask) k_amul<6, true><<<grid_for(k_amul<6, true>, a.N), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd);
+        else k_amul<6><<<grid_for(k_amul<6>, a.N), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd);
+        break;
+    case 7:
+        if (a.ifMask) k_amul<7, true><<<grid_for(k_amul<7, true>, a.N, 2), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd);
+        else k_amul<7><<<grid_for(k_amul<7>, a.N, 2), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd);
+        break;
+    case 8:
+        if (a.ifMask) k_amul<8, true><<<grid_for(k_amul<8, true>, a.N), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd);
+        else k_amul<8><<<grid_for(k_amul<8>, a.N), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd);
+        break;
+    case 9:
+        if (a.ifMask) k_amul<9, true><<<grid_for(k_amul<9, true>, a.N, 2), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd);
+        else k_amul<9><<<grid_for(k_amul<9>, a.N, 2), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd);
+        break;
     default: k_amul<0><<<grid_for(k_amul<0>, a.N), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd); break;
     }
 }
@@ -1004,10 +1026,22 @@ void launch_amul_dot(cudaStream_t s, int variant, const MeshArgs& a, const Works
         break;
     case 4: k_amul_dot<4><<<grid_for(k_amul_dot<4>, a.N), kThreads, 0, s>>>(a, w, f, sell_wn, sell_wo); break;
     case 5: launch_hot(k_amul_dot<5>, grid_for(k_amul_dot<5>, a.N, 2), kThreads, s, a, w, f, sell_wn, sell_wo); break;
-    case 6: launch_hot(k_amul_dot<6>, grid_for(k_amul_dot<6>, a.N), kThreads, s, a, w, f, sell_wn, sell_wo); break;
-    case 7: launch_hot(k_amul_dot<7>, grid_for(k_amul_dot<7>, a.N, 2), kThreads, s, a, w, f, sell_wn, sell_wo); break;
-    case 8: launch_hot(k_amul_dot<8>, grid_for(k_amul_dot<8>, a.N), kThreads, s, a, w, f, sell_wn, sell_wo); break;
-    case 9: launch_hot(k_amul_dot<9>, grid_for(k_amul_dot<9>, a.N, 2), kThreads, s, a, w, f, sell_wn, sell_wo); break;
+    case 6:
+        if (a.ifMask) launch_hot(k_amul_dot<6, true>, grid_for(k_amul_dot<6, true>, a.N), kThreads, s, a, w, f, sell_wn, sell_wo);
+        else launch_hot(k_amul_dot<6>, grid_for(k_amul_dot<6>, a.N), kThreads, s, a, w, f, sell_wn, sell_wo);
+        break;
+    case 7:
+        if (a.ifMask) launch_hot(k_amul_dot<7, true>, grid_for(k_amul_dot<7, true>, a.N, 2), kThreads, s, a, w, f, sell_wn, sell_wo);
+        else launch_hot(k_amul_dot<7>, grid_for(k_amul_dot<7>, a.N, 2), kThreads, s, a, w, f, sell_wn, sell_wo);
+        break;
+    case 8:
+        if (a.ifMask) launch_hot(k_amul_dot<8, true>, grid_for(k_amul_dot<8, true>, a.N), kThreads, s, a, w, f, sell_wn, sell_wo);
+        else launch_hot(k_amul_dot<8>, grid_for(k_amul_dot<8>, a.N), kThreads, s, a, w, f, sell_wn, sell_wo);
+        break;
+    case 9:
+        if (a.ifMask) launch_hot(k_amul_dot<9, true>, grid_for(k_amul_dot<9, true>, a.N, 2), kThreads, s, a, w, f, sell_wn, sell_wo);
+        else launch_hot(k_amul_dot<9>, grid_for(k_amul_dot<9>, a.N, 2), kThreads, s, a, w, f, sell_wn, sell_wo);
+        break;
     default: launch_hot(k_amul_dot<0>, grid_for(k_amul_dot<0>, a.N), kThreads, s, a, w, f, sell_wn, sell_wo); break;
     }
 }
