@@ -38,6 +38,11 @@ __device__ __forceinline__ double add_iface(const MeshArgs& a, int c, double s, 
     return s;
 }
 
+__device__ __forceinline__ bool is_iface_row(const MeshArgs& a, int c)
+{
+    return a.ifMask && ((__ldg(a.ifMask + (c >> 5)) >> (c & 31)) & 1u);
+}
+
 // ---------------------------------------------------------------------------- variant 2
 __device__ __forceinline__ double amul_row_unrolled(const MeshArgs& a, int c, const double* __restrict__ diag,
                                                     const double* __restrict__ upper,
@@ -156,7 +161,10 @@ __device__ __forceinline__ void amul_rows2(const MeshArgs& a, int c, int e, cons
 // entry = upper[ownerStart[column] + position] (L2 hit: the owner's row streamed it).
 // When every chunk has the same widths (hex meshes) the slot bases are arithmetic and
 // the per-chunk meta load drops out of the dependency chain.
-template <int R, bool IF = false>
+// IFM (interface mode): 0 no processor faces, 1 add the interface terms inline,
+// 2 deferred -- interface rows keep only their internal-face sum (finished later by
+// k_iface_rows once the halo has arrived) and are left out of this kernel's dot.
+template <int R, int IFM = 0>
 __device__ __forceinline__ void amul_rows_sell(const MeshArgs& a, int c, int wn_u, int wo_u,
                                                const double* __restrict__ diag, const double* __restrict__ upper,
                                                const double* __restrict__ iface, const double* __restrict__ x,
@@ -190,9 +198,9 @@ __device__ __forceinline__ void amul_rows_sell(const MeshArgs& a, int c, int wn_
 #pragma unroll
         for (int r = 0; r < R; ++r)
             if (c + 32 * r < a.N) {
-                const double v = amul_row(a, cc[r], diag, upper, iface, x, xr, nullptr);
+                const double v = amul_row(a, cc[r], diag, upper, iface, x, xr, nullptr, IFM != 2);
                 y[cc[r]] = v;
-                if (dot) acc += v * xc[r];
+                if (dot && (IFM != 2 || !is_iface_row(a, cc[r]))) acc += v * xc[r];
             }
         return;
     }
@@ -233,10 +241,10 @@ __device__ __forceinline__ void amul_rows_sell(const MeshArgs& a, int c, int wn_
 #pragma unroll
         for (int j = 0; j < W; ++j)
             if (nb[r][j] >= 0) s = s + uo[r][j] * xo[r][j];
-        if constexpr (IF) s = add_iface(a, cc[r], s, iface, xr);
+        if constexpr (IFM == 1) s = add_iface(a, cc[r], s, iface, xr);
         if (c + 32 * r < a.N) {
             y[cc[r]] = s;
-            if (dot) acc += s * xc[r];
+            if (dot && (IFM != 2 || !is_iface_row(a, cc[r]))) acc += s * xc[r];
         }
     }
 }
@@ -248,7 +256,7 @@ __device__ __forceinline__ void amul_rows_sell(const MeshArgs& a, int c, int wn_
 // coefficient at upper_s[32 wo (col >> 5) + 32 pos + (col & 31)] -- an L2 hit of the
 // owner's chunk -- so no row extent is loaded at all: two dependent levels, DRAM bytes
 // ~ 16 per face + 24 per cell (the algorithmic minimum of SURVEY §8(d)).
-template <int R, bool IF = false>
+template <int R, int IFM = 0>
 __device__ __forceinline__ void amul_rows_ell(const MeshArgs& a, int c, int wn, int wo,
                                               const double* __restrict__ diag, const double* __restrict__ upper,
                                               const double* __restrict__ upper_s, const double* __restrict__ iface,
@@ -262,9 +270,9 @@ __device__ __forceinline__ void amul_rows_ell(const MeshArgs& a, int c, int wn, 
         for (int r = 0; r < R; ++r) {
             const int cr = c + 32 * r;
             if (cr < a.N) {
-                const double v = amul_row(a, cr, diag, upper, iface, x, xr, nullptr);
+                const double v = amul_row(a, cr, diag, upper, iface, x, xr, nullptr, IFM != 2);
                 y[cr] = v;
-                if (dot) acc += v * x[cr];
+                if (dot && (IFM != 2 || !is_iface_row(a, cr))) acc += v * x[cr];
             }
         }
         return;
@@ -308,10 +316,10 @@ __device__ __forceinline__ void amul_rows_ell(const MeshArgs& a, int c, int wn, 
 #pragma unroll
         for (int j = 0; j < W; ++j)
             if (nb[r][j] >= 0) s = s + uo[r][j] * xo[r][j];
-        if constexpr (IF) s = add_iface(a, cc[r], s, iface, xr);
+        if constexpr (IFM == 1) s = add_iface(a, cc[r], s, iface, xr);
         if (c + 32 * r < a.N) {
             y[cc[r]] = s;
-            if (dot) acc += s * xc[r];
+            if (dot && (IFM != 2 || !is_iface_row(a, cc[r]))) acc += s * xc[r];
         }
     }
 }

@@ -247,18 +247,39 @@ void record(spuma_mesh m, std::vector<cudaEvent_t>& ev, int idx, cudaStream_t s)
     cudaEventRecordWithFlags(ev[idx], s, cudaEventRecordExternal);
 }
 
-// one PCG iteration (A11, A7h, A7-A8, A9-A10) on stream s
+// one PCG iteration (A11, A7h, A7-A8, A9-A10) on stream s.  P > 1 with processor faces
+// and an ELL/SELL Amul: the halo (pack + NCCL send/recv on the comm stream) overlaps
+// the Amul of every row, whose interface rows are finished by k_iface_rows once the
+// halo has arrived (SURVEY §8(e) "overlapped with the interior Amul").
 spuma_status enqueue_iteration(spuma_mesh m, cudaStream_t s, std::vector<cudaEvent_t>* ev, int slot)
 {
     const MeshArgs a = mesh_args(m);
     const bool fin = m->n_ranks == 1;
+    const int rv = resolve_amul_variant(m->amul_variant, a);
+    const bool overlap = !fin && m->n_iface > 0 && rv >= 6 && rv <= 9;
     if (ev) record(m, *ev, slot * 6 + 0, s);
     launch_direction(s, m->grid, a, m->ws);
     if (ev) record(m, *ev, slot * 6 + 1, s);
-    SPUMA_TRY(halo_exchange(m, m->ws.pA, m->ws.xr, s));
-    if (ev) record(m, *ev, slot * 6 + 2, s);
-    launch_amul_dot(s, m->amul_variant, a, m->ws, fin, m->sell_wn, m->sell_wo);
-    if (ev) record(m, *ev, slot * 6 + 3, s);
+    if (overlap) {
+        if (!m->external_comm) {
+            SPUMA_CUDA(cudaEventRecord(m->ev_fork, s));
+            SPUMA_CUDA(cudaStreamWaitEvent(m->comm_stream, m->ev_fork, 0));
+            SPUMA_TRY(halo_exchange(m, m->ws.pA, m->ws.xr, m->comm_stream));
+            SPUMA_CUDA(cudaEventRecord(m->ev_join, m->comm_stream));
+        }
+        if (ev) record(m, *ev, slot * 6 + 2, s);
+        launch_amul_dot(s, m->amul_variant, a, m->ws, fin, m->sell_wn, m->sell_wo, true);
+        if (ev) record(m, *ev, slot * 6 + 3, s);
+        if (m->external_comm) SPUMA_TRY(halo_exchange(m, m->ws.pA, m->ws.xr, s));
+        else SPUMA_CUDA(cudaStreamWaitEvent(s, m->ev_join, 0));
+        launch_iface_rows(s, a, m->ws, m->d_ifRows, m->n_ifRows);
+        m->stats.kernel_launches += 1;
+    } else {
+        SPUMA_TRY(halo_exchange(m, m->ws.pA, m->ws.xr, s));
+        if (ev) record(m, *ev, slot * 6 + 2, s);
+        launch_amul_dot(s, m->amul_variant, a, m->ws, fin, m->sell_wn, m->sell_wo);
+        if (ev) record(m, *ev, slot * 6 + 3, s);
+    }
     if (!fin) SPUMA_TRY(reduce_finalize(m, 3, s));
     if (ev) record(m, *ev, slot * 6 + 4, s);
     launch_update(s, m->grid, a, m->ws, fin);
@@ -367,7 +388,7 @@ void spuma_free(spuma_mesh m)
                      m->d_owner, m->d_neighbour, m->d_ownerStart, m->d_losortStart, m->d_losort, m->d_ownerLo,
                      m->d_perm, m->d_face_map, m->d_delta, m->d_weights, m->d_magSf, m->d_bkind, m->d_bcell,
                      m->d_bproc, m->d_bmagSf, m->d_bdelta, m->d_bweight, m->d_bvalue, m->d_bgamma_r,
-                     m->d_bis_owner, m->d_bStart, m->d_bFace, m->d_ifStart, m->d_ifIdx, m->d_if_cell, m->d_ifMask,
+                     m->d_bis_owner, m->d_bStart, m->d_bFace, m->d_ifStart, m->d_ifIdx, m->d_if_cell, m->d_ifMask, m->d_ifRows,
                      m->d_sendbuf, m->d_cell_a, m->d_cell_b, m->d_cell_c, m->d_cell_d, m->d_cell_e, m->d_cell_t,
                      m->d_face_a, m->d_face_t, m->d_iface_a, m->ws.wA, m->ws.rA, m->ws.pA, m->ws.rD, m->ws.sumA,
                      m->ws.xr, m->ws.part, m->ws.scal, m->ws.ptrs};
@@ -380,6 +401,8 @@ void spuma_free(spuma_mesh m)
     if (m->h_scal) cudaFreeHost(m->h_scal);
     if (m->comm) ncclCommDestroy(m->comm);
     if (m->comm_stream) cudaStreamDestroy(m->comm_stream);
+    if (m->ev_fork) cudaEventDestroy(m->ev_fork);
+    if (m->ev_join) cudaEventDestroy(m->ev_join);
     if (m->own_stream && m->stream) cudaStreamDestroy(m->stream);
     delete m;
 }
@@ -566,6 +589,11 @@ static spuma_status mesh_create_impl(const spuma_mesh_desc* d, spuma_mesh m)
         std::vector<unsigned> mask((N + 31) / 32 + 1, 0u);
         for (int c : if_cell) mask[c >> 5] |= 1u << (c & 31);
         SPUMA_TRY(upload(&m->d_ifMask, mask, s));
+        std::vector<int> rows;
+        for (int c = 0; c < N; ++c)
+            if ((mask[c >> 5] >> (c & 31)) & 1u) rows.push_back(c);
+        m->n_ifRows = (int)rows.size();
+        SPUMA_TRY(upload(&m->d_ifRows, rows, s));
     }
     SPUMA_TRY(dalloc(&m->d_bdelta, m->Fb));
     SPUMA_TRY(dalloc(&m->d_bweight, m->Fb));
@@ -626,6 +654,9 @@ static spuma_status mesh_create_impl(const spuma_mesh_desc* d, spuma_mesh m)
                 m->cb_offsets.push_back(P.iface_offset);
                 m->cb_counts.push_back(P.n_faces);
             }
+        SPUMA_CUDA(cudaStreamCreateWithFlags(&m->comm_stream, cudaStreamNonBlocking));
+        SPUMA_CUDA(cudaEventCreateWithFlags(&m->ev_fork, cudaEventDisableTiming));
+        SPUMA_CUDA(cudaEventCreateWithFlags(&m->ev_join, cudaEventDisableTiming));
         if (!d->nccl_unique_id) {
             m->external_comm = true;
             SPUMA_CUDA(cudaMallocHost(reinterpret_cast<void**>(&m->h_send), sizeof(double) * (m->n_iface + 1)));

@@ -114,6 +114,9 @@ struct spuma_mesh_s {
     // device: interfaces
     int *d_ifStart = nullptr, *d_ifIdx = nullptr, *d_if_cell = nullptr;  // if_cell: [n_iface] local cell
     unsigned* d_ifMask = nullptr;
+    int* d_ifRows = nullptr;          // cells with processor faces, ascending
+    int n_ifRows = 0;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;  // halo / interior overlap
     double* d_sendbuf = nullptr;     // [n_iface] packed x for the neighbours
     // staging (renumbering / host pointers), allocated on first use
     double *d_cell_a = nullptr, *d_cell_b = nullptr, *d_cell_c = nullptr, *d_cell_d = nullptr,
@@ -196,7 +199,9 @@ void launch_setup1(cudaStream_t s, int grid, const MeshArgs& a, const Workspace&
 void launch_setup2(cudaStream_t s, int grid, const MeshArgs& a, const Workspace& w, bool fin);
 void launch_direction(cudaStream_t s, int grid, const MeshArgs& a, const Workspace& w);
 void launch_amul_dot(cudaStream_t s, int variant, const MeshArgs& a, const Workspace& w, bool fin, int sell_wn,
-                     int sell_wo);
+                     int sell_wo, bool deferred = false);
+int resolve_amul_variant(int variant, const MeshArgs& a);  // variant actually run on this mesh
+void launch_iface_rows(cudaStream_t s, const MeshArgs& a, const Workspace& w, const int* rows, int n_rows);
 constexpr int kPad = 8;  // padding elements on internal arrays (16-byte TMA windows may overrun by <= 3)
 void launch_update(cudaStream_t s, int grid, const MeshArgs& a, const Workspace& w, bool fin);
 // P > 1: finalise from the gathered rank partials ([n_ranks][4], rank order)

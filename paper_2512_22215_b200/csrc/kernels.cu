@@ -144,7 +144,7 @@ __device__ void finalize(DevScal* s, int stage, const double* g)
 __device__ __forceinline__ double amul_row(const MeshArgs& a, int c, const double* __restrict__ diag,
                                            const double* __restrict__ upper, const double* __restrict__ iface,
                                            const double* __restrict__ x, const double* __restrict__ xr,
-                                           double* rowsum)
+                                           double* rowsum, bool iface_terms = true)
 {
     double s = diag[c] * x[c];
     double r = diag[c];
@@ -160,7 +160,7 @@ __device__ __forceinline__ double amul_row(const MeshArgs& a, int c, const doubl
         s = s + u * x[a.neighbour[f]];
         r = r + u;
     }
-    if (a.ifStart) {
+    if (a.ifStart && iface_terms) {
         const int j1 = a.ifStart[c + 1];
         for (int j = a.ifStart[c]; j < j1; ++j) {
             const int i = a.ifIdx[j];
@@ -444,7 +444,7 @@ constexpr int amul_min_ctas()
     return V == 4 ? 8 : (V == 3 ? 4 : ((V == 5 || V == 7 || V == 9) ? 3 : ((V == 6 || V == 8) ? 5 : 6)));
 }
 
-template <int V, bool IF = false>
+template <int V, int IFM = 0>
 __global__ void __launch_bounds__(V == 3 ? tma::kBlock : kThreads, amul_min_ctas<V>())
     k_amul(MeshArgs a, const double* __restrict__ diag, const double* __restrict__ upper,
            const double* __restrict__ iface, const double* __restrict__ x, const double* __restrict__ xr,
@@ -467,13 +467,13 @@ __global__ void __launch_bounds__(V == 3 ? tma::kBlock : kThreads, amul_min_ctas
         double acc = 0.0;
         const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
         for (int t0 = (blockIdx.x * (kThreads / 32) + warp) * 32 * R; t0 < a.N; t0 += gridDim.x * kThreads * R)
-            amul_rows_sell<R, IF>(a, t0 + lane, bd.sell_wn, bd.sell_wo, diag, upper, iface, x, xr, y, acc, false);
+            amul_rows_sell<R, IFM>(a, t0 + lane, bd.sell_wn, bd.sell_wo, diag, upper, iface, x, xr, y, acc, false);
     } else if constexpr (V == 8 || V == 9) {
         constexpr int R = V == 9 ? 2 : 1;
         double acc = 0.0;
         const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
         for (int t0 = (blockIdx.x * (kThreads / 32) + warp) * 32 * R; t0 < a.N; t0 += gridDim.x * kThreads * R)
-            amul_rows_ell<R, IF>(a, t0 + lane, a.ell_wn, a.ell_wo, diag, upper, a.upper_s, iface, x, xr, y, acc, false);
+            amul_rows_ell<R, IFM>(a, t0 + lane, a.ell_wn, a.ell_wo, diag, upper, a.upper_s, iface, x, xr, y, acc, false);
     } else {
         for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < a.N; c += gridDim.x * blockDim.x)
             y[c] = V == 2 ? amul_row_unrolled(a, c, diag, upper, iface, x, xr)
@@ -572,7 +572,7 @@ __global__ void __launch_bounds__(kThreads) k_direction(int N, Workspace w)
 }
 
 // A7 + A8: wA = A pA, partial wA.pA -> alpha
-template <int V, bool IF = false>
+template <int V, int IFM = 0>
 __global__ void __launch_bounds__(V == 3 ? tma::kBlock : kThreads, amul_min_ctas<V>())
     k_amul_dot(MeshArgs a, Workspace w, int fin, int sell_wn, int sell_wo)
 {
@@ -599,14 +599,14 @@ __global__ void __launch_bounds__(V == 3 ? tma::kBlock : kThreads, amul_min_ctas
         double acc = 0.0;
         const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
         for (int t0 = (blockIdx.x * (kThreads / 32) + warp) * 32 * R; t0 < a.N; t0 += gridDim.x * kThreads * R)
-            amul_rows_sell<R, IF>(a, t0 + lane, sell_wn, sell_wo, p.diag, p.upper, p.iface, w.pA, w.xr, w.wA, acc, true);
+            amul_rows_sell<R, IFM>(a, t0 + lane, sell_wn, sell_wo, p.diag, p.upper, p.iface, w.pA, w.xr, w.wA, acc, true);
         v[0] = acc;
     } else if constexpr (V == 8 || V == 9) {
         constexpr int R = V == 9 ? 2 : 1;
         double acc = 0.0;
         const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
         for (int t0 = (blockIdx.x * (kThreads / 32) + warp) * 32 * R; t0 < a.N; t0 += gridDim.x * kThreads * R)
-            amul_rows_ell<R, IF>(a, t0 + lane, a.ell_wn, a.ell_wo, p.diag, p.upper, a.upper_s, p.iface, w.pA, w.xr, w.wA,
+            amul_rows_ell<R, IFM>(a, t0 + lane, a.ell_wn, a.ell_wo, p.diag, p.upper, a.upper_s, p.iface, w.pA, w.xr, w.wA,
                              acc, true);
         v[0] = acc;
     } else {
@@ -773,6 +773,31 @@ void launch_pcg_single(cudaStream_t s, const MeshArgs& a, const Workspace& w)
     k_pcg_single<<<1, kSmallThreads, 0, s>>>(a, w);
 }
 
+// A7 interface rows (P > 1, deferred mode): rows[] = cells with processor faces
+// (ascending).  wA[c] already holds the internal-face sum; add the interface terms
+// in (patch, face) order (bitwise the one-pass row, Q10) and the rows' share of
+// wA.pA, then complete this rank's partial: rank_part[0] = interior + interface rows.
+__global__ void __launch_bounds__(kThreads) k_iface_rows(MeshArgs a, Workspace w, const int* __restrict__ rows,
+                                                         int n_rows)
+{
+    if (w.scal->done) return;
+    const DevPtrs p = *w.ptrs;
+    double v[1] = {0.0};
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_rows; i += gridDim.x * blockDim.x) {
+        const int c = rows[i];
+        double y = w.wA[c];
+        const int j1 = a.ifStart[c + 1];
+        for (int j = a.ifStart[c]; j < j1; ++j) {
+            const int q = a.ifIdx[j];
+            y = y + p.iface[q] * w.xr[q];
+        }
+        w.wA[c] = y;
+        v[0] += y * w.pA[c];
+    }
+    if (grid_sum<1>(v, w.part, &w.scal->ticket[4]) && threadIdx.x == 0)
+        w.scal->rank_part[0] = w.scal->rank_part[0] + v[0];
+}
+
 // P > 1: global sums of the gathered rank partials in rank order, then finalise
 __global__ void k_finalize(int stage, const double* __restrict__ gathered, int n_ranks, Workspace w)
 {
@@ -873,10 +898,15 @@ int occupancy_grid(int N, int* grid_faces, int F)
     g = std::max(g, grid_for(k_amul_dot<7>, N, 2));
     g = std::max(g, grid_for(k_amul_dot<8>, N));
     g = std::max(g, grid_for(k_amul_dot<9>, N, 2));
-    g = std::max(g, grid_for(k_amul_dot<6, true>, N));
-    g = std::max(g, grid_for(k_amul_dot<7, true>, N, 2));
-    g = std::max(g, grid_for(k_amul_dot<8, true>, N));
-    g = std::max(g, grid_for(k_amul_dot<9, true>, N, 2));
+    g = std::max(g, grid_for(k_amul_dot<6, 1>, N));
+    g = std::max(g, grid_for(k_amul_dot<7, 1>, N, 2));
+    g = std::max(g, grid_for(k_amul_dot<8, 1>, N));
+    g = std::max(g, grid_for(k_amul_dot<9, 1>, N, 2));
+    g = std::max(g, grid_for(k_amul_dot<6, 2>, N));
+    g = std::max(g, grid_for(k_amul_dot<7, 2>, N, 2));
+    g = std::max(g, grid_for(k_amul_dot<8, 2>, N));
+    g = std::max(g, grid_for(k_amul_dot<9, 2>, N, 2));
+    g = std::max(g, grid_for(k_iface_rows, N));
     g = std::max(g, grid_for(k_update, N, 2));
     if (grid_faces) *grid_faces = grid_for(k_face_coeffs, F);
     return g;
@@ -940,19 +970,19 @@ void launch_amul(cudaStream_t s, int variant, const MeshArgs& a, const double* d
     case 4: k_amul<4><<<grid_for(k_amul<4>, a.N), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd); break;
     case 5: k_amul<5><<<grid_for(k_amul<5>, a.N, 2), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd); break;
     case 6:
-        if (a.ifMask) k_amul<6, true><<<grid_for(k_amul<6, true>, a.N), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd);
+        if (a.ifMask) k_amul<6, 1><<<grid_for(k_amul<6, 1>, a.N), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd);
         else k_amul<6><<<grid_for(k_amul<6>, a.N), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd);
         break;
     case 7:
-        if (a.ifMask) k_amul<7, true><<<grid_for(k_amul<7, true>, a.N, 2), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd);
+        if (a.ifMask) k_amul<7, 1><<<grid_for(k_amul<7, 1>, a.N, 2), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd);
         else k_amul<7><<<grid_for(k_amul<7>, a.N, 2), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd);
         break;
     case 8:
-        if (a.ifMask) k_amul<8, true><<<grid_for(k_amul<8, true>, a.N), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd);
+        if (a.ifMask) k_amul<8, 1><<<grid_for(k_amul<8, 1>, a.N), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd);
         else k_amul<8><<<grid_for(k_amul<8>, a.N), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd);
         break;
     case 9:
-        if (a.ifMask) k_amul<9, true><<<grid_for(k_amul<9, true>, a.N, 2), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd);
+        if (a.ifMask) k_amul<9, 1><<<grid_for(k_amul<9, 1>, a.N, 2), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd);
         else k_amul<9><<<grid_for(k_amul<9>, a.N, 2), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd);
         break;
     default: k_amul<0><<<grid_for(k_amul<0>, a.N), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd); break;
@@ -1012,12 +1042,27 @@ void launch_direction(cudaStream_t s, int grid, const MeshArgs& a, const Workspa
     launch_hot(k_direction, grid_for(k_direction, a.N, 2), kThreads, s, a.N, w);
 }
 
-void launch_amul_dot(cudaStream_t s, int variant, const MeshArgs& a, const Workspace& w, bool fin, int sell_wn,
-                     int sell_wo)
+int resolve_amul_variant(int variant, const MeshArgs& a)
 {
-    const int f = fin ? 1 : 0;
     if ((variant == 8 || variant == 9) && !a.upper_s) variant -= 2;  // no uniform-width layout: SELL
     if ((variant == 6 || variant == 7) && !a.sell_n) variant = 5;    // layout not encodable on this mesh
+    return variant;
+}
+
+void launch_amul_dot(cudaStream_t s, int variant, const MeshArgs& a, const Workspace& w, bool fin, int sell_wn,
+                     int sell_wo, bool deferred)
+{
+    const int f = fin ? 1 : 0;
+    variant = resolve_amul_variant(variant, a);
+    if (deferred && a.ifMask) {  // interface rows finished by k_iface_rows after the halo
+        switch (variant) {
+        case 6: launch_hot(k_amul_dot<6, 2>, grid_for(k_amul_dot<6, 2>, a.N), kThreads, s, a, w, f, sell_wn, sell_wo); return;
+        case 7: launch_hot(k_amul_dot<7, 2>, grid_for(k_amul_dot<7, 2>, a.N, 2), kThreads, s, a, w, f, sell_wn, sell_wo); return;
+        case 8: launch_hot(k_amul_dot<8, 2>, grid_for(k_amul_dot<8, 2>, a.N), kThreads, s, a, w, f, sell_wn, sell_wo); return;
+        case 9: launch_hot(k_amul_dot<9, 2>, grid_for(k_amul_dot<9, 2>, a.N, 2), kThreads, s, a, w, f, sell_wn, sell_wo); return;
+        default: break;  // other variants add the interface terms inline (halo must precede them)
+        }
+    }
     switch (variant) {
     case 1: k_amul_dot<1><<<grid_for(k_amul_dot<1>, a.N), kThreads, 0, s>>>(a, w, f, sell_wn, sell_wo); break;
     case 2: k_amul_dot<2><<<grid_for(k_amul_dot<2>, a.N), kThreads, 0, s>>>(a, w, f, sell_wn, sell_wo); break;
@@ -1027,19 +1072,19 @@ void launch_amul_dot(cudaStream_t s, int variant, const MeshArgs& a, const Works
     case 4: k_amul_dot<4><<<grid_for(k_amul_dot<4>, a.N), kThreads, 0, s>>>(a, w, f, sell_wn, sell_wo); break;
     case 5: launch_hot(k_amul_dot<5>, grid_for(k_amul_dot<5>, a.N, 2), kThreads, s, a, w, f, sell_wn, sell_wo); break;
     case 6:
-        if (a.ifMask) launch_hot(k_amul_dot<6, true>, grid_for(k_amul_dot<6, true>, a.N), kThreads, s, a, w, f, sell_wn, sell_wo);
+        if (a.ifMask) launch_hot(k_amul_dot<6, 1>, grid_for(k_amul_dot<6, 1>, a.N), kThreads, s, a, w, f, sell_wn, sell_wo);
         else launch_hot(k_amul_dot<6>, grid_for(k_amul_dot<6>, a.N), kThreads, s, a, w, f, sell_wn, sell_wo);
         break;
     case 7:
-        if (a.ifMask) launch_hot(k_amul_dot<7, true>, grid_for(k_amul_dot<7, true>, a.N, 2), kThreads, s, a, w, f, sell_wn, sell_wo);
+        if (a.ifMask) launch_hot(k_amul_dot<7, 1>, grid_for(k_amul_dot<7, 1>, a.N, 2), kThreads, s, a, w, f, sell_wn, sell_wo);
         else launch_hot(k_amul_dot<7>, grid_for(k_amul_dot<7>, a.N, 2), kThreads, s, a, w, f, sell_wn, sell_wo);
         break;
     case 8:
-        if (a.ifMask) launch_hot(k_amul_dot<8, true>, grid_for(k_amul_dot<8, true>, a.N), kThreads, s, a, w, f, sell_wn, sell_wo);
+        if (a.ifMask) launch_hot(k_amul_dot<8, 1>, grid_for(k_amul_dot<8, 1>, a.N), kThreads, s, a, w, f, sell_wn, sell_wo);
         else launch_hot(k_amul_dot<8>, grid_for(k_amul_dot<8>, a.N), kThreads, s, a, w, f, sell_wn, sell_wo);
         break;
     case 9:
-        if (a.ifMask) launch_hot(k_amul_dot<9, true>, grid_for(k_amul_dot<9, true>, a.N, 2), kThreads, s, a, w, f, sell_wn, sell_wo);
+        if (a.ifMask) launch_hot(k_amul_dot<9, 1>, grid_for(k_amul_dot<9, 1>, a.N, 2), kThreads, s, a, w, f, sell_wn, sell_wo);
         else launch_hot(k_amul_dot<9>, grid_for(k_amul_dot<9>, a.N, 2), kThreads, s, a, w, f, sell_wn, sell_wo);
         break;
     default: launch_hot(k_amul_dot<0>, grid_for(k_amul_dot<0>, a.N), kThreads, s, a, w, f, sell_wn, sell_wo); break;
@@ -1050,6 +1095,12 @@ void launch_update(cudaStream_t s, int grid, const MeshArgs& a, const Workspace&
 {
     (void)grid;
     launch_hot(k_update, grid_for(k_update, a.N, 2), kThreads, s, a.N, w, fin ? 1 : 0);
+}
+
+void launch_iface_rows(cudaStream_t s, const MeshArgs& a, const Workspace& w, const int* rows, int n_rows)
+{
+    if (n_rows <= 0) return;
+    k_iface_rows<<<grid_for(k_iface_rows, n_rows), kThreads, 0, s>>>(a, w, rows, n_rows);
 }
 
 void launch_finalize(cudaStream_t s, int stage, const double* gathered, int n_ranks, const Workspace& w)

@@ -53,6 +53,9 @@ def _callbacks(rank):
 
 def _case(P, how):
     import gen
+    if how == "lattice":  # un-permuted blocks: uniform ELL widths -> the overlapped fast path
+        m = gen.box(8 * P, 8, 6, (float(P), 1.0, 0.75))
+        return m, gen.gamma_lognormal(m), gen.rhs(m), gen.block_parts(m, (P, 1, 1))
     m = gen.permute(gen.perturbed(10, 0.2), seed=6)
     gamma, b = gen.gamma_lognormal(m), gen.rhs(m)
     part = gen.rcb_parts(m, P) if how == "rcb" else gen.block_parts(m, (P, 1, 1))
@@ -77,6 +80,7 @@ def _worker(rank, P, how, port, q):
         me = subs[rank]
         h = S.Mesh.from_mesh(me, rank=rank, n_ranks=P)
         h.set_comm_callbacks(*_callbacks(rank))
+        h.set_option(S.spuma.OPT_SMALL_SOLVE_MAX_CELLS, 0)  # the multi-rank batch path
         f64 = dict(dtype=torch.float64, device="cuda")
         diag, upper = torch.empty(me.n_cells, **f64), torch.empty(me.n_faces, **f64)
         src = torch.as_tensor(bs[rank], **f64)
@@ -113,6 +117,12 @@ def _worker(rank, P, how, port, q):
         allp = [None] * P
         dist.all_gather_object(allp, perf)
         assert all(p == allp[0] for p in allp)  # identical decisions on every rank
+        # the inline-interface Amul (variant 0: halo before the Amul) gives the same iterates
+        h.set_option(S.spuma.OPT_AMUL_VARIANT, 0)
+        psi0 = torch.zeros(me.n_cells, **f64)
+        p0 = h.pcg_solve(diag, upper, iface, src, psi0, 0.0, 0.0, n, n)
+        assert p0["n_iterations"] == n
+        assert np.max(np.abs(psi0.cpu().numpy() - loc)) <= 1e-9 * max(np.max(np.abs(loc)), 1e-300)
         h.free()
         q.put((rank, "ok"))
     except BaseException:
@@ -123,7 +133,7 @@ def _worker(rank, P, how, port, q):
             dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("P,how", [(2, "block"), (3, "rcb"), (4, "rcb")])
+@pytest.mark.parametrize("P,how", [(2, "block"), (3, "rcb"), (4, "rcb"), (2, "lattice"), (4, "lattice")])
 def test_multirank_on_one_gpu_matches_decomposed_oracle(P, how):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
