@@ -182,6 +182,30 @@ spuma_status spuma_pcg_solve(spuma_mesh m, const spuma_scalar* diag, const spuma
 /* Release everything the handle owns (NULL-safe). */
 void spuma_free(spuma_mesh m);
 
+/* ---------------- around the path (the pressure step's neighbours) ----------------
+ * Oriented face fields (phi, flux) are owner -> neighbour in the CALLER's numbering; with
+ * renumber = 1 faces whose owner/neighbour swapped are negated on entry and exit.  Per-patch
+ * arrays are arrays of per-patch pointers (NULL entries read as zero / are not written). */
+
+/* fvc::surfaceIntegrate (profile row "surfaceIntegrate") -- the pressure
+ * source fvc::div(phiHbyA):  out[c] = (sum of the outward fluxes of c: +phi on faces it owns,
+ * -phi on faces where it is the neighbour, +patch_phi on its non-empty boundary faces) / V[c],
+ * accumulated in face order, then (patch, face) order.  phi [n_faces], V, out [n_cells]. */
+spuma_status spuma_surface_integrate(spuma_mesh m, const spuma_scalar* phi, const spuma_scalar* const* patch_phi,
+                                     const spuma_scalar* V, spuma_scalar* out);
+
+/* fvMatrix::flux of the assembled fvm::laplacian(gamma, psi) (lduMatrix::faceH):
+ *   internal  flux[f] = upper[f] psi[N] - upper[f] psi[P]
+ *   boundary  internalCoeffs psi_P - boundaryCoeffs (x psi_remote on processor faces):
+ *             fixedValue (g|S|)(-delta) psi_P - (-(g|S|))(delta p_b); zeroGradient/empty 0.
+ * gamma / patch_value as given to spuma_assemble_laplacian; flux [n_faces] and patch_flux may be
+ * NULL; if phi (and/or patch_phi) is given the SIMPLE correction phi -= flux is applied in place.
+ * n_ranks > 1: collective (psi and gamma halo).  iface_coeffs is reserved (may be NULL). */
+spuma_status spuma_face_flux(spuma_mesh m, const spuma_scalar* gamma, const spuma_scalar* const* patch_value,
+                             const spuma_scalar* upper, const spuma_scalar* iface_coeffs, const spuma_scalar* psi,
+                             spuma_scalar* flux, spuma_scalar* const* patch_flux, spuma_scalar* phi,
+                             spuma_scalar* const* patch_phi);
+
 /* ---------------- diagnostics (parity tests, benchmark harness) ---------------- */
 
 /* y = A x (lduMatrix::Amul), with the processor-interface terms when

@@ -87,6 +87,8 @@ def _L():
             lib.or_sumA.argtypes = [ci, ci] + [vp] * 5 + [ci] + [vp] * 3
             lib.or_pcg.argtypes = [ci, ctypes.POINTER(_Domain), ctypes.POINTER(Controls), ctypes.POINTER(Perf)]
             lib.or_pcg.restype = ci
+            lib.or_surface_integrate.argtypes = [ci, ci, vp, vp, vp, ci] + [vp] * 5
+            lib.or_face_flux.argtypes = [ci] + [vp] * 6 + [ci] + [vp] * 11
             lib.or_dense_from_ldu.argtypes = [ci, ci] + [vp] * 6
             lib.or_dense_matvec.argtypes = [ci, vp, vp, vp]
             lib.or_dense_solve.argtypes = [ci, vp, vp, vp]
@@ -348,6 +350,68 @@ def gamma_halo(meshes: Sequence[gen.Mesh], gammas: Sequence[np.ndarray]):
         out.append([np.array([gammas[lut[int(g)][0]][lut[int(g)][1]] for g in p.neighbour_gid])
                     for p in processor_patches(m)])
     return out
+
+
+# --------------------------------------------------------------------------- O9
+def _patch_field(mesh, values):
+    """Concatenate per-patch face values (None -> zeros) in patch order."""
+    xs = []
+    for i, p in enumerate(mesh.patches):
+        v = None if values is None else values[i]
+        xs.append(np.zeros(p.n_faces) if v is None else np.asarray(v, np.float64))
+    return _f64(np.concatenate(xs) if xs else np.zeros(0))
+
+
+def surface_integrate(mesh: gen.Mesh, phi, patch_phi=None, V=None) -> np.ndarray:
+    """fvc::surfaceIntegrate(phi) (P:513; S:620-626): per cell (sum of outward fluxes) / V."""
+    lib = _L()
+    out = np.empty(mesh.n_cells)
+    own, nbr, ph = _i32(mesh.owner), _i32(mesh.neighbour), _f64(phi)
+    bkind = _i32(np.concatenate([np.full(p.n_faces, p.kind, np.int32) for p in mesh.patches]) if mesh.patches else np.zeros(0))
+    bcells = _bcat(mesh, "face_cells", np.int32)
+    bphi = _patch_field(mesh, patch_phi)
+    Vv = _f64(mesh.V if V is None else V)
+    lib.or_surface_integrate(mesh.n_cells, mesh.n_faces, _p(own), _p(nbr), _p(ph), bkind.shape[0], _p(bkind),
+                             _p(bcells), _p(bphi), _p(Vv), _p(out))
+    return out
+
+
+def face_flux(mesh: gen.Mesh, upper, psi, gamma=None, geo: Optional[Geometry] = None, gamma_remote=None,
+              psi_remote=None, lower=None):
+    """fvMatrix::flux of fvm::laplacian(gamma, psi) (lduMatrix::faceH, P:553; S:325-331) with the
+    boundary contributions. Returns (internal flux [F], list of per-patch flux arrays)."""
+    lib = _L()
+    geo = geo or geometry(mesh)
+    lower = upper if lower is None else lower
+    F = mesh.n_faces
+    flux = np.empty(F)
+    bkind = _i32(np.concatenate([np.full(p.n_faces, p.kind, np.int32) for p in mesh.patches]) if mesh.patches else np.zeros(0))
+    bcells = _bcat(mesh, "face_cells", np.int32)
+    bmag = _bcat(mesh, "magSf", np.float64)
+    bval = _bcat(mesh, "value", np.float64)
+    bown = _bcat(mesh, "is_owner", np.int8)
+
+    def proc_field(vals):
+        xs, k = [], 0
+        for p in mesh.patches:
+            if p.kind == PROCESSOR and vals is not None:
+                xs.append(np.asarray(vals[k], np.float64))
+                k += 1
+            else:
+                xs.append(np.zeros(p.n_faces))
+        return _f64(np.concatenate(xs) if xs else np.zeros(0))
+
+    bgr, bpr = proc_field(gamma_remote), proc_field(psi_remote)
+    bflux = np.zeros(bkind.shape[0])
+    own, nbr, lo, up, ps = _i32(mesh.owner), _i32(mesh.neighbour), _f64(lower), _f64(upper), _f64(psi)
+    g = None if gamma is None else _f64(gamma)
+    lib.or_face_flux(F, _p(own), _p(nbr), _p(lo), _p(up), _p(ps), _p(flux), bkind.shape[0], _p(bkind), _p(bcells),
+                     _p(bmag), _p(geo.bdelta), _p(geo.bweight), _p(bval), _p(bgr), _p(bown), _p(g), _p(bpr), _p(bflux))
+    out, off = [], 0
+    for p in mesh.patches:
+        out.append(bflux[off:off + p.n_faces].copy())
+        off += p.n_faces
+    return flux, out
 
 
 # --------------------------------------------------------------------------- O7

@@ -19,6 +19,7 @@
  *   O5 Amul         or_amul, or_sumA                                      P:506 "SpMVM (Amul + Tmul)", P:519 sumA
  *   O6 PCG          or_pcg (P >= 1 domains, O8 when P > 1)                P:961, P:1033-1041 (pcgDiag)
  *   O7 dense        or_dense_from_ldu, or_dense_matvec, or_dense_solve    brute force for N <= 64
+ *   O9 around       or_surface_integrate, or_face_flux
  *
  * Pins (tests/test_oracle_*.py, -m "not gpu"): SPEC chain examples,
  * closed-form Poisson eigenmodes (Dirichlet / Neumann) and linear exactness,
@@ -373,6 +374,63 @@ void or_sumA(int n_cells, int n_faces, const int* owner, const int* neighbour, c
         sumA[neighbour[f]] += upper[f];
     }
     for (int i = 0; i < n_iface; ++i) sumA[iface_cells[i]] += iface_coeffs[i];
+}
+
+/* ------------------------------------------------------------------------- */
+/* O9 around the path: fvc::surfaceIntegrate -- the pressure  */
+/* source fvc::div(phiHbyA) -- and fvMatrix::flux (lduMatrix::faceH plus the  */
+/* boundary contributions) for the flux correction phi = phiHbyA - flux.      */
+/* Paper: profile rows "surfaceIntegrate" and "lduMatrix::faceH"      */
+/* (P:553); SPEC S:620-626 (surface_integrate), S:325-331 (face_h).           */
+/* ------------------------------------------------------------------------- */
+
+/* out[c] = (sum over internal faces in face order of +phi (owner) / -phi (neighbour),
+ * then the boundary faces of c in (patch, face) order, empty patches excluded) / V[c] */
+void or_surface_integrate(int n_cells, int n_faces, const int* owner, const int* neighbour, const double* phi,
+                          int n_bfaces, const int* bkind, const int* bcells, const double* bphi, const double* V,
+                          double* out)
+{
+    for (int c = 0; c < n_cells; ++c) out[c] = 0.0;
+    for (int f = 0; f < n_faces; ++f) {
+        out[owner[f]] += phi[f];
+        out[neighbour[f]] -= phi[f];
+    }
+    for (int b = 0; b < n_bfaces; ++b)
+        if (bkind[b] != OR_EMPTY) out[bcells[b]] += bphi[b];
+    for (int c = 0; c < n_cells; ++c) out[c] /= V[c];
+}
+
+/* fvMatrix::flux of the assembled fvm::laplacian(gamma, psi):
+ *   internal (faceH):  flux[f] = Upper[f] psi[N] - Lower[f] psi[P]
+ *   boundary:          internalCoeffs psi_P - boundaryCoeffs (x psi_remote when coupled), i.e.
+ *     fixedValue:  (gms (-delta)) psi_P - ((-gms) (delta p_b))
+ *     processor:   (gms (-delta)) psi_P - (((-gms) delta) psi_remote)   (global-orientation gms)
+ *     zeroGradient / empty: 0 */
+void or_face_flux(int n_faces, const int* owner, const int* neighbour, const double* lower, const double* upper,
+                  const double* psi, double* flux, int n_bfaces, const int* bkind, const int* bcells,
+                  const double* bmagSf, const double* bdelta, const double* bweight, const double* bvalue,
+                  const double* bgamma_r, const signed char* bis_owner, const double* gamma,
+                  const double* bpsi_r, double* bflux)
+{
+    for (int f = 0; f < n_faces; ++f) flux[f] = upper[f] * psi[neighbour[f]] - lower[f] * psi[owner[f]];
+    for (int b = 0; b < n_bfaces; ++b) {
+        const int P = bcells[b];
+        const double gP = gamma ? gamma[P] : 1.0;
+        bflux[b] = 0.0;
+        if (bkind[b] == OR_FIXED_VALUE) {
+            const double gms = gP * bmagSf[b];
+            bflux[b] = (gms * (-bdelta[b])) * psi[P] - ((-gms) * (bdelta[b] * bvalue[b]));
+        } else if (bkind[b] == OR_PROCESSOR) {
+            double gf = 1.0;
+            if (gamma) {
+                const double gO = bis_owner[b] ? gP : bgamma_r[b];
+                const double gN = bis_owner[b] ? bgamma_r[b] : gP;
+                gf = bweight[b] * (gO - gN) + gN;
+            }
+            const double gms = gf * bmagSf[b];
+            bflux[b] = (gms * (-bdelta[b])) * psi[P] - (((-gms) * bdelta[b]) * bpsi_r[b]);
+        }
+    }
 }
 
 /* ------------------------------------------------------------------------- */

@@ -186,6 +186,67 @@ spuma_status iface_in(spuma_mesh m, const double* p, const double** out)
     return SPUMA_OK;
 }
 
+// oriented face field (e.g. a flux, owner -> neighbour) -> internal numbering/orientation
+spuma_status oriented_in(spuma_mesh m, const double* p, double** buf, double** out)
+{
+    const bool dev = is_device_ptr(p);
+    if (!m->renumber && dev) {
+        *out = const_cast<double*>(p);
+        return SPUMA_OK;
+    }
+    if (!*buf) SPUMA_TRY(dalloc(buf, m->F));
+    if (!m->renumber) {
+        SPUMA_CUDA(cudaMemcpyAsync(*buf, p, sizeof(double) * m->F, cudaMemcpyHostToDevice, m->stream));
+    } else {
+        const double* src = p;
+        if (!dev) {
+            if (!m->d_face_t) SPUMA_TRY(dalloc(&m->d_face_t, std::max(m->F, m->N)));
+            SPUMA_CUDA(cudaMemcpyAsync(m->d_face_t, p, sizeof(double) * m->F, cudaMemcpyHostToDevice, m->stream));
+            src = m->d_face_t;
+        }
+        launch_gather_signed(m->stream, m->F, m->d_face_map, m->d_face_flip, src, *buf);
+    }
+    *out = *buf;
+    return SPUMA_OK;
+}
+
+spuma_status oriented_out(spuma_mesh m, double* p, const double* buf)
+{
+    if (buf == p) return SPUMA_OK;
+    if (!m->renumber) {
+        SPUMA_CUDA(cudaMemcpyAsync(p, buf, sizeof(double) * m->F, cudaMemcpyDefault, m->stream));
+        return SPUMA_OK;
+    }
+    if (!m->d_face_t) SPUMA_TRY(dalloc(&m->d_face_t, std::max(m->F, m->N)));
+    launch_scatter_signed(m->stream, m->F, m->d_face_map, m->d_face_flip, buf, m->d_face_t);
+    SPUMA_CUDA(cudaMemcpyAsync(p, m->d_face_t, sizeof(double) * m->F, cudaMemcpyDefault, m->stream));
+    return SPUMA_OK;
+}
+
+// per-patch face values (array of per-patch pointers, NULL entries = 0) -> concatenated device buffer
+spuma_status patches_in(spuma_mesh m, const double* const* pv, double* dst, bool skip_empty_kinds)
+{
+    SPUMA_CUDA(cudaMemsetAsync(dst, 0, sizeof(double) * std::max(m->Fb, 1), m->stream));
+    if (!pv) return SPUMA_OK;
+    for (size_t p = 0; p < m->patches.size(); ++p) {
+        const Patch& P = m->patches[p];
+        if (!pv[p] || P.n_faces == 0 || (skip_empty_kinds && P.kind == SPUMA_PATCH_EMPTY)) continue;
+        SPUMA_CUDA(cudaMemcpyAsync(dst + P.offset, pv[p], sizeof(double) * P.n_faces, cudaMemcpyDefault, m->stream));
+    }
+    return SPUMA_OK;
+}
+
+spuma_status patches_out(spuma_mesh m, double* const* pv, const double* src)
+{
+    if (!pv) return SPUMA_OK;
+    for (size_t p = 0; p < m->patches.size(); ++p) {
+        const Patch& P = m->patches[p];
+        if (!pv[p] || P.n_faces == 0) continue;
+        SPUMA_CUDA(cudaMemcpyAsync(pv[p], src + P.offset, sizeof(double) * P.n_faces, cudaMemcpyDefault, m->stream));
+    }
+    return SPUMA_OK;
+}
+
 // ---------------------------------------------------------------------------
 // halo exchange over NCCL (processor patches)
 // ---------------------------------------------------------------------------
@@ -388,7 +449,8 @@ void spuma_free(spuma_mesh m)
                      m->d_owner, m->d_neighbour, m->d_ownerStart, m->d_losortStart, m->d_losort, m->d_ownerLo,
                      m->d_perm, m->d_face_map, m->d_delta, m->d_weights, m->d_magSf, m->d_bkind, m->d_bcell,
                      m->d_bproc, m->d_bmagSf, m->d_bdelta, m->d_bweight, m->d_bvalue, m->d_bgamma_r,
-                     m->d_bis_owner, m->d_bStart, m->d_bFace, m->d_ifStart, m->d_ifIdx, m->d_if_cell, m->d_ifMask, m->d_ifRows,
+                     m->d_bis_owner, m->d_bStart, m->d_bFace, m->d_bAllStart, m->d_bAllFace, m->d_face_flip,
+                     m->d_bphi, m->d_bflux, m->d_face_b, m->d_face_c, m->d_ifStart, m->d_ifIdx, m->d_if_cell, m->d_ifMask, m->d_ifRows,
                      m->d_sendbuf, m->d_cell_a, m->d_cell_b, m->d_cell_c, m->d_cell_d, m->d_cell_e, m->d_cell_t,
                      m->d_face_a, m->d_face_t, m->d_iface_a, m->ws.wA, m->ws.rA, m->ws.pA, m->ws.rD, m->ws.sumA,
                      m->ws.xr, m->ws.part, m->ws.scal, m->ws.ptrs};
@@ -481,6 +543,7 @@ static spuma_status mesh_create_impl(const spuma_mesh_desc* d, spuma_mesh m)
         std::vector<int> o2, n2;
         std::vector<char> flip;
         rekey_faces(N, F, m->h_perm.data(), owner.data(), neighbour.data(), o2, n2, m->h_face_map, flip);
+        m->h_face_flip.assign(flip.begin(), flip.end());
         std::vector<double> Sf2(3 * (size_t)F), magSf2(F), Cf2(3 * (size_t)F), C2(3 * (size_t)N);
         for (int g = 0; g < F; ++g) {
             const int f = m->h_face_map[g];
@@ -548,6 +611,12 @@ static spuma_status mesh_create_impl(const spuma_mesh_desc* d, spuma_mesh m)
     m->n_iface = iface_off;
     std::vector<int> bStart, bFace;
     cell_lists(N, bcell, contributes, bStart, bFace);
+    std::vector<int> bAllStart, bAllFace;
+    {
+        std::vector<char> nonempty(bkind.size());
+        for (size_t i = 0; i < bkind.size(); ++i) nonempty[i] = bkind[i] != SPUMA_PATCH_EMPTY;
+        cell_lists(N, bcell, nonempty, bAllStart, bAllFace);
+    }
     std::vector<int> ifStart, ifIdx;
     cell_lists(N, if_cell, std::vector<char>(if_cell.size(), 1), ifStart, ifIdx);
 
@@ -573,6 +642,7 @@ static spuma_status mesh_create_impl(const spuma_mesh_desc* d, spuma_mesh m)
     if (m->renumber) {
         SPUMA_TRY(upload(&m->d_perm, m->h_perm, s));
         SPUMA_TRY(upload(&m->d_face_map, m->h_face_map, s));
+        SPUMA_TRY(upload(&m->d_face_flip, m->h_face_flip, s));
     }
     SPUMA_TRY(upload(&m->d_magSf, magSf, s));
     SPUMA_TRY(upload(&m->d_bkind, bkind, s));
@@ -582,6 +652,10 @@ static spuma_status mesh_create_impl(const spuma_mesh_desc* d, spuma_mesh m)
     SPUMA_TRY(upload(&m->d_bis_owner, bown, s));
     SPUMA_TRY(upload(&m->d_bStart, bStart, s));
     SPUMA_TRY(upload(&m->d_bFace, bFace, s));
+    SPUMA_TRY(upload(&m->d_bAllStart, bAllStart, s));
+    SPUMA_TRY(upload(&m->d_bAllFace, bAllFace, s));
+    SPUMA_TRY(dalloc(&m->d_bphi, m->Fb));
+    SPUMA_TRY(dalloc(&m->d_bflux, m->Fb));
     SPUMA_TRY(upload(&m->d_ifStart, ifStart, s));
     SPUMA_TRY(upload(&m->d_ifIdx, ifIdx, s));
     SPUMA_TRY(upload(&m->d_if_cell, if_cell, s));
@@ -912,6 +986,76 @@ spuma_status spuma_pcg_solve(spuma_mesh m, const spuma_scalar* diag, const spuma
     m->stats.iterations += fs.n;
     SPUMA_TRY(cells_out(m, psi, P.psi));
     SPUMA_CUDA(cudaStreamSynchronize(s));
+    return SPUMA_OK;
+}
+
+spuma_status spuma_surface_integrate(spuma_mesh m, const spuma_scalar* phi, const spuma_scalar* const* patch_phi,
+                                     const spuma_scalar* V, spuma_scalar* out)
+{
+    if (!m) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "mesh is NULL");
+    if ((m->F > 0 && !phi) || (m->N > 0 && (!V || !out))) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "NULL array");
+    cudaStream_t s = m->stream;
+    double* phi_i = nullptr;
+    SPUMA_TRY(oriented_in(m, phi, &m->d_face_b, &phi_i));
+    SPUMA_TRY(patches_in(m, patch_phi, m->d_bphi, true));
+    const double* V_i = nullptr;
+    SPUMA_TRY(cells_in(m, V, R_X, &V_i));
+    double* out_i = out;
+    if (m->renumber || !is_device_ptr(out)) {
+        if (!m->d_cell_t) SPUMA_TRY(dalloc(&m->d_cell_t, m->N));
+        out_i = m->d_cell_t;
+    }
+    launch_surface_integrate(s, mesh_args(m), phi_i, m->d_bAllStart, m->d_bAllFace, m->d_bphi, V_i, out_i);
+    m->stats.kernel_launches += 1;
+    SPUMA_TRY(cells_out(m, out, out_i));
+    SPUMA_CUDA(cudaStreamSynchronize(s));
+    SPUMA_CUDA(cudaGetLastError());
+    return SPUMA_OK;
+}
+
+spuma_status spuma_face_flux(spuma_mesh m, const spuma_scalar* gamma, const spuma_scalar* const* patch_value,
+                             const spuma_scalar* upper, const spuma_scalar* iface_coeffs, const spuma_scalar* psi,
+                             spuma_scalar* flux, spuma_scalar* const* patch_flux, spuma_scalar* phi,
+                             spuma_scalar* const* patch_phi)
+{
+    (void)iface_coeffs;
+    if (!m) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "mesh is NULL");
+    if ((m->F > 0 && !upper) || (m->N > 0 && !psi)) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "NULL array");
+    cudaStream_t s = m->stream;
+    for (size_t p = 0; p < m->patches.size(); ++p)
+        if (m->patches[p].kind == SPUMA_PATCH_FIXED_VALUE && m->patches[p].n_faces > 0 && (!patch_value || !patch_value[p]))
+            return set_error(SPUMA_ERR_INVALID_ARGUMENT, "missing fixedValue values for patch " + std::to_string(p));
+    SPUMA_TRY(patches_in(m, patch_value, m->d_bvalue, true));
+    const double *u_i = nullptr, *psi_i = nullptr, *g = nullptr;
+    SPUMA_TRY(faces_in(m, upper, &u_i));
+    SPUMA_TRY(cells_in(m, psi, R_PSI, &psi_i));
+    if (gamma) SPUMA_TRY(cells_in(m, gamma, R_GAMMA, &g));
+    if (m->n_ranks > 1) {  // psi (and gamma) of the remote cells of processor faces
+        SPUMA_TRY(halo_exchange(m, psi_i, m->ws.xr, s));
+        if (g) SPUMA_TRY(halo_exchange(m, g, m->d_bgamma_r, s));
+    }
+    double* phi_i = nullptr;
+    if (phi) SPUMA_TRY(oriented_in(m, phi, &m->d_face_b, &phi_i));
+    double* flux_i = nullptr;
+    if (flux) {
+        flux_i = flux;
+        if (m->renumber || !is_device_ptr(flux)) {
+            if (!m->d_face_c) SPUMA_TRY(dalloc(&m->d_face_c, m->F));
+            flux_i = m->d_face_c;
+        }
+    }
+    if (patch_phi) SPUMA_TRY(patches_in(m, patch_phi, m->d_bphi, false));
+    launch_face_flux(s, m->F, m->d_owner, m->d_neighbour, u_i, psi_i, flux_i, phi_i);
+    launch_bface_flux(s, m->Fb, m->d_bkind, m->d_bcell, m->d_bproc, m->d_bmagSf, m->d_bdelta, m->d_bweight,
+                      m->d_bvalue, m->d_bgamma_r, m->d_bis_owner, g, psi_i, m->ws.xr, m->d_bflux,
+                      patch_phi ? m->d_bphi : nullptr);
+    m->stats.kernel_launches += 2;
+    if (flux) SPUMA_TRY(oriented_out(m, flux, flux_i));
+    if (phi) SPUMA_TRY(oriented_out(m, phi, phi_i));
+    SPUMA_TRY(patches_out(m, patch_flux, m->d_bflux));
+    if (patch_phi) SPUMA_TRY(patches_out(m, patch_phi, m->d_bphi));
+    SPUMA_CUDA(cudaStreamSynchronize(s));
+    SPUMA_CUDA(cudaGetLastError());
     return SPUMA_OK;
 }
 

@@ -93,6 +93,7 @@ struct spuma_mesh_s {
     std::vector<spuma::Patch> patches;
     // host copies of the derived addressing (internal numbering) for diagnostics
     std::vector<int> h_perm, h_face_map, h_owner, h_neighbour, h_ownerStart, h_losort, h_losortStart;
+    std::vector<signed char> h_face_flip;
 
     // device: addressing (internal numbering)
     int *d_owner = nullptr, *d_neighbour = nullptr, *d_ownerStart = nullptr, *d_losortStart = nullptr;
@@ -111,6 +112,10 @@ struct spuma_mesh_s {
     double* d_bgamma_r = nullptr;    // [n_iface] remote gamma (gamma halo)
     signed char* d_bis_owner = nullptr;
     int *d_bStart = nullptr, *d_bFace = nullptr;   // per-cell lists of contributing boundary faces
+    int *d_bAllStart = nullptr, *d_bAllFace = nullptr;  // per-cell lists of all non-empty boundary faces
+    signed char* d_face_flip = nullptr;  // renumber: internal face orientation reversed w.r.t. the caller
+    double *d_bphi = nullptr, *d_bflux = nullptr;       // [Fb] staging of per-patch face fields
+    double *d_face_b = nullptr, *d_face_c = nullptr;    // [F] staging of oriented face fields
     // device: interfaces
     int *d_ifStart = nullptr, *d_ifIdx = nullptr, *d_if_cell = nullptr;  // if_cell: [n_iface] local cell
     unsigned* d_ifMask = nullptr;
@@ -202,6 +207,18 @@ void launch_amul_dot(cudaStream_t s, int variant, const MeshArgs& a, const Works
                      int sell_wo, bool deferred = false);
 int resolve_amul_variant(int variant, const MeshArgs& a);  // variant actually run on this mesh
 void launch_iface_rows(cudaStream_t s, const MeshArgs& a, const Workspace& w, const int* rows, int n_rows);
+void launch_surface_integrate(cudaStream_t s, const MeshArgs& a, const double* phi, const int* bStart,
+                              const int* bFace, const double* bphi, const double* V, double* out);
+void launch_face_flux(cudaStream_t s, int F, const int* owner, const int* neighbour, const double* upper,
+                      const double* psi, double* flux, double* phi);
+void launch_bface_flux(cudaStream_t s, int Fb, const int* bkind, const int* bcell, const int* bproc,
+                       const double* bmagSf, const double* bdelta, const double* bweight, const double* bvalue,
+                       const double* bgamma_r, const signed char* bis_owner, const double* gamma, const double* psi,
+                       const double* psi_r, double* bflux, double* bphi);
+void launch_gather_signed(cudaStream_t s, int n, const int* idx, const signed char* flip, const double* in,
+                          double* out);
+void launch_scatter_signed(cudaStream_t s, int n, const int* idx, const signed char* flip, const double* in,
+                           double* out);
 constexpr int kPad = 8;  // padding elements on internal arrays (16-byte TMA windows may overrun by <= 3)
 void launch_update(cudaStream_t s, int grid, const MeshArgs& a, const Workspace& w, bool fin);
 // P > 1: finalise from the gathered rank partials ([n_ranks][4], rank order)

@@ -773,6 +773,93 @@ void launch_pcg_single(cudaStream_t s, const MeshArgs& a, const Workspace& w)
     k_pcg_single<<<1, kSmallThreads, 0, s>>>(a, w);
 }
 
+// ---------------------------------------------------------------------------
+// Around the path: fvc::surfaceIntegrate and fvMatrix::flux
+// ---------------------------------------------------------------------------
+
+// out[c] = (-phi of faces with neighbour c in losort order, +phi of faces with owner c
+// in face order, +bphi of c's non-empty boundary faces in (patch, face) order) / V[c]:
+// the oracle's face-loop order, so bitwise ("surfaceIntegrate").
+__global__ void __launch_bounds__(kThreads)
+    k_surface_integrate(MeshArgs a, const double* __restrict__ phi, const int* __restrict__ bStart,
+                        const int* __restrict__ bFace, const double* __restrict__ bphi,
+                        const double* __restrict__ V, double* __restrict__ out)
+{
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < a.N; c += gridDim.x * blockDim.x) {
+        double s = 0.0;
+        const int k1 = a.losortStart[c + 1];
+        for (int k = a.losortStart[c]; k < k1; ++k) s = s - phi[a.losort[k]];
+        const int f1 = a.ownerStart[c + 1];
+        for (int f = a.ownerStart[c]; f < f1; ++f) s = s + phi[f];
+        const int j1 = bStart[c + 1];
+        for (int j = bStart[c]; j < j1; ++j) s = s + bphi[bFace[j]];
+        out[c] = s / V[c];
+    }
+}
+
+// fvMatrix::flux, internal faces: faceH = Upper psi_N - Lower psi_P;
+// phi != nullptr: the SIMPLE correction phi -= flux in place.
+__global__ void __launch_bounds__(kThreads)
+    k_face_flux(int F, const int* __restrict__ owner, const int* __restrict__ neighbour,
+                const double* __restrict__ upper, const double* __restrict__ psi, double* __restrict__ flux,
+                double* __restrict__ phi)
+{
+    for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < F; f += gridDim.x * blockDim.x) {
+        const double u = upper[f];
+        const double q = u * psi[neighbour[f]] - u * psi[owner[f]];
+        if (flux) flux[f] = q;
+        if (phi) phi[f] = phi[f] - q;
+    }
+}
+
+// boundary faces: internalCoeffs psi_P - boundaryCoeffs (x psi_remote for processor faces)
+__global__ void __launch_bounds__(kThreads)
+    k_bface_flux(int Fb, const int* __restrict__ bkind, const int* __restrict__ bcell, const int* __restrict__ bproc,
+                 const double* __restrict__ bmagSf, const double* __restrict__ bdelta,
+                 const double* __restrict__ bweight, const double* __restrict__ bvalue,
+                 const double* __restrict__ bgamma_r, const signed char* __restrict__ bis_owner,
+                 const double* __restrict__ gamma, const double* __restrict__ psi, const double* __restrict__ psi_r,
+                 double* __restrict__ bflux, double* __restrict__ bphi)
+{
+    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < Fb; b += gridDim.x * blockDim.x) {
+        const int P = bcell[b];
+        const double gP = gamma ? gamma[P] : 1.0;
+        double q = 0.0;
+        if (bkind[b] == SPUMA_PATCH_FIXED_VALUE) {
+            const double gms = gP * bmagSf[b];
+            q = (gms * (-bdelta[b])) * psi[P] - ((-gms) * (bdelta[b] * bvalue[b]));
+        } else if (bkind[b] == SPUMA_PATCH_PROCESSOR) {
+            const int i = bproc[b];
+            double gf = 1.0;
+            if (gamma) {
+                const double gr = bgamma_r[i];
+                const double gO = bis_owner[b] ? gP : gr;
+                const double gN = bis_owner[b] ? gr : gP;
+                gf = bweight[b] * (gO - gN) + gN;
+            }
+            const double gms = gf * bmagSf[b];
+            q = (gms * (-bdelta[b])) * psi[P] - (((-gms) * bdelta[b]) * psi_r[i]);
+        }
+        bflux[b] = q;
+        if (bphi) bphi[b] = bphi[b] - q;
+    }
+}
+
+// oriented face field <-> internal numbering: out[i] = sign(flip[i]) in[idx[i]] (gather)
+// or out[idx[i]] = sign(flip[i]) in[i] (scatter)
+__global__ void k_gather_signed(int n, const int* __restrict__ idx, const signed char* __restrict__ flip,
+                                const double* __restrict__ in, double* __restrict__ out)
+{
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        out[i] = flip[i] ? -in[idx[i]] : in[idx[i]];
+}
+__global__ void k_scatter_signed(int n, const int* __restrict__ idx, const signed char* __restrict__ flip,
+                                 const double* __restrict__ in, double* __restrict__ out)
+{
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        out[idx[i]] = flip[i] ? -in[i] : in[i];
+}
+
 // A7 interface rows (P > 1, deferred mode): rows[] = cells with processor faces
 // (ascending).  wA[c] already holds the internal-face sum; add the interface terms
 // in (patch, face) order (bitwise the one-pass row, Q10) and the rows' share of
@@ -1095,6 +1182,45 @@ void launch_update(cudaStream_t s, int grid, const MeshArgs& a, const Workspace&
 {
     (void)grid;
     launch_hot(k_update, grid_for(k_update, a.N, 2), kThreads, s, a.N, w, fin ? 1 : 0);
+}
+
+void launch_surface_integrate(cudaStream_t s, const MeshArgs& a, const double* phi, const int* bStart,
+                              const int* bFace, const double* bphi, const double* V, double* out)
+{
+    if (a.N <= 0) return;
+    k_surface_integrate<<<grid_for(k_surface_integrate, a.N), kThreads, 0, s>>>(a, phi, bStart, bFace, bphi, V, out);
+}
+
+void launch_face_flux(cudaStream_t s, int F, const int* owner, const int* neighbour, const double* upper,
+                      const double* psi, double* flux, double* phi)
+{
+    if (F <= 0) return;
+    k_face_flux<<<grid_for(k_face_flux, F), kThreads, 0, s>>>(F, owner, neighbour, upper, psi, flux, phi);
+}
+
+void launch_bface_flux(cudaStream_t s, int Fb, const int* bkind, const int* bcell, const int* bproc,
+                       const double* bmagSf, const double* bdelta, const double* bweight, const double* bvalue,
+                       const double* bgamma_r, const signed char* bis_owner, const double* gamma, const double* psi,
+                       const double* psi_r, double* bflux, double* bphi)
+{
+    if (Fb <= 0) return;
+    k_bface_flux<<<grid_for(k_bface_flux, Fb), kThreads, 0, s>>>(Fb, bkind, bcell, bproc, bmagSf, bdelta, bweight,
+                                                                 bvalue, bgamma_r, bis_owner, gamma, psi, psi_r,
+                                                                 bflux, bphi);
+}
+
+void launch_gather_signed(cudaStream_t s, int n, const int* idx, const signed char* flip, const double* in,
+                          double* out)
+{
+    if (n <= 0) return;
+    k_gather_signed<<<grid_for(k_gather_signed, n), kThreads, 0, s>>>(n, idx, flip, in, out);
+}
+
+void launch_scatter_signed(cudaStream_t s, int n, const int* idx, const signed char* flip, const double* in,
+                           double* out)
+{
+    if (n <= 0) return;
+    k_scatter_signed<<<grid_for(k_scatter_signed, n), kThreads, 0, s>>>(n, idx, flip, in, out);
 }
 
 void launch_iface_rows(cudaStream_t s, const MeshArgs& a, const Workspace& w, const int* rows, int n_rows)

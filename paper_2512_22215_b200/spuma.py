@@ -103,6 +103,9 @@ def lib():
         L.spuma_free.argtypes = [_vp]
         L.spuma_free.restype = None
         L.spuma_amul.argtypes = [_vp] * 6
+        if hasattr(L, "spuma_surface_integrate"):
+            L.spuma_surface_integrate.argtypes = [_vp] * 5
+            L.spuma_face_flux.argtypes = [_vp] * 10
         L.spuma_mesh_get_addressing.argtypes = [_vp] * 8
         L.spuma_mesh_get_geometry.argtypes = [_vp] * 4
         L.spuma_get_stats.argtypes = [_vp, ctypes.POINTER(Stats)]
@@ -118,7 +121,8 @@ def lib():
         for name in ("spuma_mesh_create", "spuma_assemble_laplacian", "spuma_pcg_solve", "spuma_amul",
                      "spuma_mesh_get_addressing", "spuma_mesh_get_geometry", "spuma_get_stats",
                      "spuma_reset_stats", "spuma_set_timing", "spuma_set_batch", "spuma_nccl_get_unique_id",
-                     "spuma_set_option", "spuma_set_comm_callbacks"):
+                     "spuma_set_option", "spuma_set_comm_callbacks", "spuma_surface_integrate",
+                     "spuma_face_flux"):
             if hasattr(L, name):
                 getattr(L, name).restype = _ci
         if L.spuma_abi_version() != ABI_VERSION:
@@ -274,6 +278,39 @@ class Mesh:
         yp, ky = _ptr(y, np.float64)
         _check(lib().spuma_amul(self._h, d, u, f, xp, yp))
         return ky
+
+    # ---------------------------------------------------------------- around the path (§8(f1))
+    @staticmethod
+    def _patch_ptrs(values, keep):
+        if values is None:
+            return None
+        arr = (_vp * max(len(values), 1))()
+        for i, v in enumerate(values):
+            p, k = _ptr(v, np.float64)
+            keep.append(k)
+            arr[i] = p
+        return arr
+
+    def surface_integrate(self, phi, patch_phi, V, out):
+        """spuma_surface_integrate: out = fvc::surfaceIntegrate(phi) (per cell, divided by V)."""
+        keep = []
+        pp = self._patch_ptrs(patch_phi, keep)
+        a, ka = _ptr(phi, np.float64)
+        v, kv = _ptr(V, np.float64)
+        o, ko = _ptr(out, np.float64)
+        _check(lib().spuma_surface_integrate(self._h, a, pp, v, o))
+        return ko
+
+    def face_flux(self, gamma, patch_values, upper, iface_coeffs, psi, flux=None, patch_flux=None, phi=None,
+                  patch_phi=None):
+        """spuma_face_flux: fvMatrix::flux of the Laplacian; phi -= flux in place when phi is given."""
+        keep = []
+        pv = self._patch_ptrs(patch_values, keep)
+        pf = self._patch_ptrs(patch_flux, keep)
+        pp = self._patch_ptrs(patch_phi, keep)
+        ptrs = [_ptr(x, np.float64) for x in (gamma, upper, iface_coeffs, psi, flux, phi)]
+        g, u, f, ps, fl, ph = [p for p, _ in ptrs]
+        _check(lib().spuma_face_flux(self._h, g, pv, u, f, ps, fl, pf, ph, pp))
 
     # ---------------------------------------------------------------- diagnostics
     def mesh_get_addressing(self) -> dict:

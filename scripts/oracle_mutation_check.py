@@ -25,12 +25,18 @@ muts = [
  ("if (fabs(wApA) / normFactor < 1e-300) {", "if (fabs(wApA) / normFactor < -1.0) {"),
  ("for (int c = 0; c < D[p].n_cells; ++c) W[p].rD[c] = 1.0 / D[p].diag[c];", "for (int c = 0; c < D[p].n_cells; ++c) W[p].rD[c] = 1.0;"),
  ("delta[i] = 1.0 / (nh[0] * e[0] + nh[1] * e[1] + nh[2] * e[2]);", "delta[i] = 1.0 / (nh[0] * e[0] + nh[1] * e[1] + nh[2] * e[2]) / 2;"),
+ ("out[neighbour[f]] -= phi[f];", "out[neighbour[f]] += phi[f];"),
+ ("if (bkind[b] != OR_EMPTY) out[bcells[b]] += bphi[b];", "out[bcells[b]] += bphi[b];"),
+ ("for (int f = 0; f < n_faces; ++f) flux[f] = upper[f] * psi[neighbour[f]] - lower[f] * psi[owner[f]];", "for (int f = 0; f < n_faces; ++f) flux[f] = upper[f] * psi[owner[f]] - lower[f] * psi[neighbour[f]];"),
+ ("bflux[b] = (gms * (-bdelta[b])) * psi[P] - ((-gms) * (bdelta[b] * bvalue[b]));", "bflux[b] = (gms * (-bdelta[b])) * psi[P] + ((-gms) * (bdelta[b] * bvalue[b]));"),
 ]
 res = []
 for a, b in muts:
     assert a in src, a
     open('oracle/oracle.c', 'w').write(src.replace(a, b))
-    r = subprocess.run([sys.executable, '-m', 'pytest', 'tests', '-x', '-q', '-m', 'not gpu'], capture_output=True, text=True)
+    import glob
+    oracle_tests = sorted(glob.glob('tests/test_oracle_*.py')) + ['tests/test_multirank_gloo.py']
+    r = subprocess.run([sys.executable, '-m', 'pytest', *oracle_tests, '-x', '-q', '-m', 'not gpu'], capture_output=True, text=True)
     caught = r.returncode != 0
     line = [l for l in r.stdout.splitlines() if l.startswith('FAILED')][:1]
     res.append((caught, a[:60], line))
