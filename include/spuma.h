@@ -260,7 +260,10 @@ typedef enum {
      * kernel launch (latency path, BASELINE config 1); default 8192; 0 disables */
     SPUMA_OPT_SMALL_SOLVE_MAX_CELLS = 1,
     /* programmatic dependent launch of the hot-loop kernels (1 = on, default; process-wide) */
-    SPUMA_OPT_PDL = 2
+    SPUMA_OPT_PDL = 2,
+    /* apply psi += alpha pA for two iterations at once (psi = (psi + a1 p1) + a2 p2: the same
+     * roundings, fewer bytes); 1 = on (default), 0 = every iteration */
+    SPUMA_OPT_DEFER_PSI = 3
 } spuma_option;
 spuma_status spuma_set_option(spuma_mesh m, int option, int value);
 

@@ -316,39 +316,51 @@ spuma_status enqueue_iteration(spuma_mesh m, cudaStream_t s, std::vector<cudaEve
 {
     const MeshArgs a = mesh_args(m);
     const bool fin = m->n_ranks == 1;
+    // deferred psi updates: iteration k (slot parity = k parity) writes direction buffer k % 2,
+    // reads the previous one, and applies psi for the pair (k-1, k) when k is odd
+    Workspace ws = m->ws;
+    int psi_mode = 0;
+    if (m->defer_psi) {
+        ws.pA = (slot & 1) ? m->ws.pA2 : m->ws.pA;
+        ws.pA_prev = (slot & 1) ? m->ws.pA : m->ws.pA2;
+        psi_mode = (slot & 1) ? 2 : 1;
+    }
     const int rv = resolve_amul_variant(m->amul_variant, a);
     const bool overlap = !fin && m->n_iface > 0 && rv >= 6 && rv <= 9;
     if (ev) record(m, *ev, slot * 6 + 0, s);
-    launch_direction(s, m->grid, a, m->ws);
+    launch_direction(s, m->grid, a, ws);
     if (ev) record(m, *ev, slot * 6 + 1, s);
     if (overlap) {
         if (!m->external_comm) {
             SPUMA_CUDA(cudaEventRecord(m->ev_fork, s));
             SPUMA_CUDA(cudaStreamWaitEvent(m->comm_stream, m->ev_fork, 0));
-            SPUMA_TRY(halo_exchange(m, m->ws.pA, m->ws.xr, m->comm_stream));
+            SPUMA_TRY(halo_exchange(m, ws.pA, ws.xr, m->comm_stream));
             SPUMA_CUDA(cudaEventRecord(m->ev_join, m->comm_stream));
         }
         if (ev) record(m, *ev, slot * 6 + 2, s);
-        launch_amul_dot(s, m->amul_variant, a, m->ws, fin, m->sell_wn, m->sell_wo, true);
+        launch_amul_dot(s, m->amul_variant, a, ws, fin, m->sell_wn, m->sell_wo, true);
         if (ev) record(m, *ev, slot * 6 + 3, s);
-        if (m->external_comm) SPUMA_TRY(halo_exchange(m, m->ws.pA, m->ws.xr, s));
+        if (m->external_comm) SPUMA_TRY(halo_exchange(m, ws.pA, ws.xr, s));
         else SPUMA_CUDA(cudaStreamWaitEvent(s, m->ev_join, 0));
-        launch_iface_rows(s, a, m->ws, m->d_ifRows, m->n_ifRows);
+        launch_iface_rows(s, a, ws, m->d_ifRows, m->n_ifRows);
         m->stats.kernel_launches += 1;
     } else {
-        SPUMA_TRY(halo_exchange(m, m->ws.pA, m->ws.xr, s));
+        SPUMA_TRY(halo_exchange(m, ws.pA, ws.xr, s));
         if (ev) record(m, *ev, slot * 6 + 2, s);
-        launch_amul_dot(s, m->amul_variant, a, m->ws, fin, m->sell_wn, m->sell_wo);
+        launch_amul_dot(s, m->amul_variant, a, ws, fin, m->sell_wn, m->sell_wo);
         if (ev) record(m, *ev, slot * 6 + 3, s);
     }
     if (!fin) SPUMA_TRY(reduce_finalize(m, 3, s));
     if (ev) record(m, *ev, slot * 6 + 4, s);
-    launch_update(s, m->grid, a, m->ws, fin);
+    launch_update(s, m->grid, a, ws, fin, psi_mode);
     if (ev) record(m, *ev, slot * 6 + 5, s);
     if (!fin) SPUMA_TRY(reduce_finalize(m, 4, s));
     m->stats.kernel_launches += 3;
     return SPUMA_OK;
 }
+
+// iterations per captured batch: even when psi updates are deferred (pairs must not straddle batches)
+int batch_eff(spuma_mesh m) { return m->batch + ((m->defer_psi && (m->batch & 1)) ? 1 : 0); }
 
 void destroy_graphs(spuma_mesh m)
 {
@@ -362,7 +374,7 @@ void destroy_graphs(spuma_mesh m)
 
 spuma_status build_graphs(spuma_mesh m)
 {
-    if (m->gexec[0] && m->gexec_timed == m->timing && m->gexec_batch == m->batch) return SPUMA_OK;
+    if (m->gexec[0] && m->gexec_timed == m->timing && m->gexec_batch == batch_eff(m)) return SPUMA_OK;
     destroy_graphs(m);
     const uint64_t launches_before = m->stats.kernel_launches;
     for (int g = 0; g < 2; ++g) {
@@ -377,7 +389,8 @@ spuma_status build_graphs(spuma_mesh m)
         spuma_status st = SPUMA_OK;
         // timing samples the first iteration of every batch (6 event nodes per batch keep the
         // capture's launch gaps unperturbed; ~100 samples per 1600-iteration solve)
-        for (int k = 0; k < m->batch && st == SPUMA_OK; ++k) st = enqueue_iteration(m, m->stream, k == 0 ? ev : nullptr, 0);
+        for (int k = 0; k < batch_eff(m) && st == SPUMA_OK; ++k)
+            st = enqueue_iteration(m, m->stream, k == 0 ? ev : nullptr, k);
         cudaError_t e = cudaStreamEndCapture(m->stream, &graph);
         if (st != SPUMA_OK) {
             if (graph) cudaGraphDestroy(graph);
@@ -390,7 +403,7 @@ spuma_status build_graphs(spuma_mesh m)
     }
     m->stats.kernel_launches = launches_before;  // capture launches nothing
     m->gexec_timed = m->timing;
-    m->gexec_batch = m->batch;
+    m->gexec_batch = batch_eff(m);
     return SPUMA_OK;
 }
 
@@ -452,7 +465,7 @@ void spuma_free(spuma_mesh m)
                      m->d_bis_owner, m->d_bStart, m->d_bFace, m->d_bAllStart, m->d_bAllFace, m->d_face_flip,
                      m->d_bphi, m->d_bflux, m->d_face_b, m->d_face_c, m->d_ifStart, m->d_ifIdx, m->d_if_cell, m->d_ifMask, m->d_ifRows,
                      m->d_sendbuf, m->d_cell_a, m->d_cell_b, m->d_cell_c, m->d_cell_d, m->d_cell_e, m->d_cell_t,
-                     m->d_face_a, m->d_face_t, m->d_iface_a, m->ws.wA, m->ws.rA, m->ws.pA, m->ws.rD, m->ws.sumA,
+                     m->d_face_a, m->d_face_t, m->d_iface_a, m->ws.wA, m->ws.rA, m->ws.pA, m->ws.pA2, m->ws.rD, m->ws.sumA,
                      m->ws.xr, m->ws.part, m->ws.scal, m->ws.ptrs};
     for (void* p : dptrs)
         if (p) cudaFree(p);
@@ -705,6 +718,8 @@ static spuma_status mesh_create_impl(const spuma_mesh_desc* d, spuma_mesh m)
     SPUMA_TRY(dalloc(&m->ws.wA, N + 1));
     SPUMA_TRY(dalloc(&m->ws.rA, N + 1));
     SPUMA_TRY(dalloc(&m->ws.pA, N + 1));
+    SPUMA_TRY(dalloc(&m->ws.pA2, N + 1));
+    m->ws.pA_prev = m->ws.pA;
     SPUMA_TRY(dalloc(&m->ws.rD, N + 1));
     SPUMA_TRY(dalloc(&m->ws.sumA, N + 1));
     SPUMA_TRY(dalloc(&m->ws.xr, m->n_iface));
@@ -937,7 +952,7 @@ spuma_status spuma_pcg_solve(spuma_mesh m, const spuma_scalar* diag, const spuma
         SPUMA_CUDA(cudaStreamSynchronize(s));
         int it = 0;
         while (!m->h_scal[0].done) {
-            SPUMA_TRY(enqueue_iteration(m, s, nullptr, 0));
+            SPUMA_TRY(enqueue_iteration(m, s, nullptr, it));
             SPUMA_CUDA(cudaMemcpyAsync(&m->h_scal[0], m->ws.scal, sizeof(DevScal), cudaMemcpyDeviceToHost, s));
             SPUMA_CUDA(cudaStreamSynchronize(s));
             if (++it > ctl->max_iter + 1) return set_error(SPUMA_ERR_STATE, "PCG loop did not terminate");
@@ -967,15 +982,20 @@ spuma_status spuma_pcg_solve(spuma_mesh m, const spuma_scalar* diag, const spuma
             done = m->h_scal[pg].done;
         }
         ++b;
-        if (b > 2 + (ctl->max_iter + m->batch - 1) / m->batch + 1)
+        if (b > 2 + (ctl->max_iter + m->gexec_batch - 1) / m->gexec_batch + 1)
             return set_error(SPUMA_ERR_STATE, "PCG batch loop did not terminate");
     }
     SPUMA_CUDA(cudaStreamSynchronize(s));
     if (m->timing && b > 0) SPUMA_TRY(account_timing(m, (b - 1) & 1, m->h_scal[(b - 1) & 1].n - prev_n));
-    m->stats.kernel_launches += launched_batches * (uint64_t)m->batch * launches_per_iteration(m);
+    m->stats.kernel_launches += launched_batches * (uint64_t)m->gexec_batch * launches_per_iteration(m);
     }
     DevScal fs;
     SPUMA_CUDA(cudaMemcpy(&fs, m->ws.scal, sizeof(DevScal), cudaMemcpyDeviceToHost));
+    if (m->defer_psi && (fs.n & 1)) {  // the last iteration's psi update is still pending
+        launch_psi_flush(s, m->N, m->ws);
+        m->stats.kernel_launches += 1;
+        SPUMA_CUDA(cudaStreamSynchronize(s));
+    }
     SPUMA_CUDA(cudaGetLastError());
     perf->initial_residual = fs.init;
     perf->final_residual = fs.fin;
@@ -1121,6 +1141,10 @@ spuma_status spuma_set_option(spuma_mesh m, int option, int value)
 {
     if (!m) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "mesh is NULL");
     switch (option) {
+    case SPUMA_OPT_DEFER_PSI:
+        if (m->defer_psi != (value != 0)) destroy_graphs(m);
+        m->defer_psi = value != 0;
+        return SPUMA_OK;
     case SPUMA_OPT_PDL:
         if (g_use_pdl != (value != 0)) destroy_graphs(m);
         g_use_pdl = value != 0;

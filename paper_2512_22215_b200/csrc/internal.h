@@ -19,7 +19,7 @@ constexpr int kPhases = 4;         // timing phases (spuma_stats.phase_ms)
 // Device-resident PCG state (A6-A12).  Written only by the finalisation code
 // (last CTA of a reduction kernel, or the 1-CTA finalise kernel when P > 1).
 struct DevScal {
-    double wArA, wArAold, wApA, alpha, beta;
+    double wArA, wArAold, wApA, alpha, beta, alpha_prev;
     double normFactor, init, fin, xbar;
     double tol, rel_tol;
     double rank_part[4];   // this rank's partial sums of the current reduction (P > 1)
@@ -62,6 +62,8 @@ struct MeshArgs {
 
 struct Workspace {
     double *wA, *rA, *pA, *rD, *sumA;
+    double* pA_prev;   // direction of the previous iteration (== pA unless psi updates are deferred)
+    double* pA2;       // second direction buffer (deferred psi updates)
     double* xr;        // [n_iface] x_remote received from the neighbours
     double* part;      // [kMaxPartials * grid] per-CTA partials
     DevScal* scal;
@@ -137,7 +139,8 @@ struct spuma_mesh_s {
     // captured iteration batches (ping-pong) and timing events
     int batch = 16;
     int small_max_cells = 8192;  // single-CTA solve at or below this many cells (1 rank)
-    int amul_variant = 8;  // ELL + coefficient copy (falls back to 6 -> 5 when the mesh is not uniform)
+    int amul_variant = 8;
+    bool defer_psi = true;  // psi += alpha pA applied every second iteration (same rounding, fewer bytes)  // ELL + coefficient copy (falls back to 6 -> 5 when the mesh is not uniform)
     bool timing = false;
     cudaGraphExec_t gexec[2] = {nullptr, nullptr};
     bool gexec_timed = false;
@@ -220,7 +223,9 @@ void launch_gather_signed(cudaStream_t s, int n, const int* idx, const signed ch
 void launch_scatter_signed(cudaStream_t s, int n, const int* idx, const signed char* flip, const double* in,
                            double* out);
 constexpr int kPad = 8;  // padding elements on internal arrays (16-byte TMA windows may overrun by <= 3)
-void launch_update(cudaStream_t s, int grid, const MeshArgs& a, const Workspace& w, bool fin);
+void launch_update(cudaStream_t s, int grid, const MeshArgs& a, const Workspace& w, bool fin, int psi_mode = 0);
+// psi_mode: 0 psi += alpha pA; 1 defer (psi untouched); 2 psi = (psi + alpha_prev pA_prev) + alpha pA
+void launch_psi_flush(cudaStream_t s, int N, const Workspace& w);  // psi += alpha_prev pA (pending update)
 // P > 1: finalise from the gathered rank partials ([n_ranks][4], rank order)
 void launch_finalize(cudaStream_t s, int stage, const double* gathered, int n_ranks, const Workspace& w);
 void launch_scal_init(cudaStream_t s, const Workspace& w, const spuma_solver_controls& c, int n_ranks);

@@ -135,6 +135,7 @@ __device__ void finalize(DevScal* s, int stage, const double* g)
         s->wArAold = s->wArA;
         s->wArA = g[0];
         s->beta = s->wArA / s->wArAold;
+        s->alpha_prev = s->alpha;  // a deferred psi update of this iteration uses it
         break;
     }
     }
@@ -550,7 +551,8 @@ __global__ void __launch_bounds__(kThreads) k_direction(int N, Workspace w)
     const int np = N >> 1;
     const double2* __restrict__ rD2 = reinterpret_cast<const double2*>(w.rD);
     const double2* __restrict__ rA2 = reinterpret_cast<const double2*>(w.rA);
-    double2* __restrict__ pA2 = reinterpret_cast<double2*>(w.pA);
+    const double2* pprev = reinterpret_cast<const double2*>(w.pA_prev);  // may alias pA (in place)
+    double2* pA2 = reinterpret_cast<double2*>(w.pA);
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < np; i += gridDim.x * blockDim.x) {
         const double2 d = rD2[i], r = rA2[i];
         double2 q;
@@ -558,7 +560,7 @@ __global__ void __launch_bounds__(kThreads) k_direction(int N, Workspace w)
             q.x = d.x * r.x;
             q.y = d.y * r.y;
         } else {
-            const double2 p = pA2[i];
+            const double2 p = pprev[i];
             q.x = d.x * r.x + beta * p.x;
             q.y = d.y * r.y + beta * p.y;
         }
@@ -566,7 +568,7 @@ __global__ void __launch_bounds__(kThreads) k_direction(int N, Workspace w)
     }
     if ((N & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
         const int c = N - 1;
-        w.pA[c] = first ? w.rD[c] * w.rA[c] : w.rD[c] * w.rA[c] + beta * w.pA[c];
+        w.pA[c] = first ? w.rD[c] * w.rA[c] : w.rD[c] * w.rA[c] + beta * w.pA_prev[c];
     }
     pdl_trigger();
 }
@@ -625,27 +627,40 @@ __global__ void __launch_bounds__(V == 3 ? tma::kBlock : kThreads, amul_min_ctas
 }
 
 // A9 + A10: psi += alpha pA; rA -= alpha wA; partials (rD rA) rA and |rA|
-__global__ void __launch_bounds__(kThreads) k_update(int N, Workspace w, int fin)
+// psi_mode 0: psi += alpha pA; 1: psi left for the next iteration (deferred); 2: the
+// deferred pair, psi = (psi + alpha_prev pA_prev) + alpha pA -- the same two roundings as
+// two separate updates, so every iterate is bitwise unchanged.
+__global__ void __launch_bounds__(kThreads) k_update(int N, Workspace w, int fin, int psi_mode)
 {
     pdl_wait();
     if (w.scal->done) return;
     const DevPtrs p = *w.ptrs;
-    const double alpha = w.scal->alpha;
+    const double alpha = w.scal->alpha, alpha_prev = w.scal->alpha_prev;
     double v[2] = {0.0, 0.0};
     const int np = N >> 1;
     double2* __restrict__ psi2 = reinterpret_cast<double2*>(p.psi);
     double2* __restrict__ rA2 = reinterpret_cast<double2*>(w.rA);
     const double2* __restrict__ pA2 = reinterpret_cast<const double2*>(w.pA);
+    const double2* __restrict__ pP2 = reinterpret_cast<const double2*>(w.pA_prev);
     const double2* __restrict__ wA2 = reinterpret_cast<const double2*>(w.wA);
     const double2* __restrict__ rD2 = reinterpret_cast<const double2*>(w.rD);
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < np; i += gridDim.x * blockDim.x) {
-        double2 x = psi2[i], r = rA2[i];
-        const double2 pp = pA2[i], ww = wA2[i], d = rD2[i];
-        x.x = x.x + alpha * pp.x;
-        x.y = x.y + alpha * pp.y;
+        double2 r = rA2[i];
+        const double2 ww = wA2[i], d = rD2[i];
+        if (psi_mode != 1) {
+            double2 x = psi2[i];
+            const double2 pp = pA2[i];
+            if (psi_mode == 2) {
+                const double2 q = pP2[i];
+                x.x = x.x + alpha_prev * q.x;
+                x.y = x.y + alpha_prev * q.y;
+            }
+            x.x = x.x + alpha * pp.x;
+            x.y = x.y + alpha * pp.y;
+            psi2[i] = x;
+        }
         r.x = r.x - alpha * ww.x;
         r.y = r.y - alpha * ww.y;
-        psi2[i] = x;
         rA2[i] = r;
         v[0] += (d.x * r.x) * r.x;
         v[0] += (d.y * r.y) * r.y;
@@ -654,7 +669,11 @@ __global__ void __launch_bounds__(kThreads) k_update(int N, Workspace w, int fin
     }
     if ((N & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
         const int c = N - 1;
-        p.psi[c] = p.psi[c] + alpha * w.pA[c];
+        if (psi_mode != 1) {
+            double x = p.psi[c];
+            if (psi_mode == 2) x = x + alpha_prev * w.pA_prev[c];
+            p.psi[c] = x + alpha * w.pA[c];
+        }
         const double r = w.rA[c] - alpha * w.wA[c];
         w.rA[c] = r;
         v[0] += (w.rD[c] * r) * r;
@@ -1178,10 +1197,25 @@ void launch_amul_dot(cudaStream_t s, int variant, const MeshArgs& a, const Works
     }
 }
 
-void launch_update(cudaStream_t s, int grid, const MeshArgs& a, const Workspace& w, bool fin)
+void launch_update(cudaStream_t s, int grid, const MeshArgs& a, const Workspace& w, bool fin, int psi_mode)
 {
     (void)grid;
-    launch_hot(k_update, grid_for(k_update, a.N, 2), kThreads, s, a.N, w, fin ? 1 : 0);
+    launch_hot(k_update, grid_for(k_update, a.N, 2), kThreads, s, a.N, w, fin ? 1 : 0, psi_mode);
+}
+
+// the pending half of a deferred pair when the loop stopped after an even-indexed iteration
+__global__ void k_psi_flush(int N, Workspace w)
+{
+    const DevPtrs p = *w.ptrs;
+    const double a = w.scal->alpha_prev;
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < N; c += gridDim.x * blockDim.x)
+        p.psi[c] = p.psi[c] + a * w.pA[c];
+}
+
+void launch_psi_flush(cudaStream_t s, int N, const Workspace& w)
+{
+    if (N <= 0) return;
+    k_psi_flush<<<grid_for(k_psi_flush, N), kThreads, 0, s>>>(N, w);
 }
 
 void launch_surface_integrate(cudaStream_t s, const MeshArgs& a, const double* phi, const int* bStart,

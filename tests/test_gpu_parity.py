@@ -443,3 +443,21 @@ def test_disconnected_components_renumbered():
     fm = O.renumber_faces(perm, owner, nbr)[2]
     ref = O.amul(rm, gen.permute_cell_field(diag, perm), upper[fm], gen.permute_cell_field(x, perm))[perm]
     assert np.array_equal(y.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("iters", [None, 1, 2, 7, 8])
+def test_deferred_psi_updates_are_bitwise_neutral(iters):
+    """SPUMA_OPT_DEFER_PSI pairs two psi updates into one pass, (psi + a1 p1) + a2 p2: the same
+    roundings in the same order, so psi and perf are bitwise those of per-iteration updates
+    (odd iteration counts exercise the final flush)."""
+    m = gen.permute(gen.perturbed(14, 0.2), seed=12)
+    g, b = gen.gamma_lognormal(m), gen.rhs(m)
+    ctl = (1e-8, 0.0, 5000, 0) if iters is None else (0.0, 0.0, iters, iters)
+    out = []
+    for defer in (0, 1):
+        h = P.Mesh.from_mesh(m)
+        h.set_option(P.spuma.OPT_SMALL_SOLVE_MAX_CELLS, 0)
+        h.set_option(P.spuma.OPT_DEFER_PSI, defer)
+        out.append(gpu_solve_case(m, g, b, 0, ctl, handle=h)[:2])
+    assert out[0][1] == out[1][1]
+    assert np.array_equal(out[0][0], out[1][0])
