@@ -317,6 +317,9 @@ def run_gpu(args, rank, world, local_rank):
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         cpu = cpu_baseline(args.n, args.cpu_iters)
+        # the paper's coefficient of equivalence (Eq. 1) in its single-core form:
+        # how many oracle cores one B200 is worth on this workload
+        cpu["coe_cores_per_gpu"] = value / cpu["value"]
     traffic = load_traffic(cfg["workload"])
     cfg.update({"global_cells": n_global, "faces_per_gpu": F, "parallelism": f"dd{world}",
                 "iterations_per_step": iters / max(len(perfs), 1), "l2": "inputs larger than L2 (no flush)",
