@@ -198,6 +198,21 @@ def cavity2d(n: int = 20) -> Mesh:
                              ("frontAndBack", ["zmin", "zmax"])], [ZERO_GRADIENT, ZERO_GRADIENT, EMPTY])
 
 
+def affine(mesh: Mesh, A, t=(0.0, 0.0, 0.0)) -> Mesh:
+    """Map the geometry by x -> A x + t (an affine, e.g. sheared, mesh): centres map directly,
+    vector areas by the cofactor det(A) A^-T, volumes by det(A).  Input generation only."""
+    A = np.asarray(A, np.float64)
+    t = np.asarray(t, np.float64)
+    cof = np.linalg.det(A) * np.linalg.inv(A).T
+    tr = lambda X: np.ascontiguousarray(X @ A.T + t)
+    vs = lambda S: np.ascontiguousarray(S @ cof.T)
+    patches = [replace(p, Sf=vs(p.Sf), magSf=np.linalg.norm(vs(p.Sf), axis=1), Cf=tr(p.Cf),
+                       neighbour_C=None if p.neighbour_C is None else tr(p.neighbour_C)) for p in mesh.patches]
+    Sf = vs(mesh.Sf)
+    return replace(mesh, Sf=Sf, magSf=np.linalg.norm(Sf, axis=1), Cf=tr(mesh.Cf), C=tr(mesh.C),
+                   V=mesh.V * np.linalg.det(A), patches=patches)
+
+
 def set_kind(mesh: Mesh, name: str, kind: int, value: Optional[np.ndarray] = None) -> Mesh:
     ps = []
     for p in mesh.patches:

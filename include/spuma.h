@@ -195,16 +195,33 @@ spuma_status spuma_surface_integrate(spuma_mesh m, const spuma_scalar* phi, cons
                                      const spuma_scalar* V, spuma_scalar* out);
 
 /* fvMatrix::flux of the assembled fvm::laplacian(gamma, psi) (lduMatrix::faceH):
- *   internal  flux[f] = upper[f] psi[N] - upper[f] psi[P]
+ *   internal  flux[f] = upper[f] psi[N] - upper[f] psi[P]  (+ corr_flux[f])
  *   boundary  internalCoeffs psi_P - boundaryCoeffs (x psi_remote on processor faces):
- *             fixedValue (g|S|)(-delta) psi_P - (-(g|S|))(delta p_b); zeroGradient/empty 0.
- * gamma / patch_value as given to spuma_assemble_laplacian; flux [n_faces] and patch_flux may be
- * NULL; if phi (and/or patch_phi) is given the SIMPLE correction phi -= flux is applied in place.
- * n_ranks > 1: collective (psi and gamma halo).  iface_coeffs is reserved (may be NULL). */
+ *             fixedValue (g|S|)(-delta) psi_P - (-(g|S|))(delta p_b); zeroGradient/empty 0
+ *             (+ patch_corr_flux).
+ * gamma / patch_value as given to spuma_assemble_laplacian; corr_flux / patch_corr_flux: the
+ * faceFluxCorrection of spuma_laplacian_correction (NULL: none); flux [n_faces] and patch_flux
+ * may be NULL; if phi (and/or patch_phi) is given the SIMPLE correction phi -= flux is applied in
+ * place.  n_ranks > 1: collective (psi and gamma halo). */
 spuma_status spuma_face_flux(spuma_mesh m, const spuma_scalar* gamma, const spuma_scalar* const* patch_value,
-                             const spuma_scalar* upper, const spuma_scalar* iface_coeffs, const spuma_scalar* psi,
-                             spuma_scalar* flux, spuma_scalar* const* patch_flux, spuma_scalar* phi,
-                             spuma_scalar* const* patch_phi);
+                             const spuma_scalar* upper, const spuma_scalar* psi, const spuma_scalar* corr_flux,
+                             const spuma_scalar* const* patch_corr_flux, spuma_scalar* flux,
+                             spuma_scalar* const* patch_flux, spuma_scalar* phi, spuma_scalar* const* patch_phi);
+
+/* Explicit non-orthogonal correction of "Gauss linear corrected" (laplacianSchemes P:1135,
+ * snGradSchemes corrected P:1145, gradSchemes Gauss linear P:1112; reading Q21):
+ *   grad p   Gauss linear: (sum of Sf p_f over the faces of c) / V, p_f = w (p_P - p_N) + p_N,
+ *            boundary p_b = p_P (zeroGradient), the patch value (fixedValue), the interpolate
+ *            with the remote cell (processor)
+ *   corr_f   (gamma_f |S|) (corrVec . (w (grad_P - grad_N) + grad_N)),
+ *            corrVec = Sf/|Sf| - (C_N - C_P) nonOrthDeltaCoeff (0 on non-coupled patches)
+ *   source  -= V fvc::div(corr)   (read-modified-written, like spuma_assemble_laplacian's)
+ * p, V [n_cells]; corr_flux [n_faces] / patch_corr_flux (outputs, may be NULL) for
+ * spuma_face_flux.  n_ranks > 1: collective (p, gamma and gradient halo). */
+spuma_status spuma_laplacian_correction(spuma_mesh m, const spuma_scalar* gamma,
+                                        const spuma_scalar* const* patch_value, const spuma_scalar* p,
+                                        const spuma_scalar* V, spuma_scalar* source, spuma_scalar* corr_flux,
+                                        spuma_scalar* const* patch_corr_flux);
 
 /* ---------------- diagnostics (parity tests, benchmark harness) ---------------- */
 

@@ -89,6 +89,8 @@ def _L():
             lib.or_pcg.restype = ci
             lib.or_surface_integrate.argtypes = [ci, ci, vp, vp, vp, ci] + [vp] * 5
             lib.or_face_flux.argtypes = [ci] + [vp] * 6 + [ci] + [vp] * 11
+            lib.or_gauss_grad.argtypes = [ci, ci] + [vp] * 5 + [ci] + [vp] * 9
+            lib.or_nonorth_flux.argtypes = [ci] + [vp] * 10 + [ci] + [vp] * 11
             lib.or_dense_from_ldu.argtypes = [ci, ci] + [vp] * 6
             lib.or_dense_matvec.argtypes = [ci, vp, vp, vp]
             lib.or_dense_solve.argtypes = [ci, vp, vp, vp]
@@ -412,6 +414,73 @@ def face_flux(mesh: gen.Mesh, upper, psi, gamma=None, geo: Optional[Geometry] = 
         out.append(bflux[off:off + p.n_faces].copy())
         off += p.n_faces
     return flux, out
+
+
+# --------------------------------------------------------------------------- O10
+def _bfield(mesh, attr, dtype=np.float64, width=1):
+    xs = []
+    for p in mesh.patches:
+        v = getattr(p, attr)
+        xs.append(np.zeros((p.n_faces, width) if width > 1 else p.n_faces, dtype) if v is None else np.asarray(v, dtype))
+    if not xs:
+        return np.zeros(0, dtype)
+    return np.ascontiguousarray(np.concatenate(xs), dtype=dtype)
+
+
+def _proc_vals(mesh, vals, width=1):
+    xs, k = [], 0
+    for p in mesh.patches:
+        if p.kind == PROCESSOR and vals is not None:
+            xs.append(np.asarray(vals[k], np.float64).reshape(p.n_faces, width) if width > 1 else np.asarray(vals[k], np.float64))
+            k += 1
+        else:
+            xs.append(np.zeros((p.n_faces, width)) if width > 1 else np.zeros(p.n_faces))
+    return _f64(np.concatenate(xs) if xs else np.zeros(0))
+
+
+def gauss_grad(mesh: gen.Mesh, p, geo: Optional[Geometry] = None, p_remote=None) -> np.ndarray:
+    """Gauss linear cell gradient of p (gaussGrad): [N, 3]."""
+    lib = _L()
+    geo = geo or geometry(mesh)
+    G = np.empty((mesh.n_cells, 3))
+    bkind = _i32(np.concatenate([np.full(q.n_faces, q.kind, np.int32) for q in mesh.patches]) if mesh.patches else np.zeros(0))
+    bcells, bSf, bval, bown = _bcat(mesh, "face_cells", np.int32), _bfield(mesh, "Sf", width=3), _bcat(mesh, "value", np.float64), _bcat(mesh, "is_owner", np.int8)
+    bpr = _proc_vals(mesh, p_remote)
+    own, nbr, Sf, pp, V = _i32(mesh.owner), _i32(mesh.neighbour), _f64(mesh.Sf), _f64(p), _f64(mesh.V)
+    lib.or_gauss_grad(mesh.n_cells, mesh.n_faces, _p(own), _p(nbr), _p(Sf), _p(geo.weights), _p(pp), bkind.shape[0],
+                      _p(bkind), _p(bcells), _p(bSf), _p(bval), _p(geo.bweight), _p(bown), _p(bpr), _p(V), _p(G))
+    return G
+
+
+def nonorth_correction(mesh: gen.Mesh, p, gamma=None, geo: Optional[Geometry] = None, gamma_remote=None,
+                       p_remote=None, G=None, G_remote=None):
+    """Explicit non-orthogonal correction of Gauss linear corrected:
+    correction flux gammaMagSf * (corrVec . interpolate(grad p)) and the source change
+    -V fvc::div(correction flux).  Returns (cflux [F], per-patch cflux, dsource [N], G)."""
+    lib = _L()
+    geo = geo or geometry(mesh)
+    if G is None:
+        G = gauss_grad(mesh, p, geo, p_remote)
+    F = mesh.n_faces
+    cflux = np.empty(F)
+    bkind = _i32(np.concatenate([np.full(q.n_faces, q.kind, np.int32) for q in mesh.patches]) if mesh.patches else np.zeros(0))
+    bcells, bSf, bmag = _bcat(mesh, "face_cells", np.int32), _bfield(mesh, "Sf", width=3), _bcat(mesh, "magSf", np.float64)
+    bown, bnC = _bcat(mesh, "is_owner", np.int8), _bfield(mesh, "neighbour_C", width=3)
+    bgr, bGr = _proc_vals(mesh, gamma_remote), _proc_vals(mesh, G_remote, width=3)
+    bcf = np.zeros(bkind.shape[0])
+    own, nbr, Sf, mag, C = _i32(mesh.owner), _i32(mesh.neighbour), _f64(mesh.Sf), _f64(mesh.magSf), _f64(mesh.C)
+    g = None if gamma is None else _f64(gamma)
+    Gc = _f64(G)
+    lib.or_nonorth_flux(F, _p(own), _p(nbr), _p(Sf), _p(mag), _p(C), _p(geo.delta), _p(geo.weights), _p(g), _p(Gc),
+                        _p(cflux), bkind.shape[0], _p(bkind), _p(bcells), _p(bSf), _p(bmag), _p(geo.bdelta),
+                        _p(geo.bweight), _p(bown), _p(bnC), _p(bgr), _p(bGr), _p(bcf))
+    pcf, off = [], 0
+    for q in mesh.patches:
+        pcf.append(bcf[off:off + q.n_faces].copy())
+        off += q.n_faces
+    div = surface_integrate(mesh, cflux, pcf)
+    dsource = -(_f64(mesh.V) * div)
+    return cflux, pcf, dsource, G
 
 
 # --------------------------------------------------------------------------- O7

@@ -20,6 +20,7 @@
  *   O6 PCG          or_pcg (P >= 1 domains, O8 when P > 1)                P:961, P:1033-1041 (pcgDiag)
  *   O7 dense        or_dense_from_ldu, or_dense_matvec, or_dense_solve    brute force for N <= 64
  *   O9 around       or_surface_integrate, or_face_flux
+ *   O10 non-orth    or_gauss_grad, or_nonorth_flux                        P:1112, P:1135, P:1145 (Gauss linear corrected)
  *
  * Pins (tests/test_oracle_*.py, -m "not gpu"): SPEC chain examples,
  * closed-form Poisson eigenmodes (Dirichlet / Neumann) and linear exactness,
@@ -430,6 +431,103 @@ void or_face_flux(int n_faces, const int* owner, const int* neighbour, const dou
             const double gms = gf * bmagSf[b];
             bflux[b] = (gms * (-bdelta[b])) * psi[P] - (((-gms) * bdelta[b]) * bpsi_r[b]);
         }
+    }
+}
+
+/* ------------------------------------------------------------------------- */
+/* O10 explicit non-orthogonal correction of "Gauss linear corrected"          */
+/* (laplacianSchemes P:1135, snGradSchemes corrected P:1145, gradSchemes      */
+/* default Gauss linear P:1112): [OF] gaussLaplacianScheme::fvmLaplacian,      */
+/* correctedSnGrad::fullGradCorrection, gaussGrad::gradf,                     */
+/* surfaceInterpolation::makeNonOrthCorrectionVectors.  Reading Q21.          */
+/* ------------------------------------------------------------------------- */
+
+/* gaussGrad (Gauss linear): p_f = w (p_P - p_N) + p_N on internal faces; G[owner] += Sf p_f,
+ * G[neighbour] -= Sf p_f in face order; then every non-empty boundary face in (patch, face)
+ * order adds bSf p_b, with p_b = p_P (zeroGradient), the patch value (fixedValue) or the
+ * global-orientation interpolate with the remote cell (processor); then G /= V.
+ * G is [3 N] (x, y, z per cell). */
+void or_gauss_grad(int n_cells, int n_faces, const int* owner, const int* neighbour, const double* Sf,
+                   const double* weights, const double* p, int n_bfaces, const int* bkind, const int* bcells,
+                   const double* bSf, const double* bvalue, const double* bweight, const signed char* bis_owner,
+                   const double* bp_r, const double* V, double* G)
+{
+    double* bp = (double*)malloc(sizeof(double) * (size_t)(n_bfaces > 0 ? n_bfaces : 1));
+    for (int b = 0; b < n_bfaces; ++b) {
+        const double pP = p[bcells[b]];
+        if (bkind[b] == OR_FIXED_VALUE) bp[b] = bvalue[b];
+        else if (bkind[b] == OR_PROCESSOR) {
+            const double pO = bis_owner[b] ? pP : bp_r[b];
+            const double pN = bis_owner[b] ? bp_r[b] : pP;
+            bp[b] = bweight[b] * (pO - pN) + pN;
+        } else bp[b] = pP;
+    }
+    for (int i = 0; i < 3 * n_cells; ++i) G[i] = 0.0;
+    for (int f = 0; f < n_faces; ++f) {
+        const double pf = weights[f] * (p[owner[f]] - p[neighbour[f]]) + p[neighbour[f]];
+        for (int k = 0; k < 3; ++k) {
+            G[3 * owner[f] + k] += Sf[3 * f + k] * pf;
+            G[3 * neighbour[f] + k] -= Sf[3 * f + k] * pf;
+        }
+    }
+    for (int b = 0; b < n_bfaces; ++b)
+        if (bkind[b] != OR_EMPTY)
+            for (int k = 0; k < 3; ++k) G[3 * bcells[b] + k] += bSf[3 * b + k] * bp[b];
+    for (int c = 0; c < n_cells; ++c)
+        for (int k = 0; k < 3; ++k) G[3 * c + k] /= V[c];
+    free(bp);
+}
+
+/* nonOrthCorrectionVectors: corr = Sf/|Sf| - (C_N - C_P) nonOrthDeltaCoeff (per component) */
+static void or_corr_vec(const double* S, double magS, const double* CP, const double* CN, double delta, double* cv)
+{
+    for (int k = 0; k < 3; ++k) cv[k] = S[k] / magS - (CN[k] - CP[k]) * delta;
+}
+
+/* correction flux gammaMagSf * (corrVec . linearInterpolate(grad p)) on internal faces (face
+ * orientation) and processor faces (outward: the owner side carries the global value, the other
+ * side its negation); 0 on non-coupled boundary faces. */
+void or_nonorth_flux(int n_faces, const int* owner, const int* neighbour, const double* Sf, const double* magSf,
+                     const double* C, const double* delta, const double* weights, const double* gamma,
+                     const double* G, double* cflux, int n_bfaces, const int* bkind, const int* bcells,
+                     const double* bSf, const double* bmagSf, const double* bdelta, const double* bweight,
+                     const signed char* bis_owner, const double* bnC, const double* bgamma_r, const double* bG_r,
+                     double* bcflux)
+{
+    for (int f = 0; f < n_faces; ++f) {
+        const int P = owner[f], N = neighbour[f];
+        double cv[3], g[3];
+        or_corr_vec(Sf + 3 * f, magSf[f], C + 3 * P, C + 3 * N, delta[f], cv);
+        for (int k = 0; k < 3; ++k) g[k] = weights[f] * (G[3 * P + k] - G[3 * N + k]) + G[3 * N + k];
+        const double corr = cv[0] * g[0] + cv[1] * g[1] + cv[2] * g[2];
+        double gf = 1.0;
+        if (gamma) gf = weights[f] * (gamma[P] - gamma[N]) + gamma[N];
+        cflux[f] = (gf * magSf[f]) * corr;
+    }
+    for (int b = 0; b < n_bfaces; ++b) {
+        bcflux[b] = 0.0;
+        if (bkind[b] != OR_PROCESSOR) continue;
+        const int L = bcells[b];
+        const int own = bis_owner[b];
+        double S[3], cv[3], g[3];
+        for (int k = 0; k < 3; ++k) S[k] = own ? bSf[3 * b + k] : -bSf[3 * b + k];
+        const double* CL = C + 3 * L;
+        const double* CR = bnC + 3 * b;
+        or_corr_vec(S, bmagSf[b], own ? CL : CR, own ? CR : CL, bdelta[b], cv);
+        for (int k = 0; k < 3; ++k) {
+            const double gO = own ? G[3 * L + k] : bG_r[3 * b + k];
+            const double gN = own ? bG_r[3 * b + k] : G[3 * L + k];
+            g[k] = bweight[b] * (gO - gN) + gN;
+        }
+        const double corr = cv[0] * g[0] + cv[1] * g[1] + cv[2] * g[2];
+        double gf = 1.0;
+        if (gamma) {
+            const double gO = own ? gamma[L] : bgamma_r[b];
+            const double gN = own ? bgamma_r[b] : gamma[L];
+            gf = bweight[b] * (gO - gN) + gN;
+        }
+        const double q = (gf * bmagSf[b]) * corr;
+        bcflux[b] = own ? q : -q;
     }
 }
 

@@ -463,7 +463,8 @@ void spuma_free(spuma_mesh m)
                      m->d_perm, m->d_face_map, m->d_delta, m->d_weights, m->d_magSf, m->d_bkind, m->d_bcell,
                      m->d_bproc, m->d_bmagSf, m->d_bdelta, m->d_bweight, m->d_bvalue, m->d_bgamma_r,
                      m->d_bis_owner, m->d_bStart, m->d_bFace, m->d_bAllStart, m->d_bAllFace, m->d_face_flip,
-                     m->d_bphi, m->d_bflux, m->d_face_b, m->d_face_c, m->d_ifStart, m->d_ifIdx, m->d_if_cell, m->d_ifMask, m->d_ifRows,
+                     m->d_bphi, m->d_bflux, m->d_face_b, m->d_face_c, m->d_Sf, m->d_C, m->d_corrvec, m->d_bSf,
+                     m->d_bnC, m->d_G, m->d_Gr, m->d_pr, m->d_bcflux, m->d_face_d, m->d_div, m->d_cell_v, m->d_ifStart, m->d_ifIdx, m->d_if_cell, m->d_ifMask, m->d_ifRows,
                      m->d_sendbuf, m->d_cell_a, m->d_cell_b, m->d_cell_c, m->d_cell_d, m->d_cell_e, m->d_cell_t,
                      m->d_face_a, m->d_face_t, m->d_iface_a, m->ws.wA, m->ws.rA, m->ws.pA, m->ws.pA2, m->ws.rD, m->ws.sumA,
                      m->ws.xr, m->ws.part, m->ws.scal, m->ws.ptrs};
@@ -703,14 +704,17 @@ static spuma_status mesh_create_impl(const spuma_mesh_desc* d, spuma_mesh m)
         launch_geometry(s, F, m->d_owner, m->d_neighbour, dSf, m->d_magSf, dC, dCf, m->d_delta, m->d_weights);
         launch_bgeometry(s, m->Fb, m->d_bkind, m->d_bcell, dbSf, m->d_bmagSf, dbCf, dC, dbnC, m->d_bis_owner,
                          m->d_bdelta, m->d_bweight);
-        m->stats.kernel_launches += (F > 0) + (m->Fb > 0);
+        SPUMA_TRY(dalloc(&m->d_corrvec, 3 * (size_t)F));
+        launch_corrvec(s, F, m->d_owner, m->d_neighbour, dSf, m->d_magSf, dC, m->d_delta, m->d_corrvec);
+        m->stats.kernel_launches += (F > 0) * 2 + (m->Fb > 0);
         SPUMA_CUDA(cudaStreamSynchronize(s));
-        cudaFree(dSf);
-        cudaFree(dC);
+        // kept for the non-orthogonal correction (gradient and processor correction vectors)
+        m->d_Sf = dSf;
+        m->d_C = dC;
+        m->d_bSf = dbSf;
+        m->d_bnC = dbnC;
         cudaFree(dCf);
-        cudaFree(dbSf);
         cudaFree(dbCf);
-        cudaFree(dbnC);
     }
 
     // ---- workspaces (allocated once: the paper's memory-pool lesson)
@@ -1034,11 +1038,10 @@ spuma_status spuma_surface_integrate(spuma_mesh m, const spuma_scalar* phi, cons
 }
 
 spuma_status spuma_face_flux(spuma_mesh m, const spuma_scalar* gamma, const spuma_scalar* const* patch_value,
-                             const spuma_scalar* upper, const spuma_scalar* iface_coeffs, const spuma_scalar* psi,
-                             spuma_scalar* flux, spuma_scalar* const* patch_flux, spuma_scalar* phi,
-                             spuma_scalar* const* patch_phi)
+                             const spuma_scalar* upper, const spuma_scalar* psi, const spuma_scalar* corr_flux,
+                             const spuma_scalar* const* patch_corr_flux, spuma_scalar* flux,
+                             spuma_scalar* const* patch_flux, spuma_scalar* phi, spuma_scalar* const* patch_phi)
 {
-    (void)iface_coeffs;
     if (!m) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "mesh is NULL");
     if ((m->F > 0 && !upper) || (m->N > 0 && !psi)) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "NULL array");
     cudaStream_t s = m->stream;
@@ -1065,15 +1068,87 @@ spuma_status spuma_face_flux(spuma_mesh m, const spuma_scalar* gamma, const spum
         }
     }
     if (patch_phi) SPUMA_TRY(patches_in(m, patch_phi, m->d_bphi, false));
-    launch_face_flux(s, m->F, m->d_owner, m->d_neighbour, u_i, psi_i, flux_i, phi_i);
+    double* cf_i = nullptr;
+    if (corr_flux) SPUMA_TRY(oriented_in(m, corr_flux, &m->d_face_d, &cf_i));
+    if (patch_corr_flux) {
+        if (!m->d_bcflux) SPUMA_TRY(dalloc(&m->d_bcflux, m->Fb));
+        SPUMA_TRY(patches_in(m, patch_corr_flux, m->d_bcflux, false));
+    }
+    launch_face_flux(s, m->F, m->d_owner, m->d_neighbour, u_i, psi_i, cf_i, flux_i, phi_i);
     launch_bface_flux(s, m->Fb, m->d_bkind, m->d_bcell, m->d_bproc, m->d_bmagSf, m->d_bdelta, m->d_bweight,
-                      m->d_bvalue, m->d_bgamma_r, m->d_bis_owner, g, psi_i, m->ws.xr, m->d_bflux,
-                      patch_phi ? m->d_bphi : nullptr);
+                      m->d_bvalue, m->d_bgamma_r, m->d_bis_owner, g, psi_i, m->ws.xr,
+                      patch_corr_flux ? m->d_bcflux : nullptr, m->d_bflux, patch_phi ? m->d_bphi : nullptr);
     m->stats.kernel_launches += 2;
     if (flux) SPUMA_TRY(oriented_out(m, flux, flux_i));
     if (phi) SPUMA_TRY(oriented_out(m, phi, phi_i));
     SPUMA_TRY(patches_out(m, patch_flux, m->d_bflux));
     if (patch_phi) SPUMA_TRY(patches_out(m, patch_phi, m->d_bphi));
+    SPUMA_CUDA(cudaStreamSynchronize(s));
+    SPUMA_CUDA(cudaGetLastError());
+    return SPUMA_OK;
+}
+
+spuma_status spuma_laplacian_correction(spuma_mesh m, const spuma_scalar* gamma,
+                                        const spuma_scalar* const* patch_value, const spuma_scalar* p,
+                                        const spuma_scalar* V, spuma_scalar* source, spuma_scalar* corr_flux,
+                                        spuma_scalar* const* patch_corr_flux)
+{
+    if (!m) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "mesh is NULL");
+    if (m->N > 0 && (!p || !V || !source)) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "NULL array");
+    cudaStream_t s = m->stream;
+    for (size_t q = 0; q < m->patches.size(); ++q)
+        if (m->patches[q].kind == SPUMA_PATCH_FIXED_VALUE && m->patches[q].n_faces > 0 && (!patch_value || !patch_value[q]))
+            return set_error(SPUMA_ERR_INVALID_ARGUMENT, "missing fixedValue values for patch " + std::to_string(q));
+    SPUMA_TRY(patches_in(m, patch_value, m->d_bvalue, true));
+    const double *p_i = nullptr, *g = nullptr, *src_in = nullptr;
+    SPUMA_TRY(cells_in(m, p, R_PSI, &p_i));
+    if (gamma) SPUMA_TRY(cells_in(m, gamma, R_GAMMA, &g));
+    SPUMA_TRY(cells_in(m, source, R_SOURCE, &src_in));
+    double* src_i = const_cast<double*>(src_in);
+    // V: its own staging buffer (the other cell roles are in use)
+    const double* V_i = V;
+    if (m->renumber || !is_device_ptr(V)) {
+        if (!m->d_cell_v) SPUMA_TRY(dalloc(&m->d_cell_v, m->N));
+        if (!m->renumber) {
+            SPUMA_CUDA(cudaMemcpyAsync(m->d_cell_v, V, sizeof(double) * m->N, cudaMemcpyHostToDevice, s));
+        } else {
+            const double* src = V;
+            if (!is_device_ptr(V)) {
+                if (!m->d_face_t) SPUMA_TRY(dalloc(&m->d_face_t, std::max(m->F, m->N)));
+                SPUMA_CUDA(cudaMemcpyAsync(m->d_face_t, V, sizeof(double) * m->N, cudaMemcpyHostToDevice, s));
+                src = m->d_face_t;
+            }
+            launch_scatter(s, m->N, m->d_perm, src, m->d_cell_v);
+        }
+        V_i = m->d_cell_v;
+    }
+    if (!m->d_G) SPUMA_TRY(dalloc(&m->d_G, 3 * (size_t)m->N));
+    if (!m->d_Gr) SPUMA_TRY(dalloc(&m->d_Gr, 3 * (size_t)m->n_iface));
+    if (!m->d_pr) SPUMA_TRY(dalloc(&m->d_pr, m->n_iface));
+    if (!m->d_bcflux) SPUMA_TRY(dalloc(&m->d_bcflux, m->Fb));
+    if (!m->d_face_d) SPUMA_TRY(dalloc(&m->d_face_d, m->F));
+    if (!m->d_div) SPUMA_TRY(dalloc(&m->d_div, m->N));
+    const MeshArgs a = mesh_args(m);
+    if (m->n_ranks > 1) {
+        SPUMA_TRY(halo_exchange(m, p_i, m->d_pr, s));
+        if (g) SPUMA_TRY(halo_exchange(m, g, m->d_bgamma_r, s));
+    }
+    launch_gauss_grad(s, a, m->d_Sf, m->d_weights, p_i, m->d_bAllStart, m->d_bAllFace, m->d_bkind, m->d_bproc,
+                      m->d_bSf, m->d_bvalue, m->d_bweight, m->d_bis_owner, m->d_pr, V_i, m->d_G);
+    if (m->n_ranks > 1)
+        for (int k = 0; k < 3; ++k)
+            SPUMA_TRY(halo_exchange(m, m->d_G + (size_t)k * m->N, m->d_Gr + (size_t)k * m->n_iface, s));
+    launch_nonorth_flux(s, m->F, m->N, m->d_owner, m->d_neighbour, m->d_corrvec, m->d_magSf, m->d_weights, g,
+                        m->d_G, m->d_face_d);
+    launch_bnonorth_flux(s, m->Fb, m->N, m->n_iface, m->d_bkind, m->d_bcell, m->d_bproc, m->d_bSf, m->d_bmagSf,
+                         m->d_bdelta, m->d_bweight, m->d_bis_owner, m->d_bnC, m->d_C, m->d_G, m->d_Gr, g,
+                         m->d_bgamma_r, m->d_bcflux);
+    launch_surface_integrate(s, a, m->d_face_d, m->d_bAllStart, m->d_bAllFace, m->d_bcflux, V_i, m->d_div);
+    launch_sub_vdiv(s, m->N, V_i, m->d_div, src_i);  // fvm.source() -= V fvc::div(correction flux)
+    m->stats.kernel_launches += 5;
+    SPUMA_TRY(cells_out(m, source, src_i));
+    if (corr_flux) SPUMA_TRY(oriented_out(m, corr_flux, m->d_face_d));
+    SPUMA_TRY(patches_out(m, patch_corr_flux, m->d_bcflux));
     SPUMA_CUDA(cudaStreamSynchronize(s));
     SPUMA_CUDA(cudaGetLastError());
     return SPUMA_OK;

@@ -118,6 +118,11 @@ struct spuma_mesh_s {
     signed char* d_face_flip = nullptr;  // renumber: internal face orientation reversed w.r.t. the caller
     double *d_bphi = nullptr, *d_bflux = nullptr;       // [Fb] staging of per-patch face fields
     double *d_face_b = nullptr, *d_face_c = nullptr;    // [F] staging of oriented face fields
+    // non-orthogonal correction: geometry kept from mesh_create (internal numbering)
+    double *d_Sf = nullptr, *d_C = nullptr, *d_corrvec = nullptr, *d_bSf = nullptr, *d_bnC = nullptr;
+    double *d_G = nullptr, *d_Gr = nullptr, *d_pr = nullptr;  // gradient [3N], remote gradient [3 n_iface], remote p
+    double *d_bcflux = nullptr, *d_face_d = nullptr;          // boundary / internal correction flux staging
+    double *d_div = nullptr, *d_cell_v = nullptr;             // [N] divergence, V staging
     // device: interfaces
     int *d_ifStart = nullptr, *d_ifIdx = nullptr, *d_if_cell = nullptr;  // if_cell: [n_iface] local cell
     unsigned* d_ifMask = nullptr;
@@ -213,13 +218,28 @@ void launch_iface_rows(cudaStream_t s, const MeshArgs& a, const Workspace& w, co
 void launch_surface_integrate(cudaStream_t s, const MeshArgs& a, const double* phi, const int* bStart,
                               const int* bFace, const double* bphi, const double* V, double* out);
 void launch_face_flux(cudaStream_t s, int F, const int* owner, const int* neighbour, const double* upper,
-                      const double* psi, double* flux, double* phi);
+                      const double* psi, const double* cflux, double* flux, double* phi);
 void launch_bface_flux(cudaStream_t s, int Fb, const int* bkind, const int* bcell, const int* bproc,
                        const double* bmagSf, const double* bdelta, const double* bweight, const double* bvalue,
                        const double* bgamma_r, const signed char* bis_owner, const double* gamma, const double* psi,
-                       const double* psi_r, double* bflux, double* bphi);
+                       const double* psi_r, const double* bcflux, double* bflux, double* bphi);
 void launch_gather_signed(cudaStream_t s, int n, const int* idx, const signed char* flip, const double* in,
                           double* out);
+void launch_corrvec(cudaStream_t s, int F, const int* owner, const int* neighbour, const double* Sf,
+                    const double* magSf, const double* C, const double* delta, double* cv);
+void launch_gauss_grad(cudaStream_t s, const MeshArgs& a, const double* Sf, const double* weights, const double* p,
+                       const int* bStart, const int* bFace, const int* bkind, const int* bproc, const double* bSf,
+                       const double* bvalue, const double* bweight, const signed char* bis_owner, const double* p_r,
+                       const double* V, double* G);
+void launch_nonorth_flux(cudaStream_t s, int F, int NC, const int* owner, const int* neighbour, const double* cv,
+                         const double* magSf, const double* weights, const double* gamma, const double* G,
+                         double* cflux);
+void launch_bnonorth_flux(cudaStream_t s, int Fb, int NC, int NI, const int* bkind, const int* bcell, const int* bproc,
+                          const double* bSf, const double* bmagSf, const double* bdelta, const double* bweight,
+                          const signed char* bis_owner, const double* bnC, const double* C, const double* G,
+                          const double* G_r, const double* gamma, const double* bgamma_r, double* bcflux);
+void launch_sub_vdiv(cudaStream_t s, int N, const double* V, const double* div, double* src);
+void launch_add(cudaStream_t s, int n, const double* in, double* out);
 void launch_scatter_signed(cudaStream_t s, int n, const int* idx, const signed char* flip, const double* in,
                            double* out);
 constexpr int kPad = 8;  // padding elements on internal arrays (16-byte TMA windows may overrun by <= 3)

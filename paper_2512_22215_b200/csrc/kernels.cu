@@ -820,12 +820,13 @@ __global__ void __launch_bounds__(kThreads)
 // phi != nullptr: the SIMPLE correction phi -= flux in place.
 __global__ void __launch_bounds__(kThreads)
     k_face_flux(int F, const int* __restrict__ owner, const int* __restrict__ neighbour,
-                const double* __restrict__ upper, const double* __restrict__ psi, double* __restrict__ flux,
-                double* __restrict__ phi)
+                const double* __restrict__ upper, const double* __restrict__ psi, const double* __restrict__ cflux,
+                double* __restrict__ flux, double* __restrict__ phi)
 {
     for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < F; f += gridDim.x * blockDim.x) {
         const double u = upper[f];
-        const double q = u * psi[neighbour[f]] - u * psi[owner[f]];
+        double q = u * psi[neighbour[f]] - u * psi[owner[f]];
+        if (cflux) q = q + cflux[f];  // fvMatrix::flux adds faceFluxCorrection
         if (flux) flux[f] = q;
         if (phi) phi[f] = phi[f] - q;
     }
@@ -838,7 +839,7 @@ __global__ void __launch_bounds__(kThreads)
                  const double* __restrict__ bweight, const double* __restrict__ bvalue,
                  const double* __restrict__ bgamma_r, const signed char* __restrict__ bis_owner,
                  const double* __restrict__ gamma, const double* __restrict__ psi, const double* __restrict__ psi_r,
-                 double* __restrict__ bflux, double* __restrict__ bphi)
+                 const double* __restrict__ bcflux, double* __restrict__ bflux, double* __restrict__ bphi)
 {
     for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < Fb; b += gridDim.x * blockDim.x) {
         const int P = bcell[b];
@@ -859,6 +860,7 @@ __global__ void __launch_bounds__(kThreads)
             const double gms = gf * bmagSf[b];
             q = (gms * (-bdelta[b])) * psi[P] - (((-gms) * bdelta[b]) * psi_r[i]);
         }
+        if (bcflux) q = q + bcflux[b];
         bflux[b] = q;
         if (bphi) bphi[b] = bphi[b] - q;
     }
@@ -877,6 +879,149 @@ __global__ void k_scatter_signed(int n, const int* __restrict__ idx, const signe
 {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
         out[idx[i]] = flip[i] ? -in[i] : in[i];
+}
+
+// ---------------------------------------------------------------------------
+// Explicit non-orthogonal correction of "Gauss linear corrected" (P:1112, P:1135,
+// P:1145): Gauss gradient, correction vectors, correction flux (reading Q21)
+// ---------------------------------------------------------------------------
+
+// nonOrthCorrectionVectors (mesh time): cv = Sf/|Sf| - (C_N - C_P) delta, per component
+__global__ void k_corrvec(int F, const int* __restrict__ owner, const int* __restrict__ neighbour,
+                          const double* __restrict__ Sf, const double* __restrict__ magSf,
+                          const double* __restrict__ C, const double* __restrict__ delta, double* __restrict__ cv)
+{
+    for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < F; f += gridDim.x * blockDim.x) {
+        const double* CP = C + 3 * (size_t)owner[f];
+        const double* CN = C + 3 * (size_t)neighbour[f];
+        for (int k = 0; k < 3; ++k) cv[3 * (size_t)f + k] = Sf[3 * (size_t)f + k] / magSf[f] - (CN[k] - CP[k]) * delta[f];
+    }
+}
+
+__device__ __forceinline__ double bface_value(int kind, double pP, double value, double w, signed char own, double pr)
+{
+    if (kind == SPUMA_PATCH_FIXED_VALUE) return value;
+    if (kind == SPUMA_PATCH_PROCESSOR) {
+        const double pO = own ? pP : pr;
+        const double pN = own ? pr : pP;
+        return w * (pO - pN) + pN;
+    }
+    return pP;  // zeroGradient
+}
+
+// Gauss linear gradient, per-cell gather in the oracle's face order (bitwise)
+__global__ void __launch_bounds__(kThreads)
+    k_gauss_grad(MeshArgs a, const double* __restrict__ Sf, const double* __restrict__ weights,
+                 const double* __restrict__ p, const int* __restrict__ bStart, const int* __restrict__ bFace,
+                 const int* __restrict__ bkind, const int* __restrict__ bproc, const double* __restrict__ bSf,
+                 const double* __restrict__ bvalue, const double* __restrict__ bweight,
+                 const signed char* __restrict__ bis_owner, const double* __restrict__ p_r,
+                 const double* __restrict__ V, double* __restrict__ G)
+{
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < a.N; c += gridDim.x * blockDim.x) {
+        const double pc = p[c];
+        double g0 = 0.0, g1 = 0.0, g2 = 0.0;
+        const int k1 = a.losortStart[c + 1];
+        for (int k = a.losortStart[c]; k < k1; ++k) {  // c is the neighbour: G -= Sf p_f
+            const int f = a.losort[k];
+            const double pf = weights[f] * (p[a.ownerLo[k]] - pc) + pc;
+            g0 = g0 - Sf[3 * (size_t)f] * pf;
+            g1 = g1 - Sf[3 * (size_t)f + 1] * pf;
+            g2 = g2 - Sf[3 * (size_t)f + 2] * pf;
+        }
+        const int f1 = a.ownerStart[c + 1];
+        for (int f = a.ownerStart[c]; f < f1; ++f) {  // c is the owner: G += Sf p_f
+            const double pn = p[a.neighbour[f]];
+            const double pf = weights[f] * (pc - pn) + pn;
+            g0 = g0 + Sf[3 * (size_t)f] * pf;
+            g1 = g1 + Sf[3 * (size_t)f + 1] * pf;
+            g2 = g2 + Sf[3 * (size_t)f + 2] * pf;
+        }
+        const int j1 = bStart[c + 1];
+        for (int j = bStart[c]; j < j1; ++j) {
+            const int b = bFace[j];
+            const int i = bproc[b];
+            const double pb = bface_value(bkind[b], pc, bvalue[b], bweight[b], bis_owner[b], i >= 0 ? p_r[i] : 0.0);
+            g0 = g0 + bSf[3 * (size_t)b] * pb;
+            g1 = g1 + bSf[3 * (size_t)b + 1] * pb;
+            g2 = g2 + bSf[3 * (size_t)b + 2] * pb;
+        }
+        G[c] = g0 / V[c];  // structure of arrays: G[k N + c]
+        G[(size_t)a.N + c] = g1 / V[c];
+        G[2 * (size_t)a.N + c] = g2 / V[c];
+    }
+}
+
+// correction flux on internal faces: (gamma_f |S|) (cv . (w (G_P - G_N) + G_N))
+__global__ void __launch_bounds__(kThreads)
+    k_nonorth_flux(int F, int NC, const int* __restrict__ owner, const int* __restrict__ neighbour,
+                   const double* __restrict__ cv, const double* __restrict__ magSf, const double* __restrict__ weights,
+                   const double* __restrict__ gamma, const double* __restrict__ G, double* __restrict__ cflux)
+{
+    for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < F; f += gridDim.x * blockDim.x) {
+        const size_t P = owner[f], N = neighbour[f];
+        const double w = weights[f];
+        double g[3];
+        for (int k = 0; k < 3; ++k) g[k] = w * (G[k * (size_t)NC + P] - G[k * (size_t)NC + N]) + G[k * (size_t)NC + N];
+        const double corr = cv[3 * (size_t)f] * g[0] + cv[3 * (size_t)f + 1] * g[1] + cv[3 * (size_t)f + 2] * g[2];
+        double gf = 1.0;
+        if (gamma) gf = w * (gamma[P] - gamma[N]) + gamma[N];
+        cflux[f] = (gf * magSf[f]) * corr;
+    }
+}
+
+// correction flux on boundary faces: processor faces in global orientation (outward sign), else 0
+__global__ void __launch_bounds__(kThreads)
+    k_bnonorth_flux(int Fb, int NC, int NI, const int* __restrict__ bkind, const int* __restrict__ bcell,
+                    const int* __restrict__ bproc,
+                    const double* __restrict__ bSf, const double* __restrict__ bmagSf, const double* __restrict__ bdelta,
+                    const double* __restrict__ bweight, const signed char* __restrict__ bis_owner,
+                    const double* __restrict__ bnC, const double* __restrict__ C, const double* __restrict__ G,
+                    const double* __restrict__ G_r, const double* __restrict__ gamma,
+                    const double* __restrict__ bgamma_r, double* __restrict__ bcflux)
+{
+    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < Fb; b += gridDim.x * blockDim.x) {
+        double q = 0.0;
+        if (bkind[b] == SPUMA_PATCH_PROCESSOR) {
+            const int L = bcell[b], i = bproc[b];
+            const bool own = bis_owner[b];
+            const double* CL = C + 3 * (size_t)L;
+            const double* CR = bnC + 3 * (size_t)b;
+            double cv[3], g[3];
+            for (int k = 0; k < 3; ++k) {
+                const double S = own ? bSf[3 * (size_t)b + k] : -bSf[3 * (size_t)b + k];
+                const double cP = own ? CL[k] : CR[k], cN = own ? CR[k] : CL[k];
+                cv[k] = S / bmagSf[b] - (cN - cP) * bdelta[b];
+                const double gL = G[k * (size_t)NC + L], gR = G_r[k * (size_t)NI + i];
+                const double gO = own ? gL : gR;
+                const double gN = own ? gR : gL;
+                g[k] = bweight[b] * (gO - gN) + gN;
+            }
+            const double corr = cv[0] * g[0] + cv[1] * g[1] + cv[2] * g[2];
+            double gf = 1.0;
+            if (gamma) {
+                const double gO = own ? gamma[L] : bgamma_r[i];
+                const double gN = own ? bgamma_r[i] : gamma[L];
+                gf = bweight[b] * (gO - gN) + gN;
+            }
+            const double v = (gf * bmagSf[b]) * corr;
+            q = own ? v : -v;
+        }
+        bcflux[b] = q;
+    }
+}
+
+// source -= V div  (div = surfaceIntegrate of the correction flux)
+__global__ void k_sub_vdiv(int N, const double* __restrict__ V, const double* __restrict__ div, double* __restrict__ src)
+{
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < N; c += gridDim.x * blockDim.x)
+        src[c] = src[c] - V[c] * div[c];
+}
+
+// add a (correction) flux: out += in
+__global__ void k_add(int n, const double* __restrict__ in, double* __restrict__ out)
+{
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = out[i] + in[i];
 }
 
 // A7 interface rows (P > 1, deferred mode): rows[] = cells with processor faces
@@ -1226,21 +1371,21 @@ void launch_surface_integrate(cudaStream_t s, const MeshArgs& a, const double* p
 }
 
 void launch_face_flux(cudaStream_t s, int F, const int* owner, const int* neighbour, const double* upper,
-                      const double* psi, double* flux, double* phi)
+                      const double* psi, const double* cflux, double* flux, double* phi)
 {
     if (F <= 0) return;
-    k_face_flux<<<grid_for(k_face_flux, F), kThreads, 0, s>>>(F, owner, neighbour, upper, psi, flux, phi);
+    k_face_flux<<<grid_for(k_face_flux, F), kThreads, 0, s>>>(F, owner, neighbour, upper, psi, cflux, flux, phi);
 }
 
 void launch_bface_flux(cudaStream_t s, int Fb, const int* bkind, const int* bcell, const int* bproc,
                        const double* bmagSf, const double* bdelta, const double* bweight, const double* bvalue,
                        const double* bgamma_r, const signed char* bis_owner, const double* gamma, const double* psi,
-                       const double* psi_r, double* bflux, double* bphi)
+                       const double* psi_r, const double* bcflux, double* bflux, double* bphi)
 {
     if (Fb <= 0) return;
     k_bface_flux<<<grid_for(k_bface_flux, Fb), kThreads, 0, s>>>(Fb, bkind, bcell, bproc, bmagSf, bdelta, bweight,
                                                                  bvalue, bgamma_r, bis_owner, gamma, psi, psi_r,
-                                                                 bflux, bphi);
+                                                                 bcflux, bflux, bphi);
 }
 
 void launch_gather_signed(cudaStream_t s, int n, const int* idx, const signed char* flip, const double* in,
@@ -1255,6 +1400,55 @@ void launch_scatter_signed(cudaStream_t s, int n, const int* idx, const signed c
 {
     if (n <= 0) return;
     k_scatter_signed<<<grid_for(k_scatter_signed, n), kThreads, 0, s>>>(n, idx, flip, in, out);
+}
+
+void launch_corrvec(cudaStream_t s, int F, const int* owner, const int* neighbour, const double* Sf,
+                    const double* magSf, const double* C, const double* delta, double* cv)
+{
+    if (F <= 0) return;
+    k_corrvec<<<grid_for(k_corrvec, F), kThreads, 0, s>>>(F, owner, neighbour, Sf, magSf, C, delta, cv);
+}
+
+void launch_gauss_grad(cudaStream_t s, const MeshArgs& a, const double* Sf, const double* weights, const double* p,
+                       const int* bStart, const int* bFace, const int* bkind, const int* bproc, const double* bSf,
+                       const double* bvalue, const double* bweight, const signed char* bis_owner, const double* p_r,
+                       const double* V, double* G)
+{
+    if (a.N <= 0) return;
+    k_gauss_grad<<<grid_for(k_gauss_grad, a.N), kThreads, 0, s>>>(a, Sf, weights, p, bStart, bFace, bkind, bproc, bSf,
+                                                                  bvalue, bweight, bis_owner, p_r, V, G);
+}
+
+void launch_nonorth_flux(cudaStream_t s, int F, int NC, const int* owner, const int* neighbour, const double* cv,
+                         const double* magSf, const double* weights, const double* gamma, const double* G,
+                         double* cflux)
+{
+    if (F <= 0) return;
+    k_nonorth_flux<<<grid_for(k_nonorth_flux, F), kThreads, 0, s>>>(F, NC, owner, neighbour, cv, magSf, weights,
+                                                                    gamma, G, cflux);
+}
+
+void launch_bnonorth_flux(cudaStream_t s, int Fb, int NC, int NI, const int* bkind, const int* bcell, const int* bproc,
+                          const double* bSf, const double* bmagSf, const double* bdelta, const double* bweight,
+                          const signed char* bis_owner, const double* bnC, const double* C, const double* G,
+                          const double* G_r, const double* gamma, const double* bgamma_r, double* bcflux)
+{
+    if (Fb <= 0) return;
+    k_bnonorth_flux<<<grid_for(k_bnonorth_flux, Fb), kThreads, 0, s>>>(Fb, NC, NI, bkind, bcell, bproc, bSf, bmagSf,
+                                                                       bdelta, bweight, bis_owner, bnC, C, G, G_r,
+                                                                       gamma, bgamma_r, bcflux);
+}
+
+void launch_sub_vdiv(cudaStream_t s, int N, const double* V, const double* div, double* src)
+{
+    if (N <= 0) return;
+    k_sub_vdiv<<<grid_for(k_sub_vdiv, N), kThreads, 0, s>>>(N, V, div, src);
+}
+
+void launch_add(cudaStream_t s, int n, const double* in, double* out)
+{
+    if (n <= 0) return;
+    k_add<<<grid_for(k_add, n), kThreads, 0, s>>>(n, in, out);
 }
 
 void launch_iface_rows(cudaStream_t s, const MeshArgs& a, const Workspace& w, const int* rows, int n_rows)

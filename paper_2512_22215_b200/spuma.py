@@ -106,7 +106,9 @@ def lib():
         L.spuma_amul.argtypes = [_vp] * 6
         if hasattr(L, "spuma_surface_integrate"):
             L.spuma_surface_integrate.argtypes = [_vp] * 5
-            L.spuma_face_flux.argtypes = [_vp] * 10
+            L.spuma_face_flux.argtypes = [_vp] * 11
+        if hasattr(L, "spuma_laplacian_correction"):
+            L.spuma_laplacian_correction.argtypes = [_vp] * 8
         L.spuma_mesh_get_addressing.argtypes = [_vp] * 8
         L.spuma_mesh_get_geometry.argtypes = [_vp] * 4
         L.spuma_get_stats.argtypes = [_vp, ctypes.POINTER(Stats)]
@@ -123,7 +125,7 @@ def lib():
                      "spuma_mesh_get_addressing", "spuma_mesh_get_geometry", "spuma_get_stats",
                      "spuma_reset_stats", "spuma_set_timing", "spuma_set_batch", "spuma_nccl_get_unique_id",
                      "spuma_set_option", "spuma_set_comm_callbacks", "spuma_surface_integrate",
-                     "spuma_face_flux"):
+                     "spuma_face_flux", "spuma_laplacian_correction"):
             if hasattr(L, name):
                 getattr(L, name).restype = _ci
         if L.spuma_abi_version() != ABI_VERSION:
@@ -302,16 +304,26 @@ class Mesh:
         _check(lib().spuma_surface_integrate(self._h, a, pp, v, o))
         return ko
 
-    def face_flux(self, gamma, patch_values, upper, iface_coeffs, psi, flux=None, patch_flux=None, phi=None,
-                  patch_phi=None):
-        """spuma_face_flux: fvMatrix::flux of the Laplacian; phi -= flux in place when phi is given."""
+    def face_flux(self, gamma, patch_values, upper, psi, corr_flux=None, patch_corr_flux=None, flux=None,
+                  patch_flux=None, phi=None, patch_phi=None):
+        """spuma_face_flux: fvMatrix::flux of the Laplacian (+ correction flux); phi -= flux in place."""
         keep = []
         pv = self._patch_ptrs(patch_values, keep)
+        pc = self._patch_ptrs(patch_corr_flux, keep)
         pf = self._patch_ptrs(patch_flux, keep)
         pp = self._patch_ptrs(patch_phi, keep)
-        ptrs = [_ptr(x, np.float64) for x in (gamma, upper, iface_coeffs, psi, flux, phi)]
-        g, u, f, ps, fl, ph = [p for p, _ in ptrs]
-        _check(lib().spuma_face_flux(self._h, g, pv, u, f, ps, fl, pf, ph, pp))
+        ptrs = [_ptr(x, np.float64) for x in (gamma, upper, psi, corr_flux, flux, phi)]
+        g, u, ps, cf, fl, ph = [p for p, _ in ptrs]
+        _check(lib().spuma_face_flux(self._h, g, pv, u, ps, cf, pc, fl, pf, ph, pp))
+
+    def laplacian_correction(self, gamma, patch_values, p, V, source, corr_flux=None, patch_corr_flux=None):
+        """spuma_laplacian_correction: source -= V div(non-orthogonal correction flux) in place."""
+        keep = []
+        pv = self._patch_ptrs(patch_values, keep)
+        pc = self._patch_ptrs(patch_corr_flux, keep)
+        ptrs = [_ptr(x, np.float64) for x in (gamma, p, V, source, corr_flux)]
+        g, pp, v, s, cf = [q for q, _ in ptrs]
+        _check(lib().spuma_laplacian_correction(self._h, g, pv, pp, v, s, cf, pc))
 
     # ---------------------------------------------------------------- diagnostics
     def mesh_get_addressing(self) -> dict:

@@ -63,7 +63,7 @@ def test_face_flux_and_correction_bitwise(kind, renumber):
     pphi = [rng.standard_normal(p.n_faces) for p in m.patches]
     phi_d = dev(phiH)
     pphi_d = [dev(x) for x in pphi]
-    h.face_flux(dev(g), pv, upper, None, dev(psi), flux, pflux, phi_d, pphi_d)
+    h.face_flux(dev(g), pv, upper, dev(psi), None, None, flux, pflux, phi_d, pphi_d)
     if renumber:
         perm = O.rcm(m.n_cells, m.owner, m.neighbour)
         rm = O.renumber_mesh(m, perm)
@@ -106,7 +106,7 @@ def test_simple_pressure_step_conserves():
     psi = torch.zeros(m.n_cells, dtype=torch.float64, device="cuda")
     perf = h.pcg_solve(diag, upper, None, src, psi, 1e-12, 0.0, 5000, 0)
     assert perf["converged"]
-    h.face_flux(gd, None, upper, None, psi, None, None, phiH, zeros)
+    h.face_flux(gd, None, upper, psi, None, None, None, None, phiH, zeros)
     h.surface_integrate(phiH, zeros, V, div)
     res = (div * V).cpu().numpy()
     assert np.sum(np.abs(res[1:])) < 1e-9 * np.sum(np.abs(b.cpu().numpy()))

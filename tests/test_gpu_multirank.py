@@ -92,6 +92,23 @@ def _worker(rank, P, how, port, q):
         assert np.array_equal(src.cpu().numpy(), s.source)
         oi = np.concatenate(s.iface) if s.iface else np.zeros(0)
         assert np.array_equal(iface.cpu().numpy()[:oi.shape[0]], oi)
+        # non-orthogonal correction with the p / gamma / gradient halos vs the decomposed oracle
+        pfield = np.cos(np.arange(m.n_cells) * 0.29)
+        ps = gen.split_cell_field(pfield, part, P)
+        p_h = O.gamma_halo(subs, ps)
+        Gs = [O.gauss_grad(sm, ps[r], p_remote=p_h[r]) for r, sm in enumerate(subs)]
+        G_h = O.gamma_halo(subs, Gs)
+        cf_o, pcf_o, ds_o, _ = O.nonorth_correction(me, ps[rank], gs[rank], gamma_remote=halo[rank],
+                                                    p_remote=p_h[rank], G=Gs[rank], G_remote=G_h[rank])
+        srcc = torch.as_tensor(bs[rank], **f64)
+        cf = torch.empty(max(me.n_faces, 1), **f64)
+        pcf = [torch.empty(max(q.n_faces, 1), **f64) for q in me.patches]
+        h.laplacian_correction(torch.as_tensor(gs[rank], **f64), None, torch.as_tensor(ps[rank], **f64),
+                               torch.as_tensor(me.V, **f64), srcc, cf, pcf)
+        assert np.array_equal(cf.cpu().numpy()[:me.n_faces], cf_o)
+        assert np.array_equal(srcc.cpu().numpy(), bs[rank] + ds_o)
+        for a, q, b in zip(pcf, me.patches, pcf_o):
+            assert np.array_equal(a.cpu().numpy()[:q.n_faces], b)
         # Amul with the halo
         x = np.cos(np.arange(m.n_cells) * 0.37)
         xs = gen.split_cell_field(x, part, P)
