@@ -62,7 +62,7 @@ def _case(P, how):
     return m, gamma, b, part
 
 
-def _worker(rank, P, how, port, q):
+def _worker(rank, P, how, port, results):
     try:
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
         import datetime
@@ -103,13 +103,13 @@ def _worker(rank, P, how, port, q):
                                                     p_remote=p_h[rank], G=Gs[rank], G_remote=G_h[rank])
         srcc = torch.as_tensor(bs[rank], **f64)
         cf = torch.empty(max(me.n_faces, 1), **f64)
-        pcf = [torch.empty(max(q.n_faces, 1), **f64) for q in me.patches]
+        pcf = [torch.empty(max(pt.n_faces, 1), **f64) for pt in me.patches]
         h.laplacian_correction(torch.as_tensor(gs[rank], **f64), None, torch.as_tensor(ps[rank], **f64),
                                torch.as_tensor(me.V, **f64), srcc, cf, pcf)
         assert np.array_equal(cf.cpu().numpy()[:me.n_faces], cf_o)
         assert np.array_equal(srcc.cpu().numpy(), bs[rank] + ds_o)
-        for a, q, b in zip(pcf, me.patches, pcf_o):
-            assert np.array_equal(a.cpu().numpy()[:q.n_faces], b)
+        for a, pt, b in zip(pcf, me.patches, pcf_o):
+            assert np.array_equal(a.cpu().numpy()[:pt.n_faces], b)
         # Amul with the halo
         x = np.cos(np.arange(m.n_cells) * 0.37)
         xs = gen.split_cell_field(x, part, P)
@@ -142,10 +142,10 @@ def _worker(rank, P, how, port, q):
         assert p0["n_iterations"] == n
         assert np.max(np.abs(psi0.cpu().numpy() - loc)) <= 1e-9 * max(np.max(np.abs(loc)), 1e-300)
         h.free()
-        q.put((rank, "ok"))
+        results.put((rank, "ok"))
     except BaseException:
         import traceback
-        q.put((rank, traceback.format_exc()))
+        results.put((rank, traceback.format_exc()))
     finally:
         if dist.is_initialized():
             dist.destroy_process_group()
