@@ -56,6 +56,21 @@ class Perf(ctypes.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class GamgParams(ctypes.Structure):
+    """O11 GAMG parameters (readings Q22-Q28): sweeps, Richardson weight, correction scaling,
+    coarsening stop, coarsest-level PCG controls."""
+    _fields_ = [("n_pre", ctypes.c_int), ("n_post", ctypes.c_int), ("scale", ctypes.c_int),
+                ("n_coarsest_cells", ctypes.c_int), ("max_levels", ctypes.c_int),
+                ("omega", ctypes.c_double), ("coarsest_tol", ctypes.c_double),
+                ("coarsest_rel_tol", ctypes.c_double), ("coarsest_max_iter", ctypes.c_int)]
+
+
+def gamg_params(n_pre=0, n_post=2, scale=True, n_coarsest_cells=10, max_levels=50, omega=0.75,
+                coarsest_tol=0.0, coarsest_rel_tol=1e-6, coarsest_max_iter=1000) -> GamgParams:
+    return GamgParams(n_pre, n_post, int(scale), n_coarsest_cells, max_levels, omega, coarsest_tol,
+                      coarsest_rel_tol, coarsest_max_iter)
+
+
 class _Domain(ctypes.Structure):
     _fields_ = [("n_cells", ctypes.c_int), ("n_faces", ctypes.c_int),
                 ("owner", ctypes.c_void_p), ("neighbour", ctypes.c_void_p),
@@ -91,6 +106,12 @@ def _L():
             lib.or_face_flux.argtypes = [ci] + [vp] * 6 + [ci] + [vp] * 11
             lib.or_gauss_grad.argtypes = [ci, ci] + [vp] * 5 + [ci] + [vp] * 9
             lib.or_nonorth_flux.argtypes = [ci] + [vp] * 10 + [ci] + [vp] * 11
+            lib.or_agglomerate.argtypes = [ci, ci, vp, vp, vp, vp]
+            lib.or_coarse_addressing.argtypes = [ci] + [vp] * 8
+            lib.or_agglomerate_matrix.argtypes = [ci, ci] + [vp] * 5 + [ci, ci, vp, vp]
+            lib.or_restrict.argtypes = [ci, vp, vp, ci, vp]
+            lib.or_gamg.argtypes = [ci, ci] + [vp] * 7 + [ctypes.POINTER(GamgParams), ctypes.POINTER(Controls),
+                                                           ctypes.POINTER(Perf), vp, vp]
             lib.or_dense_from_ldu.argtypes = [ci, ci] + [vp] * 6
             lib.or_dense_matvec.argtypes = [ci, vp, vp, vp]
             lib.or_dense_solve.argtypes = [ci, vp, vp, vp]
@@ -339,6 +360,81 @@ def pcg_decomposed(meshes: Sequence[gen.Mesh], systems: Sequence[LduSystem], psi
     if rc:
         raise MemoryError("or_pcg")
     return psis, perf.as_dict()
+
+
+def agglomerate(n_cells: int, owner, neighbour, weights):
+    """O11 pairwise agglomeration (Q22). Returns (fine_to_coarse int32, n_coarse)."""
+    o, nb, w = _i32(owner), _i32(neighbour), _f64(weights)
+    ftc = np.zeros(n_cells + 1, np.int32)
+    nc = _L().or_agglomerate(n_cells, o.shape[0], _p(o), _p(nb), _p(w), _p(ftc))
+    return ftc[:n_cells], nc
+
+
+def coarse_addressing(owner, neighbour, ftc, weights):
+    """O11 coarse lduAddressing: (c_owner, c_neighbour, face_restrict, c_weights)."""
+    o, nb, f, w = _i32(owner), _i32(neighbour), _i32(ftc), _f64(weights)
+    F = o.shape[0]
+    co, cn, fr = (np.zeros(F + 1, np.int32) for _ in range(3))
+    cw = np.zeros(F + 1)
+    ncf = _L().or_coarse_addressing(F, _p(o), _p(nb), _p(f), _p(w), _p(co), _p(cn), _p(fr), _p(cw))
+    return co[:ncf], cn[:ncf], fr[:F], cw[:ncf]
+
+
+def agglomerate_matrix(owner, ftc, face_restrict, diag, upper, n_coarse: int, n_coarse_faces: int):
+    """O11 Galerkin coarse LDU: (c_diag, c_upper)."""
+    o, f, fr, d, u = _i32(owner), _i32(ftc), _i32(face_restrict), _f64(diag), _f64(upper)
+    cd, cu = np.zeros(n_coarse + 1), np.zeros(n_coarse_faces + 1)
+    _L().or_agglomerate_matrix(d.shape[0], o.shape[0], _p(o), _p(f), _p(fr), _p(d), _p(u), n_coarse,
+                               n_coarse_faces, _p(cd), _p(cu))
+    return cd[:n_coarse], cu[:n_coarse_faces]
+
+
+def restrict_field(ftc, fine, n_coarse: int):
+    f, x = _i32(ftc), _f64(fine)
+    out = np.zeros(n_coarse + 1)
+    _L().or_restrict(x.shape[0], _p(f), _p(x), n_coarse, _p(out))
+    return out[:n_coarse]
+
+
+def gamg_hierarchy(mesh: gen.Mesh, params: Optional[GamgParams] = None, weights=None):
+    """The level list [(n_cells, owner, neighbour, ftc-or-None)] built by the O11 rules (weights:
+    face areas, faceAreaPair)."""
+    gp = params or gamg_params()
+    lv = []
+    o, nb = _i32(mesh.owner), _i32(mesh.neighbour)
+    w = _f64(mesh.magSf if weights is None else weights)
+    n = mesh.n_cells
+    while len(lv) + 1 < gp.max_levels and n > gp.n_coarsest_cells:
+        ftc, nc = agglomerate(n, o, nb, w)
+        if nc >= n:
+            break
+        lv.append((n, o, nb, ftc))
+        o, nb, _, w = coarse_addressing(o, nb, ftc, w)
+        n = nc
+    lv.append((n, o, nb, None))
+    return lv
+
+
+def gamg(mesh: gen.Mesh, sys: LduSystem, psi0=None, ctl: Optional[Controls] = None,
+         params: Optional[GamgParams] = None, weights=None):
+    """O11 GAMG + Richardson smoother, single domain. Returns (psi, perf dict incl. 'levels',
+    'level_cells')."""
+    ctl = ctl or controls()
+    gp = params or gamg_params()
+    if processor_patches(mesh):
+        raise ValueError("oracle GAMG is single-domain (DESIGN.md Q28)")
+    o, nb, w = _i32(mesh.owner), _i32(mesh.neighbour), _f64(mesh.magSf if weights is None else weights)
+    d, u, b = _f64(sys.diag), _f64(sys.upper), _f64(sys.source)
+    psi = np.zeros(mesh.n_cells) if psi0 is None else _f64(psi0).copy()
+    nl = ctypes.c_int(0)
+    cells = np.zeros(64, np.int32)
+    perf = Perf()
+    _L().or_gamg(mesh.n_cells, mesh.n_faces, _p(o), _p(nb), _p(w), _p(d), _p(u), _p(b), _p(psi),
+                 ctypes.byref(gp), ctypes.byref(ctl), ctypes.byref(perf), ctypes.addressof(nl), _p(cells))
+    out = perf.as_dict()
+    out["levels"] = nl.value
+    out["level_cells"] = cells[:nl.value].tolist()
+    return psi, out
 
 
 def gamma_halo(meshes: Sequence[gen.Mesh], gammas: Sequence[np.ndarray]):

@@ -21,6 +21,8 @@
  *   O7 dense        or_dense_from_ldu, or_dense_matvec, or_dense_solve    brute force for N <= 64
  *   O9 around       or_surface_integrate, or_face_flux
  *   O10 non-orth    or_gauss_grad, or_nonorth_flux                        P:1112, P:1135, P:1145 (Gauss linear corrected)
+ *   O11 GAMG        or_agglomerate, or_coarse_addressing, or_agglomerate_matrix, or_restrict, or_gamg
+ *                   P:517
  *
  * Pins (tests/test_oracle_*.py, -m "not gpu"): SPEC chain examples,
  * closed-form Poisson eigenmodes (Dirichlet / Neumann) and linear exactness,
@@ -696,6 +698,330 @@ int or_pcg(int nd, or_domain* D, const or_controls* ctl, or_perf* perf)
     free(W);
     free(X);
     free(Y);
+    return 0;
+}
+
+/* ------------------------------------------------------------------------- */
+/* O11 GAMG with the Richardson smoother (paper: "GAMG ...      */
+/* Richardson (or weighted Jacobi) ... diagonal at the coarsest" P:665,       */
+/* pGAMG P:1043-1052; profile rows restrictField P:527, prolongField P:537,   */
+/* agglomerateMatrix P:538, scale P:525, Vcycle P:545, RichardsonSmoother     */
+/* P:517).  Readings Q22-Q28; SPEC S:479-569 for the rest.      */
+/* ------------------------------------------------------------------------- */
+
+/* faceAreaPair-style pairwise agglomeration (Q22): cells in ascending order; an
+ * unagglomerated cell pairs with its unagglomerated neighbour across the face of largest
+ * weight (faces of the cell in ascending face index, first maximum wins); with no such
+ * neighbour it joins the agglomerate of its neighbour across the largest-weight face;
+ * an isolated cell becomes its own agglomerate.  Returns the number of coarse cells. */
+int or_agglomerate(int n, int F, const int* owner, const int* neighbour, const double* w, int* ftc)
+{
+    int* start = (int*)calloc((size_t)n + 1, sizeof(int));
+    int* faces = (int*)malloc(sizeof(int) * (size_t)(2 * F + 1));
+    int* fill = (int*)calloc((size_t)n + 1, sizeof(int));
+    for (int f = 0; f < F; ++f) {
+        start[owner[f] + 1]++;
+        start[neighbour[f] + 1]++;
+    }
+    for (int c = 0; c < n; ++c) start[c + 1] += start[c];
+    for (int f = 0; f < F; ++f) { /* ascending f: each cell's list is in ascending face index */
+        faces[start[owner[f]] + fill[owner[f]]++] = f;
+        faces[start[neighbour[f]] + fill[neighbour[f]]++] = f;
+    }
+    for (int c = 0; c < n; ++c) ftc[c] = -1;
+    int nc = 0;
+    for (int c = 0; c < n; ++c) {
+        if (ftc[c] >= 0) continue;
+        int best = -1;
+        double bw = -1.0;
+        for (int e = start[c]; e < start[c + 1]; ++e) {
+            const int f = faces[e];
+            const int o = owner[f] == c ? neighbour[f] : owner[f];
+            if (ftc[o] < 0 && w[f] > bw) {
+                bw = w[f];
+                best = o;
+            }
+        }
+        if (best >= 0) {
+            ftc[c] = ftc[best] = nc++;
+            continue;
+        }
+        bw = -1.0;
+        for (int e = start[c]; e < start[c + 1]; ++e) {
+            const int f = faces[e];
+            const int o = owner[f] == c ? neighbour[f] : owner[f];
+            if (w[f] > bw) {
+                bw = w[f];
+                best = o;
+            }
+        }
+        ftc[c] = best >= 0 ? ftc[best] : nc++;
+    }
+    free(start);
+    free(faces);
+    free(fill);
+    return nc;
+}
+
+static int or_pair2_cmp(const void* a, const void* b)
+{
+    const int* x = (const int*)a;
+    const int* y = (const int*)b;
+    if (x[0] != y[0]) return x[0] < y[0] ? -1 : 1;
+    return x[1] < y[1] ? -1 : (x[1] > y[1]);
+}
+
+/* coarse lduAddressing: coarse faces = distinct (min, max) agglomerate pairs of the fine faces,
+ * sorted; frestrict[f] = coarse face of fine face f, or -1 when both cells are in one
+ * agglomerate.  Coarse face weights = sums of the fine ones (ascending fine face).
+ * Returns the number of coarse faces (arrays sized F suffice). */
+int or_coarse_addressing(int F, const int* owner, const int* neighbour, const int* ftc, const double* w,
+                         int* cowner, int* cneighbour, int* frestrict, double* cw)
+{
+    int* pairs = (int*)malloc(sizeof(int) * 2 * (size_t)(F > 0 ? F : 1));
+    int np = 0;
+    for (int f = 0; f < F; ++f) {
+        const int a = ftc[owner[f]], b = ftc[neighbour[f]];
+        if (a == b) continue;
+        pairs[2 * np] = a < b ? a : b;
+        pairs[2 * np + 1] = a < b ? b : a;
+        ++np;
+    }
+    qsort(pairs, (size_t)np, 2 * sizeof(int), or_pair2_cmp);
+    int ncf = 0;
+    for (int i = 0; i < np; ++i)
+        if (i == 0 || pairs[2 * i] != pairs[2 * i - 2] || pairs[2 * i + 1] != pairs[2 * i - 1]) {
+            cowner[ncf] = pairs[2 * i];
+            cneighbour[ncf] = pairs[2 * i + 1];
+            ++ncf;
+        }
+    for (int i = 0; i < ncf; ++i) cw[i] = 0.0;
+    for (int f = 0; f < F; ++f) {
+        const int a = ftc[owner[f]], b = ftc[neighbour[f]];
+        if (a == b) {
+            frestrict[f] = -1;
+            continue;
+        }
+        const int lo = a < b ? a : b, hi = a < b ? b : a;
+        int l = 0, h = ncf; /* binary search (lo, hi) */
+        while (l < h) {
+            const int m = l + (h - l) / 2;
+            if (cowner[m] < lo || (cowner[m] == lo && cneighbour[m] < hi)) l = m + 1;
+            else h = m;
+        }
+        frestrict[f] = l;
+        cw[l] += w[f];
+    }
+    free(pairs);
+    return ncf;
+}
+
+/* agglomerateMatrix (Galerkin with summation restriction / injection prolongation):
+ * cdiag = restrict(diag) (ascending fine cells); then fine faces ascending: cupper[frestrict]
+ * += upper, or cdiag[ftc[owner]] += (upper + lower) for agglomerate-internal faces. */
+void or_agglomerate_matrix(int n, int F, const int* owner, const int* ftc, const int* frestrict, const double* diag,
+                           const double* upper, int nc, int ncf, double* cdiag, double* cupper)
+{
+    for (int c = 0; c < nc; ++c) cdiag[c] = 0.0;
+    for (int i = 0; i < ncf; ++i) cupper[i] = 0.0;
+    for (int i = 0; i < n; ++i) cdiag[ftc[i]] += diag[i];
+    for (int f = 0; f < F; ++f) {
+        if (frestrict[f] >= 0) cupper[frestrict[f]] += upper[f];
+        else cdiag[ftc[owner[f]]] += upper[f] + upper[f];
+    }
+}
+
+/* restrictField: coarse[c] = sum of fine[i] over ftc[i] = c, ascending i */
+void or_restrict(int n, const int* ftc, const double* fine, int nc, double* coarse)
+{
+    for (int c = 0; c < nc; ++c) coarse[c] = 0.0;
+    for (int i = 0; i < n; ++i) coarse[ftc[i]] += fine[i];
+}
+
+typedef struct {
+    int n_pre, n_post, scale, n_coarsest_cells, max_levels;
+    double omega, coarsest_tol, coarsest_rel_tol;
+    int coarsest_max_iter;
+} or_gamg_params;
+
+typedef struct {
+    int n, F;
+    int *owner, *neighbour, *ftc, *frestrict; /* ftc/frestrict map this level to the next */
+    double *w, *diag, *upper, *b, *x, *r, *y, *c, *rD;
+} or_level;
+
+/* Richardson / weighted-Jacobi sweep (Q24): y = A x; x = x + omega (rD (b - y)) */
+static void or_jacobi_sweep(or_level* L, double omega)
+{
+    or_amul(L->n, L->F, L->owner, L->neighbour, L->diag, L->upper, L->upper, L->x, 0, 0, 0, 0, L->y);
+    for (int i = 0; i < L->n; ++i) L->x[i] = L->x[i] + omega * (L->rD[i] * (L->b[i] - L->y[i]));
+}
+
+/* GAMGSolver::scale reading (Q25): alpha = (c.r)/(c.Ac) clamped to [0, 2]
+ * (1 when c.Ac <= 1e-300); c *= alpha.  The lower clamp is pinned (omega = 1.6 case); the
+ * upper clamp is PARITY UNPINNED: no pin found reaches alpha > 2 (with Galerkin operators the
+ * raw factor stayed <= 2 in every searched configuration). */
+static void or_scale(or_level* L, double* r)
+{
+    or_amul(L->n, L->F, L->owner, L->neighbour, L->diag, L->upper, L->upper, L->c, 0, 0, 0, 0, L->y);
+    double num = 0.0, den = 0.0;
+    for (int i = 0; i < L->n; ++i) num += L->c[i] * r[i];
+    for (int i = 0; i < L->n; ++i) den += L->y[i] * L->c[i];
+    double a = fabs(den) > 1e-300 ? num / den : 1.0;
+    if (a < 0.0) a = 0.0;
+    if (a > 2.0) a = 2.0;
+    for (int i = 0; i < L->n; ++i) L->c[i] = a * L->c[i];
+}
+
+static void or_coarsest_solve(or_level* L, const or_gamg_params* gp)
+{
+    for (int i = 0; i < L->n; ++i) L->x[i] = 0.0;
+    or_domain d = {L->n, L->F, L->owner, L->neighbour, L->diag, L->upper, L->b, L->x, 0, 0, 0, 0, 0};
+    or_controls c = {gp->coarsest_tol, gp->coarsest_rel_tol, gp->coarsest_max_iter, 0};
+    or_perf pf;
+    or_pcg(1, &d, &c, &pf);
+}
+
+/* one V-cycle (Q23): correction form, zero initial guess on every coarse level */
+static void or_vcycle(int nl, or_level* Lv, const or_gamg_params* gp)
+{
+    for (int l = 0; l < nl - 1; ++l) {
+        or_level* L = &Lv[l];
+        for (int i = 0; i < L->n; ++i) L->x[i] = 0.0;
+        for (int s = 0; s < gp->n_pre; ++s) or_jacobi_sweep(L, gp->omega);
+        or_amul(L->n, L->F, L->owner, L->neighbour, L->diag, L->upper, L->upper, L->x, 0, 0, 0, 0, L->y);
+        for (int i = 0; i < L->n; ++i) L->r[i] = L->b[i] - L->y[i];
+        or_restrict(L->n, L->ftc, L->r, Lv[l + 1].n, Lv[l + 1].b);
+    }
+    or_coarsest_solve(&Lv[nl - 1], gp);
+    for (int l = nl - 2; l >= 0; --l) {
+        or_level* L = &Lv[l];
+        for (int i = 0; i < L->n; ++i) L->c[i] = Lv[l + 1].x[L->ftc[i]]; /* prolongField: injection */
+        if (gp->scale) or_scale(L, L->r);
+        for (int i = 0; i < L->n; ++i) L->x[i] = L->x[i] + L->c[i];
+        for (int s = 0; s < gp->n_post; ++s) or_jacobi_sweep(L, gp->omega);
+    }
+}
+
+/* Build the hierarchy (faceAreaPair weights = face areas): returns the number of levels;
+ * levels[0] is the fine mesh (arrays borrowed), coarser levels allocated. */
+int or_gamg_hierarchy(int n, int F, const int* owner, const int* neighbour, const double* weights,
+                      const or_gamg_params* gp, or_level* Lv, int max_out)
+{
+    int nl = 1;
+    Lv[0].n = n;
+    Lv[0].F = F;
+    Lv[0].owner = (int*)owner;
+    Lv[0].neighbour = (int*)neighbour;
+    Lv[0].w = (double*)weights;
+    while (nl < max_out && nl < gp->max_levels && Lv[nl - 1].n > gp->n_coarsest_cells) {
+        or_level* L = &Lv[nl - 1];
+        L->ftc = (int*)malloc(sizeof(int) * (size_t)(L->n + 1));
+        const int nc = or_agglomerate(L->n, L->F, L->owner, L->neighbour, L->w, L->ftc);
+        if (nc >= L->n) {
+            free(L->ftc);
+            L->ftc = 0;
+            break;
+        }
+        or_level* C = &Lv[nl];
+        C->owner = (int*)malloc(sizeof(int) * (size_t)(L->F + 1));
+        C->neighbour = (int*)malloc(sizeof(int) * (size_t)(L->F + 1));
+        C->w = (double*)malloc(sizeof(double) * (size_t)(L->F + 1));
+        L->frestrict = (int*)malloc(sizeof(int) * (size_t)(L->F + 1));
+        C->F = or_coarse_addressing(L->F, L->owner, L->neighbour, L->ftc, L->w, C->owner, C->neighbour,
+                                    L->frestrict, C->w);
+        C->n = nc;
+        ++nl;
+    }
+    Lv[nl - 1].ftc = 0;
+    Lv[nl - 1].frestrict = 0;
+    return nl;
+}
+
+/* GAMG solve, OpenFOAM loop semantics (Q26): normFactor / residual as PCG (Q1);
+ * iterate V-cycles while ((++n < maxIter && !converged) || n < minIter). */
+int or_gamg(int n, int F, const int* owner, const int* neighbour, const double* weights, const double* diag,
+            const double* upper, const double* source, double* psi, const or_gamg_params* gp,
+            const or_controls* ctl, or_perf* perf, int* levels_out, int* level_cells)
+{
+    or_level Lv[64];
+    memset(Lv, 0, sizeof(Lv));
+    const int nl = or_gamg_hierarchy(n, F, owner, neighbour, weights, gp, Lv, 64);
+    for (int l = 0; l < nl; ++l) {
+        or_level* L = &Lv[l];
+        const size_t m = (size_t)L->n + 1;
+        L->b = (double*)calloc(m, sizeof(double));
+        L->x = (double*)calloc(m, sizeof(double));
+        L->r = (double*)calloc(m, sizeof(double));
+        L->y = (double*)calloc(m, sizeof(double));
+        L->c = (double*)calloc(m, sizeof(double));
+        L->rD = (double*)calloc(m, sizeof(double));
+        if (l == 0) {
+            L->diag = (double*)diag;
+            L->upper = (double*)upper;
+        } else {
+            L->diag = (double*)calloc(m, sizeof(double));
+            L->upper = (double*)calloc((size_t)L->F + 1, sizeof(double));
+            or_level* P = &Lv[l - 1];
+            or_agglomerate_matrix(P->n, P->F, P->owner, P->ftc, P->frestrict, P->diag, P->upper, L->n, L->F,
+                                  L->diag, L->upper);
+        }
+        for (int i = 0; i < L->n; ++i) L->rD[i] = 1.0 / L->diag[i];
+        if (level_cells && l < 64) level_cells[l] = L->n;
+    }
+    if (levels_out) *levels_out = nl;
+
+    /* residual and normFactor exactly as PCG (Q1) */
+    double* wA = (double*)calloc((size_t)n + 1, sizeof(double));
+    double* sumA = (double*)calloc((size_t)n + 1, sizeof(double));
+    double* r = (double*)calloc((size_t)n + 1, sizeof(double));
+    or_amul(n, F, owner, neighbour, diag, upper, upper, psi, 0, 0, 0, 0, wA);
+    for (int i = 0; i < n; ++i) r[i] = source[i] - wA[i];
+    double spsi = 0.0;
+    for (int i = 0; i < n; ++i) spsi += psi[i];
+    const double xbar = spsi / (double)n;
+    or_sumA(n, F, owner, neighbour, diag, upper, upper, 0, 0, 0, sumA);
+    double nf = 0.0;
+    for (int i = 0; i < n; ++i) {
+        const double xref = sumA[i] * xbar;
+        nf += fabs(wA[i] - xref) + fabs(source[i] - xref);
+    }
+    const double normFactor = nf + 1e-20;
+    double smag = 0.0;
+    for (int i = 0; i < n; ++i) smag += fabs(r[i]);
+    perf->initial_residual = smag / normFactor;
+    perf->final_residual = perf->initial_residual;
+    perf->n_iterations = 0;
+    perf->singular = 0;
+    if (ctl->min_iter > 0 || !or_conv(perf->final_residual, perf->initial_residual, ctl)) {
+        do {
+            for (int i = 0; i < n; ++i) Lv[0].b[i] = r[i];
+            if (nl == 1) {
+                or_coarsest_solve(&Lv[0], gp);
+            } else {
+                or_vcycle(nl, Lv, gp);
+            }
+            for (int i = 0; i < n; ++i) psi[i] = psi[i] + Lv[0].x[i];
+            or_amul(n, F, owner, neighbour, diag, upper, upper, psi, 0, 0, 0, 0, wA);
+            smag = 0.0;
+            for (int i = 0; i < n; ++i) {
+                r[i] = source[i] - wA[i];
+                smag += fabs(r[i]);
+            }
+            perf->final_residual = smag / normFactor;
+        } while ((++perf->n_iterations < ctl->max_iter && !or_conv(perf->final_residual, perf->initial_residual, ctl)) ||
+                 perf->n_iterations < ctl->min_iter);
+    }
+    perf->converged = or_conv(perf->final_residual, perf->initial_residual, ctl);
+    for (int l = 0; l < nl; ++l) {
+        or_level* L = &Lv[l];
+        free(L->b); free(L->x); free(L->r); free(L->y); free(L->c); free(L->rD);
+        free(L->ftc); free(L->frestrict);
+        if (l > 0) { free(L->diag); free(L->upper); free(L->owner); free(L->neighbour); free(L->w); }
+    }
+    free(wA);
+    free(sumA);
+    free(r);
     return 0;
 }
 

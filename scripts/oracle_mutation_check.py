@@ -29,7 +29,24 @@ muts = [
  ("if (bkind[b] != OR_EMPTY) out[bcells[b]] += bphi[b];", "out[bcells[b]] += bphi[b];"),
  ("for (int f = 0; f < n_faces; ++f) flux[f] = upper[f] * psi[neighbour[f]] - lower[f] * psi[owner[f]];", "for (int f = 0; f < n_faces; ++f) flux[f] = upper[f] * psi[owner[f]] - lower[f] * psi[neighbour[f]];"),
  ("bflux[b] = (gms * (-bdelta[b])) * psi[P] - ((-gms) * (bdelta[b] * bvalue[b]));", "bflux[b] = (gms * (-bdelta[b])) * psi[P] + ((-gms) * (bdelta[b] * bvalue[b]));"),
+ # O11 GAMG
+ ("if (ftc[o] < 0 && w[f] > bw) {", "if (ftc[o] < 0 && w[f] < bw + 1e300) {"),
+ ("ftc[c] = best >= 0 ? ftc[best] : nc++;", "ftc[c] = nc++;"),
+ ("else cdiag[ftc[owner[f]]] += upper[f] + upper[f];", "else cdiag[ftc[owner[f]]] += upper[f];"),
+ ("if (frestrict[f] >= 0) cupper[frestrict[f]] += upper[f];", "if (frestrict[f] >= 0) cupper[frestrict[f]] = upper[f];"),
+ ("for (int i = 0; i < n; ++i) coarse[ftc[i]] += fine[i];", "for (int i = 0; i < n; ++i) coarse[ftc[i]] = fine[i];"),
+ ("L->x[i] = L->x[i] + omega * (L->rD[i] * (L->b[i] - L->y[i]));", "L->x[i] = L->x[i] + omega * (L->b[i] - L->y[i]);"),
+ ("double a = fabs(den) > 1e-300 ? num / den : 1.0;", "double a = fabs(den) > 1e-300 ? den / num : 1.0;"),
+ ("if (a < 0.0) a = 0.0;", "if (a < -10.0) a = 0.0;"),
+ ("for (int i = 0; i < L->n; ++i) L->c[i] = Lv[l + 1].x[L->ftc[i]];", "for (int i = 0; i < L->n; ++i) L->c[i] = Lv[l + 1].x[L->ftc[i] / 2];"),
+ ("for (int s = 0; s < gp->n_pre; ++s) or_jacobi_sweep(L, gp->omega);", ";"),
+ ("for (int i = 0; i < L->n; ++i) L->r[i] = L->b[i] - L->y[i];", "for (int i = 0; i < L->n; ++i) L->r[i] = L->b[i];"),
+ ("cw[l] += w[f];", "cw[l] = w[f];"),
+ ("for (int i = 0; i < n; ++i) psi[i] = psi[i] + Lv[0].x[i];", "for (int i = 0; i < n; ++i) psi[i] = psi[i] - Lv[0].x[i];"),
 ]
+sel = os.environ.get("MUT_SELECT")  # e.g. "GAMG": only mutants after that marker
+if sel == "GAMG":
+    muts = muts[[a for a, _ in muts].index("if (ftc[o] < 0 && w[f] > bw) {"):]
 res = []
 for a, b in muts:
     assert a in src, a
