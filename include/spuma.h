@@ -182,6 +182,54 @@ spuma_status spuma_pcg_solve(spuma_mesh m, const spuma_scalar* diag, const spuma
 /* Release everything the handle owns (NULL-safe). */
 void spuma_free(spuma_mesh m);
 
+/* ---------------- GAMG with the Richardson smoother ----------------
+ * PAPER.md P:665 ("GAMG ... Richardson smoother ... diagonal at the coarsest level"),
+ * pGAMG controls P:1043-1052, profile rows restrictField / prolongField /
+ * agglomerateMatrix / scale / Vcycle P:517-545.  Readings Q22-Q28:
+ * faceAreaPair pairwise agglomeration on |S_f| (Q22), Galerkin coarse matrices (Q27),
+ * V-cycle in correction form (Q23) with weighted-Jacobi sweeps (Q24), energy-optimal
+ * correction scaling clamped to [0, 2] (Q25), PCG + diagonal at the coarsest level (Q26),
+ * PCG's normFactor / convergence / loop semantics with one V-cycle per iteration (Q28). */
+typedef struct spuma_gamg_params {
+    int n_pre_sweeps;               /* Richardson sweeps before restriction (default 0)           */
+    int n_post_sweeps;              /* sweeps after the coarse correction (default 2)             */
+    int scale_correction;           /* 1: scale the prolonged correction (default 1)              */
+    int n_cells_in_coarsest_level;  /* coarsening stops at or below this many cells (default 10)  */
+    int max_levels;                 /* including the finest (default 50)                          */
+    double omega;                   /* Richardson weight (default 0.75)                           */
+    double coarsest_tolerance;      /* coarsest PCG tolerance (default 0)                         */
+    double coarsest_rel_tol;        /* coarsest PCG relTol (default 1e-6)                         */
+    int coarsest_max_iter;          /* coarsest PCG maxIter (default 1000)                        */
+} spuma_gamg_params;
+
+/* Fill *p with the defaults above. */
+void spuma_gamg_default_params(spuma_gamg_params* p);
+
+/*
+ * Solve A psi = source by GAMG (arguments as spuma_pcg_solve; params NULL: defaults).
+ * The level hierarchy depends only on the mesh, n_cells_in_coarsest_level and max_levels:
+ * it is built on the host at the first call (and when those change) and kept by the
+ * handle; every call re-forms the coarse matrices from diag/upper on the device.
+ * perf->n_iterations counts V-cycles.  Single-rank handles only (n_ranks > 1 ->
+ * SPUMA_ERR_STATE: coarse-level processor interfaces are out of scope, Q28).
+ * Errors: INVALID_ARGUMENT (NULL arrays/perf, negative limits, max_levels < 1,
+ * n_post_sweeps/n_pre_sweeps < 0), STATE, CUDA, OUT_OF_MEMORY.
+ */
+spuma_status spuma_gamg_solve(spuma_mesh m, const spuma_scalar* diag, const spuma_scalar* upper,
+                              const spuma_scalar* iface_coeffs, const spuma_scalar* source, spuma_scalar* psi,
+                              const spuma_solver_controls* ctl, const spuma_gamg_params* params,
+                              spuma_solver_perf* perf);
+
+/*
+ * Diagnostics of the hierarchy built by the last spuma_gamg_solve (or built now from
+ * params, NULL: defaults): *n_levels; level_cells / level_faces [max_levels] (may be
+ * NULL); ftc: if non-NULL and level < *n_levels - 1, the fine-to-coarse map of that
+ * level [cells of the level], in the handle's INTERNAL numbering (spuma_mesh_get_addressing).
+ */
+spuma_status spuma_gamg_get_hierarchy(spuma_mesh m, const spuma_gamg_params* params, int max_levels,
+                                      int* n_levels, int* level_cells, int* level_faces, int level,
+                                      spuma_label* ftc);
+
 /* ---------------- around the path (the pressure step's neighbours) ----------------
  * Oriented face fields (phi, flux) are owner -> neighbour in the CALLER's numbering; with
  * renumber = 1 faces whose owner/neighbour swapped are negated on entry and exit.  Per-patch

@@ -421,6 +421,255 @@ spuma_status account_timing(spuma_mesh m, int g, int executed)
     return SPUMA_OK;
 }
 
+
+// ---------------------------------------------------------------------------
+// GAMG: hierarchy on the device, per-solve Galerkin products, one
+// captured V-cycle + residual per iteration (kernels in gamg.cu)
+// ---------------------------------------------------------------------------
+}  // namespace
+
+struct GamgState {
+    int n_coarsest = -1, max_levels = -1;            // key of the hierarchy
+    std::vector<spuma::GLevel> lv;
+    std::vector<int> cells, faces;
+    std::vector<std::vector<int>> ftc;               // host copies (diagnostics)
+    std::vector<void*> allocs;
+    double *alpha = nullptr, *part = nullptr;        // per-level scale factors, reduction partials
+    unsigned* ticket = nullptr;
+    spuma::Workspace cws{};                          // coarsest-level PCG
+    spuma::DevPtrs* h_cptrs = nullptr;               // pinned
+    cudaGraphExec_t gexec = nullptr;
+    spuma_gamg_params gkey{};
+    int launches_per_cycle = 0;
+};
+
+namespace {
+
+void gamg_release(spuma_mesh m)
+{
+    GamgState* G = m->gamg;
+    if (!G) return;
+    if (m->stream) cudaStreamSynchronize(m->stream);
+    if (G->gexec) cudaGraphExecDestroy(G->gexec);
+    for (void* p : G->allocs)
+        if (p) cudaFree(p);
+    if (G->h_cptrs) cudaFreeHost(G->h_cptrs);
+    delete G;
+    m->gamg = nullptr;
+}
+
+template <class T>
+spuma_status galloc(GamgState* G, T** p, size_t n)
+{
+    SPUMA_TRY(dalloc(p, n));
+    G->allocs.push_back(*p);
+    return SPUMA_OK;
+}
+
+template <class T>
+spuma_status gupload(GamgState* G, T** p, const std::vector<T>& v, cudaStream_t s)
+{
+    SPUMA_TRY(upload(p, v, s));
+    G->allocs.push_back(*p);
+    return SPUMA_OK;
+}
+
+spuma_status gamg_ensure(spuma_mesh m, const spuma_gamg_params& gp)
+{
+    if (m->gamg && m->gamg->n_coarsest == gp.n_cells_in_coarsest_level && m->gamg->max_levels == gp.max_levels)
+        return SPUMA_OK;
+    gamg_release(m);
+    cudaStream_t s = m->stream;
+    std::vector<double> w(m->F);
+    if (m->F) SPUMA_CUDA(cudaMemcpy(w.data(), m->d_magSf, sizeof(double) * m->F, cudaMemcpyDeviceToHost));
+    std::vector<int> ownerLo(m->F);
+    for (int k = 0; k < m->F; ++k) ownerLo[k] = m->h_owner[m->h_losort[k]];
+    std::vector<GamgHostLevel> H =
+        gamg_hierarchy(m->N, m->F, m->h_owner, m->h_neighbour, m->h_ownerStart, m->h_losortStart, m->h_losort,
+                       ownerLo, w, gp.n_cells_in_coarsest_level, gp.max_levels);
+    GamgState* G = new GamgState();
+    m->gamg = G;
+    G->n_coarsest = gp.n_cells_in_coarsest_level;
+    G->max_levels = gp.max_levels;
+    const int nl = (int)H.size();
+    G->lv.resize(nl);
+    int max_grid = 1;
+    for (int l = 0; l < nl; ++l) {
+        GamgHostLevel& h = H[l];
+        GLevel& L = G->lv[l];
+        L = GLevel{};
+        const int n = h.n;
+        G->cells.push_back(n);
+        G->faces.push_back(h.F);
+        if (l == 0) {
+            L.a = mesh_args(m);
+            L.a.ifStart = nullptr;
+            L.a.ifMask = nullptr;
+            L.a.n_iface = 0;
+            L.rD = m->ws.rD;
+            L.b = m->ws.rA;
+        } else {
+            L.a = MeshArgs{};
+            L.a.N = n;
+            L.a.F = h.F;
+            int *os, *ls, *lo, *olo, *nb, *ow;
+            SPUMA_TRY(gupload(G, &os, h.ownerStart, s));
+            SPUMA_TRY(gupload(G, &ls, h.losortStart, s));
+            SPUMA_TRY(gupload(G, &lo, h.losort, s));
+            SPUMA_TRY(gupload(G, &olo, h.ownerLo, s));
+            SPUMA_TRY(gupload(G, &nb, h.neighbour, s));
+            SPUMA_TRY(gupload(G, &ow, h.owner, s));
+            L.a.ownerStart = os;
+            L.a.losortStart = ls;
+            L.a.losort = lo;
+            L.a.ownerLo = olo;
+            L.a.neighbour = nb;
+            L.a.owner = ow;
+            SPUMA_TRY(galloc(G, &L.diag, n));
+            SPUMA_TRY(galloc(G, &L.upper, h.F));
+            SPUMA_TRY(galloc(G, &L.b, n));
+        }
+        SPUMA_TRY(galloc(G, &L.x, n));
+        SPUMA_TRY(galloc(G, &L.x2, n));
+        SPUMA_TRY(galloc(G, &L.r, n));
+        SPUMA_TRY(galloc(G, &L.p, n));
+        SPUMA_TRY(galloc(G, &L.q, n));
+        L.grid = gamg_grid(n);
+        max_grid = std::max(max_grid, L.grid);
+        if (l + 1 < nl) {
+            int *ftc, *cs, *cl, *cis, *cil, *cfs, *cfl;
+            SPUMA_TRY(gupload(G, &ftc, h.ftc, s));
+            SPUMA_TRY(gupload(G, &cs, h.cStart, s));
+            SPUMA_TRY(gupload(G, &cl, h.cList, s));
+            SPUMA_TRY(gupload(G, &cis, h.ciStart, s));
+            SPUMA_TRY(gupload(G, &cil, h.ciList, s));
+            SPUMA_TRY(gupload(G, &cfs, h.cfStart, s));
+            SPUMA_TRY(gupload(G, &cfl, h.cfList, s));
+            L.ftc = ftc;
+            L.cStart = cs;
+            L.cList = cl;
+            L.ciStart = cis;
+            L.ciList = cil;
+            L.cfStart = cfs;
+            L.cfList = cfl;
+            L.nc = H[l + 1].n;
+            L.ncf = H[l + 1].F;
+            G->ftc.push_back(h.ftc);
+        }
+        h = GamgHostLevel{};  // release host memory early
+    }
+    SPUMA_TRY(galloc(G, &G->alpha, nl));
+    SPUMA_TRY(galloc(G, &G->part, (size_t)kMaxPartials * max_grid));
+    SPUMA_TRY(galloc(G, &G->ticket, 4));
+    const int nc = G->cells[nl - 1];
+    Workspace& c = G->cws;
+    SPUMA_TRY(galloc(G, &c.wA, nc));
+    SPUMA_TRY(galloc(G, &c.rA, nc));
+    SPUMA_TRY(galloc(G, &c.pA, nc));
+    SPUMA_TRY(galloc(G, &c.rD, nc));
+    SPUMA_TRY(galloc(G, &c.sumA, nc));
+    c.pA_prev = c.pA;
+    SPUMA_TRY(galloc(G, &c.part, kMaxPartials));
+    SPUMA_TRY(galloc(G, &c.scal, 1));
+    SPUMA_TRY(galloc(G, &c.ptrs, 1));
+    SPUMA_CUDA(cudaMallocHost(reinterpret_cast<void**>(&G->h_cptrs), sizeof(DevPtrs)));
+    SPUMA_CUDA(cudaStreamSynchronize(s));
+    return SPUMA_OK;
+}
+
+// One V-cycle (Q23) + the outer residual (Q28), enqueued on s (captured or direct).
+int gamg_enqueue_cycle(spuma_mesh m, const spuma_gamg_params& gp, cudaStream_t s)
+{
+    GamgState* G = m->gamg;
+    const DevPtrs* P = m->ws.ptrs;
+    const int nl = (int)G->lv.size();
+    std::vector<GLevel>& lv = G->lv;
+    int k = 0;
+    Workspace w0 = m->ws;
+    w0.part = G->part;
+    if (nl == 1) {  // the finest level is the coarsest: exact-ish solve of A x = r, psi += x
+        cudaMemsetAsync(lv[0].x, 0, sizeof(double) * lv[0].a.N, s);
+        launch_pcg_single(s, lv[0].a, G->cws);
+        launch_add(s, lv[0].a.N, lv[0].x, m->h_ptrs->psi);
+        launch_gamg_residual(s, lv[0], w0);
+        return 3;
+    }
+    std::vector<double*> xcur(nl, nullptr);  // buffer holding x_l; nullptr: x_l == 0
+    for (int l = 0; l + 1 < nl; ++l) {
+        GLevel& L = lv[l];
+        double* xl = nullptr;
+        if (gp.n_pre_sweeps > 0) {
+            cudaMemsetAsync(L.x, 0, sizeof(double) * L.a.N, s);
+            double *xin = L.x, *xout = L.x2;
+            for (int i = 0; i < gp.n_pre_sweeps; ++i, ++k) {
+                launch_gamg_smooth(s, L, P, xin, xout, gp.omega, nullptr, nullptr, false);
+                std::swap(xin, xout);
+            }
+            xl = xin;
+        }
+        launch_gamg_restrict(s, L, lv[l + 1], P, xl);
+        ++k;
+        xcur[l] = xl;
+    }
+    GLevel& Lc = lv[nl - 1];
+    cudaMemsetAsync(Lc.x, 0, sizeof(double) * Lc.a.N, s);
+    launch_pcg_single(s, Lc.a, G->cws);
+    ++k;
+    xcur[nl - 1] = Lc.x;
+    for (int l = nl - 2; l >= 0; --l) {
+        GLevel& L = lv[l];
+        const double* xc = xcur[l + 1];
+        const double* r = xcur[l] ? L.r : L.b;
+        double* out = xcur[l] == L.x ? L.x2 : L.x;
+        double* other = out == L.x ? L.x2 : L.x;
+        int done_sweeps = 0;
+        if (gp.scale_correction) {
+            launch_gamg_scale(s, L, P, xcur[l], xc, r, gp.omega, gp.n_post_sweeps > 0, G->part, G->ticket,
+                              G->alpha + l);
+            ++k;
+            if (gp.n_post_sweeps > 0) {  // sweeps 1 (+2) in one kernel, sweep 1 prepared by the scale
+                const bool two = gp.n_post_sweeps >= 2;
+                done_sweeps = two ? 2 : 1;
+                const bool acc = l == 0 && done_sweeps == gp.n_post_sweeps;
+                launch_gamg_post(s, L, P, G->alpha + l, gp.omega, out, two, acc);
+                ++k;
+                if (!acc) {
+                    xcur[l] = out;
+                    std::swap(out, other);
+                }
+            } else {
+                launch_gamg_correct(s, L, P, xcur[l], xc, G->alpha + l, out, l == 0);
+                xcur[l] = out;
+                ++k;
+                std::swap(out, other);
+            }
+        } else if (gp.n_post_sweeps > 0) {  // unscaled: the correction is fused into the first sweep
+            const bool acc = l == 0 && gp.n_post_sweeps == 1;
+            launch_gamg_smooth(s, L, P, xcur[l], out, gp.omega, xc, nullptr, acc);
+            done_sweeps = 1;
+            ++k;
+            if (!acc) {
+                xcur[l] = out;
+                std::swap(out, other);
+            }
+        } else {
+            launch_gamg_correct(s, L, P, xcur[l], xc, nullptr, out, l == 0);
+            xcur[l] = out;
+            ++k;
+        }
+        for (int i = done_sweeps; i < gp.n_post_sweeps; ++i, ++k) {
+            const bool last = i + 1 == gp.n_post_sweeps;
+            launch_gamg_smooth(s, L, P, xcur[l], out, gp.omega, nullptr, nullptr, l == 0 && last);
+            if (!(l == 0 && last)) {
+                xcur[l] = out;
+                std::swap(out, other);
+            }
+        }
+    }
+    launch_gamg_residual(s, lv[0], w0);
+    return k + 1;
+}
+
 uint64_t launches_per_iteration(spuma_mesh m)
 {
     uint64_t k = 3;
@@ -454,6 +703,7 @@ void spuma_free(spuma_mesh m)
     if (!m) return;
     if (m->stream) cudaStreamSynchronize(m->stream);
     destroy_graphs(m);
+    gamg_release(m);
     for (int i = 0; i < 2; ++i) {
         if (m->batch_done[i]) cudaEventDestroy(m->batch_done[i]);
         if (m->asm_ev[i]) cudaEventDestroy(m->asm_ev[i]);
@@ -1250,6 +1500,141 @@ spuma_status spuma_set_batch(spuma_mesh m, int iterations)
     if (!m) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "mesh is NULL");
     if (iterations < 1 || iterations > 256) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "batch out of range");
     m->batch = iterations;
+    return SPUMA_OK;
+}
+
+
+void spuma_gamg_default_params(spuma_gamg_params* p)
+{
+    if (!p) return;
+    p->n_pre_sweeps = 0;
+    p->n_post_sweeps = 2;
+    p->scale_correction = 1;
+    p->n_cells_in_coarsest_level = 10;
+    p->max_levels = 50;
+    p->omega = 0.75;
+    p->coarsest_tolerance = 0.0;
+    p->coarsest_rel_tol = 1e-6;
+    p->coarsest_max_iter = 1000;
+}
+
+static spuma_status gamg_check_params(const spuma_gamg_params& gp)
+{
+    if (gp.n_pre_sweeps < 0 || gp.n_post_sweeps < 0 || gp.max_levels < 1 || gp.coarsest_max_iter < 0)
+        return set_error(SPUMA_ERR_INVALID_ARGUMENT, "invalid GAMG parameters");
+    return SPUMA_OK;
+}
+
+spuma_status spuma_gamg_solve(spuma_mesh m, const spuma_scalar* diag, const spuma_scalar* upper,
+                              const spuma_scalar* iface_coeffs, const spuma_scalar* source, spuma_scalar* psi,
+                              const spuma_solver_controls* ctl, const spuma_gamg_params* params,
+                              spuma_solver_perf* perf)
+{
+    (void)iface_coeffs;
+    if (!m) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "mesh is NULL");
+    if (!ctl || !perf) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "NULL controls/perf");
+    if (m->n_ranks > 1) return set_error(SPUMA_ERR_STATE, "GAMG is single-rank (DESIGN.md Q28)");
+    if (m->N > 0 && (!diag || !source || !psi)) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "NULL array");
+    if (m->F > 0 && !upper) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "upper is NULL");
+    if (ctl->max_iter < 0 || ctl->min_iter < 0) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "negative iteration limit");
+    spuma_gamg_params gp;
+    spuma_gamg_default_params(&gp);
+    if (params) gp = *params;
+    SPUMA_TRY(gamg_check_params(gp));
+    if (m->N == 0) {
+        *perf = spuma_solver_perf{};
+        return SPUMA_OK;
+    }
+    cudaStream_t s = m->stream;
+    DevPtrs P{};
+    const double* psi_in = nullptr;
+    SPUMA_TRY(cells_in(m, diag, R_DIAG, &P.diag));
+    SPUMA_TRY(faces_in(m, upper, &P.upper));
+    SPUMA_TRY(cells_in(m, source, R_SOURCE, &P.source));
+    SPUMA_TRY(cells_in(m, psi, R_PSI, &psi_in));
+    P.psi = const_cast<double*>(psi_in);
+    SPUMA_TRY(gamg_ensure(m, gp));
+    GamgState* G = m->gamg;
+    const int nl = (int)G->lv.size();
+    *m->h_ptrs = P;
+    SPUMA_CUDA(cudaMemcpyAsync(m->ws.ptrs, m->h_ptrs, sizeof(DevPtrs), cudaMemcpyHostToDevice, s));
+    const GLevel& Lc = G->lv[nl - 1];
+    *G->h_cptrs = DevPtrs{nl == 1 ? P.diag : Lc.diag, nl == 1 ? P.upper : Lc.upper, nullptr, Lc.b ? Lc.b : m->ws.rA,
+                          Lc.x};
+    SPUMA_CUDA(cudaMemcpyAsync(G->cws.ptrs, G->h_cptrs, sizeof(DevPtrs), cudaMemcpyHostToDevice, s));
+    // per-solve: Galerkin coarse matrices (Q27), outer scalars, coarsest PCG controls, A6 setup
+    for (int l = 0; l + 1 < nl; ++l) launch_gamg_agg(s, G->lv[l], G->lv[l + 1], m->ws.ptrs);
+    launch_scal_init(s, m->ws, *ctl, 1);
+    const spuma_solver_controls cc{gp.coarsest_tolerance, gp.coarsest_rel_tol, gp.coarsest_max_iter, 0};
+    launch_scal_init(s, G->cws, cc, 1);
+    const MeshArgs a0 = G->lv[0].a;
+    launch_setup1(s, m->grid, a0, m->ws, true);
+    launch_setup2(s, m->grid, a0, m->ws, true);
+    m->stats.kernel_launches += (uint64_t)(nl - 1) + 4;
+
+    // one V-cycle per graph launch (nl == 1: direct launches, psi is a per-call pointer)
+    const bool use_graph = nl > 1;
+    if (use_graph && (!G->gexec || std::memcmp(&G->gkey, &gp, sizeof gp) != 0)) {
+        if (G->gexec) cudaGraphExecDestroy(G->gexec);
+        G->gexec = nullptr;
+        cudaGraph_t graph = nullptr;
+        SPUMA_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        G->launches_per_cycle = gamg_enqueue_cycle(m, gp, s);
+        cudaError_t e = cudaStreamEndCapture(s, &graph);
+        SPUMA_CUDA(e);
+        e = cudaGraphInstantiate(&G->gexec, graph, 0);
+        cudaGraphDestroy(graph);
+        SPUMA_CUDA(e);
+        G->gkey = gp;
+    }
+    SPUMA_CUDA(cudaMemcpyAsync(&m->h_scal[0], m->ws.scal, sizeof(DevScal), cudaMemcpyDeviceToHost, s));
+    SPUMA_CUDA(cudaStreamSynchronize(s));
+    int cycles = 0;
+    while (!m->h_scal[0].done) {
+        if (use_graph) SPUMA_CUDA(cudaGraphLaunch(G->gexec, s));
+        else G->launches_per_cycle = gamg_enqueue_cycle(m, gp, s);
+        SPUMA_CUDA(cudaMemcpyAsync(&m->h_scal[0], m->ws.scal, sizeof(DevScal), cudaMemcpyDeviceToHost, s));
+        SPUMA_CUDA(cudaStreamSynchronize(s));
+        if (++cycles > ctl->max_iter + 1) return set_error(SPUMA_ERR_STATE, "GAMG loop did not terminate");
+    }
+    SPUMA_CUDA(cudaGetLastError());
+    m->stats.kernel_launches += (uint64_t)cycles * (uint64_t)G->launches_per_cycle;
+    const DevScal fs = m->h_scal[0];
+    perf->initial_residual = fs.init;
+    perf->final_residual = fs.fin;
+    perf->n_iterations = fs.n;
+    perf->converged = fs.converged;
+    perf->singular = 0;
+    m->stats.solves += 1;
+    m->stats.iterations += fs.n;
+    SPUMA_TRY(cells_out(m, psi, P.psi));
+    SPUMA_CUDA(cudaStreamSynchronize(s));
+    return SPUMA_OK;
+}
+
+spuma_status spuma_gamg_get_hierarchy(spuma_mesh m, const spuma_gamg_params* params, int max_levels,
+                                      int* n_levels, int* level_cells, int* level_faces, int level,
+                                      spuma_label* ftc)
+{
+    if (!m || !n_levels) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "NULL argument");
+    spuma_gamg_params gp;
+    spuma_gamg_default_params(&gp);
+    if (params) gp = *params;
+    else if (m->gamg) gp.n_cells_in_coarsest_level = m->gamg->n_coarsest, gp.max_levels = m->gamg->max_levels;
+    SPUMA_TRY(gamg_check_params(gp));
+    if (m->n_ranks > 1) return set_error(SPUMA_ERR_STATE, "GAMG is single-rank (DESIGN.md Q28)");
+    SPUMA_TRY(gamg_ensure(m, gp));
+    const GamgState* G = m->gamg;
+    const int nl = (int)G->lv.size();
+    *n_levels = nl;
+    for (int l = 0; l < nl && l < max_levels; ++l) {
+        if (level_cells) level_cells[l] = G->cells[l];
+        if (level_faces) level_faces[l] = G->faces[l];
+    }
+    if (ftc) {
+        if (level < 0 || level >= nl - 1) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "level has no coarser level");
+        std::memcpy(ftc, G->ftc[level].data(), sizeof(int) * G->ftc[level].size());
+    }
     return SPUMA_OK;
 }
 

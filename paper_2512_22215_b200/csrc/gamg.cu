@@ -1,0 +1,287 @@
+// gamg.cu -- sm_100a kernels of GAMG with the Richardson smoother (
+// PAPER.md P:665, profile rows P:517-545; readings Q22-Q28 in DESIGN.md §3).
+//
+// Every level is an lduAddressing mesh, so every operator is a per-row GATHER in the
+// oracle's face order (Q10) -- bitwise the oracle's row values (--fmad=false).  The
+// V-cycle fuses what the oracle does in separate passes where the data allows:
+//   restriction  b_{l+1}[C] = sum over the fine cells of C of (b - A x)  (one kernel per
+//                level, per COARSE cell; the residual is formed on the fly)
+//   prolongation + scale + first post-sweep: the correction x + alpha xc[ftc[j]] is
+//                evaluated inside the sweep's row gather, never stored
+//   last post-sweep on level 0 accumulates straight into psi
+// Reductions (scale factor, residual norm) use the fixed-shape last-CTA pattern.
+#include "device.cuh"
+#include "internal.h"
+
+namespace spuma {
+namespace {
+
+// row of A applied to an implicit vector x(j), in the oracle's order (Q10, no interfaces)
+template <class X>
+__device__ __forceinline__ double row_ax(const MeshArgs& a, int c, const double* __restrict__ diag,
+                                         const double* __restrict__ upper, const X& x)
+{
+    double s = diag[c] * x(c);
+    const int k1 = a.losortStart[c + 1];
+    for (int k = a.losortStart[c]; k < k1; ++k) s = s + upper[a.losort[k]] * x(a.ownerLo[k]);
+    const int f1 = a.ownerStart[c + 1];
+    for (int f = a.ownerStart[c]; f < f1; ++f) s = s + upper[f] * x(a.neighbour[f]);
+    return s;
+}
+
+struct XPlain {
+    const double* __restrict__ x;
+    __device__ __forceinline__ double operator()(int j) const { return x[j]; }
+};
+
+// x(j) = x[j] + alpha xc[ftc[j]]  (prolongation by injection, scaled; x == nullptr: zero)
+struct XCorr {
+    const double* __restrict__ x;
+    const double* __restrict__ xc;
+    const int* __restrict__ ftc;
+    double alpha;
+    __device__ __forceinline__ double operator()(int j) const
+    {
+        return (x ? x[j] : 0.0) + alpha * xc[ftc[j]];
+    }
+};
+
+struct XInj {  // c(j) = xc[ftc[j]]
+    const double* __restrict__ xc;
+    const int* __restrict__ ftc;
+    __device__ __forceinline__ double operator()(int j) const { return xc[ftc[j]]; }
+};
+
+__device__ __forceinline__ const double* level_diag(const GLevel& L, const DevPtrs* P)
+{
+    return L.diag ? L.diag : P->diag;
+}
+__device__ __forceinline__ const double* level_upper(const GLevel& L, const DevPtrs* P)
+{
+    return L.upper ? L.upper : P->upper;
+}
+
+// agglomerateMatrix (Q27): coarse diag = fine diags of the members (ascending) + (u + l) of
+// the agglomerate-internal faces (ascending); coarse upper = fine uppers of its faces.
+__global__ void __launch_bounds__(kThreads) k_gamg_agg(GLevel F, GLevel C, const DevPtrs* __restrict__ P)
+{
+    const double* __restrict__ fd = level_diag(F, P);
+    const double* __restrict__ fu = level_upper(F, P);
+    const int stride = gridDim.x * blockDim.x;
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < F.nc; c += stride) {
+        double d = 0.0;
+        for (int k = F.cStart[c]; k < F.cStart[c + 1]; ++k) d = d + fd[F.cList[k]];
+        for (int k = F.ciStart[c]; k < F.ciStart[c + 1]; ++k) {
+            const double u = fu[F.ciList[k]];
+            d = d + (u + u);
+        }
+        C.diag[c] = d;
+    }
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < F.ncf; e += stride) {
+        double u = 0.0;
+        for (int k = F.cfStart[e]; k < F.cfStart[e + 1]; ++k) u = u + fu[F.cfList[k]];
+        C.upper[e] = u;
+    }
+}
+
+// restrictField of the residual (Q23): C.b[c] = sum_{i in c} (b_i - (A x)_i); r_i stored
+// for the scale step when x is not zero.
+__global__ void __launch_bounds__(kThreads) k_gamg_restrict(GLevel F, GLevel C, const DevPtrs* __restrict__ P,
+                                                            const double* __restrict__ x)
+{
+    const double* __restrict__ fd = level_diag(F, P);
+    const double* __restrict__ fu = level_upper(F, P);
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < F.nc; c += gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int k = F.cStart[c]; k < F.cStart[c + 1]; ++k) {
+            const int i = F.cList[k];
+            double r = F.b[i];
+            if (x) {
+                r = r - row_ax(F.a, i, fd, fu, XPlain{x});
+                F.r[i] = r;
+            }
+            s = s + r;
+        }
+        C.b[c] = s;
+    }
+}
+
+// Richardson sweep (Q24): xout = x + omega (rD (b - A x)), x = xin or (xin + alpha xc[ftc])
+// when xc is given (the prolonged correction of the first post-sweep); psi_acc: psi += xout.
+__global__ void __launch_bounds__(kThreads) k_gamg_smooth(GLevel L, const DevPtrs* __restrict__ P,
+                                                          const double* __restrict__ xin, double* __restrict__ xout,
+                                                          double omega, const double* __restrict__ xc,
+                                                          const double* __restrict__ alpha, int psi_acc)
+{
+    const double* __restrict__ d = level_diag(L, P);
+    const double* __restrict__ u = level_upper(L, P);
+    double* __restrict__ psi = P->psi;
+    const double a = alpha ? *alpha : 1.0;
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < L.a.N; c += gridDim.x * blockDim.x) {
+        double xi, y;
+        if (xc) {
+            const XCorr X{xin, xc, L.ftc, a};
+            xi = X(c);
+            y = row_ax(L.a, c, d, u, X);
+        } else {
+            xi = xin[c];
+            y = row_ax(L.a, c, d, u, XPlain{xin});
+        }
+        const double xn = xi + omega * ((1.0 / d[c]) * (L.b[c] - y));
+        if (psi_acc) psi[c] = psi[c] + xn;
+        else xout[c] = xn;
+    }
+}
+
+// GAMGSolver::scale reading (Q25): alpha = (c.r)/(c.Ac) clamped to [0, 2], c = xc[ftc].
+// With pq (nPost >= 1) the first post-sweep is prepared here, split by linearity in alpha
+// (reading Q29): with x' = x + alpha c,  A x' = (b - r) + alpha Ac, so the sweep
+//   x1 = x' + omega rD (r - alpha Ac) = alpha p + q,
+//   p = c - omega rD Ac,  q = x + omega rD r       (x = pre-smoothed correction or 0)
+// and k_gamg_post needs two direct loads per neighbour instead of a gather of its own.
+__global__ void __launch_bounds__(kThreads) k_gamg_scale(GLevel L, const DevPtrs* __restrict__ P,
+                                                         const double* __restrict__ x, const double* __restrict__ xc,
+                                                         const double* __restrict__ r, double omega, int pq,
+                                                         double* part, unsigned* ticket, double* alpha)
+{
+    const double* __restrict__ d = level_diag(L, P);
+    const double* __restrict__ u = level_upper(L, P);
+    const XInj X{xc, L.ftc};
+    double v[2] = {0.0, 0.0};
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < L.a.N; c += gridDim.x * blockDim.x) {
+        const double ci = X(c);
+        const double aci = row_ax(L.a, c, d, u, X);
+        const double ri = r[c];
+        if (pq) {
+            const double rd = 1.0 / d[c];
+            L.p[c] = ci - omega * (rd * aci);
+            L.q[c] = (x ? x[c] : 0.0) + omega * (rd * ri);
+        }
+        v[0] += ci * ri;
+        v[1] += aci * ci;
+    }
+    if (grid_sum<2>(v, part, ticket) && threadIdx.x == 0) {
+        double a = fabs(v[1]) > 1e-300 ? v[0] / v[1] : 1.0;
+        a = a < 0.0 ? 0.0 : (a > 2.0 ? 2.0 : a);
+        *alpha = a;
+    }
+}
+
+// x + alpha xc[ftc] without a post-sweep (nPost = 0); psi_acc: psi += it
+__global__ void __launch_bounds__(kThreads) k_gamg_correct(GLevel L, const DevPtrs* __restrict__ P,
+                                                           const double* __restrict__ x, const double* __restrict__ xc,
+                                                           const double* __restrict__ alpha, double* __restrict__ out,
+                                                           int psi_acc)
+{
+    const XCorr X{x, xc, L.ftc, alpha ? *alpha : 1.0};
+    double* __restrict__ psi = P->psi;
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < L.a.N; c += gridDim.x * blockDim.x) {
+        const double xn = X(c);
+        if (psi_acc) psi[c] = psi[c] + xn;
+        else out[c] = xn;
+    }
+}
+
+struct XPQ {  // x1(j) = alpha p_j + q_j
+    const double* __restrict__ p;
+    const double* __restrict__ q;
+    double alpha;
+    __device__ __forceinline__ double operator()(int j) const { return alpha * p[j] + q[j]; }
+};
+
+// Post-sweeps 1 (+2) after k_gamg_scale: x1 = alpha p + q; two: x2 = x1 + omega rD (b - A x1)
+// in one gather with x1 formed at the neighbours.  psi_acc: psi += result.
+__global__ void __launch_bounds__(kThreads) k_gamg_post(GLevel L, const DevPtrs* __restrict__ P,
+                                                        const double* __restrict__ alpha, double omega,
+                                                        double* __restrict__ out, int two, int psi_acc)
+{
+    const double* __restrict__ d = level_diag(L, P);
+    const double* __restrict__ u = level_upper(L, P);
+    double* __restrict__ psi = P->psi;
+    const XPQ X{L.p, L.q, *alpha};
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < L.a.N; c += gridDim.x * blockDim.x) {
+        const double x1 = X(c);
+        double xn = x1;
+        if (two) xn = x1 + omega * ((1.0 / d[c]) * (L.b[c] - row_ax(L.a, c, d, u, X)));
+        if (psi_acc) psi[c] = psi[c] + xn;
+        else out[c] = xn;
+    }
+}
+
+// end of a GAMG iteration (Q28): rA = source - A psi, final residual, n++, convergence, done
+__global__ void __launch_bounds__(kThreads) k_gamg_residual(GLevel L, Workspace w)
+{
+    const DevPtrs p = *w.ptrs;
+    double v[1] = {0.0};
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < L.a.N; c += gridDim.x * blockDim.x) {
+        const double r = p.source[c] - row_ax(L.a, c, p.diag, p.upper, XPlain{p.psi});
+        w.rA[c] = r;
+        v[0] += fabs(r);
+    }
+    if (grid_sum<1>(v, w.part, &w.scal->ticket[2]) && threadIdx.x == 0) {
+        DevScal* s = w.scal;
+        s->fin = v[0] / s->normFactor;
+        s->n = s->n + 1;
+        const bool c = conv(s->fin, s->init, s->tol, s->rel_tol);
+        s->converged = c;
+        if (!((s->n < s->max_iter && !c) || s->n < s->min_iter)) s->done = 1;
+    }
+}
+
+}  // namespace
+
+static int g_gamg_max_grid = 0;
+
+int gamg_grid(int n)
+{
+    if (!g_gamg_max_grid) {
+        int dev = 0, sms = 148, occ = 4;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gamg_smooth, kThreads, 0);
+        g_gamg_max_grid = sms * (occ > 0 ? occ : 1);
+    }
+    const int g = (n + kThreads - 1) / kThreads;
+    return g < 1 ? 1 : (g > g_gamg_max_grid ? g_gamg_max_grid : g);
+}
+
+void launch_gamg_agg(cudaStream_t s, const GLevel& fine, const GLevel& coarse, const DevPtrs* P)
+{
+    k_gamg_agg<<<gamg_grid(fine.nc > fine.ncf ? fine.nc : fine.ncf), kThreads, 0, s>>>(fine, coarse, P);
+}
+
+void launch_gamg_restrict(cudaStream_t s, const GLevel& fine, const GLevel& coarse, const DevPtrs* P, const double* x)
+{
+    k_gamg_restrict<<<gamg_grid(fine.nc), kThreads, 0, s>>>(fine, coarse, P, x);
+}
+
+void launch_gamg_smooth(cudaStream_t s, const GLevel& L, const DevPtrs* P, const double* xin, double* xout,
+                        double omega, const double* xc, const double* alpha, bool psi_acc)
+{
+    k_gamg_smooth<<<L.grid, kThreads, 0, s>>>(L, P, xin, xout, omega, xc, alpha, psi_acc ? 1 : 0);
+}
+
+void launch_gamg_scale(cudaStream_t s, const GLevel& L, const DevPtrs* P, const double* x, const double* xc,
+                       const double* r, double omega, bool pq, double* part, unsigned* ticket, double* alpha)
+{
+    k_gamg_scale<<<L.grid, kThreads, 0, s>>>(L, P, x, xc, r, omega, pq ? 1 : 0, part, ticket, alpha);
+}
+
+void launch_gamg_correct(cudaStream_t s, const GLevel& L, const DevPtrs* P, const double* x, const double* xc,
+                         const double* alpha, double* out, bool psi_acc)
+{
+    k_gamg_correct<<<L.grid, kThreads, 0, s>>>(L, P, x, xc, alpha, out, psi_acc ? 1 : 0);
+}
+
+void launch_gamg_post(cudaStream_t s, const GLevel& L, const DevPtrs* P, const double* alpha, double omega,
+                      double* out, bool two, bool psi_acc)
+{
+    k_gamg_post<<<L.grid, kThreads, 0, s>>>(L, P, alpha, omega, out, two ? 1 : 0, psi_acc ? 1 : 0);
+}
+
+void launch_gamg_residual(cudaStream_t s, const GLevel& L, const Workspace& w)
+{
+    k_gamg_residual<<<L.grid, kThreads, 0, s>>>(L, w);
+}
+
+}  // namespace spuma

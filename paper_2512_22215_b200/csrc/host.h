@@ -28,4 +28,25 @@ SellHost build_sell(int N, const std::vector<int>& ownerStart, const std::vector
 // per-cell lists of the items i with keep[i], in input order
 void cell_lists(int N, const std::vector<int>& cell_of, const std::vector<char>& keep, std::vector<int>& start,
                 std::vector<int>& items);
+
+// GAMG hierarchy (readings Q22, Q27).  Level l's arrays; ftc and the
+// next level's agglomeration lists are empty on the coarsest level.
+struct GamgHostLevel {
+    int n = 0, F = 0;
+    std::vector<int> owner, neighbour, ownerStart, losort, losortStart, ownerLo;  // l >= 1 (level 0: the mesh's)
+    std::vector<double> w;                      // face weights (level 0: |Sf|)
+    std::vector<int> ftc;                       // [n] fine -> coarse cell of the next level
+    std::vector<int> frestrict;                 // [F] fine face -> coarse face, -1 inside an agglomerate
+    std::vector<int> cStart, cList;             // next level: coarse cell -> fine cells (ascending)
+    std::vector<int> ciStart, ciList;           // next level: coarse cell -> agglomerate-internal fine faces
+    std::vector<int> cfStart, cfList;           // next level: coarse face -> fine faces (ascending)
+};
+// Levels are added while the current level has more than n_coarsest cells, the pairwise
+// pass reduces the count and fewer than max_levels exist.  Level 0 takes the given
+// addressing (sorted lduAddressing + derived arrays) and weights.
+std::vector<GamgHostLevel> gamg_hierarchy(int N, int F, const std::vector<int>& owner,
+                                          const std::vector<int>& neighbour, const std::vector<int>& ownerStart,
+                                          const std::vector<int>& losortStart, const std::vector<int>& losort,
+                                          const std::vector<int>& ownerLo, const std::vector<double>& w,
+                                          int n_coarsest, int max_levels);
 }  // namespace spuma

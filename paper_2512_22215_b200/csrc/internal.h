@@ -70,6 +70,24 @@ struct Workspace {
     DevPtrs* ptrs;
 };
 
+// One GAMG level on the device, captured by value.  Level 0 reads its
+// matrix, source and psi through DevPtrs (per-call pointers); its b is Workspace::rA.
+struct GLevel {
+    MeshArgs a;                   // this level's lduAddressing (no interfaces, no SELL)
+    double* diag;                 // nullptr on level 0
+    double* upper;                // nullptr on level 0
+    double* rD;                   // 1/diag
+    double* b;                    // right-hand side of the level's correction equation
+    double *x, *x2, *r;           // correction (ping-pong) and residual after pre-smoothing
+    double *p, *q;                // first post-sweep = alpha p + q (k_gamg_scale / k_gamg_post)
+    const int* ftc;               // [N] -> next level's cell, nullptr on the coarsest
+    const int *cStart, *cList;    // next level: coarse cell -> fine cells
+    const int *ciStart, *ciList;  // next level: coarse cell -> agglomerate-internal fine faces
+    const int *cfStart, *cfList;  // next level: coarse face -> fine faces
+    int nc, ncf;                  // next level's size
+    int grid;                     // CTAs of this level's cell kernels (fixed: deterministic reductions)
+};
+
 struct Patch {
     int kind, n_faces, offset;   // offset into the concatenated boundary arrays
     int neighbour_rank;          // processor
@@ -77,6 +95,8 @@ struct Patch {
 };
 
 }  // namespace spuma
+
+struct GamgState;  // api.cu
 
 struct spuma_mesh_s {
     int N = 0, F = 0, Fb = 0, n_iface = 0;
@@ -155,6 +175,7 @@ struct spuma_mesh_s {
     cudaEvent_t asm_ev[2] = {nullptr, nullptr};
 
     spuma_stats stats{};
+    GamgState* gamg = nullptr;  // GAMG hierarchy + captured cycle, built on first spuma_gamg_solve
 };
 
 // error plumbing (api.cu)
@@ -251,5 +272,19 @@ void launch_finalize(cudaStream_t s, int stage, const double* gathered, int n_ra
 void launch_scal_init(cudaStream_t s, const Workspace& w, const spuma_solver_controls& c, int n_ranks);
 void launch_pcg_single(cudaStream_t s, const MeshArgs& a, const Workspace& w);  // whole solve, 1 CTA
 int occupancy_grid(int N, int* grid_faces, int F);
+// GAMG (gamg.cu).  P = the handle's DevPtrs (level 0's matrix, source, psi).
+int gamg_grid(int n);
+void launch_gamg_agg(cudaStream_t s, const GLevel& fine, const GLevel& coarse, const DevPtrs* P);
+void launch_gamg_restrict(cudaStream_t s, const GLevel& fine, const GLevel& coarse, const DevPtrs* P,
+                          const double* x);                       // x nullptr: the level's x is zero
+void launch_gamg_smooth(cudaStream_t s, const GLevel& L, const DevPtrs* P, const double* xin, double* xout,
+                        double omega, const double* xc, const double* alpha, bool psi_acc);
+void launch_gamg_scale(cudaStream_t s, const GLevel& L, const DevPtrs* P, const double* x, const double* xc,
+                       const double* r, double omega, bool pq, double* part, unsigned* ticket, double* alpha);
+void launch_gamg_correct(cudaStream_t s, const GLevel& L, const DevPtrs* P, const double* x, const double* xc,
+                         const double* alpha, double* out, bool psi_acc);
+void launch_gamg_residual(cudaStream_t s, const GLevel& L, const Workspace& w);
+void launch_gamg_post(cudaStream_t s, const GLevel& L, const DevPtrs* P, const double* alpha, double omega,
+                      double* out, bool two, bool psi_acc);
 extern bool g_use_pdl;  // programmatic dependent launch of the hot-loop kernels (process-wide)
 }  // namespace spuma

@@ -63,6 +63,24 @@ class SolverPerf(ctypes.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class GamgParams(ctypes.Structure):
+    """spuma_gamg_params (include/spuma.h; readings Q22-Q28)."""
+    _fields_ = [("n_pre_sweeps", _ci), ("n_post_sweeps", _ci), ("scale_correction", _ci),
+                ("n_cells_in_coarsest_level", _ci), ("max_levels", _ci), ("omega", _cd),
+                ("coarsest_tolerance", _cd), ("coarsest_rel_tol", _cd), ("coarsest_max_iter", _ci)]
+
+
+def gamg_params(**kw) -> GamgParams:
+    """Defaults of spuma_gamg_default_params, overridden by keyword (field names above)."""
+    p = GamgParams()
+    lib().spuma_gamg_default_params(ctypes.byref(p))
+    for k, v in kw.items():
+        if k not in dict(GamgParams._fields_):
+            raise TypeError(f"unknown GAMG parameter {k}")
+        setattr(p, k, v)
+    return p
+
+
 EXCHANGE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_int),
                                ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
                                ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double))
@@ -119,6 +137,12 @@ def lib():
         L.spuma_nccl_get_unique_id.argtypes = [_vp]
         if hasattr(L, "spuma_set_comm_callbacks"):  # absent only in older A/B builds
             L.spuma_set_comm_callbacks.argtypes = [_vp, ctypes.POINTER(CommCallbacks)]
+        if hasattr(L, "spuma_gamg_solve"):
+            L.spuma_gamg_default_params.argtypes = [ctypes.POINTER(GamgParams)]
+            L.spuma_gamg_default_params.restype = None
+            L.spuma_gamg_solve.argtypes = [_vp] * 6 + [ctypes.POINTER(SolverControls), ctypes.POINTER(GamgParams),
+                                                       ctypes.POINTER(SolverPerf)]
+            L.spuma_gamg_get_hierarchy.argtypes = [_vp, ctypes.POINTER(GamgParams), _ci, _vp, _vp, _vp, _ci, _vp]
         L.spuma_last_error.restype = ctypes.c_char_p
         L.spuma_abi_version.restype = _ci
         for name in ("spuma_mesh_create", "spuma_assemble_laplacian", "spuma_pcg_solve", "spuma_amul",
@@ -271,6 +295,38 @@ class Mesh:
         p, kp = _ptr(psi, np.float64)
         _check(lib().spuma_pcg_solve(self._h, d, u, f, s, p, ctypes.byref(ctl), ctypes.byref(perf)))
         return perf.as_dict()
+
+    def gamg_solve(self, diag, upper, iface_coeffs, source, psi, tolerance=1e-6, rel_tol=0.0, max_iter=1000,
+                   min_iter=0, params: Optional[GamgParams] = None) -> dict:
+        """spuma_gamg_solve; psi updated in place; n_iterations = V-cycles."""
+        ctl = SolverControls(tolerance, rel_tol, max_iter, min_iter)
+        perf = SolverPerf()
+        d, kd = _ptr(diag, np.float64)
+        u, ku = _ptr(upper, np.float64)
+        f, kf = _ptr(iface_coeffs, np.float64)
+        s, ks = _ptr(source, np.float64)
+        p, kp = _ptr(psi, np.float64)
+        _check(lib().spuma_gamg_solve(self._h, d, u, f, s, p, ctypes.byref(ctl),
+                                      None if params is None else ctypes.byref(params), ctypes.byref(perf)))
+        return perf.as_dict()
+
+    def gamg_hierarchy(self, params: Optional[GamgParams] = None, with_ftc: bool = True) -> dict:
+        """spuma_gamg_get_hierarchy: level sizes and (internal-numbering) fine-to-coarse maps."""
+        nl = ctypes.c_int(0)
+        cells = np.zeros(64, np.int32)
+        faces = np.zeros(64, np.int32)
+        pp = None if params is None else ctypes.byref(params)
+        _check(lib().spuma_gamg_get_hierarchy(self._h, pp, 64, ctypes.addressof(nl), cells.ctypes.data,
+                                              faces.ctypes.data, -1, None))
+        n = nl.value
+        out = {"levels": n, "cells": cells[:n].tolist(), "faces": faces[:n].tolist(), "ftc": []}
+        if with_ftc:
+            for level in range(n - 1):
+                ftc = np.zeros(int(cells[level]), np.int32)
+                _check(lib().spuma_gamg_get_hierarchy(self._h, pp, 64, ctypes.addressof(nl), None, None, level,
+                                                      ftc.ctypes.data))
+                out["ftc"].append(ftc)
+        return out
 
     def amul(self, diag, upper, iface_coeffs, x, y):
         """spuma_amul: y = A x."""
