@@ -62,13 +62,18 @@ class GamgParams(ctypes.Structure):
     _fields_ = [("n_pre", ctypes.c_int), ("n_post", ctypes.c_int), ("scale", ctypes.c_int),
                 ("n_coarsest_cells", ctypes.c_int), ("max_levels", ctypes.c_int),
                 ("omega", ctypes.c_double), ("coarsest_tol", ctypes.c_double),
-                ("coarsest_rel_tol", ctypes.c_double), ("coarsest_max_iter", ctypes.c_int)]
+                ("coarsest_rel_tol", ctypes.c_double), ("coarsest_max_iter", ctypes.c_int),
+                ("smoother", ctypes.c_int), ("n_inner", ctypes.c_int)]
+
+
+RICHARDSON, GS2 = 0, 1
 
 
 def gamg_params(n_pre=0, n_post=2, scale=True, n_coarsest_cells=10, max_levels=50, omega=0.75,
-                coarsest_tol=0.0, coarsest_rel_tol=1e-6, coarsest_max_iter=1000) -> GamgParams:
+                coarsest_tol=0.0, coarsest_rel_tol=1e-6, coarsest_max_iter=1000, smoother=RICHARDSON,
+                n_inner=1) -> GamgParams:
     return GamgParams(n_pre, n_post, int(scale), n_coarsest_cells, max_levels, omega, coarsest_tol,
-                      coarsest_rel_tol, coarsest_max_iter)
+                      coarsest_rel_tol, coarsest_max_iter, smoother, n_inner)
 
 
 class _Domain(ctypes.Structure):

@@ -842,6 +842,8 @@ typedef struct {
     int n_pre, n_post, scale, n_coarsest_cells, max_levels;
     double omega, coarsest_tol, coarsest_rel_tol;
     int coarsest_max_iter;
+    int smoother; /* 0 Richardson (Q24), 1 two-stage Gauss-Seidel (Q30) */
+    int n_inner;  /* two-stage GS: Jacobi-Richardson inner iterations */
 } or_gamg_params;
 
 typedef struct {
@@ -855,6 +857,37 @@ static void or_jacobi_sweep(or_level* L, double omega)
 {
     or_amul(L->n, L->F, L->owner, L->neighbour, L->diag, L->upper, L->upper, L->x, 0, 0, 0, 0, L->y);
     for (int i = 0; i < L->n; ++i) L->x[i] = L->x[i] + omega * (L->rD[i] * (L->b[i] - L->y[i]));
+}
+
+/* Two-stage Gauss-Seidel sweep (Q30, Berger-Vergiat et al. 2021): x = x + z with
+ * z ~ (D + L)^-1 r, r = b - A x, L = strictly lower part (row c: faces with neighbour c,
+ * coefficient lower = upper), by n_inner Jacobi-Richardson iterations
+ * z_0 = rD r,  z_{k+1} = rD (r - L z_k)  (lower sums in face order). */
+static void or_gs2_sweep(or_level* L, int n_inner)
+{
+    or_amul(L->n, L->F, L->owner, L->neighbour, L->diag, L->upper, L->upper, L->x, 0, 0, 0, 0, L->y);
+    double* r = (double*)malloc(sizeof(double) * (size_t)(L->n + 1));
+    double* z = (double*)malloc(sizeof(double) * (size_t)(L->n + 1));
+    double* t = (double*)malloc(sizeof(double) * (size_t)(L->n + 1));
+    for (int i = 0; i < L->n; ++i) {
+        r[i] = L->b[i] - L->y[i];
+        z[i] = L->rD[i] * r[i];
+    }
+    for (int k = 0; k < n_inner; ++k) {
+        for (int i = 0; i < L->n; ++i) t[i] = r[i];
+        for (int f = 0; f < L->F; ++f) t[L->neighbour[f]] -= L->upper[f] * z[L->owner[f]];
+        for (int i = 0; i < L->n; ++i) z[i] = L->rD[i] * t[i];
+    }
+    for (int i = 0; i < L->n; ++i) L->x[i] = L->x[i] + z[i];
+    free(r);
+    free(z);
+    free(t);
+}
+
+static void or_smooth(or_level* L, const or_gamg_params* gp)
+{
+    if (gp->smoother == 1) or_gs2_sweep(L, gp->n_inner);
+    else or_jacobi_sweep(L, gp->omega);
 }
 
 /* GAMGSolver::scale reading (Q25): alpha = (c.r)/(c.Ac) clamped to [0, 2]
@@ -888,7 +921,7 @@ static void or_vcycle(int nl, or_level* Lv, const or_gamg_params* gp)
     for (int l = 0; l < nl - 1; ++l) {
         or_level* L = &Lv[l];
         for (int i = 0; i < L->n; ++i) L->x[i] = 0.0;
-        for (int s = 0; s < gp->n_pre; ++s) or_jacobi_sweep(L, gp->omega);
+        for (int s = 0; s < gp->n_pre; ++s) or_smooth(L, gp);
         or_amul(L->n, L->F, L->owner, L->neighbour, L->diag, L->upper, L->upper, L->x, 0, 0, 0, 0, L->y);
         for (int i = 0; i < L->n; ++i) L->r[i] = L->b[i] - L->y[i];
         or_restrict(L->n, L->ftc, L->r, Lv[l + 1].n, Lv[l + 1].b);
@@ -899,7 +932,7 @@ static void or_vcycle(int nl, or_level* Lv, const or_gamg_params* gp)
         for (int i = 0; i < L->n; ++i) L->c[i] = Lv[l + 1].x[L->ftc[i]]; /* prolongField: injection */
         if (gp->scale) or_scale(L, L->r);
         for (int i = 0; i < L->n; ++i) L->x[i] = L->x[i] + L->c[i];
-        for (int s = 0; s < gp->n_post; ++s) or_jacobi_sweep(L, gp->omega);
+        for (int s = 0; s < gp->n_post; ++s) or_smooth(L, gp);
     }
 }
 

@@ -39,10 +39,13 @@ muts = [
  ("double a = fabs(den) > 1e-300 ? num / den : 1.0;", "double a = fabs(den) > 1e-300 ? den / num : 1.0;"),
  ("if (a < 0.0) a = 0.0;", "if (a < -10.0) a = 0.0;"),
  ("for (int i = 0; i < L->n; ++i) L->c[i] = Lv[l + 1].x[L->ftc[i]];", "for (int i = 0; i < L->n; ++i) L->c[i] = Lv[l + 1].x[L->ftc[i] / 2];"),
- ("for (int s = 0; s < gp->n_pre; ++s) or_jacobi_sweep(L, gp->omega);", ";"),
+ ("for (int s = 0; s < gp->n_pre; ++s) or_smooth(L, gp);", ";"),
  ("for (int i = 0; i < L->n; ++i) L->r[i] = L->b[i] - L->y[i];", "for (int i = 0; i < L->n; ++i) L->r[i] = L->b[i];"),
  ("cw[l] += w[f];", "cw[l] = w[f];"),
  ("for (int i = 0; i < n; ++i) psi[i] = psi[i] + Lv[0].x[i];", "for (int i = 0; i < n; ++i) psi[i] = psi[i] - Lv[0].x[i];"),
+ ("for (int f = 0; f < L->F; ++f) t[L->neighbour[f]] -= L->upper[f] * z[L->owner[f]];", "for (int f = 0; f < L->F; ++f) t[L->owner[f]] -= L->upper[f] * z[L->neighbour[f]];"),
+ ("for (int i = 0; i < L->n; ++i) z[i] = L->rD[i] * t[i];", "for (int i = 0; i < L->n; ++i) z[i] = t[i];"),
+ ("    if (gp->smoother == 1) or_gs2_sweep(L, gp->n_inner);", "    if (gp->smoother == 1) or_gs2_sweep(L, gp->n_inner > 0 ? gp->n_inner - 1 : 0);"),
 ]
 sel = os.environ.get("MUT_SELECT")  # e.g. "GAMG": only mutants after that marker
 if sel == "GAMG":
@@ -50,13 +53,17 @@ if sel == "GAMG":
 res = []
 for a, b in muts:
     assert a in src, a
-    open('oracle/oracle.c', 'w').write(src.replace(a, b))
-    import glob
-    oracle_tests = sorted(glob.glob('tests/test_oracle_*.py')) + ['tests/test_multirank_gloo.py']
-    r = subprocess.run([sys.executable, '-m', 'pytest', *oracle_tests, '-x', '-q', '-m', 'not gpu'], capture_output=True, text=True)
-    caught = r.returncode != 0
-    line = [l for l in r.stdout.splitlines() if l.startswith('FAILED')][:1]
-    res.append((caught, a[:60], line))
-    print(caught, a[:70], line, flush=True)
-open('oracle/oracle.c', 'w').write(src)
+try:
+  for a, b in muts:
+      assert a in src, a
+      open('oracle/oracle.c', 'w').write(src.replace(a, b))
+      import glob
+      oracle_tests = sorted(glob.glob('tests/test_oracle_*.py')) + ['tests/test_multirank_gloo.py']
+      r = subprocess.run([sys.executable, '-m', 'pytest', *oracle_tests, '-x', '-q', '-m', 'not gpu'], capture_output=True, text=True)
+      caught = r.returncode != 0
+      line = [l for l in r.stdout.splitlines() if l.startswith('FAILED')][:1]
+      res.append((caught, a[:60], line))
+      print(caught, a[:70], line, flush=True)
+finally:
+    open('oracle/oracle.c', 'w').write(src)
 print('ALL CAUGHT' if all(c for c, *_ in res) else 'SOME MISSED')

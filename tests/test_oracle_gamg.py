@@ -11,6 +11,8 @@ Independent of the oracle's own loops:
 - one GAMG iteration equals a textbook two-grid / three-grid cycle written with dense
   matrices (Galerkin coarse operator, weighted Jacobi, exact coarse solve, energy-optimal
   correction scaling clamped to [0, 2]);
+- two-stage Gauss-Seidel (Q30): the same dense cycle with z = D^-1 (r - L z) inner iterations,
+  and with enough inner iterations the exact forward triangular solve (scipy);
 - single-level hierarchy: one cycle is the exact (dense) solve;
 - fixed point and convergence to the dense solution, far fewer cycles than PCG iterations."""
 import numpy as np
@@ -131,6 +133,20 @@ def test_restrict_prolong_adjoint():
     assert np.dot(rc, xc) == pytest.approx(np.dot(r, R @ xc), rel=1e-13)
 
 
+def _dense_smooth(A, b, x, gp):
+    if gp.smoother == O.GS2:
+        r = b - A @ x
+        if gp.n_inner >= A.shape[0]:  # D^-1 L is nilpotent: the inner iteration is the exact forward solve
+            import scipy.linalg
+            return x + scipy.linalg.solve_triangular(np.tril(A), r, lower=True)
+        Lo, d = np.tril(A, -1), np.diag(A)
+        z = r / d
+        for _ in range(gp.n_inner):
+            z = (r - Lo @ z) / d
+        return x + z
+    return x + gp.omega * ((b - A @ x) / np.diag(A))
+
+
 def _dense_cycle(As, Rs, b, gp):
     """Textbook V-cycle with dense Galerkin operators (correction form, zero initial guess)."""
     L = len(As)
@@ -141,7 +157,7 @@ def _dense_cycle(As, Rs, b, gp):
     for l in range(L - 1):
         x[l] = np.zeros(As[l].shape[0])
         for _ in range(gp.n_pre):
-            x[l] = x[l] + gp.omega * ((bl[l] - As[l] @ x[l]) / np.diag(As[l]))
+            x[l] = _dense_smooth(As[l], bl[l], x[l], gp)
         rl[l] = bl[l] - As[l] @ x[l]
         bl[l + 1] = Rs[l].T @ rl[l]
     x[L - 1] = np.linalg.solve(As[L - 1], bl[L - 1])
@@ -153,19 +169,25 @@ def _dense_cycle(As, Rs, b, gp):
             c = a * c
         x[l] = x[l] + c
         for _ in range(gp.n_post):
-            x[l] = x[l] + gp.omega * ((bl[l] - As[l] @ x[l]) / np.diag(As[l]))
+            x[l] = _dense_smooth(As[l], bl[l], x[l], gp)
     return x[0]
 
 
-@pytest.mark.parametrize("n_coarsest,scale,n_pre,n_post,omega", [
-    (40, True, 0, 2, 0.75), (40, False, 1, 1, 0.6), (20, True, 1, 2, 0.75), (10, True, 0, 3, 0.9),
-    (10, True, 1, 1, 1.6)])  # omega = 1.6 (divergent Jacobi): the raw scale factor goes negative -> clamp 0
-def test_one_cycle_equals_dense_multigrid(n_coarsest, scale, n_pre, n_post, omega):
+@pytest.mark.parametrize("n_coarsest,scale,n_pre,n_post,omega,smoother,n_inner", [
+    (40, True, 0, 2, 0.75, 0, 1), (40, False, 1, 1, 0.6, 0, 1), (20, True, 1, 2, 0.75, 0, 1),
+    (10, True, 0, 3, 0.9, 0, 1),
+    (10, True, 1, 1, 1.6, 0, 1),   # omega = 1.6 (divergent Jacobi): the raw scale factor goes negative -> clamp 0
+    (10, True, 0, 2, 0.75, 1, 1),  # two-stage Gauss-Seidel (Q30), one inner iteration
+    (20, True, 1, 1, 0.75, 1, 3),
+    (40, False, 0, 1, 0.75, 1, 0),  # zero inner iterations: a plain Jacobi step
+    (40, True, 1, 2, 0.75, 1, 64),  # 64 >= cells: exact Gauss-Seidel (forward triangular solve)
+])
+def test_one_cycle_equals_dense_multigrid(n_coarsest, scale, n_pre, n_post, omega, smoother, n_inner):
     m = gen.perturbed(4, 0.25)  # 64 cells -> 32 -> 16 -> 8 ...
     g = gen.gamma_lognormal(m)
     s = O.assemble(m, g, 0, 0.0, source=gen.rhs(m))
     gp = O.gamg_params(n_pre=n_pre, n_post=n_post, scale=scale, n_coarsest_cells=n_coarsest, omega=omega,
-                       coarsest_rel_tol=1e-15, coarsest_max_iter=500)
+                       coarsest_rel_tol=1e-15, coarsest_max_iter=500, smoother=smoother, n_inner=n_inner)
     lv = O.gamg_hierarchy(m, gp)
     A = dense_ldu(m.n_cells, m.owner, m.neighbour, s.diag, s.upper)
     As, Rs = [A], []
@@ -188,6 +210,15 @@ def test_single_level_cycle_is_exact_solve():
     assert perf["levels"] == 1
     A = dense_ldu(m.n_cells, m.owner, m.neighbour, s.diag, s.upper)
     assert np.allclose(psi, np.linalg.solve(A, s.source), rtol=1e-12, atol=1e-14)
+
+
+def test_gs2_converges_faster_than_richardson():
+    """Two-stage Gauss-Seidel (Q30) is the stronger smoother: fewer cycles to the same tolerance."""
+    m = gen.cube(12)
+    s = O.assemble(m, gen.gamma_lognormal(m), 0, 0.0, source=gen.rhs(m))
+    _, pr = O.gamg(m, s, None, O.controls(1e-9, 0.0, 300, 0))
+    _, pg = O.gamg(m, s, None, O.controls(1e-9, 0.0, 300, 0), O.gamg_params(smoother=O.GS2))
+    assert pr["converged"] and pg["converged"] and pg["n_iterations"] < pr["n_iterations"]
 
 
 def test_fixed_point_and_convergence():
