@@ -187,7 +187,8 @@ void spuma_free(spuma_mesh m);
  * pGAMG controls P:1043-1052, profile rows restrictField / prolongField /
  * agglomerateMatrix / scale / Vcycle P:517-545.  Readings Q22-Q28:
  * faceAreaPair pairwise agglomeration on |S_f| (Q22), Galerkin coarse matrices (Q27),
- * V-cycle in correction form (Q23) with weighted-Jacobi sweeps (Q24), energy-optimal
+ * V-cycle in correction form (Q23) with weighted-Jacobi sweeps (Q24) or two-stage
+ * Gauss-Seidel sweeps (Q30, the paper's second GPU smoother), energy-optimal
  * correction scaling clamped to [0, 2] (Q25), PCG + diagonal at the coarsest level (Q26),
  * PCG's normFactor / convergence / loop semantics with one V-cycle per iteration (Q28). */
 typedef struct spuma_gamg_params {
@@ -200,7 +201,10 @@ typedef struct spuma_gamg_params {
     double coarsest_tolerance;      /* coarsest PCG tolerance (default 0)                         */
     double coarsest_rel_tol;        /* coarsest PCG relTol (default 1e-6)                         */
     int coarsest_max_iter;          /* coarsest PCG maxIter (default 1000)                        */
+    int smoother;                   /* SPUMA_SMOOTHER_RICHARDSON (default) or _GS2 (Q30)          */
+    int n_inner;                    /* two-stage Gauss-Seidel: inner Jacobi-Richardson iterations (default 1) */
 } spuma_gamg_params;
+enum { SPUMA_SMOOTHER_RICHARDSON = 0, SPUMA_SMOOTHER_GS2 = 1 };
 
 /* Fill *p with the defaults above. */
 void spuma_gamg_default_params(spuma_gamg_params* p);

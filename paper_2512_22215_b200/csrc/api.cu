@@ -594,16 +594,40 @@ int gamg_enqueue_cycle(spuma_mesh m, const spuma_gamg_params& gp, cudaStream_t s
         launch_gamg_residual(s, lv[0], w0);
         return 3;
     }
+    // one smoother sweep on level L: from x' = xin (+ alpha xc[ftc] if xc) into out (acc: psi += x)
+    auto sweep = [&](GLevel& L, const double* xin, const double* xc, const double* alpha, double* out,
+                     bool acc) {
+        if (gp.smoother != SPUMA_SMOOTHER_GS2) {
+            launch_gamg_smooth(s, L, P, xin, out, gp.omega, xc, alpha, acc);
+            ++k;
+            return;
+        }
+        launch_gamg_gs2_res(s, L, P, xin, xc, alpha, L.r);  // two-stage Gauss-Seidel (Q30)
+        ++k;
+        if (gp.n_inner == 0) {
+            launch_gamg_gs2_upd(s, L, P, xin, xc, alpha, L.r, nullptr, out, true, true, acc);
+            ++k;
+            return;
+        }
+        const double* zin = nullptr;
+        double* zb[2] = {L.p, L.q};
+        for (int it = 0; it < gp.n_inner; ++it, ++k) {
+            const bool last = it + 1 == gp.n_inner;
+            double* zo = last ? out : zb[it & 1];
+            launch_gamg_gs2_upd(s, L, P, xin, xc, alpha, L.r, zin, zo, false, last, acc);
+            zin = zo;
+        }
+    };
     std::vector<double*> xcur(nl, nullptr);  // buffer holding x_l; nullptr: x_l == 0
     for (int l = 0; l + 1 < nl; ++l) {
         GLevel& L = lv[l];
         double* xl = nullptr;
         if (gp.n_pre_sweeps > 0) {
-            cudaMemsetAsync(L.x, 0, sizeof(double) * L.a.N, s);
-            double *xin = L.x, *xout = L.x2;
-            for (int i = 0; i < gp.n_pre_sweeps; ++i, ++k) {
-                launch_gamg_smooth(s, L, P, xin, xout, gp.omega, nullptr, nullptr, false);
-                std::swap(xin, xout);
+            double *xin = nullptr, *xout = L.x;
+            for (int i = 0; i < gp.n_pre_sweeps; ++i) {
+                sweep(L, xin, nullptr, nullptr, xout, false);
+                xin = xout;
+                xout = xout == L.x ? L.x2 : L.x;
             }
             xl = xin;
         }
@@ -616,50 +640,42 @@ int gamg_enqueue_cycle(spuma_mesh m, const spuma_gamg_params& gp, cudaStream_t s
     launch_pcg_single(s, Lc.a, G->cws);
     ++k;
     xcur[nl - 1] = Lc.x;
+    const bool pq = gp.smoother != SPUMA_SMOOTHER_GS2 && gp.scale_correction && gp.n_post_sweeps > 0;
     for (int l = nl - 2; l >= 0; --l) {
         GLevel& L = lv[l];
         const double* xc = xcur[l + 1];
         const double* r = xcur[l] ? L.r : L.b;
         double* out = xcur[l] == L.x ? L.x2 : L.x;
         double* other = out == L.x ? L.x2 : L.x;
+        const double* alpha = gp.scale_correction ? G->alpha + l : nullptr;
         int done_sweeps = 0;
         if (gp.scale_correction) {
-            launch_gamg_scale(s, L, P, xcur[l], xc, r, gp.omega, gp.n_post_sweeps > 0, G->part, G->ticket,
-                              G->alpha + l);
-            ++k;
-            if (gp.n_post_sweeps > 0) {  // sweeps 1 (+2) in one kernel, sweep 1 prepared by the scale
-                const bool two = gp.n_post_sweeps >= 2;
-                done_sweeps = two ? 2 : 1;
-                const bool acc = l == 0 && done_sweeps == gp.n_post_sweeps;
-                launch_gamg_post(s, L, P, G->alpha + l, gp.omega, out, two, acc);
-                ++k;
-                if (!acc) {
-                    xcur[l] = out;
-                    std::swap(out, other);
-                }
-            } else {
-                launch_gamg_correct(s, L, P, xcur[l], xc, G->alpha + l, out, l == 0);
-                xcur[l] = out;
-                ++k;
-                std::swap(out, other);
-            }
-        } else if (gp.n_post_sweeps > 0) {  // unscaled: the correction is fused into the first sweep
-            const bool acc = l == 0 && gp.n_post_sweeps == 1;
-            launch_gamg_smooth(s, L, P, xcur[l], out, gp.omega, xc, nullptr, acc);
-            done_sweeps = 1;
-            ++k;
-            if (!acc) {
-                xcur[l] = out;
-                std::swap(out, other);
-            }
-        } else {
-            launch_gamg_correct(s, L, P, xcur[l], xc, nullptr, out, l == 0);
-            xcur[l] = out;
+            launch_gamg_scale(s, L, P, xcur[l], xc, r, gp.omega, pq, G->part, G->ticket, G->alpha + l);
             ++k;
         }
-        for (int i = done_sweeps; i < gp.n_post_sweeps; ++i, ++k) {
+        bool acc = false;
+        if (pq) {  // Richardson: sweeps 1 (+2) in one kernel, sweep 1 prepared by the scale (Q29)
+            const bool two = gp.n_post_sweeps >= 2;
+            done_sweeps = two ? 2 : 1;
+            acc = l == 0 && done_sweeps == gp.n_post_sweeps;
+            launch_gamg_post(s, L, P, G->alpha + l, gp.omega, out, two, acc);
+            ++k;
+        } else if (gp.n_post_sweeps > 0) {  // the correction folded into the first sweep
+            done_sweeps = 1;
+            acc = l == 0 && gp.n_post_sweeps == 1;
+            sweep(L, xcur[l], xc, alpha, out, acc);
+        } else {
+            acc = l == 0;
+            launch_gamg_correct(s, L, P, xcur[l], xc, alpha, out, acc);
+            ++k;
+        }
+        if (!acc) {
+            xcur[l] = out;
+            std::swap(out, other);
+        }
+        for (int i = done_sweeps; i < gp.n_post_sweeps; ++i) {
             const bool last = i + 1 == gp.n_post_sweeps;
-            launch_gamg_smooth(s, L, P, xcur[l], out, gp.omega, nullptr, nullptr, l == 0 && last);
+            sweep(L, xcur[l], nullptr, nullptr, out, l == 0 && last);
             if (!(l == 0 && last)) {
                 xcur[l] = out;
                 std::swap(out, other);
@@ -1516,11 +1532,14 @@ void spuma_gamg_default_params(spuma_gamg_params* p)
     p->coarsest_tolerance = 0.0;
     p->coarsest_rel_tol = 1e-6;
     p->coarsest_max_iter = 1000;
+    p->smoother = SPUMA_SMOOTHER_RICHARDSON;
+    p->n_inner = 1;
 }
 
 static spuma_status gamg_check_params(const spuma_gamg_params& gp)
 {
-    if (gp.n_pre_sweeps < 0 || gp.n_post_sweeps < 0 || gp.max_levels < 1 || gp.coarsest_max_iter < 0)
+    if (gp.n_pre_sweeps < 0 || gp.n_post_sweeps < 0 || gp.max_levels < 1 || gp.coarsest_max_iter < 0 ||
+        gp.n_inner < 0 || (gp.smoother != SPUMA_SMOOTHER_RICHARDSON && gp.smoother != SPUMA_SMOOTHER_GS2))
         return set_error(SPUMA_ERR_INVALID_ARGUMENT, "invalid GAMG parameters");
     return SPUMA_OK;
 }

@@ -46,6 +46,10 @@ struct XCorr {
     }
 };
 
+struct XZero {
+    __device__ __forceinline__ double operator()(int) const { return 0.0; }
+};
+
 struct XInj {  // c(j) = xc[ftc[j]]
     const double* __restrict__ xc;
     const int* __restrict__ ftc;
@@ -123,9 +127,12 @@ __global__ void __launch_bounds__(kThreads) k_gamg_smooth(GLevel L, const DevPtr
             const XCorr X{xin, xc, L.ftc, a};
             xi = X(c);
             y = row_ax(L.a, c, d, u, X);
-        } else {
+        } else if (xin) {
             xi = xin[c];
             y = row_ax(L.a, c, d, u, XPlain{xin});
+        } else {  // x == 0 (first pre-sweep)
+            xi = 0.0;
+            y = row_ax(L.a, c, d, u, XZero{});
         }
         const double xn = xi + omega * ((1.0 / d[c]) * (L.b[c] - y));
         if (psi_acc) psi[c] = psi[c] + xn;
@@ -208,6 +215,62 @@ __global__ void __launch_bounds__(kThreads) k_gamg_post(GLevel L, const DevPtrs*
     }
 }
 
+// Two-stage Gauss-Seidel (Q30), stage 1: r = b - A x' with x' = xin (+ alpha xc[ftc] when xc
+// is given: the prolonged correction folded into the first post-sweep; xin nullptr: zero).
+__global__ void __launch_bounds__(kThreads) k_gamg_gs2_res(GLevel L, const DevPtrs* __restrict__ P,
+                                                           const double* __restrict__ xin,
+                                                           const double* __restrict__ xc,
+                                                           const double* __restrict__ alpha, double* __restrict__ r)
+{
+    const double* __restrict__ d = level_diag(L, P);
+    const double* __restrict__ u = level_upper(L, P);
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < L.a.N; c += gridDim.x * blockDim.x) {
+        double y;
+        if (xc) y = row_ax(L.a, c, d, u, XCorr{xin, xc, L.ftc, alpha ? *alpha : 1.0});
+        else if (xin) y = row_ax(L.a, c, d, u, XPlain{xin});
+        else y = row_ax(L.a, c, d, u, XZero{});
+        r[c] = L.b[c] - y;
+    }
+}
+
+// Stage 2, one Jacobi-Richardson iteration of (D + L) z = r:  z = rD (r - L zprev), the
+// lower sum over the faces with neighbour c in face (losort) order; zprev = zin, or rD r
+// when zin is nullptr (the first iteration).  last: x = x' + z (psi_acc: psi += x) instead
+// of storing z.  n_inner == 0 is one launch with skip_lower (z = rD r).
+__global__ void __launch_bounds__(kThreads) k_gamg_gs2_upd(GLevel L, const DevPtrs* __restrict__ P,
+                                                           const double* __restrict__ xin,
+                                                           const double* __restrict__ xc,
+                                                           const double* __restrict__ alpha,
+                                                           const double* __restrict__ r,
+                                                           const double* __restrict__ zin, double* __restrict__ out,
+                                                           int skip_lower, int last, int psi_acc)
+{
+    const double* __restrict__ d = level_diag(L, P);
+    const double* __restrict__ u = level_upper(L, P);
+    double* __restrict__ psi = P->psi;
+    const double a = alpha ? *alpha : 1.0;
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < L.a.N; c += gridDim.x * blockDim.x) {
+        double t = r[c];
+        if (!skip_lower) {
+            const int k1 = L.a.losortStart[c + 1];
+            for (int k = L.a.losortStart[c]; k < k1; ++k) {
+                const int j = L.a.ownerLo[k];
+                const double zj = zin ? zin[j] : (1.0 / d[j]) * r[j];
+                t = t - u[L.a.losort[k]] * zj;
+            }
+        }
+        const double z = (1.0 / d[c]) * t;
+        if (!last) {
+            out[c] = z;
+            continue;
+        }
+        const double xp = xc ? XCorr{xin, xc, L.ftc, a}(c) : (xin ? xin[c] : 0.0);
+        const double xn = xp + z;
+        if (psi_acc) psi[c] = psi[c] + xn;
+        else out[c] = xn;
+    }
+}
+
 // end of a GAMG iteration (Q28): rA = source - A psi, final residual, n++, convergence, done
 __global__ void __launch_bounds__(kThreads) k_gamg_residual(GLevel L, Workspace w)
 {
@@ -277,6 +340,20 @@ void launch_gamg_post(cudaStream_t s, const GLevel& L, const DevPtrs* P, const d
                       double* out, bool two, bool psi_acc)
 {
     k_gamg_post<<<L.grid, kThreads, 0, s>>>(L, P, alpha, omega, out, two ? 1 : 0, psi_acc ? 1 : 0);
+}
+
+void launch_gamg_gs2_res(cudaStream_t s, const GLevel& L, const DevPtrs* P, const double* xin, const double* xc,
+                         const double* alpha, double* r)
+{
+    k_gamg_gs2_res<<<L.grid, kThreads, 0, s>>>(L, P, xin, xc, alpha, r);
+}
+
+void launch_gamg_gs2_upd(cudaStream_t s, const GLevel& L, const DevPtrs* P, const double* xin, const double* xc,
+                         const double* alpha, const double* r, const double* zin, double* out, bool skip_lower,
+                         bool last, bool psi_acc)
+{
+    k_gamg_gs2_upd<<<L.grid, kThreads, 0, s>>>(L, P, xin, xc, alpha, r, zin, out, skip_lower ? 1 : 0, last ? 1 : 0,
+                                               psi_acc ? 1 : 0);
 }
 
 void launch_gamg_residual(cudaStream_t s, const GLevel& L, const Workspace& w)

@@ -286,5 +286,10 @@ void launch_gamg_correct(cudaStream_t s, const GLevel& L, const DevPtrs* P, cons
 void launch_gamg_residual(cudaStream_t s, const GLevel& L, const Workspace& w);
 void launch_gamg_post(cudaStream_t s, const GLevel& L, const DevPtrs* P, const double* alpha, double omega,
                       double* out, bool two, bool psi_acc);
+void launch_gamg_gs2_res(cudaStream_t s, const GLevel& L, const DevPtrs* P, const double* xin, const double* xc,
+                         const double* alpha, double* r);
+void launch_gamg_gs2_upd(cudaStream_t s, const GLevel& L, const DevPtrs* P, const double* xin, const double* xc,
+                         const double* alpha, const double* r, const double* zin, double* out, bool skip_lower,
+                         bool last, bool psi_acc);
 extern bool g_use_pdl;  // programmatic dependent launch of the hot-loop kernels (process-wide)
 }  // namespace spuma

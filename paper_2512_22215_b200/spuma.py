@@ -67,7 +67,11 @@ class GamgParams(ctypes.Structure):
     """spuma_gamg_params (include/spuma.h; readings Q22-Q28)."""
     _fields_ = [("n_pre_sweeps", _ci), ("n_post_sweeps", _ci), ("scale_correction", _ci),
                 ("n_cells_in_coarsest_level", _ci), ("max_levels", _ci), ("omega", _cd),
-                ("coarsest_tolerance", _cd), ("coarsest_rel_tol", _cd), ("coarsest_max_iter", _ci)]
+                ("coarsest_tolerance", _cd), ("coarsest_rel_tol", _cd), ("coarsest_max_iter", _ci),
+                ("smoother", _ci), ("n_inner", _ci)]
+
+
+SMOOTHER_RICHARDSON, SMOOTHER_GS2 = 0, 1
 
 
 def gamg_params(**kw) -> GamgParams:

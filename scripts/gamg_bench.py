@@ -44,7 +44,7 @@ def cycle_bytes(cells, faces):
     return tot
 
 
-def run(name, m, gamma, tol, rel_tol=0.0, reps=3):
+def run(name, m, gamma, tol, rel_tol=0.0, reps=3, params=None):
     t0 = time.perf_counter()
     h = P.Mesh.from_mesh(m, renumber=False, stream=torch.cuda.current_stream().cuda_stream)
     t_create = time.perf_counter() - t0
@@ -62,7 +62,7 @@ def run(name, m, gamma, tol, rel_tol=0.0, reps=3):
         torch.cuda.synchronize()
         e0.record()
         if kind == "gamg":
-            perf = h.gamg_solve(diag, upper, None, s, psi, tol, rel_tol, 300, 0)
+            perf = h.gamg_solve(diag, upper, None, s, psi, tol, rel_tol, 300, 0, params=params)
         else:
             perf = h.pcg_solve(diag, upper, None, s, psi, tol, rel_tol, 5000, 0)
         e1.record()
@@ -72,7 +72,7 @@ def run(name, m, gamma, tol, rel_tol=0.0, reps=3):
     t1 = time.perf_counter()
     solve("gamg")  # builds the hierarchy + captures the cycle
     t_hier = time.perf_counter() - t1
-    hier = h.gamg_hierarchy(with_ftc=False)
+    hier = h.gamg_hierarchy(params, with_ftc=False)
     rg = min((solve("gamg") for _ in range(reps)), key=lambda r: r[1])
     solve("pcg")
     rp = min((solve("pcg") for _ in range(reps)), key=lambda r: r[1])
@@ -97,4 +97,8 @@ if __name__ == "__main__":
     for n in ns:
         m = gen.cube(n)
         run(f"cube {n}^3 gamma=1 tol 1e-6", m, None, 1e-6)
-        run(f"cube {n}^3 gamma=lognormal pGAMG (1e-9, relTol 1e-3)", m, gen.gamma_lognormal(m), 1e-9, 1e-3)
+        g = gen.gamma_lognormal(m)
+        run(f"cube {n}^3 gamma=lognormal pGAMG (1e-9, relTol 1e-3)", m, g, 1e-9, 1e-3)
+        gs2 = P.gamg_params(smoother=P.spuma.SMOOTHER_GS2)
+        run(f"cube {n}^3 gamma=1 tol 1e-6, two-stage GS", m, None, 1e-6, params=gs2)
+        run(f"cube {n}^3 gamma=lognormal pGAMG, two-stage GS", m, g, 1e-9, 1e-3, params=gs2)

@@ -29,7 +29,7 @@ def _oparams(gp):
     return O.gamg_params(n_pre=gp.n_pre_sweeps, n_post=gp.n_post_sweeps, scale=bool(gp.scale_correction),
                          n_coarsest_cells=gp.n_cells_in_coarsest_level, max_levels=gp.max_levels, omega=gp.omega,
                          coarsest_tol=gp.coarsest_tolerance, coarsest_rel_tol=gp.coarsest_rel_tol,
-                         coarsest_max_iter=gp.coarsest_max_iter)
+                         coarsest_max_iter=gp.coarsest_max_iter, smoother=gp.smoother, n_inner=gp.n_inner)
 
 
 class Case:
@@ -136,7 +136,12 @@ def test_paper_controls_pgamg():
     dict(n_post_sweeps=3, omega=0.6, n_cells_in_coarsest_level=40),
     dict(max_levels=3),
     dict(n_post_sweeps=1, omega=1.6),  # divergent Jacobi: the scale factor clamps at 0
-], ids=["pre1", "pre2-post0", "noscale", "post3-omega", "3levels", "clamp"])
+    dict(smoother=1),                                  # two-stage Gauss-Seidel (Q30)
+    dict(smoother=1, n_inner=3, n_pre_sweeps=1),
+    dict(smoother=1, n_inner=0, scale_correction=0),
+    dict(smoother=1, n_post_sweeps=1, n_inner=2),
+], ids=["pre1", "pre2-post0", "noscale", "post3-omega", "3levels", "clamp", "gs2", "gs2-inner3-pre1",
+        "gs2-inner0-noscale", "gs2-post1-inner2"])
 def test_parameter_variants_one_cycle_and_solve(kw):
     m = gen.permute(gen.perturbed(9, 0.2), seed=3)
     c = Case(m, gen.gamma_lognormal(m))
@@ -144,8 +149,17 @@ def test_parameter_variants_one_cycle_and_solve(kw):
     psi_g, pg = c.gpu((0.0, 0.0, 2, 2), gp)
     psi_o, po = c.oracle((0.0, 0.0, 2, 2), gp)
     assert rel_l2(psi_g, psi_o) <= 1e-10
-    if kw.get("omega", 0.75) < 1.0:
+    if kw.get("omega", 0.75) < 1.0 or kw.get("smoother"):
         _solve_parity(c, (1e-8, 0.0, 400, 0), gp)
+
+
+@pytest.mark.parametrize("renumber", [False, True])
+def test_gs2_solve_parity(renumber):
+    m = gen.permute(gen.perturbed(11, 0.15), seed=5)
+    c = Case(m, gen.gamma_lognormal(m), renumber=renumber)
+    pg, po = _solve_parity(c, (1e-9, 0.0, 300, 0), P.gamg_params(smoother=1))
+    _, pr = c.oracle((1e-9, 0.0, 300, 0))
+    assert pg["converged"] and po["n_iterations"] < pr["n_iterations"]
 
 
 def test_single_level_hierarchy():
