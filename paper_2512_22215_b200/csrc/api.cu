@@ -508,6 +508,8 @@ spuma_status gamg_ensure(spuma_mesh m, const spuma_gamg_params& gp)
             L.a.n_iface = 0;
             L.rD = m->ws.rD;
             L.b = m->ws.rA;
+            L.ell = (m->d_upper_s && m->d_sell_n && m->sell_wn >= 0 && m->sell_wn <= 3 && m->sell_wo >= 0 &&
+                     m->sell_wo <= 3) ? 1 : 0;
         } else {
             L.a = MeshArgs{};
             L.a.N = n;
@@ -1583,6 +1585,10 @@ spuma_status spuma_gamg_solve(spuma_mesh m, const spuma_scalar* diag, const spum
     SPUMA_CUDA(cudaMemcpyAsync(G->cws.ptrs, G->h_cptrs, sizeof(DevPtrs), cudaMemcpyHostToDevice, s));
     // per-solve: Galerkin coarse matrices (Q27), outer scalars, coarsest PCG controls, A6 setup
     for (int l = 0; l + 1 < nl; ++l) launch_gamg_agg(s, G->lv[l], G->lv[l + 1], m->ws.ptrs);
+    if (G->lv[0].ell) {  // level 0 rows over ELL: this call's coefficients in owner-slot order
+        launch_ell_coeffs(s, G->lv[0].a, P.upper, m->d_upper_s);
+        m->stats.kernel_launches += 1;
+    }
     launch_scal_init(s, m->ws, *ctl, 1);
     const spuma_solver_controls cc{gp.coarsest_tolerance, gp.coarsest_rel_tol, gp.coarsest_max_iter, 0};
     launch_scal_init(s, G->cws, cc, 1);

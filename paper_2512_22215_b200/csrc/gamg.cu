@@ -29,6 +29,46 @@ __device__ __forceinline__ double row_ax(const MeshArgs& a, int c, const double*
     return s;
 }
 
+// The same row over the ELL layout of a uniform mesh (level 0): slot j of the
+// 32-cell chunk of c, neighbour side packed (owner column << 5 | position), coefficients in
+// owner-slot order (upper_s).  Same summation order as row_ax, so bitwise the same value.
+template <class X>
+__device__ __forceinline__ double row_ax_ell(const MeshArgs& a, int c, const double* __restrict__ diag, const X& x)
+{
+    constexpr int W = 3;
+    const int wn = a.ell_wn, wo = a.ell_wo, k = c >> 5, l = c & 31;
+    unsigned pk[W];
+    int nb[W];
+    double uo[W], un[W];
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+        pk[j] = j < wn ? __ldg(a.sell_n + (size_t)32 * wn * k + 32 * j + l) : 0xFFFFFFFFu;
+        nb[j] = j < wo ? __ldg(a.sell_o + (size_t)32 * wo * k + 32 * j + l) : -1;
+        uo[j] = j < wo ? __ldg(a.upper_s + (size_t)32 * wo * k + 32 * j + l) : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+        const int col = (int)(pk[j] >> 5), pos = (int)(pk[j] & 31u);
+        un[j] = pk[j] != 0xFFFFFFFFu ? __ldg(a.upper_s + (size_t)32 * wo * (col >> 5) + 32 * pos + (col & 31)) : 0.0;
+    }
+    double s = diag[c] * x(c);
+#pragma unroll
+    for (int j = 0; j < W; ++j)
+        if (pk[j] != 0xFFFFFFFFu) s = s + un[j] * x((int)(pk[j] >> 5));
+#pragma unroll
+    for (int j = 0; j < W; ++j)
+        if (nb[j] >= 0) s = s + uo[j] * x(nb[j]);
+    return s;
+}
+
+template <bool ELL, class X>
+__device__ __forceinline__ double rowA(const GLevel& L, int c, const double* __restrict__ d,
+                                       const double* __restrict__ u, const X& x)
+{
+    if constexpr (ELL) return row_ax_ell(L.a, c, d, x);
+    else return row_ax(L.a, c, d, u, x);
+}
+
 struct XPlain {
     const double* __restrict__ x;
     __device__ __forceinline__ double operator()(int j) const { return x[j]; }
@@ -112,6 +152,7 @@ __global__ void __launch_bounds__(kThreads) k_gamg_restrict(GLevel F, GLevel C, 
 
 // Richardson sweep (Q24): xout = x + omega (rD (b - A x)), x = xin or (xin + alpha xc[ftc])
 // when xc is given (the prolonged correction of the first post-sweep); psi_acc: psi += xout.
+template <bool ELL>
 __global__ void __launch_bounds__(kThreads) k_gamg_smooth(GLevel L, const DevPtrs* __restrict__ P,
                                                           const double* __restrict__ xin, double* __restrict__ xout,
                                                           double omega, const double* __restrict__ xc,
@@ -126,13 +167,13 @@ __global__ void __launch_bounds__(kThreads) k_gamg_smooth(GLevel L, const DevPtr
         if (xc) {
             const XCorr X{xin, xc, L.ftc, a};
             xi = X(c);
-            y = row_ax(L.a, c, d, u, X);
+            y = rowA<ELL>(L, c, d, u, X);
         } else if (xin) {
             xi = xin[c];
-            y = row_ax(L.a, c, d, u, XPlain{xin});
+            y = rowA<ELL>(L, c, d, u, XPlain{xin});
         } else {  // x == 0 (first pre-sweep)
             xi = 0.0;
-            y = row_ax(L.a, c, d, u, XZero{});
+            y = rowA<ELL>(L, c, d, u, XZero{});
         }
         const double xn = xi + omega * ((1.0 / d[c]) * (L.b[c] - y));
         if (psi_acc) psi[c] = psi[c] + xn;
@@ -146,6 +187,7 @@ __global__ void __launch_bounds__(kThreads) k_gamg_smooth(GLevel L, const DevPtr
 //   x1 = x' + omega rD (r - alpha Ac) = alpha p + q,
 //   p = c - omega rD Ac,  q = x + omega rD r       (x = pre-smoothed correction or 0)
 // and k_gamg_post needs two direct loads per neighbour instead of a gather of its own.
+template <bool ELL>
 __global__ void __launch_bounds__(kThreads) k_gamg_scale(GLevel L, const DevPtrs* __restrict__ P,
                                                          const double* __restrict__ x, const double* __restrict__ xc,
                                                          const double* __restrict__ r, double omega, int pq,
@@ -157,7 +199,7 @@ __global__ void __launch_bounds__(kThreads) k_gamg_scale(GLevel L, const DevPtrs
     double v[2] = {0.0, 0.0};
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < L.a.N; c += gridDim.x * blockDim.x) {
         const double ci = X(c);
-        const double aci = row_ax(L.a, c, d, u, X);
+        const double aci = rowA<ELL>(L, c, d, u, X);
         const double ri = r[c];
         if (pq) {
             const double rd = 1.0 / d[c];
@@ -198,6 +240,7 @@ struct XPQ {  // x1(j) = alpha p_j + q_j
 
 // Post-sweeps 1 (+2) after k_gamg_scale: x1 = alpha p + q; two: x2 = x1 + omega rD (b - A x1)
 // in one gather with x1 formed at the neighbours.  psi_acc: psi += result.
+template <bool ELL>
 __global__ void __launch_bounds__(kThreads) k_gamg_post(GLevel L, const DevPtrs* __restrict__ P,
                                                         const double* __restrict__ alpha, double omega,
                                                         double* __restrict__ out, int two, int psi_acc)
@@ -209,7 +252,7 @@ __global__ void __launch_bounds__(kThreads) k_gamg_post(GLevel L, const DevPtrs*
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < L.a.N; c += gridDim.x * blockDim.x) {
         const double x1 = X(c);
         double xn = x1;
-        if (two) xn = x1 + omega * ((1.0 / d[c]) * (L.b[c] - row_ax(L.a, c, d, u, X)));
+        if (two) xn = x1 + omega * ((1.0 / d[c]) * (L.b[c] - rowA<ELL>(L, c, d, u, X)));
         if (psi_acc) psi[c] = psi[c] + xn;
         else out[c] = xn;
     }
@@ -217,6 +260,7 @@ __global__ void __launch_bounds__(kThreads) k_gamg_post(GLevel L, const DevPtrs*
 
 // Two-stage Gauss-Seidel (Q30), stage 1: r = b - A x' with x' = xin (+ alpha xc[ftc] when xc
 // is given: the prolonged correction folded into the first post-sweep; xin nullptr: zero).
+template <bool ELL>
 __global__ void __launch_bounds__(kThreads) k_gamg_gs2_res(GLevel L, const DevPtrs* __restrict__ P,
                                                            const double* __restrict__ xin,
                                                            const double* __restrict__ xc,
@@ -226,9 +270,9 @@ __global__ void __launch_bounds__(kThreads) k_gamg_gs2_res(GLevel L, const DevPt
     const double* __restrict__ u = level_upper(L, P);
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < L.a.N; c += gridDim.x * blockDim.x) {
         double y;
-        if (xc) y = row_ax(L.a, c, d, u, XCorr{xin, xc, L.ftc, alpha ? *alpha : 1.0});
-        else if (xin) y = row_ax(L.a, c, d, u, XPlain{xin});
-        else y = row_ax(L.a, c, d, u, XZero{});
+        if (xc) y = rowA<ELL>(L, c, d, u, XCorr{xin, xc, L.ftc, alpha ? *alpha : 1.0});
+        else if (xin) y = rowA<ELL>(L, c, d, u, XPlain{xin});
+        else y = rowA<ELL>(L, c, d, u, XZero{});
         r[c] = L.b[c] - y;
     }
 }
@@ -272,12 +316,13 @@ __global__ void __launch_bounds__(kThreads) k_gamg_gs2_upd(GLevel L, const DevPt
 }
 
 // end of a GAMG iteration (Q28): rA = source - A psi, final residual, n++, convergence, done
+template <bool ELL>
 __global__ void __launch_bounds__(kThreads) k_gamg_residual(GLevel L, Workspace w)
 {
     const DevPtrs p = *w.ptrs;
     double v[1] = {0.0};
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < L.a.N; c += gridDim.x * blockDim.x) {
-        const double r = p.source[c] - row_ax(L.a, c, p.diag, p.upper, XPlain{p.psi});
+        const double r = p.source[c] - rowA<ELL>(L, c, p.diag, p.upper, XPlain{p.psi});
         w.rA[c] = r;
         v[0] += fabs(r);
     }
@@ -301,7 +346,7 @@ int gamg_grid(int n)
         int dev = 0, sms = 148, occ = 4;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gamg_smooth, kThreads, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gamg_smooth<false>, kThreads, 0);
         g_gamg_max_grid = sms * (occ > 0 ? occ : 1);
     }
     const int g = (n + kThreads - 1) / kThreads;
@@ -321,13 +366,15 @@ void launch_gamg_restrict(cudaStream_t s, const GLevel& fine, const GLevel& coar
 void launch_gamg_smooth(cudaStream_t s, const GLevel& L, const DevPtrs* P, const double* xin, double* xout,
                         double omega, const double* xc, const double* alpha, bool psi_acc)
 {
-    k_gamg_smooth<<<L.grid, kThreads, 0, s>>>(L, P, xin, xout, omega, xc, alpha, psi_acc ? 1 : 0);
+    if (L.ell) k_gamg_smooth<true><<<L.grid, kThreads, 0, s>>>(L, P, xin, xout, omega, xc, alpha, psi_acc ? 1 : 0);
+    else k_gamg_smooth<false><<<L.grid, kThreads, 0, s>>>(L, P, xin, xout, omega, xc, alpha, psi_acc ? 1 : 0);
 }
 
 void launch_gamg_scale(cudaStream_t s, const GLevel& L, const DevPtrs* P, const double* x, const double* xc,
                        const double* r, double omega, bool pq, double* part, unsigned* ticket, double* alpha)
 {
-    k_gamg_scale<<<L.grid, kThreads, 0, s>>>(L, P, x, xc, r, omega, pq ? 1 : 0, part, ticket, alpha);
+    if (L.ell) k_gamg_scale<true><<<L.grid, kThreads, 0, s>>>(L, P, x, xc, r, omega, pq ? 1 : 0, part, ticket, alpha);
+    else k_gamg_scale<false><<<L.grid, kThreads, 0, s>>>(L, P, x, xc, r, omega, pq ? 1 : 0, part, ticket, alpha);
 }
 
 void launch_gamg_correct(cudaStream_t s, const GLevel& L, const DevPtrs* P, const double* x, const double* xc,
@@ -339,13 +386,15 @@ void launch_gamg_correct(cudaStream_t s, const GLevel& L, const DevPtrs* P, cons
 void launch_gamg_post(cudaStream_t s, const GLevel& L, const DevPtrs* P, const double* alpha, double omega,
                       double* out, bool two, bool psi_acc)
 {
-    k_gamg_post<<<L.grid, kThreads, 0, s>>>(L, P, alpha, omega, out, two ? 1 : 0, psi_acc ? 1 : 0);
+    if (L.ell) k_gamg_post<true><<<L.grid, kThreads, 0, s>>>(L, P, alpha, omega, out, two ? 1 : 0, psi_acc ? 1 : 0);
+    else k_gamg_post<false><<<L.grid, kThreads, 0, s>>>(L, P, alpha, omega, out, two ? 1 : 0, psi_acc ? 1 : 0);
 }
 
 void launch_gamg_gs2_res(cudaStream_t s, const GLevel& L, const DevPtrs* P, const double* xin, const double* xc,
                          const double* alpha, double* r)
 {
-    k_gamg_gs2_res<<<L.grid, kThreads, 0, s>>>(L, P, xin, xc, alpha, r);
+    if (L.ell) k_gamg_gs2_res<true><<<L.grid, kThreads, 0, s>>>(L, P, xin, xc, alpha, r);
+    else k_gamg_gs2_res<false><<<L.grid, kThreads, 0, s>>>(L, P, xin, xc, alpha, r);
 }
 
 void launch_gamg_gs2_upd(cudaStream_t s, const GLevel& L, const DevPtrs* P, const double* xin, const double* xc,
@@ -358,7 +407,8 @@ void launch_gamg_gs2_upd(cudaStream_t s, const GLevel& L, const DevPtrs* P, cons
 
 void launch_gamg_residual(cudaStream_t s, const GLevel& L, const Workspace& w)
 {
-    k_gamg_residual<<<L.grid, kThreads, 0, s>>>(L, w);
+    if (L.ell) k_gamg_residual<true><<<L.grid, kThreads, 0, s>>>(L, w);
+    else k_gamg_residual<false><<<L.grid, kThreads, 0, s>>>(L, w);
 }
 
 }  // namespace spuma

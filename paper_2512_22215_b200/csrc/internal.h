@@ -86,6 +86,7 @@ struct GLevel {
     const int *cfStart, *cfList;  // next level: coarse face -> fine faces
     int nc, ncf;                  // next level's size
     int grid;                     // CTAs of this level's cell kernels (fixed: deterministic reductions)
+    int ell;                      // 1: rows over the ELL layout (a.sell_*, a.upper_s; level 0 of a uniform mesh)
 };
 
 struct Patch {
