@@ -117,6 +117,12 @@ def _L():
             lib.or_restrict.argtypes = [ci, vp, vp, ci, vp]
             lib.or_gamg.argtypes = [ci, ci] + [vp] * 7 + [ctypes.POINTER(GamgParams), ctypes.POINTER(Controls),
                                                            ctypes.POINTER(Perf), vp, vp]
+            lib.or_ilu_factor.argtypes = [ci, ci] + [vp] * 6
+            lib.or_ilu_precondition.argtypes = [ci, ci] + [vp] * 7 + [ci, ci]
+            lib.or_pcg_pc.argtypes = [ci, ci] + [vp] * 6 + [ctypes.POINTER(Controls), ci, ci, ctypes.POINTER(Perf)]
+            lib.or_pbicg.argtypes = [ci, ci] + [vp] * 7 + [ctypes.POINTER(Controls), ci, ci, ctypes.POINTER(Perf)]
+            lib.or_tmul.argtypes = [ci, ci] + [vp] * 7
+            lib.or_ldu_to_csr.argtypes = [ci, ci] + [vp] * 5
             lib.or_dense_from_ldu.argtypes = [ci, ci] + [vp] * 6
             lib.or_dense_matvec.argtypes = [ci, vp, vp, vp]
             lib.or_dense_solve.argtypes = [ci, vp, vp, vp]
@@ -440,6 +446,77 @@ def gamg(mesh: gen.Mesh, sys: LduSystem, psi0=None, ctl: Optional[Controls] = No
     out["levels"] = nl.value
     out["level_cells"] = cells[:nl.value].tolist()
     return psi, out
+
+
+# O12 preconditioner kinds (readings Q31-Q33)
+DIAGONAL, DIC, DILU, ADILU = 0, 1, 2, 3
+
+
+def ilu_factor(owner, neighbour, diag, upper, lower=None) -> np.ndarray:
+    """[OF] DIC / DILU reciprocal diagonal (lower None: DIC, lower = upper)."""
+    o, nb, d, u = _i32(owner), _i32(neighbour), _f64(diag), _f64(upper)
+    lo = u if lower is None else _f64(lower)
+    rD = np.zeros(d.shape[0] + 1)
+    _L().or_ilu_factor(d.shape[0], o.shape[0], _p(o), _p(nb), _p(d), _p(u), _p(lo), _p(rD))
+    return rD[:d.shape[0]]
+
+
+def ilu_precondition(owner, neighbour, rD, upper, r, lower=None, transpose=False, k=-1) -> np.ndarray:
+    """[OF] DIC/DILU precondition(T); k >= 0: aDILU with k Jacobi-style passes per sweep (Q33)."""
+    o, nb, d, u, x = _i32(owner), _i32(neighbour), _f64(rD), _f64(upper), _f64(r)
+    lo = u if lower is None else _f64(lower)
+    w = np.zeros(d.shape[0] + 1)
+    _L().or_ilu_precondition(d.shape[0], o.shape[0], _p(o), _p(nb), _p(d), _p(u), _p(lo), _p(x), _p(w),
+                             int(transpose), int(k))
+    return w[:d.shape[0]]
+
+
+def pcg_pc(mesh: gen.Mesh, sys: LduSystem, kind=DIAGONAL, k=2, psi0=None, ctl: Optional[Controls] = None):
+    """PCG with a diagonal / DIC / DILU / aDILU preconditioner, single domain (O12)."""
+    ctl = ctl or controls()
+    o, nb, d, u, b = _i32(mesh.owner), _i32(mesh.neighbour), _f64(sys.diag), _f64(sys.upper), _f64(sys.source)
+    psi = np.zeros(mesh.n_cells) if psi0 is None else _f64(psi0).copy()
+    perf = Perf()
+    _L().or_pcg_pc(mesh.n_cells, mesh.n_faces, _p(o), _p(nb), _p(d), _p(u), _p(b), _p(psi), ctypes.byref(ctl),
+                   int(kind), int(k), ctypes.byref(perf))
+    return psi, perf.as_dict()
+
+
+def pbicg(owner, neighbour, diag, upper, lower, source, kind=DILU, k=2, psi0=None,
+          ctl: Optional[Controls] = None):
+    """[OF] PBiCG (O12, Q32) on an asymmetric LDU system."""
+    ctl = ctl or controls()
+    o, nb, d, u, lo, b = (_i32(owner), _i32(neighbour), _f64(diag), _f64(upper), _f64(lower), _f64(source))
+    psi = np.zeros(d.shape[0]) if psi0 is None else _f64(psi0).copy()
+    perf = Perf()
+    _L().or_pbicg(d.shape[0], o.shape[0], _p(o), _p(nb), _p(d), _p(u), _p(lo), _p(b), _p(psi), ctypes.byref(ctl),
+                  int(kind), int(k), ctypes.byref(perf))
+    return psi, perf.as_dict()
+
+
+def tmul(owner, neighbour, diag, upper, lower, x) -> np.ndarray:
+    o, nb, d, u, lo, xx = _i32(owner), _i32(neighbour), _f64(diag), _f64(upper), _f64(lower), _f64(x)
+    y = np.zeros(d.shape[0] + 1)
+    _L().or_tmul(d.shape[0], o.shape[0], _p(o), _p(nb), _p(d), _p(u), _p(lo), _p(xx), _p(y))
+    return y[:d.shape[0]]
+
+
+def amul_asym(owner, neighbour, diag, upper, lower, x) -> np.ndarray:
+    """y = A x for lower != upper (row owner: upper, row neighbour: lower)."""
+    o, nb, d, u, lo, xx = _i32(owner), _i32(neighbour), _f64(diag), _f64(upper), _f64(lower), _f64(x)
+    y = np.zeros(d.shape[0] + 1)
+    _L().or_amul(d.shape[0], o.shape[0], _p(o), _p(nb), _p(d), _p(lo), _p(u), _p(xx), 0, None, None, None, _p(y))
+    return y[:d.shape[0]]
+
+
+def ldu_to_csr(n_cells: int, owner, neighbour):
+    """O12 LDU -> CSR: (row_ptr, col, map) with map into [diag | upper | lower] (Q34)."""
+    o, nb = _i32(owner), _i32(neighbour)
+    F = o.shape[0]
+    nnz = n_cells + 2 * F
+    rp, col, mp = np.zeros(n_cells + 1, np.int32), np.zeros(nnz + 1, np.int32), np.zeros(nnz + 1, np.int32)
+    _L().or_ldu_to_csr(n_cells, F, _p(o), _p(nb), _p(rp), _p(col), _p(mp))
+    return rp, col[:nnz], mp[:nnz]
 
 
 def gamma_halo(meshes: Sequence[gen.Mesh], gammas: Sequence[np.ndarray]):

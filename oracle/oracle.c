@@ -21,6 +21,8 @@
  *   O7 dense        or_dense_from_ldu, or_dense_matvec, or_dense_solve    brute force for N <= 64
  *   O9 around       or_surface_integrate, or_face_flux
  *   O10 non-orth    or_gauss_grad, or_nonorth_flux                        P:1112, P:1135, P:1145 (Gauss linear corrected)
+ *   O12 precond.    or_ilu_factor, or_ilu_precondition, or_pcg_pc, or_pbicg, or_tmul, or_ldu_to_csr
+ *                   P:509
  *   O11 GAMG        or_agglomerate, or_coarse_addressing, or_agglomerate_matrix, or_restrict, or_gamg
  *                   P:517
  *
@@ -1056,6 +1058,267 @@ int or_gamg(int n, int F, const int* owner, const int* neighbour, const double* 
     free(sumA);
     free(r);
     return 0;
+}
+
+/* ------------------------------------------------------------------------- */
+/* O12 preconditioners (readings Q31-Q35): diagonal, DIC,  */
+/* DILU, aDILU; PCG with any of them; PBiCG (*/
+/* P:566); LDU -> CSR map.                           */
+/* ------------------------------------------------------------------------- */
+
+/* [OF] DIC/DILU calcReciprocalD: rD = diag; faces in order: rD[nbr] -= upper*lower/rD[own];
+ * then rD = 1/rD (DIC: lower = upper). */
+void or_ilu_factor(int n, int F, const int* owner, const int* neighbour, const double* diag, const double* upper,
+                   const double* lower, double* rD)
+{
+    for (int c = 0; c < n; ++c) rD[c] = diag[c];
+    for (int f = 0; f < F; ++f) rD[neighbour[f]] -= upper[f] * lower[f] / rD[owner[f]];
+    for (int c = 0; c < n; ++c) rD[c] = 1.0 / rD[c];
+}
+
+/* [OF] DIC/DILU precondition: w = rD r; forward over faces: w[nbr] -= rD[nbr]*lower*w[own];
+ * backward over faces in reverse: w[own] -= rD[own]*upper*w[nbr].  transpose (preconditionT)
+ * swaps the roles of lower and upper.  k >= 0 (aDILU, Q33): each sweep replaced by k
+ * Jacobi-style passes of the same face update reading the previous pass's values. */
+void or_ilu_precondition(int n, int F, const int* owner, const int* neighbour, const double* rD, const double* upper,
+                         const double* lower, const double* r, double* w, int transpose, int k)
+{
+    const double* lo = transpose ? upper : lower;
+    const double* up = transpose ? lower : upper;
+    for (int c = 0; c < n; ++c) w[c] = rD[c] * r[c];
+    if (k < 0) {
+        for (int f = 0; f < F; ++f) w[neighbour[f]] -= rD[neighbour[f]] * lo[f] * w[owner[f]];
+        for (int f = F - 1; f >= 0; --f) w[owner[f]] -= rD[owner[f]] * up[f] * w[neighbour[f]];
+        return;
+    }
+    double* y0 = (double*)malloc(sizeof(double) * (size_t)(n + 1));
+    double* prev = (double*)malloc(sizeof(double) * (size_t)(n + 1));
+    for (int c = 0; c < n; ++c) y0[c] = w[c];
+    for (int it = 0; it < k; ++it) { /* forward: w = rD r - (rD lower) w_prev */
+        for (int c = 0; c < n; ++c) prev[c] = w[c];
+        for (int c = 0; c < n; ++c) w[c] = y0[c];
+        for (int f = 0; f < F; ++f) w[neighbour[f]] -= rD[neighbour[f]] * lo[f] * prev[owner[f]];
+    }
+    for (int c = 0; c < n; ++c) y0[c] = w[c];
+    for (int it = 0; it < k; ++it) { /* backward: w = y - (rD upper) w_prev */
+        for (int c = 0; c < n; ++c) prev[c] = w[c];
+        for (int c = 0; c < n; ++c) w[c] = y0[c];
+        for (int f = F - 1; f >= 0; --f) w[owner[f]] -= rD[owner[f]] * up[f] * prev[neighbour[f]];
+    }
+    free(y0);
+    free(prev);
+}
+
+enum { OR_PC_DIAGONAL = 0, OR_PC_DIC = 1, OR_PC_DILU = 2, OR_PC_ADILU = 3 };
+
+static void or_pc_setup(int kind, int n, int F, const int* owner, const int* neighbour, const double* diag,
+                        const double* upper, const double* lower, double* rD)
+{
+    if (kind == OR_PC_DIAGONAL) {
+        for (int c = 0; c < n; ++c) rD[c] = 1.0 / diag[c];
+    } else {
+        or_ilu_factor(n, F, owner, neighbour, diag, upper, kind == OR_PC_DIC ? upper : lower, rD);
+    }
+}
+
+static void or_pc_apply(int kind, int k, int n, int F, const int* owner, const int* neighbour, const double* rD,
+                        const double* upper, const double* lower, const double* r, double* w, int transpose)
+{
+    if (kind == OR_PC_DIAGONAL) {
+        for (int c = 0; c < n; ++c) w[c] = rD[c] * r[c];
+    } else {
+        or_ilu_precondition(n, F, owner, neighbour, rD, upper, kind == OR_PC_DIC ? upper : lower, r, w, transpose,
+                            kind == OR_PC_ADILU ? k : -1);
+    }
+}
+
+/* normFactor (Q1) of a single domain */
+static double or_norm_factor(int n, int F, const int* owner, const int* neighbour, const double* diag,
+                             const double* lower, const double* upper, const double* source, const double* psi,
+                             const double* wA)
+{
+    double* sumA = (double*)malloc(sizeof(double) * (size_t)(n + 1));
+    for (int c = 0; c < n; ++c) sumA[c] = diag[c]; /* row sums: row owner holds upper, row neighbour lower */
+    for (int f = 0; f < F; ++f) {
+        sumA[owner[f]] += upper[f];
+        sumA[neighbour[f]] += lower[f];
+    }
+    double spsi = 0.0;
+    for (int c = 0; c < n; ++c) spsi += psi[c];
+    const double xbar = spsi / (double)n;
+    double nf = 0.0;
+    for (int c = 0; c < n; ++c) {
+        const double xref = sumA[c] * xbar;
+        nf += fabs(wA[c] - xref) + fabs(source[c] - xref);
+    }
+    free(sumA);
+    return nf + 1e-20;
+}
+
+/* PCG with a general preconditioner (single domain), OpenFOAM PCG::solve (Q1-Q4):
+ * wA = M^-1 rA; wArA = wA.rA; pA = wA (+ beta pA); wA = A pA; alpha = wArA / wA.pA;
+ * psi += alpha pA; rA -= alpha wA; final = |rA| / normFactor. */
+int or_pcg_pc(int n, int F, const int* owner, const int* neighbour, const double* diag, const double* upper,
+              const double* source, double* psi, const or_controls* ctl, int kind, int k, or_perf* perf)
+{
+    double* wA = (double*)calloc((size_t)n + 1, sizeof(double));
+    double* rA = (double*)calloc((size_t)n + 1, sizeof(double));
+    double* pA = (double*)calloc((size_t)n + 1, sizeof(double));
+    double* rD = (double*)calloc((size_t)n + 1, sizeof(double));
+    or_amul(n, F, owner, neighbour, diag, upper, upper, psi, 0, 0, 0, 0, wA);
+    for (int c = 0; c < n; ++c) rA[c] = source[c] - wA[c];
+    const double normFactor = or_norm_factor(n, F, owner, neighbour, diag, upper, upper, source, psi, wA);
+    double s = 0.0;
+    for (int c = 0; c < n; ++c) s += fabs(rA[c]);
+    perf->initial_residual = s / normFactor;
+    perf->final_residual = perf->initial_residual;
+    perf->n_iterations = 0;
+    perf->singular = 0;
+    if (ctl->min_iter > 0 || !or_conv(perf->final_residual, perf->initial_residual, ctl)) {
+        or_pc_setup(kind, n, F, owner, neighbour, diag, upper, upper, rD);
+        double wArA = 1e20, wArAold;
+        do {
+            wArAold = wArA;
+            or_pc_apply(kind, k, n, F, owner, neighbour, rD, upper, upper, rA, wA, 0);
+            wArA = 0.0;
+            for (int c = 0; c < n; ++c) wArA += wA[c] * rA[c];
+            if (perf->n_iterations == 0) {
+                for (int c = 0; c < n; ++c) pA[c] = wA[c];
+            } else {
+                const double beta = wArA / wArAold;
+                for (int c = 0; c < n; ++c) pA[c] = wA[c] + beta * pA[c];
+            }
+            or_amul(n, F, owner, neighbour, diag, upper, upper, pA, 0, 0, 0, 0, wA);
+            double wApA = 0.0;
+            for (int c = 0; c < n; ++c) wApA += wA[c] * pA[c];
+            if (fabs(wApA) / normFactor < 1e-300) {
+                perf->singular = 1;
+                break;
+            }
+            const double alpha = wArA / wApA;
+            s = 0.0;
+            for (int c = 0; c < n; ++c) {
+                psi[c] += alpha * pA[c];
+                rA[c] -= alpha * wA[c];
+                s += fabs(rA[c]);
+            }
+            perf->final_residual = s / normFactor;
+        } while ((++perf->n_iterations < ctl->max_iter && !or_conv(perf->final_residual, perf->initial_residual, ctl)) ||
+                 perf->n_iterations < ctl->min_iter);
+    }
+    perf->converged = or_conv(perf->final_residual, perf->initial_residual, ctl);
+    free(wA); free(rA); free(pA); free(rD);
+    return 0;
+}
+
+/* Tmul: y = A^T x (upper and lower swap roles) */
+void or_tmul(int n, int F, const int* owner, const int* neighbour, const double* diag, const double* upper,
+             const double* lower, const double* x, double* y)
+{
+    or_amul(n, F, owner, neighbour, diag, upper, lower, x, 0, 0, 0, 0, y); /* or_amul(diag, lower, upper): swapped */
+}
+
+/* [OF] PBiCG::solve (Q32): rA = b - A psi, rT = b - A^T psi; per iteration wA = M^-1 rA,
+ * wT = M^-T rT, wArT = wA.rT, pA/pT = w + beta p, wA = A pA, wT = A^T pT, wApT = wA.pT,
+ * alpha = wArT/wApT, psi += alpha pA, rA -= alpha wA, rT -= alpha wT. */
+int or_pbicg(int n, int F, const int* owner, const int* neighbour, const double* diag, const double* upper,
+             const double* lower, const double* source, double* psi, const or_controls* ctl, int kind, int k,
+             or_perf* perf)
+{
+    double* wA = (double*)calloc((size_t)n + 1, sizeof(double));
+    double* wT = (double*)calloc((size_t)n + 1, sizeof(double));
+    double* rA = (double*)calloc((size_t)n + 1, sizeof(double));
+    double* rT = (double*)calloc((size_t)n + 1, sizeof(double));
+    double* pA = (double*)calloc((size_t)n + 1, sizeof(double));
+    double* pT = (double*)calloc((size_t)n + 1, sizeof(double));
+    double* rD = (double*)calloc((size_t)n + 1, sizeof(double));
+    or_amul(n, F, owner, neighbour, diag, lower, upper, psi, 0, 0, 0, 0, wA);
+    or_tmul(n, F, owner, neighbour, diag, upper, lower, psi, wT);
+    for (int c = 0; c < n; ++c) {
+        rA[c] = source[c] - wA[c];
+        rT[c] = source[c] - wT[c];
+    }
+    const double normFactor = or_norm_factor(n, F, owner, neighbour, diag, lower, upper, source, psi, wA);
+    double s = 0.0;
+    for (int c = 0; c < n; ++c) s += fabs(rA[c]);
+    perf->initial_residual = s / normFactor;
+    perf->final_residual = perf->initial_residual;
+    perf->n_iterations = 0;
+    perf->singular = 0;
+    if (ctl->min_iter > 0 || !or_conv(perf->final_residual, perf->initial_residual, ctl)) {
+        or_pc_setup(kind, n, F, owner, neighbour, diag, upper, lower, rD);
+        double wArT = 1e300, wArTold;
+        do {
+            wArTold = wArT;
+            or_pc_apply(kind, k, n, F, owner, neighbour, rD, upper, lower, rA, wA, 0);
+            or_pc_apply(kind, k, n, F, owner, neighbour, rD, upper, lower, rT, wT, 1);
+            wArT = 0.0;
+            for (int c = 0; c < n; ++c) wArT += wA[c] * rT[c];
+            if (perf->n_iterations == 0) {
+                for (int c = 0; c < n; ++c) {
+                    pA[c] = wA[c];
+                    pT[c] = wT[c];
+                }
+            } else {
+                const double beta = wArT / wArTold;
+                for (int c = 0; c < n; ++c) {
+                    pA[c] = wA[c] + beta * pA[c];
+                    pT[c] = wT[c] + beta * pT[c];
+                }
+            }
+            or_amul(n, F, owner, neighbour, diag, lower, upper, pA, 0, 0, 0, 0, wA);
+            or_tmul(n, F, owner, neighbour, diag, upper, lower, pT, wT);
+            double wApT = 0.0;
+            for (int c = 0; c < n; ++c) wApT += wA[c] * pT[c];
+            if (fabs(wApT) / normFactor < 1e-300) {
+                perf->singular = 1;
+                break;
+            }
+            const double alpha = wArT / wApT;
+            s = 0.0;
+            for (int c = 0; c < n; ++c) {
+                psi[c] += alpha * pA[c];
+                rA[c] -= alpha * wA[c];
+                rT[c] -= alpha * wT[c];
+                s += fabs(rA[c]);
+            }
+            perf->final_residual = s / normFactor;
+        } while ((++perf->n_iterations < ctl->max_iter && !or_conv(perf->final_residual, perf->initial_residual, ctl)) ||
+                 perf->n_iterations < ctl->min_iter);
+    }
+    perf->converged = or_conv(perf->final_residual, perf->initial_residual, ctl);
+    free(wA); free(wT); free(rA); free(rT); free(pA); free(pT); free(rD);
+    return 0;
+}
+
+/* LDU -> CSR (Q34; "a map computed by the Radix sort ... of the sparsity pattern"):
+ * rows ascending, columns ascending within a row; map[k] indexes [diag (n) | upper (F) | lower (F)]:
+ * row P col N (P = owner) is upper[f], row N col P is lower[f].  row_ptr [n+1], col/map [n+2F]. */
+static int or_csr_cmp(const void* a, const void* b)
+{
+    const int* x = (const int*)a;
+    const int* y = (const int*)b;
+    if (x[0] != y[0]) return x[0] < y[0] ? -1 : 1;
+    return x[1] < y[1] ? -1 : (x[1] > y[1]);
+}
+
+void or_ldu_to_csr(int n, int F, const int* owner, const int* neighbour, int* row_ptr, int* col, int* map)
+{
+    const int nnz = n + 2 * F;
+    int* t = (int*)malloc(sizeof(int) * 3 * (size_t)(nnz + 1));
+    int m = 0;
+    for (int c = 0; c < n; ++c, ++m) t[3 * m] = c, t[3 * m + 1] = c, t[3 * m + 2] = c;
+    for (int f = 0; f < F; ++f, ++m) t[3 * m] = owner[f], t[3 * m + 1] = neighbour[f], t[3 * m + 2] = n + f;
+    for (int f = 0; f < F; ++f, ++m) t[3 * m] = neighbour[f], t[3 * m + 1] = owner[f], t[3 * m + 2] = n + F + f;
+    qsort(t, (size_t)nnz, 3 * sizeof(int), or_csr_cmp);
+    for (int c = 0; c <= n; ++c) row_ptr[c] = 0;
+    for (int i = 0; i < nnz; ++i) {
+        row_ptr[t[3 * i] + 1]++;
+        col[i] = t[3 * i + 1];
+        map[i] = t[3 * i + 2];
+    }
+    for (int c = 0; c < n; ++c) row_ptr[c + 1] += row_ptr[c];
+    free(t);
 }
 
 /* ------------------------------------------------------------------------- */

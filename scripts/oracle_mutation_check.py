@@ -46,10 +46,23 @@ muts = [
  ("for (int f = 0; f < L->F; ++f) t[L->neighbour[f]] -= L->upper[f] * z[L->owner[f]];", "for (int f = 0; f < L->F; ++f) t[L->owner[f]] -= L->upper[f] * z[L->neighbour[f]];"),
  ("for (int i = 0; i < L->n; ++i) z[i] = L->rD[i] * t[i];", "for (int i = 0; i < L->n; ++i) z[i] = t[i];"),
  ("    if (gp->smoother == 1) or_gs2_sweep(L, gp->n_inner);", "    if (gp->smoother == 1) or_gs2_sweep(L, gp->n_inner > 0 ? gp->n_inner - 1 : 0);"),
+ # O12 preconditioners / PBiCG / CSR
+ ("for (int f = 0; f < F; ++f) rD[neighbour[f]] -= upper[f] * lower[f] / rD[owner[f]];", "for (int f = 0; f < F; ++f) rD[neighbour[f]] -= upper[f] * lower[f] / rD[neighbour[f]];"),
+ ("    for (int c = 0; c < n; ++c) rD[c] = 1.0 / rD[c];\n}", "    ;\n}"),
+ ("for (int f = 0; f < F; ++f) w[neighbour[f]] -= rD[neighbour[f]] * lo[f] * w[owner[f]];", "for (int f = 0; f < F; ++f) w[neighbour[f]] -= rD[neighbour[f]] * up[f] * w[owner[f]];"),
+ ("for (int f = F - 1; f >= 0; --f) w[owner[f]] -= rD[owner[f]] * up[f] * w[neighbour[f]];\n        return;", "for (int f = 0; f < F; ++f) w[owner[f]] -= rD[owner[f]] * up[f] * w[neighbour[f]];\n        return;"),
+ ("w[neighbour[f]] -= rD[neighbour[f]] * lo[f] * prev[owner[f]];", "w[neighbour[f]] -= rD[neighbour[f]] * lo[f] * w[owner[f]];"),
+ ("                rT[c] -= alpha * wT[c];", "                rT[c] -= alpha * wA[c];"),
+ ("or_pc_apply(kind, k, n, F, owner, neighbour, rD, upper, lower, rT, wT, 1);", "or_pc_apply(kind, k, n, F, owner, neighbour, rD, upper, lower, rT, wT, 0);"),
+ ("    or_amul(n, F, owner, neighbour, diag, upper, lower, x, 0, 0, 0, 0, y); /* or_amul(diag, lower, upper): swapped */", "    or_amul(n, F, owner, neighbour, diag, lower, upper, x, 0, 0, 0, 0, y);"),
+ ("t[3 * m + 2] = n + F + f;", "t[3 * m + 2] = n + f;"),
+ ("        sumA[owner[f]] += upper[f];\n        sumA[neighbour[f]] += lower[f];", "        sumA[owner[f]] += lower[f];\n        sumA[neighbour[f]] += upper[f];"),
 ]
 sel = os.environ.get("MUT_SELECT")  # e.g. "GAMG": only mutants after that marker
 if sel == "GAMG":
     muts = muts[[a for a, _ in muts].index("if (ftc[o] < 0 && w[f] > bw) {"):]
+elif sel == "O12":
+    muts = muts[[a for a, _ in muts].index("for (int f = 0; f < F; ++f) rD[neighbour[f]] -= upper[f] * lower[f] / rD[owner[f]];"):]
 res = []
 for a, b in muts:
     assert a in src, a

@@ -45,3 +45,20 @@ def lattice_modes(dims, ks, kind):
 def eigenvalue(dims, ks, coefs):
     """lambda = -sum_d coef_d 4 sin^2(pi k_d / (2 n_d)) (ghost-mirror identity)."""
     return -sum(c * 4.0 * np.sin(np.pi * k / (2.0 * n)) ** 2 for n, k, c in zip(dims, ks, coefs))
+
+
+def asym_system(mesh, seed=0, skew=0.4):
+    """Test input for the asymmetric solvers (§8(f3)): the Laplacian's coefficients made
+    asymmetric like a convection-diffusion operator, upper = u (1 + e), lower = u (1 - e),
+    e ~ U(-skew, skew) per face, and a diagonal that dominates the row sums by 5 %
+    (negative, like the Laplacian).  Returns (diag, upper, lower, source)."""
+    import oracle as O
+    s = O.assemble(mesh, None, -1)
+    rng = np.random.default_rng(seed)
+    e = rng.uniform(-skew, skew, mesh.n_faces)
+    upper, lower = s.upper * (1 + e), s.upper * (1 - e)
+    off = np.zeros(mesh.n_cells)
+    np.add.at(off, mesh.owner, np.abs(upper))
+    np.add.at(off, mesh.neighbour, np.abs(lower))
+    diag = -1.05 * np.maximum(off, 1e-12)
+    return diag, upper, lower, rng.standard_normal(mesh.n_cells) * mesh.V
