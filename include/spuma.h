@@ -234,6 +234,69 @@ spuma_status spuma_gamg_get_hierarchy(spuma_mesh m, const spuma_gamg_params* par
                                       int* n_levels, int* level_cells, int* level_faces, int level,
                                       spuma_label* ftc);
 
+/* ---------------- preconditioned solvers (readings Q31-Q35) ----------------
+ * DIC / DILU (OpenFOAM's incomplete factorisations with a diagonal-only factor, P:566, P:665,
+ * P:672), aDILU (DILU factor, each triangular sweep replaced by n_sweeps Jacobi-style passes,
+ * reading Q33 — the paper's "aDILUPreconditioner", never defined), diagonal.  The
+ * factor and the exact sweeps are sequential recurrences in face order; libspuma runs them
+ * as dependency-scheduled persistent kernels, bitwise equal to the sequential loops for any
+ * numbering (their critical path is the mesh's dependency depth: a colour / wavefront
+ * numbering makes them fast, the natural order of an n^3 box has depth ~3n).
+ * All of these are single-rank (n_ranks > 1 -> SPUMA_ERR_STATE). */
+typedef enum spuma_precond_kind {
+    SPUMA_PC_DIAGONAL = 0,
+    SPUMA_PC_DIC = 1,
+    SPUMA_PC_DILU = 2,
+    SPUMA_PC_ADILU = 3
+} spuma_precond_kind;
+
+typedef struct spuma_preconditioner {
+    int kind;      /* spuma_precond_kind                                   */
+    int n_sweeps;  /* aDILU: Jacobi-style passes per triangular sweep (2)  */
+} spuma_preconditioner;
+
+/*
+ * PCG (Q1-Q4 semantics) with the preconditioner pc (NULL: diagonal): per iteration
+ * wA = M^-1 rA, wArA = wA.rA, pA = wA + beta pA, wA = A pA, alpha = wArA / wA.pA, psi and rA
+ * updated.  Arguments as spuma_pcg_solve (symmetric matrix: upper only).  Errors as
+ * spuma_pcg_solve plus STATE (n_ranks > 1), INVALID_ARGUMENT (unknown kind, n_sweeps < 0).
+ */
+spuma_status spuma_pcg_solve_pc(spuma_mesh m, const spuma_scalar* diag, const spuma_scalar* upper,
+                                const spuma_scalar* source, spuma_scalar* psi, const spuma_solver_controls* ctl,
+                                const spuma_preconditioner* pc, spuma_solver_perf* perf);
+
+/*
+ * PBiCG (Q32) for an asymmetric LDU matrix: lower [n_faces] is
+ * the coefficient of row neighbour, column owner; upper of row owner, column neighbour.
+ * pc NULL: aDILU with 2 passes (the paper's setting).  psi in/out.  Single-rank.
+ */
+spuma_status spuma_pbicg_solve(spuma_mesh m, const spuma_scalar* diag, const spuma_scalar* upper,
+                               const spuma_scalar* lower, const spuma_scalar* source, spuma_scalar* psi,
+                               const spuma_solver_controls* ctl, const spuma_preconditioner* pc,
+                               spuma_solver_perf* perf);
+
+/*
+ * Diagnostics of the above: w = M^-1 r (transpose != 0: M^-T r) with M built from
+ * (diag, upper, lower) (lower NULL: = upper), and y = A x (transpose: A^T x) of the
+ * asymmetric matrix.  Arrays [n_cells] / [n_faces] in the caller's numbering.
+ */
+spuma_status spuma_precondition(spuma_mesh m, const spuma_scalar* diag, const spuma_scalar* upper,
+                                const spuma_scalar* lower, const spuma_preconditioner* pc, const spuma_scalar* r,
+                                spuma_scalar* w, int transpose);
+spuma_status spuma_amul_asym(spuma_mesh m, const spuma_scalar* diag, const spuma_scalar* upper,
+                             const spuma_scalar* lower, const spuma_scalar* x, spuma_scalar* y, int transpose);
+
+/*
+ * LDU -> CSR (Q34, the map AmgX-style consumers need): row_ptr [n_cells+1],
+ * col [n_cells + 2 n_faces] with ascending columns per row, map [same] indexing the
+ * concatenation [diag | upper | lower]; host or device pointers.  The values of a matrix are
+ * then spuma_csr_values (a device gather).  Handles built with renumber = 0 only
+ * (SPUMA_ERR_STATE otherwise): the CSR is in the caller's numbering.
+ */
+spuma_status spuma_ldu_to_csr(spuma_mesh m, spuma_label* row_ptr, spuma_label* col, spuma_label* map);
+spuma_status spuma_csr_values(spuma_mesh m, const spuma_scalar* diag, const spuma_scalar* upper,
+                              const spuma_scalar* lower, spuma_scalar* values);
+
 /* ---------------- around the path (the pressure step's neighbours) ----------------
  * Oriented face fields (phi, flux) are owner -> neighbour in the CALLER's numbering; with
  * renumber = 1 faces whose owner/neighbour swapped are negated on entry and exit.  Per-patch

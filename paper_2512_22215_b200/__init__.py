@@ -5,6 +5,6 @@ The product is libspuma.so (csrc/: host C++ + sm_100a CUDA kernels + NCCL);
 ``spuma`` is its thin ctypes binding.  This package never imports ``oracle``.
 """
 from . import spuma
-from .spuma import GamgParams, Mesh, SpumaError, gamg_params, mesh_create, nccl_get_unique_id  # noqa: F401
+from .spuma import GamgParams, Mesh, Preconditioner, SpumaError, gamg_params, mesh_create, nccl_get_unique_id  # noqa: F401
 
 __all__ = ["spuma", "Mesh", "SpumaError", "GamgParams", "gamg_params", "mesh_create", "nccl_get_unique_id"]

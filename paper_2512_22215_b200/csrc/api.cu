@@ -688,6 +688,148 @@ int gamg_enqueue_cycle(spuma_mesh m, const spuma_gamg_params& gp, cudaStream_t s
     return k + 1;
 }
 
+// ---------------------------------------------------------------------------
+// preconditioned solvers (§8(f3)/(f4)): level schedules + buffers, kept by the handle
+// ---------------------------------------------------------------------------
+}  // namespace
+
+struct PcState {
+    int *order_f = nullptr, *order_b = nullptr, *flag = nullptr;
+    unsigned* counter = nullptr;
+    int depth_f = 0, depth_b = 0;
+    double *raw = nullptr, *rD = nullptr, *t1 = nullptr, *t2 = nullptr;
+    double *wT = nullptr, *rT = nullptr, *pT = nullptr, *part = nullptr;
+    double *u_in = nullptr, *l_in = nullptr, *u_int = nullptr, *l_int = nullptr;
+    int* csr_map = nullptr;  // device copy of the CSR map
+    int nnz = 0;
+};
+
+namespace {
+
+void pc_release(spuma_mesh m)
+{
+    PcState* P = m->pc;
+    if (!P) return;
+    void* ptrs[] = {P->order_f, P->order_b, P->flag, P->counter, P->raw, P->rD, P->t1, P->t2, P->wT, P->rT,
+                    P->pT, P->part, P->u_in, P->l_in, P->u_int, P->l_int, P->csr_map};
+    for (void* q : ptrs)
+        if (q) cudaFree(q);
+    delete P;
+    m->pc = nullptr;
+}
+
+// dependency levels: forward row c waits on the owners of its neighbour-side faces, backward
+// row c on the neighbours of its owner-side faces; rows sorted by level (ascending cell within)
+spuma_status pc_ensure(spuma_mesh m)
+{
+    if (m->pc) return SPUMA_OK;
+    PcState* P = new PcState();
+    m->pc = P;
+    const int N = m->N;
+    std::vector<int> lf(N, 0), lb(N, 0);
+    for (int c = 0; c < N; ++c)
+        for (int k = m->h_losortStart[c]; k < m->h_losortStart[c + 1]; ++k)
+            lf[c] = std::max(lf[c], lf[m->h_owner[m->h_losort[k]]] + 1);
+    for (int c = N - 1; c >= 0; --c)
+        for (int f = m->h_ownerStart[c]; f < m->h_ownerStart[c + 1]; ++f)
+            lb[c] = std::max(lb[c], lb[m->h_neighbour[f]] + 1);
+    auto order_by = [N](const std::vector<int>& lev, int& depth) {
+        depth = 0;
+        for (int c = 0; c < N; ++c) depth = std::max(depth, lev[c] + 1);
+        std::vector<int> start(depth + 1, 0), ord(N);
+        for (int c = 0; c < N; ++c) start[lev[c] + 1]++;
+        for (int d = 0; d < depth; ++d) start[d + 1] += start[d];
+        for (int c = 0; c < N; ++c) ord[start[lev[c]]++] = c;
+        return ord;
+    };
+    cudaStream_t s = m->stream;
+    SPUMA_TRY(upload(&P->order_f, order_by(lf, P->depth_f), s));
+    SPUMA_TRY(upload(&P->order_b, order_by(lb, P->depth_b), s));
+    SPUMA_TRY(dalloc(&P->flag, N + 1));
+    SPUMA_TRY(dalloc(&P->counter, 1));
+    for (double** b : {&P->raw, &P->rD, &P->t1, &P->t2, &P->wT, &P->rT, &P->pT}) SPUMA_TRY(dalloc(b, N));
+    SPUMA_TRY(dalloc(&P->part, (size_t)kMaxPartials * pc_grid(N)));
+    SPUMA_CUDA(cudaStreamSynchronize(s));
+    return SPUMA_OK;
+}
+
+// (upper, lower) in internal numbering; lower == nullptr: lower = upper
+spuma_status pair_in(spuma_mesh m, const double* u, const double* l, const double** uo, const double** lo)
+{
+    if (!l) {
+        SPUMA_TRY(faces_in(m, u, uo));
+        *lo = *uo;
+        return SPUMA_OK;
+    }
+    PcState* P = m->pc;
+    cudaStream_t s = m->stream;
+    const bool du = is_device_ptr(u), dl = is_device_ptr(l);
+    if (!m->renumber && du && dl) {
+        *uo = u;
+        *lo = l;
+        return SPUMA_OK;
+    }
+    for (double** b : {&P->u_in, &P->l_in, &P->u_int, &P->l_int})
+        if (!*b) SPUMA_TRY(dalloc(b, m->F));
+    const double* su = u;
+    const double* sl = l;
+    if (!du) {
+        SPUMA_CUDA(cudaMemcpyAsync(P->u_in, u, sizeof(double) * m->F, cudaMemcpyHostToDevice, s));
+        su = P->u_in;
+    }
+    if (!dl) {
+        SPUMA_CUDA(cudaMemcpyAsync(P->l_in, l, sizeof(double) * m->F, cudaMemcpyHostToDevice, s));
+        sl = P->l_in;
+    }
+    if (!m->renumber) {
+        *uo = su;
+        *lo = sl;
+        return SPUMA_OK;
+    }
+    launch_gather_pair(s, m->F, m->d_face_map, m->d_face_flip, su, sl, P->u_int, P->l_int);
+    *uo = P->u_int;
+    *lo = P->l_int;
+    return SPUMA_OK;
+}
+
+spuma_status pc_check(spuma_mesh m, const spuma_preconditioner& pc)
+{
+    if (m->n_ranks > 1) return set_error(SPUMA_ERR_STATE, "preconditioned solvers are single-rank (DESIGN.md §3)");
+    if (pc.kind < SPUMA_PC_DIAGONAL || pc.kind > SPUMA_PC_ADILU || pc.n_sweeps < 0)
+        return set_error(SPUMA_ERR_INVALID_ARGUMENT, "invalid preconditioner");
+    return SPUMA_OK;
+}
+
+// M from (diag, upper, lower): rD into P->rD (diagonal: 1/diag)
+void pc_setup(spuma_mesh m, const spuma_preconditioner& pc, const double* d, const double* u, const double* l)
+{
+    PcState* P = m->pc;
+    const MeshArgs a = mesh_args(m);
+    if (pc.kind == SPUMA_PC_DIAGONAL) {
+        launch_recip(m->stream, m->N, d, P->rD);
+        return;
+    }
+    launch_ilu_factor(m->stream, a, P->order_f, d, u, pc.kind == SPUMA_PC_DIC ? u : l, P->raw, P->rD, P->flag,
+                      P->counter);
+}
+
+void pc_apply(spuma_mesh m, const spuma_preconditioner& pc, const double* u, const double* l, const double* r,
+              double* w, bool transpose, const DevScal* scal)
+{
+    PcState* P = m->pc;
+    const int k = pc.kind == SPUMA_PC_DIAGONAL ? 0 : (pc.kind == SPUMA_PC_ADILU ? pc.n_sweeps : -1);
+    launch_ilu_precondition(m->stream, mesh_args(m), P->order_f, P->order_b, P->rD, u,
+                            pc.kind == SPUMA_PC_DIC ? u : l, r, w, P->t1, P->t2, P->flag, P->counter, k, transpose,
+                            scal);
+}
+
+uint64_t pc_launches(const spuma_preconditioner& pc)
+{
+    if (pc.kind == SPUMA_PC_DIAGONAL) return 1;
+    if (pc.kind == SPUMA_PC_ADILU) return pc.n_sweeps ? 1 + 2 * (uint64_t)pc.n_sweeps : 1;
+    return 2;
+}
+
 uint64_t launches_per_iteration(spuma_mesh m)
 {
     uint64_t k = 3;
@@ -722,6 +864,7 @@ void spuma_free(spuma_mesh m)
     if (m->stream) cudaStreamSynchronize(m->stream);
     destroy_graphs(m);
     gamg_release(m);
+    pc_release(m);
     for (int i = 0; i < 2; ++i) {
         if (m->batch_done[i]) cudaEventDestroy(m->batch_done[i]);
         if (m->asm_ev[i]) cudaEventDestroy(m->asm_ev[i]);
@@ -1660,6 +1803,238 @@ spuma_status spuma_gamg_get_hierarchy(spuma_mesh m, const spuma_gamg_params* par
         if (level < 0 || level >= nl - 1) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "level has no coarser level");
         std::memcpy(ftc, G->ftc[level].data(), sizeof(int) * G->ftc[level].size());
     }
+    return SPUMA_OK;
+}
+
+spuma_status spuma_pcg_solve_pc(spuma_mesh m, const spuma_scalar* diag, const spuma_scalar* upper,
+                                const spuma_scalar* source, spuma_scalar* psi, const spuma_solver_controls* ctl,
+                                const spuma_preconditioner* pcp, spuma_solver_perf* perf)
+{
+    if (!m) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "mesh is NULL");
+    if (!ctl || !perf) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "NULL controls/perf");
+    if (m->N > 0 && (!diag || !source || !psi)) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "NULL array");
+    if (m->F > 0 && !upper) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "upper is NULL");
+    if (ctl->max_iter < 0 || ctl->min_iter < 0) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "negative iteration limit");
+    const spuma_preconditioner pc = pcp ? *pcp : spuma_preconditioner{SPUMA_PC_DIAGONAL, 0};
+    SPUMA_TRY(pc_check(m, pc));
+    if (m->N == 0) {
+        *perf = spuma_solver_perf{};
+        return SPUMA_OK;
+    }
+    SPUMA_TRY(pc_ensure(m));
+    cudaStream_t s = m->stream;
+    DevPtrs Pp{};
+    const double* psi_in = nullptr;
+    SPUMA_TRY(cells_in(m, diag, R_DIAG, &Pp.diag));
+    SPUMA_TRY(faces_in(m, upper, &Pp.upper));
+    SPUMA_TRY(cells_in(m, source, R_SOURCE, &Pp.source));
+    SPUMA_TRY(cells_in(m, psi, R_PSI, &psi_in));
+    Pp.psi = const_cast<double*>(psi_in);
+    *m->h_ptrs = Pp;
+    SPUMA_CUDA(cudaMemcpyAsync(m->ws.ptrs, m->h_ptrs, sizeof(DevPtrs), cudaMemcpyHostToDevice, s));
+    launch_scal_init(s, m->ws, *ctl, 1);
+    const MeshArgs a = mesh_args(m);
+    if (amul_uses_ell(m->amul_variant) && m->d_upper_s) launch_ell_coeffs(s, a, Pp.upper, m->d_upper_s);
+    launch_setup1(s, m->grid, a, m->ws, true);
+    launch_setup2(s, m->grid, a, m->ws, true);
+    pc_setup(m, pc, Pp.diag, Pp.upper, Pp.upper);
+    m->stats.kernel_launches += 5;
+    PcState* P = m->pc;
+    Workspace w = m->ws;
+    SPUMA_CUDA(cudaMemcpyAsync(&m->h_scal[0], w.scal, sizeof(DevScal), cudaMemcpyDeviceToHost, s));
+    SPUMA_CUDA(cudaStreamSynchronize(s));
+    int it = 0;
+    while (!m->h_scal[0].done) {
+        for (int b = 0; b < 8; ++b) {  // kernels are no-ops once the device 'done' flag is set
+            pc_apply(m, pc, Pp.upper, Pp.upper, w.rA, w.wA, false, w.scal);
+            launch_pc_dot(s, m->N, w.wA, w.rA, P->part, w.scal);
+            launch_pc_direction(s, m->N, w.wA, w.pA, nullptr, nullptr, w.scal);
+            launch_amul_dot(s, m->amul_variant, a, w, true, m->sell_wn, m->sell_wo);
+            launch_update(s, m->grid, a, w, true, 0);
+            m->stats.kernel_launches += pc_launches(pc) + 4;
+        }
+        SPUMA_CUDA(cudaMemcpyAsync(&m->h_scal[0], w.scal, sizeof(DevScal), cudaMemcpyDeviceToHost, s));
+        SPUMA_CUDA(cudaStreamSynchronize(s));
+        it += 8;
+        if (it > ctl->max_iter + 16) return set_error(SPUMA_ERR_STATE, "PCG loop did not terminate");
+    }
+    SPUMA_CUDA(cudaGetLastError());
+    const DevScal fs = m->h_scal[0];
+    perf->initial_residual = fs.init;
+    perf->final_residual = fs.fin;
+    perf->n_iterations = fs.n;
+    perf->converged = fs.converged;
+    perf->singular = fs.singular;
+    m->stats.solves += 1;
+    m->stats.iterations += fs.n;
+    SPUMA_TRY(cells_out(m, psi, Pp.psi));
+    SPUMA_CUDA(cudaStreamSynchronize(s));
+    return SPUMA_OK;
+}
+
+spuma_status spuma_pbicg_solve(spuma_mesh m, const spuma_scalar* diag, const spuma_scalar* upper,
+                               const spuma_scalar* lower, const spuma_scalar* source, spuma_scalar* psi,
+                               const spuma_solver_controls* ctl, const spuma_preconditioner* pcp,
+                               spuma_solver_perf* perf)
+{
+    if (!m) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "mesh is NULL");
+    if (!ctl || !perf) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "NULL controls/perf");
+    if (m->N > 0 && (!diag || !source || !psi)) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "NULL array");
+    if (m->F > 0 && (!upper || !lower)) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "upper/lower is NULL");
+    if (ctl->max_iter < 0 || ctl->min_iter < 0) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "negative iteration limit");
+    const spuma_preconditioner pc = pcp ? *pcp : spuma_preconditioner{SPUMA_PC_ADILU, 2};
+    SPUMA_TRY(pc_check(m, pc));
+    if (m->N == 0) {
+        *perf = spuma_solver_perf{};
+        return SPUMA_OK;
+    }
+    SPUMA_TRY(pc_ensure(m));
+    PcState* P = m->pc;
+    cudaStream_t s = m->stream;
+    const double *d_i, *s_i, *psi_c, *u_i, *l_i;
+    SPUMA_TRY(cells_in(m, diag, R_DIAG, &d_i));
+    SPUMA_TRY(cells_in(m, source, R_SOURCE, &s_i));
+    SPUMA_TRY(cells_in(m, psi, R_PSI, &psi_c));
+    SPUMA_TRY(pair_in(m, upper, lower, &u_i, &l_i));
+    double* psi_i = const_cast<double*>(psi_c);
+    Workspace w = m->ws;
+    const MeshArgs a = mesh_args(m);
+    launch_scal_init(s, w, *ctl, 1);
+    launch_bicg_setup(s, a, d_i, u_i, l_i, s_i, psi_i, w.wA, P->wT, w.rA, P->rT, w.sumA, P->part, w.scal);
+    pc_setup(m, pc, d_i, u_i, l_i);
+    m->stats.kernel_launches += 4;
+    SPUMA_CUDA(cudaMemcpyAsync(&m->h_scal[0], w.scal, sizeof(DevScal), cudaMemcpyDeviceToHost, s));
+    SPUMA_CUDA(cudaStreamSynchronize(s));
+    int it = 0;
+    while (!m->h_scal[0].done) {
+        for (int b = 0; b < 8; ++b) {
+            pc_apply(m, pc, u_i, l_i, w.rA, w.wA, false, w.scal);
+            pc_apply(m, pc, u_i, l_i, P->rT, P->wT, true, w.scal);
+            launch_pc_dot(s, m->N, w.wA, P->rT, P->part, w.scal);
+            launch_pc_direction(s, m->N, w.wA, w.pA, P->wT, P->pT, w.scal);
+            launch_bicg_amul_tmul(s, a, d_i, u_i, l_i, w.pA, P->pT, w.wA, P->wT, P->part, w.scal);
+            launch_bicg_update(s, m->N, psi_i, w.pA, w.rA, w.wA, P->rT, P->wT, P->part, w.scal);
+            m->stats.kernel_launches += 2 * pc_launches(pc) + 4;
+        }
+        SPUMA_CUDA(cudaMemcpyAsync(&m->h_scal[0], w.scal, sizeof(DevScal), cudaMemcpyDeviceToHost, s));
+        SPUMA_CUDA(cudaStreamSynchronize(s));
+        it += 8;
+        if (it > ctl->max_iter + 16) return set_error(SPUMA_ERR_STATE, "PBiCG loop did not terminate");
+    }
+    SPUMA_CUDA(cudaGetLastError());
+    const DevScal fs = m->h_scal[0];
+    perf->initial_residual = fs.init;
+    perf->final_residual = fs.fin;
+    perf->n_iterations = fs.n;
+    perf->converged = fs.converged;
+    perf->singular = fs.singular;
+    m->stats.solves += 1;
+    m->stats.iterations += fs.n;
+    SPUMA_TRY(cells_out(m, psi, psi_i));
+    SPUMA_CUDA(cudaStreamSynchronize(s));
+    return SPUMA_OK;
+}
+
+spuma_status spuma_precondition(spuma_mesh m, const spuma_scalar* diag, const spuma_scalar* upper,
+                                const spuma_scalar* lower, const spuma_preconditioner* pcp, const spuma_scalar* r,
+                                spuma_scalar* wout, int transpose)
+{
+    if (!m || !pcp) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (m->N > 0 && (!diag || !r || !wout)) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "NULL array");
+    if (m->F > 0 && !upper) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "upper is NULL");
+    SPUMA_TRY(pc_check(m, *pcp));
+    if (m->N == 0) return SPUMA_OK;
+    SPUMA_TRY(pc_ensure(m));
+    PcState* P = m->pc;
+    cudaStream_t s = m->stream;
+    const double *d_i, *r_i, *u_i, *l_i;
+    SPUMA_TRY(cells_in(m, diag, R_DIAG, &d_i));
+    SPUMA_TRY(cells_in(m, r, R_X, &r_i));
+    SPUMA_TRY(pair_in(m, upper, lower, &u_i, &l_i));
+    pc_setup(m, *pcp, d_i, u_i, l_i);
+    if (!m->d_cell_t) SPUMA_TRY(dalloc(&m->d_cell_t, m->N));
+    pc_apply(m, *pcp, u_i, l_i, r_i, m->d_cell_t, transpose != 0, nullptr);
+    m->stats.kernel_launches += 2 + pc_launches(*pcp);
+    SPUMA_TRY(cells_out(m, wout, m->d_cell_t));
+    SPUMA_CUDA(cudaStreamSynchronize(s));
+    SPUMA_CUDA(cudaGetLastError());
+    (void)P;
+    return SPUMA_OK;
+}
+
+spuma_status spuma_amul_asym(spuma_mesh m, const spuma_scalar* diag, const spuma_scalar* upper,
+                             const spuma_scalar* lower, const spuma_scalar* x, spuma_scalar* y, int transpose)
+{
+    if (!m) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "mesh is NULL");
+    if (m->N > 0 && (!diag || !x || !y)) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "NULL array");
+    if (m->F > 0 && (!upper || !lower)) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "upper/lower is NULL");
+    if (m->N == 0) return SPUMA_OK;
+    SPUMA_TRY(pc_ensure(m));
+    cudaStream_t s = m->stream;
+    const double *d_i, *x_i, *u_i, *l_i;
+    SPUMA_TRY(cells_in(m, diag, R_DIAG, &d_i));
+    SPUMA_TRY(cells_in(m, x, R_X, &x_i));
+    SPUMA_TRY(pair_in(m, upper, lower, &u_i, &l_i));
+    if (!m->d_cell_t) SPUMA_TRY(dalloc(&m->d_cell_t, m->N));
+    launch_amul_asym(s, mesh_args(m), d_i, u_i, l_i, x_i, m->d_cell_t, transpose != 0);
+    m->stats.kernel_launches += 1;
+    SPUMA_TRY(cells_out(m, y, m->d_cell_t));
+    SPUMA_CUDA(cudaStreamSynchronize(s));
+    SPUMA_CUDA(cudaGetLastError());
+    return SPUMA_OK;
+}
+
+spuma_status spuma_ldu_to_csr(spuma_mesh m, spuma_label* row_ptr, spuma_label* col, spuma_label* map)
+{
+    if (!m || !row_ptr || !col || !map) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (m->renumber) return set_error(SPUMA_ERR_STATE, "LDU->CSR needs a handle built with renumber = 0");
+    const int N = m->N, F = m->F, nnz = N + 2 * F;
+    // per row: lower-triangle entries (faces with neighbour c: column owner, ascending because
+    // losort is owner-ascending), the diagonal, then owner faces (column neighbour, ascending)
+    std::vector<int> rp(N + 1), cl(nnz), mp(nnz);
+    rp[0] = 0;
+    int k = 0;
+    for (int c = 0; c < N; ++c) {
+        for (int j = m->h_losortStart[c]; j < m->h_losortStart[c + 1]; ++j) {
+            const int f = m->h_losort[j];
+            cl[k] = m->h_owner[f];
+            mp[k++] = N + F + f;
+        }
+        cl[k] = c;
+        mp[k++] = c;
+        for (int f = m->h_ownerStart[c]; f < m->h_ownerStart[c + 1]; ++f) {
+            cl[k] = m->h_neighbour[f];
+            mp[k++] = N + f;
+        }
+        rp[c + 1] = k;
+    }
+    auto put = [&](spuma_label* dst, const std::vector<int>& v) -> spuma_status {
+        if (is_device_ptr(dst)) SPUMA_CUDA(cudaMemcpy(dst, v.data(), sizeof(int) * v.size(), cudaMemcpyHostToDevice));
+        else std::memcpy(dst, v.data(), sizeof(int) * v.size());
+        return SPUMA_OK;
+    };
+    SPUMA_TRY(put(row_ptr, rp));
+    SPUMA_TRY(put(col, cl));
+    SPUMA_TRY(put(map, mp));
+    SPUMA_TRY(pc_ensure(m));
+    if (!m->pc->csr_map) SPUMA_TRY(upload(&m->pc->csr_map, mp, m->stream));
+    m->pc->nnz = nnz;
+    SPUMA_CUDA(cudaStreamSynchronize(m->stream));
+    return SPUMA_OK;
+}
+
+spuma_status spuma_csr_values(spuma_mesh m, const spuma_scalar* diag, const spuma_scalar* upper,
+                              const spuma_scalar* lower, spuma_scalar* values)
+{
+    if (!m || !diag || !values || (m->F > 0 && (!upper || !lower)))
+        return set_error(SPUMA_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (!m->pc || !m->pc->csr_map) return set_error(SPUMA_ERR_STATE, "call spuma_ldu_to_csr first");
+    if (!is_device_ptr(diag) || !is_device_ptr(upper) || !is_device_ptr(lower) || !is_device_ptr(values))
+        return set_error(SPUMA_ERR_INVALID_ARGUMENT, "spuma_csr_values takes device arrays");
+    launch_csr_values(m->stream, m->pc->nnz, m->N, m->F, m->pc->csr_map, diag, upper, lower, values);
+    m->stats.kernel_launches += 1;
+    SPUMA_CUDA(cudaStreamSynchronize(m->stream));
+    SPUMA_CUDA(cudaGetLastError());
     return SPUMA_OK;
 }
 

@@ -98,6 +98,7 @@ struct Patch {
 }  // namespace spuma
 
 struct GamgState;  // api.cu
+struct PcState;    // api.cu: preconditioned solvers (§8(f3)/(f4))
 
 struct spuma_mesh_s {
     int N = 0, F = 0, Fb = 0, n_iface = 0;
@@ -177,6 +178,7 @@ struct spuma_mesh_s {
 
     spuma_stats stats{};
     GamgState* gamg = nullptr;  // GAMG hierarchy + captured cycle, built on first spuma_gamg_solve
+    PcState* pc = nullptr;      // level schedules + buffers of the DIC/DILU/PBiCG solvers
 };
 
 // error plumbing (api.cu)
@@ -273,6 +275,32 @@ void launch_finalize(cudaStream_t s, int stage, const double* gathered, int n_ra
 void launch_scal_init(cudaStream_t s, const Workspace& w, const spuma_solver_controls& c, int n_ranks);
 void launch_pcg_single(cudaStream_t s, const MeshArgs& a, const Workspace& w);  // whole solve, 1 CTA
 int occupancy_grid(int N, int* grid_faces, int F);
+// preconditioned solvers (precond.cu)
+int pc_grid(int n);
+void launch_recip(cudaStream_t s, int N, const double* in, double* out);  // out = 1 / in
+void launch_ilu_factor(cudaStream_t s, const MeshArgs& a, const int* order, const double* diag, const double* upper,
+                       const double* lower, double* raw, double* rD, int* flag, unsigned* counter);
+void launch_ilu_precondition(cudaStream_t s, const MeshArgs& a, const int* order_f, const int* order_b,
+                             const double* rD, const double* upper, const double* lower, const double* r, double* w,
+                             double* t1, double* t2, int* flag, unsigned* counter, int k, bool transpose,
+                             const DevScal* scal);
+void launch_pc_dot(cudaStream_t s, int N, const double* w, const double* r, double* part, DevScal* scal);
+void launch_pc_direction(cudaStream_t s, int N, const double* wA, double* pA, const double* wT, double* pT,
+                         const DevScal* scal);
+void launch_bicg_amul_tmul(cudaStream_t s, const MeshArgs& a, const double* diag, const double* upper,
+                           const double* lower, const double* pA, const double* pT, double* wA, double* wT,
+                           double* part, DevScal* scal);
+void launch_bicg_update(cudaStream_t s, int N, double* psi, const double* pA, double* rA, const double* wA, double* rT,
+                        const double* wT, double* part, DevScal* scal);
+void launch_bicg_setup(cudaStream_t s, const MeshArgs& a, const double* diag, const double* upper,
+                       const double* lower, const double* source, const double* psi, double* wA, double* wT,
+                       double* rA, double* rT, double* sumA, double* part, DevScal* scal);
+void launch_csr_values(cudaStream_t s, int nnz, int N, int F, const int* map, const double* diag,
+                       const double* upper, const double* lower, double* vals);
+void launch_gather_pair(cudaStream_t s, int F, const int* map, const signed char* flip, const double* u,
+                        const double* l, double* uo, double* lo);
+void launch_amul_asym(cudaStream_t s, const MeshArgs& a, const double* diag, const double* upper,
+                      const double* lower, const double* x, double* y, bool transpose);
 // GAMG (gamg.cu).  P = the handle's DevPtrs (level 0's matrix, source, psi).
 int gamg_grid(int n);
 void launch_gamg_agg(cudaStream_t s, const GLevel& fine, const GLevel& coarse, const DevPtrs* P);

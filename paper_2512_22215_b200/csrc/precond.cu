@@ -1,0 +1,452 @@
+// precond.cu -- sm_100a kernels of the preconditioned solvers around the path
+// (readings Q31-Q35): DIC / DILU factor and sweeps, aDILU passes,
+// the PCG/PBiCG vector kernels, asymmetric Amul/Tmul, LDU -> CSR value gather.
+//
+// The DIC/DILU recurrences are sequential in face order.  They run as ONE persistent
+// "sync-free" kernel per sweep: threads claim rows in level-schedule order (host-built,
+// rows sorted by dependency depth) from an atomic counter, spin (acquire loads) on the
+// ready flags of the rows they depend on, then publish their value (release store).  Each
+// row sums its faces in the oracle's order, so the result is bitwise that of the
+// sequential loop for ANY cell numbering; the critical path is the dependency depth.  A
+// row only waits on rows claimed earlier, whose threads are already running: no deadlock.
+#include "device.cuh"
+#include "internal.h"
+
+namespace spuma {
+namespace {
+
+__device__ __forceinline__ int ld_acquire(const int* p)
+{
+    int v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v)
+{
+    asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void wait_ready(const int* flag, int j)
+{
+    while (ld_acquire(flag + j) == 0) {
+    }
+}
+
+// Factor (Q31): raw[c] = diag[c] - sum over faces with neighbour c (face order) of
+// upper*lower/raw[owner]; the reciprocal is taken by k_ilu_recip afterwards.
+__global__ void __launch_bounds__(kThreads) k_ilu_factor(MeshArgs a, const int* __restrict__ order,
+                                                         const double* __restrict__ diag,
+                                                         const double* __restrict__ upper,
+                                                         const double* __restrict__ lower, double* raw, int* flag,
+                                                         unsigned* counter)
+{
+    for (;;) {
+        const unsigned i = atomicAdd(counter, 1u);
+        if (i >= (unsigned)a.N) break;
+        const int c = order[i];
+        double t = diag[c];
+        for (int k = a.losortStart[c]; k < a.losortStart[c + 1]; ++k) {
+            const int j = a.ownerLo[k], f = a.losort[k];
+            wait_ready(flag, j);
+            t = t - upper[f] * lower[f] / __ldcg(raw + j);
+        }
+        __stcg(raw + c, t);
+        st_release(flag + c, 1);
+    }
+}
+
+__global__ void k_ilu_recip(int N, const double* __restrict__ raw, double* __restrict__ rD)
+{
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < N; c += gridDim.x * blockDim.x) rD[c] = 1.0 / raw[c];
+}
+
+// Forward sweep: w[c] = rD[c] r[c], then w[c] -= rD[c]*lo[f]*w[owner] over the faces with
+// neighbour c in face order.
+__global__ void __launch_bounds__(kThreads) k_ilu_fwd(MeshArgs a, const int* __restrict__ order,
+                                                      const double* __restrict__ rD, const double* __restrict__ lo,
+                                                      const double* __restrict__ r, double* w, int* flag,
+                                                      unsigned* counter, const DevScal* scal)
+{
+    if (scal && scal->done) return;
+    for (;;) {
+        const unsigned i = atomicAdd(counter, 1u);
+        if (i >= (unsigned)a.N) break;
+        const int c = order[i];
+        const double rd = rD[c];
+        double t = rd * r[c];
+        for (int k = a.losortStart[c]; k < a.losortStart[c + 1]; ++k) {
+            const int j = a.ownerLo[k];
+            wait_ready(flag, j);
+            t = t - rd * lo[a.losort[k]] * __ldcg(w + j);
+        }
+        __stcg(w + c, t);
+        st_release(flag + c, 1);
+    }
+}
+
+// Backward sweep (rows in reverse dependency order): w[c] -= rD[c]*up[f]*w[neighbour] over the
+// faces with owner c in DESCENDING face order.  w holds the forward result on entry.
+__global__ void __launch_bounds__(kThreads) k_ilu_bwd(MeshArgs a, const int* __restrict__ order,
+                                                      const double* __restrict__ rD, const double* __restrict__ up,
+                                                      double* w, int* flag, unsigned* counter, const DevScal* scal)
+{
+    if (scal && scal->done) return;
+    for (;;) {
+        const unsigned i = atomicAdd(counter, 1u);
+        if (i >= (unsigned)a.N) break;
+        const int c = order[i];
+        const double rd = rD[c];
+        double t = __ldcg(w + c);
+        for (int f = a.ownerStart[c + 1] - 1; f >= a.ownerStart[c]; --f) {
+            const int j = a.neighbour[f];
+            wait_ready(flag, j);
+            t = t - rd * up[f] * __ldcg(w + j);
+        }
+        __stcg(w + c, t);
+        st_release(flag + c, 1);
+    }
+}
+
+// aDILU (Q33) forward pass: out[c] = y0[c] - sum (rD[c]*lo[f]) * prev[owner] (face order);
+// y0 == nullptr: y0 = rD r.  Backward pass: out[c] = y0[c] - sum over owner faces in
+// descending order of (rD[c]*up[f]) * prev[neighbour].
+__global__ void __launch_bounds__(kThreads) k_adilu_pass(MeshArgs a, int backward, const double* __restrict__ rD,
+                                                         const double* __restrict__ coef,
+                                                         const double* __restrict__ r,
+                                                         const double* __restrict__ y0,
+                                                         const double* __restrict__ prev, double* __restrict__ out,
+                                                         const DevScal* scal)
+{
+    if (scal && scal->done) return;
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < a.N; c += gridDim.x * blockDim.x) {
+        const double rd = rD[c];
+        double t = y0 ? y0[c] : rd * r[c];
+        if (!backward) {
+            for (int k = a.losortStart[c]; k < a.losortStart[c + 1]; ++k)
+                t = t - rd * coef[a.losort[k]] * prev[a.ownerLo[k]];
+        } else {
+            for (int f = a.ownerStart[c + 1] - 1; f >= a.ownerStart[c]; --f) t = t - rd * coef[f] * prev[a.neighbour[f]];
+        }
+        out[c] = t;
+    }
+}
+
+// w = rD r (diagonal preconditioner; also aDILU with k = 0)
+__global__ void k_pc_diag(int N, const double* __restrict__ rD, const double* __restrict__ r, double* __restrict__ w,
+                          const DevScal* scal)
+{
+    if (scal && scal->done) return;
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < N; c += gridDim.x * blockDim.x) w[c] = rD[c] * r[c];
+}
+
+// wArA (PCG) / wArT (PBiCG) = w . r; beta = wArA / wArAold (used from the second iteration)
+__global__ void __launch_bounds__(kThreads) k_pc_dot(int N, const double* __restrict__ w, const double* __restrict__ r,
+                                                     double* part, DevScal* scal)
+{
+    if (scal->done) return;
+    double v[1] = {0.0};
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < N; c += gridDim.x * blockDim.x) v[0] += w[c] * r[c];
+    if (grid_sum<1>(v, part, &scal->ticket[5]) && threadIdx.x == 0) {
+        scal->wArA = v[0];
+        scal->beta = scal->wArA / scal->wArAold;
+    }
+}
+
+// pA = wA (+ beta pA); pT = wT (+ beta pT) when pT != nullptr
+__global__ void k_pc_direction(int N, const double* __restrict__ wA, double* __restrict__ pA,
+                               const double* __restrict__ wT, double* __restrict__ pT, const DevScal* scal)
+{
+    if (scal->done) return;
+    const bool first = scal->n == 0;
+    const double beta = scal->beta;
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < N; c += gridDim.x * blockDim.x) {
+        pA[c] = first ? wA[c] : wA[c] + beta * pA[c];
+        if (pT) pT[c] = first ? wT[c] : wT[c] + beta * pT[c];
+    }
+}
+
+// asymmetric row of A (upper on the owner side, lower on the neighbour side) and of A^T
+__device__ __forceinline__ double row_asym(const MeshArgs& a, int c, const double* __restrict__ diag,
+                                           const double* __restrict__ nbr_coef, const double* __restrict__ own_coef,
+                                           const double* __restrict__ x)
+{
+    double s = diag[c] * x[c];
+    for (int k = a.losortStart[c]; k < a.losortStart[c + 1]; ++k) s = s + nbr_coef[a.losort[k]] * x[a.ownerLo[k]];
+    for (int f = a.ownerStart[c]; f < a.ownerStart[c + 1]; ++f) s = s + own_coef[f] * x[a.neighbour[f]];
+    return s;
+}
+
+// PBiCG: wA = A pA, wT = A^T pT, wApT = wA . pT -> alpha, singularity (Q32)
+__global__ void __launch_bounds__(kThreads) k_bicg_amul_tmul(MeshArgs a, const double* __restrict__ diag,
+                                                             const double* __restrict__ upper,
+                                                             const double* __restrict__ lower,
+                                                             const double* __restrict__ pA,
+                                                             const double* __restrict__ pT, double* __restrict__ wA,
+                                                             double* __restrict__ wT, double* part, DevScal* scal)
+{
+    if (scal->done) return;
+    double v[1] = {0.0};
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < a.N; c += gridDim.x * blockDim.x) {
+        const double ya = row_asym(a, c, diag, lower, upper, pA);
+        const double yt = row_asym(a, c, diag, upper, lower, pT);
+        wA[c] = ya;
+        wT[c] = yt;
+        v[0] += ya * pT[c];
+    }
+    if (grid_sum<1>(v, part, &scal->ticket[6]) && threadIdx.x == 0) {
+        scal->wApA = v[0];
+        if (fabs(scal->wApA) / scal->normFactor < 1e-300) {
+            scal->singular = 1;
+            scal->done = 1;
+        } else {
+            scal->alpha = scal->wArA / scal->wApA;
+        }
+    }
+}
+
+// PBiCG update: psi += alpha pA, rA -= alpha wA, rT -= alpha wT; final residual, n++, done
+__global__ void __launch_bounds__(kThreads) k_bicg_update(int N, double* __restrict__ psi,
+                                                          const double* __restrict__ pA,
+                                                          double* __restrict__ rA, const double* __restrict__ wA,
+                                                          double* __restrict__ rT, const double* __restrict__ wT,
+                                                          double* part, DevScal* scal)
+{
+    if (scal->done) return;
+    const double alpha = scal->alpha;
+    double v[1] = {0.0};
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < N; c += gridDim.x * blockDim.x) {
+        psi[c] = psi[c] + alpha * pA[c];
+        const double r = rA[c] - alpha * wA[c];
+        rA[c] = r;
+        if (rT) rT[c] = rT[c] - alpha * wT[c];
+        v[0] += fabs(r);
+    }
+    if (grid_sum<1>(v, part, &scal->ticket[7]) && threadIdx.x == 0) {
+        scal->fin = v[0] / scal->normFactor;
+        scal->n = scal->n + 1;
+        const bool c = conv(scal->fin, scal->init, scal->tol, scal->rel_tol);
+        scal->converged = c;
+        if (!((scal->n < scal->max_iter && !c) || scal->n < scal->min_iter)) scal->done = 1;
+        scal->wArAold = scal->wArA;
+    }
+}
+
+// PBiCG setup: wA = A psi, wT = A^T psi, rA = b - wA, rT = b - wT, sumA = row sums (Q35),
+// partial sum of psi -> finalize(1) gives gAverage(psi)
+__global__ void __launch_bounds__(kThreads) k_bicg_setup(MeshArgs a, const double* __restrict__ diag,
+                                                         const double* __restrict__ upper,
+                                                         const double* __restrict__ lower,
+                                                         const double* __restrict__ source,
+                                                         const double* __restrict__ psi, double* __restrict__ wA,
+                                                         double* __restrict__ wT, double* __restrict__ rA,
+                                                         double* __restrict__ rT, double* __restrict__ sumA,
+                                                         double* part, DevScal* scal)
+{
+    double v[2] = {0.0, 0.0};
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < a.N; c += gridDim.x * blockDim.x) {
+        const double ya = row_asym(a, c, diag, lower, upper, psi);
+        const double yt = row_asym(a, c, diag, upper, lower, psi);
+        double s = diag[c];
+        for (int k = a.losortStart[c]; k < a.losortStart[c + 1]; ++k) s = s + lower[a.losort[k]];
+        for (int f = a.ownerStart[c]; f < a.ownerStart[c + 1]; ++f) s = s + upper[f];
+        wA[c] = ya;
+        wT[c] = yt;
+        rA[c] = source[c] - ya;
+        rT[c] = source[c] - yt;
+        sumA[c] = s;
+        v[0] += psi[c];
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) v[1] = (double)a.N;
+    if (grid_sum<2>(v, part, &scal->ticket[0]) && threadIdx.x == 0) scal->xbar = v[0] / v[1];
+}
+
+// normFactor and initial residual from wA, sumA, rA (Q1) -> the loop decision
+__global__ void __launch_bounds__(kThreads) k_pc_setup2(int N, const double* __restrict__ wA,
+                                                        const double* __restrict__ sumA,
+                                                        const double* __restrict__ source,
+                                                        const double* __restrict__ rA, double* part, DevScal* s)
+{
+    const double xbar = s->xbar;
+    double v[2] = {0.0, 0.0};
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < N; c += gridDim.x * blockDim.x) {
+        const double xref = sumA[c] * xbar;
+        v[0] += fabs(wA[c] - xref) + fabs(source[c] - xref);
+        v[1] += fabs(rA[c]);
+    }
+    if (grid_sum<2>(v, part, &s->ticket[1]) && threadIdx.x == 0) {
+        s->normFactor = v[0] + 1e-20;
+        s->init = v[1] / s->normFactor;
+        s->fin = s->init;
+        s->wArA = 1e300;
+        s->wArAold = 1e300;
+        s->n = 0;
+        s->singular = 0;
+        s->converged = conv(s->fin, s->init, s->tol, s->rel_tol);
+        s->done = !(s->min_iter > 0 || !s->converged);
+    }
+}
+
+// CSR values: vals[k] = [diag | upper | lower][map[k]]
+__global__ void k_csr_values(int nnz, int N, int F, const int* __restrict__ map, const double* __restrict__ diag,
+                             const double* __restrict__ upper, const double* __restrict__ lower,
+                             double* __restrict__ vals)
+{
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += gridDim.x * blockDim.x) {
+        const int m = map[k];
+        vals[k] = m < N ? diag[m] : (m < N + F ? upper[m - N] : lower[m - N - F]);
+    }
+}
+
+// internal (upper, lower) from the caller's through the face map; faces whose orientation RCM
+// reversed swap their two coefficients
+__global__ void k_gather_pair(int F, const int* __restrict__ map, const signed char* __restrict__ flip,
+                              const double* __restrict__ u, const double* __restrict__ l, double* __restrict__ uo,
+                              double* __restrict__ lo)
+{
+    for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < F; f += gridDim.x * blockDim.x) {
+        const int g = map[f];
+        const bool sw = flip && flip[f];
+        uo[f] = sw ? l[g] : u[g];
+        lo[f] = sw ? u[g] : l[g];
+    }
+}
+
+__global__ void k_amul_asym(MeshArgs a, const double* __restrict__ diag, const double* __restrict__ upper,
+                            const double* __restrict__ lower, const double* __restrict__ x, double* __restrict__ y,
+                            int transpose)
+{
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < a.N; c += gridDim.x * blockDim.x)
+        y[c] = transpose ? row_asym(a, c, diag, upper, lower, x) : row_asym(a, c, diag, lower, upper, x);
+}
+
+int persistent_grid(const void* kernel)
+{
+    static int sms = 0;
+    int dev = 0, occ = 1;
+    if (!sms) {
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kThreads, 0);
+    return sms * (occ > 0 ? occ : 1);
+}
+
+int cell_grid(int n)
+{
+    const int g = (n + kThreads - 1) / kThreads;
+    return g < 1 ? 1 : (g > 148 * 8 ? 148 * 8 : g);
+}
+
+}  // namespace
+
+// grids of the reduction kernels are fixed per N (deterministic partial order)
+int pc_grid(int n) { return cell_grid(n); }
+
+void launch_ilu_factor(cudaStream_t s, const MeshArgs& a, const int* order, const double* diag, const double* upper,
+                       const double* lower, double* raw, double* rD, int* flag, unsigned* counter)
+{
+    cudaMemsetAsync(flag, 0, sizeof(int) * (a.N + 1), s);
+    cudaMemsetAsync(counter, 0, sizeof(unsigned), s);
+    k_ilu_factor<<<persistent_grid((const void*)k_ilu_factor), kThreads, 0, s>>>(a, order, diag, upper, lower, raw,
+                                                                                 flag, counter);
+    k_ilu_recip<<<cell_grid(a.N), kThreads, 0, s>>>(a.N, raw, rD);
+}
+
+// w = M^-1 r (transpose: M^-T r).  k < 0: exact sweeps; k >= 0: aDILU with k passes per sweep.
+void launch_ilu_precondition(cudaStream_t s, const MeshArgs& a, const int* order_f, const int* order_b,
+                             const double* rD, const double* upper, const double* lower, const double* r, double* w,
+                             double* t1, double* t2, int* flag, unsigned* counter, int k, bool transpose,
+                             const DevScal* scal)
+{
+    const double* lo = transpose ? upper : lower;
+    const double* up = transpose ? lower : upper;
+    if (k < 0) {
+        cudaMemsetAsync(flag, 0, sizeof(int) * (a.N + 1), s);
+        cudaMemsetAsync(counter, 0, sizeof(unsigned), s);
+        k_ilu_fwd<<<persistent_grid((const void*)k_ilu_fwd), kThreads, 0, s>>>(a, order_f, rD, lo, r, w, flag, counter,
+                                                                             scal);
+        cudaMemsetAsync(flag, 0, sizeof(int) * (a.N + 1), s);
+        cudaMemsetAsync(counter, 0, sizeof(unsigned), s);
+        k_ilu_bwd<<<persistent_grid((const void*)k_ilu_bwd), kThreads, 0, s>>>(a, order_b, rD, up, w, flag, counter,
+                                                                             scal);
+        return;
+    }
+    if (k == 0) {
+        k_pc_diag<<<cell_grid(a.N), kThreads, 0, s>>>(a.N, rD, r, w, scal);
+        return;
+    }
+    // forward passes: prev_0 = y_0 = rD r in t1; out_i alternates t2, t1, ... (y_0 stays implicit via r)
+    k_pc_diag<<<cell_grid(a.N), kThreads, 0, s>>>(a.N, rD, r, t1, scal);
+    double* prev = t1;
+    for (int it = 0; it < k; ++it) {
+        double* out = prev == t1 ? t2 : t1;
+        k_adilu_pass<<<cell_grid(a.N), kThreads, 0, s>>>(a, 0, rD, lo, r, nullptr, prev, out, scal);
+        prev = out;
+    }
+    // backward passes from w_0 = y (kept in Y): out_i alternates Z / w so that out_k = w
+    double* Y = prev;
+    double* Z = Y == t1 ? t2 : t1;
+    const double* bprev = Y;
+    for (int it = 0; it < k; ++it) {
+        double* out = ((k - 1 - it) & 1) ? Z : w;
+        k_adilu_pass<<<cell_grid(a.N), kThreads, 0, s>>>(a, 1, rD, up, r, Y, bprev, out, scal);
+        bprev = out;
+    }
+}
+
+void launch_recip(cudaStream_t s, int N, const double* in, double* out)
+{
+    k_ilu_recip<<<cell_grid(N), kThreads, 0, s>>>(N, in, out);
+}
+
+void launch_pc_dot(cudaStream_t s, int N, const double* w, const double* r, double* part, DevScal* scal)
+{
+    k_pc_dot<<<cell_grid(N), kThreads, 0, s>>>(N, w, r, part, scal);
+}
+
+void launch_pc_direction(cudaStream_t s, int N, const double* wA, double* pA, const double* wT, double* pT,
+                         const DevScal* scal)
+{
+    k_pc_direction<<<cell_grid(N), kThreads, 0, s>>>(N, wA, pA, wT, pT, scal);
+}
+
+void launch_bicg_amul_tmul(cudaStream_t s, const MeshArgs& a, const double* diag, const double* upper,
+                           const double* lower, const double* pA, const double* pT, double* wA, double* wT,
+                           double* part, DevScal* scal)
+{
+    k_bicg_amul_tmul<<<cell_grid(a.N), kThreads, 0, s>>>(a, diag, upper, lower, pA, pT, wA, wT, part, scal);
+}
+
+void launch_bicg_update(cudaStream_t s, int N, double* psi, const double* pA, double* rA, const double* wA, double* rT,
+                        const double* wT, double* part, DevScal* scal)
+{
+    k_bicg_update<<<cell_grid(N), kThreads, 0, s>>>(N, psi, pA, rA, wA, rT, wT, part, scal);
+}
+
+void launch_bicg_setup(cudaStream_t s, const MeshArgs& a, const double* diag, const double* upper,
+                       const double* lower, const double* source, const double* psi, double* wA, double* wT,
+                       double* rA, double* rT, double* sumA, double* part, DevScal* scal)
+{
+    k_bicg_setup<<<cell_grid(a.N), kThreads, 0, s>>>(a, diag, upper, lower, source, psi, wA, wT, rA, rT, sumA, part,
+                                                    scal);
+    k_pc_setup2<<<cell_grid(a.N), kThreads, 0, s>>>(a.N, wA, sumA, source, rA, part, scal);
+}
+
+void launch_gather_pair(cudaStream_t s, int F, const int* map, const signed char* flip, const double* u,
+                        const double* l, double* uo, double* lo)
+{
+    k_gather_pair<<<cell_grid(F), kThreads, 0, s>>>(F, map, flip, u, l, uo, lo);
+}
+
+void launch_amul_asym(cudaStream_t s, const MeshArgs& a, const double* diag, const double* upper,
+                      const double* lower, const double* x, double* y, bool transpose)
+{
+    k_amul_asym<<<cell_grid(a.N), kThreads, 0, s>>>(a, diag, upper, lower, x, y, transpose ? 1 : 0);
+}
+
+void launch_csr_values(cudaStream_t s, int nnz, int N, int F, const int* map, const double* diag,
+                       const double* upper, const double* lower, double* vals)
+{
+    k_csr_values<<<cell_grid(nnz), kThreads, 0, s>>>(nnz, N, F, map, diag, upper, lower, vals);
+}
+
+}  // namespace spuma

@@ -85,6 +85,14 @@ def gamg_params(**kw) -> GamgParams:
     return p
 
 
+class Preconditioner(ctypes.Structure):
+    """spuma_preconditioner (readings Q31-Q33)."""
+    _fields_ = [("kind", _ci), ("n_sweeps", _ci)]
+
+
+PC_DIAGONAL, PC_DIC, PC_DILU, PC_ADILU = 0, 1, 2, 3
+
+
 EXCHANGE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_int),
                                ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
                                ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double))
@@ -147,6 +155,15 @@ def lib():
             L.spuma_gamg_solve.argtypes = [_vp] * 6 + [ctypes.POINTER(SolverControls), ctypes.POINTER(GamgParams),
                                                        ctypes.POINTER(SolverPerf)]
             L.spuma_gamg_get_hierarchy.argtypes = [_vp, ctypes.POINTER(GamgParams), _ci, _vp, _vp, _vp, _ci, _vp]
+        if hasattr(L, "spuma_pbicg_solve"):
+            L.spuma_pcg_solve_pc.argtypes = [_vp] * 5 + [ctypes.POINTER(SolverControls), ctypes.POINTER(Preconditioner),
+                                                         ctypes.POINTER(SolverPerf)]
+            L.spuma_pbicg_solve.argtypes = [_vp] * 6 + [ctypes.POINTER(SolverControls), ctypes.POINTER(Preconditioner),
+                                                        ctypes.POINTER(SolverPerf)]
+            L.spuma_precondition.argtypes = [_vp] * 4 + [ctypes.POINTER(Preconditioner), _vp, _vp, _ci]
+            L.spuma_amul_asym.argtypes = [_vp] * 6 + [_ci]
+            L.spuma_ldu_to_csr.argtypes = [_vp] * 4
+            L.spuma_csr_values.argtypes = [_vp] * 5
         L.spuma_last_error.restype = ctypes.c_char_p
         L.spuma_abi_version.restype = _ci
         for name in ("spuma_mesh_create", "spuma_assemble_laplacian", "spuma_pcg_solve", "spuma_amul",
@@ -331,6 +348,59 @@ class Mesh:
                                                       ftc.ctypes.data))
                 out["ftc"].append(ftc)
         return out
+
+    # ---------------------------------------------------------------- §8(f3)/(f4)
+    def pcg_solve_pc(self, diag, upper, source, psi, tolerance=1e-6, rel_tol=0.0, max_iter=5000, min_iter=0,
+                     kind=PC_DIAGONAL, n_sweeps=2) -> dict:
+        """spuma_pcg_solve_pc: PCG with a diagonal / DIC / DILU / aDILU preconditioner."""
+        ctl, perf, pc = SolverControls(tolerance, rel_tol, max_iter, min_iter), SolverPerf(), Preconditioner(kind, n_sweeps)
+        d, kd = _ptr(diag, np.float64)
+        u, ku = _ptr(upper, np.float64)
+        s, ks = _ptr(source, np.float64)
+        p, kp = _ptr(psi, np.float64)
+        _check(lib().spuma_pcg_solve_pc(self._h, d, u, s, p, ctypes.byref(ctl), ctypes.byref(pc), ctypes.byref(perf)))
+        return perf.as_dict()
+
+    def pbicg_solve(self, diag, upper, lower, source, psi, tolerance=1e-6, rel_tol=0.0, max_iter=1000, min_iter=0,
+                    kind=PC_ADILU, n_sweeps=2) -> dict:
+        """spuma_pbicg_solve: PBiCG on an asymmetric LDU matrix."""
+        ctl, perf, pc = SolverControls(tolerance, rel_tol, max_iter, min_iter), SolverPerf(), Preconditioner(kind, n_sweeps)
+        d, kd = _ptr(diag, np.float64)
+        u, ku = _ptr(upper, np.float64)
+        lo, kl = _ptr(lower, np.float64)
+        s, ks = _ptr(source, np.float64)
+        p, kp = _ptr(psi, np.float64)
+        _check(lib().spuma_pbicg_solve(self._h, d, u, lo, s, p, ctypes.byref(ctl), ctypes.byref(pc),
+                                       ctypes.byref(perf)))
+        return perf.as_dict()
+
+    def precondition(self, diag, upper, lower, r, w, kind, n_sweeps=2, transpose=False):
+        pc = Preconditioner(kind, n_sweeps)
+        d, kd = _ptr(diag, np.float64)
+        u, ku = _ptr(upper, np.float64)
+        lo, kl = _ptr(lower, np.float64)
+        rp, kr = _ptr(r, np.float64)
+        wp, kw = _ptr(w, np.float64)
+        _check(lib().spuma_precondition(self._h, d, u, lo, ctypes.byref(pc), rp, wp, int(transpose)))
+        return kw
+
+    def amul_asym(self, diag, upper, lower, x, y, transpose=False):
+        d, kd = _ptr(diag, np.float64)
+        u, ku = _ptr(upper, np.float64)
+        lo, kl = _ptr(lower, np.float64)
+        xp, kx = _ptr(x, np.float64)
+        yp, ky = _ptr(y, np.float64)
+        _check(lib().spuma_amul_asym(self._h, d, u, lo, xp, yp, int(transpose)))
+        return ky
+
+    def ldu_to_csr(self):
+        N, F = self.n_cells, self.n_faces
+        rp, col, mp = np.zeros(N + 1, np.int32), np.zeros(N + 2 * F, np.int32), np.zeros(N + 2 * F, np.int32)
+        _check(lib().spuma_ldu_to_csr(self._h, rp.ctypes.data, col.ctypes.data, mp.ctypes.data))
+        return rp, col, mp
+
+    def csr_values(self, diag, upper, lower, values):
+        _check(lib().spuma_csr_values(self._h, diag.data_ptr(), upper.data_ptr(), lower.data_ptr(), values.data_ptr()))
 
     def amul(self, diag, upper, iface_coeffs, x, y):
         """spuma_amul: y = A x."""
