@@ -697,6 +697,7 @@ struct PcState {
     int *order_f = nullptr, *order_b = nullptr, *flag = nullptr;
     unsigned* counter = nullptr;
     int depth_f = 0, depth_b = 0;
+    int width_f = 0, width_b = 0;  // widest dependency level (rows that can run concurrently)
     double *raw = nullptr, *rD = nullptr, *t1 = nullptr, *t2 = nullptr;
     double *wT = nullptr, *rT = nullptr, *pT = nullptr, *part = nullptr;
     double *u_in = nullptr, *l_in = nullptr, *u_int = nullptr, *l_int = nullptr;
@@ -733,18 +734,20 @@ spuma_status pc_ensure(spuma_mesh m)
     for (int c = N - 1; c >= 0; --c)
         for (int f = m->h_ownerStart[c]; f < m->h_ownerStart[c + 1]; ++f)
             lb[c] = std::max(lb[c], lb[m->h_neighbour[f]] + 1);
-    auto order_by = [N](const std::vector<int>& lev, int& depth) {
+    auto order_by = [N](const std::vector<int>& lev, int& depth, int& width) {
         depth = 0;
         for (int c = 0; c < N; ++c) depth = std::max(depth, lev[c] + 1);
         std::vector<int> start(depth + 1, 0), ord(N);
         for (int c = 0; c < N; ++c) start[lev[c] + 1]++;
+        width = 0;
+        for (int d = 0; d < depth; ++d) width = std::max(width, start[d + 1]);
         for (int d = 0; d < depth; ++d) start[d + 1] += start[d];
         for (int c = 0; c < N; ++c) ord[start[lev[c]]++] = c;
         return ord;
     };
     cudaStream_t s = m->stream;
-    SPUMA_TRY(upload(&P->order_f, order_by(lf, P->depth_f), s));
-    SPUMA_TRY(upload(&P->order_b, order_by(lb, P->depth_b), s));
+    SPUMA_TRY(upload(&P->order_f, order_by(lf, P->depth_f, P->width_f), s));
+    SPUMA_TRY(upload(&P->order_b, order_by(lb, P->depth_b, P->width_b), s));
     SPUMA_TRY(dalloc(&P->flag, N + 1));
     SPUMA_TRY(dalloc(&P->counter, 1));
     for (double** b : {&P->raw, &P->rD, &P->t1, &P->t2, &P->wT, &P->rT, &P->pT}) SPUMA_TRY(dalloc(b, N));
@@ -810,7 +813,7 @@ void pc_setup(spuma_mesh m, const spuma_preconditioner& pc, const double* d, con
         return;
     }
     launch_ilu_factor(m->stream, a, P->order_f, d, u, pc.kind == SPUMA_PC_DIC ? u : l, P->raw, P->rD, P->flag,
-                      P->counter);
+                      P->counter, P->width_f);
 }
 
 void pc_apply(spuma_mesh m, const spuma_preconditioner& pc, const double* u, const double* l, const double* r,
@@ -820,7 +823,7 @@ void pc_apply(spuma_mesh m, const spuma_preconditioner& pc, const double* u, con
     const int k = pc.kind == SPUMA_PC_DIAGONAL ? 0 : (pc.kind == SPUMA_PC_ADILU ? pc.n_sweeps : -1);
     launch_ilu_precondition(m->stream, mesh_args(m), P->order_f, P->order_b, P->rD, u,
                             pc.kind == SPUMA_PC_DIC ? u : l, r, w, P->t1, P->t2, P->flag, P->counter, k, transpose,
-                            scal);
+                            scal, P->width_f, P->width_b);
 }
 
 uint64_t pc_launches(const spuma_preconditioner& pc)

@@ -279,11 +279,11 @@ int occupancy_grid(int N, int* grid_faces, int F);
 int pc_grid(int n);
 void launch_recip(cudaStream_t s, int N, const double* in, double* out);  // out = 1 / in
 void launch_ilu_factor(cudaStream_t s, const MeshArgs& a, const int* order, const double* diag, const double* upper,
-                       const double* lower, double* raw, double* rD, int* flag, unsigned* counter);
+                       const double* lower, double* raw, double* rD, int* flag, unsigned* counter, int width);
 void launch_ilu_precondition(cudaStream_t s, const MeshArgs& a, const int* order_f, const int* order_b,
                              const double* rD, const double* upper, const double* lower, const double* r, double* w,
                              double* t1, double* t2, int* flag, unsigned* counter, int k, bool transpose,
-                             const DevScal* scal);
+                             const DevScal* scal, int width_f = 1 << 30, int width_b = 1 << 30);
 void launch_pc_dot(cudaStream_t s, int N, const double* w, const double* r, double* part, DevScal* scal);
 void launch_pc_direction(cudaStream_t s, int N, const double* wA, double* pA, const double* wT, double* pT,
                          const DevScal* scal);

@@ -27,8 +27,36 @@ __device__ __forceinline__ void st_release(int* p, int v)
 }
 __device__ __forceinline__ void wait_ready(const int* flag, int j)
 {
-    while (ld_acquire(flag + j) == 0) {
+    if (ld_acquire(flag + j)) return;
+    unsigned ns = 32;
+    while (!ld_acquire(flag + j)) {  // back off: keep the L2 free for the rows that can progress
+        __nanosleep(ns);
+        ns = ns < 512 ? 2 * ns : 512;
     }
+}
+
+// wait until the flags of all n (<= kDep) dependencies are set: all polls in flight at once
+constexpr int kDep = 8;
+__device__ __forceinline__ void wait_all(const int* flag, const int* js, int n)
+{
+    unsigned ns = 32;
+    for (;;) {
+        bool ok = true;
+#pragma unroll
+        for (int d = 0; d < kDep; ++d)
+            if (d < n && !ld_acquire(flag + js[d])) ok = false;
+        if (ok) return;
+        __nanosleep(ns);
+        ns = ns < 512 ? 2 * ns : 512;
+    }
+}
+
+// a warp claims 32 consecutive rows of the schedule with one atomic
+__device__ __forceinline__ unsigned claim_rows(unsigned* counter)
+{
+    unsigned base = 0;
+    if ((threadIdx.x & 31) == 0) base = atomicAdd(counter, 32u);
+    return __shfl_sync(0xffffffffu, base, 0) + (threadIdx.x & 31);
 }
 
 // Factor (Q31): raw[c] = diag[c] - sum over faces with neighbour c (face order) of
@@ -40,11 +68,29 @@ __global__ void __launch_bounds__(kThreads) k_ilu_factor(MeshArgs a, const int* 
                                                          unsigned* counter)
 {
     for (;;) {
-        const unsigned i = atomicAdd(counter, 1u);
-        if (i >= (unsigned)a.N) break;
+        const unsigned i = claim_rows(counter);
+        if (i - (threadIdx.x & 31) >= (unsigned)a.N) break;  // warp-uniform exit
+        if (i >= (unsigned)a.N) continue;
         const int c = order[i];
+        const int k0 = a.losortStart[c], nd = a.losortStart[c + 1] - k0;
+        int js[kDep];
+        double cf[kDep], v[kDep];
+#pragma unroll
+        for (int d = 0; d < kDep; ++d)
+            if (d < nd) {
+                const int f = a.losort[k0 + d];
+                js[d] = a.ownerLo[k0 + d];
+                cf[d] = upper[f] * lower[f];
+            }
+        wait_all(flag, js, nd < kDep ? nd : kDep);
+#pragma unroll
+        for (int d = 0; d < kDep; ++d)
+            if (d < nd) v[d] = __ldcg(raw + js[d]);
         double t = diag[c];
-        for (int k = a.losortStart[c]; k < a.losortStart[c + 1]; ++k) {
+#pragma unroll
+        for (int d = 0; d < kDep; ++d)
+            if (d < nd) t = t - cf[d] / v[d];
+        for (int k = k0 + kDep; k < k0 + nd; ++k) {  // rows with more than kDep lower faces
             const int j = a.ownerLo[k], f = a.losort[k];
             wait_ready(flag, j);
             t = t - upper[f] * lower[f] / __ldcg(raw + j);
@@ -68,12 +114,29 @@ __global__ void __launch_bounds__(kThreads) k_ilu_fwd(MeshArgs a, const int* __r
 {
     if (scal && scal->done) return;
     for (;;) {
-        const unsigned i = atomicAdd(counter, 1u);
-        if (i >= (unsigned)a.N) break;
+        const unsigned i = claim_rows(counter);
+        if (i - (threadIdx.x & 31) >= (unsigned)a.N) break;
+        if (i >= (unsigned)a.N) continue;
         const int c = order[i];
         const double rd = rD[c];
+        const int k0 = a.losortStart[c], nd = a.losortStart[c + 1] - k0;
+        int js[kDep];
+        double cf[kDep], v[kDep];
+#pragma unroll
+        for (int d = 0; d < kDep; ++d)
+            if (d < nd) {
+                js[d] = a.ownerLo[k0 + d];
+                cf[d] = rd * lo[a.losort[k0 + d]];
+            }
         double t = rd * r[c];
-        for (int k = a.losortStart[c]; k < a.losortStart[c + 1]; ++k) {
+        wait_all(flag, js, nd < kDep ? nd : kDep);
+#pragma unroll
+        for (int d = 0; d < kDep; ++d)
+            if (d < nd) v[d] = __ldcg(w + js[d]);
+#pragma unroll
+        for (int d = 0; d < kDep; ++d)
+            if (d < nd) t = t - cf[d] * v[d];
+        for (int k = k0 + kDep; k < k0 + nd; ++k) {
             const int j = a.ownerLo[k];
             wait_ready(flag, j);
             t = t - rd * lo[a.losort[k]] * __ldcg(w + j);
@@ -91,12 +154,29 @@ __global__ void __launch_bounds__(kThreads) k_ilu_bwd(MeshArgs a, const int* __r
 {
     if (scal && scal->done) return;
     for (;;) {
-        const unsigned i = atomicAdd(counter, 1u);
-        if (i >= (unsigned)a.N) break;
+        const unsigned i = claim_rows(counter);
+        if (i - (threadIdx.x & 31) >= (unsigned)a.N) break;
+        if (i >= (unsigned)a.N) continue;
         const int c = order[i];
         const double rd = rD[c];
+        const int f1 = a.ownerStart[c + 1] - 1, nd = f1 + 1 - a.ownerStart[c];
+        int js[kDep];
+        double cf[kDep], v[kDep];
+#pragma unroll
+        for (int d = 0; d < kDep; ++d)
+            if (d < nd) {
+                js[d] = a.neighbour[f1 - d];
+                cf[d] = rd * up[f1 - d];
+            }
         double t = __ldcg(w + c);
-        for (int f = a.ownerStart[c + 1] - 1; f >= a.ownerStart[c]; --f) {
+        wait_all(flag, js, nd < kDep ? nd : kDep);
+#pragma unroll
+        for (int d = 0; d < kDep; ++d)
+            if (d < nd) v[d] = __ldcg(w + js[d]);
+#pragma unroll
+        for (int d = 0; d < kDep; ++d)
+            if (d < nd) t = t - cf[d] * v[d];
+        for (int f = f1 - kDep; f >= a.ownerStart[c]; --f) {
             const int j = a.neighbour[f];
             wait_ready(flag, j);
             t = t - rd * up[f] * __ldcg(w + j);
@@ -318,7 +398,7 @@ __global__ void k_amul_asym(MeshArgs a, const double* __restrict__ diag, const d
         y[c] = transpose ? row_asym(a, c, diag, upper, lower, x) : row_asym(a, c, diag, lower, upper, x);
 }
 
-int persistent_grid(const void* kernel)
+int persistent_grid(const void* kernel, int cap_threads = 1 << 30)
 {
     static int sms = 0;
     int dev = 0, occ = 1;
@@ -327,7 +407,9 @@ int persistent_grid(const void* kernel)
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     }
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kThreads, 0);
-    return sms * (occ > 0 ? occ : 1);
+    const int full = sms * (occ > 0 ? occ : 1);
+    const int want = (cap_threads + kThreads - 1) / kThreads;
+    return want < 1 ? 1 : (want < full ? want : full);
 }
 
 int cell_grid(int n)
@@ -342,12 +424,12 @@ int cell_grid(int n)
 int pc_grid(int n) { return cell_grid(n); }
 
 void launch_ilu_factor(cudaStream_t s, const MeshArgs& a, const int* order, const double* diag, const double* upper,
-                       const double* lower, double* raw, double* rD, int* flag, unsigned* counter)
+                       const double* lower, double* raw, double* rD, int* flag, unsigned* counter, int width)
 {
     cudaMemsetAsync(flag, 0, sizeof(int) * (a.N + 1), s);
     cudaMemsetAsync(counter, 0, sizeof(unsigned), s);
-    k_ilu_factor<<<persistent_grid((const void*)k_ilu_factor), kThreads, 0, s>>>(a, order, diag, upper, lower, raw,
-                                                                                 flag, counter);
+    k_ilu_factor<<<persistent_grid((const void*)k_ilu_factor, 2 * width), kThreads, 0, s>>>(a, order, diag, upper,
+                                                                                           lower, raw, flag, counter);
     k_ilu_recip<<<cell_grid(a.N), kThreads, 0, s>>>(a.N, raw, rD);
 }
 
@@ -355,19 +437,19 @@ void launch_ilu_factor(cudaStream_t s, const MeshArgs& a, const int* order, cons
 void launch_ilu_precondition(cudaStream_t s, const MeshArgs& a, const int* order_f, const int* order_b,
                              const double* rD, const double* upper, const double* lower, const double* r, double* w,
                              double* t1, double* t2, int* flag, unsigned* counter, int k, bool transpose,
-                             const DevScal* scal)
+                             const DevScal* scal, int width_f, int width_b)
 {
     const double* lo = transpose ? upper : lower;
     const double* up = transpose ? lower : upper;
     if (k < 0) {
         cudaMemsetAsync(flag, 0, sizeof(int) * (a.N + 1), s);
         cudaMemsetAsync(counter, 0, sizeof(unsigned), s);
-        k_ilu_fwd<<<persistent_grid((const void*)k_ilu_fwd), kThreads, 0, s>>>(a, order_f, rD, lo, r, w, flag, counter,
-                                                                             scal);
+        k_ilu_fwd<<<persistent_grid((const void*)k_ilu_fwd, 2 * width_f), kThreads, 0, s>>>(a, order_f, rD, lo, r, w,
+                                                                                           flag, counter, scal);
         cudaMemsetAsync(flag, 0, sizeof(int) * (a.N + 1), s);
         cudaMemsetAsync(counter, 0, sizeof(unsigned), s);
-        k_ilu_bwd<<<persistent_grid((const void*)k_ilu_bwd), kThreads, 0, s>>>(a, order_b, rD, up, w, flag, counter,
-                                                                             scal);
+        k_ilu_bwd<<<persistent_grid((const void*)k_ilu_bwd, 2 * width_b), kThreads, 0, s>>>(a, order_b, rD, up, w,
+                                                                                           flag, counter, scal);
         return;
     }
     if (k == 0) {
