@@ -633,12 +633,11 @@ int gamg_enqueue_cycle(spuma_mesh m, const spuma_gamg_params& gp, cudaStream_t s
             }
             xl = xin;
         }
-        launch_gamg_restrict(s, L, lv[l + 1], P, xl);
+        launch_gamg_restrict(s, L, lv[l + 1], P, xl, l + 2 == nl ? lv[l + 1].x : nullptr);  // zeroes x_coarsest
         ++k;
         xcur[l] = xl;
     }
     GLevel& Lc = lv[nl - 1];
-    cudaMemsetAsync(Lc.x, 0, sizeof(double) * Lc.a.N, s);
     launch_pcg_single(s, Lc.a, G->cws);
     ++k;
     xcur[nl - 1] = Lc.x;
@@ -1635,7 +1634,13 @@ spuma_status spuma_set_option(spuma_mesh m, int option, int value)
         m->defer_psi = value != 0;
         return SPUMA_OK;
     case SPUMA_OPT_PDL:
-        if (g_use_pdl != (value != 0)) destroy_graphs(m);
+        if (g_use_pdl != (value != 0)) {
+            destroy_graphs(m);
+            if (m->gamg && m->gamg->gexec) {  // the captured V-cycle embeds the launch attribute too
+                cudaGraphExecDestroy(m->gamg->gexec);
+                m->gamg->gexec = nullptr;
+            }
+        }
         g_use_pdl = value != 0;
         return SPUMA_OK;
     case SPUMA_OPT_SMALL_SOLVE_MAX_CELLS:

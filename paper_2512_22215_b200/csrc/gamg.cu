@@ -131,8 +131,10 @@ __global__ void __launch_bounds__(kThreads) k_gamg_agg(GLevel F, GLevel C, const
 // restrictField of the residual (Q23): C.b[c] = sum_{i in c} (b_i - (A x)_i); r_i stored
 // for the scale step when x is not zero.
 __global__ void __launch_bounds__(kThreads) k_gamg_restrict(GLevel F, GLevel C, const DevPtrs* __restrict__ P,
-                                                            const double* __restrict__ x)
+                                                            const double* __restrict__ x, double* __restrict__ zero_x)
 {
+    pdl_wait();  // predecessor complete and visible (PDL launch)
+    pdl_trigger();
     const double* __restrict__ fd = level_diag(F, P);
     const double* __restrict__ fu = level_upper(F, P);
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < F.nc; c += gridDim.x * blockDim.x) {
@@ -147,6 +149,7 @@ __global__ void __launch_bounds__(kThreads) k_gamg_restrict(GLevel F, GLevel C, 
             s = s + r;
         }
         C.b[c] = s;
+        if (zero_x) zero_x[c] = 0.0;
     }
 }
 
@@ -158,6 +161,8 @@ __global__ void __launch_bounds__(kThreads) k_gamg_smooth(GLevel L, const DevPtr
                                                           double omega, const double* __restrict__ xc,
                                                           const double* __restrict__ alpha, int psi_acc)
 {
+    pdl_wait();  // predecessor complete and visible (PDL launch)
+    pdl_trigger();
     const double* __restrict__ d = level_diag(L, P);
     const double* __restrict__ u = level_upper(L, P);
     double* __restrict__ psi = P->psi;
@@ -193,6 +198,8 @@ __global__ void __launch_bounds__(kThreads) k_gamg_scale(GLevel L, const DevPtrs
                                                          const double* __restrict__ r, double omega, int pq,
                                                          double* part, unsigned* ticket, double* alpha)
 {
+    pdl_wait();  // predecessor complete and visible (PDL launch)
+    pdl_trigger();
     const double* __restrict__ d = level_diag(L, P);
     const double* __restrict__ u = level_upper(L, P);
     const XInj X{xc, L.ftc};
@@ -222,6 +229,8 @@ __global__ void __launch_bounds__(kThreads) k_gamg_correct(GLevel L, const DevPt
                                                            const double* __restrict__ alpha, double* __restrict__ out,
                                                            int psi_acc)
 {
+    pdl_wait();  // predecessor complete and visible (PDL launch)
+    pdl_trigger();
     const XCorr X{x, xc, L.ftc, alpha ? *alpha : 1.0};
     double* __restrict__ psi = P->psi;
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < L.a.N; c += gridDim.x * blockDim.x) {
@@ -245,6 +254,8 @@ __global__ void __launch_bounds__(kThreads) k_gamg_post(GLevel L, const DevPtrs*
                                                         const double* __restrict__ alpha, double omega,
                                                         double* __restrict__ out, int two, int psi_acc)
 {
+    pdl_wait();  // predecessor complete and visible (PDL launch)
+    pdl_trigger();
     const double* __restrict__ d = level_diag(L, P);
     const double* __restrict__ u = level_upper(L, P);
     double* __restrict__ psi = P->psi;
@@ -266,6 +277,8 @@ __global__ void __launch_bounds__(kThreads) k_gamg_gs2_res(GLevel L, const DevPt
                                                            const double* __restrict__ xc,
                                                            const double* __restrict__ alpha, double* __restrict__ r)
 {
+    pdl_wait();  // predecessor complete and visible (PDL launch)
+    pdl_trigger();
     const double* __restrict__ d = level_diag(L, P);
     const double* __restrict__ u = level_upper(L, P);
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < L.a.N; c += gridDim.x * blockDim.x) {
@@ -289,6 +302,8 @@ __global__ void __launch_bounds__(kThreads) k_gamg_gs2_upd(GLevel L, const DevPt
                                                            const double* __restrict__ zin, double* __restrict__ out,
                                                            int skip_lower, int last, int psi_acc)
 {
+    pdl_wait();  // predecessor complete and visible (PDL launch)
+    pdl_trigger();
     const double* __restrict__ d = level_diag(L, P);
     const double* __restrict__ u = level_upper(L, P);
     double* __restrict__ psi = P->psi;
@@ -319,6 +334,8 @@ __global__ void __launch_bounds__(kThreads) k_gamg_gs2_upd(GLevel L, const DevPt
 template <bool ELL>
 __global__ void __launch_bounds__(kThreads) k_gamg_residual(GLevel L, Workspace w)
 {
+    pdl_wait();  // predecessor complete and visible (PDL launch)
+    pdl_trigger();
     const DevPtrs p = *w.ptrs;
     double v[1] = {0.0};
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < L.a.N; c += gridDim.x * blockDim.x) {
@@ -337,6 +354,23 @@ __global__ void __launch_bounds__(kThreads) k_gamg_residual(GLevel L, Workspace 
 }
 
 }  // namespace
+
+// every cycle kernel is launched with programmatic stream serialization (PDL): its CTAs may be
+// scheduled while the predecessor drains and wait in griddepcontrol.wait (g_use_pdl)
+template <typename... KArgs, typename... Args>
+static void glaunch(void (*kernel)(KArgs...), int grid, cudaStream_t s, Args... args)
+{
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = g_use_pdl ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
 
 static int g_gamg_max_grid = 0;
 
@@ -358,57 +392,58 @@ void launch_gamg_agg(cudaStream_t s, const GLevel& fine, const GLevel& coarse, c
     k_gamg_agg<<<gamg_grid(fine.nc > fine.ncf ? fine.nc : fine.ncf), kThreads, 0, s>>>(fine, coarse, P);
 }
 
-void launch_gamg_restrict(cudaStream_t s, const GLevel& fine, const GLevel& coarse, const DevPtrs* P, const double* x)
+void launch_gamg_restrict(cudaStream_t s, const GLevel& fine, const GLevel& coarse, const DevPtrs* P, const double* x,
+                          double* zero_x)
 {
-    k_gamg_restrict<<<gamg_grid(fine.nc), kThreads, 0, s>>>(fine, coarse, P, x);
+    glaunch(k_gamg_restrict, gamg_grid(fine.nc), s, fine, coarse, P, x, zero_x);
 }
 
 void launch_gamg_smooth(cudaStream_t s, const GLevel& L, const DevPtrs* P, const double* xin, double* xout,
                         double omega, const double* xc, const double* alpha, bool psi_acc)
 {
-    if (L.ell) k_gamg_smooth<true><<<L.grid, kThreads, 0, s>>>(L, P, xin, xout, omega, xc, alpha, psi_acc ? 1 : 0);
-    else k_gamg_smooth<false><<<L.grid, kThreads, 0, s>>>(L, P, xin, xout, omega, xc, alpha, psi_acc ? 1 : 0);
+    if (L.ell) glaunch(k_gamg_smooth<true>, L.grid, s, L, P, xin, xout, omega, xc, alpha, psi_acc ? 1 : 0);
+    else glaunch(k_gamg_smooth<false>, L.grid, s, L, P, xin, xout, omega, xc, alpha, psi_acc ? 1 : 0);
 }
 
 void launch_gamg_scale(cudaStream_t s, const GLevel& L, const DevPtrs* P, const double* x, const double* xc,
                        const double* r, double omega, bool pq, double* part, unsigned* ticket, double* alpha)
 {
-    if (L.ell) k_gamg_scale<true><<<L.grid, kThreads, 0, s>>>(L, P, x, xc, r, omega, pq ? 1 : 0, part, ticket, alpha);
-    else k_gamg_scale<false><<<L.grid, kThreads, 0, s>>>(L, P, x, xc, r, omega, pq ? 1 : 0, part, ticket, alpha);
+    if (L.ell) glaunch(k_gamg_scale<true>, L.grid, s, L, P, x, xc, r, omega, pq ? 1 : 0, part, ticket, alpha);
+    else glaunch(k_gamg_scale<false>, L.grid, s, L, P, x, xc, r, omega, pq ? 1 : 0, part, ticket, alpha);
 }
 
 void launch_gamg_correct(cudaStream_t s, const GLevel& L, const DevPtrs* P, const double* x, const double* xc,
                          const double* alpha, double* out, bool psi_acc)
 {
-    k_gamg_correct<<<L.grid, kThreads, 0, s>>>(L, P, x, xc, alpha, out, psi_acc ? 1 : 0);
+    glaunch(k_gamg_correct, L.grid, s, L, P, x, xc, alpha, out, psi_acc ? 1 : 0);
 }
 
 void launch_gamg_post(cudaStream_t s, const GLevel& L, const DevPtrs* P, const double* alpha, double omega,
                       double* out, bool two, bool psi_acc)
 {
-    if (L.ell) k_gamg_post<true><<<L.grid, kThreads, 0, s>>>(L, P, alpha, omega, out, two ? 1 : 0, psi_acc ? 1 : 0);
-    else k_gamg_post<false><<<L.grid, kThreads, 0, s>>>(L, P, alpha, omega, out, two ? 1 : 0, psi_acc ? 1 : 0);
+    if (L.ell) glaunch(k_gamg_post<true>, L.grid, s, L, P, alpha, omega, out, two ? 1 : 0, psi_acc ? 1 : 0);
+    else glaunch(k_gamg_post<false>, L.grid, s, L, P, alpha, omega, out, two ? 1 : 0, psi_acc ? 1 : 0);
 }
 
 void launch_gamg_gs2_res(cudaStream_t s, const GLevel& L, const DevPtrs* P, const double* xin, const double* xc,
                          const double* alpha, double* r)
 {
-    if (L.ell) k_gamg_gs2_res<true><<<L.grid, kThreads, 0, s>>>(L, P, xin, xc, alpha, r);
-    else k_gamg_gs2_res<false><<<L.grid, kThreads, 0, s>>>(L, P, xin, xc, alpha, r);
+    if (L.ell) glaunch(k_gamg_gs2_res<true>, L.grid, s, L, P, xin, xc, alpha, r);
+    else glaunch(k_gamg_gs2_res<false>, L.grid, s, L, P, xin, xc, alpha, r);
 }
 
 void launch_gamg_gs2_upd(cudaStream_t s, const GLevel& L, const DevPtrs* P, const double* xin, const double* xc,
                          const double* alpha, const double* r, const double* zin, double* out, bool skip_lower,
                          bool last, bool psi_acc)
 {
-    k_gamg_gs2_upd<<<L.grid, kThreads, 0, s>>>(L, P, xin, xc, alpha, r, zin, out, skip_lower ? 1 : 0, last ? 1 : 0,
-                                               psi_acc ? 1 : 0);
+    glaunch(k_gamg_gs2_upd, L.grid, s, L, P, xin, xc, alpha, r, zin, out, skip_lower ? 1 : 0, last ? 1 : 0,
+            psi_acc ? 1 : 0);
 }
 
 void launch_gamg_residual(cudaStream_t s, const GLevel& L, const Workspace& w)
 {
-    if (L.ell) k_gamg_residual<true><<<L.grid, kThreads, 0, s>>>(L, w);
-    else k_gamg_residual<false><<<L.grid, kThreads, 0, s>>>(L, w);
+    if (L.ell) glaunch(k_gamg_residual<true>, L.grid, s, L, w);
+    else glaunch(k_gamg_residual<false>, L.grid, s, L, w);
 }
 
 }  // namespace spuma

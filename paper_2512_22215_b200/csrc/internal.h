@@ -305,7 +305,7 @@ void launch_amul_asym(cudaStream_t s, const MeshArgs& a, const double* diag, con
 int gamg_grid(int n);
 void launch_gamg_agg(cudaStream_t s, const GLevel& fine, const GLevel& coarse, const DevPtrs* P);
 void launch_gamg_restrict(cudaStream_t s, const GLevel& fine, const GLevel& coarse, const DevPtrs* P,
-                          const double* x);                       // x nullptr: the level's x is zero
+                          const double* x, double* zero_x = nullptr);  // x nullptr: the level's x is zero
 void launch_gamg_smooth(cudaStream_t s, const GLevel& L, const DevPtrs* P, const double* xin, double* xout,
                         double omega, const double* xc, const double* alpha, bool psi_acc);
 void launch_gamg_scale(cudaStream_t s, const GLevel& L, const DevPtrs* P, const double* x, const double* xc,
