@@ -530,6 +530,23 @@ spuma_status gamg_ensure(spuma_mesh m, const spuma_gamg_params& gp)
             SPUMA_TRY(galloc(G, &L.diag, n));
             SPUMA_TRY(galloc(G, &L.upper, h.F));
             SPUMA_TRY(galloc(G, &L.b, n));
+            // coarse levels of hex meshes stay structured: rows over ELL when the widths are
+            // uniform (<= 3 per side); k_gamg_agg then also writes the owner-slot coefficients
+            const SellHost sh = build_sell(n, h.ownerStart, h.losortStart, h.losort, h.ownerLo, h.neighbour);
+            if (sh.ok && sh.uniform_wn >= 0 && sh.uniform_wn <= 3 && sh.uniform_wo >= 0 && sh.uniform_wo <= 3) {
+                unsigned* sn;
+                int* so;
+                double* us;
+                SPUMA_TRY(gupload(G, &sn, sh.nslot, s));
+                SPUMA_TRY(gupload(G, &so, sh.oslot, s));
+                SPUMA_TRY(galloc(G, &us, (size_t)32 * sh.uniform_wo * ((n + 31) / 32)));
+                L.a.sell_n = sn;
+                L.a.sell_o = so;
+                L.a.upper_s = us;
+                L.a.ell_wn = sh.uniform_wn;
+                L.a.ell_wo = sh.uniform_wo;
+                L.ell = 1;
+            }
         }
         SPUMA_TRY(galloc(G, &L.x, n));
         SPUMA_TRY(galloc(G, &L.x2, n));

@@ -125,6 +125,10 @@ __global__ void __launch_bounds__(kThreads) k_gamg_agg(GLevel F, GLevel C, const
         double u = 0.0;
         for (int k = F.cfStart[e]; k < F.cfStart[e + 1]; ++k) u = u + fu[F.cfList[k]];
         C.upper[e] = u;
+        if (C.ell) {  // owner-slot copy for the ELL rows of the coarse level
+            const int c = C.a.owner[e];
+            const_cast<double*>(C.a.upper_s)[(size_t)32 * C.a.ell_wo * (c >> 5) + 32 * (e - C.a.ownerStart[c]) + (c & 31)] = u;
+        }
     }
 }
 

@@ -69,6 +69,7 @@ CASES = [
     ("perturbed-permuted", lambda: gen.permute(gen.perturbed(10, 0.2), seed=7)),
     ("cavity20", lambda: gen.cavity2d(20)),
     ("box-ragged", lambda: gen.box(13, 7, 5, (1.0, 0.6, 0.4))),
+    ("cube32-regular", lambda: gen.cube(32)),  # h = 2^-5: exact equal areas -> every level uniform ELL
 ]
 
 
