@@ -395,7 +395,12 @@ typedef enum {
     SPUMA_OPT_PDL = 2,
     /* apply psi += alpha pA for two iterations at once (psi = (psi + a1 p1) + a2 p2: the same
      * roundings, fewer bytes); 1 = on (default), 0 = every iteration */
-    SPUMA_OPT_DEFER_PSI = 3
+    SPUMA_OPT_DEFER_PSI = 3,
+    /* GAMG: the levels from the first one (below the finest) with at most this many cells
+     * down to the coarsest run in ONE single-CTA kernel per V-cycle (Richardson, scaled
+     * correction, nPre = 0); default 1024 (same-box A/B: 256-1024 best, 4096+ slower); 0 = one
+     * launch per level and step */
+    SPUMA_OPT_GAMG_TAIL_CELLS = 4
 } spuma_option;
 spuma_status spuma_set_option(spuma_mesh m, int option, int value);
 

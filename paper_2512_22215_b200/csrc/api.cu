@@ -440,7 +440,9 @@ struct GamgState {
     spuma::DevPtrs* h_cptrs = nullptr;               // pinned
     cudaGraphExec_t gexec = nullptr;
     spuma_gamg_params gkey{};
+    int gkey_tail = -1;                              // tail threshold the graph was captured with
     int launches_per_cycle = 0;
+    spuma::GLevel* d_lv = nullptr;                   // device copy of lv (the single-CTA tail reads it)
 };
 
 namespace {
@@ -577,6 +579,8 @@ spuma_status gamg_ensure(spuma_mesh m, const spuma_gamg_params& gp)
         }
         h = GamgHostLevel{};  // release host memory early
     }
+    SPUMA_TRY(galloc(G, &G->d_lv, nl));
+    SPUMA_CUDA(cudaMemcpyAsync(G->d_lv, G->lv.data(), sizeof(GLevel) * nl, cudaMemcpyHostToDevice, s));
     SPUMA_TRY(galloc(G, &G->alpha, nl));
     SPUMA_TRY(galloc(G, &G->part, (size_t)kMaxPartials * max_grid));
     SPUMA_TRY(galloc(G, &G->ticket, 4));
@@ -637,8 +641,19 @@ int gamg_enqueue_cycle(spuma_mesh m, const spuma_gamg_params& gp, cudaStream_t s
             zin = zo;
         }
     };
+    // the small levels t..nl-1 in one CTA (k_gamg_tail) when the configuration allows it
+    int t = nl;
+    if (m->gamg_tail_cells > 0 && gp.smoother == SPUMA_SMOOTHER_RICHARDSON && gp.scale_correction &&
+        gp.n_pre_sweeps == 0 && gp.n_post_sweeps >= 1) {
+        for (int l = 1; l < nl; ++l)
+            if (lv[l].a.N <= m->gamg_tail_cells) {
+                t = l;
+                break;
+            }
+        if (t >= nl - 1) t = nl;
+    }
     std::vector<double*> xcur(nl, nullptr);  // buffer holding x_l; nullptr: x_l == 0
-    for (int l = 0; l + 1 < nl; ++l) {
+    for (int l = 0; l + 1 < nl && l < t; ++l) {
         GLevel& L = lv[l];
         double* xl = nullptr;
         if (gp.n_pre_sweeps > 0) {
@@ -655,11 +670,18 @@ int gamg_enqueue_cycle(spuma_mesh m, const spuma_gamg_params& gp, cudaStream_t s
         xcur[l] = xl;
     }
     GLevel& Lc = lv[nl - 1];
-    launch_pcg_single(s, Lc.a, G->cws);
-    ++k;
-    xcur[nl - 1] = Lc.x;
+    if (t < nl) {
+        launch_gamg_tail(s, G->d_lv, t, nl, G->cws, gp.omega, gp.n_post_sweeps);
+        ++k;
+        const bool in_x = gp.n_post_sweeps <= 2 || ((gp.n_post_sweeps - 2) & 1) == 0;
+        xcur[t] = in_x ? lv[t].x : lv[t].x2;
+    } else {
+        launch_pcg_single(s, Lc.a, G->cws);
+        ++k;
+        xcur[nl - 1] = Lc.x;
+    }
     const bool pq = gp.smoother != SPUMA_SMOOTHER_GS2 && gp.scale_correction && gp.n_post_sweeps > 0;
-    for (int l = nl - 2; l >= 0; --l) {
+    for (int l = (t < nl ? t - 1 : nl - 2); l >= 0; --l) {
         GLevel& L = lv[l];
         const double* xc = xcur[l + 1];
         const double* r = xcur[l] ? L.r : L.b;
@@ -1646,6 +1668,10 @@ spuma_status spuma_set_option(spuma_mesh m, int option, int value)
 {
     if (!m) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "mesh is NULL");
     switch (option) {
+    case SPUMA_OPT_GAMG_TAIL_CELLS:
+        if (value < 0) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "negative GAMG tail size");
+        m->gamg_tail_cells = value;  // the captured V-cycle is re-captured at the next solve
+        return SPUMA_OK;
     case SPUMA_OPT_DEFER_PSI:
         if (m->defer_psi != (value != 0)) destroy_graphs(m);
         m->defer_psi = value != 0;
@@ -1767,7 +1793,7 @@ spuma_status spuma_gamg_solve(spuma_mesh m, const spuma_scalar* diag, const spum
 
     // one V-cycle per graph launch (nl == 1: direct launches, psi is a per-call pointer)
     const bool use_graph = nl > 1;
-    if (use_graph && (!G->gexec || std::memcmp(&G->gkey, &gp, sizeof gp) != 0)) {
+    if (use_graph && (!G->gexec || std::memcmp(&G->gkey, &gp, sizeof gp) != 0 || G->gkey_tail != m->gamg_tail_cells)) {
         if (G->gexec) cudaGraphExecDestroy(G->gexec);
         G->gexec = nullptr;
         cudaGraph_t graph = nullptr;
@@ -1779,6 +1805,7 @@ spuma_status spuma_gamg_solve(spuma_mesh m, const spuma_scalar* diag, const spum
         cudaGraphDestroy(graph);
         SPUMA_CUDA(e);
         G->gkey = gp;
+        G->gkey_tail = m->gamg_tail_cells;
     }
     SPUMA_CUDA(cudaMemcpyAsync(&m->h_scal[0], m->ws.scal, sizeof(DevScal), cudaMemcpyDeviceToHost, s));
     SPUMA_CUDA(cudaStreamSynchronize(s));
@@ -1970,7 +1997,6 @@ spuma_status spuma_precondition(spuma_mesh m, const spuma_scalar* diag, const sp
     SPUMA_TRY(pc_check(m, *pcp));
     if (m->N == 0) return SPUMA_OK;
     SPUMA_TRY(pc_ensure(m));
-    PcState* P = m->pc;
     cudaStream_t s = m->stream;
     const double *d_i, *r_i, *u_i, *l_i;
     SPUMA_TRY(cells_in(m, diag, R_DIAG, &d_i));
@@ -1983,7 +2009,6 @@ spuma_status spuma_precondition(spuma_mesh m, const spuma_scalar* diag, const sp
     SPUMA_TRY(cells_out(m, wout, m->d_cell_t));
     SPUMA_CUDA(cudaStreamSynchronize(s));
     SPUMA_CUDA(cudaGetLastError());
-    (void)P;
     return SPUMA_OK;
 }
 

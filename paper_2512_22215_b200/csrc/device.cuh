@@ -112,4 +112,141 @@ static __device__ __forceinline__ double amul_row(const MeshArgs& a, int c, cons
     return s;
 }
 
+// Finalisation steps of the PCG scalars, from global sums g[].
+static __device__ void finalize(DevScal* s, int stage, const double* g)
+{
+    switch (stage) {
+    case 1:  // gAverage(psi) = gSum(psi) / gSum(nCells)
+        s->xbar = g[0] / g[1];
+        break;
+    case 2: {  // normFactor, initial residual, first wArA, iterate-at-all decision (Q1, Q3)
+        s->normFactor = g[0] + 1e-20;
+        s->init = g[1] / s->normFactor;
+        s->fin = s->init;
+        s->wArA = g[2];
+        s->wArAold = 1e20;
+        s->n = 0;
+        s->singular = 0;
+        s->converged = conv(s->fin, s->init, s->tol, s->rel_tol);
+        s->done = !(s->min_iter > 0 || !s->converged);
+        break;
+    }
+    case 3: {  // alpha = wArA / wApA, checkSingularity (Q4)
+        s->wApA = g[0];
+        if (fabs(s->wApA) / s->normFactor < 1e-300) {
+            s->singular = 1;
+            s->done = 1;
+        } else {
+            s->alpha = s->wArA / s->wApA;
+        }
+        break;
+    }
+    case 4: {  // final residual, convergence, loop condition, beta for the next direction
+        s->fin = g[1] / s->normFactor;
+        s->n = s->n + 1;
+        const bool c = conv(s->fin, s->init, s->tol, s->rel_tol);
+        s->converged = c;
+        if (!((s->n < s->max_iter && !c) || s->n < s->min_iter)) s->done = 1;
+        s->wArAold = s->wArA;
+        s->wArA = g[0];
+        s->beta = s->wArA / s->wArAold;
+        s->alpha_prev = s->alpha;  // a deferred psi update of this iteration uses it
+        break;
+    }
+    }
+}
+
+template <int NV>
+__device__ __forceinline__ void cta_sum_1024(double (&v)[NV])
+{
+    __shared__ double sh[NV][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int i = 0; i < NV; ++i)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v[i] += __shfl_down_sync(0xffffffffu, v[i], o);
+    if (lane == 0)
+#pragma unroll
+        for (int i = 0; i < NV; ++i) sh[i][warp] = v[i];
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            double t = lane < nw ? sh[i][lane] : 0.0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
+            v[i] = t;
+        }
+    }
+    __syncthreads();
+}
+
+// The whole PCG solve (A6-A12) by one CTA of kSmallThreads threads (small meshes, GAMG coarsest level).
+static __device__ void pcg_single_body(const MeshArgs& a, const Workspace& w)
+{
+    const DevPtrs p = *w.ptrs;
+    DevScal* sc = w.scal;
+    const int N = a.N, t = threadIdx.x;
+    {  // A6: wA = A psi, sumA, gAverage(psi)
+        double v[2] = {0.0, 0.0};
+        for (int c = t; c < N; c += kSmallThreads) {
+            double rs;
+            w.wA[c] = amul_row(a, c, p.diag, p.upper, p.iface, p.psi, w.xr, &rs);
+            w.sumA[c] = rs;
+            v[0] += p.psi[c];
+        }
+        if (t == 0) v[1] = (double)N;
+        cta_sum_1024<2>(v);
+        if (t == 0) finalize(sc, 1, v);
+        __syncthreads();
+    }
+    {  // A6: residual, normFactor, rD, first wArA
+        const double xbar = sc->xbar;
+        double v[3] = {0.0, 0.0, 0.0};
+        for (int c = t; c < N; c += kSmallThreads) {
+            const double b = p.source[c], wa = w.wA[c];
+            const double r = b - wa;
+            const double xref = w.sumA[c] * xbar;
+            const double rd = 1.0 / p.diag[c];
+            w.rA[c] = r;
+            w.rD[c] = rd;
+            v[0] += fabs(wa - xref) + fabs(b - xref);
+            v[1] += fabs(r);
+            v[2] += (rd * r) * r;
+        }
+        cta_sum_1024<3>(v);
+        if (t == 0) finalize(sc, 2, v);
+        __syncthreads();
+    }
+    while (!sc->done) {
+        const bool first = sc->n == 0;
+        const double beta = sc->beta;
+        for (int c = t; c < N; c += kSmallThreads)  // A11
+            w.pA[c] = first ? w.rD[c] * w.rA[c] : w.rD[c] * w.rA[c] + beta * w.pA[c];
+        __syncthreads();
+        double v[2] = {0.0, 0.0};
+        for (int c = t; c < N; c += kSmallThreads) {  // A7
+            const double y = amul_row(a, c, p.diag, p.upper, p.iface, w.pA, w.xr, nullptr);
+            w.wA[c] = y;
+            v[0] += y * w.pA[c];
+        }
+        cta_sum_1024<1>(reinterpret_cast<double(&)[1]>(v[0]));
+        if (t == 0) finalize(sc, 3, v);  // A8
+        __syncthreads();
+        if (sc->done) break;
+        const double alpha = sc->alpha;
+        v[0] = v[1] = 0.0;
+        for (int c = t; c < N; c += kSmallThreads) {  // A9
+            p.psi[c] = p.psi[c] + alpha * w.pA[c];
+            const double r = w.rA[c] - alpha * w.wA[c];
+            w.rA[c] = r;
+            v[0] += (w.rD[c] * r) * r;
+            v[1] += fabs(r);
+        }
+        cta_sum_1024<2>(v);
+        if (t == 0) finalize(sc, 4, v);  // A10
+        __syncthreads();
+    }
+}
+
 }  // namespace spuma

@@ -357,7 +357,87 @@ __global__ void __launch_bounds__(kThreads) k_gamg_residual(GLevel L, Workspace 
     }
 }
 
+// The small levels t..nl-1 of a V-cycle in ONE CTA (Richardson, scaled correction, nPre = 0):
+// restrictions down, the coarsest PCG (pcg_single_body), then per level the scale step and the
+// fused post-sweeps, phases separated by __syncthreads() instead of ~3 launches per level.
+// Same arithmetic as the per-level kernels (only the reduction shape of the scale dots
+// differs).  Level t's b comes from the preceding restriction kernel; its result is left in
+// lv[t].x or lv[t].x2 exactly as the per-level path leaves it.
+__global__ void __launch_bounds__(kSmallThreads) k_gamg_tail(const GLevel* __restrict__ lv, int t, int nl,
+                                                             Workspace cws, double omega, int n_post)
+{
+    pdl_wait();
+    const int tid = threadIdx.x;
+    __shared__ double s_alpha;
+    for (int l = t; l + 1 < nl; ++l) {  // restriction (x_l = 0: r = b)
+        const GLevel& L = lv[l];
+        const GLevel& C = lv[l + 1];
+        for (int c = tid; c < L.nc; c += kSmallThreads) {
+            double s = 0.0;
+            for (int k = L.cStart[c]; k < L.cStart[c + 1]; ++k) s = s + L.b[L.cList[k]];
+            C.b[c] = s;
+            if (l + 2 == nl) C.x[c] = 0.0;
+        }
+        __syncthreads();
+    }
+    pcg_single_body(lv[nl - 1].a, cws);
+    __syncthreads();
+    for (int l = nl - 2; l >= t; --l) {
+        const GLevel& L = lv[l];
+        const GLevel& C = lv[l + 1];
+        const double* xc = (l + 1 == nl - 1 || n_post == 1 || ((n_post - 2) & 1) == 0) ? C.x : C.x2;
+        const double* d = L.diag;
+        const double* u = L.upper;
+        const XInj X{xc, L.ftc};
+        double v[2] = {0.0, 0.0};
+        for (int c = tid; c < L.a.N; c += kSmallThreads) {  // scale + p/q (Q25, Q29)
+            const double ci = X(c);
+            const double aci = L.ell ? row_ax_ell(L.a, c, d, X) : row_ax(L.a, c, d, u, X);
+            const double ri = L.b[c];
+            const double rd = 1.0 / d[c];
+            L.p[c] = ci - omega * (rd * aci);
+            L.q[c] = 0.0 + omega * (rd * ri);
+            v[0] += ci * ri;
+            v[1] += aci * ci;
+        }
+        cta_sum_1024<2>(v);
+        if (tid == 0) {
+            double a = fabs(v[1]) > 1e-300 ? v[0] / v[1] : 1.0;
+            s_alpha = a < 0.0 ? 0.0 : (a > 2.0 ? 2.0 : a);
+        }
+        __syncthreads();
+        const XPQ Y{L.p, L.q, s_alpha};
+        for (int c = tid; c < L.a.N; c += kSmallThreads) {  // post-sweeps 1 (+2)
+            const double x1 = Y(c);
+            double xn = x1;
+            if (n_post >= 2)
+                xn = x1 + omega * ((1.0 / d[c]) * (L.b[c] - (L.ell ? row_ax_ell(L.a, c, d, Y) : row_ax(L.a, c, d, u, Y))));
+            L.x[c] = xn;
+        }
+        __syncthreads();
+        double* xin = L.x;
+        double* xout = L.x2;
+        for (int i = 2; i < n_post; ++i) {  // further plain sweeps
+            for (int c = tid; c < L.a.N; c += kSmallThreads) {
+                const XPlain Z{xin};
+                const double y = L.ell ? row_ax_ell(L.a, c, d, Z) : row_ax(L.a, c, d, u, Z);
+                xout[c] = xin[c] + omega * ((1.0 / d[c]) * (L.b[c] - y));
+            }
+            __syncthreads();
+            double* tmp = xin;
+            xin = xout;
+            xout = tmp;
+        }
+    }
+}
+
 }  // namespace
+
+void launch_gamg_tail(cudaStream_t s, const GLevel* d_lv, int t, int nl, const Workspace& cws, double omega,
+                      int n_post)
+{
+    k_gamg_tail<<<1, kSmallThreads, 0, s>>>(d_lv, t, nl, cws, omega, n_post);
+}
 
 // every cycle kernel is launched with programmatic stream serialization (PDL): its CTAs may be
 // scheduled while the predecessor drains and wait in griddepcontrol.wait (g_use_pdl)

@@ -13,6 +13,7 @@
 namespace spuma {
 
 constexpr int kThreads = 256;      // threads per CTA of every cell/face kernel (8 warps)
+constexpr int kSmallThreads = 1024;  // the single-CTA solves (small meshes, GAMG coarsest level / tail)
 constexpr int kMaxPartials = 4;    // reduction values per kernel
 constexpr int kPhases = 4;         // timing phases (spuma_stats.phase_ms)
 
@@ -169,6 +170,7 @@ struct spuma_mesh_s {
     int amul_variant = 8;
     bool defer_psi = true;  // psi += alpha pA applied every second iteration (same rounding, fewer bytes)  // ELL + coefficient copy (falls back to 6 -> 5 when the mesh is not uniform)
     bool timing = false;
+    int gamg_tail_cells = 1024;  // GAMG: levels from the first one at or below this size run in one CTA (0: off)
     cudaGraphExec_t gexec[2] = {nullptr, nullptr};
     bool gexec_timed = false;
     int gexec_batch = 0;
@@ -313,6 +315,9 @@ void launch_gamg_scale(cudaStream_t s, const GLevel& L, const DevPtrs* P, const 
 void launch_gamg_correct(cudaStream_t s, const GLevel& L, const DevPtrs* P, const double* x, const double* xc,
                          const double* alpha, double* out, bool psi_acc);
 void launch_gamg_residual(cudaStream_t s, const GLevel& L, const Workspace& w);
+// levels t..nl-1 of the V-cycle in one CTA (Richardson, scaled, nPre = 0); d_lv: device copy of the levels
+void launch_gamg_tail(cudaStream_t s, const GLevel* d_lv, int t, int nl, const Workspace& cws, double omega,
+                      int n_post);
 void launch_gamg_post(cudaStream_t s, const GLevel& L, const DevPtrs* P, const double* alpha, double omega,
                       double* out, bool two, bool psi_acc);
 void launch_gamg_gs2_res(cudaStream_t s, const GLevel& L, const DevPtrs* P, const double* xin, const double* xc,

@@ -47,6 +47,9 @@ def cycle_bytes(cells, faces):
 def run(name, m, gamma, tol, rel_tol=0.0, reps=3, params=None):
     t0 = time.perf_counter()
     h = P.Mesh.from_mesh(m, renumber=False, stream=torch.cuda.current_stream().cuda_stream)
+    if os.environ.get("GAMG_TAIL") is not None:  # A/B: single-CTA tail threshold (0 = off)
+        h.set_option(P.spuma.OPT_GAMG_TAIL_CELLS, int(os.environ["GAMG_TAIL"]))
+        name += f" [tail {os.environ['GAMG_TAIL']}]"
     if os.environ.get("GAMG_PDL") == "0":  # A/B: plain launches
         h.set_option(P.spuma.OPT_PDL, 0)
         name += " [PDL off]"

@@ -211,3 +211,23 @@ def test_invalid_arguments():
         c.gpu((1e-6, 0.0, 10, 0), P.gamg_params(max_levels=0))
     with pytest.raises(P.SpumaError):
         c.gpu((1e-6, 0.0, 10, 0), P.gamg_params(n_post_sweeps=-1))
+
+
+@pytest.mark.parametrize("tail", [0, 4096, 100000])
+@pytest.mark.parametrize("name,make", [("perturbed14", lambda: gen.perturbed(14, 0.15)),
+                                       ("cube32", lambda: gen.cube(32))])
+def test_single_cta_tail_on_off(name, make, tail):
+    """SPUMA_OPT_GAMG_TAIL_CELLS: the small levels in one CTA (k_gamg_tail) or one launch per
+    level and step; both against the oracle (one cycle and a full solve)."""
+    m = make()
+    c = Case(m, gen.gamma_lognormal(m))
+    c.h.set_option(P.spuma.OPT_GAMG_TAIL_CELLS, tail)
+    psi_g, pg = c.gpu((0.0, 0.0, 1, 1))
+    psi_o, po = c.oracle((0.0, 0.0, 1, 1))
+    assert rel_l2(psi_g, psi_o) <= 1e-11
+    _solve_parity(c, (1e-9, 0.0, 300, 0))
+    for kw in (dict(n_post_sweeps=1), dict(n_post_sweeps=3), dict(n_post_sweeps=4, omega=0.6)):
+        gp = P.gamg_params(**kw)
+        psi_g, _ = c.gpu((0.0, 0.0, 2, 2), gp)
+        psi_o, _ = c.oracle((0.0, 0.0, 2, 2), gp)
+        assert rel_l2(psi_g, psi_o) <= 1e-10, kw
