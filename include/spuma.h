@@ -297,6 +297,26 @@ spuma_status spuma_ldu_to_csr(spuma_mesh m, spuma_label* row_ptr, spuma_label* c
 spuma_status spuma_csr_values(spuma_mesh m, const spuma_scalar* diag, const spuma_scalar* upper,
                               const spuma_scalar* lower, spuma_scalar* values);
 
+/* ---------------- host-only diagnostics (no device access) ----------------
+ * The host logic of libspuma, callable without a GPU so it can be checked on any machine:
+ * addressing validation + RCM (A0/A1, Q12), the GAMG hierarchy (Q22: faceAreaPair pairing on
+ * face_weights, n_coarsest / max_levels as spuma_gamg_params), the DIC/DILU dependency
+ * schedules (rows sorted by dependency level) and the LDU -> CSR map (Q34).  All arrays are
+ * host memory in the caller's numbering; owner/neighbour must be valid lduAddressing
+ * (SPUMA_ERR_ADDRESSING otherwise).  ftc: the fine-to-coarse maps of every level but the
+ * coarsest, concatenated (sum of level_cells[0 .. n_levels-2] entries).  order_*: [n_cells]. */
+spuma_status spuma_host_rcm(int n_cells, int n_faces, const spuma_label* owner, const spuma_label* neighbour,
+                            spuma_label* perm);
+spuma_status spuma_host_gamg_hierarchy(int n_cells, int n_faces, const spuma_label* owner,
+                                       const spuma_label* neighbour, const spuma_scalar* face_weights,
+                                       int n_coarsest, int max_levels, int max_out, int* n_levels,
+                                       int* level_cells, int* level_faces, spuma_label* ftc);
+spuma_status spuma_host_level_schedule(int n_cells, int n_faces, const spuma_label* owner,
+                                       const spuma_label* neighbour, spuma_label* order_f, spuma_label* order_b,
+                                       int* depth_f, int* depth_b);
+spuma_status spuma_host_ldu_to_csr(int n_cells, int n_faces, const spuma_label* owner, const spuma_label* neighbour,
+                                   spuma_label* row_ptr, spuma_label* col, spuma_label* map);
+
 /* ---------------- around the path (the pressure step's neighbours) ----------------
  * Oriented face fields (phi, flux) are owner -> neighbour in the CALLER's numbering; with
  * renumber = 1 faces whose owner/neighbour swapped are negated on entry and exit.  Per-patch

@@ -765,27 +765,12 @@ spuma_status pc_ensure(spuma_mesh m)
     PcState* P = new PcState();
     m->pc = P;
     const int N = m->N;
-    std::vector<int> lf(N, 0), lb(N, 0);
-    for (int c = 0; c < N; ++c)
-        for (int k = m->h_losortStart[c]; k < m->h_losortStart[c + 1]; ++k)
-            lf[c] = std::max(lf[c], lf[m->h_owner[m->h_losort[k]]] + 1);
-    for (int c = N - 1; c >= 0; --c)
-        for (int f = m->h_ownerStart[c]; f < m->h_ownerStart[c + 1]; ++f)
-            lb[c] = std::max(lb[c], lb[m->h_neighbour[f]] + 1);
-    auto order_by = [N](const std::vector<int>& lev, int& depth, int& width) {
-        depth = 0;
-        for (int c = 0; c < N; ++c) depth = std::max(depth, lev[c] + 1);
-        std::vector<int> start(depth + 1, 0), ord(N);
-        for (int c = 0; c < N; ++c) start[lev[c] + 1]++;
-        width = 0;
-        for (int d = 0; d < depth; ++d) width = std::max(width, start[d + 1]);
-        for (int d = 0; d < depth; ++d) start[d + 1] += start[d];
-        for (int c = 0; c < N; ++c) ord[start[lev[c]]++] = c;
-        return ord;
-    };
+    std::vector<int> of, ob;
+    level_schedule(N, m->h_owner, m->h_neighbour, m->h_ownerStart, m->h_losortStart, m->h_losort, of, ob, P->depth_f,
+                   P->depth_b, P->width_f, P->width_b);
     cudaStream_t s = m->stream;
-    SPUMA_TRY(upload(&P->order_f, order_by(lf, P->depth_f, P->width_f), s));
-    SPUMA_TRY(upload(&P->order_b, order_by(lb, P->depth_b, P->width_b), s));
+    SPUMA_TRY(upload(&P->order_f, of, s));
+    SPUMA_TRY(upload(&P->order_b, ob, s));
     SPUMA_TRY(dalloc(&P->flag, N + 1));
     SPUMA_TRY(dalloc(&P->counter, 1));
     for (double** b : {&P->raw, &P->rD, &P->t1, &P->t2, &P->wT, &P->rT, &P->pT}) SPUMA_TRY(dalloc(b, N));
@@ -2038,26 +2023,10 @@ spuma_status spuma_ldu_to_csr(spuma_mesh m, spuma_label* row_ptr, spuma_label* c
 {
     if (!m || !row_ptr || !col || !map) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "NULL argument");
     if (m->renumber) return set_error(SPUMA_ERR_STATE, "LDU->CSR needs a handle built with renumber = 0");
-    const int N = m->N, F = m->F, nnz = N + 2 * F;
-    // per row: lower-triangle entries (faces with neighbour c: column owner, ascending because
-    // losort is owner-ascending), the diagonal, then owner faces (column neighbour, ascending)
-    std::vector<int> rp(N + 1), cl(nnz), mp(nnz);
-    rp[0] = 0;
-    int k = 0;
-    for (int c = 0; c < N; ++c) {
-        for (int j = m->h_losortStart[c]; j < m->h_losortStart[c + 1]; ++j) {
-            const int f = m->h_losort[j];
-            cl[k] = m->h_owner[f];
-            mp[k++] = N + F + f;
-        }
-        cl[k] = c;
-        mp[k++] = c;
-        for (int f = m->h_ownerStart[c]; f < m->h_ownerStart[c + 1]; ++f) {
-            cl[k] = m->h_neighbour[f];
-            mp[k++] = N + f;
-        }
-        rp[c + 1] = k;
-    }
+    std::vector<int> rp, cl, mp;
+    ldu_to_csr_host(m->N, m->F, m->h_owner, m->h_neighbour, m->h_ownerStart, m->h_losortStart, m->h_losort, rp, cl,
+                    mp);
+    const int nnz = m->N + 2 * m->F;
     auto put = [&](spuma_label* dst, const std::vector<int>& v) -> spuma_status {
         if (is_device_ptr(dst)) SPUMA_CUDA(cudaMemcpy(dst, v.data(), sizeof(int) * v.size(), cudaMemcpyHostToDevice));
         else std::memcpy(dst, v.data(), sizeof(int) * v.size());
@@ -2085,6 +2054,87 @@ spuma_status spuma_csr_values(spuma_mesh m, const spuma_scalar* diag, const spum
     m->stats.kernel_launches += 1;
     SPUMA_CUDA(cudaStreamSynchronize(m->stream));
     SPUMA_CUDA(cudaGetLastError());
+    return SPUMA_OK;
+}
+
+// ---------------- host-only diagnostics (no device access; CPU-testable host logic) ----------------
+static spuma_status host_addressing(int n, int F, const spuma_label* owner, const spuma_label* neighbour,
+                                    std::vector<int>& o, std::vector<int>& nb, std::vector<int>& os,
+                                    std::vector<int>& ls, std::vector<int>& lo, std::vector<int>& olo)
+{
+    if (n < 0 || F < 0 || (F > 0 && (!owner || !neighbour))) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "bad sizes");
+    std::string why;
+    if (!valid_addressing(n, F, owner, neighbour, &why)) return set_error(SPUMA_ERR_ADDRESSING, why);
+    o.assign(owner, owner + F);
+    nb.assign(neighbour, neighbour + F);
+    derived_addressing(n, F, o.data(), nb.data(), os, lo, ls, olo);
+    return SPUMA_OK;
+}
+
+spuma_status spuma_host_rcm(int n_cells, int n_faces, const spuma_label* owner, const spuma_label* neighbour,
+                            spuma_label* perm)
+{
+    std::vector<int> o, nb, os, ls, lo, olo;
+    SPUMA_TRY(host_addressing(n_cells, n_faces, owner, neighbour, o, nb, os, ls, lo, olo));
+    if (!perm) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "perm is NULL");
+    const std::vector<int> p = rcm_permutation(n_cells, n_faces, owner, neighbour);
+    std::memcpy(perm, p.data(), sizeof(int) * p.size());
+    return SPUMA_OK;
+}
+
+spuma_status spuma_host_gamg_hierarchy(int n_cells, int n_faces, const spuma_label* owner,
+                                       const spuma_label* neighbour, const spuma_scalar* face_weights,
+                                       int n_coarsest, int max_levels, int max_out, int* n_levels,
+                                       int* level_cells, int* level_faces, spuma_label* ftc)
+{
+    std::vector<int> o, nb, os, ls, lo, olo;
+    SPUMA_TRY(host_addressing(n_cells, n_faces, owner, neighbour, o, nb, os, ls, lo, olo));
+    if (!n_levels || (n_faces > 0 && !face_weights) || max_levels < 1)
+        return set_error(SPUMA_ERR_INVALID_ARGUMENT, "NULL argument / max_levels < 1");
+    std::vector<double> w(face_weights, face_weights + n_faces);
+    const std::vector<GamgHostLevel> H = gamg_hierarchy(n_cells, n_faces, o, nb, os, ls, lo, olo, w, n_coarsest,
+                                                        max_levels);
+    *n_levels = (int)H.size();
+    size_t off = 0;
+    for (int l = 0; l < (int)H.size(); ++l) {
+        if (l < max_out) {
+            if (level_cells) level_cells[l] = H[l].n;
+            if (level_faces) level_faces[l] = H[l].F;
+        }
+        if (ftc && l + 1 < (int)H.size()) {  // concatenated fine-to-coarse maps of every level but the coarsest
+            std::memcpy(ftc + off, H[l].ftc.data(), sizeof(int) * H[l].ftc.size());
+            off += H[l].ftc.size();
+        }
+    }
+    return SPUMA_OK;
+}
+
+spuma_status spuma_host_level_schedule(int n_cells, int n_faces, const spuma_label* owner,
+                                       const spuma_label* neighbour, spuma_label* order_f, spuma_label* order_b,
+                                       int* depth_f, int* depth_b)
+{
+    std::vector<int> o, nb, os, ls, lo, olo;
+    SPUMA_TRY(host_addressing(n_cells, n_faces, owner, neighbour, o, nb, os, ls, lo, olo));
+    if (!order_f || !order_b || !depth_f || !depth_b) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "NULL argument");
+    std::vector<int> of, ob;
+    int wf, wb;
+    level_schedule(n_cells, o, nb, os, ls, lo, of, ob, *depth_f, *depth_b, wf, wb);
+    std::memcpy(order_f, of.data(), sizeof(int) * of.size());
+    std::memcpy(order_b, ob.data(), sizeof(int) * ob.size());
+    return SPUMA_OK;
+}
+
+spuma_status spuma_host_ldu_to_csr(int n_cells, int n_faces, const spuma_label* owner, const spuma_label* neighbour,
+                                   spuma_label* row_ptr, spuma_label* col, spuma_label* map)
+{
+    std::vector<int> o, nb, os, ls, lo, olo;
+    SPUMA_TRY(host_addressing(n_cells, n_faces, owner, neighbour, o, nb, os, ls, lo, olo));
+    if (!row_ptr || !col || !map) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "NULL argument");
+    std::vector<int> rp, cl, mp;
+    ldu_to_csr_host(n_cells, n_faces, o, nb, os, ls, lo, rp, cl, mp);
+    std::memcpy(row_ptr, rp.data(), sizeof(int) * rp.size());
+    std::memcpy(col, cl.data(), sizeof(int) * cl.size());
+    std::memcpy(map, mp.data(), sizeof(int) * mp.size());
     return SPUMA_OK;
 }
 

@@ -29,6 +29,21 @@ SellHost build_sell(int N, const std::vector<int>& ownerStart, const std::vector
 void cell_lists(int N, const std::vector<int>& cell_of, const std::vector<char>& keep, std::vector<int>& start,
                 std::vector<int>& items);
 
+// Dependency levels of the DIC/DILU recurrences (§8(f3)/(f4)): forward row c waits on the owners
+// of its neighbour-side faces, backward row c on the neighbours of its owner-side faces.  order_*
+// = rows sorted by level (ascending cell within a level); depth = number of levels; width = the
+// widest level.
+void level_schedule(int N, const std::vector<int>& owner, const std::vector<int>& neighbour,
+                    const std::vector<int>& ownerStart, const std::vector<int>& losortStart,
+                    const std::vector<int>& losort, std::vector<int>& order_f, std::vector<int>& order_b,
+                    int& depth_f, int& depth_b, int& width_f, int& width_b);
+// LDU -> CSR (Q34): per row the neighbour-side faces in losort order (owners ascending), the
+// diagonal, the owner-side faces; map into [diag (N) | upper (F) | lower (F)].
+void ldu_to_csr_host(int N, int F, const std::vector<int>& owner, const std::vector<int>& neighbour,
+                     const std::vector<int>& ownerStart, const std::vector<int>& losortStart,
+                     const std::vector<int>& losort, std::vector<int>& row_ptr, std::vector<int>& col,
+                     std::vector<int>& map);
+
 // GAMG hierarchy (readings Q22, Q27).  Level l's arrays; ftc and the
 // next level's agglomeration lists are empty on the coarsest level.
 struct GamgHostLevel {

@@ -206,4 +206,55 @@ SellHost build_sell(int N, const std::vector<int>& ownerStart, const std::vector
     return S;
 }
 
+void level_schedule(int N, const std::vector<int>& owner, const std::vector<int>& neighbour,
+                    const std::vector<int>& ownerStart, const std::vector<int>& losortStart,
+                    const std::vector<int>& losort, std::vector<int>& order_f, std::vector<int>& order_b,
+                    int& depth_f, int& depth_b, int& width_f, int& width_b)
+{
+    std::vector<int> lf(N, 0), lb(N, 0);
+    for (int c = 0; c < N; ++c)
+        for (int k = losortStart[c]; k < losortStart[c + 1]; ++k) lf[c] = std::max(lf[c], lf[owner[losort[k]]] + 1);
+    for (int c = N - 1; c >= 0; --c)
+        for (int f = ownerStart[c]; f < ownerStart[c + 1]; ++f) lb[c] = std::max(lb[c], lb[neighbour[f]] + 1);
+    auto order_by = [N](const std::vector<int>& lev, std::vector<int>& ord, int& depth, int& width) {
+        depth = 0;
+        for (int c = 0; c < N; ++c) depth = std::max(depth, lev[c] + 1);
+        std::vector<int> start(depth + 1, 0);
+        for (int c = 0; c < N; ++c) start[lev[c] + 1]++;
+        width = 0;
+        for (int d = 0; d < depth; ++d) width = std::max(width, start[d + 1]);
+        for (int d = 0; d < depth; ++d) start[d + 1] += start[d];
+        ord.assign(N, 0);
+        for (int c = 0; c < N; ++c) ord[start[lev[c]]++] = c;
+    };
+    order_by(lf, order_f, depth_f, width_f);
+    order_by(lb, order_b, depth_b, width_b);
+}
+
+void ldu_to_csr_host(int N, int F, const std::vector<int>& owner, const std::vector<int>& neighbour,
+                     const std::vector<int>& ownerStart, const std::vector<int>& losortStart,
+                     const std::vector<int>& losort, std::vector<int>& row_ptr, std::vector<int>& col,
+                     std::vector<int>& map)
+{
+    const int nnz = N + 2 * F;
+    row_ptr.assign(N + 1, 0);
+    col.assign(nnz, 0);
+    map.assign(nnz, 0);
+    int k = 0;
+    for (int c = 0; c < N; ++c) {
+        for (int j = losortStart[c]; j < losortStart[c + 1]; ++j) {
+            const int f = losort[j];
+            col[k] = owner[f];
+            map[k++] = N + F + f;
+        }
+        col[k] = c;
+        map[k++] = c;
+        for (int f = ownerStart[c]; f < ownerStart[c + 1]; ++f) {
+            col[k] = neighbour[f];
+            map[k++] = N + f;
+        }
+        row_ptr[c + 1] = k;
+    }
+}
+
 }  // namespace spuma

@@ -165,6 +165,11 @@ def lib():
             L.spuma_amul_asym.argtypes = [_vp] * 6 + [_ci]
             L.spuma_ldu_to_csr.argtypes = [_vp] * 4
             L.spuma_csr_values.argtypes = [_vp] * 5
+        if hasattr(L, "spuma_host_rcm"):
+            L.spuma_host_rcm.argtypes = [_ci, _ci, _vp, _vp, _vp]
+            L.spuma_host_gamg_hierarchy.argtypes = [_ci, _ci, _vp, _vp, _vp, _ci, _ci, _ci, _vp, _vp, _vp, _vp]
+            L.spuma_host_level_schedule.argtypes = [_ci, _ci, _vp, _vp, _vp, _vp, _vp, _vp]
+            L.spuma_host_ldu_to_csr.argtypes = [_ci, _ci] + [_vp] * 5
         L.spuma_last_error.restype = ctypes.c_char_p
         L.spuma_abi_version.restype = _ci
         for name in ("spuma_mesh_create", "spuma_assemble_laplacian", "spuma_pcg_solve", "spuma_amul",
@@ -526,3 +531,57 @@ class Mesh:
 
 
 mesh_create = Mesh.mesh_create
+
+
+# ---------------------------------------------------------------- host-only diagnostics (no device)
+def _addr(owner, neighbour):
+    return np.ascontiguousarray(owner, np.int32), np.ascontiguousarray(neighbour, np.int32)
+
+
+def host_rcm(n_cells: int, owner, neighbour) -> np.ndarray:
+    """spuma_host_rcm: the RCM permutation libspuma applies with renumber = 1 (perm[old] = new)."""
+    o, nb = _addr(owner, neighbour)
+    perm = np.zeros(max(n_cells, 1), np.int32)
+    _check(lib().spuma_host_rcm(n_cells, o.shape[0], o.ctypes.data, nb.ctypes.data, perm.ctypes.data))
+    return perm[:n_cells]
+
+
+def host_gamg_hierarchy(n_cells: int, owner, neighbour, face_weights, n_coarsest=10, max_levels=50) -> dict:
+    """spuma_host_gamg_hierarchy: level sizes and the fine-to-coarse maps libspuma builds."""
+    o, nb = _addr(owner, neighbour)
+    w = np.ascontiguousarray(face_weights, np.float64)
+    nl = ctypes.c_int(0)
+    cells, faces = np.zeros(64, np.int32), np.zeros(64, np.int32)
+    _check(lib().spuma_host_gamg_hierarchy(n_cells, o.shape[0], o.ctypes.data, nb.ctypes.data, w.ctypes.data,
+                                           n_coarsest, max_levels, 64, ctypes.addressof(nl), cells.ctypes.data,
+                                           faces.ctypes.data, None))
+    n = nl.value
+    ftc = np.zeros(max(int(cells[:n - 1].sum()), 1), np.int32)
+    _check(lib().spuma_host_gamg_hierarchy(n_cells, o.shape[0], o.ctypes.data, nb.ctypes.data, w.ctypes.data,
+                                           n_coarsest, max_levels, 64, ctypes.addressof(nl), None, None,
+                                           ftc.ctypes.data))
+    maps, off = [], 0
+    for k in range(n - 1):
+        maps.append(ftc[off:off + cells[k]].copy())
+        off += int(cells[k])
+    return {"levels": n, "cells": cells[:n].tolist(), "faces": faces[:n].tolist(), "ftc": maps}
+
+
+def host_level_schedule(n_cells: int, owner, neighbour):
+    """spuma_host_level_schedule: (order_f, order_b, depth_f, depth_b) of the DIC/DILU sweeps."""
+    o, nb = _addr(owner, neighbour)
+    of, ob = np.zeros(max(n_cells, 1), np.int32), np.zeros(max(n_cells, 1), np.int32)
+    df, db = ctypes.c_int(0), ctypes.c_int(0)
+    _check(lib().spuma_host_level_schedule(n_cells, o.shape[0], o.ctypes.data, nb.ctypes.data, of.ctypes.data,
+                                           ob.ctypes.data, ctypes.addressof(df), ctypes.addressof(db)))
+    return of[:n_cells], ob[:n_cells], df.value, db.value
+
+
+def host_ldu_to_csr(n_cells: int, owner, neighbour):
+    """spuma_host_ldu_to_csr: (row_ptr, col, map into [diag | upper | lower])."""
+    o, nb = _addr(owner, neighbour)
+    nnz = n_cells + 2 * o.shape[0]
+    rp, col, mp = np.zeros(n_cells + 1, np.int32), np.zeros(max(nnz, 1), np.int32), np.zeros(max(nnz, 1), np.int32)
+    _check(lib().spuma_host_ldu_to_csr(n_cells, o.shape[0], o.ctypes.data, nb.ctypes.data, rp.ctypes.data,
+                                       col.ctypes.data, mp.ctypes.data))
+    return rp, col[:nnz], mp[:nnz]

@@ -1,0 +1,67 @@
+"""libspuma's host logic on the CPU (no device): the product's own C++ (csrc/mesh_host.cpp,
+csrc/gamg_host.cpp) through the host-only C-ABI, checked against the oracle (bit-exact integer
+work): RCM (Q12), the GAMG hierarchy (Q22), the DIC/DILU dependency schedules, LDU -> CSR (Q34)."""
+import numpy as np
+import pytest
+
+import gen
+import oracle as O
+from paper_2512_22215_b200 import spuma as S
+
+MESHES = [("cube9", lambda: gen.cube(9)), ("perturbed-permuted", lambda: gen.permute(gen.perturbed(8, 0.25), seed=3)),
+          ("cavity", lambda: gen.cavity2d(13)), ("box-ragged", lambda: gen.box(11, 6, 5, (1.0, 0.7, 0.3))),
+          ("cube16", lambda: gen.cube(16))]
+
+
+@pytest.mark.parametrize("name,make", MESHES)
+def test_host_rcm_matches_oracle(name, make):
+    m = make()
+    assert np.array_equal(S.host_rcm(m.n_cells, m.owner, m.neighbour), O.rcm(m.n_cells, m.owner, m.neighbour))
+
+
+@pytest.mark.parametrize("params", [dict(), dict(n_coarsest=40), dict(max_levels=3)])
+@pytest.mark.parametrize("name,make", MESHES)
+def test_host_gamg_hierarchy_matches_oracle(name, make, params):
+    m = make()
+    hh = S.host_gamg_hierarchy(m.n_cells, m.owner, m.neighbour, m.magSf, params.get("n_coarsest", 10),
+                               params.get("max_levels", 50))
+    ho = O.gamg_hierarchy(m, O.gamg_params(n_coarsest_cells=params.get("n_coarsest", 10),
+                                           max_levels=params.get("max_levels", 50)))
+    assert hh["levels"] == len(ho)
+    assert hh["cells"] == [lv[0] for lv in ho]
+    assert hh["faces"][1:] == [int(lv[1].shape[0]) for lv in ho[1:]]
+    for k in range(len(ho) - 1):
+        assert np.array_equal(hh["ftc"][k], ho[k][3]), k
+
+
+@pytest.mark.parametrize("name,make", MESHES)
+def test_host_level_schedule_is_a_valid_topological_order(name, make):
+    """Every row comes after the rows its forward (resp. backward) recurrence reads; the depth is
+    the longest dependency chain (1 + max over dependencies, computed here independently)."""
+    m = make()
+    of, ob, df, db = S.host_level_schedule(m.n_cells, m.owner, m.neighbour)
+    assert sorted(of.tolist()) == list(range(m.n_cells)) and sorted(ob.tolist()) == list(range(m.n_cells))
+    pos_f, pos_b = np.empty(m.n_cells, int), np.empty(m.n_cells, int)
+    pos_f[of] = np.arange(m.n_cells)
+    pos_b[ob] = np.arange(m.n_cells)
+    assert np.all(pos_f[m.owner] < pos_f[m.neighbour])   # forward: row neighbour reads row owner
+    assert np.all(pos_b[m.neighbour] < pos_b[m.owner])   # backward: row owner reads row neighbour
+    lev = np.zeros(m.n_cells, int)
+    for f in np.argsort(m.neighbour, kind="stable"):
+        lev[m.neighbour[f]] = max(lev[m.neighbour[f]], lev[m.owner[f]] + 1)
+    assert df == lev.max() + 1
+
+
+@pytest.mark.parametrize("name,make", MESHES)
+def test_host_ldu_to_csr_matches_oracle(name, make):
+    m = make()
+    rp, col, mp = S.host_ldu_to_csr(m.n_cells, m.owner, m.neighbour)
+    orp, ocol, omp = O.ldu_to_csr(m.n_cells, m.owner, m.neighbour)
+    assert np.array_equal(rp, orp) and np.array_equal(col, ocol) and np.array_equal(mp, omp)
+
+
+def test_host_functions_reject_bad_addressing():
+    with pytest.raises(S.SpumaError):
+        S.host_rcm(3, np.array([1], np.int32), np.array([0], np.int32))  # owner > neighbour
+    with pytest.raises(S.SpumaError):
+        S.host_ldu_to_csr(2, np.array([0, 0], np.int32), np.array([1, 1], np.int32)[::-1].copy() * 5)
