@@ -420,7 +420,12 @@ typedef enum {
      * down to the coarsest run in ONE single-CTA kernel per V-cycle (Richardson, scaled
      * correction, nPre = 0); default 1024 (same-box A/B: 256-1024 best, 4096+ slower); 0 = one
      * launch per level and step */
-    SPUMA_OPT_GAMG_TAIL_CELLS = 4
+    SPUMA_OPT_GAMG_TAIL_CELLS = 4,
+    /* PCG hot loop: form the direction pA = rD rA + beta pA inside the Amul gather instead of
+     * a separate pass (single rank, deferred psi, ELL layout; bitwise the same iterates).
+     * 0 = separate k_direction (default: measured faster); 1 = fused, rD read;
+     * 2 = fused, rD = 1/diag in place */
+    SPUMA_OPT_FUSE_DIRECTION = 5
 } spuma_option;
 spuma_status spuma_set_option(spuma_mesh m, int option, int value);
 

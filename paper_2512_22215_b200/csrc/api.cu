@@ -327,6 +327,19 @@ spuma_status enqueue_iteration(spuma_mesh m, cudaStream_t s, std::vector<cudaEve
     }
     const int rv = resolve_amul_variant(m->amul_variant, a);
     const bool overlap = !fin && m->n_iface > 0 && rv >= 6 && rv <= 9;
+    if (fin && m->defer_psi && m->fuse_direction && rv == 8 && fused_direction_ok(a)) {
+        // direction formed inside the Amul gather (one pass less per iteration)
+        if (ev) record(m, *ev, slot * 6 + 0, s);
+        if (ev) record(m, *ev, slot * 6 + 1, s);
+        if (ev) record(m, *ev, slot * 6 + 2, s);
+        launch_amul_dot_dir(s, a, ws, m->fuse_direction == 2);
+        if (ev) record(m, *ev, slot * 6 + 3, s);
+        if (ev) record(m, *ev, slot * 6 + 4, s);
+        launch_update(s, m->grid, a, ws, fin, psi_mode);
+        if (ev) record(m, *ev, slot * 6 + 5, s);
+        m->stats.kernel_launches += 2;
+        return SPUMA_OK;
+    }
     if (ev) record(m, *ev, slot * 6 + 0, s);
     launch_direction(s, m->grid, a, ws);
     if (ev) record(m, *ev, slot * 6 + 1, s);
@@ -1653,6 +1666,11 @@ spuma_status spuma_set_option(spuma_mesh m, int option, int value)
 {
     if (!m) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "mesh is NULL");
     switch (option) {
+    case SPUMA_OPT_FUSE_DIRECTION:
+        if (value < 0 || value > 2) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "fuse_direction is 0, 1 or 2");
+        if (m->fuse_direction != value) destroy_graphs(m);
+        m->fuse_direction = value;
+        return SPUMA_OK;
     case SPUMA_OPT_GAMG_TAIL_CELLS:
         if (value < 0) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "negative GAMG tail size");
         m->gamg_tail_cells = value;  // the captured V-cycle is re-captured at the next solve

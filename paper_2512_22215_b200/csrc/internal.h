@@ -170,6 +170,7 @@ struct spuma_mesh_s {
     int amul_variant = 8;
     bool defer_psi = true;  // psi += alpha pA applied every second iteration (same rounding, fewer bytes)  // ELL + coefficient copy (falls back to 6 -> 5 when the mesh is not uniform)
     bool timing = false;
+    int fuse_direction = 0;      // 0: k_direction + k_amul_dot (default: faster); 1: fused, rD read; 2: fused, 1/diag inline
     int gamg_tail_cells = 1024;  // GAMG: levels from the first one at or below this size run in one CTA (0: off)
     cudaGraphExec_t gexec[2] = {nullptr, nullptr};
     bool gexec_timed = false;
@@ -271,7 +272,10 @@ void launch_scatter_signed(cudaStream_t s, int n, const int* idx, const signed c
 constexpr int kPad = 8;  // padding elements on internal arrays (16-byte TMA windows may overrun by <= 3)
 void launch_update(cudaStream_t s, int grid, const MeshArgs& a, const Workspace& w, bool fin, int psi_mode = 0);
 // psi_mode: 0 psi += alpha pA; 1 defer (psi untouched); 2 psi = (psi + alpha_prev pA_prev) + alpha pA
-void launch_psi_flush(cudaStream_t s, int N, const Workspace& w);  // psi += alpha_prev pA (pending update)
+void launch_psi_flush(cudaStream_t s, int N, const Workspace& w);
+// A11+A7+A8 in one kernel (ELL, single rank, deferred psi): see kernels.cu
+bool fused_direction_ok(const MeshArgs& a);
+void launch_amul_dot_dir(cudaStream_t s, const MeshArgs& a, const Workspace& w, bool inline_rd);  // psi += alpha_prev pA (pending update)
 // P > 1: finalise from the gathered rank partials ([n_ranks][4], rank order)
 void launch_finalize(cudaStream_t s, int stage, const double* gathered, int n_ranks, const Workspace& w);
 void launch_scal_init(cudaStream_t s, const Workspace& w, const spuma_solver_controls& c, int n_ranks);

@@ -476,6 +476,75 @@ __global__ void __launch_bounds__(V == 3 ? tma::kBlock : kThreads, amul_min_ctas
     }
 }
 
+// A11 + A7 + A8 fused (ELL, single rank, deferred psi => pA / pA_prev are distinct buffers):
+// the direction pA = rD rA + beta pA_prev (n == 0: rD rA) is formed for the row AND at its
+// neighbours inside the Amul gather, written once for the row, and wA = A pA, wA.pA -> alpha.
+// The separate k_direction pass (32 B/cell) disappears.  INL: rD = 1/diag computed in place
+// (diag is streamed anyway; IEEE division: bitwise the stored rD), else read rD.  Same values
+// in the same order as k_direction + k_amul_dot<8> on the same grid: bitwise the same iterates.
+template <bool INL>
+__global__ void __launch_bounds__(kThreads, amul_min_ctas<8>()) k_amul_dot_dir(MeshArgs a, Workspace w)
+{
+    pdl_wait();
+    if (w.scal->done) return;
+    const DevPtrs p = *w.ptrs;
+    const bool first = w.scal->n == 0;
+    const double beta = w.scal->beta;
+    const double* __restrict__ diag = p.diag;
+    const double* __restrict__ rD = w.rD;
+    const double* __restrict__ rA = w.rA;
+    const double* __restrict__ pprev = w.pA_prev;
+    auto P = [&](int j) -> double {
+        const double rd = INL ? 1.0 / __ldg(diag + j) : __ldg(rD + j);
+        return first ? rd * __ldg(rA + j) : rd * __ldg(rA + j) + beta * __ldg(pprev + j);
+    };
+    constexpr int W = 3;
+    const int wn = a.ell_wn, wo = a.ell_wo;
+    double acc = 0.0;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int t0 = (blockIdx.x * (kThreads / 32) + warp) * 32; t0 < a.N; t0 += gridDim.x * kThreads) {
+        const int c0 = t0 + lane;
+        const int c = min(c0, a.N - 1);
+        const int k = c >> 5;
+        unsigned pk[W];
+        int nb[W];
+        double uo[W], un[W];
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+            pk[j] = j < wn ? __ldg(a.sell_n + (size_t)32 * wn * k + 32 * j + lane) : 0xFFFFFFFFu;
+            nb[j] = j < wo ? __ldg(a.sell_o + (size_t)32 * wo * k + 32 * j + lane) : -1;
+            uo[j] = j < wo ? __ldg(a.upper_s + (size_t)32 * wo * k + 32 * j + lane) : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+            const int col = (int)(pk[j] >> 5), pos = (int)(pk[j] & 31u);
+            un[j] = pk[j] != 0xFFFFFFFFu ? __ldg(a.upper_s + (size_t)32 * wo * (col >> 5) + 32 * pos + (col & 31)) : 0.0;
+        }
+        const double xc = P(c);
+        double xn[W], xo[W];
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+            xn[j] = P(pk[j] != 0xFFFFFFFFu ? (int)(pk[j] >> 5) : c);
+            xo[j] = P(nb[j] >= 0 ? nb[j] : c);
+        }
+        double sum = __ldg(diag + c) * xc;
+#pragma unroll
+        for (int j = 0; j < W; ++j)
+            if (pk[j] != 0xFFFFFFFFu) sum = sum + un[j] * xn[j];
+#pragma unroll
+        for (int j = 0; j < W; ++j)
+            if (nb[j] >= 0) sum = sum + uo[j] * xo[j];
+        if (c0 < a.N) {
+            w.pA[c] = xc;
+            w.wA[c] = sum;
+            acc += sum * xc;
+        }
+    }
+    double v[1] = {acc};
+    pdl_trigger();
+    if (grid_sum<1>(v, w.part, &w.scal->ticket[2]) && threadIdx.x == 0) finalize(w.scal, 3, v);
+}
+
 // A9 + A10: psi += alpha pA; rA -= alpha wA; partials (rD rA) rA and |rA|
 // psi_mode 0: psi += alpha pA; 1: psi left for the next iteration (deferred); 2: the
 // deferred pair, psi = (psi + alpha_prev pA_prev) + alpha pA -- the same two roundings as
@@ -1100,6 +1169,18 @@ void launch_amul_dot(cudaStream_t s, int variant, const MeshArgs& a, const Works
         break;
     default: launch_hot(k_amul_dot<0>, grid_for(k_amul_dot<0>, a.N), kThreads, s, a, w, f, sell_wn, sell_wo); break;
     }
+}
+
+bool fused_direction_ok(const MeshArgs& a)
+{
+    return a.ell_wn >= 0 && a.ell_wn <= 3 && a.ell_wo >= 0 && a.ell_wo <= 3 && a.upper_s && a.sell_n && !a.ifMask;
+}
+
+void launch_amul_dot_dir(cudaStream_t s, const MeshArgs& a, const Workspace& w, bool inline_rd)
+{
+    const int g = grid_for(k_amul_dot<8>, a.N);  // the unfused kernel's grid: same reduction shape
+    if (inline_rd) launch_hot(k_amul_dot_dir<true>, g, kThreads, s, a, w);
+    else launch_hot(k_amul_dot_dir<false>, g, kThreads, s, a, w);
 }
 
 void launch_update(cudaStream_t s, int grid, const MeshArgs& a, const Workspace& w, bool fin, int psi_mode)

@@ -461,3 +461,18 @@ def test_deferred_psi_updates_are_bitwise_neutral(iters):
         out.append(gpu_solve_case(m, g, b, 0, ctl, handle=h)[:2])
     assert out[0][1] == out[1][1]
     assert np.array_equal(out[0][0], out[1][0])
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+def test_fused_direction_is_bitwise_neutral(mode):
+    """SPUMA_OPT_FUSE_DIRECTION: the direction formed inside the Amul gather gives bitwise the
+    iterates of the separate k_direction pass (same values, same order, same reduction grid)."""
+    m = gen.perturbed(20, 0.15)
+    g, b = gen.gamma_lognormal(m), gen.rhs(m)
+    h = P.Mesh.from_mesh(m)
+    res = []
+    for fm in (0, mode):
+        h.set_option(P.spuma.OPT_FUSE_DIRECTION, fm)
+        psi, perf, _, _ = gpu_solve_case(m, g, b, 0, (1e-8, 0.0, 5000, 0), handle=h)
+        res.append((psi, perf))
+    assert res[0][1] == res[1][1] and np.array_equal(res[0][0], res[1][0])
