@@ -467,7 +467,7 @@ def test_deferred_psi_updates_are_bitwise_neutral(iters):
 def test_fused_direction_is_bitwise_neutral(mode):
     """SPUMA_OPT_FUSE_DIRECTION: the direction formed inside the Amul gather gives bitwise the
     iterates of the separate k_direction pass (same values, same order, same reduction grid)."""
-    m = gen.perturbed(20, 0.15)
+    m = gen.perturbed(24, 0.15)  # 13824 cells: above the single-CTA threshold, ELL layout
     g, b = gen.gamma_lognormal(m), gen.rhs(m)
     h = P.Mesh.from_mesh(m)
     res = []
