@@ -862,6 +862,18 @@ void pc_apply(spuma_mesh m, const spuma_preconditioner& pc, const double* u, con
                             scal, P->width_f, P->width_b);
 }
 
+// the sweeps' deadlock guard (flag[N], precond.cu): read and clear after a solve
+spuma_status pc_guard(spuma_mesh m)
+{
+    int err = 0;
+    SPUMA_CUDA(cudaMemcpy(&err, m->pc->flag + m->N, sizeof(int), cudaMemcpyDeviceToHost));
+    if (err) {
+        SPUMA_CUDA(cudaMemset(m->pc->flag + m->N, 0, sizeof(int)));
+        return set_error(SPUMA_ERR_STATE, "DIC/DILU sweep: a dependency never became ready (deadlock guard)");
+    }
+    return SPUMA_OK;
+}
+
 uint64_t pc_launches(const spuma_preconditioner& pc)
 {
     if (pc.kind == SPUMA_PC_DIAGONAL) return 1;
@@ -1914,6 +1926,7 @@ spuma_status spuma_pcg_solve_pc(spuma_mesh m, const spuma_scalar* diag, const sp
         if (it > ctl->max_iter + 16) return set_error(SPUMA_ERR_STATE, "PCG loop did not terminate");
     }
     SPUMA_CUDA(cudaGetLastError());
+    SPUMA_TRY(pc_guard(m));
     const DevScal fs = m->h_scal[0];
     perf->initial_residual = fs.init;
     perf->final_residual = fs.fin;
@@ -1977,6 +1990,7 @@ spuma_status spuma_pbicg_solve(spuma_mesh m, const spuma_scalar* diag, const spu
         if (it > ctl->max_iter + 16) return set_error(SPUMA_ERR_STATE, "PBiCG loop did not terminate");
     }
     SPUMA_CUDA(cudaGetLastError());
+    SPUMA_TRY(pc_guard(m));
     const DevScal fs = m->h_scal[0];
     perf->initial_residual = fs.init;
     perf->final_residual = fs.fin;
@@ -2009,6 +2023,8 @@ spuma_status spuma_precondition(spuma_mesh m, const spuma_scalar* diag, const sp
     if (!m->d_cell_t) SPUMA_TRY(dalloc(&m->d_cell_t, m->N));
     pc_apply(m, *pcp, u_i, l_i, r_i, m->d_cell_t, transpose != 0, nullptr);
     m->stats.kernel_launches += 2 + pc_launches(*pcp);
+    SPUMA_CUDA(cudaStreamSynchronize(s));
+    SPUMA_TRY(pc_guard(m));
     SPUMA_TRY(cells_out(m, wout, m->d_cell_t));
     SPUMA_CUDA(cudaStreamSynchronize(s));
     SPUMA_CUDA(cudaGetLastError());

@@ -25,21 +25,31 @@ __device__ __forceinline__ void st_release(int* p, int v)
 {
     asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-__device__ __forceinline__ void wait_ready(const int* flag, int j)
+// Deadlock guard: a dependency that never arrives (a corrupted schedule) must not hang the GPU.
+// After kSpinLimit polls (~2 s with the back-off) the row gives up, raises flag[N] (the error
+// word past the row flags, read by the host after the solve) and continues.
+constexpr unsigned kSpinLimit = 1u << 22;
+__device__ __forceinline__ void spin_fail(int* err) { atomicExch(err, 1); }
+
+__device__ __forceinline__ void wait_ready(const int* flag, int j, int* err)
 {
     if (ld_acquire(flag + j)) return;
-    unsigned ns = 32;
+    unsigned ns = 32, polls = 0;
     while (!ld_acquire(flag + j)) {  // back off: keep the L2 free for the rows that can progress
         __nanosleep(ns);
         ns = ns < 512 ? 2 * ns : 512;
+        if (++polls > kSpinLimit) {
+            spin_fail(err);
+            return;
+        }
     }
 }
 
 // wait until the flags of all n (<= kDep) dependencies are set: all polls in flight at once
 constexpr int kDep = 8;
-__device__ __forceinline__ void wait_all(const int* flag, const int* js, int n)
+__device__ __forceinline__ void wait_all(const int* flag, const int* js, int n, int* err)
 {
-    unsigned ns = 32;
+    unsigned ns = 32, polls = 0;
     for (;;) {
         bool ok = true;
 #pragma unroll
@@ -48,6 +58,10 @@ __device__ __forceinline__ void wait_all(const int* flag, const int* js, int n)
         if (ok) return;
         __nanosleep(ns);
         ns = ns < 512 ? 2 * ns : 512;
+        if (++polls > kSpinLimit) {
+            spin_fail(err);
+            return;
+        }
     }
 }
 
@@ -82,7 +96,7 @@ __global__ void __launch_bounds__(kThreads) k_ilu_factor(MeshArgs a, const int* 
                 js[d] = a.ownerLo[k0 + d];
                 cf[d] = upper[f] * lower[f];
             }
-        wait_all(flag, js, nd < kDep ? nd : kDep);
+        wait_all(flag, js, nd < kDep ? nd : kDep, flag + a.N);
 #pragma unroll
         for (int d = 0; d < kDep; ++d)
             if (d < nd) v[d] = __ldcg(raw + js[d]);
@@ -92,7 +106,7 @@ __global__ void __launch_bounds__(kThreads) k_ilu_factor(MeshArgs a, const int* 
             if (d < nd) t = t - cf[d] / v[d];
         for (int k = k0 + kDep; k < k0 + nd; ++k) {  // rows with more than kDep lower faces
             const int j = a.ownerLo[k], f = a.losort[k];
-            wait_ready(flag, j);
+            wait_ready(flag, j, flag + a.N);
             t = t - upper[f] * lower[f] / __ldcg(raw + j);
         }
         __stcg(raw + c, t);
@@ -129,7 +143,7 @@ __global__ void __launch_bounds__(kThreads) k_ilu_fwd(MeshArgs a, const int* __r
                 cf[d] = rd * lo[a.losort[k0 + d]];
             }
         double t = rd * r[c];
-        wait_all(flag, js, nd < kDep ? nd : kDep);
+        wait_all(flag, js, nd < kDep ? nd : kDep, flag + a.N);
 #pragma unroll
         for (int d = 0; d < kDep; ++d)
             if (d < nd) v[d] = __ldcg(w + js[d]);
@@ -138,7 +152,7 @@ __global__ void __launch_bounds__(kThreads) k_ilu_fwd(MeshArgs a, const int* __r
             if (d < nd) t = t - cf[d] * v[d];
         for (int k = k0 + kDep; k < k0 + nd; ++k) {
             const int j = a.ownerLo[k];
-            wait_ready(flag, j);
+            wait_ready(flag, j, flag + a.N);
             t = t - rd * lo[a.losort[k]] * __ldcg(w + j);
         }
         __stcg(w + c, t);
@@ -169,7 +183,7 @@ __global__ void __launch_bounds__(kThreads) k_ilu_bwd(MeshArgs a, const int* __r
                 cf[d] = rd * up[f1 - d];
             }
         double t = __ldcg(w + c);
-        wait_all(flag, js, nd < kDep ? nd : kDep);
+        wait_all(flag, js, nd < kDep ? nd : kDep, flag + a.N);
 #pragma unroll
         for (int d = 0; d < kDep; ++d)
             if (d < nd) v[d] = __ldcg(w + js[d]);
@@ -178,7 +192,7 @@ __global__ void __launch_bounds__(kThreads) k_ilu_bwd(MeshArgs a, const int* __r
             if (d < nd) t = t - cf[d] * v[d];
         for (int f = f1 - kDep; f >= a.ownerStart[c]; --f) {
             const int j = a.neighbour[f];
-            wait_ready(flag, j);
+            wait_ready(flag, j, flag + a.N);
             t = t - rd * up[f] * __ldcg(w + j);
         }
         __stcg(w + c, t);
@@ -426,7 +440,7 @@ int pc_grid(int n) { return cell_grid(n); }
 void launch_ilu_factor(cudaStream_t s, const MeshArgs& a, const int* order, const double* diag, const double* upper,
                        const double* lower, double* raw, double* rD, int* flag, unsigned* counter, int width)
 {
-    cudaMemsetAsync(flag, 0, sizeof(int) * (a.N + 1), s);
+    cudaMemsetAsync(flag, 0, sizeof(int) * a.N, s);
     cudaMemsetAsync(counter, 0, sizeof(unsigned), s);
     k_ilu_factor<<<persistent_grid((const void*)k_ilu_factor, 2 * width), kThreads, 0, s>>>(a, order, diag, upper,
                                                                                            lower, raw, flag, counter);
@@ -442,11 +456,11 @@ void launch_ilu_precondition(cudaStream_t s, const MeshArgs& a, const int* order
     const double* lo = transpose ? upper : lower;
     const double* up = transpose ? lower : upper;
     if (k < 0) {
-        cudaMemsetAsync(flag, 0, sizeof(int) * (a.N + 1), s);
+        cudaMemsetAsync(flag, 0, sizeof(int) * a.N, s);
         cudaMemsetAsync(counter, 0, sizeof(unsigned), s);
         k_ilu_fwd<<<persistent_grid((const void*)k_ilu_fwd, 2 * width_f), kThreads, 0, s>>>(a, order_f, rD, lo, r, w,
                                                                                            flag, counter, scal);
-        cudaMemsetAsync(flag, 0, sizeof(int) * (a.N + 1), s);
+        cudaMemsetAsync(flag, 0, sizeof(int) * a.N, s);
         cudaMemsetAsync(counter, 0, sizeof(unsigned), s);
         k_ilu_bwd<<<persistent_grid((const void*)k_ilu_bwd, 2 * width_b), kThreads, 0, s>>>(a, order_b, rD, up, w,
                                                                                            flag, counter, scal);
