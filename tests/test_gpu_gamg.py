@@ -231,3 +231,19 @@ def test_single_cta_tail_on_off(name, make, tail):
         psi_g, _ = c.gpu((0.0, 0.0, 2, 2), gp)
         psi_o, _ = c.oracle((0.0, 0.0, 2, 2), gp)
         assert rel_l2(psi_g, psi_o) <= 1e-10, kw
+
+
+def test_large_one_cycle_and_hierarchy_100cubed():
+    """BASELINE-size parity (C2/C5 100^3, 1M cells, 18 levels): hierarchy bit-exact and two
+    V-cycles against the oracle (relative L2 <= 1e-11), gamma log-normal."""
+    m = gen.cube(100)
+    c = Case(m, gen.gamma_lognormal(m))
+    hg = c.h.gamg_hierarchy()
+    ho = O.gamg_hierarchy(m)
+    assert hg["cells"] == [lv[0] for lv in ho]
+    for k in range(len(ho) - 1):
+        assert np.array_equal(hg["ftc"][k], ho[k][3]), k
+    psi_g, pg = c.gpu((0.0, 0.0, 2, 2))
+    psi_o, po = c.oracle((0.0, 0.0, 2, 2))
+    assert pg["final_residual"] == pytest.approx(po["final_residual"], rel=1e-9)
+    assert rel_l2(psi_g, psi_o) <= 1e-11
