@@ -117,6 +117,8 @@ def _L():
             lib.or_restrict.argtypes = [ci, vp, vp, ci, vp]
             lib.or_gamg.argtypes = [ci, ci] + [vp] * 7 + [ctypes.POINTER(GamgParams), ctypes.POINTER(Controls),
                                                            ctypes.POINTER(Perf), vp, vp]
+            lib.or_pcg_dd_pc.argtypes = [ci, ctypes.POINTER(_Domain), ctypes.POINTER(Controls), ci, ci,
+                                         ctypes.POINTER(Perf)]
             lib.or_ilu_factor.argtypes = [ci, ci] + [vp] * 6
             lib.or_ilu_precondition.argtypes = [ci, ci] + [vp] * 7 + [ci, ci]
             lib.or_pcg_pc.argtypes = [ci, ci] + [vp] * 6 + [ctypes.POINTER(Controls), ci, ci, ctypes.POINTER(Perf)]
@@ -332,9 +334,10 @@ def pcg(mesh: gen.Mesh, sys: LduSystem, psi0=None, ctl: Optional[Controls] = Non
 
 
 def pcg_decomposed(meshes: Sequence[gen.Mesh], systems: Sequence[LduSystem], psi0=None,
-                   ctl: Optional[Controls] = None):
+                   ctl: Optional[Controls] = None, kind: int = 0, k: int = 2):
     """O8: PCG over P sub-domains run sequentially; x_remote copied between
-    domains before every Amul; global sums in rank order."""
+    domains before every Amul; global sums in rank order.  kind != 0: the O12 preconditioner
+    applied per domain on its own faces (processor-local, Q31)."""
     ctl = ctl or controls()
     P = len(meshes)
     keep = []
@@ -367,7 +370,10 @@ def pcg_decomposed(meshes: Sequence[gen.Mesh], systems: Sequence[LduSystem], psi
         d.n_iface = ic.shape[0]
         d.iface_cells, d.iface_coeffs, d.iface_src_domain, d.iface_src_cell = [_p(a) for a in arrs[5:]]
     perf = Perf()
-    rc = _L().or_pcg(P, doms, ctypes.byref(ctl), ctypes.byref(perf))
+    if kind:
+        rc = _L().or_pcg_dd_pc(P, doms, ctypes.byref(ctl), int(kind), int(k), ctypes.byref(perf))
+    else:
+        rc = _L().or_pcg(P, doms, ctypes.byref(ctl), ctypes.byref(perf))
     if rc:
         raise MemoryError("or_pcg")
     return psis, perf.as_dict()

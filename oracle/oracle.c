@@ -577,7 +577,24 @@ static void or_dom_amul(int nd, or_domain* D, or_work* W, double* const* x, doub
                 D[p].n_iface, D[p].iface_cells, D[p].iface_coeffs, W[p].xr, y[p]);
 }
 
-int or_pcg(int nd, or_domain* D, const or_controls* ctl, or_perf* perf)
+static void or_pc_setup(int kind, int n, int F, const int* owner, const int* neighbour, const double* diag,
+                        const double* upper, const double* lower, double* rD);
+static void or_pc_apply(int kind, int k, int n, int F, const int* owner, const int* neighbour, const double* rD,
+                        const double* upper, const double* lower, const double* r, double* w, int transpose);
+
+/* PCG over nd domains (O6/O8) with the preconditioner `kind` (O12) applied per domain on its
+ * own faces: the processor-local factorisation OpenFOAM uses on decomposed meshes (Q31); kind 0
+ * (diagonal) is the A9 fused form rD rA. */
+static int or_pcg_impl(int nd, or_domain* D, const or_controls* ctl, int kind, int k, or_perf* perf);
+
+int or_pcg(int nd, or_domain* D, const or_controls* ctl, or_perf* perf) { return or_pcg_impl(nd, D, ctl, 0, 0, perf); }
+
+int or_pcg_dd_pc(int nd, or_domain* D, const or_controls* ctl, int kind, int k, or_perf* perf)
+{
+    return or_pcg_impl(nd, D, ctl, kind, k, perf);
+}
+
+static int or_pcg_impl(int nd, or_domain* D, const or_controls* ctl, int kind, int k, or_perf* perf)
 {
     or_work* W = (or_work*)calloc((size_t)nd, sizeof(or_work));
     double** X = (double**)malloc(sizeof(double*) * (size_t)nd);
@@ -633,19 +650,28 @@ int or_pcg(int nd, or_domain* D, const or_controls* ctl, or_perf* perf)
     perf->initial_residual = smag / normFactor;
     perf->final_residual = perf->initial_residual;
 
-    for (int p = 0; p < nd; ++p)
-        for (int c = 0; c < D[p].n_cells; ++c) W[p].rD[c] = 1.0 / D[p].diag[c];
+    for (int p = 0; p < nd; ++p) {
+        if (kind == 0) {
+            for (int c = 0; c < D[p].n_cells; ++c) W[p].rD[c] = 1.0 / D[p].diag[c];
+        } else {
+            or_pc_setup(kind, D[p].n_cells, D[p].n_faces, D[p].owner, D[p].neighbour, D[p].diag, D[p].upper,
+                        D[p].upper, W[p].rD);
+        }
+    }
 
     double wArA = 1e20, wArAold;
     if (ctl->min_iter > 0 || !or_conv(perf->final_residual, perf->initial_residual, ctl)) {
         do {
             wArAold = wArA;
-            /* precondition wA = rD rA ; wArA = gSumProd(wA, rA) */
+            /* precondition wA = M^-1 rA (per domain) ; wArA = gSumProd(wA, rA) */
             wArA = 0.0;
             for (int p = 0; p < nd; ++p) {
+                if (kind != 0)
+                    or_pc_apply(kind, k, D[p].n_cells, D[p].n_faces, D[p].owner, D[p].neighbour, W[p].rD,
+                                D[p].upper, D[p].upper, W[p].rA, W[p].wA, 0);
                 double s = 0.0;
                 for (int c = 0; c < D[p].n_cells; ++c) {
-                    W[p].wA[c] = W[p].rD[c] * W[p].rA[c];
+                    if (kind == 0) W[p].wA[c] = W[p].rD[c] * W[p].rA[c];
                     s += W[p].wA[c] * W[p].rA[c];
                 }
                 wArA += s;
