@@ -242,7 +242,8 @@ spuma_status spuma_gamg_get_hierarchy(spuma_mesh m, const spuma_gamg_params* par
  * as dependency-scheduled persistent kernels, bitwise equal to the sequential loops for any
  * numbering (their critical path is the mesh's dependency depth: a colour / wavefront
  * numbering makes them fast, the natural order of an n^3 box has depth ~3n).
- * All of these are single-rank (n_ranks > 1 -> SPUMA_ERR_STATE). */
+ * spuma_pcg_solve_pc runs on decomposed meshes too; the others are single-rank
+ * (n_ranks > 1 -> SPUMA_ERR_STATE). */
 typedef enum spuma_precond_kind {
     SPUMA_PC_DIAGONAL = 0,
     SPUMA_PC_DIC = 1,
@@ -258,12 +259,16 @@ typedef struct spuma_preconditioner {
 /*
  * PCG (Q1-Q4 semantics) with the preconditioner pc (NULL: diagonal): per iteration
  * wA = M^-1 rA, wArA = wA.rA, pA = wA + beta pA, wA = A pA, alpha = wArA / wA.pA, psi and rA
- * updated.  Arguments as spuma_pcg_solve (symmetric matrix: upper only).  Errors as
- * spuma_pcg_solve plus STATE (n_ranks > 1), INVALID_ARGUMENT (unknown kind, n_sweeps < 0).
+ * updated.  Arguments as spuma_pcg_solve (symmetric matrix: upper only; iface_coeffs as
+ * produced by spuma_assemble_laplacian when n_ranks > 1).  Multi-rank: collective; the
+ * preconditioner is factorised and applied on each rank's own faces (processor-local, as
+ * OpenFOAM on decomposed meshes, Q31), the Amul and the dot products are global.  Errors as
+ * spuma_pcg_solve plus INVALID_ARGUMENT (unknown kind, n_sweeps < 0).
  */
 spuma_status spuma_pcg_solve_pc(spuma_mesh m, const spuma_scalar* diag, const spuma_scalar* upper,
-                                const spuma_scalar* source, spuma_scalar* psi, const spuma_solver_controls* ctl,
-                                const spuma_preconditioner* pc, spuma_solver_perf* perf);
+                                const spuma_scalar* iface_coeffs, const spuma_scalar* source, spuma_scalar* psi,
+                                const spuma_solver_controls* ctl, const spuma_preconditioner* pc,
+                                spuma_solver_perf* perf);
 
 /*
  * PBiCG (Q32) for an asymmetric LDU matrix: lower [n_faces] is

@@ -831,9 +831,10 @@ spuma_status pair_in(spuma_mesh m, const double* u, const double* l, const doubl
     return SPUMA_OK;
 }
 
-spuma_status pc_check(spuma_mesh m, const spuma_preconditioner& pc)
+spuma_status pc_check(spuma_mesh m, const spuma_preconditioner& pc, bool multi_rank_ok = false)
 {
-    if (m->n_ranks > 1) return set_error(SPUMA_ERR_STATE, "preconditioned solvers are single-rank (DESIGN.md §3)");
+    if (m->n_ranks > 1 && !multi_rank_ok)
+        return set_error(SPUMA_ERR_STATE, "this preconditioned solver is single-rank (DESIGN.md §3)");
     if (pc.kind < SPUMA_PC_DIAGONAL || pc.kind > SPUMA_PC_ADILU || pc.n_sweeps < 0)
         return set_error(SPUMA_ERR_INVALID_ARGUMENT, "invalid preconditioner");
     return SPUMA_OK;
@@ -1874,17 +1875,19 @@ spuma_status spuma_gamg_get_hierarchy(spuma_mesh m, const spuma_gamg_params* par
 }
 
 spuma_status spuma_pcg_solve_pc(spuma_mesh m, const spuma_scalar* diag, const spuma_scalar* upper,
-                                const spuma_scalar* source, spuma_scalar* psi, const spuma_solver_controls* ctl,
-                                const spuma_preconditioner* pcp, spuma_solver_perf* perf)
+                                const spuma_scalar* iface_coeffs, const spuma_scalar* source, spuma_scalar* psi,
+                                const spuma_solver_controls* ctl, const spuma_preconditioner* pcp,
+                                spuma_solver_perf* perf)
 {
     if (!m) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "mesh is NULL");
     if (!ctl || !perf) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "NULL controls/perf");
     if (m->N > 0 && (!diag || !source || !psi)) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "NULL array");
     if (m->F > 0 && !upper) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "upper is NULL");
+    if (m->n_iface > 0 && !iface_coeffs) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "iface_coeffs is NULL");
     if (ctl->max_iter < 0 || ctl->min_iter < 0) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "negative iteration limit");
     const spuma_preconditioner pc = pcp ? *pcp : spuma_preconditioner{SPUMA_PC_DIAGONAL, 0};
-    SPUMA_TRY(pc_check(m, pc));
-    if (m->N == 0) {
+    SPUMA_TRY(pc_check(m, pc, true));
+    if (m->N == 0 && m->n_ranks == 1) {
         *perf = spuma_solver_perf{};
         return SPUMA_OK;
     }
@@ -1897,32 +1900,44 @@ spuma_status spuma_pcg_solve_pc(spuma_mesh m, const spuma_scalar* diag, const sp
     SPUMA_TRY(cells_in(m, source, R_SOURCE, &Pp.source));
     SPUMA_TRY(cells_in(m, psi, R_PSI, &psi_in));
     Pp.psi = const_cast<double*>(psi_in);
+    if (m->n_iface) SPUMA_TRY(iface_in(m, iface_coeffs, &Pp.iface));
     *m->h_ptrs = Pp;
     SPUMA_CUDA(cudaMemcpyAsync(m->ws.ptrs, m->h_ptrs, sizeof(DevPtrs), cudaMemcpyHostToDevice, s));
-    launch_scal_init(s, m->ws, *ctl, 1);
+    launch_scal_init(s, m->ws, *ctl, m->n_ranks);
     const MeshArgs a = mesh_args(m);
+    const bool fin = m->n_ranks == 1;
     if (amul_uses_ell(m->amul_variant) && m->d_upper_s) launch_ell_coeffs(s, a, Pp.upper, m->d_upper_s);
-    launch_setup1(s, m->grid, a, m->ws, true);
-    launch_setup2(s, m->grid, a, m->ws, true);
-    pc_setup(m, pc, Pp.diag, Pp.upper, Pp.upper);
+    SPUMA_TRY(halo_exchange(m, Pp.psi, m->ws.xr, s));
+    launch_setup1(s, m->grid, a, m->ws, fin);
+    if (!fin) SPUMA_TRY(reduce_finalize(m, 1, s));
+    launch_setup2(s, m->grid, a, m->ws, fin);
+    if (!fin) SPUMA_TRY(reduce_finalize(m, 2, s));
+    pc_setup(m, pc, Pp.diag, Pp.upper, Pp.upper);  // processor-local factorisation (Q31)
     m->stats.kernel_launches += 5;
     PcState* P = m->pc;
     Workspace w = m->ws;
     SPUMA_CUDA(cudaMemcpyAsync(&m->h_scal[0], w.scal, sizeof(DevScal), cudaMemcpyDeviceToHost, s));
     SPUMA_CUDA(cudaStreamSynchronize(s));
+    // external comm (host callbacks): one iteration per check; otherwise 8 (no-op kernels past
+    // 'done'; every rank runs the same launches and collectives)
+    const int per_check = m->external_comm ? 1 : 8;
     int it = 0;
     while (!m->h_scal[0].done) {
-        for (int b = 0; b < 8; ++b) {  // kernels are no-ops once the device 'done' flag is set
+        for (int b = 0; b < per_check; ++b) {
             pc_apply(m, pc, Pp.upper, Pp.upper, w.rA, w.wA, false, w.scal);
-            launch_pc_dot(s, m->N, w.wA, w.rA, P->part, w.scal);
+            launch_pc_dot(s, m->N, w.wA, w.rA, P->part, w.scal, fin);
+            if (!fin) SPUMA_TRY(reduce_finalize(m, 5, s));
             launch_pc_direction(s, m->N, w.wA, w.pA, nullptr, nullptr, w.scal);
-            launch_amul_dot(s, m->amul_variant, a, w, true, m->sell_wn, m->sell_wo);
-            launch_update(s, m->grid, a, w, true, 0);
+            SPUMA_TRY(halo_exchange(m, w.pA, w.xr, s));
+            launch_amul_dot(s, m->amul_variant, a, w, fin, m->sell_wn, m->sell_wo);
+            if (!fin) SPUMA_TRY(reduce_finalize(m, 3, s));
+            launch_update(s, m->grid, a, w, fin, 0);
+            if (!fin) SPUMA_TRY(reduce_finalize(m, 4, s));
             m->stats.kernel_launches += pc_launches(pc) + 4;
         }
         SPUMA_CUDA(cudaMemcpyAsync(&m->h_scal[0], w.scal, sizeof(DevScal), cudaMemcpyDeviceToHost, s));
         SPUMA_CUDA(cudaStreamSynchronize(s));
-        it += 8;
+        it += per_check;
         if (it > ctl->max_iter + 16) return set_error(SPUMA_ERR_STATE, "PCG loop did not terminate");
     }
     SPUMA_CUDA(cudaGetLastError());

@@ -153,6 +153,10 @@ static __device__ void finalize(DevScal* s, int stage, const double* g)
         s->alpha_prev = s->alpha;  // a deferred psi update of this iteration uses it
         break;
     }
+    case 5:  // preconditioned loops (§8(f4)): wArA = wA.rA from the general preconditioner, beta
+        s->wArA = g[0];
+        s->beta = s->wArA / s->wArAold;
+        break;
     }
 }
 

@@ -290,7 +290,8 @@ void launch_ilu_precondition(cudaStream_t s, const MeshArgs& a, const int* order
                              const double* rD, const double* upper, const double* lower, const double* r, double* w,
                              double* t1, double* t2, int* flag, unsigned* counter, int k, bool transpose,
                              const DevScal* scal, int width_f = 1 << 30, int width_b = 1 << 30);
-void launch_pc_dot(cudaStream_t s, int N, const double* w, const double* r, double* part, DevScal* scal);
+void launch_pc_dot(cudaStream_t s, int N, const double* w, const double* r, double* part, DevScal* scal,
+                   bool fin = true);
 void launch_pc_direction(cudaStream_t s, int N, const double* wA, double* pA, const double* wT, double* pT,
                          const DevScal* scal);
 void launch_bicg_amul_tmul(cudaStream_t s, const MeshArgs& a, const double* diag, const double* upper,

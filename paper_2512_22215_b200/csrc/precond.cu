@@ -234,14 +234,14 @@ __global__ void k_pc_diag(int N, const double* __restrict__ rD, const double* __
 
 // wArA (PCG) / wArT (PBiCG) = w . r; beta = wArA / wArAold (used from the second iteration)
 __global__ void __launch_bounds__(kThreads) k_pc_dot(int N, const double* __restrict__ w, const double* __restrict__ r,
-                                                     double* part, DevScal* scal)
+                                                     double* part, DevScal* scal, int fin)
 {
     if (scal->done) return;
     double v[1] = {0.0};
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < N; c += gridDim.x * blockDim.x) v[0] += w[c] * r[c];
     if (grid_sum<1>(v, part, &scal->ticket[5]) && threadIdx.x == 0) {
-        scal->wArA = v[0];
-        scal->beta = scal->wArA / scal->wArAold;
+        if (fin) finalize(scal, 5, v);
+        else scal->rank_part[0] = v[0];  // P > 1: global sum + finalize(5) by reduce_finalize
     }
 }
 
@@ -494,9 +494,9 @@ void launch_recip(cudaStream_t s, int N, const double* in, double* out)
     k_ilu_recip<<<cell_grid(N), kThreads, 0, s>>>(N, in, out);
 }
 
-void launch_pc_dot(cudaStream_t s, int N, const double* w, const double* r, double* part, DevScal* scal)
+void launch_pc_dot(cudaStream_t s, int N, const double* w, const double* r, double* part, DevScal* scal, bool fin)
 {
-    k_pc_dot<<<cell_grid(N), kThreads, 0, s>>>(N, w, r, part, scal);
+    k_pc_dot<<<cell_grid(N), kThreads, 0, s>>>(N, w, r, part, scal, fin ? 1 : 0);
 }
 
 void launch_pc_direction(cudaStream_t s, int N, const double* wA, double* pA, const double* wT, double* pT,

@@ -158,7 +158,7 @@ def lib():
                                                        ctypes.POINTER(SolverPerf)]
             L.spuma_gamg_get_hierarchy.argtypes = [_vp, ctypes.POINTER(GamgParams), _ci, _vp, _vp, _vp, _ci, _vp]
         if hasattr(L, "spuma_pbicg_solve"):
-            L.spuma_pcg_solve_pc.argtypes = [_vp] * 5 + [ctypes.POINTER(SolverControls), ctypes.POINTER(Preconditioner),
+            L.spuma_pcg_solve_pc.argtypes = [_vp] * 6 + [ctypes.POINTER(SolverControls), ctypes.POINTER(Preconditioner),
                                                          ctypes.POINTER(SolverPerf)]
             L.spuma_pbicg_solve.argtypes = [_vp] * 6 + [ctypes.POINTER(SolverControls), ctypes.POINTER(Preconditioner),
                                                         ctypes.POINTER(SolverPerf)]
@@ -358,14 +358,17 @@ class Mesh:
 
     # ---------------------------------------------------------------- §8(f3)/(f4)
     def pcg_solve_pc(self, diag, upper, source, psi, tolerance=1e-6, rel_tol=0.0, max_iter=5000, min_iter=0,
-                     kind=PC_DIAGONAL, n_sweeps=2) -> dict:
-        """spuma_pcg_solve_pc: PCG with a diagonal / DIC / DILU / aDILU preconditioner."""
+                     kind=PC_DIAGONAL, n_sweeps=2, iface_coeffs=None) -> dict:
+        """spuma_pcg_solve_pc: PCG with a diagonal / DIC / DILU / aDILU preconditioner
+        (processor-local on decomposed meshes)."""
         ctl, perf, pc = SolverControls(tolerance, rel_tol, max_iter, min_iter), SolverPerf(), Preconditioner(kind, n_sweeps)
         d, kd = _ptr(diag, np.float64)
         u, ku = _ptr(upper, np.float64)
+        f, kf = _ptr(iface_coeffs, np.float64)
         s, ks = _ptr(source, np.float64)
         p, kp = _ptr(psi, np.float64)
-        _check(lib().spuma_pcg_solve_pc(self._h, d, u, s, p, ctypes.byref(ctl), ctypes.byref(pc), ctypes.byref(perf)))
+        _check(lib().spuma_pcg_solve_pc(self._h, d, u, f, s, p, ctypes.byref(ctl), ctypes.byref(pc),
+                                        ctypes.byref(perf)))
         return perf.as_dict()
 
     def pbicg_solve(self, diag, upper, lower, source, psi, tolerance=1e-6, rel_tol=0.0, max_iter=1000, min_iter=0,

@@ -135,6 +135,22 @@ def _worker(rank, P, how, port, results):
         allp = [None] * P
         dist.all_gather_object(allp, perf)
         assert all(p == allp[0] for p in allp)  # identical decisions on every rank
+        # PCG with processor-local DIC / aDILU (Q31) vs the decomposed oracle
+        for kind, okind in ((S.spuma.PC_DIC, O.DIC), (S.spuma.PC_ADILU, O.ADILU)):
+            psi_k = torch.zeros(me.n_cells, **f64)
+            pk = h.pcg_solve_pc(diag, upper, src, psi_k, 1e-9, 0.0, 3000, 0, kind=kind, iface_coeffs=iface)
+            pso, pko = O.pcg_decomposed(subs, systems, None, O.controls(1e-9, 0.0, 3000, 0), kind=okind)
+            assert abs(pk["n_iterations"] - pko["n_iterations"]) <= 2, (kind, pk, pko)
+            nk = min(pk["n_iterations"], pko["n_iterations"])
+            psi_k.zero_()
+            h.pcg_solve_pc(diag, upper, src, psi_k, 0.0, 0.0, nk, nk, kind=kind, iface_coeffs=iface)
+            pso, _ = O.pcg_decomposed(subs, systems, None, O.controls(0.0, 0.0, nk, nk), kind=okind)
+            lk = psi_k.cpu().numpy()
+            numk = np.array([np.sum((lk - pso[rank]) ** 2), np.sum(pso[rank] ** 2)])
+            totk = [torch.empty(2, dtype=torch.float64) for _ in range(P)]
+            dist.all_gather(totk, torch.from_numpy(numk))
+            errk = np.sqrt(sum(t[0].item() for t in totk) / sum(t[1].item() for t in totk))
+            assert errk <= 1e-9, (kind, errk)
         # the inline-interface Amul (variant 0: halo before the Amul) gives the same iterates
         h.set_option(S.spuma.OPT_AMUL_VARIANT, 0)
         psi0 = torch.zeros(me.n_cells, **f64)
