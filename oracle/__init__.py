@@ -119,6 +119,8 @@ def _L():
                                                            ctypes.POINTER(Perf), vp, vp]
             lib.or_pcg_dd_pc.argtypes = [ci, ctypes.POINTER(_Domain), ctypes.POINTER(Controls), ci, ci,
                                          ctypes.POINTER(Perf)]
+            lib.or_pbicg_dd.argtypes = [ci, ctypes.POINTER(_Domain), vp, vp, ctypes.POINTER(Controls), ci, ci,
+                                        ctypes.POINTER(Perf)]
             lib.or_ilu_factor.argtypes = [ci, ci] + [vp] * 6
             lib.or_ilu_precondition.argtypes = [ci, ci] + [vp] * 7 + [ci, ci]
             lib.or_pcg_pc.argtypes = [ci, ci] + [vp] * 6 + [ctypes.POINTER(Controls), ci, ci, ctypes.POINTER(Perf)]
@@ -498,6 +500,50 @@ def pbicg(owner, neighbour, diag, upper, lower, source, kind=DILU, k=2, psi0=Non
     _L().or_pbicg(d.shape[0], o.shape[0], _p(o), _p(nb), _p(d), _p(u), _p(lo), _p(b), _p(psi), ctypes.byref(ctl),
                   int(kind), int(k), ctypes.byref(perf))
     return psi, perf.as_dict()
+
+
+def pbicg_decomposed(meshes: Sequence[gen.Mesh], systems: Sequence[dict], psi0=None,
+                     ctl: Optional[Controls] = None, kind: int = 3, k: int = 2):
+    """O8 + O12: PBiCG over P sub-domains.  systems[r]: dict(diag, upper, lower, source, iface,
+    iface_t) with iface / iface_t per processor patch (the Amul / Tmul coefficients, Q32)."""
+    ctl = ctl or controls()
+    P = len(meshes)
+    keep, doms, psis = [], (_Domain * P)(), []
+    lut = {}
+    if P > 1:
+        for r, m in enumerate(meshes):
+            for loc, g in enumerate(m.gid):
+                lut[int(g)] = (r, loc)
+    lowers = (ctypes.c_void_p * P)()
+    ifts = (ctypes.c_void_p * P)()
+    for r, (m, s) in enumerate(zip(meshes, systems)):
+        psi = np.zeros(m.n_cells) if psi0 is None else _f64(psi0[r]).copy()
+        psis.append(psi)
+        pp = processor_patches(m)
+        if pp:
+            ic = _i32(np.concatenate([p.face_cells for p in pp]))
+            ico = _f64(np.concatenate(s["iface"]))
+            ict = _f64(np.concatenate(s["iface_t"]))
+            src = [lut[int(g)] for p in pp for g in p.neighbour_gid]
+            sd, sc = _i32([a for a, _ in src]), _i32([b for _, b in src])
+        else:
+            ic, ico, ict = np.zeros(0, np.int32), np.zeros(0), np.zeros(0)
+            sd, sc = np.zeros(0, np.int32), np.zeros(0, np.int32)
+        arrs = [_i32(m.owner), _i32(m.neighbour), _f64(s["diag"]), _f64(s["upper"]), _f64(s["source"]), ic, ico, sd,
+                sc, _f64(s["lower"]), ict]
+        keep.append(arrs)
+        d = doms[r]
+        d.n_cells, d.n_faces = m.n_cells, m.n_faces
+        d.owner, d.neighbour, d.diag, d.upper, d.source = [_p(a) for a in arrs[:5]]
+        d.psi = _p(psi)
+        d.n_iface = ic.shape[0]
+        d.iface_cells, d.iface_coeffs, d.iface_src_domain, d.iface_src_cell = [_p(a) for a in arrs[5:9]]
+        lowers[r] = _p(arrs[9])
+        ifts[r] = _p(arrs[10])
+    perf = Perf()
+    _L().or_pbicg_dd(P, doms, ctypes.addressof(lowers), ctypes.addressof(ifts), ctypes.byref(ctl), int(kind), int(k),
+                     ctypes.byref(perf))
+    return psis, perf.as_dict()
 
 
 def tmul(owner, neighbour, diag, upper, lower, x) -> np.ndarray:

@@ -1317,6 +1317,151 @@ int or_pbicg(int n, int F, const int* owner, const int* neighbour, const double*
     return 0;
 }
 
+/* [OF] PBiCG over nd domains (O8 + Q32): lower[p] the domain's lower coefficients; iface_t[p]
+ * the coefficients Tmul uses on its processor faces (A^T couples row P to the remote cell with
+ * A[remote][P]); the preconditioner is processor-local (Q31); sums in rank order; sumA of the
+ * normFactor = diag + row's upper/lower + its Amul interface coefficients (Q17, Q35). */
+int or_pbicg_dd(int nd, or_domain* D, const double* const* lower, const double* const* iface_t,
+                const or_controls* ctl, int kind, int k, or_perf* perf)
+{
+    double **wA = (double**)calloc((size_t)nd, sizeof(double*)), **wT = (double**)calloc((size_t)nd, sizeof(double*));
+    double **rA = (double**)calloc((size_t)nd, sizeof(double*)), **rT = (double**)calloc((size_t)nd, sizeof(double*));
+    double **pA = (double**)calloc((size_t)nd, sizeof(double*)), **pT = (double**)calloc((size_t)nd, sizeof(double*));
+    double **rD = (double**)calloc((size_t)nd, sizeof(double*)), **xr = (double**)calloc((size_t)nd, sizeof(double*));
+    for (int p = 0; p < nd; ++p) {
+        const size_t n = (size_t)D[p].n_cells + 1;
+        wA[p] = (double*)calloc(n, sizeof(double));
+        wT[p] = (double*)calloc(n, sizeof(double));
+        rA[p] = (double*)calloc(n, sizeof(double));
+        rT[p] = (double*)calloc(n, sizeof(double));
+        pA[p] = (double*)calloc(n, sizeof(double));
+        pT[p] = (double*)calloc(n, sizeof(double));
+        rD[p] = (double*)calloc(n, sizeof(double));
+        xr[p] = (double*)calloc((size_t)D[p].n_iface + 1, sizeof(double));
+    }
+    /* y = A x (T = 0) or A^T x (T = 1) on every domain, x_remote from the other domains */
+#define OR_DD_MUL(T, X, Y)                                                                                         \
+    do {                                                                                                           \
+        for (int p = 0; p < nd; ++p)                                                                               \
+            for (int i = 0; i < D[p].n_iface; ++i) xr[p][i] = (X)[D[p].iface_src_domain[i]][D[p].iface_src_cell[i]]; \
+        for (int p = 0; p < nd; ++p)                                                                               \
+            or_amul(D[p].n_cells, D[p].n_faces, D[p].owner, D[p].neighbour, D[p].diag, (T) ? D[p].upper : lower[p], \
+                    (T) ? lower[p] : D[p].upper, (X)[p], D[p].n_iface, D[p].iface_cells,                          \
+                    (T) ? iface_t[p] : D[p].iface_coeffs, xr[p], (Y)[p]);                                          \
+    } while (0)
+    double** psi = (double**)calloc((size_t)nd, sizeof(double*));
+    for (int p = 0; p < nd; ++p) psi[p] = D[p].psi;
+    OR_DD_MUL(0, psi, wA);
+    OR_DD_MUL(1, psi, wT);
+    for (int p = 0; p < nd; ++p)
+        for (int c = 0; c < D[p].n_cells; ++c) {
+            rA[p][c] = D[p].source[c] - wA[p][c];
+            rT[p][c] = D[p].source[c] - wT[p][c];
+        }
+    double spsi = 0.0, ncell = 0.0;
+    for (int p = 0; p < nd; ++p) {
+        double t = 0.0;
+        for (int c = 0; c < D[p].n_cells; ++c) t += D[p].psi[c];
+        spsi += t;
+        ncell += (double)D[p].n_cells;
+    }
+    const double xbar = spsi / ncell;
+    double normFactor = 0.0;
+    for (int p = 0; p < nd; ++p) {
+        double* sumA = (double*)calloc((size_t)D[p].n_cells + 1, sizeof(double));
+        for (int c = 0; c < D[p].n_cells; ++c) sumA[c] = D[p].diag[c];
+        for (int f = 0; f < D[p].n_faces; ++f) {
+            sumA[D[p].owner[f]] += D[p].upper[f];
+            sumA[D[p].neighbour[f]] += lower[p][f];
+        }
+        for (int i = 0; i < D[p].n_iface; ++i) sumA[D[p].iface_cells[i]] += D[p].iface_coeffs[i];
+        double t = 0.0;
+        for (int c = 0; c < D[p].n_cells; ++c) {
+            const double xref = sumA[c] * xbar;
+            t += fabs(wA[p][c] - xref) + fabs(D[p].source[c] - xref);
+        }
+        normFactor += t;
+        free(sumA);
+    }
+    normFactor += 1e-20;
+    double smag = 0.0;
+    for (int p = 0; p < nd; ++p) {
+        double t = 0.0;
+        for (int c = 0; c < D[p].n_cells; ++c) t += fabs(rA[p][c]);
+        smag += t;
+    }
+    perf->initial_residual = smag / normFactor;
+    perf->final_residual = perf->initial_residual;
+    perf->n_iterations = 0;
+    perf->singular = 0;
+    if (ctl->min_iter > 0 || !or_conv(perf->final_residual, perf->initial_residual, ctl)) {
+        for (int p = 0; p < nd; ++p)
+            or_pc_setup(kind, D[p].n_cells, D[p].n_faces, D[p].owner, D[p].neighbour, D[p].diag, D[p].upper,
+                        lower[p], rD[p]);
+        double wArT = 1e300, wArTold;
+        do {
+            wArTold = wArT;
+            wArT = 0.0;
+            for (int p = 0; p < nd; ++p) {
+                or_pc_apply(kind, k, D[p].n_cells, D[p].n_faces, D[p].owner, D[p].neighbour, rD[p], D[p].upper,
+                            lower[p], rA[p], wA[p], 0);
+                or_pc_apply(kind, k, D[p].n_cells, D[p].n_faces, D[p].owner, D[p].neighbour, rD[p], D[p].upper,
+                            lower[p], rT[p], wT[p], 1);
+                double t = 0.0;
+                for (int c = 0; c < D[p].n_cells; ++c) t += wA[p][c] * rT[p][c];
+                wArT += t;
+            }
+            for (int p = 0; p < nd; ++p) {
+                if (perf->n_iterations == 0) {
+                    for (int c = 0; c < D[p].n_cells; ++c) {
+                        pA[p][c] = wA[p][c];
+                        pT[p][c] = wT[p][c];
+                    }
+                } else {
+                    const double beta = wArT / wArTold;
+                    for (int c = 0; c < D[p].n_cells; ++c) {
+                        pA[p][c] = wA[p][c] + beta * pA[p][c];
+                        pT[p][c] = wT[p][c] + beta * pT[p][c];
+                    }
+                }
+            }
+            OR_DD_MUL(0, pA, wA);
+            OR_DD_MUL(1, pT, wT);
+            double wApT = 0.0;
+            for (int p = 0; p < nd; ++p) {
+                double t = 0.0;
+                for (int c = 0; c < D[p].n_cells; ++c) t += wA[p][c] * pT[p][c];
+                wApT += t;
+            }
+            if (fabs(wApT) / normFactor < 1e-300) {
+                perf->singular = 1;
+                break;
+            }
+            const double alpha = wArT / wApT;
+            smag = 0.0;
+            for (int p = 0; p < nd; ++p) {
+                double t = 0.0;
+                for (int c = 0; c < D[p].n_cells; ++c) {
+                    D[p].psi[c] += alpha * pA[p][c];
+                    rA[p][c] -= alpha * wA[p][c];
+                    rT[p][c] -= alpha * wT[p][c];
+                    t += fabs(rA[p][c]);
+                }
+                smag += t;
+            }
+            perf->final_residual = smag / normFactor;
+        } while ((++perf->n_iterations < ctl->max_iter && !or_conv(perf->final_residual, perf->initial_residual, ctl)) ||
+                 perf->n_iterations < ctl->min_iter);
+    }
+#undef OR_DD_MUL
+    perf->converged = or_conv(perf->final_residual, perf->initial_residual, ctl);
+    for (int p = 0; p < nd; ++p) {
+        free(wA[p]); free(wT[p]); free(rA[p]); free(rT[p]); free(pA[p]); free(pT[p]); free(rD[p]); free(xr[p]);
+    }
+    free(wA); free(wT); free(rA); free(rT); free(pA); free(pT); free(rD); free(xr); free(psi);
+    return 0;
+}
+
 /* LDU -> CSR (Q34; "a map computed by the Radix sort ... of the sparsity pattern"):
  * rows ascending, columns ascending within a row; map[k] indexes [diag (n) | upper (F) | lower (F)]:
  * row P col N (P = owner) is upper[f], row N col P is lower[f].  row_ptr [n+1], col/map [n+2F]. */

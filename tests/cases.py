@@ -62,3 +62,33 @@ def asym_system(mesh, seed=0, skew=0.4):
     np.add.at(off, mesh.neighbour, np.abs(lower))
     diag = -1.05 * np.maximum(off, 1e-12)
     return diag, upper, lower, rng.standard_normal(mesh.n_cells) * mesh.V
+
+
+def asym_decomposed(mesh, part, seed=0, skew=0.4, sym=False):
+    """The asym_system of `mesh` split over the parts of `part` (gen.decompose): per domain
+    dict(diag, upper, lower, source, iface, iface_t) -- processor faces carry A[P][N] = upper
+    and A[N][P] = lower of the undecomposed face, oriented by is_owner (Amul: own row's entry,
+    Tmul: the remote row's entry).  sym: lower = upper.  Returns (subs, systems, global)."""
+    import gen
+    d, u, l, b = asym_system(mesh, seed=seed, skew=skew)
+    if sym:
+        l = u.copy()
+    P = int(part.max()) + 1
+    subs = gen.decompose(mesh, part, P)
+    gidx = {int(f): i for i, f in enumerate(mesh.gface)}
+    loc = {int(g): i for i, g in enumerate(mesh.gid)}
+    systems = []
+    for sm in subs:
+        fi = np.array([gidx[int(f)] for f in sm.gface], dtype=np.int64)
+        assert np.array_equal(mesh.gid[mesh.owner[fi]], sm.gid[sm.owner])  # orientation kept
+        ci = np.array([loc[int(g)] for g in sm.gid], dtype=np.int64)
+        iface, iface_t = [], []
+        for pt in sm.patches:
+            if pt.kind != gen.PROCESSOR:
+                continue
+            gi = np.array([gidx[int(f)] for f in pt.global_face], dtype=np.int64)
+            own = np.asarray(pt.is_owner, bool)
+            iface.append(np.where(own, u[gi], l[gi]))
+            iface_t.append(np.where(own, l[gi], u[gi]))
+        systems.append(dict(diag=d[ci], upper=u[fi], lower=l[fi], source=b[ci], iface=iface, iface_t=iface_t))
+    return subs, systems, (d, u, l, b)

@@ -201,3 +201,55 @@ def test_normfactor_uses_row_sums_on_asymmetric_system():
     _, perf = O.pbicg(m.owner, m.neighbour, diag, upper, lower, b, O.DILU, psi0=np.full(m.n_cells, 1.5),
                       ctl=O.controls(1e-9, 0.0, 1, 1))
     assert perf["initial_residual"] == pytest.approx(1.0, rel=1e-10)
+
+
+# ---- decomposed PBiCG (O8 + O12, Q31/Q32) ----
+from cases import asym_decomposed  # noqa: E402
+
+
+def _gather(mesh, subs, xs):
+    loc = {int(g): i for i, g in enumerate(mesh.gid)}
+    out = np.zeros(mesh.n_cells)
+    for sm, x in zip(subs, xs):
+        out[[loc[int(g)] for g in sm.gid]] = x
+    return out
+
+
+def test_pbicg_decomposed_single_domain_is_pbicg():
+    m = gen.perturbed(6, 0.2)
+    part = np.zeros(m.n_cells, np.int64)
+    subs, systems, (d, u, l, b) = asym_decomposed(m, part, seed=3)
+    for kind in (O.DILU, O.ADILU):
+        a, pa = O.pbicg_decomposed(subs, systems, None, O.controls(1e-10, 0.0, 500, 0), kind)
+        s = systems[0]
+        ref, pr = O.pbicg(subs[0].owner, subs[0].neighbour, s["diag"], s["upper"], s["lower"], s["source"], kind, 2,
+                          None, O.controls(1e-10, 0.0, 500, 0))
+        assert pa["n_iterations"] == pr["n_iterations"] and np.array_equal(a[0], ref)
+
+
+@pytest.mark.parametrize("P,how", [(2, "block"), (4, "rcb")])
+def test_pbicg_decomposed_reaches_global_dense_solution(P, how):
+    m = gen.permute(gen.perturbed(8, 0.2), seed=4)
+    part = gen.rcb_parts(m, P) if how == "rcb" else gen.block_parts(m, (P, 1, 1))
+    subs, systems, (d, u, l, b) = asym_decomposed(m, part, seed=5)
+    A = _dense_asym(m.n_cells, m.owner, m.neighbour, d, u, l)
+    exact = np.linalg.solve(A, b)
+    for kind in (O.DIAGONAL, O.DILU, O.ADILU):
+        xs, perf = O.pbicg_decomposed(subs, systems, None, O.controls(1e-13, 0.0, 2000, 0), kind)
+        assert perf["converged"] and not perf["singular"]
+        got = _gather(m, subs, xs)
+        assert np.linalg.norm(got - exact) / np.linalg.norm(exact) < 1e-9, kind
+
+
+def test_pbicg_decomposed_symmetric_follows_decomposed_pcg():
+    """lower = upper, iface_t = iface: BiCG with a symmetric (processor-local DIC) preconditioner
+    produces the decomposed CG iterates."""
+    m = gen.perturbed(7, 0.2)
+    part = gen.block_parts(m, (2, 1, 1))
+    subs, systems, _ = asym_decomposed(m, part, seed=6, sym=True)
+    lsys = [O.LduSystem(s["diag"], s["upper"], s["source"], s["iface"]) for s in systems]
+    for n in (1, 4, 12):
+        xb, pb = O.pbicg_decomposed(subs, systems, None, O.controls(0.0, 0.0, n, n), O.DIC)
+        xc, pc = O.pcg_decomposed(subs, lsys, None, O.controls(0.0, 0.0, n, n), kind=O.DIC)
+        gb, gc = _gather(m, subs, xb), _gather(m, subs, xc)
+        assert np.linalg.norm(gb - gc) / np.linalg.norm(gc) < 1e-11, n
