@@ -242,8 +242,8 @@ spuma_status spuma_gamg_get_hierarchy(spuma_mesh m, const spuma_gamg_params* par
  * as dependency-scheduled persistent kernels, bitwise equal to the sequential loops for any
  * numbering (their critical path is the mesh's dependency depth: a colour / wavefront
  * numbering makes them fast, the natural order of an n^3 box has depth ~3n).
- * spuma_pcg_solve_pc runs on decomposed meshes too; the others are single-rank
- * (n_ranks > 1 -> SPUMA_ERR_STATE). */
+ * spuma_pcg_solve_pc and spuma_pbicg_solve run on decomposed meshes too; the diagnostics
+ * are single-rank (n_ranks > 1 -> SPUMA_ERR_STATE). */
 typedef enum spuma_precond_kind {
     SPUMA_PC_DIAGONAL = 0,
     SPUMA_PC_DIC = 1,
@@ -273,10 +273,14 @@ spuma_status spuma_pcg_solve_pc(spuma_mesh m, const spuma_scalar* diag, const sp
 /*
  * PBiCG (Q32) for an asymmetric LDU matrix: lower [n_faces] is
  * the coefficient of row neighbour, column owner; upper of row owner, column neighbour.
- * pc NULL: aDILU with 2 passes (the paper's setting).  psi in/out.  Single-rank.
+ * n_ranks > 1 (collective): iface_coeffs [sum of processor faces] = this rank's row entry
+ * A[P][remote] of each processor face (used by Amul), iface_coeffs_t = the remote row's entry
+ * A[remote][P] (used by Tmul); both NULL on a single rank.  The preconditioner is
+ * processor-local (Q31).  pc NULL: aDILU with 2 passes (the paper's setting).  psi in/out.
  */
 spuma_status spuma_pbicg_solve(spuma_mesh m, const spuma_scalar* diag, const spuma_scalar* upper,
-                               const spuma_scalar* lower, const spuma_scalar* source, spuma_scalar* psi,
+                               const spuma_scalar* lower, const spuma_scalar* iface_coeffs,
+                               const spuma_scalar* iface_coeffs_t, const spuma_scalar* source, spuma_scalar* psi,
                                const spuma_solver_controls* ctl, const spuma_preconditioner* pc,
                                spuma_solver_perf* perf);
 

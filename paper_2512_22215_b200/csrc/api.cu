@@ -753,6 +753,7 @@ struct PcState {
     double *wT = nullptr, *rT = nullptr, *pT = nullptr, *part = nullptr;
     double *u_in = nullptr, *l_in = nullptr, *u_int = nullptr, *l_int = nullptr;
     int* csr_map = nullptr;  // device copy of the CSR map
+    double *iface_t = nullptr, *xrT = nullptr;  // PBiCG: Tmul interface coefficients (staging), pT halo
     int nnz = 0;
 };
 
@@ -763,7 +764,7 @@ void pc_release(spuma_mesh m)
     PcState* P = m->pc;
     if (!P) return;
     void* ptrs[] = {P->order_f, P->order_b, P->flag, P->counter, P->raw, P->rD, P->t1, P->t2, P->wT, P->rT,
-                    P->pT, P->part, P->u_in, P->l_in, P->u_int, P->l_int, P->csr_map};
+                    P->pT, P->part, P->u_in, P->l_in, P->u_int, P->l_int, P->csr_map, P->iface_t, P->xrT};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     delete P;
@@ -1956,7 +1957,8 @@ spuma_status spuma_pcg_solve_pc(spuma_mesh m, const spuma_scalar* diag, const sp
 }
 
 spuma_status spuma_pbicg_solve(spuma_mesh m, const spuma_scalar* diag, const spuma_scalar* upper,
-                               const spuma_scalar* lower, const spuma_scalar* source, spuma_scalar* psi,
+                               const spuma_scalar* lower, const spuma_scalar* iface_coeffs,
+                               const spuma_scalar* iface_coeffs_t, const spuma_scalar* source, spuma_scalar* psi,
                                const spuma_solver_controls* ctl, const spuma_preconditioner* pcp,
                                spuma_solver_perf* perf)
 {
@@ -1964,44 +1966,70 @@ spuma_status spuma_pbicg_solve(spuma_mesh m, const spuma_scalar* diag, const spu
     if (!ctl || !perf) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "NULL controls/perf");
     if (m->N > 0 && (!diag || !source || !psi)) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "NULL array");
     if (m->F > 0 && (!upper || !lower)) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "upper/lower is NULL");
+    if (m->n_iface > 0 && (!iface_coeffs || !iface_coeffs_t))
+        return set_error(SPUMA_ERR_INVALID_ARGUMENT, "iface_coeffs / iface_coeffs_t is NULL");
     if (ctl->max_iter < 0 || ctl->min_iter < 0) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "negative iteration limit");
     const spuma_preconditioner pc = pcp ? *pcp : spuma_preconditioner{SPUMA_PC_ADILU, 2};
-    SPUMA_TRY(pc_check(m, pc));
-    if (m->N == 0) {
+    SPUMA_TRY(pc_check(m, pc, true));
+    if (m->N == 0 && m->n_ranks == 1) {
         *perf = spuma_solver_perf{};
         return SPUMA_OK;
     }
     SPUMA_TRY(pc_ensure(m));
     PcState* P = m->pc;
     cudaStream_t s = m->stream;
-    const double *d_i, *s_i, *psi_c, *u_i, *l_i;
+    const bool fin = m->n_ranks == 1;
+    const double *d_i, *s_i, *psi_c, *u_i, *l_i, *if_i = nullptr, *ift_i = nullptr;
     SPUMA_TRY(cells_in(m, diag, R_DIAG, &d_i));
     SPUMA_TRY(cells_in(m, source, R_SOURCE, &s_i));
     SPUMA_TRY(cells_in(m, psi, R_PSI, &psi_c));
     SPUMA_TRY(pair_in(m, upper, lower, &u_i, &l_i));
+    if (m->n_iface) {
+        SPUMA_TRY(iface_in(m, iface_coeffs, &if_i));
+        if (!P->iface_t) SPUMA_TRY(dalloc(&P->iface_t, m->n_iface));
+        if (!P->xrT) SPUMA_TRY(dalloc(&P->xrT, m->n_iface));
+        if (is_device_ptr(iface_coeffs_t)) ift_i = iface_coeffs_t;
+        else {
+            SPUMA_CUDA(cudaMemcpyAsync(P->iface_t, iface_coeffs_t, sizeof(double) * m->n_iface, cudaMemcpyHostToDevice,
+                                       s));
+            ift_i = P->iface_t;
+        }
+    }
     double* psi_i = const_cast<double*>(psi_c);
     Workspace w = m->ws;
     const MeshArgs a = mesh_args(m);
-    launch_scal_init(s, w, *ctl, 1);
-    launch_bicg_setup(s, a, d_i, u_i, l_i, s_i, psi_i, w.wA, P->wT, w.rA, P->rT, w.sumA, P->part, w.scal);
-    pc_setup(m, pc, d_i, u_i, l_i);
+    launch_scal_init(s, w, *ctl, m->n_ranks);
+    SPUMA_TRY(halo_exchange(m, psi_i, w.xr, s));
+    launch_bicg_setup1(s, a, d_i, u_i, l_i, if_i, ift_i, w.xr, s_i, psi_i, w.wA, P->wT, w.rA, P->rT, w.sumA, P->part,
+                       w.scal, fin);
+    if (!fin) SPUMA_TRY(reduce_finalize(m, 1, s));
+    launch_pc_setup2(s, m->N, w.wA, w.sumA, s_i, w.rA, P->part, w.scal, fin);
+    if (!fin) SPUMA_TRY(reduce_finalize(m, 2, s));
+    pc_setup(m, pc, d_i, u_i, l_i);  // processor-local (Q31)
     m->stats.kernel_launches += 4;
     SPUMA_CUDA(cudaMemcpyAsync(&m->h_scal[0], w.scal, sizeof(DevScal), cudaMemcpyDeviceToHost, s));
     SPUMA_CUDA(cudaStreamSynchronize(s));
+    const int per_check = m->external_comm ? 1 : 8;
     int it = 0;
     while (!m->h_scal[0].done) {
-        for (int b = 0; b < 8; ++b) {
+        for (int b = 0; b < per_check; ++b) {
             pc_apply(m, pc, u_i, l_i, w.rA, w.wA, false, w.scal);
             pc_apply(m, pc, u_i, l_i, P->rT, P->wT, true, w.scal);
-            launch_pc_dot(s, m->N, w.wA, P->rT, P->part, w.scal);
+            launch_pc_dot(s, m->N, w.wA, P->rT, P->part, w.scal, fin);
+            if (!fin) SPUMA_TRY(reduce_finalize(m, 5, s));
             launch_pc_direction(s, m->N, w.wA, w.pA, P->wT, P->pT, w.scal);
-            launch_bicg_amul_tmul(s, a, d_i, u_i, l_i, w.pA, P->pT, w.wA, P->wT, P->part, w.scal);
-            launch_bicg_update(s, m->N, psi_i, w.pA, w.rA, w.wA, P->rT, P->wT, P->part, w.scal);
+            SPUMA_TRY(halo_exchange(m, w.pA, w.xr, s));
+            SPUMA_TRY(halo_exchange(m, P->pT, P->xrT, s));
+            launch_bicg_amul_tmul(s, a, d_i, u_i, l_i, if_i, ift_i, w.pA, P->pT, w.xr, P->xrT, w.wA, P->wT, P->part,
+                                  w.scal, fin);
+            if (!fin) SPUMA_TRY(reduce_finalize(m, 3, s));
+            launch_bicg_update(s, m->N, psi_i, w.pA, w.rA, w.wA, P->rT, P->wT, P->part, w.scal, fin);
+            if (!fin) SPUMA_TRY(reduce_finalize(m, 4, s));
             m->stats.kernel_launches += 2 * pc_launches(pc) + 4;
         }
         SPUMA_CUDA(cudaMemcpyAsync(&m->h_scal[0], w.scal, sizeof(DevScal), cudaMemcpyDeviceToHost, s));
         SPUMA_CUDA(cudaStreamSynchronize(s));
-        it += 8;
+        it += per_check;
         if (it > ctl->max_iter + 16) return set_error(SPUMA_ERR_STATE, "PBiCG loop did not terminate");
     }
     SPUMA_CUDA(cudaGetLastError());

@@ -295,13 +295,17 @@ void launch_pc_dot(cudaStream_t s, int N, const double* w, const double* r, doub
 void launch_pc_direction(cudaStream_t s, int N, const double* wA, double* pA, const double* wT, double* pT,
                          const DevScal* scal);
 void launch_bicg_amul_tmul(cudaStream_t s, const MeshArgs& a, const double* diag, const double* upper,
-                           const double* lower, const double* pA, const double* pT, double* wA, double* wT,
-                           double* part, DevScal* scal);
+                           const double* lower, const double* iface, const double* iface_t, const double* pA,
+                           const double* pT, const double* xr, const double* xrT, double* wA, double* wT,
+                           double* part, DevScal* scal, bool fin);
 void launch_bicg_update(cudaStream_t s, int N, double* psi, const double* pA, double* rA, const double* wA, double* rT,
-                        const double* wT, double* part, DevScal* scal);
-void launch_bicg_setup(cudaStream_t s, const MeshArgs& a, const double* diag, const double* upper,
-                       const double* lower, const double* source, const double* psi, double* wA, double* wT,
-                       double* rA, double* rT, double* sumA, double* part, DevScal* scal);
+                        const double* wT, double* part, DevScal* scal, bool fin);
+void launch_bicg_setup1(cudaStream_t s, const MeshArgs& a, const double* diag, const double* upper,
+                        const double* lower, const double* iface, const double* iface_t, const double* xr,
+                        const double* source, const double* psi, double* wA, double* wT, double* rA, double* rT,
+                        double* sumA, double* part, DevScal* scal, bool fin);
+void launch_pc_setup2(cudaStream_t s, int N, const double* wA, const double* sumA, const double* source,
+                      const double* rA, double* part, DevScal* scal, bool fin);
 void launch_csr_values(cudaStream_t s, int nnz, int N, int F, const int* map, const double* diag,
                        const double* upper, const double* lower, double* vals);
 void launch_gather_pair(cudaStream_t s, int F, const int* map, const signed char* flip, const double* u,

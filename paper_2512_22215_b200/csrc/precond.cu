@@ -258,90 +258,95 @@ __global__ void k_pc_direction(int N, const double* __restrict__ wA, double* __r
     }
 }
 
-// asymmetric row of A (upper on the owner side, lower on the neighbour side) and of A^T
+// asymmetric row of A (upper on the owner side, lower on the neighbour side) and of A^T, then the
+// processor-interface terms icoef * x_remote in (patch, face) order (Q10) when icoef is given
 __device__ __forceinline__ double row_asym(const MeshArgs& a, int c, const double* __restrict__ diag,
                                            const double* __restrict__ nbr_coef, const double* __restrict__ own_coef,
-                                           const double* __restrict__ x)
+                                           const double* __restrict__ x, const double* __restrict__ icoef = nullptr,
+                                           const double* __restrict__ xr = nullptr)
 {
     double s = diag[c] * x[c];
     for (int k = a.losortStart[c]; k < a.losortStart[c + 1]; ++k) s = s + nbr_coef[a.losort[k]] * x[a.ownerLo[k]];
     for (int f = a.ownerStart[c]; f < a.ownerStart[c + 1]; ++f) s = s + own_coef[f] * x[a.neighbour[f]];
+    if (icoef && a.ifStart)
+        for (int j = a.ifStart[c]; j < a.ifStart[c + 1]; ++j) s = s + icoef[a.ifIdx[j]] * xr[a.ifIdx[j]];
     return s;
 }
 
-// PBiCG: wA = A pA, wT = A^T pT, wApT = wA . pT -> alpha, singularity (Q32)
+// PBiCG: wA = A pA, wT = A^T pT, wApT = wA . pT -> alpha, singularity (Q32; finalize stage 3)
 __global__ void __launch_bounds__(kThreads) k_bicg_amul_tmul(MeshArgs a, const double* __restrict__ diag,
                                                              const double* __restrict__ upper,
                                                              const double* __restrict__ lower,
+                                                             const double* __restrict__ iface,
+                                                             const double* __restrict__ iface_t,
                                                              const double* __restrict__ pA,
-                                                             const double* __restrict__ pT, double* __restrict__ wA,
-                                                             double* __restrict__ wT, double* part, DevScal* scal)
+                                                             const double* __restrict__ pT,
+                                                             const double* __restrict__ xr,
+                                                             const double* __restrict__ xrT, double* __restrict__ wA,
+                                                             double* __restrict__ wT, double* part, DevScal* scal,
+                                                             int fin)
 {
     if (scal->done) return;
     double v[1] = {0.0};
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < a.N; c += gridDim.x * blockDim.x) {
-        const double ya = row_asym(a, c, diag, lower, upper, pA);
-        const double yt = row_asym(a, c, diag, upper, lower, pT);
+        const double ya = row_asym(a, c, diag, lower, upper, pA, iface, xr);
+        const double yt = row_asym(a, c, diag, upper, lower, pT, iface_t, xrT);
         wA[c] = ya;
         wT[c] = yt;
         v[0] += ya * pT[c];
     }
     if (grid_sum<1>(v, part, &scal->ticket[6]) && threadIdx.x == 0) {
-        scal->wApA = v[0];
-        if (fabs(scal->wApA) / scal->normFactor < 1e-300) {
-            scal->singular = 1;
-            scal->done = 1;
-        } else {
-            scal->alpha = scal->wArA / scal->wApA;
-        }
+        if (fin) finalize(scal, 3, v);
+        else scal->rank_part[0] = v[0];
     }
 }
 
-// PBiCG update: psi += alpha pA, rA -= alpha wA, rT -= alpha wT; final residual, n++, done
+// PBiCG update: psi += alpha pA, rA -= alpha wA, rT -= alpha wT; |rA| -> finalize stage 4
 __global__ void __launch_bounds__(kThreads) k_bicg_update(int N, double* __restrict__ psi,
                                                           const double* __restrict__ pA,
                                                           double* __restrict__ rA, const double* __restrict__ wA,
                                                           double* __restrict__ rT, const double* __restrict__ wT,
-                                                          double* part, DevScal* scal)
+                                                          double* part, DevScal* scal, int fin)
 {
     if (scal->done) return;
     const double alpha = scal->alpha;
-    double v[1] = {0.0};
+    double v[2] = {0.0, 0.0};
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < N; c += gridDim.x * blockDim.x) {
         psi[c] = psi[c] + alpha * pA[c];
         const double r = rA[c] - alpha * wA[c];
         rA[c] = r;
         if (rT) rT[c] = rT[c] - alpha * wT[c];
-        v[0] += fabs(r);
+        v[1] += fabs(r);
     }
-    if (grid_sum<1>(v, part, &scal->ticket[7]) && threadIdx.x == 0) {
-        scal->fin = v[0] / scal->normFactor;
-        scal->n = scal->n + 1;
-        const bool c = conv(scal->fin, scal->init, scal->tol, scal->rel_tol);
-        scal->converged = c;
-        if (!((scal->n < scal->max_iter && !c) || scal->n < scal->min_iter)) scal->done = 1;
-        scal->wArAold = scal->wArA;
+    if (grid_sum<2>(v, part, &scal->ticket[7]) && threadIdx.x == 0) {
+        if (fin) finalize(scal, 4, v);
+        else scal->rank_part[0] = v[0], scal->rank_part[1] = v[1];
     }
 }
 
-// PBiCG setup: wA = A psi, wT = A^T psi, rA = b - wA, rT = b - wT, sumA = row sums (Q35),
-// partial sum of psi -> finalize(1) gives gAverage(psi)
+// PBiCG setup: wA = A psi, wT = A^T psi, rA = b - wA, rT = b - wT, sumA = row sums incl. the
+// Amul interface coefficients (Q17, Q35); sum of psi and N -> finalize stage 1 (gAverage)
 __global__ void __launch_bounds__(kThreads) k_bicg_setup(MeshArgs a, const double* __restrict__ diag,
                                                          const double* __restrict__ upper,
                                                          const double* __restrict__ lower,
+                                                         const double* __restrict__ iface,
+                                                         const double* __restrict__ iface_t,
+                                                         const double* __restrict__ xr,
                                                          const double* __restrict__ source,
                                                          const double* __restrict__ psi, double* __restrict__ wA,
                                                          double* __restrict__ wT, double* __restrict__ rA,
                                                          double* __restrict__ rT, double* __restrict__ sumA,
-                                                         double* part, DevScal* scal)
+                                                         double* part, DevScal* scal, int fin)
 {
     double v[2] = {0.0, 0.0};
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < a.N; c += gridDim.x * blockDim.x) {
-        const double ya = row_asym(a, c, diag, lower, upper, psi);
-        const double yt = row_asym(a, c, diag, upper, lower, psi);
+        const double ya = row_asym(a, c, diag, lower, upper, psi, iface, xr);
+        const double yt = row_asym(a, c, diag, upper, lower, psi, iface_t, xr);
         double s = diag[c];
         for (int k = a.losortStart[c]; k < a.losortStart[c + 1]; ++k) s = s + lower[a.losort[k]];
         for (int f = a.ownerStart[c]; f < a.ownerStart[c + 1]; ++f) s = s + upper[f];
+        if (iface && a.ifStart)
+            for (int j = a.ifStart[c]; j < a.ifStart[c + 1]; ++j) s = s + iface[a.ifIdx[j]];
         wA[c] = ya;
         wT[c] = yt;
         rA[c] = source[c] - ya;
@@ -350,32 +355,29 @@ __global__ void __launch_bounds__(kThreads) k_bicg_setup(MeshArgs a, const doubl
         v[0] += psi[c];
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) v[1] = (double)a.N;
-    if (grid_sum<2>(v, part, &scal->ticket[0]) && threadIdx.x == 0) scal->xbar = v[0] / v[1];
+    if (grid_sum<2>(v, part, &scal->ticket[0]) && threadIdx.x == 0) {
+        if (fin) finalize(scal, 1, v);
+        else scal->rank_part[0] = v[0], scal->rank_part[1] = v[1];
+    }
 }
 
-// normFactor and initial residual from wA, sumA, rA (Q1) -> the loop decision
+// normFactor and initial residual from wA, sumA, rA (Q1) -> finalize stage 2 (loop decision)
 __global__ void __launch_bounds__(kThreads) k_pc_setup2(int N, const double* __restrict__ wA,
                                                         const double* __restrict__ sumA,
                                                         const double* __restrict__ source,
-                                                        const double* __restrict__ rA, double* part, DevScal* s)
+                                                        const double* __restrict__ rA, double* part, DevScal* s,
+                                                        int fin)
 {
     const double xbar = s->xbar;
-    double v[2] = {0.0, 0.0};
+    double v[3] = {0.0, 0.0, 0.0};
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < N; c += gridDim.x * blockDim.x) {
         const double xref = sumA[c] * xbar;
         v[0] += fabs(wA[c] - xref) + fabs(source[c] - xref);
         v[1] += fabs(rA[c]);
     }
-    if (grid_sum<2>(v, part, &s->ticket[1]) && threadIdx.x == 0) {
-        s->normFactor = v[0] + 1e-20;
-        s->init = v[1] / s->normFactor;
-        s->fin = s->init;
-        s->wArA = 1e300;
-        s->wArAold = 1e300;
-        s->n = 0;
-        s->singular = 0;
-        s->converged = conv(s->fin, s->init, s->tol, s->rel_tol);
-        s->done = !(s->min_iter > 0 || !s->converged);
+    if (grid_sum<3>(v, part, &s->ticket[1]) && threadIdx.x == 0) {
+        if (fin) finalize(s, 2, v);
+        else s->rank_part[0] = v[0], s->rank_part[1] = v[1], s->rank_part[2] = 0.0;
     }
 }
 
@@ -506,25 +508,33 @@ void launch_pc_direction(cudaStream_t s, int N, const double* wA, double* pA, co
 }
 
 void launch_bicg_amul_tmul(cudaStream_t s, const MeshArgs& a, const double* diag, const double* upper,
-                           const double* lower, const double* pA, const double* pT, double* wA, double* wT,
-                           double* part, DevScal* scal)
+                           const double* lower, const double* iface, const double* iface_t, const double* pA,
+                           const double* pT, const double* xr, const double* xrT, double* wA, double* wT,
+                           double* part, DevScal* scal, bool fin)
 {
-    k_bicg_amul_tmul<<<cell_grid(a.N), kThreads, 0, s>>>(a, diag, upper, lower, pA, pT, wA, wT, part, scal);
+    k_bicg_amul_tmul<<<cell_grid(a.N), kThreads, 0, s>>>(a, diag, upper, lower, iface, iface_t, pA, pT, xr, xrT, wA,
+                                                        wT, part, scal, fin ? 1 : 0);
 }
 
 void launch_bicg_update(cudaStream_t s, int N, double* psi, const double* pA, double* rA, const double* wA, double* rT,
-                        const double* wT, double* part, DevScal* scal)
+                        const double* wT, double* part, DevScal* scal, bool fin)
 {
-    k_bicg_update<<<cell_grid(N), kThreads, 0, s>>>(N, psi, pA, rA, wA, rT, wT, part, scal);
+    k_bicg_update<<<cell_grid(N), kThreads, 0, s>>>(N, psi, pA, rA, wA, rT, wT, part, scal, fin ? 1 : 0);
 }
 
-void launch_bicg_setup(cudaStream_t s, const MeshArgs& a, const double* diag, const double* upper,
-                       const double* lower, const double* source, const double* psi, double* wA, double* wT,
-                       double* rA, double* rT, double* sumA, double* part, DevScal* scal)
+void launch_bicg_setup1(cudaStream_t s, const MeshArgs& a, const double* diag, const double* upper,
+                        const double* lower, const double* iface, const double* iface_t, const double* xr,
+                        const double* source, const double* psi, double* wA, double* wT, double* rA, double* rT,
+                        double* sumA, double* part, DevScal* scal, bool fin)
 {
-    k_bicg_setup<<<cell_grid(a.N), kThreads, 0, s>>>(a, diag, upper, lower, source, psi, wA, wT, rA, rT, sumA, part,
-                                                    scal);
-    k_pc_setup2<<<cell_grid(a.N), kThreads, 0, s>>>(a.N, wA, sumA, source, rA, part, scal);
+    k_bicg_setup<<<cell_grid(a.N), kThreads, 0, s>>>(a, diag, upper, lower, iface, iface_t, xr, source, psi, wA, wT,
+                                                    rA, rT, sumA, part, scal, fin ? 1 : 0);
+}
+
+void launch_pc_setup2(cudaStream_t s, int N, const double* wA, const double* sumA, const double* source,
+                      const double* rA, double* part, DevScal* scal, bool fin)
+{
+    k_pc_setup2<<<cell_grid(N), kThreads, 0, s>>>(N, wA, sumA, source, rA, part, scal, fin ? 1 : 0);
 }
 
 void launch_gather_pair(cudaStream_t s, int F, const int* map, const signed char* flip, const double* u,

@@ -160,7 +160,7 @@ def lib():
         if hasattr(L, "spuma_pbicg_solve"):
             L.spuma_pcg_solve_pc.argtypes = [_vp] * 6 + [ctypes.POINTER(SolverControls), ctypes.POINTER(Preconditioner),
                                                          ctypes.POINTER(SolverPerf)]
-            L.spuma_pbicg_solve.argtypes = [_vp] * 6 + [ctypes.POINTER(SolverControls), ctypes.POINTER(Preconditioner),
+            L.spuma_pbicg_solve.argtypes = [_vp] * 8 + [ctypes.POINTER(SolverControls), ctypes.POINTER(Preconditioner),
                                                         ctypes.POINTER(SolverPerf)]
             L.spuma_precondition.argtypes = [_vp] * 4 + [ctypes.POINTER(Preconditioner), _vp, _vp, _ci]
             L.spuma_amul_asym.argtypes = [_vp] * 6 + [_ci]
@@ -372,15 +372,17 @@ class Mesh:
         return perf.as_dict()
 
     def pbicg_solve(self, diag, upper, lower, source, psi, tolerance=1e-6, rel_tol=0.0, max_iter=1000, min_iter=0,
-                    kind=PC_ADILU, n_sweeps=2) -> dict:
-        """spuma_pbicg_solve: PBiCG on an asymmetric LDU matrix."""
+                    kind=PC_ADILU, n_sweeps=2, iface_coeffs=None, iface_coeffs_t=None) -> dict:
+        """spuma_pbicg_solve: PBiCG on an asymmetric LDU matrix (iface_*: decomposed meshes)."""
         ctl, perf, pc = SolverControls(tolerance, rel_tol, max_iter, min_iter), SolverPerf(), Preconditioner(kind, n_sweeps)
         d, kd = _ptr(diag, np.float64)
         u, ku = _ptr(upper, np.float64)
         lo, kl = _ptr(lower, np.float64)
+        f, kf = _ptr(iface_coeffs, np.float64)
+        ft, kft = _ptr(iface_coeffs_t, np.float64)
         s, ks = _ptr(source, np.float64)
         p, kp = _ptr(psi, np.float64)
-        _check(lib().spuma_pbicg_solve(self._h, d, u, lo, s, p, ctypes.byref(ctl), ctypes.byref(pc),
+        _check(lib().spuma_pbicg_solve(self._h, d, u, lo, f, ft, s, p, ctypes.byref(ctl), ctypes.byref(pc),
                                        ctypes.byref(perf)))
         return perf.as_dict()
 

@@ -151,6 +151,30 @@ def _worker(rank, P, how, port, results):
             dist.all_gather(totk, torch.from_numpy(numk))
             errk = np.sqrt(sum(t[0].item() for t in totk) / sum(t[1].item() for t in totk))
             assert errk <= 1e-9, (kind, errk)
+        # PBiCG on an asymmetric decomposed system: Amul / Tmul interface coefficients, pA and
+        # pT halos, processor-local DILU / aDILU (Q31, Q32) vs the decomposed oracle
+        from cases import asym_decomposed
+        asubs, asys, _ = asym_decomposed(m, part, seed=7)
+        A_ = asys[rank]
+        cat = lambda xs: torch.as_tensor(np.concatenate(xs) if xs else np.zeros(1), **f64)
+        for kind, okind in ((S.spuma.PC_ADILU, O.ADILU), (S.spuma.PC_DILU, O.DILU)):
+            def run_gpu(ctl):
+                x = torch.zeros(me.n_cells, **f64)
+                pf = h.pbicg_solve(torch.as_tensor(A_["diag"], **f64), torch.as_tensor(A_["upper"], **f64),
+                                   torch.as_tensor(A_["lower"], **f64), torch.as_tensor(A_["source"], **f64), x,
+                                   *ctl, kind=kind, iface_coeffs=cat(A_["iface"]), iface_coeffs_t=cat(A_["iface_t"]))
+                return x.cpu().numpy(), pf
+            xg, pg = run_gpu((1e-10, 0.0, 1000, 0))
+            xo, po = O.pbicg_decomposed(asubs, asys, None, O.controls(1e-10, 0.0, 1000, 0), okind)
+            assert pg["converged"] and abs(pg["n_iterations"] - po["n_iterations"]) <= 2, (kind, pg, po)
+            nb = min(pg["n_iterations"], po["n_iterations"])
+            xg, _ = run_gpu((0.0, 0.0, nb, nb))
+            xo, _ = O.pbicg_decomposed(asubs, asys, None, O.controls(0.0, 0.0, nb, nb), okind)
+            numb = np.array([np.sum((xg - xo[rank]) ** 2), np.sum(xo[rank] ** 2)])
+            totb = [torch.empty(2, dtype=torch.float64) for _ in range(P)]
+            dist.all_gather(totb, torch.from_numpy(numb))
+            errb = np.sqrt(sum(t[0].item() for t in totb) / sum(t[1].item() for t in totb))
+            assert errb <= 1e-9, (kind, errb)
         # the inline-interface Amul (variant 0: halo before the Amul) gives the same iterates
         h.set_option(S.spuma.OPT_AMUL_VARIANT, 0)
         psi0 = torch.zeros(me.n_cells, **f64)
