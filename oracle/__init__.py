@@ -117,6 +117,12 @@ def _L():
             lib.or_restrict.argtypes = [ci, vp, vp, ci, vp]
             lib.or_gamg.argtypes = [ci, ci] + [vp] * 7 + [ctypes.POINTER(GamgParams), ctypes.POINTER(Controls),
                                                            ctypes.POINTER(Perf), vp, vp]
+            lib.or_gamg_dd.argtypes = [ci, ctypes.POINTER(_Domain), vp, ctypes.POINTER(GamgParams),
+                                       ctypes.POINTER(Controls), ctypes.POINTER(Perf), vp, vp, vp]
+            lib.or_gamg_dd.restype = ci
+            lib.or_gamg_dd_dense_level.argtypes = [ci, ctypes.POINTER(_Domain), vp, ctypes.POINTER(GamgParams),
+                                                   ci, ci, vp, vp]
+            lib.or_gamg_dd_dense_level.restype = ci
             lib.or_pcg_dd_pc.argtypes = [ci, ctypes.POINTER(_Domain), ctypes.POINTER(Controls), ci, ci,
                                          ctypes.POINTER(Perf)]
             lib.or_pbicg_dd.argtypes = [ci, ctypes.POINTER(_Domain), vp, vp, ctypes.POINTER(Controls), ci, ci,
@@ -335,17 +341,13 @@ def pcg(mesh: gen.Mesh, sys: LduSystem, psi0=None, ctl: Optional[Controls] = Non
     return psi[0], perf
 
 
-def pcg_decomposed(meshes: Sequence[gen.Mesh], systems: Sequence[LduSystem], psi0=None,
-                   ctl: Optional[Controls] = None, kind: int = 0, k: int = 2):
-    """O8: PCG over P sub-domains run sequentially; x_remote copied between
-    domains before every Amul; global sums in rank order.  kind != 0: the O12 preconditioner
-    applied per domain on its own faces (processor-local, Q31)."""
-    ctl = ctl or controls()
+def _domains(meshes: Sequence[gen.Mesh], systems, psi0=None):
+    """The O8 domain table: per domain its LDU system, psi (copied), and the interface
+    sources (domain, local cell) of its processor faces in (patch, face) order."""
     P = len(meshes)
     keep = []
     doms = (_Domain * P)()
     psis = []
-    # gid -> (domain, local) lookup for interface sources
     lut = {}
     if P > 1:
         for r, m in enumerate(meshes):
@@ -371,6 +373,17 @@ def pcg_decomposed(meshes: Sequence[gen.Mesh], systems: Sequence[LduSystem], psi
         d.psi = _p(psi)
         d.n_iface = ic.shape[0]
         d.iface_cells, d.iface_coeffs, d.iface_src_domain, d.iface_src_cell = [_p(a) for a in arrs[5:]]
+    return doms, psis, keep
+
+
+def pcg_decomposed(meshes: Sequence[gen.Mesh], systems: Sequence[LduSystem], psi0=None,
+                   ctl: Optional[Controls] = None, kind: int = 0, k: int = 2):
+    """O8: PCG over P sub-domains run sequentially; x_remote copied between
+    domains before every Amul; global sums in rank order.  kind != 0: the O12 preconditioner
+    applied per domain on its own faces (processor-local, Q31)."""
+    ctl = ctl or controls()
+    P = len(meshes)
+    doms, psis, keep = _domains(meshes, systems, psi0)
     perf = Perf()
     if kind:
         rc = _L().or_pcg_dd_pc(P, doms, ctypes.byref(ctl), int(kind), int(k), ctypes.byref(perf))
@@ -379,6 +392,56 @@ def pcg_decomposed(meshes: Sequence[gen.Mesh], systems: Sequence[LduSystem], psi
     if rc:
         raise MemoryError("or_pcg")
     return psis, perf.as_dict()
+
+
+def _weights(meshes, weights):
+    ws = [_f64(m.magSf if weights is None else weights[r]) for r, m in enumerate(meshes)]
+    tab = (ctypes.c_void_p * len(ws))(*[_p(w) for w in ws])
+    return ws, tab
+
+
+def gamg_decomposed(meshes: Sequence[gen.Mesh], systems: Sequence[LduSystem], psi0=None,
+                    ctl: Optional[Controls] = None, params: Optional[GamgParams] = None, weights=None):
+    """O11dd: GAMG over P sub-domains (readings Q36-Q38): processor-local agglomeration,
+    coarse interfaces by first occurrence, decomposed Amul / sums on every level, decomposed
+    PCG on the coarsest level.  Returns (psis, perf dict incl. 'levels', 'level_cells'
+    [[per level] per domain], 'level_ifaces')."""
+    ctl = ctl or controls()
+    gp = params or gamg_params()
+    P = len(meshes)
+    doms, psis, keep = _domains(meshes, systems, psi0)
+    ws, tab = _weights(meshes, weights)
+    nl = ctypes.c_int(0)
+    cells = np.zeros(64 * P, np.int32)
+    ifs = np.zeros(64 * P, np.int32)
+    perf = Perf()
+    rc = _L().or_gamg_dd(P, doms, ctypes.addressof(tab), ctypes.byref(gp), ctypes.byref(ctl), ctypes.byref(perf),
+                         ctypes.addressof(nl), _p(cells), _p(ifs))
+    if rc:
+        raise ValueError("or_gamg_dd")
+    out = perf.as_dict()
+    out["levels"] = nl.value
+    out["level_cells"] = [cells[64 * r:64 * r + nl.value].tolist() for r in range(P)]
+    out["level_ifaces"] = [ifs[64 * r:64 * r + nl.value].tolist() for r in range(P)]
+    return psis, out
+
+
+def gamg_dd_dense_level(meshes: Sequence[gen.Mesh], systems: Sequence[LduSystem], level: int,
+                        params: Optional[GamgParams] = None, weights=None, cap: int = 2048):
+    """O11dd: the global operator of one level of the decomposed hierarchy (dense, cells
+    domain-major) and the global fine-to-coarse map into it (level > 0), for the Galerkin pin."""
+    gp = params or gamg_params()
+    P = len(meshes)
+    doms, _, keep = _domains(meshes, systems)
+    ws, tab = _weights(meshes, weights)
+    A = np.zeros(cap * cap)
+    nfine = sum(m.n_cells for m in meshes)
+    ftc = np.zeros(nfine + 1, np.int32)
+    n = _L().or_gamg_dd_dense_level(P, doms, ctypes.addressof(tab), ctypes.byref(gp), int(level), int(cap),
+                                    _p(A), _p(ftc))
+    if n < 0:
+        raise ValueError("no such level or capacity too small")
+    return A[:n * n].reshape(n, n).copy(), ftc
 
 
 def agglomerate(n_cells: int, owner, neighbour, weights):

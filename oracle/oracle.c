@@ -25,6 +25,8 @@
  *                   P:509
  *   O11 GAMG        or_agglomerate, or_coarse_addressing, or_agglomerate_matrix, or_restrict, or_gamg
  *                   P:517
+ *   O11dd GAMG dd   or_gamg_dd, or_gamg_dd_dense_level (decomposed hierarchy, coarse interfaces;
+ *                   readings Q36-Q38)
  *
  * Pins (tests/test_oracle_*.py, -m "not gpu"): SPEC chain examples,
  * closed-form Poisson eigenmodes (Dirichlet / Neumann) and linear exactness,
@@ -1084,6 +1086,418 @@ int or_gamg(int n, int F, const int* owner, const int* neighbour, const double* 
     free(sumA);
     free(r);
     return 0;
+}
+
+/* ------------------------------------------------------------------------- */
+/* O11dd GAMG on a decomposed mesh (nd domains; readings Q36-Q38, DESIGN.md   */
+/* §3).  OpenFOAM's parallel GAMG keeps the agglomeration processor-local and */
+/* agglomerates the processor interfaces alongside ([OF] GAMGAgglomeration,   */
+/* processorGAMGInterface); the paper runs GAMG decomposed on 1-8 GPUs with   */
+/* the coarsening unchanged.                        */
+/*   Q36 levels: every domain agglomerates its own internal faces (Q22); a    */
+/*       level is added while sum_p n_p > nd * nCellsInCoarsestLevel and the  */
+/*       pass reduces sum_p n_p (nd = 1: exactly Q22's rule).                 */
+/*   Q37 coarse interfaces: per domain, the fine interface faces in their     */
+/*       (patch, face) order map to coarse interface faces = distinct         */
+/*       (neighbour domain, local coarse cell, remote coarse cell) triples    */
+/*       numbered by first occurrence; coefficient = sum of the fine ones in  */
+/*       ascending fine order (both sides see the same faces in the same      */
+/*       order, Q13, so both get bitwise the same coarse coefficients).       */
+/*   Q38 cycle: the single-domain V-cycle (Q23-Q30) with every A x a          */
+/*       decomposed Amul (remote x copied across the interfaces first), every */
+/*       dot a per-domain sum added in domain order, the two-stage GS lower   */
+/*       sweep domain-local (like DILU, Q31), and the coarsest level solved   */
+/*       by the decomposed PCG (O8) over the coarsest interfaces.             */
+/* ------------------------------------------------------------------------- */
+
+typedef struct {
+    or_level l;          /* per-domain level (borrowed arrays on level 0) */
+    int n_if;
+    int *if_cell, *if_src_dom, *if_src_cell;
+    double* if_coef;
+    int* if_restrict;    /* fine interface face -> coarse interface face of the next level */
+    double* xr;
+} or_dlevel;
+
+static void or_dd_amul(int nd, or_dlevel* L, double* const* x, double* const* y)
+{
+    for (int p = 0; p < nd; ++p)
+        for (int i = 0; i < L[p].n_if; ++i) L[p].xr[i] = x[L[p].if_src_dom[i]][L[p].if_src_cell[i]];
+    for (int p = 0; p < nd; ++p)
+        or_amul(L[p].l.n, L[p].l.F, L[p].l.owner, L[p].l.neighbour, L[p].l.diag, L[p].l.upper, L[p].l.upper, x[p],
+                L[p].n_if, L[p].if_cell, L[p].if_coef, L[p].xr, y[p]);
+}
+
+/* y_p = A x_p over all domains with x = the level's x (or c when use_c) */
+static void or_dd_amul_field(int nd, or_dlevel* L, int use_c)
+{
+    double* X[256];
+    double* Y[256];
+    for (int p = 0; p < nd; ++p) {
+        X[p] = use_c ? L[p].l.c : L[p].l.x;
+        Y[p] = L[p].l.y;
+    }
+    or_dd_amul(nd, L, X, Y);
+}
+
+/* Build the decomposed hierarchy (Q36, Q37) and, with diag != NULL, the Galerkin matrices
+ * (Q27 per domain + coarse interface coefficients).  Returns the number of levels. */
+static int or_dd_build(int nd, const or_domain* D, const double* const* weights, const or_gamg_params* gp,
+                       or_dlevel** Lv, int max_out)
+{
+    Lv[0] = (or_dlevel*)calloc((size_t)nd, sizeof(or_dlevel));
+    for (int p = 0; p < nd; ++p) {
+        or_dlevel* d = &Lv[0][p];
+        d->l.n = D[p].n_cells;
+        d->l.F = D[p].n_faces;
+        d->l.owner = (int*)D[p].owner;
+        d->l.neighbour = (int*)D[p].neighbour;
+        d->l.w = (double*)weights[p];
+        d->l.diag = (double*)D[p].diag;
+        d->l.upper = (double*)D[p].upper;
+        d->n_if = D[p].n_iface;
+        d->if_cell = (int*)D[p].iface_cells;
+        d->if_src_dom = (int*)D[p].iface_src_domain;
+        d->if_src_cell = (int*)D[p].iface_src_cell;
+        d->if_coef = (double*)D[p].iface_coeffs;
+    }
+    int nl = 1;
+    for (;;) {
+        or_dlevel* F = Lv[nl - 1];
+        long long nfine = 0;
+        for (int p = 0; p < nd; ++p) nfine += F[p].l.n;
+        if (!(nl < max_out && nl < gp->max_levels && nfine > (long long)nd * gp->n_coarsest_cells)) break;
+        long long ncoarse = 0;
+        int* nc = (int*)calloc((size_t)nd, sizeof(int));
+        for (int p = 0; p < nd; ++p) {
+            F[p].l.ftc = (int*)malloc(sizeof(int) * (size_t)(F[p].l.n + 1));
+            nc[p] = or_agglomerate(F[p].l.n, F[p].l.F, F[p].l.owner, F[p].l.neighbour, F[p].l.w, F[p].l.ftc);
+            ncoarse += nc[p];
+        }
+        if (ncoarse >= nfine) {
+            for (int p = 0; p < nd; ++p) {
+                free(F[p].l.ftc);
+                F[p].l.ftc = 0;
+            }
+            free(nc);
+            break;
+        }
+        or_dlevel* C = (or_dlevel*)calloc((size_t)nd, sizeof(or_dlevel));
+        for (int p = 0; p < nd; ++p) {
+            or_level* L = &F[p].l;
+            or_level* K = &C[p].l;
+            K->owner = (int*)malloc(sizeof(int) * (size_t)(L->F + 1));
+            K->neighbour = (int*)malloc(sizeof(int) * (size_t)(L->F + 1));
+            K->w = (double*)malloc(sizeof(double) * (size_t)(L->F + 1));
+            L->frestrict = (int*)malloc(sizeof(int) * (size_t)(L->F + 1));
+            K->F = or_coarse_addressing(L->F, L->owner, L->neighbour, L->ftc, L->w, K->owner, K->neighbour,
+                                        L->frestrict, K->w);
+            K->n = nc[p];
+            /* Q37: coarse interface faces by first occurrence of (domain, local, remote) */
+            const int m = F[p].n_if;
+            C[p].if_cell = (int*)malloc(sizeof(int) * (size_t)(m + 1));
+            C[p].if_src_dom = (int*)malloc(sizeof(int) * (size_t)(m + 1));
+            C[p].if_src_cell = (int*)malloc(sizeof(int) * (size_t)(m + 1));
+            F[p].if_restrict = (int*)malloc(sizeof(int) * (size_t)(m + 1));
+            int k = 0;
+            for (int i = 0; i < m; ++i) {
+                const int q = F[p].if_src_dom[i];
+                const int a = L->ftc[F[p].if_cell[i]];
+                const int b = F[q].l.ftc[F[p].if_src_cell[i]];
+                int j = 0;
+                while (j < k && !(C[p].if_src_dom[j] == q && C[p].if_cell[j] == a && C[p].if_src_cell[j] == b)) ++j;
+                if (j == k) {
+                    C[p].if_src_dom[k] = q;
+                    C[p].if_cell[k] = a;
+                    C[p].if_src_cell[k] = b;
+                    ++k;
+                }
+                F[p].if_restrict[i] = j;
+            }
+            C[p].n_if = k;
+        }
+        free(nc);
+        Lv[nl++] = C;
+    }
+    for (int p = 0; p < nd; ++p) {
+        Lv[nl - 1][p].l.ftc = 0;
+        Lv[nl - 1][p].l.frestrict = 0;
+        Lv[nl - 1][p].if_restrict = 0;
+    }
+    /* Galerkin matrices (Q27) + coarse interface coefficients (Q37) */
+    for (int l = 1; l < nl; ++l)
+        for (int p = 0; p < nd; ++p) {
+            or_dlevel* f = &Lv[l - 1][p];
+            or_dlevel* c = &Lv[l][p];
+            c->l.diag = (double*)calloc((size_t)c->l.n + 1, sizeof(double));
+            c->l.upper = (double*)calloc((size_t)c->l.F + 1, sizeof(double));
+            or_agglomerate_matrix(f->l.n, f->l.F, f->l.owner, f->l.ftc, f->l.frestrict, f->l.diag, f->l.upper,
+                                  c->l.n, c->l.F, c->l.diag, c->l.upper);
+            c->if_coef = (double*)calloc((size_t)c->n_if + 1, sizeof(double));
+            for (int i = 0; i < f->n_if; ++i) c->if_coef[f->if_restrict[i]] += f->if_coef[i];
+        }
+    for (int l = 0; l < nl; ++l)
+        for (int p = 0; p < nd; ++p) {
+            or_level* L = &Lv[l][p].l;
+            const size_t m = (size_t)L->n + 1;
+            L->b = (double*)calloc(m, sizeof(double));
+            L->x = (double*)calloc(m, sizeof(double));
+            L->r = (double*)calloc(m, sizeof(double));
+            L->y = (double*)calloc(m, sizeof(double));
+            L->c = (double*)calloc(m, sizeof(double));
+            L->rD = (double*)calloc(m, sizeof(double));
+            for (int i = 0; i < L->n; ++i) L->rD[i] = 1.0 / L->diag[i];
+            Lv[l][p].xr = (double*)calloc((size_t)Lv[l][p].n_if + 1, sizeof(double));
+        }
+    return nl;
+}
+
+static void or_dd_free(int nd, or_dlevel** Lv, int nl)
+{
+    for (int l = 0; l < nl; ++l) {
+        for (int p = 0; p < nd; ++p) {
+            or_dlevel* d = &Lv[l][p];
+            or_level* L = &d->l;
+            free(L->b); free(L->x); free(L->r); free(L->y); free(L->c); free(L->rD);
+            free(L->ftc); free(L->frestrict); free(d->if_restrict); free(d->xr);
+            if (l > 0) {
+                free(L->diag); free(L->upper); free(L->owner); free(L->neighbour); free(L->w);
+                free(d->if_cell); free(d->if_src_dom); free(d->if_src_cell); free(d->if_coef);
+            }
+        }
+        free(Lv[l]);
+    }
+}
+
+static void or_dd_smooth(int nd, or_dlevel* Lv, const or_gamg_params* gp)
+{
+    or_dd_amul_field(nd, Lv, 0);
+    for (int p = 0; p < nd; ++p) {
+        or_level* L = &Lv[p].l;
+        if (gp->smoother != 1) {
+            for (int i = 0; i < L->n; ++i) L->x[i] = L->x[i] + gp->omega * (L->rD[i] * (L->b[i] - L->y[i]));
+            continue;
+        }
+        /* two-stage Gauss-Seidel (Q30), the lower sweep on the domain's own faces (Q38) */
+        double* r = (double*)malloc(sizeof(double) * (size_t)(L->n + 1));
+        double* z = (double*)malloc(sizeof(double) * (size_t)(L->n + 1));
+        double* t = (double*)malloc(sizeof(double) * (size_t)(L->n + 1));
+        for (int i = 0; i < L->n; ++i) {
+            r[i] = L->b[i] - L->y[i];
+            z[i] = L->rD[i] * r[i];
+        }
+        for (int k = 0; k < gp->n_inner; ++k) {
+            for (int i = 0; i < L->n; ++i) t[i] = r[i];
+            for (int f = 0; f < L->F; ++f) t[L->neighbour[f]] -= L->upper[f] * z[L->owner[f]];
+            for (int i = 0; i < L->n; ++i) z[i] = L->rD[i] * t[i];
+        }
+        for (int i = 0; i < L->n; ++i) L->x[i] = L->x[i] + z[i];
+        free(r);
+        free(z);
+        free(t);
+    }
+}
+
+/* Q25 over domains: alpha = (sum_p c.r) / (sum_p Ac.c), clamped to [0, 2] */
+static void or_dd_scale(int nd, or_dlevel* Lv)
+{
+    or_dd_amul_field(nd, Lv, 1);
+    double num = 0.0, den = 0.0;
+    for (int p = 0; p < nd; ++p) {
+        or_level* L = &Lv[p].l;
+        double s = 0.0;
+        for (int i = 0; i < L->n; ++i) s += L->c[i] * L->r[i];
+        num += s;
+    }
+    for (int p = 0; p < nd; ++p) {
+        or_level* L = &Lv[p].l;
+        double s = 0.0;
+        for (int i = 0; i < L->n; ++i) s += L->y[i] * L->c[i];
+        den += s;
+    }
+    double a = fabs(den) > 1e-300 ? num / den : 1.0;
+    if (a < 0.0) a = 0.0;
+    if (a > 2.0) a = 2.0;
+    for (int p = 0; p < nd; ++p)
+        for (int i = 0; i < Lv[p].l.n; ++i) Lv[p].l.c[i] = a * Lv[p].l.c[i];
+}
+
+static void or_dd_coarsest(int nd, or_dlevel* Lv, const or_gamg_params* gp)
+{
+    or_domain* d = (or_domain*)calloc((size_t)nd, sizeof(or_domain));
+    for (int p = 0; p < nd; ++p) {
+        or_level* L = &Lv[p].l;
+        for (int i = 0; i < L->n; ++i) L->x[i] = 0.0;
+        or_domain q = {L->n, L->F, L->owner, L->neighbour, L->diag, L->upper, L->b, L->x,
+                       Lv[p].n_if, Lv[p].if_cell, Lv[p].if_coef, Lv[p].if_src_dom, Lv[p].if_src_cell};
+        d[p] = q;
+    }
+    or_controls c = {gp->coarsest_tol, gp->coarsest_rel_tol, gp->coarsest_max_iter, 0};
+    or_perf pf;
+    or_pcg(nd, d, &c, &pf);
+    free(d);
+}
+
+static void or_dd_vcycle(int nd, int nl, or_dlevel** Lv, const or_gamg_params* gp)
+{
+    for (int l = 0; l < nl - 1; ++l) {
+        for (int p = 0; p < nd; ++p)
+            for (int i = 0; i < Lv[l][p].l.n; ++i) Lv[l][p].l.x[i] = 0.0;
+        for (int s = 0; s < gp->n_pre; ++s) or_dd_smooth(nd, Lv[l], gp);
+        or_dd_amul_field(nd, Lv[l], 0);
+        for (int p = 0; p < nd; ++p) {
+            or_level* L = &Lv[l][p].l;
+            for (int i = 0; i < L->n; ++i) L->r[i] = L->b[i] - L->y[i];
+            or_restrict(L->n, L->ftc, L->r, Lv[l + 1][p].l.n, Lv[l + 1][p].l.b);
+        }
+    }
+    or_dd_coarsest(nd, Lv[nl - 1], gp);
+    for (int l = nl - 2; l >= 0; --l) {
+        for (int p = 0; p < nd; ++p) {
+            or_level* L = &Lv[l][p].l;
+            for (int i = 0; i < L->n; ++i) L->c[i] = Lv[l + 1][p].l.x[L->ftc[i]];
+        }
+        if (gp->scale) or_dd_scale(nd, Lv[l]);
+        for (int p = 0; p < nd; ++p) {
+            or_level* L = &Lv[l][p].l;
+            for (int i = 0; i < L->n; ++i) L->x[i] = L->x[i] + L->c[i];
+        }
+        for (int s = 0; s < gp->n_post; ++s) or_dd_smooth(nd, Lv[l], gp);
+    }
+}
+
+/* Decomposed GAMG solve (Q36-Q38 + the outer loop of Q28 with decomposed sums, as O8).
+ * level_cells[p * 64 + l] / level_ifaces[p * 64 + l]: per-domain level sizes (may be NULL). */
+int or_gamg_dd(int nd, or_domain* D, const double* const* weights, const or_gamg_params* gp, const or_controls* ctl,
+               or_perf* perf, int* levels_out, int* level_cells, int* level_ifaces)
+{
+    if (nd < 1 || nd > 256) return 1;
+    or_dlevel* Lv[64];
+    const int nl = or_dd_build(nd, D, weights, gp, Lv, 64);
+    if (levels_out) *levels_out = nl;
+    for (int p = 0; p < nd; ++p)
+        for (int l = 0; l < nl; ++l) {
+            if (level_cells) level_cells[p * 64 + l] = Lv[l][p].l.n;
+            if (level_ifaces) level_ifaces[p * 64 + l] = Lv[l][p].n_if;
+        }
+    double* wA[256];
+    double* r[256];
+    double* sumA[256];
+    double* psi[256];
+    for (int p = 0; p < nd; ++p) {
+        wA[p] = (double*)calloc((size_t)D[p].n_cells + 1, sizeof(double));
+        r[p] = (double*)calloc((size_t)D[p].n_cells + 1, sizeof(double));
+        sumA[p] = (double*)calloc((size_t)D[p].n_cells + 1, sizeof(double));
+        psi[p] = D[p].psi;
+    }
+    /* residual and normFactor exactly as the decomposed PCG (Q1, O8) */
+    or_dd_amul(nd, Lv[0], psi, wA);
+    double spsi = 0.0, ncell = 0.0;
+    for (int p = 0; p < nd; ++p) {
+        double s = 0.0;
+        for (int c = 0; c < D[p].n_cells; ++c) s += psi[p][c];
+        spsi += s;
+        ncell += (double)D[p].n_cells;
+    }
+    const double xbar = spsi / ncell;
+    double normFactor = 0.0, smag = 0.0;
+    for (int p = 0; p < nd; ++p) {
+        or_sumA(D[p].n_cells, D[p].n_faces, D[p].owner, D[p].neighbour, D[p].diag, D[p].upper, D[p].upper,
+                D[p].n_iface, D[p].iface_cells, D[p].iface_coeffs, sumA[p]);
+        double s = 0.0;
+        for (int c = 0; c < D[p].n_cells; ++c) {
+            const double xref = sumA[p][c] * xbar;
+            s += fabs(wA[p][c] - xref) + fabs(D[p].source[c] - xref);
+        }
+        normFactor += s;
+    }
+    normFactor += 1e-20;
+    for (int p = 0; p < nd; ++p) {
+        double s = 0.0;
+        for (int c = 0; c < D[p].n_cells; ++c) {
+            r[p][c] = D[p].source[c] - wA[p][c];
+            s += fabs(r[p][c]);
+        }
+        smag += s;
+    }
+    perf->initial_residual = smag / normFactor;
+    perf->final_residual = perf->initial_residual;
+    perf->n_iterations = 0;
+    perf->singular = 0;
+    if (ctl->min_iter > 0 || !or_conv(perf->final_residual, perf->initial_residual, ctl)) {
+        do {
+            for (int p = 0; p < nd; ++p)
+                for (int c = 0; c < D[p].n_cells; ++c) Lv[0][p].l.b[c] = r[p][c];
+            if (nl == 1) or_dd_coarsest(nd, Lv[0], gp);
+            else or_dd_vcycle(nd, nl, Lv, gp);
+            for (int p = 0; p < nd; ++p)
+                for (int c = 0; c < D[p].n_cells; ++c) psi[p][c] = psi[p][c] + Lv[0][p].l.x[c];
+            or_dd_amul(nd, Lv[0], psi, wA);
+            smag = 0.0;
+            for (int p = 0; p < nd; ++p) {
+                double s = 0.0;
+                for (int c = 0; c < D[p].n_cells; ++c) {
+                    r[p][c] = D[p].source[c] - wA[p][c];
+                    s += fabs(r[p][c]);
+                }
+                smag += s;
+            }
+            perf->final_residual = smag / normFactor;
+        } while ((++perf->n_iterations < ctl->max_iter && !or_conv(perf->final_residual, perf->initial_residual, ctl)) ||
+                 perf->n_iterations < ctl->min_iter);
+    }
+    perf->converged = or_conv(perf->final_residual, perf->initial_residual, ctl);
+    for (int p = 0; p < nd; ++p) {
+        free(wA[p]);
+        free(r[p]);
+        free(sumA[p]);
+    }
+    or_dd_free(nd, Lv, nl);
+    return 0;
+}
+
+/* The global operator of level `level` of the decomposed hierarchy as a dense matrix (cells
+ * numbered domain-major: domain p's cells after those of domains < p) and, for level > 0, the
+ * global fine-to-coarse map of level - 1 -- for the Galerkin pin R^T A R (tests only).
+ * Returns the global cell count of the level, or -1 (no such level / capacity too small). */
+int or_gamg_dd_dense_level(int nd, const or_domain* D, const double* const* weights, const or_gamg_params* gp,
+                           int level, int cap, double* A, int* ftc_global)
+{
+    if (nd < 1 || nd > 256) return -1;
+    or_dlevel* Lv[64];
+    const int nl = or_dd_build(nd, D, weights, gp, Lv, 64);
+    int ret = -1;
+    if (level >= 0 && level < nl) {
+        int off[257];
+        off[0] = 0;
+        for (int p = 0; p < nd; ++p) off[p + 1] = off[p] + Lv[level][p].l.n;
+        const int n = off[nd];
+        if (n <= cap) {
+            for (int i = 0; i < n * n; ++i) A[i] = 0.0;
+            for (int p = 0; p < nd; ++p) {
+                const or_dlevel* d = &Lv[level][p];
+                for (int c = 0; c < d->l.n; ++c) A[(off[p] + c) * n + off[p] + c] += d->l.diag[c];
+                for (int f = 0; f < d->l.F; ++f) {
+                    const int o = off[p] + d->l.owner[f], nb = off[p] + d->l.neighbour[f];
+                    A[o * n + nb] += d->l.upper[f];
+                    A[nb * n + o] += d->l.upper[f];
+                }
+                for (int i = 0; i < d->n_if; ++i)
+                    A[(off[p] + d->if_cell[i]) * n + off[d->if_src_dom[i]] + d->if_src_cell[i]] += d->if_coef[i];
+            }
+            if (level > 0 && ftc_global) {
+                int offf[257];
+                offf[0] = 0;
+                for (int p = 0; p < nd; ++p) offf[p + 1] = offf[p] + Lv[level - 1][p].l.n;
+                for (int p = 0; p < nd; ++p)
+                    for (int i = 0; i < Lv[level - 1][p].l.n; ++i)
+                        ftc_global[offf[p] + i] = off[p] + Lv[level - 1][p].l.ftc[i];
+            }
+            ret = n;
+        }
+    }
+    or_dd_free(nd, Lv, nl);
+    return ret;
 }
 
 /* ------------------------------------------------------------------------- */
