@@ -214,8 +214,13 @@ void spuma_gamg_default_params(spuma_gamg_params* p);
  * The level hierarchy depends only on the mesh, n_cells_in_coarsest_level and max_levels:
  * it is built on the host at the first call (and when those change) and kept by the
  * handle; every call re-forms the coarse matrices from diag/upper on the device.
- * perf->n_iterations counts V-cycles.  Single-rank handles only (n_ranks > 1 ->
- * SPUMA_ERR_STATE: coarse-level processor interfaces are out of scope, Q28).
+ * perf->n_iterations counts V-cycles.  Decomposed meshes (n_ranks > 1; collective, every
+ * rank calls it; iface_coeffs as spuma_pcg_solve): readings Q36-Q38 -- processor-local
+ * agglomeration with the level count decided on the global cell count, coarse processor
+ * interfaces = distinct (local, remote) agglomerate pairs by first occurrence with summed
+ * coefficients, the halo of every gathered vector before each row kernel, rank-order sums
+ * for the scale factors and the residual, and PCG + diagonal over all ranks on the
+ * coarsest level; V-cycles are launched directly (not captured).
  * Errors: INVALID_ARGUMENT (NULL arrays/perf, negative limits, max_levels < 1,
  * n_post_sweeps/n_pre_sweeps < 0), STATE, CUDA, OUT_OF_MEMORY.
  */

@@ -282,24 +282,61 @@ spuma_status halo_exchange(spuma_mesh m, const double* x, double* xr, cudaStream
     return SPUMA_OK;
 }
 
-// every rank gets all ranks' 4 partials (rank order) and finalises identically
-spuma_status reduce_finalize(spuma_mesh m, int stage, cudaStream_t s)
+// all ranks' 4 partials (device, [4]) into out ([4 * n_ranks], rank order) on stream s
+spuma_status allgather4(spuma_mesh m, const double* in, double* out, cudaStream_t s)
 {
-    double* gathered = m->ws.part;  // free after the reduction kernel finished
     if (m->external_comm) {
         if (!m->cb.allgather) return set_error(SPUMA_ERR_STATE, "external comm: callbacks not set");
-        SPUMA_CUDA(cudaMemcpyAsync(m->h_part, m->ws.scal->rank_part, 4 * sizeof(double), cudaMemcpyDeviceToHost, s));
+        SPUMA_CUDA(cudaMemcpyAsync(m->h_part, in, 4 * sizeof(double), cudaMemcpyDeviceToHost, s));
         SPUMA_CUDA(cudaStreamSynchronize(s));
         if (m->cb.allgather(m->cb.ctx, m->h_part, m->h_part + 4, 4) != 0)
             return set_error(SPUMA_ERR_NCCL, "external comm: allgather callback failed");
-        SPUMA_CUDA(cudaMemcpyAsync(gathered, m->h_part + 4, 4 * sizeof(double) * m->n_ranks, cudaMemcpyHostToDevice, s));
-        launch_finalize(s, stage, gathered, m->n_ranks, m->ws);
-        m->stats.kernel_launches += 1;
+        SPUMA_CUDA(cudaMemcpyAsync(out, m->h_part + 4, 4 * sizeof(double) * m->n_ranks, cudaMemcpyHostToDevice, s));
         return SPUMA_OK;
     }
-    SPUMA_NCCL(ncclAllGather(m->ws.scal->rank_part, gathered, 4, ncclDouble, m->comm, s));
-    launch_finalize(s, stage, gathered, m->n_ranks, m->ws);
+    SPUMA_NCCL(ncclAllGather(in, out, 4, ncclDouble, m->comm, s));
+    return SPUMA_OK;
+}
+
+// every rank gets all ranks' 4 partials (rank order) and finalises identically
+spuma_status reduce_finalize_ws(spuma_mesh m, const Workspace& w, int stage, cudaStream_t s)
+{
+    double* gathered = w.part;  // free after the reduction kernel finished
+    SPUMA_TRY(allgather4(m, w.scal->rank_part, gathered, s));
+    launch_finalize(s, stage, gathered, m->n_ranks, w);
     m->stats.kernel_launches += 1;
+    return SPUMA_OK;
+}
+
+spuma_status reduce_finalize(spuma_mesh m, int stage, cudaStream_t s) { return reduce_finalize_ws(m, m->ws, stage, s); }
+
+// processor-patch exchange of a level's interface values (device buffers; per-patch counts of
+// the level, peers and order of level 0's patches): recv[offset_p ..) <- the neighbour's send
+spuma_status exchange_counts(spuma_mesh m, const std::vector<int>& counts, const double* send, double* recv,
+                             cudaStream_t s)
+{
+    int n = 0;
+    std::vector<int> offsets(counts.size());
+    for (size_t p = 0; p < counts.size(); ++p) offsets[p] = n, n += counts[p];
+    if (m->external_comm) {
+        if (!m->cb.exchange) return set_error(SPUMA_ERR_STATE, "external comm: callbacks not set");
+        std::vector<double> hs(n + 1), hr(n + 1);
+        if (n) SPUMA_CUDA(cudaMemcpyAsync(hs.data(), send, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+        SPUMA_CUDA(cudaStreamSynchronize(s));
+        if (m->cb.exchange(m->cb.ctx, (int)counts.size(), m->cb_peers.data(), offsets.data(), counts.data(), hs.data(),
+                           hr.data()) != 0)
+            return set_error(SPUMA_ERR_NCCL, "external comm: exchange callback failed");
+        if (n) SPUMA_CUDA(cudaMemcpyAsync(recv, hr.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s));
+        SPUMA_CUDA(cudaStreamSynchronize(s));  // hr is a stack buffer
+        return SPUMA_OK;
+    }
+    SPUMA_NCCL(ncclGroupStart());
+    for (size_t p = 0; p < counts.size(); ++p) {
+        if (counts[p] == 0) continue;
+        SPUMA_NCCL(ncclSend(send + offsets[p], counts[p], ncclDouble, m->cb_peers[p], m->comm, s));
+        SPUMA_NCCL(ncclRecv(recv + offsets[p], counts[p], ncclDouble, m->cb_peers[p], m->comm, s));
+    }
+    SPUMA_NCCL(ncclGroupEnd());
     return SPUMA_OK;
 }
 
@@ -456,6 +493,11 @@ struct GamgState {
     int gkey_tail = -1;                              // tail threshold the graph was captured with
     int launches_per_cycle = 0;
     spuma::GLevel* d_lv = nullptr;                   // device copy of lv (the single-CTA tail reads it)
+    // n_ranks > 1 (readings Q36-Q38): per-level per-patch interface counts, this rank's
+    // reduction partials and the gathered ones
+    std::vector<std::vector<int>> if_count;
+    double *rank_part = nullptr, *gathered = nullptr;
+    bool dd = false;
 };
 
 namespace {
@@ -489,6 +531,51 @@ spuma_status gupload(GamgState* G, T** p, const std::vector<T>& v, cudaStream_t 
     return SPUMA_OK;
 }
 
+// host collectives of the decomposed hierarchy build (GamgComm, gamg_host.cpp)
+bool host_allgather4(void* ctx, const double* in, double* out)
+{
+    spuma_mesh m = static_cast<spuma_mesh>(ctx);
+    if (m->external_comm) return m->cb.allgather && m->cb.allgather(m->cb.ctx, in, out, 4) == 0;
+    double* d = nullptr;
+    if (cudaMalloc(reinterpret_cast<void**>(&d), sizeof(double) * 4 * (m->n_ranks + 1)) != cudaSuccess) return false;
+    bool ok = cudaMemcpy(d, in, 4 * sizeof(double), cudaMemcpyHostToDevice) == cudaSuccess &&
+              ncclAllGather(d, d + 4, 4, ncclDouble, m->comm, m->stream) == ncclSuccess &&
+              cudaMemcpyAsync(out, d + 4, 4 * sizeof(double) * m->n_ranks, cudaMemcpyDeviceToHost, m->stream) ==
+                  cudaSuccess &&
+              cudaStreamSynchronize(m->stream) == cudaSuccess;
+    cudaFree(d);
+    return ok;
+}
+
+bool host_exchange(void* ctx, const std::vector<int>& counts, const std::vector<double>& send,
+                   std::vector<double>& recv)
+{
+    spuma_mesh m = static_cast<spuma_mesh>(ctx);
+    const size_t n = send.size();
+    if (m->external_comm) {
+        std::vector<int> offsets(counts.size());
+        int o = 0;
+        for (size_t p = 0; p < counts.size(); ++p) offsets[p] = o, o += counts[p];
+        std::vector<double> hs(send), hr(n + 1);
+        hs.push_back(0.0);
+        if (!m->cb.exchange ||
+            m->cb.exchange(m->cb.ctx, (int)counts.size(), m->cb_peers.data(), offsets.data(), counts.data(), hs.data(),
+                           hr.data()) != 0)
+            return false;
+        recv.assign(hr.begin(), hr.begin() + n);
+        return true;
+    }
+    double* d = nullptr;
+    if (cudaMalloc(reinterpret_cast<void**>(&d), sizeof(double) * (2 * n + 1)) != cudaSuccess) return false;
+    bool ok = (n == 0 || cudaMemcpy(d, send.data(), sizeof(double) * n, cudaMemcpyHostToDevice) == cudaSuccess) &&
+              exchange_counts(m, counts, d, d + n, m->stream) == SPUMA_OK &&
+              (n == 0 || cudaMemcpyAsync(recv.data(), d + n, sizeof(double) * n, cudaMemcpyDeviceToHost, m->stream) ==
+                             cudaSuccess) &&
+              cudaStreamSynchronize(m->stream) == cudaSuccess;
+    cudaFree(d);
+    return ok;
+}
+
 spuma_status gamg_ensure(spuma_mesh m, const spuma_gamg_params& gp)
 {
     if (m->gamg && m->gamg->n_coarsest == gp.n_cells_in_coarsest_level && m->gamg->max_levels == gp.max_levels)
@@ -499,11 +586,26 @@ spuma_status gamg_ensure(spuma_mesh m, const spuma_gamg_params& gp)
     if (m->F) SPUMA_CUDA(cudaMemcpy(w.data(), m->d_magSf, sizeof(double) * m->F, cudaMemcpyDeviceToHost));
     std::vector<int> ownerLo(m->F);
     for (int k = 0; k < m->F; ++k) ownerLo[k] = m->h_owner[m->h_losort[k]];
-    std::vector<GamgHostLevel> H =
-        gamg_hierarchy(m->N, m->F, m->h_owner, m->h_neighbour, m->h_ownerStart, m->h_losortStart, m->h_losort,
-                       ownerLo, w, gp.n_cells_in_coarsest_level, gp.max_levels);
+    const bool dd = m->n_ranks > 1;
+    std::vector<GamgHostLevel> H;
+    if (dd) {  // decomposed hierarchy (Q36, Q37): collective over the ranks
+        GamgComm comm;
+        comm.n_ranks = m->n_ranks;
+        comm.allgather4 = host_allgather4;
+        comm.exchange = host_exchange;
+        comm.ctx = m;
+        bool ok = true;
+        H = gamg_hierarchy_dd(m->N, m->F, m->h_owner, m->h_neighbour, m->h_ownerStart, m->h_losortStart, m->h_losort,
+                              ownerLo, w, m->h_if_cell, m->cb_counts, gp.n_cells_in_coarsest_level, gp.max_levels,
+                              comm, &ok);
+        if (!ok) return set_error(SPUMA_ERR_NCCL, "GAMG hierarchy: collective failed");
+    } else {
+        H = gamg_hierarchy(m->N, m->F, m->h_owner, m->h_neighbour, m->h_ownerStart, m->h_losortStart, m->h_losort,
+                           ownerLo, w, gp.n_cells_in_coarsest_level, gp.max_levels);
+    }
     GamgState* G = new GamgState();
     m->gamg = G;
+    G->dd = dd;
     G->n_coarsest = gp.n_cells_in_coarsest_level;
     G->max_levels = gp.max_levels;
     const int nl = (int)H.size();
@@ -570,6 +672,35 @@ spuma_status gamg_ensure(spuma_mesh m, const spuma_gamg_params& gp)
         SPUMA_TRY(galloc(G, &L.q, n));
         L.grid = gamg_grid(n);
         max_grid = std::max(max_grid, L.grid);
+        if (dd) {  // processor interfaces of the level (a.ifStart / a.ifIdx per cell, Q10 order)
+            const int ni = (int)h.if_cell.size();
+            G->if_count.push_back(h.if_count);
+            L.n_if = ni;
+            int *ifs, *ifi, *ifc;
+            SPUMA_TRY(gupload(G, &ifs, h.ifStart, s));
+            SPUMA_TRY(gupload(G, &ifi, h.ifIdx, s));
+            SPUMA_TRY(gupload(G, &ifc, h.if_cell, s));
+            L.a.ifStart = ifs;
+            L.a.ifIdx = ifi;
+            L.a.ifMask = nullptr;
+            L.a.n_iface = ni;
+            L.if_cell = ifc;
+            SPUMA_TRY(galloc(G, &L.xr, ni));
+            SPUMA_TRY(galloc(G, &L.sendbuf, ni));
+            if (l > 0) {
+                double* ic;
+                SPUMA_TRY(galloc(G, &ic, ni));
+                L.iface = ic;
+            }
+            if (l + 1 < nl) {
+                int *cs, *cl;
+                SPUMA_TRY(gupload(G, &cs, h.cifStart, s));
+                SPUMA_TRY(gupload(G, &cl, h.cifList, s));
+                L.cifStart = cs;
+                L.cifList = cl;
+                L.ncif = (int)H[l + 1].if_cell.size();
+            }
+        }
         if (l + 1 < nl) {
             int *ftc, *cs, *cl, *cis, *cil, *cfs, *cfl;
             SPUMA_TRY(gupload(G, &ftc, h.ftc, s));
@@ -605,16 +736,69 @@ spuma_status gamg_ensure(spuma_mesh m, const spuma_gamg_params& gp)
     SPUMA_TRY(galloc(G, &c.rD, nc));
     SPUMA_TRY(galloc(G, &c.sumA, nc));
     c.pA_prev = c.pA;
-    SPUMA_TRY(galloc(G, &c.part, kMaxPartials));
+    SPUMA_TRY(galloc(G, &c.part, (size_t)kMaxPartials * std::max(occupancy_grid(nc, nullptr, 0), m->n_ranks)));
     SPUMA_TRY(galloc(G, &c.scal, 1));
+    if (dd) {
+        c.xr = G->lv[nl - 1].xr;
+        SPUMA_TRY(galloc(G, &G->rank_part, 4));
+        SPUMA_TRY(galloc(G, &G->gathered, (size_t)4 * m->n_ranks));
+    }
     SPUMA_TRY(galloc(G, &c.ptrs, 1));
     SPUMA_CUDA(cudaMallocHost(reinterpret_cast<void**>(&G->h_cptrs), sizeof(DevPtrs)));
     SPUMA_CUDA(cudaStreamSynchronize(s));
     return SPUMA_OK;
 }
 
-// One V-cycle (Q23) + the outer residual (Q28), enqueued on s (captured or direct).
-int gamg_enqueue_cycle(spuma_mesh m, const spuma_gamg_params& gp, cudaStream_t s)
+// The coarsest level of a decomposed hierarchy (Q38): PCG + diagonal over all ranks (O8
+// semantics) from x = 0 -- the main path's multi-rank kernels (setup, direction, Amul with
+// inline interface terms after the halo, update) and rank-order finalisation, with the
+// coarsest level's addressing and interfaces and the coarsest workspace.
+spuma_status gamg_coarsest_dd(spuma_mesh m, const spuma_gamg_params& gp, cudaStream_t s, int* k)
+{
+    GamgState* G = m->gamg;
+    GLevel& Lc = G->lv.back();
+    const std::vector<int>& cnt = G->if_count.back();
+    Workspace c = G->cws;
+    const MeshArgs a = Lc.a;
+    const spuma_solver_controls cc{gp.coarsest_tolerance, gp.coarsest_rel_tol, gp.coarsest_max_iter, 0};
+    launch_scal_init(s, c, cc, m->n_ranks);
+    SPUMA_CUDA(cudaMemsetAsync(Lc.x, 0, sizeof(double) * (a.N + kPad), s));
+    launch_pack(s, Lc.n_if, Lc.if_cell, Lc.x, Lc.sendbuf);
+    SPUMA_TRY(exchange_counts(m, cnt, Lc.sendbuf, Lc.xr, s));
+    launch_setup1(s, 0, a, c, false);
+    SPUMA_TRY(reduce_finalize_ws(m, c, 1, s));
+    launch_setup2(s, 0, a, c, false);
+    SPUMA_TRY(reduce_finalize_ws(m, c, 2, s));
+    *k += 4;
+    DevScal* hs = &m->h_scal[1];
+    SPUMA_CUDA(cudaMemcpyAsync(hs, c.scal, sizeof(DevScal), cudaMemcpyDeviceToHost, s));
+    SPUMA_CUDA(cudaStreamSynchronize(s));
+    const int per_check = m->external_comm ? 1 : 8;  // no-op kernels past 'done' (same on every rank)
+    int it = 0;
+    while (!hs->done) {
+        for (int b = 0; b < per_check; ++b) {
+            launch_direction(s, 0, a, c);
+            launch_pack(s, Lc.n_if, Lc.if_cell, c.pA, Lc.sendbuf);
+            SPUMA_TRY(exchange_counts(m, cnt, Lc.sendbuf, Lc.xr, s));
+            launch_amul_dot(s, 0, a, c, false, -1, -1);
+            SPUMA_TRY(reduce_finalize_ws(m, c, 3, s));
+            launch_update(s, 0, a, c, false, 0);
+            SPUMA_TRY(reduce_finalize_ws(m, c, 4, s));
+            *k += 4;
+        }
+        SPUMA_CUDA(cudaMemcpyAsync(hs, c.scal, sizeof(DevScal), cudaMemcpyDeviceToHost, s));
+        SPUMA_CUDA(cudaStreamSynchronize(s));
+        it += per_check;
+        if (it > gp.coarsest_max_iter + 16) return set_error(SPUMA_ERR_STATE, "coarsest PCG did not terminate");
+    }
+    return SPUMA_OK;
+}
+
+// One V-cycle (Q23) + the outer residual (Q28), enqueued on s (captured or direct).  On a
+// decomposed mesh (G->dd; direct launches only) every row kernel is preceded by the halo of the
+// vector it gathers, every reduction is finished from the gathered rank partials, and the
+// coarsest level is gamg_coarsest_dd (readings Q36-Q38).
+int gamg_enqueue_cycle(spuma_mesh m, const spuma_gamg_params& gp, cudaStream_t s, spuma_status* st = nullptr)
 {
     GamgState* G = m->gamg;
     const DevPtrs* P = m->ws.ptrs;
@@ -623,16 +807,42 @@ int gamg_enqueue_cycle(spuma_mesh m, const spuma_gamg_params& gp, cudaStream_t s
     int k = 0;
     Workspace w0 = m->ws;
     w0.part = G->part;
+    const bool dd = G->dd;
+    spuma_status err = SPUMA_OK;
+    if (st) *st = SPUMA_OK;
+    // dd: the neighbours' values of the vector the next row kernel of level L gathers
+    auto halo = [&](const GLevel& L, int mode, const double* x, const double* xc, const double* alpha,
+                    const double* p, const double* q) {
+        if (!dd || err != SPUMA_OK) return;
+        launch_gamg_pack(s, L, mode, x, xc, alpha, p, q);
+        ++k;
+        err = exchange_counts(m, G->if_count[&L - lv.data()], L.sendbuf, L.xr, s);
+    };
+    auto reduce = [&](int what, double* alpha) {
+        if (err != SPUMA_OK) return;
+        err = allgather4(m, G->rank_part, G->gathered, s);
+        launch_gamg_fin(s, what, G->gathered, m->n_ranks, alpha, m->ws.scal);
+        ++k;
+    };
+    double* rp = dd ? G->rank_part : nullptr;
     if (nl == 1) {  // the finest level is the coarsest: exact-ish solve of A x = r, psi += x
-        cudaMemsetAsync(lv[0].x, 0, sizeof(double) * lv[0].a.N, s);
-        launch_pcg_single(s, lv[0].a, G->cws);
+        if (dd) {
+            err = gamg_coarsest_dd(m, gp, s, &k);
+        } else {
+            cudaMemsetAsync(lv[0].x, 0, sizeof(double) * lv[0].a.N, s);
+            launch_pcg_single(s, lv[0].a, G->cws);
+        }
         launch_add(s, lv[0].a.N, lv[0].x, m->h_ptrs->psi);
-        launch_gamg_residual(s, lv[0], w0);
-        return 3;
+        halo(lv[0], 0, m->h_ptrs->psi, nullptr, nullptr, nullptr, nullptr);
+        launch_gamg_residual(s, lv[0], w0, rp);
+        if (dd) reduce(1, nullptr);
+        if (st) *st = err;
+        return k + 3;
     }
     // one smoother sweep on level L: from x' = xin (+ alpha xc[ftc] if xc) into out (acc: psi += x)
     auto sweep = [&](GLevel& L, const double* xin, const double* xc, const double* alpha, double* out,
                      bool acc) {
+        halo(L, xc ? 1 : 0, xin, xc, alpha, nullptr, nullptr);
         if (gp.smoother != SPUMA_SMOOTHER_GS2) {
             launch_gamg_smooth(s, L, P, xin, out, gp.omega, xc, alpha, acc);
             ++k;
@@ -656,7 +866,7 @@ int gamg_enqueue_cycle(spuma_mesh m, const spuma_gamg_params& gp, cudaStream_t s
     };
     // the small levels t..nl-1 in one CTA (k_gamg_tail) when the configuration allows it
     int t = nl;
-    if (m->gamg_tail_cells > 0 && gp.smoother == SPUMA_SMOOTHER_RICHARDSON && gp.scale_correction &&
+    if (!dd && m->gamg_tail_cells > 0 && gp.smoother == SPUMA_SMOOTHER_RICHARDSON && gp.scale_correction &&
         gp.n_pre_sweeps == 0 && gp.n_post_sweeps >= 1) {
         for (int l = 1; l < nl; ++l)
             if (lv[l].a.N <= m->gamg_tail_cells) {
@@ -678,6 +888,7 @@ int gamg_enqueue_cycle(spuma_mesh m, const spuma_gamg_params& gp, cudaStream_t s
             }
             xl = xin;
         }
+        if (xl) halo(L, 0, xl, nullptr, nullptr, nullptr, nullptr);
         launch_gamg_restrict(s, L, lv[l + 1], P, xl, l + 2 == nl ? lv[l + 1].x : nullptr);  // zeroes x_coarsest
         ++k;
         xcur[l] = xl;
@@ -688,6 +899,9 @@ int gamg_enqueue_cycle(spuma_mesh m, const spuma_gamg_params& gp, cudaStream_t s
         ++k;
         const bool in_x = gp.n_post_sweeps <= 2 || ((gp.n_post_sweeps - 2) & 1) == 0;
         xcur[t] = in_x ? lv[t].x : lv[t].x2;
+    } else if (dd) {
+        if (err == SPUMA_OK) err = gamg_coarsest_dd(m, gp, s, &k);
+        xcur[nl - 1] = Lc.x;
     } else {
         launch_pcg_single(s, Lc.a, G->cws);
         ++k;
@@ -703,14 +917,17 @@ int gamg_enqueue_cycle(spuma_mesh m, const spuma_gamg_params& gp, cudaStream_t s
         const double* alpha = gp.scale_correction ? G->alpha + l : nullptr;
         int done_sweeps = 0;
         if (gp.scale_correction) {
-            launch_gamg_scale(s, L, P, xcur[l], xc, r, gp.omega, pq, G->part, G->ticket, G->alpha + l);
+            halo(L, 2, nullptr, xc, nullptr, nullptr, nullptr);
+            launch_gamg_scale(s, L, P, xcur[l], xc, r, gp.omega, pq, G->part, G->ticket, G->alpha + l, rp);
             ++k;
+            if (dd) reduce(0, G->alpha + l);
         }
         bool acc = false;
         if (pq) {  // Richardson: sweeps 1 (+2) in one kernel, sweep 1 prepared by the scale (Q29)
             const bool two = gp.n_post_sweeps >= 2;
             done_sweeps = two ? 2 : 1;
             acc = l == 0 && done_sweeps == gp.n_post_sweeps;
+            if (two) halo(L, 3, nullptr, nullptr, G->alpha + l, L.p, L.q);
             launch_gamg_post(s, L, P, G->alpha + l, gp.omega, out, two, acc);
             ++k;
         } else if (gp.n_post_sweeps > 0) {  // the correction folded into the first sweep
@@ -735,7 +952,10 @@ int gamg_enqueue_cycle(spuma_mesh m, const spuma_gamg_params& gp, cudaStream_t s
             }
         }
     }
-    launch_gamg_residual(s, lv[0], w0);
+    halo(lv[0], 0, m->h_ptrs->psi, nullptr, nullptr, nullptr, nullptr);
+    launch_gamg_residual(s, lv[0], w0, rp);
+    if (dd) reduce(1, nullptr);
+    if (st) *st = err;
     return k + 1;
 }
 
@@ -1137,6 +1357,7 @@ static spuma_status mesh_create_impl(const spuma_mesh_desc* d, spuma_mesh m)
     SPUMA_TRY(upload(&m->d_ifStart, ifStart, s));
     SPUMA_TRY(upload(&m->d_ifIdx, ifIdx, s));
     SPUMA_TRY(upload(&m->d_if_cell, if_cell, s));
+    m->h_if_cell = if_cell;
     {
         std::vector<unsigned> mask((N + 31) / 32 + 1, 0u);
         for (int c : if_cell) mask[c >> 5] |= 1u << (c & 31);
@@ -1762,18 +1983,17 @@ spuma_status spuma_gamg_solve(spuma_mesh m, const spuma_scalar* diag, const spum
                               const spuma_solver_controls* ctl, const spuma_gamg_params* params,
                               spuma_solver_perf* perf)
 {
-    (void)iface_coeffs;
     if (!m) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "mesh is NULL");
     if (!ctl || !perf) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "NULL controls/perf");
-    if (m->n_ranks > 1) return set_error(SPUMA_ERR_STATE, "GAMG is single-rank (DESIGN.md Q28)");
     if (m->N > 0 && (!diag || !source || !psi)) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "NULL array");
+    if (m->n_iface > 0 && !iface_coeffs) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "iface_coeffs is NULL");
     if (m->F > 0 && !upper) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "upper is NULL");
     if (ctl->max_iter < 0 || ctl->min_iter < 0) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "negative iteration limit");
     spuma_gamg_params gp;
     spuma_gamg_default_params(&gp);
     if (params) gp = *params;
     SPUMA_TRY(gamg_check_params(gp));
-    if (m->N == 0) {
+    if (m->N == 0 && m->n_ranks == 1) {
         *perf = spuma_solver_perf{};
         return SPUMA_OK;
     }
@@ -1785,14 +2005,16 @@ spuma_status spuma_gamg_solve(spuma_mesh m, const spuma_scalar* diag, const spum
     SPUMA_TRY(cells_in(m, source, R_SOURCE, &P.source));
     SPUMA_TRY(cells_in(m, psi, R_PSI, &psi_in));
     P.psi = const_cast<double*>(psi_in);
+    if (m->n_iface) SPUMA_TRY(iface_in(m, iface_coeffs, &P.iface));
     SPUMA_TRY(gamg_ensure(m, gp));
+    const bool dd = m->gamg->dd;
     GamgState* G = m->gamg;
     const int nl = (int)G->lv.size();
     *m->h_ptrs = P;
     SPUMA_CUDA(cudaMemcpyAsync(m->ws.ptrs, m->h_ptrs, sizeof(DevPtrs), cudaMemcpyHostToDevice, s));
     const GLevel& Lc = G->lv[nl - 1];
-    *G->h_cptrs = DevPtrs{nl == 1 ? P.diag : Lc.diag, nl == 1 ? P.upper : Lc.upper, nullptr, Lc.b ? Lc.b : m->ws.rA,
-                          Lc.x};
+    *G->h_cptrs = DevPtrs{nl == 1 ? P.diag : Lc.diag, nl == 1 ? P.upper : Lc.upper, nl == 1 ? P.iface : Lc.iface,
+                          Lc.b ? Lc.b : m->ws.rA, Lc.x};
     SPUMA_CUDA(cudaMemcpyAsync(G->cws.ptrs, G->h_cptrs, sizeof(DevPtrs), cudaMemcpyHostToDevice, s));
     // per-solve: Galerkin coarse matrices (Q27), outer scalars, coarsest PCG controls, A6 setup
     for (int l = 0; l + 1 < nl; ++l) launch_gamg_agg(s, G->lv[l], G->lv[l + 1], m->ws.ptrs);
@@ -1800,16 +2022,25 @@ spuma_status spuma_gamg_solve(spuma_mesh m, const spuma_scalar* diag, const spum
         launch_ell_coeffs(s, G->lv[0].a, P.upper, m->d_upper_s);
         m->stats.kernel_launches += 1;
     }
-    launch_scal_init(s, m->ws, *ctl, 1);
+    launch_scal_init(s, m->ws, *ctl, dd ? m->n_ranks : 1);
     const spuma_solver_controls cc{gp.coarsest_tolerance, gp.coarsest_rel_tol, gp.coarsest_max_iter, 0};
     launch_scal_init(s, G->cws, cc, 1);
-    const MeshArgs a0 = G->lv[0].a;
-    launch_setup1(s, m->grid, a0, m->ws, true);
-    launch_setup2(s, m->grid, a0, m->ws, true);
+    if (dd) {  // A6 over the ranks: normFactor, initial residual (interface terms after the psi halo)
+        const MeshArgs a0 = mesh_args(m);
+        SPUMA_TRY(halo_exchange(m, P.psi, m->ws.xr, s));
+        launch_setup1(s, m->grid, a0, m->ws, false);
+        SPUMA_TRY(reduce_finalize(m, 1, s));
+        launch_setup2(s, m->grid, a0, m->ws, false);
+        SPUMA_TRY(reduce_finalize(m, 2, s));
+    } else {
+        const MeshArgs a0 = G->lv[0].a;
+        launch_setup1(s, m->grid, a0, m->ws, true);
+        launch_setup2(s, m->grid, a0, m->ws, true);
+    }
     m->stats.kernel_launches += (uint64_t)(nl - 1) + 4;
 
-    // one V-cycle per graph launch (nl == 1: direct launches, psi is a per-call pointer)
-    const bool use_graph = nl > 1;
+    // one V-cycle per graph launch (nl == 1 or a decomposed mesh: direct launches)
+    const bool use_graph = nl > 1 && !dd;
     if (use_graph && (!G->gexec || std::memcmp(&G->gkey, &gp, sizeof gp) != 0 || G->gkey_tail != m->gamg_tail_cells)) {
         if (G->gexec) cudaGraphExecDestroy(G->gexec);
         G->gexec = nullptr;
@@ -1828,8 +2059,13 @@ spuma_status spuma_gamg_solve(spuma_mesh m, const spuma_scalar* diag, const spum
     SPUMA_CUDA(cudaStreamSynchronize(s));
     int cycles = 0;
     while (!m->h_scal[0].done) {
-        if (use_graph) SPUMA_CUDA(cudaGraphLaunch(G->gexec, s));
-        else G->launches_per_cycle = gamg_enqueue_cycle(m, gp, s);
+        if (use_graph) {
+            SPUMA_CUDA(cudaGraphLaunch(G->gexec, s));
+        } else {
+            spuma_status st = SPUMA_OK;
+            G->launches_per_cycle = gamg_enqueue_cycle(m, gp, s, &st);
+            if (st != SPUMA_OK) return st;
+        }
         SPUMA_CUDA(cudaMemcpyAsync(&m->h_scal[0], m->ws.scal, sizeof(DevScal), cudaMemcpyDeviceToHost, s));
         SPUMA_CUDA(cudaStreamSynchronize(s));
         if (++cycles > ctl->max_iter + 1) return set_error(SPUMA_ERR_STATE, "GAMG loop did not terminate");
@@ -1859,8 +2095,7 @@ spuma_status spuma_gamg_get_hierarchy(spuma_mesh m, const spuma_gamg_params* par
     if (params) gp = *params;
     else if (m->gamg) gp.n_cells_in_coarsest_level = m->gamg->n_coarsest, gp.max_levels = m->gamg->max_levels;
     SPUMA_TRY(gamg_check_params(gp));
-    if (m->n_ranks > 1) return set_error(SPUMA_ERR_STATE, "GAMG is single-rank (DESIGN.md Q28)");
-    SPUMA_TRY(gamg_ensure(m, gp));
+    SPUMA_TRY(gamg_ensure(m, gp));  // collective on a decomposed mesh when the hierarchy is (re)built
     const GamgState* G = m->gamg;
     const int nl = (int)G->lv.size();
     *n_levels = nl;

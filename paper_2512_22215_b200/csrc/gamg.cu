@@ -61,12 +61,29 @@ __device__ __forceinline__ double row_ax_ell(const MeshArgs& a, int c, const dou
     return s;
 }
 
-template <bool ELL, class X>
-__device__ __forceinline__ double rowA(const GLevel& L, int c, const double* __restrict__ d,
-                                       const double* __restrict__ u, const X& x)
+// + the processor-interface terms of row c in (patch, face) order (Q10), reading the halo xr
+// of the same implicit vector (packed by the neighbours before this kernel)
+template <bool IF>
+__device__ __forceinline__ double add_if(const GLevel& L, const double* __restrict__ ic, int c, double s)
 {
-    if constexpr (ELL) return row_ax_ell(L.a, c, d, x);
-    else return row_ax(L.a, c, d, u, x);
+    if constexpr (IF) {
+        const int k1 = L.a.ifStart[c + 1];
+        for (int k = L.a.ifStart[c]; k < k1; ++k) {
+            const int i = L.a.ifIdx[k];
+            s = s + ic[i] * L.xr[i];
+        }
+    }
+    return s;
+}
+
+template <bool ELL, bool IF = false, class X>
+__device__ __forceinline__ double rowA(const GLevel& L, int c, const double* __restrict__ d,
+                                       const double* __restrict__ u, const double* __restrict__ ic, const X& x)
+{
+    double s;
+    if constexpr (ELL) s = row_ax_ell(L.a, c, d, x);
+    else s = row_ax(L.a, c, d, u, x);
+    return add_if<IF>(L, ic, c, s);
 }
 
 struct XPlain {
@@ -104,6 +121,10 @@ __device__ __forceinline__ const double* level_upper(const GLevel& L, const DevP
 {
     return L.upper ? L.upper : P->upper;
 }
+__device__ __forceinline__ const double* level_iface(const GLevel& L, const DevPtrs* P)
+{
+    return L.iface ? L.iface : P->iface;
+}
 
 // agglomerateMatrix (Q27): coarse diag = fine diags of the members (ascending) + (u + l) of
 // the agglomerate-internal faces (ascending); coarse upper = fine uppers of its faces.
@@ -121,6 +142,14 @@ __global__ void __launch_bounds__(kThreads) k_gamg_agg(GLevel F, GLevel C, const
         }
         C.diag[c] = d;
     }
+    if (F.cifStart) {  // coarse interface coefficients: sums of the fine ones, ascending (Q37)
+        const double* __restrict__ fi = level_iface(F, P);
+        for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < F.ncif; e += stride) {
+            double v = 0.0;
+            for (int k = F.cifStart[e]; k < F.cifStart[e + 1]; ++k) v = v + fi[F.cifList[k]];
+            const_cast<double*>(C.iface)[e] = v;
+        }
+    }
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < F.ncf; e += stride) {
         double u = 0.0;
         for (int k = F.cfStart[e]; k < F.cfStart[e + 1]; ++k) u = u + fu[F.cfList[k]];
@@ -134,6 +163,7 @@ __global__ void __launch_bounds__(kThreads) k_gamg_agg(GLevel F, GLevel C, const
 
 // restrictField of the residual (Q23): C.b[c] = sum_{i in c} (b_i - (A x)_i); r_i stored
 // for the scale step when x is not zero.
+template <bool IF>
 __global__ void __launch_bounds__(kThreads) k_gamg_restrict(GLevel F, GLevel C, const DevPtrs* __restrict__ P,
                                                             const double* __restrict__ x, double* __restrict__ zero_x)
 {
@@ -147,7 +177,7 @@ __global__ void __launch_bounds__(kThreads) k_gamg_restrict(GLevel F, GLevel C, 
             const int i = F.cList[k];
             double r = F.b[i];
             if (x) {
-                r = r - row_ax(F.a, i, fd, fu, XPlain{x});
+                r = r - add_if<IF>(F, level_iface(F, P), i, row_ax(F.a, i, fd, fu, XPlain{x}));
                 F.r[i] = r;
             }
             s = s + r;
@@ -159,7 +189,7 @@ __global__ void __launch_bounds__(kThreads) k_gamg_restrict(GLevel F, GLevel C, 
 
 // Richardson sweep (Q24): xout = x + omega (rD (b - A x)), x = xin or (xin + alpha xc[ftc])
 // when xc is given (the prolonged correction of the first post-sweep); psi_acc: psi += xout.
-template <bool ELL>
+template <bool ELL, bool IF>
 __global__ void __launch_bounds__(kThreads) k_gamg_smooth(GLevel L, const DevPtrs* __restrict__ P,
                                                           const double* __restrict__ xin, double* __restrict__ xout,
                                                           double omega, const double* __restrict__ xc,
@@ -169,6 +199,7 @@ __global__ void __launch_bounds__(kThreads) k_gamg_smooth(GLevel L, const DevPtr
     pdl_trigger();
     const double* __restrict__ d = level_diag(L, P);
     const double* __restrict__ u = level_upper(L, P);
+    const double* __restrict__ ic = level_iface(L, P);
     double* __restrict__ psi = P->psi;
     const double a = alpha ? *alpha : 1.0;
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < L.a.N; c += gridDim.x * blockDim.x) {
@@ -176,13 +207,13 @@ __global__ void __launch_bounds__(kThreads) k_gamg_smooth(GLevel L, const DevPtr
         if (xc) {
             const XCorr X{xin, xc, L.ftc, a};
             xi = X(c);
-            y = rowA<ELL>(L, c, d, u, X);
+            y = rowA<ELL, IF>(L, c, d, u, ic, X);
         } else if (xin) {
             xi = xin[c];
-            y = rowA<ELL>(L, c, d, u, XPlain{xin});
+            y = rowA<ELL, IF>(L, c, d, u, ic, XPlain{xin});
         } else {  // x == 0 (first pre-sweep)
             xi = 0.0;
-            y = rowA<ELL>(L, c, d, u, XZero{});
+            y = rowA<ELL, IF>(L, c, d, u, ic, XZero{});
         }
         const double xn = xi + omega * ((1.0 / d[c]) * (L.b[c] - y));
         if (psi_acc) psi[c] = psi[c] + xn;
@@ -196,21 +227,23 @@ __global__ void __launch_bounds__(kThreads) k_gamg_smooth(GLevel L, const DevPtr
 //   x1 = x' + omega rD (r - alpha Ac) = alpha p + q,
 //   p = c - omega rD Ac,  q = x + omega rD r       (x = pre-smoothed correction or 0)
 // and k_gamg_post needs two direct loads per neighbour instead of a gather of its own.
-template <bool ELL>
+template <bool ELL, bool IF>
 __global__ void __launch_bounds__(kThreads) k_gamg_scale(GLevel L, const DevPtrs* __restrict__ P,
                                                          const double* __restrict__ x, const double* __restrict__ xc,
                                                          const double* __restrict__ r, double omega, int pq,
-                                                         double* part, unsigned* ticket, double* alpha)
+                                                         double* part, unsigned* ticket, double* alpha,
+                                                         double* rank_part)
 {
     pdl_wait();  // predecessor complete and visible (PDL launch)
     pdl_trigger();
     const double* __restrict__ d = level_diag(L, P);
     const double* __restrict__ u = level_upper(L, P);
+    const double* __restrict__ ic = level_iface(L, P);
     const XInj X{xc, L.ftc};
     double v[2] = {0.0, 0.0};
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < L.a.N; c += gridDim.x * blockDim.x) {
         const double ci = X(c);
-        const double aci = rowA<ELL>(L, c, d, u, X);
+        const double aci = rowA<ELL, IF>(L, c, d, u, ic, X);
         const double ri = r[c];
         if (pq) {
             const double rd = 1.0 / d[c];
@@ -221,6 +254,13 @@ __global__ void __launch_bounds__(kThreads) k_gamg_scale(GLevel L, const DevPtrs
         v[1] += aci * ci;
     }
     if (grid_sum<2>(v, part, ticket) && threadIdx.x == 0) {
+        if (rank_part) {  // n_ranks > 1: this rank's two dots; alpha by k_gamg_fin after the all-gather
+            rank_part[0] = v[0];
+            rank_part[1] = v[1];
+            rank_part[2] = 0.0;
+            rank_part[3] = 0.0;
+            return;
+        }
         double a = fabs(v[1]) > 1e-300 ? v[0] / v[1] : 1.0;
         a = a < 0.0 ? 0.0 : (a > 2.0 ? 2.0 : a);
         *alpha = a;
@@ -253,7 +293,7 @@ struct XPQ {  // x1(j) = alpha p_j + q_j
 
 // Post-sweeps 1 (+2) after k_gamg_scale: x1 = alpha p + q; two: x2 = x1 + omega rD (b - A x1)
 // in one gather with x1 formed at the neighbours.  psi_acc: psi += result.
-template <bool ELL>
+template <bool ELL, bool IF>
 __global__ void __launch_bounds__(kThreads) k_gamg_post(GLevel L, const DevPtrs* __restrict__ P,
                                                         const double* __restrict__ alpha, double omega,
                                                         double* __restrict__ out, int two, int psi_acc)
@@ -262,12 +302,13 @@ __global__ void __launch_bounds__(kThreads) k_gamg_post(GLevel L, const DevPtrs*
     pdl_trigger();
     const double* __restrict__ d = level_diag(L, P);
     const double* __restrict__ u = level_upper(L, P);
+    const double* __restrict__ ic = level_iface(L, P);
     double* __restrict__ psi = P->psi;
     const XPQ X{L.p, L.q, *alpha};
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < L.a.N; c += gridDim.x * blockDim.x) {
         const double x1 = X(c);
         double xn = x1;
-        if (two) xn = x1 + omega * ((1.0 / d[c]) * (L.b[c] - rowA<ELL>(L, c, d, u, X)));
+        if (two) xn = x1 + omega * ((1.0 / d[c]) * (L.b[c] - rowA<ELL, IF>(L, c, d, u, ic, X)));
         if (psi_acc) psi[c] = psi[c] + xn;
         else out[c] = xn;
     }
@@ -275,7 +316,7 @@ __global__ void __launch_bounds__(kThreads) k_gamg_post(GLevel L, const DevPtrs*
 
 // Two-stage Gauss-Seidel (Q30), stage 1: r = b - A x' with x' = xin (+ alpha xc[ftc] when xc
 // is given: the prolonged correction folded into the first post-sweep; xin nullptr: zero).
-template <bool ELL>
+template <bool ELL, bool IF>
 __global__ void __launch_bounds__(kThreads) k_gamg_gs2_res(GLevel L, const DevPtrs* __restrict__ P,
                                                            const double* __restrict__ xin,
                                                            const double* __restrict__ xc,
@@ -285,11 +326,12 @@ __global__ void __launch_bounds__(kThreads) k_gamg_gs2_res(GLevel L, const DevPt
     pdl_trigger();
     const double* __restrict__ d = level_diag(L, P);
     const double* __restrict__ u = level_upper(L, P);
+    const double* __restrict__ ic = level_iface(L, P);
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < L.a.N; c += gridDim.x * blockDim.x) {
         double y;
-        if (xc) y = rowA<ELL>(L, c, d, u, XCorr{xin, xc, L.ftc, alpha ? *alpha : 1.0});
-        else if (xin) y = rowA<ELL>(L, c, d, u, XPlain{xin});
-        else y = rowA<ELL>(L, c, d, u, XZero{});
+        if (xc) y = rowA<ELL, IF>(L, c, d, u, ic, XCorr{xin, xc, L.ftc, alpha ? *alpha : 1.0});
+        else if (xin) y = rowA<ELL, IF>(L, c, d, u, ic, XPlain{xin});
+        else y = rowA<ELL, IF>(L, c, d, u, ic, XZero{});
         r[c] = L.b[c] - y;
     }
 }
@@ -335,19 +377,24 @@ __global__ void __launch_bounds__(kThreads) k_gamg_gs2_upd(GLevel L, const DevPt
 }
 
 // end of a GAMG iteration (Q28): rA = source - A psi, final residual, n++, convergence, done
-template <bool ELL>
-__global__ void __launch_bounds__(kThreads) k_gamg_residual(GLevel L, Workspace w)
+template <bool ELL, bool IF>
+__global__ void __launch_bounds__(kThreads) k_gamg_residual(GLevel L, Workspace w, double* rank_part)
 {
     pdl_wait();  // predecessor complete and visible (PDL launch)
     pdl_trigger();
     const DevPtrs p = *w.ptrs;
     double v[1] = {0.0};
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < L.a.N; c += gridDim.x * blockDim.x) {
-        const double r = p.source[c] - rowA<ELL>(L, c, p.diag, p.upper, XPlain{p.psi});
+        const double r = p.source[c] - rowA<ELL, IF>(L, c, p.diag, p.upper, p.iface, XPlain{p.psi});
         w.rA[c] = r;
         v[0] += fabs(r);
     }
     if (grid_sum<1>(v, w.part, &w.scal->ticket[2]) && threadIdx.x == 0) {
+        if (rank_part) {  // n_ranks > 1: finished by k_gamg_fin after the all-gather
+            rank_part[0] = v[0];
+            rank_part[1] = rank_part[2] = rank_part[3] = 0.0;
+            return;
+        }
         DevScal* s = w.scal;
         s->fin = v[0] / s->normFactor;
         s->n = s->n + 1;
@@ -355,6 +402,46 @@ __global__ void __launch_bounds__(kThreads) k_gamg_residual(GLevel L, Workspace 
         s->converged = c;
         if (!((s->n < s->max_iter && !c) || s->n < s->min_iter)) s->done = 1;
     }
+}
+
+// halo source of the level's next row kernel (n_ranks > 1): the implicit vector at the
+// interface cells, formed exactly as the row kernels form it (same rounding)
+__global__ void __launch_bounds__(kThreads) k_gamg_pack(GLevel L, int mode, const double* __restrict__ x,
+                                                        const double* __restrict__ xc,
+                                                        const double* __restrict__ alpha,
+                                                        const double* __restrict__ p, const double* __restrict__ q)
+{
+    const double a = alpha ? *alpha : 1.0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < L.n_if; i += gridDim.x * blockDim.x) {
+        const int c = L.if_cell[i];
+        double v;
+        if (mode == 1) v = XCorr{x, xc, L.ftc, a}(c);
+        else if (mode == 2) v = XInj{xc, L.ftc}(c);
+        else if (mode == 3) v = XPQ{p, q, a}(c);
+        else v = x ? x[c] : 0.0;
+        L.sendbuf[i] = v;
+    }
+}
+
+// rank-order sums of the gathered partials (every rank computes the same bits)
+__global__ void k_gamg_fin(int what, const double* __restrict__ g, int n_ranks, double* alpha, DevScal* s)
+{
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double v0 = 0.0, v1 = 0.0;
+    for (int r = 0; r < n_ranks; ++r) {
+        v0 += g[4 * r];
+        v1 += g[4 * r + 1];
+    }
+    if (what == 0) {  // Q25
+        double a = fabs(v1) > 1e-300 ? v0 / v1 : 1.0;
+        *alpha = a < 0.0 ? 0.0 : (a > 2.0 ? 2.0 : a);
+        return;
+    }
+    s->fin = v0 / s->normFactor;  // Q28
+    s->n = s->n + 1;
+    const bool c = conv(s->fin, s->init, s->tol, s->rel_tol);
+    s->converged = c;
+    if (!((s->n < s->max_iter && !c) || s->n < s->min_iter)) s->done = 1;
 }
 
 // The small levels t..nl-1 of a V-cycle in ONE CTA (Richardson, scaled correction, nPre = 0):
@@ -464,7 +551,7 @@ int gamg_grid(int n)
         int dev = 0, sms = 148, occ = 4;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gamg_smooth<false>, kThreads, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gamg_smooth<false, false>, kThreads, 0);
         g_gamg_max_grid = sms * (occ > 0 ? occ : 1);
     }
     const int g = (n + kThreads - 1) / kThreads;
@@ -476,24 +563,37 @@ void launch_gamg_agg(cudaStream_t s, const GLevel& fine, const GLevel& coarse, c
     k_gamg_agg<<<gamg_grid(fine.nc > fine.ncf ? fine.nc : fine.ncf), kThreads, 0, s>>>(fine, coarse, P);
 }
 
+// the <ELL, IF> instance of a row kernel for level L (IF: the level has processor interfaces)
+#define GAMG_DISPATCH(K, L, ...)                                                  \
+    do {                                                                          \
+        const bool if_ = (L).a.ifStart != nullptr;                                \
+        if ((L).ell) {                                                            \
+            if (if_) glaunch(K<true, true>, (L).grid, s, __VA_ARGS__);            \
+            else glaunch(K<true, false>, (L).grid, s, __VA_ARGS__);               \
+        } else {                                                                  \
+            if (if_) glaunch(K<false, true>, (L).grid, s, __VA_ARGS__);           \
+            else glaunch(K<false, false>, (L).grid, s, __VA_ARGS__);              \
+        }                                                                         \
+    } while (0)
+
 void launch_gamg_restrict(cudaStream_t s, const GLevel& fine, const GLevel& coarse, const DevPtrs* P, const double* x,
                           double* zero_x)
 {
-    glaunch(k_gamg_restrict, gamg_grid(fine.nc), s, fine, coarse, P, x, zero_x);
+    if (fine.a.ifStart && x) glaunch(k_gamg_restrict<true>, gamg_grid(fine.nc), s, fine, coarse, P, x, zero_x);
+    else glaunch(k_gamg_restrict<false>, gamg_grid(fine.nc), s, fine, coarse, P, x, zero_x);
 }
 
 void launch_gamg_smooth(cudaStream_t s, const GLevel& L, const DevPtrs* P, const double* xin, double* xout,
                         double omega, const double* xc, const double* alpha, bool psi_acc)
 {
-    if (L.ell) glaunch(k_gamg_smooth<true>, L.grid, s, L, P, xin, xout, omega, xc, alpha, psi_acc ? 1 : 0);
-    else glaunch(k_gamg_smooth<false>, L.grid, s, L, P, xin, xout, omega, xc, alpha, psi_acc ? 1 : 0);
+    GAMG_DISPATCH(k_gamg_smooth, L, L, P, xin, xout, omega, xc, alpha, psi_acc ? 1 : 0);
 }
 
 void launch_gamg_scale(cudaStream_t s, const GLevel& L, const DevPtrs* P, const double* x, const double* xc,
-                       const double* r, double omega, bool pq, double* part, unsigned* ticket, double* alpha)
+                       const double* r, double omega, bool pq, double* part, unsigned* ticket, double* alpha,
+                       double* rank_part)
 {
-    if (L.ell) glaunch(k_gamg_scale<true>, L.grid, s, L, P, x, xc, r, omega, pq ? 1 : 0, part, ticket, alpha);
-    else glaunch(k_gamg_scale<false>, L.grid, s, L, P, x, xc, r, omega, pq ? 1 : 0, part, ticket, alpha);
+    GAMG_DISPATCH(k_gamg_scale, L, L, P, x, xc, r, omega, pq ? 1 : 0, part, ticket, alpha, rank_part);
 }
 
 void launch_gamg_correct(cudaStream_t s, const GLevel& L, const DevPtrs* P, const double* x, const double* xc,
@@ -505,15 +605,13 @@ void launch_gamg_correct(cudaStream_t s, const GLevel& L, const DevPtrs* P, cons
 void launch_gamg_post(cudaStream_t s, const GLevel& L, const DevPtrs* P, const double* alpha, double omega,
                       double* out, bool two, bool psi_acc)
 {
-    if (L.ell) glaunch(k_gamg_post<true>, L.grid, s, L, P, alpha, omega, out, two ? 1 : 0, psi_acc ? 1 : 0);
-    else glaunch(k_gamg_post<false>, L.grid, s, L, P, alpha, omega, out, two ? 1 : 0, psi_acc ? 1 : 0);
+    GAMG_DISPATCH(k_gamg_post, L, L, P, alpha, omega, out, two ? 1 : 0, psi_acc ? 1 : 0);
 }
 
 void launch_gamg_gs2_res(cudaStream_t s, const GLevel& L, const DevPtrs* P, const double* xin, const double* xc,
                          const double* alpha, double* r)
 {
-    if (L.ell) glaunch(k_gamg_gs2_res<true>, L.grid, s, L, P, xin, xc, alpha, r);
-    else glaunch(k_gamg_gs2_res<false>, L.grid, s, L, P, xin, xc, alpha, r);
+    GAMG_DISPATCH(k_gamg_gs2_res, L, L, P, xin, xc, alpha, r);
 }
 
 void launch_gamg_gs2_upd(cudaStream_t s, const GLevel& L, const DevPtrs* P, const double* xin, const double* xc,
@@ -524,10 +622,21 @@ void launch_gamg_gs2_upd(cudaStream_t s, const GLevel& L, const DevPtrs* P, cons
             psi_acc ? 1 : 0);
 }
 
-void launch_gamg_residual(cudaStream_t s, const GLevel& L, const Workspace& w)
+void launch_gamg_residual(cudaStream_t s, const GLevel& L, const Workspace& w, double* rank_part)
 {
-    if (L.ell) glaunch(k_gamg_residual<true>, L.grid, s, L, w);
-    else glaunch(k_gamg_residual<false>, L.grid, s, L, w);
+    GAMG_DISPATCH(k_gamg_residual, L, L, w, rank_part);
+}
+
+void launch_gamg_pack(cudaStream_t s, const GLevel& L, int mode, const double* x, const double* xc,
+                      const double* alpha, const double* p, const double* q)
+{
+    if (L.n_if <= 0) return;
+    k_gamg_pack<<<gamg_grid(L.n_if), kThreads, 0, s>>>(L, mode, x, xc, alpha, p, q);
+}
+
+void launch_gamg_fin(cudaStream_t s, int what, const double* gathered, int n_ranks, double* alpha, DevScal* scal)
+{
+    k_gamg_fin<<<1, 32, 0, s>>>(what, gathered, n_ranks, alpha, scal);
 }
 
 }  // namespace spuma

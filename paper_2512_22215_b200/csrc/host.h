@@ -55,6 +55,10 @@ struct GamgHostLevel {
     std::vector<int> cStart, cList;             // next level: coarse cell -> fine cells (ascending)
     std::vector<int> ciStart, ciList;           // next level: coarse cell -> agglomerate-internal fine faces
     std::vector<int> cfStart, cfList;           // next level: coarse face -> fine faces (ascending)
+    // processor interfaces of the level (n_ranks > 1; readings Q36-Q38): faces in (patch, face)
+    // order, per-patch counts, per-cell lists (Q10 order) and, towards the next level, the
+    // coarse interface face -> fine interface faces lists (ascending) of the Galerkin sums
+    std::vector<int> if_cell, if_count, ifStart, ifIdx, cifStart, cifList;
 };
 // Levels are added while the current level has more than n_coarsest cells, the pairwise
 // pass reduces the count and fewer than max_levels exist.  Level 0 takes the given
@@ -64,4 +68,24 @@ std::vector<GamgHostLevel> gamg_hierarchy(int N, int F, const std::vector<int>& 
                                           const std::vector<int>& losortStart, const std::vector<int>& losort,
                                           const std::vector<int>& ownerLo, const std::vector<double>& w,
                                           int n_coarsest, int max_levels);
+
+// Decomposed hierarchy (readings Q36, Q37): processor-local agglomeration; a level is added
+// while sum over ranks of the level's cells > n_ranks * n_coarsest and the pass reduces that
+// sum; coarse interface faces per patch = distinct (local coarse, remote coarse) pairs by
+// first occurrence over the fine interface faces.  The two collectives are passed in:
+// allgather4(in[4], out[4 * n_ranks]) and exchange(per-patch counts, send, recv) over the
+// processor patches (same peers as level 0).  Level 0's if_cell / if_count are given.
+struct GamgComm {
+    int n_ranks = 1;
+    bool (*allgather4)(void* ctx, const double* in, double* out) = nullptr;
+    bool (*exchange)(void* ctx, const std::vector<int>& counts, const std::vector<double>& send,
+                     std::vector<double>& recv) = nullptr;
+    void* ctx = nullptr;
+};
+std::vector<GamgHostLevel> gamg_hierarchy_dd(int N, int F, const std::vector<int>& owner,
+                                             const std::vector<int>& neighbour, const std::vector<int>& ownerStart,
+                                             const std::vector<int>& losortStart, const std::vector<int>& losort,
+                                             const std::vector<int>& ownerLo, const std::vector<double>& w,
+                                             const std::vector<int>& if_cell, const std::vector<int>& if_count,
+                                             int n_coarsest, int max_levels, const GamgComm& comm, bool* ok);
 }  // namespace spuma

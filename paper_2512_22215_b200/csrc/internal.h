@@ -88,6 +88,14 @@ struct GLevel {
     int nc, ncf;                  // next level's size
     int grid;                     // CTAs of this level's cell kernels (fixed: deterministic reductions)
     int ell;                      // 1: rows over the ELL layout (a.sell_*, a.upper_s; level 0 of a uniform mesh)
+    // processor interfaces (n_ranks > 1, readings Q36-Q38): a.ifStart / a.ifIdx per cell
+    const double* iface;          // [n_if] coefficients (nullptr on level 0: DevPtrs::iface)
+    double* xr;                   // [n_if] the neighbours' values of the vector a row kernel gathers
+    double* sendbuf;              // [n_if] packed local values for the neighbours
+    const int* if_cell;           // [n_if] local cell of each interface face
+    int n_if;
+    const int *cifStart, *cifList;  // next level: coarse interface face -> fine interface faces
+    int ncif;                     // next level's interface faces
 };
 
 struct Patch {
@@ -114,6 +122,7 @@ struct spuma_mesh_s {
     spuma_comm_callbacks cb{};
     double *h_send = nullptr, *h_recv = nullptr, *h_part = nullptr;  // pinned (external comm)
     std::vector<int> cb_peers, cb_offsets, cb_counts;
+    std::vector<int> h_if_cell;          // [n_iface] local cell of each processor face, (patch, face) order
 
     std::vector<spuma::Patch> patches;
     // host copies of the derived addressing (internal numbering) for diagnostics
@@ -320,10 +329,18 @@ void launch_gamg_restrict(cudaStream_t s, const GLevel& fine, const GLevel& coar
 void launch_gamg_smooth(cudaStream_t s, const GLevel& L, const DevPtrs* P, const double* xin, double* xout,
                         double omega, const double* xc, const double* alpha, bool psi_acc);
 void launch_gamg_scale(cudaStream_t s, const GLevel& L, const DevPtrs* P, const double* x, const double* xc,
-                       const double* r, double omega, bool pq, double* part, unsigned* ticket, double* alpha);
+                       const double* r, double omega, bool pq, double* part, unsigned* ticket, double* alpha,
+                       double* rank_part = nullptr);  // rank_part: write the two dots there (n_ranks > 1)
 void launch_gamg_correct(cudaStream_t s, const GLevel& L, const DevPtrs* P, const double* x, const double* xc,
                          const double* alpha, double* out, bool psi_acc);
-void launch_gamg_residual(cudaStream_t s, const GLevel& L, const Workspace& w);
+void launch_gamg_residual(cudaStream_t s, const GLevel& L, const Workspace& w, double* rank_part = nullptr);
+// n_ranks > 1: L.sendbuf[i] = X(if_cell[i]) for X = 0: x (nullptr: 0), 1: x + alpha xc[ftc],
+// 2: xc[ftc], 3: alpha p + q -- the vector the next row kernel of the level gathers
+void launch_gamg_pack(cudaStream_t s, const GLevel& L, int mode, const double* x, const double* xc,
+                      const double* alpha, const double* p, const double* q);
+// n_ranks > 1: finish a reduction from the gathered rank partials ([n_ranks][4], rank order):
+// what 0: alpha = clamp(sum g0 / sum g1) (Q25); what 1: the outer residual (Q28) into scal
+void launch_gamg_fin(cudaStream_t s, int what, const double* gathered, int n_ranks, double* alpha, DevScal* scal);
 // levels t..nl-1 of the V-cycle in one CTA (Richardson, scaled, nPre = 0); d_lv: device copy of the levels
 void launch_gamg_tail(cudaStream_t s, const GLevel* d_lv, int t, int nl, const Workspace& cws, double omega,
                       int n_post);
