@@ -439,7 +439,19 @@ typedef enum {
      * a separate pass (single rank, deferred psi, ELL layout; bitwise the same iterates).
      * 0 = separate k_direction (default: measured faster); 1 = fused, rD read;
      * 2 = fused, rD = 1/diag in place */
-    SPUMA_OPT_FUSE_DIRECTION = 5
+    SPUMA_OPT_FUSE_DIRECTION = 5,
+    /* PCG hot loop: alternate the cell sweep direction of consecutive kernels (direction
+     * ascending, Amul descending, update ascending, next iteration the reverse) so that each
+     * kernel starts on the lines its predecessor left in L2.  Same operations per element;
+     * only the order of the per-thread partial sums of the dots changes (deterministic).
+     * 1 = on (default), 0 = all ascending */
+    SPUMA_OPT_ALT_SWEEP = 6,
+    /* ELL Amul (variant 8): chunks of 32 cells whose column offsets (col - c) take at most 3
+     * values per side store those offsets once per chunk and one 32-bit word per cell instead
+     * of 6 explicit 32-bit slot indices (~19 B/cell less; bitwise the same rows).  0 = explicit
+     * slots everywhere (default: same-box A/B at 200^3 measured no gain -- the row gather is
+     * bound by its two dependent load levels, not by the bytes), 1 = on */
+    SPUMA_OPT_ELL_STENCIL = 7
 } spuma_option;
 spuma_status spuma_set_option(spuma_mesh m, int option, int value);
 

@@ -277,6 +277,55 @@ __device__ __forceinline__ void amul_rows_ell(const MeshArgs& a, int c, int wn, 
         }
         return;
     }
+    if constexpr (R == 1) {
+        // chunk-stencil rows: the chunk's <= 3 column offsets per side are warp-
+        // uniform loads, one 32-bit word per cell replaces the 6 explicit slot indices; same
+        // slots, same order (offsets ascending = losort / face order), so the same value
+        const int k = c >> 5;
+        if (a.cmeta) {
+            // one dependent level as in the explicit rows: meta, cell word, diag, x and the
+            // owner-side coefficients (compact slots) are all issued before any of them is used
+            const int4 m0 = __ldg(reinterpret_cast<const int4*>(a.cmeta) + 2 * k);
+            const int4 m1 = __ldg(reinterpret_cast<const int4*>(a.cmeta) + 2 * k + 1);
+            const int cr = min(c, a.N - 1);
+            const unsigned bits = __ldg(a.clane + cr);
+            const double dg = __ldg(diag + cr), xcv = __ldg(x + cr);
+            double uc[W];
+#pragma unroll
+            for (int j = 0; j < W; ++j) uc[j] = j < wo ? __ldg(upper_s + (size_t)32 * wo * k + 32 * j + l) : 0.0;
+            if (m0.x) {
+                const int dn[W] = {m0.y, m0.z, m0.w}, dq[W] = {m1.x, m1.y, m1.z};
+                double un[W], xn[W], xo[W];
+#pragma unroll
+                for (int t = 0; t < W; ++t) {
+                    const bool vn = (bits >> t) & 1u;
+                    const int col = vn ? cr + dn[t] : cr;
+                    const int pos = (int)((bits >> (6 + 5 * t)) & 31u);
+                    un[t] = vn ? __ldg(upper_s + (size_t)32 * wo * (col >> 5) + 32 * pos + (col & 31)) : 0.0;
+                    xn[t] = __ldg(x + col);
+                    const bool vo = (bits >> (3 + t)) & 1u;
+                    xo[t] = __ldg(x + (vo ? cr + dq[t] : cr));
+                }
+                double s = dg * xcv;
+#pragma unroll
+                for (int t = 0; t < W; ++t)
+                    if ((bits >> t) & 1u) s = s + un[t] * xn[t];
+#pragma unroll
+                for (int t = 0; t < W; ++t)
+                    if ((bits >> (3 + t)) & 1u) {  // owner-side offset t = compact slot popc(lower bits)
+                        const int so = __popc((bits >> 3) & ((1u << t) - 1u));
+                        const double u = so == 0 ? uc[0] : (so == 1 ? uc[1] : uc[2]);
+                        s = s + u * xo[t];
+                    }
+                if constexpr (IFM == 1) s = add_iface(a, cr, s, iface, xr);
+                if (c < a.N) {
+                    y[cr] = s;
+                    if (dot && (IFM != 2 || !is_iface_row(a, cr))) acc += s * xcv;
+                }
+                return;
+            }
+        }
+    }
     int cc[R];
     double dg[R], xc[R];
     unsigned pk[R][W];

@@ -88,6 +88,8 @@ MeshArgs mesh_args(const spuma_mesh m)
     a.ell_wn = m->sell_wn;
     a.ell_wo = m->sell_wo;
     a.upper_s = m->d_upper_s;
+    a.cmeta = m->ell_stencil ? m->d_cmeta : nullptr;
+    a.clane = m->ell_stencil ? m->d_clane : nullptr;
     return a;
 }
 
@@ -363,6 +365,9 @@ spuma_status enqueue_iteration(spuma_mesh m, cudaStream_t s, std::vector<cudaEve
         psi_mode = (slot & 1) ? 2 : 1;
     }
     const int rv = resolve_amul_variant(m->amul_variant, a);
+    // alternating sweeps (slot parity): C asc, A desc, B asc | C desc, A asc, B desc | ...
+    const bool odd = m->alt_sweep && (slot & 1);
+    const bool alt = m->alt_sweep;
     const bool overlap = !fin && m->n_iface > 0 && rv >= 6 && rv <= 9;
     if (fin && m->defer_psi && m->fuse_direction && rv == 8 && fused_direction_ok(a)) {
         // direction formed inside the Amul gather (one pass less per iteration)
@@ -378,7 +383,7 @@ spuma_status enqueue_iteration(spuma_mesh m, cudaStream_t s, std::vector<cudaEve
         return SPUMA_OK;
     }
     if (ev) record(m, *ev, slot * 6 + 0, s);
-    launch_direction(s, m->grid, a, ws);
+    launch_direction(s, m->grid, a, ws, odd);
     if (ev) record(m, *ev, slot * 6 + 1, s);
     if (overlap) {
         if (!m->external_comm) {
@@ -397,12 +402,12 @@ spuma_status enqueue_iteration(spuma_mesh m, cudaStream_t s, std::vector<cudaEve
     } else {
         SPUMA_TRY(halo_exchange(m, ws.pA, ws.xr, s));
         if (ev) record(m, *ev, slot * 6 + 2, s);
-        launch_amul_dot(s, m->amul_variant, a, ws, fin, m->sell_wn, m->sell_wo);
+        launch_amul_dot(s, m->amul_variant, a, ws, fin, m->sell_wn, m->sell_wo, false, alt && !odd);
         if (ev) record(m, *ev, slot * 6 + 3, s);
     }
     if (!fin) SPUMA_TRY(reduce_finalize(m, 3, s));
     if (ev) record(m, *ev, slot * 6 + 4, s);
-    launch_update(s, m->grid, a, ws, fin, psi_mode);
+    launch_update(s, m->grid, a, ws, fin, psi_mode, odd);
     if (ev) record(m, *ev, slot * 6 + 5, s);
     if (!fin) SPUMA_TRY(reduce_finalize(m, 4, s));
     m->stats.kernel_launches += 3;
@@ -1142,7 +1147,7 @@ void spuma_free(spuma_mesh m)
         if (m->batch_done[i]) cudaEventDestroy(m->batch_done[i]);
         if (m->asm_ev[i]) cudaEventDestroy(m->asm_ev[i]);
     }
-    void* dptrs[] = {m->d_sell_meta, m->d_sell_n, m->d_sell_o, m->d_upper_s,
+    void* dptrs[] = {m->d_sell_meta, m->d_sell_n, m->d_sell_o, m->d_upper_s, m->d_cmeta, m->d_clane,
                      m->d_owner, m->d_neighbour, m->d_ownerStart, m->d_losortStart, m->d_losort, m->d_ownerLo,
                      m->d_perm, m->d_face_map, m->d_delta, m->d_weights, m->d_magSf, m->d_bkind, m->d_bcell,
                      m->d_bproc, m->d_bmagSf, m->d_bdelta, m->d_bweight, m->d_bvalue, m->d_bgamma_r,
@@ -1332,6 +1337,14 @@ static spuma_status mesh_create_impl(const spuma_mesh_desc* d, spuma_mesh m)
             m->sell_wn = sell.uniform_wn;
             m->sell_wo = sell.uniform_wo;
             if (m->sell_wo >= 0) SPUMA_TRY(dalloc(&m->d_upper_s, (size_t)32 * m->sell_wo * ((N + 31) / 32)));
+            if (m->sell_wn >= 0 && m->sell_wn <= 3 && m->sell_wo >= 0 && m->sell_wo <= 3) {
+                const EllStencil st =
+                    build_ell_stencil(N, m->h_ownerStart, m->h_losortStart, m->h_losort, ownerLo, neighbour);
+                if (st.compressed > 0) {
+                    SPUMA_TRY(upload(&m->d_cmeta, st.meta, s));
+                    SPUMA_TRY(upload(&m->d_clane, st.lane, s));
+                }
+            }
             SPUMA_TRY(upload(&m->d_sell_meta, sell.meta, s));
             SPUMA_TRY(upload(&m->d_sell_n, sell.nslot, s));
             SPUMA_TRY(upload(&m->d_sell_o, sell.oslot, s));
@@ -1905,6 +1918,16 @@ spuma_status spuma_set_option(spuma_mesh m, int option, int value)
         if (value < 0 || value > 2) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "fuse_direction is 0, 1 or 2");
         if (m->fuse_direction != value) destroy_graphs(m);
         m->fuse_direction = value;
+        return SPUMA_OK;
+    case SPUMA_OPT_ELL_STENCIL:
+        if (value < 0 || value > 1) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "ell_stencil is 0 or 1");
+        if (m->ell_stencil != (value != 0)) destroy_graphs(m);
+        m->ell_stencil = value != 0;
+        return SPUMA_OK;
+    case SPUMA_OPT_ALT_SWEEP:
+        if (value < 0 || value > 1) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "alt_sweep is 0 or 1");
+        if (m->alt_sweep != (value != 0)) destroy_graphs(m);
+        m->alt_sweep = value != 0;
         return SPUMA_OK;
     case SPUMA_OPT_GAMG_TAIL_CELLS:
         if (value < 0) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "negative GAMG tail size");

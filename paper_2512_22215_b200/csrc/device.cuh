@@ -10,6 +10,20 @@ namespace spuma {
 // ---------------------------------------------------------------------------
 
 // Sum NV values over the CTA; the result is valid in thread 0.
+// Grid-stride index sequence of this thread over [0, n): ascending, or descending when rev
+// (consecutive kernels that alternate the direction start on the lines the previous one
+// touched last, which are still in L2).  The same indices either way; only the order (and
+// hence the rounding of per-thread partial sums) changes.
+struct GridStride {
+    int i0, st, cnt, rev;
+    __device__ __forceinline__ GridStride(int n, int r)
+        : i0(blockIdx.x * blockDim.x + threadIdx.x), st(gridDim.x * blockDim.x), rev(r)
+    {
+        cnt = i0 < n ? (n - 1 - i0) / st + 1 : 0;
+    }
+    __device__ __forceinline__ int at(int j) const { return i0 + (rev ? cnt - 1 - j : j) * st; }
+};
+
 template <int NV>
 __device__ __forceinline__ void cta_sum(double (&v)[NV])
 {

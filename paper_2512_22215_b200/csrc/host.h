@@ -25,6 +25,21 @@ SellHost build_sell(int N, const std::vector<int>& ownerStart, const std::vector
                     const std::vector<int>& losort, const std::vector<int>& ownerLo,
                     const std::vector<int>& neighbour);
 
+// Chunk-stencil compression of the uniform ELL rows (variant 8): per 32-cell
+// chunk, the distinct column offsets (col - c) of each side when there are at most 3 per side
+// (meta[8 k] = 1; meta[8 k + 1 .. 3] neighbour side, [8 k + 4 .. 6] owner side, ascending,
+// unused = 0); per cell one word: bit t = neighbour-side offset t present, bit 3 + t =
+// owner-side offset t present, bits 6 + 5 t = position of the neighbour-side face t in its
+// owner's faces.  Chunks with more distinct offsets keep meta[8 k] = 0 (explicit slots).
+struct EllStencil {
+    std::vector<int> meta;
+    std::vector<unsigned> lane;
+    int compressed = 0;  // chunks encoded
+};
+EllStencil build_ell_stencil(int N, const std::vector<int>& ownerStart, const std::vector<int>& losortStart,
+                             const std::vector<int>& losort, const std::vector<int>& ownerLo,
+                             const std::vector<int>& neighbour);
+
 // per-cell lists of the items i with keep[i], in input order
 void cell_lists(int N, const std::vector<int>& cell_of, const std::vector<char>& keep, std::vector<int>& start,
                 std::vector<int>& items);

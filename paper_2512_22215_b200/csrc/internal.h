@@ -59,6 +59,8 @@ struct MeshArgs {
     const int* sell_o;       // owner-side slots (neighbour column)
     int ell_wn, ell_wo;      // uniform chunk widths (ELL) or -1
     const double* upper_s;   // owner-slot ordered coefficient copy (variants 8/9), refreshed per call
+    const int* cmeta;        // chunk-stencil compression of the ELL rows (variant 8; host.h build_ell_stencil)
+    const unsigned* clane;   //   or nullptr
 };
 
 struct Workspace {
@@ -136,6 +138,9 @@ struct spuma_mesh_s {
     int* d_sell_meta = nullptr;
     int sell_wn = -1, sell_wo = -1;  // uniform chunk widths (ELL-like) or -1
     double* d_upper_s = nullptr;     // [32 * sell_wo * chunks] (uniform layout only)
+    int* d_cmeta = nullptr;          // chunk-stencil ELL compression (uniform layout only)
+    unsigned* d_clane = nullptr;
+    bool ell_stencil = false;        // use it (SPUMA_OPT_ELL_STENCIL; measured neutral -> off)
     unsigned* d_sell_n = nullptr;
     int* d_sell_o = nullptr;
     // device: geometry
@@ -180,6 +185,7 @@ struct spuma_mesh_s {
     bool defer_psi = true;  // psi += alpha pA applied every second iteration (same rounding, fewer bytes)  // ELL + coefficient copy (falls back to 6 -> 5 when the mesh is not uniform)
     bool timing = false;
     int fuse_direction = 0;      // 0: k_direction + k_amul_dot (default: faster); 1: fused, rD read; 2: fused, 1/diag inline
+    bool alt_sweep = true;       // alternate the sweep direction of consecutive hot-loop kernels (L2 reuse)
     int gamg_tail_cells = 1024;  // GAMG: levels from the first one at or below this size run in one CTA (0: off)
     cudaGraphExec_t gexec[2] = {nullptr, nullptr};
     bool gexec_timed = false;
@@ -246,9 +252,11 @@ void launch_pack(cudaStream_t s, int n, const int* cell, const double* x, double
 // PCG (A6-A12). `fin` = true when this rank finalises itself (P == 1).
 void launch_setup1(cudaStream_t s, int grid, const MeshArgs& a, const Workspace& w, bool fin);
 void launch_setup2(cudaStream_t s, int grid, const MeshArgs& a, const Workspace& w, bool fin);
-void launch_direction(cudaStream_t s, int grid, const MeshArgs& a, const Workspace& w);
+void launch_direction(cudaStream_t s, int grid, const MeshArgs& a, const Workspace& w, bool reverse = false);
 void launch_amul_dot(cudaStream_t s, int variant, const MeshArgs& a, const Workspace& w, bool fin, int sell_wn,
-                     int sell_wo, bool deferred = false);
+                     int sell_wo, bool deferred = false, bool reverse = false);
+// reverse: the kernel sweeps its cells in descending order (alternating sweep directions between
+// consecutive kernels lets each one start on the lines its predecessor left in L2)
 int resolve_amul_variant(int variant, const MeshArgs& a);  // variant actually run on this mesh
 void launch_iface_rows(cudaStream_t s, const MeshArgs& a, const Workspace& w, const int* rows, int n_rows);
 void launch_surface_integrate(cudaStream_t s, const MeshArgs& a, const double* phi, const int* bStart,
@@ -279,7 +287,8 @@ void launch_add(cudaStream_t s, int n, const double* in, double* out);
 void launch_scatter_signed(cudaStream_t s, int n, const int* idx, const signed char* flip, const double* in,
                            double* out);
 constexpr int kPad = 8;  // padding elements on internal arrays (16-byte TMA windows may overrun by <= 3)
-void launch_update(cudaStream_t s, int grid, const MeshArgs& a, const Workspace& w, bool fin, int psi_mode = 0);
+void launch_update(cudaStream_t s, int grid, const MeshArgs& a, const Workspace& w, bool fin, int psi_mode = 0,
+                   bool reverse = false);
 // psi_mode: 0 psi += alpha pA; 1 defer (psi untouched); 2 psi = (psi + alpha_prev pA_prev) + alpha pA
 void launch_psi_flush(cudaStream_t s, int N, const Workspace& w);
 // A11+A7+A8 in one kernel (ELL, single rank, deferred psi): see kernels.cu

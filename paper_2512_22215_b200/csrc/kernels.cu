@@ -392,7 +392,7 @@ __global__ void __launch_bounds__(kThreads) k_setup2(MeshArgs a, Workspace w, in
 // ---------------------------------------------------------------------------
 
 // A11 pA = rD rA + beta pA  (n == 0: pA = rD rA)
-__global__ void __launch_bounds__(kThreads) k_direction(int N, Workspace w)
+__global__ void __launch_bounds__(kThreads) k_direction(int N, Workspace w, int rev)
 {
     pdl_wait();
     if (w.scal->done) return;
@@ -403,7 +403,9 @@ __global__ void __launch_bounds__(kThreads) k_direction(int N, Workspace w)
     const double2* __restrict__ rA2 = reinterpret_cast<const double2*>(w.rA);
     const double2* pprev = reinterpret_cast<const double2*>(w.pA_prev);  // may alias pA (in place)
     double2* pA2 = reinterpret_cast<double2*>(w.pA);
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < np; i += gridDim.x * blockDim.x) {
+    const GridStride gs(np, rev);
+    for (int j = 0; j < gs.cnt; ++j) {
+        const int i = gs.at(j);
         const double2 d = rD2[i], r = rA2[i];
         double2 q;
         if (first) {
@@ -426,7 +428,7 @@ __global__ void __launch_bounds__(kThreads) k_direction(int N, Workspace w)
 // A7 + A8: wA = A pA, partial wA.pA -> alpha
 template <int V, int IFM = 0>
 __global__ void __launch_bounds__(V == 3 ? tma::kBlock : kThreads, amul_min_ctas<V>())
-    k_amul_dot(MeshArgs a, Workspace w, int fin, int sell_wn, int sell_wo)
+    k_amul_dot(MeshArgs a, Workspace w, int fin, int sell_wn, int sell_wo, int rev)
 {
     pdl_wait();
     if (w.scal->done) return;
@@ -457,9 +459,13 @@ __global__ void __launch_bounds__(V == 3 ? tma::kBlock : kThreads, amul_min_ctas
         constexpr int R = V == 9 ? 2 : 1;
         double acc = 0.0;
         const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-        for (int t0 = (blockIdx.x * (kThreads / 32) + warp) * 32 * R; t0 < a.N; t0 += gridDim.x * kThreads * R)
+        const int st = gridDim.x * kThreads * R, t00 = (blockIdx.x * (kThreads / 32) + warp) * 32 * R;
+        const int cnt = t00 < a.N ? (a.N - 1 - t00) / st + 1 : 0;
+        for (int j = 0; j < cnt; ++j) {  // rev: descending sweep (L2 reuse, see GridStride)
+            const int t0 = t00 + (rev ? cnt - 1 - j : j) * st;
             amul_rows_ell<R, IFM>(a, t0 + lane, a.ell_wn, a.ell_wo, p.diag, p.upper, a.upper_s, p.iface, w.pA, w.xr, w.wA,
                              acc, true);
+        }
         v[0] = acc;
     } else {
         for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < a.N; c += gridDim.x * blockDim.x) {
@@ -549,7 +555,7 @@ __global__ void __launch_bounds__(kThreads, amul_min_ctas<8>()) k_amul_dot_dir(M
 // psi_mode 0: psi += alpha pA; 1: psi left for the next iteration (deferred); 2: the
 // deferred pair, psi = (psi + alpha_prev pA_prev) + alpha pA -- the same two roundings as
 // two separate updates, so every iterate is bitwise unchanged.
-__global__ void __launch_bounds__(kThreads) k_update(int N, Workspace w, int fin, int psi_mode)
+__global__ void __launch_bounds__(kThreads) k_update(int N, Workspace w, int fin, int psi_mode, int rev)
 {
     pdl_wait();
     if (w.scal->done) return;
@@ -563,7 +569,9 @@ __global__ void __launch_bounds__(kThreads) k_update(int N, Workspace w, int fin
     const double2* __restrict__ pP2 = reinterpret_cast<const double2*>(w.pA_prev);
     const double2* __restrict__ wA2 = reinterpret_cast<const double2*>(w.wA);
     const double2* __restrict__ rD2 = reinterpret_cast<const double2*>(w.rD);
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < np; i += gridDim.x * blockDim.x) {
+    const GridStride gs(np, rev);
+    for (int j = 0; j < gs.cnt; ++j) {
+        const int i = gs.at(j);
         double2 r = rA2[i];
         const double2 ww = wA2[i], d = rD2[i];
         if (psi_mode != 1) {
@@ -1116,10 +1124,10 @@ void launch_setup2(cudaStream_t s, int grid, const MeshArgs& a, const Workspace&
     k_setup2<<<grid_for(k_setup2, a.N), kThreads, 0, s>>>(a, w, fin ? 1 : 0);
 }
 
-void launch_direction(cudaStream_t s, int grid, const MeshArgs& a, const Workspace& w)
+void launch_direction(cudaStream_t s, int grid, const MeshArgs& a, const Workspace& w, bool reverse)
 {
     (void)grid;
-    launch_hot(k_direction, grid_for(k_direction, a.N, 2), kThreads, s, a.N, w);
+    launch_hot(k_direction, grid_for(k_direction, a.N, 2), kThreads, s, a.N, w, reverse ? 1 : 0);
 }
 
 int resolve_amul_variant(int variant, const MeshArgs& a)
@@ -1130,44 +1138,44 @@ int resolve_amul_variant(int variant, const MeshArgs& a)
 }
 
 void launch_amul_dot(cudaStream_t s, int variant, const MeshArgs& a, const Workspace& w, bool fin, int sell_wn,
-                     int sell_wo, bool deferred)
+                     int sell_wo, bool deferred, bool reverse)
 {
-    const int f = fin ? 1 : 0;
+    const int f = fin ? 1 : 0, r = reverse ? 1 : 0;
     variant = resolve_amul_variant(variant, a);
     if (deferred && a.ifMask) {  // interface rows finished by k_iface_rows after the halo
         switch (variant) {
-        case 6: launch_hot(k_amul_dot<6, 2>, grid_for(k_amul_dot<6, 2>, a.N), kThreads, s, a, w, f, sell_wn, sell_wo); return;
-        case 7: launch_hot(k_amul_dot<7, 2>, grid_for(k_amul_dot<7, 2>, a.N, 2), kThreads, s, a, w, f, sell_wn, sell_wo); return;
-        case 8: launch_hot(k_amul_dot<8, 2>, grid_for(k_amul_dot<8, 2>, a.N), kThreads, s, a, w, f, sell_wn, sell_wo); return;
-        case 9: launch_hot(k_amul_dot<9, 2>, grid_for(k_amul_dot<9, 2>, a.N, 2), kThreads, s, a, w, f, sell_wn, sell_wo); return;
+        case 6: launch_hot(k_amul_dot<6, 2>, grid_for(k_amul_dot<6, 2>, a.N), kThreads, s, a, w, f, sell_wn, sell_wo, r); return;
+        case 7: launch_hot(k_amul_dot<7, 2>, grid_for(k_amul_dot<7, 2>, a.N, 2), kThreads, s, a, w, f, sell_wn, sell_wo, r); return;
+        case 8: launch_hot(k_amul_dot<8, 2>, grid_for(k_amul_dot<8, 2>, a.N), kThreads, s, a, w, f, sell_wn, sell_wo, r); return;
+        case 9: launch_hot(k_amul_dot<9, 2>, grid_for(k_amul_dot<9, 2>, a.N, 2), kThreads, s, a, w, f, sell_wn, sell_wo, r); return;
         default: break;  // other variants add the interface terms inline (halo must precede them)
         }
     }
     switch (variant) {
-    case 1: k_amul_dot<1><<<grid_for(k_amul_dot<1>, a.N), kThreads, 0, s>>>(a, w, f, sell_wn, sell_wo); break;
-    case 2: k_amul_dot<2><<<grid_for(k_amul_dot<2>, a.N), kThreads, 0, s>>>(a, w, f, sell_wn, sell_wo); break;
+    case 1: k_amul_dot<1><<<grid_for(k_amul_dot<1>, a.N), kThreads, 0, s>>>(a, w, f, sell_wn, sell_wo, r); break;
+    case 2: k_amul_dot<2><<<grid_for(k_amul_dot<2>, a.N), kThreads, 0, s>>>(a, w, f, sell_wn, sell_wo, r); break;
     case 3:
-        k_amul_dot<3><<<grid_for(k_amul_dot<3>, (a.N + tma::kCells - 1) / tma::kCells, 1, 1), tma::kBlock, 0, s>>>(a, w, f, sell_wn, sell_wo);
+        k_amul_dot<3><<<grid_for(k_amul_dot<3>, (a.N + tma::kCells - 1) / tma::kCells, 1, 1), tma::kBlock, 0, s>>>(a, w, f, sell_wn, sell_wo, r);
         break;
-    case 4: k_amul_dot<4><<<grid_for(k_amul_dot<4>, a.N), kThreads, 0, s>>>(a, w, f, sell_wn, sell_wo); break;
-    case 5: launch_hot(k_amul_dot<5>, grid_for(k_amul_dot<5>, a.N, 2), kThreads, s, a, w, f, sell_wn, sell_wo); break;
+    case 4: k_amul_dot<4><<<grid_for(k_amul_dot<4>, a.N), kThreads, 0, s>>>(a, w, f, sell_wn, sell_wo, r); break;
+    case 5: launch_hot(k_amul_dot<5>, grid_for(k_amul_dot<5>, a.N, 2), kThreads, s, a, w, f, sell_wn, sell_wo, r); break;
     case 6:
-        if (a.ifMask) launch_hot(k_amul_dot<6, 1>, grid_for(k_amul_dot<6, 1>, a.N), kThreads, s, a, w, f, sell_wn, sell_wo);
-        else launch_hot(k_amul_dot<6>, grid_for(k_amul_dot<6>, a.N), kThreads, s, a, w, f, sell_wn, sell_wo);
+        if (a.ifMask) launch_hot(k_amul_dot<6, 1>, grid_for(k_amul_dot<6, 1>, a.N), kThreads, s, a, w, f, sell_wn, sell_wo, r);
+        else launch_hot(k_amul_dot<6>, grid_for(k_amul_dot<6>, a.N), kThreads, s, a, w, f, sell_wn, sell_wo, r);
         break;
     case 7:
-        if (a.ifMask) launch_hot(k_amul_dot<7, 1>, grid_for(k_amul_dot<7, 1>, a.N, 2), kThreads, s, a, w, f, sell_wn, sell_wo);
-        else launch_hot(k_amul_dot<7>, grid_for(k_amul_dot<7>, a.N, 2), kThreads, s, a, w, f, sell_wn, sell_wo);
+        if (a.ifMask) launch_hot(k_amul_dot<7, 1>, grid_for(k_amul_dot<7, 1>, a.N, 2), kThreads, s, a, w, f, sell_wn, sell_wo, r);
+        else launch_hot(k_amul_dot<7>, grid_for(k_amul_dot<7>, a.N, 2), kThreads, s, a, w, f, sell_wn, sell_wo, r);
         break;
     case 8:
-        if (a.ifMask) launch_hot(k_amul_dot<8, 1>, grid_for(k_amul_dot<8, 1>, a.N), kThreads, s, a, w, f, sell_wn, sell_wo);
-        else launch_hot(k_amul_dot<8>, grid_for(k_amul_dot<8>, a.N), kThreads, s, a, w, f, sell_wn, sell_wo);
+        if (a.ifMask) launch_hot(k_amul_dot<8, 1>, grid_for(k_amul_dot<8, 1>, a.N), kThreads, s, a, w, f, sell_wn, sell_wo, r);
+        else launch_hot(k_amul_dot<8>, grid_for(k_amul_dot<8>, a.N), kThreads, s, a, w, f, sell_wn, sell_wo, r);
         break;
     case 9:
-        if (a.ifMask) launch_hot(k_amul_dot<9, 1>, grid_for(k_amul_dot<9, 1>, a.N, 2), kThreads, s, a, w, f, sell_wn, sell_wo);
-        else launch_hot(k_amul_dot<9>, grid_for(k_amul_dot<9>, a.N, 2), kThreads, s, a, w, f, sell_wn, sell_wo);
+        if (a.ifMask) launch_hot(k_amul_dot<9, 1>, grid_for(k_amul_dot<9, 1>, a.N, 2), kThreads, s, a, w, f, sell_wn, sell_wo, r);
+        else launch_hot(k_amul_dot<9>, grid_for(k_amul_dot<9>, a.N, 2), kThreads, s, a, w, f, sell_wn, sell_wo, r);
         break;
-    default: launch_hot(k_amul_dot<0>, grid_for(k_amul_dot<0>, a.N), kThreads, s, a, w, f, sell_wn, sell_wo); break;
+    default: launch_hot(k_amul_dot<0>, grid_for(k_amul_dot<0>, a.N), kThreads, s, a, w, f, sell_wn, sell_wo, r); break;
     }
 }
 
@@ -1183,10 +1191,11 @@ void launch_amul_dot_dir(cudaStream_t s, const MeshArgs& a, const Workspace& w, 
     else launch_hot(k_amul_dot_dir<false>, g, kThreads, s, a, w);
 }
 
-void launch_update(cudaStream_t s, int grid, const MeshArgs& a, const Workspace& w, bool fin, int psi_mode)
+void launch_update(cudaStream_t s, int grid, const MeshArgs& a, const Workspace& w, bool fin, int psi_mode,
+                   bool reverse)
 {
     (void)grid;
-    launch_hot(k_update, grid_for(k_update, a.N, 2), kThreads, s, a.N, w, fin ? 1 : 0, psi_mode);
+    launch_hot(k_update, grid_for(k_update, a.N, 2), kThreads, s, a.N, w, fin ? 1 : 0, psi_mode, reverse ? 1 : 0);
 }
 
 // the pending half of a deferred pair when the loop stopped after an even-indexed iteration

@@ -206,6 +206,53 @@ SellHost build_sell(int N, const std::vector<int>& ownerStart, const std::vector
     return S;
 }
 
+EllStencil build_ell_stencil(int N, const std::vector<int>& ownerStart, const std::vector<int>& losortStart,
+                             const std::vector<int>& losort, const std::vector<int>& ownerLo,
+                             const std::vector<int>& neighbour)
+{
+    EllStencil E;
+    const int chunks = (N + 31) / 32;
+    E.meta.assign(8 * (size_t)chunks, 0);
+    E.lane.assign((size_t)N, 0u);
+    for (int k = 0; k < chunks; ++k) {
+        const int c0 = 32 * k, c1 = std::min(N, c0 + 32);
+        std::vector<long long> dn, dO;
+        bool ok = true;
+        for (int c = c0; c < c1 && ok; ++c) {
+            for (int q = losortStart[c]; q < losortStart[c + 1]; ++q) {
+                dn.push_back((long long)ownerLo[q] - c);
+                if (losort[q] - ownerStart[ownerLo[q]] >= 32) ok = false;
+            }
+            for (int f = ownerStart[c]; f < ownerStart[c + 1]; ++f) dO.push_back((long long)neighbour[f] - c);
+        }
+        std::sort(dn.begin(), dn.end());
+        dn.erase(std::unique(dn.begin(), dn.end()), dn.end());
+        std::sort(dO.begin(), dO.end());
+        dO.erase(std::unique(dO.begin(), dO.end()), dO.end());
+        if (!ok || dn.size() > 3 || dO.size() > 3) continue;
+        for (size_t t = 0; t < dn.size(); ++t) E.meta[8 * k + 1 + t] = (int)dn[t];
+        for (size_t t = 0; t < dO.size(); ++t) E.meta[8 * k + 4 + t] = (int)dO[t];
+        for (int c = c0; c < c1; ++c) {
+            unsigned w = 0;
+            for (int q = losortStart[c]; q < losortStart[c + 1]; ++q) {
+                const long long d = (long long)ownerLo[q] - c;
+                const int t = (int)(std::lower_bound(dn.begin(), dn.end(), d) - dn.begin());
+                w |= 1u << t;
+                w |= (unsigned)(losort[q] - ownerStart[ownerLo[q]]) << (6 + 5 * t);
+            }
+            for (int f = ownerStart[c]; f < ownerStart[c + 1]; ++f) {
+                const long long d = (long long)neighbour[f] - c;
+                const int t = (int)(std::lower_bound(dO.begin(), dO.end(), d) - dO.begin());
+                w |= 1u << (3 + t);
+            }
+            E.lane[c] = w;
+        }
+        E.meta[8 * k] = 1;
+        E.compressed++;
+    }
+    return E;
+}
+
 void level_schedule(int N, const std::vector<int>& owner, const std::vector<int>& neighbour,
                     const std::vector<int>& ownerStart, const std::vector<int>& losortStart,
                     const std::vector<int>& losort, std::vector<int>& order_f, std::vector<int>& order_b,

@@ -470,9 +470,70 @@ def test_fused_direction_is_bitwise_neutral(mode):
     m = gen.perturbed(24, 0.15)  # 13824 cells: above the single-CTA threshold, ELL layout
     g, b = gen.gamma_lognormal(m), gen.rhs(m)
     h = P.Mesh.from_mesh(m)
+    h.set_option(P.spuma.OPT_ALT_SWEEP, 0)  # the fused kernel sweeps ascending only
     res = []
     for fm in (0, mode):
         h.set_option(P.spuma.OPT_FUSE_DIRECTION, fm)
         psi, perf, _, _ = gpu_solve_case(m, g, b, 0, (1e-8, 0.0, 5000, 0), handle=h)
         res.append((psi, perf))
     assert res[0][1] == res[1][1] and np.array_equal(res[0][0], res[1][0])
+
+
+def _two_lattices():
+    """two lattice blocks numbered one after the other: chunks inside a block have <= 3 column
+    offsets per side (stencil-compressed), the chunk straddling the blocks has more (explicit)"""
+    a = gen.box(9, 5, 3, (1, 1, 1))
+    b = gen.box(7, 6, 2, (1, 1, 1))
+    n = a.n_cells + b.n_cells
+    owner = np.concatenate([a.owner, b.owner + a.n_cells]).astype(np.int32)
+    nbr = np.concatenate([a.neighbour, b.neighbour + a.n_cells]).astype(np.int32)
+    return gen.Mesh(n, owner, nbr, np.concatenate([a.Sf, b.Sf]), np.concatenate([a.magSf, b.magSf]),
+                    np.concatenate([a.Cf, b.Cf]), np.concatenate([a.C, b.C + 5.0]), np.concatenate([a.V, b.V]), [])
+
+
+@pytest.mark.parametrize("name,mesh", [("cube33", gen.cube(33)), ("cavity20", gen.cavity2d(20)),
+                                       ("box_odd", gen.box(37, 11, 5)), ("two_lattices", _two_lattices())],
+                         ids=["cube33", "cavity20", "box_odd", "two_lattices"])
+def test_ell_stencil_rows_bit_exact(name, mesh):
+    """SPUMA_OPT_ELL_STENCIL: the chunk-stencil rows (per-chunk column offsets + one word per
+    cell) give bitwise the explicit-slot rows and the oracle's Amul, and a PCG solve is bitwise
+    unchanged (same Amul values, same reduction order)."""
+    rng = np.random.default_rng(9)
+    diag = rng.uniform(-4, -1, mesh.n_cells)
+    upper = rng.uniform(0.1, 1, mesh.n_faces)
+    x = rng.standard_normal(mesh.n_cells)
+    ref = O.amul(mesh, diag, upper, x)
+    h = P.Mesh.from_mesh(mesh)
+    out = []
+    for st in (1, 0):
+        h.set_option(P.spuma.OPT_ELL_STENCIL, st)
+        y = torch.empty(mesh.n_cells, dtype=torch.float64, device="cuda")
+        h.amul(dev(diag), dev(upper), None, dev(x), y)
+        out.append(y.cpu().numpy())
+        assert np.array_equal(out[-1], ref), st
+    g, b = gen.gamma_lognormal(mesh), gen.rhs(mesh)
+    h.set_option(P.spuma.OPT_SMALL_SOLVE_MAX_CELLS, 0)
+    res = []
+    for st in (1, 0):
+        h.set_option(P.spuma.OPT_ELL_STENCIL, st)
+        psi, perf, _, _ = gpu_solve_case(mesh, g, b, 0, (0.0, 0.0, 300, 300), handle=h)
+        res.append((psi, perf))
+    assert res[0][1] == res[1][1] and np.array_equal(res[0][0], res[1][0])
+
+
+def test_alt_sweep_changes_only_the_dot_rounding():
+    """SPUMA_OPT_ALT_SWEEP reverses the sweep of every other hot-loop kernel: the same element
+    operations, per-thread partial sums in the other order -> iterates equal to rounding,
+    iteration counts within 1, both within the Q11 bar of the oracle."""
+    m = gen.perturbed(26, 0.15)
+    g, b = gen.gamma_lognormal(m), gen.rhs(m)
+    _, po, _ = O.solve_case(m, g, b, 0, 0.0, O.controls(1e-8))
+    h = P.Mesh.from_mesh(m)
+    res = []
+    for alt in (1, 0):
+        h.set_option(P.spuma.OPT_ALT_SWEEP, alt)
+        psi, perf, _, _ = gpu_solve_case(m, g, b, 0, (1e-8, 0.0, 5000, 0), handle=h)
+        assert abs(perf["n_iterations"] - po["n_iterations"]) <= 2
+        res.append((psi, perf))
+    assert abs(res[0][1]["n_iterations"] - res[1][1]["n_iterations"]) <= 1
+    assert rel_l2(res[0][0], res[1][0]) <= 1e-9
