@@ -418,7 +418,9 @@ spuma_status spuma_set_batch(spuma_mesh m, int iterations);
  * producer/consumer pipeline (cp.async.bulk + mbarrier), 4 per-row at 8 CTAs/SM,
  * 5 unrolled two rows per thread, 6/7 SELL-C-32 slot layout with packed neighbour
  * side (one / two rows per thread), 8/9 ELL with a per-solve owner-slot ordered
- * coefficient copy (no row extents streamed; one / two rows per thread).
+ * coefficient copy (no row extents streamed; one / two rows per thread), 10 (default) the
+ * ELL rows of 8 software-pipelined (the next row's slot loads issued before the current
+ * row's gathers).
  * Errors: INVALID_ARGUMENT. */
 typedef enum {
     SPUMA_OPT_AMUL_VARIANT = 0,

@@ -373,6 +373,96 @@ __device__ __forceinline__ void amul_rows_ell(const MeshArgs& a, int c, int wn, 
     }
 }
 
+// Variant 10: the ELL rows of variant 8 software-pipelined across the grid-stride loop -- the
+// first-level loads of the thread's NEXT row (diag, x, the six slots, the owner-side
+// coefficients) are issued before the second-level gathers of the current row, so two rows'
+// worth of loads are in flight per thread (the row gather is latency-bound at the register-
+// capped occupancy).  Same slots, same order: bitwise the variant-8 rows.
+struct EllL1 {
+    int c;
+    double dg, xc;
+    unsigned pk[3];
+    int nb[3];
+    double uo[3];
+};
+
+__device__ __forceinline__ void ell_load1(const MeshArgs& a, int c, int wn, int wo, const double* __restrict__ diag,
+                                          const double* __restrict__ upper_s, const double* __restrict__ x, EllL1& L)
+{
+    L.c = c;
+    const int cc = min(c, a.N - 1), k = cc >> 5, l = c & 31;
+    L.dg = __ldg(diag + cc);
+    L.xc = __ldg(x + cc);
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+        L.pk[j] = j < wn ? __ldg(a.sell_n + (size_t)32 * wn * k + 32 * j + l) : 0xFFFFFFFFu;
+        L.nb[j] = j < wo ? __ldg(a.sell_o + (size_t)32 * wo * k + 32 * j + l) : -1;
+        L.uo[j] = j < wo ? __ldg(upper_s + (size_t)32 * wo * k + 32 * j + l) : 0.0;
+    }
+}
+
+template <int IFM>
+__device__ __forceinline__ void ell_finish(const MeshArgs& a, const EllL1& L, int wo, const double* __restrict__ upper_s,
+                                           const double* __restrict__ iface, const double* __restrict__ x,
+                                           const double* __restrict__ xr, double* __restrict__ y, double& acc, bool dot)
+{
+    const int cc = min(L.c, a.N - 1);
+    double un[3], xn[3], xo[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+        const bool vn = L.pk[j] != 0xFFFFFFFFu;
+        const int col = vn ? (int)(L.pk[j] >> 5) : cc;
+        const int pos = (int)(L.pk[j] & 31u);
+        un[j] = vn ? __ldg(upper_s + (size_t)32 * wo * (col >> 5) + 32 * pos + (col & 31)) : 0.0;
+        xn[j] = __ldg(x + col);
+        xo[j] = __ldg(x + (L.nb[j] >= 0 ? L.nb[j] : cc));
+    }
+    double s = L.dg * L.xc;
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+        if (L.pk[j] != 0xFFFFFFFFu) s = s + un[j] * xn[j];
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+        if (L.nb[j] >= 0) s = s + L.uo[j] * xo[j];
+    if constexpr (IFM == 1) s = add_iface(a, cc, s, iface, xr);
+    if (L.c < a.N) {
+        y[cc] = s;
+        if (dot && (IFM != 2 || !is_iface_row(a, cc))) acc += s * L.xc;
+    }
+}
+
+// the grid-stride row loop of variant 10 (rev: descending, SPUMA_OPT_ALT_SWEEP)
+template <int IFM>
+__device__ __forceinline__ void amul_ell_pipelined(const MeshArgs& a, const double* __restrict__ diag,
+                                                   const double* __restrict__ upper,
+                                                   const double* __restrict__ iface, const double* __restrict__ x,
+                                                   const double* __restrict__ xr, double* __restrict__ y, double& acc,
+                                                   bool dot, int rev)
+{
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int st = gridDim.x * blockDim.x, t00 = (blockIdx.x * (blockDim.x / 32) + warp) * 32;
+    const int cnt = t00 < a.N ? (a.N - 1 - t00) / st + 1 : 0;
+    const int wn = a.ell_wn, wo = a.ell_wo;
+    if (wn > 3 || wo > 3) {  // not an ELL mesh: plain per-row gathers
+        for (int j = 0; j < cnt; ++j) {
+            const int c = t00 + (rev ? cnt - 1 - j : j) * st + lane;
+            if (c < a.N) {
+                const double v = amul_row(a, c, diag, upper, iface, x, xr, nullptr, IFM != 2);
+                y[c] = v;
+                if (dot && (IFM != 2 || !is_iface_row(a, c))) acc += v * x[c];
+            }
+        }
+        return;
+    }
+    EllL1 cur, nxt;
+    if (cnt > 0) ell_load1(a, t00 + (rev ? cnt - 1 : 0) * st + lane, wn, wo, diag, a.upper_s, x, cur);
+    for (int j = 0; j < cnt; ++j) {
+        if (j + 1 < cnt) ell_load1(a, t00 + (rev ? cnt - 2 - j : j + 1) * st + lane, wn, wo, diag, a.upper_s, x, nxt);
+        ell_finish<IFM>(a, cur, wo, a.upper_s, iface, x, xr, y, acc, dot);
+        cur = nxt;
+    }
+}
+
 // ---------------------------------------------------------------------------- variant 3 (TMA)
 namespace tma {
 

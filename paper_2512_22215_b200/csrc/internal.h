@@ -181,7 +181,7 @@ struct spuma_mesh_s {
     // captured iteration batches (ping-pong) and timing events
     int batch = 16;
     int small_max_cells = 8192;  // single-CTA solve at or below this many cells (1 rank)
-    int amul_variant = 8;
+    int amul_variant = 10;  // ELL rows, software-pipelined (falls back to 6 -> 5 off uniform meshes)
     bool defer_psi = true;  // psi += alpha pA applied every second iteration (same rounding, fewer bytes)  // ELL + coefficient copy (falls back to 6 -> 5 when the mesh is not uniform)
     bool timing = false;
     int fuse_direction = 0;      // 0: k_direction + k_amul_dot (default: faster); 1: fused, rD read; 2: fused, 1/diag inline

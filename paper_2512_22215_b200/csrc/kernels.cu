@@ -292,7 +292,7 @@ __global__ void __launch_bounds__(kThreads)
 template <int V>
 constexpr int amul_min_ctas()
 {
-    return V == 4 ? 8 : (V == 3 ? 4 : ((V == 5 || V == 7 || V == 9) ? 3 : ((V == 6 || V == 8) ? 5 : 6)));
+    return V == 4 ? 8 : (V == 3 ? 4 : ((V == 5 || V == 7 || V == 9) ? 3 : ((V == 6 || V == 8) ? 5 : (V == 10 ? 4 : 6))));
 }
 
 template <int V, int IFM = 0>
@@ -325,6 +325,9 @@ __global__ void __launch_bounds__(V == 3 ? tma::kBlock : kThreads, amul_min_ctas
         const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
         for (int t0 = (blockIdx.x * (kThreads / 32) + warp) * 32 * R; t0 < a.N; t0 += gridDim.x * kThreads * R)
             amul_rows_ell<R, IFM>(a, t0 + lane, a.ell_wn, a.ell_wo, diag, upper, a.upper_s, iface, x, xr, y, acc, false);
+    } else if constexpr (V == 10) {
+        double acc = 0.0;
+        amul_ell_pipelined<IFM>(a, diag, upper, iface, x, xr, y, acc, false, 0);
     } else {
         for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < a.N; c += gridDim.x * blockDim.x)
             y[c] = V == 2 ? amul_row_unrolled(a, c, diag, upper, iface, x, xr)
@@ -466,6 +469,10 @@ __global__ void __launch_bounds__(V == 3 ? tma::kBlock : kThreads, amul_min_ctas
             amul_rows_ell<R, IFM>(a, t0 + lane, a.ell_wn, a.ell_wo, p.diag, p.upper, a.upper_s, p.iface, w.pA, w.xr, w.wA,
                              acc, true);
         }
+        v[0] = acc;
+    } else if constexpr (V == 10) {
+        double acc = 0.0;
+        amul_ell_pipelined<IFM>(a, p.diag, p.upper, p.iface, w.pA, w.xr, w.wA, acc, true, rev);
         v[0] = acc;
     } else {
         for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < a.N; c += gridDim.x * blockDim.x) {
@@ -994,6 +1001,9 @@ int occupancy_grid(int N, int* grid_faces, int F)
     g = std::max(g, grid_for(k_amul_dot<7, 2>, N, 2));
     g = std::max(g, grid_for(k_amul_dot<8, 2>, N));
     g = std::max(g, grid_for(k_amul_dot<9, 2>, N, 2));
+    g = std::max(g, grid_for(k_amul_dot<10>, N));
+    g = std::max(g, grid_for(k_amul_dot<10, 1>, N));
+    g = std::max(g, grid_for(k_amul_dot<10, 2>, N));
     g = std::max(g, grid_for(k_iface_rows, N));
     g = std::max(g, grid_for(k_update, N, 2));
     if (grid_faces) *grid_faces = grid_for(k_face_coeffs, F);
@@ -1045,6 +1055,7 @@ void launch_amul(cudaStream_t s, int variant, const MeshArgs& a, const double* d
                  int sell_wo)
 {
     if (a.N <= 0) return;
+    if (variant == 10 && !a.upper_s) variant = 6;
     if ((variant == 8 || variant == 9) && !a.upper_s) variant -= 2;
     if ((variant == 6 || variant == 7) && !a.sell_n) variant = 5;
     const tma::Bounds bd{a.F, x_len, a.N, sell_wn, sell_wo};
@@ -1073,6 +1084,10 @@ void launch_amul(cudaStream_t s, int variant, const MeshArgs& a, const double* d
         if (a.ifMask) k_amul<9, 1><<<grid_for(k_amul<9, 1>, a.N, 2), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd);
         else k_amul<9><<<grid_for(k_amul<9>, a.N, 2), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd);
         break;
+    case 10:
+        if (a.ifMask) k_amul<10, 1><<<grid_for(k_amul<10, 1>, a.N), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd);
+        else k_amul<10><<<grid_for(k_amul<10>, a.N), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd);
+        break;
     default: k_amul<0><<<grid_for(k_amul<0>, a.N), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd); break;
     }
 }
@@ -1087,7 +1102,7 @@ __global__ void k_ell_coeffs(MeshArgs a, const double* __restrict__ upper, doubl
     }
 }
 
-bool amul_uses_ell(int variant) { return variant == 8 || variant == 9; }
+bool amul_uses_ell(int variant) { return variant == 8 || variant == 9 || variant == 10; }
 
 void launch_ell_coeffs(cudaStream_t s, const MeshArgs& a, const double* upper, double* upper_s)
 {
@@ -1132,6 +1147,7 @@ void launch_direction(cudaStream_t s, int grid, const MeshArgs& a, const Workspa
 
 int resolve_amul_variant(int variant, const MeshArgs& a)
 {
+    if (variant == 10 && !a.upper_s) variant = 6;
     if ((variant == 8 || variant == 9) && !a.upper_s) variant -= 2;  // no uniform-width layout: SELL
     if ((variant == 6 || variant == 7) && !a.sell_n) variant = 5;    // layout not encodable on this mesh
     return variant;
@@ -1148,6 +1164,7 @@ void launch_amul_dot(cudaStream_t s, int variant, const MeshArgs& a, const Works
         case 7: launch_hot(k_amul_dot<7, 2>, grid_for(k_amul_dot<7, 2>, a.N, 2), kThreads, s, a, w, f, sell_wn, sell_wo, r); return;
         case 8: launch_hot(k_amul_dot<8, 2>, grid_for(k_amul_dot<8, 2>, a.N), kThreads, s, a, w, f, sell_wn, sell_wo, r); return;
         case 9: launch_hot(k_amul_dot<9, 2>, grid_for(k_amul_dot<9, 2>, a.N, 2), kThreads, s, a, w, f, sell_wn, sell_wo, r); return;
+        case 10: launch_hot(k_amul_dot<10, 2>, grid_for(k_amul_dot<10, 2>, a.N), kThreads, s, a, w, f, sell_wn, sell_wo, r); return;
         default: break;  // other variants add the interface terms inline (halo must precede them)
         }
     }
@@ -1174,6 +1191,10 @@ void launch_amul_dot(cudaStream_t s, int variant, const MeshArgs& a, const Works
     case 9:
         if (a.ifMask) launch_hot(k_amul_dot<9, 1>, grid_for(k_amul_dot<9, 1>, a.N, 2), kThreads, s, a, w, f, sell_wn, sell_wo, r);
         else launch_hot(k_amul_dot<9>, grid_for(k_amul_dot<9>, a.N, 2), kThreads, s, a, w, f, sell_wn, sell_wo, r);
+        break;
+    case 10:
+        if (a.ifMask) launch_hot(k_amul_dot<10, 1>, grid_for(k_amul_dot<10, 1>, a.N), kThreads, s, a, w, f, sell_wn, sell_wo, r);
+        else launch_hot(k_amul_dot<10>, grid_for(k_amul_dot<10>, a.N), kThreads, s, a, w, f, sell_wn, sell_wo, r);
         break;
     default: launch_hot(k_amul_dot<0>, grid_for(k_amul_dot<0>, a.N), kThreads, s, a, w, f, sell_wn, sell_wo, r); break;
     }
