@@ -222,6 +222,10 @@ def run_gpu(args, rank, world, local_rank):
         uid = obj[0]
     h = P.Mesh.from_mesh(mesh, stream=stream.cuda_stream, rank=rank, n_ranks=world, nccl_unique_id=uid)
     h.set_batch(args.batch)
+    if args.amul_variant is not None:
+        h.set_option(P.spuma.OPT_AMUL_VARIANT, args.amul_variant)
+    if args.alt_sweep is not None:
+        h.set_option(P.spuma.OPT_ALT_SWEEP, args.alt_sweep)
     f64 = dict(dtype=torch.float64, device=dev)
     diag, upper = torch.empty(N, **f64), torch.empty(F, **f64)
     b_dev = torch.as_tensor(b, **f64)
@@ -356,6 +360,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-kernel-timing", action="store_true")
+    ap.add_argument("--amul-variant", type=int, default=None, help="A/B only (default: the library's)")
+    ap.add_argument("--alt-sweep", type=int, default=None, help="A/B only (default: the library's)")
     args = ap.parse_args()
     rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
     if args.impl == "reference":
