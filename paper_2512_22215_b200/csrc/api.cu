@@ -284,6 +284,18 @@ spuma_status halo_exchange(spuma_mesh m, const double* x, double* xr, cudaStream
     return SPUMA_OK;
 }
 
+// NCCL communicator health, polled when an iteration batch ends (SURVEY §5 failure detection):
+// an asynchronous NCCL error (a peer died, a network failure) surfaces as SPUMA_ERR_NCCL
+spuma_status nccl_async_check(spuma_mesh m)
+{
+    if (!m->comm) return SPUMA_OK;
+    ncclResult_t r = ncclSuccess;
+    SPUMA_NCCL(ncclCommGetAsyncError(m->comm, &r));
+    if (r != ncclSuccess && r != ncclInProgress)
+        return set_error(SPUMA_ERR_NCCL, std::string("NCCL asynchronous error: ") + ncclGetErrorString(r));
+    return SPUMA_OK;
+}
+
 // all ranks' 4 partials (device, [4]) into out ([4 * n_ranks], rank order) on stream s
 spuma_status allgather4(spuma_mesh m, const double* in, double* out, cudaStream_t s)
 {
@@ -1468,6 +1480,7 @@ static spuma_status mesh_create_impl(const spuma_mesh_desc* d, spuma_mesh m)
 
 spuma_status spuma_mesh_create(const spuma_mesh_desc* d, spuma_mesh* out)
 {
+    SPUMA_NVTX("spuma_mesh_create");
     if (!out) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "out is NULL");
     *out = nullptr;
     if (!d) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "desc is NULL");
@@ -1495,6 +1508,7 @@ spuma_status spuma_assemble_laplacian(spuma_mesh m, const spuma_scalar* gamma, c
                                       spuma_label ref_cell, spuma_scalar ref_value, spuma_scalar* diag,
                                       spuma_scalar* upper, spuma_scalar* source, spuma_scalar* iface_coeffs)
 {
+    SPUMA_NVTX("spuma_assemble_laplacian");
     if (!m) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "mesh is NULL");
     if ((m->N > 0 && (!diag || !source)) || (m->F > 0 && !upper))
         return set_error(SPUMA_ERR_INVALID_ARGUMENT, "NULL diag/upper/source");
@@ -1562,6 +1576,7 @@ spuma_status spuma_assemble_laplacian(spuma_mesh m, const spuma_scalar* gamma, c
 spuma_status spuma_amul(spuma_mesh m, const spuma_scalar* diag, const spuma_scalar* upper,
                         const spuma_scalar* iface_coeffs, const spuma_scalar* x, spuma_scalar* y)
 {
+    SPUMA_NVTX("spuma_amul");
     if (!m) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "mesh is NULL");
     if (m->N > 0 && (!diag || !x || !y)) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "NULL array");
     if (m->F > 0 && !upper) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "upper is NULL");
@@ -1595,6 +1610,7 @@ spuma_status spuma_pcg_solve(spuma_mesh m, const spuma_scalar* diag, const spuma
                              const spuma_scalar* iface_coeffs, const spuma_scalar* source, spuma_scalar* psi,
                              const spuma_solver_controls* ctl, spuma_solver_perf* perf)
 {
+    SPUMA_NVTX("spuma_pcg_solve");
     if (!m) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "mesh is NULL");
     if (!ctl || !perf) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "NULL controls/perf");
     if (m->N > 0 && (!diag || !source || !psi)) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "NULL array");
@@ -1636,6 +1652,7 @@ spuma_status spuma_pcg_solve(spuma_mesh m, const spuma_scalar* diag, const spuma
     }
 
     // ---- A6 setup
+    spuma::NvtxRange nvtx_loop("A6 setup + A7-A11 loop");
     const MeshArgs a = mesh_args(m);
     if (amul_uses_ell(m->amul_variant) && m->d_upper_s) {
         launch_ell_coeffs(s, a, P.upper, m->d_upper_s);
@@ -1682,6 +1699,7 @@ spuma_status spuma_pcg_solve(spuma_mesh m, const spuma_scalar* diag, const spuma
                 prev_n = m->h_scal[pg].n;
             }
             done = m->h_scal[pg].done;
+            SPUMA_TRY(nccl_async_check(m));
         }
         ++b;
         if (b > 2 + (ctl->max_iter + m->gexec_batch - 1) / m->gexec_batch + 1)
@@ -1714,6 +1732,7 @@ spuma_status spuma_pcg_solve(spuma_mesh m, const spuma_scalar* diag, const spuma
 spuma_status spuma_surface_integrate(spuma_mesh m, const spuma_scalar* phi, const spuma_scalar* const* patch_phi,
                                      const spuma_scalar* V, spuma_scalar* out)
 {
+    SPUMA_NVTX("spuma_surface_integrate");
     if (!m) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "mesh is NULL");
     if ((m->F > 0 && !phi) || (m->N > 0 && (!V || !out))) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "NULL array");
     cudaStream_t s = m->stream;
@@ -1740,6 +1759,7 @@ spuma_status spuma_face_flux(spuma_mesh m, const spuma_scalar* gamma, const spum
                              const spuma_scalar* const* patch_corr_flux, spuma_scalar* flux,
                              spuma_scalar* const* patch_flux, spuma_scalar* phi, spuma_scalar* const* patch_phi)
 {
+    SPUMA_NVTX("spuma_face_flux");
     if (!m) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "mesh is NULL");
     if ((m->F > 0 && !upper) || (m->N > 0 && !psi)) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "NULL array");
     cudaStream_t s = m->stream;
@@ -1791,6 +1811,7 @@ spuma_status spuma_laplacian_correction(spuma_mesh m, const spuma_scalar* gamma,
                                         const spuma_scalar* V, spuma_scalar* source, spuma_scalar* corr_flux,
                                         spuma_scalar* const* patch_corr_flux)
 {
+    SPUMA_NVTX("spuma_laplacian_correction");
     if (!m) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "mesh is NULL");
     if (m->N > 0 && (!p || !V || !source)) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "NULL array");
     cudaStream_t s = m->stream;
@@ -2006,6 +2027,7 @@ spuma_status spuma_gamg_solve(spuma_mesh m, const spuma_scalar* diag, const spum
                               const spuma_solver_controls* ctl, const spuma_gamg_params* params,
                               spuma_solver_perf* perf)
 {
+    SPUMA_NVTX("spuma_gamg_solve");
     if (!m) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "mesh is NULL");
     if (!ctl || !perf) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "NULL controls/perf");
     if (m->N > 0 && (!diag || !source || !psi)) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "NULL array");
@@ -2138,6 +2160,7 @@ spuma_status spuma_pcg_solve_pc(spuma_mesh m, const spuma_scalar* diag, const sp
                                 const spuma_solver_controls* ctl, const spuma_preconditioner* pcp,
                                 spuma_solver_perf* perf)
 {
+    SPUMA_NVTX("spuma_pcg_solve_pc");
     if (!m) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "mesh is NULL");
     if (!ctl || !perf) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "NULL controls/perf");
     if (m->N > 0 && (!diag || !source || !psi)) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "NULL array");
@@ -2220,6 +2243,7 @@ spuma_status spuma_pbicg_solve(spuma_mesh m, const spuma_scalar* diag, const spu
                                const spuma_solver_controls* ctl, const spuma_preconditioner* pcp,
                                spuma_solver_perf* perf)
 {
+    SPUMA_NVTX("spuma_pbicg_solve");
     if (!m) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "mesh is NULL");
     if (!ctl || !perf) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "NULL controls/perf");
     if (m->N > 0 && (!diag || !source || !psi)) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "NULL array");
@@ -2309,6 +2333,7 @@ spuma_status spuma_precondition(spuma_mesh m, const spuma_scalar* diag, const sp
                                 const spuma_scalar* lower, const spuma_preconditioner* pcp, const spuma_scalar* r,
                                 spuma_scalar* wout, int transpose)
 {
+    SPUMA_NVTX("spuma_precondition");
     if (!m || !pcp) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "NULL argument");
     if (m->N > 0 && (!diag || !r || !wout)) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "NULL array");
     if (m->F > 0 && !upper) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "upper is NULL");
@@ -2335,6 +2360,7 @@ spuma_status spuma_precondition(spuma_mesh m, const spuma_scalar* diag, const sp
 spuma_status spuma_amul_asym(spuma_mesh m, const spuma_scalar* diag, const spuma_scalar* upper,
                              const spuma_scalar* lower, const spuma_scalar* x, spuma_scalar* y, int transpose)
 {
+    SPUMA_NVTX("spuma_amul_asym");
     if (!m) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "mesh is NULL");
     if (m->N > 0 && (!diag || !x || !y)) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "NULL array");
     if (m->F > 0 && (!upper || !lower)) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "upper/lower is NULL");
@@ -2380,6 +2406,7 @@ spuma_status spuma_ldu_to_csr(spuma_mesh m, spuma_label* row_ptr, spuma_label* c
 spuma_status spuma_csr_values(spuma_mesh m, const spuma_scalar* diag, const spuma_scalar* upper,
                               const spuma_scalar* lower, spuma_scalar* values)
 {
+    SPUMA_NVTX("spuma_csr_values");
     if (!m || !diag || !values || (m->F > 0 && (!upper || !lower)))
         return set_error(SPUMA_ERR_INVALID_ARGUMENT, "NULL argument");
     if (!m->pc || !m->pc->csr_map) return set_error(SPUMA_ERR_STATE, "call spuma_ldu_to_csr first");

@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>  // header-only; ranges are no-ops unless a profiler is attached
 
 #include <cstdint>
 #include <string>
@@ -198,6 +199,18 @@ struct spuma_mesh_s {
     GamgState* gamg = nullptr;  // GAMG hierarchy + captured cycle, built on first spuma_gamg_solve
     PcState* pc = nullptr;      // level schedules + buffers of the DIC/DILU/PBiCG solvers
 };
+
+// NVTX range per C-ABI call and solver phase (SURVEY §5 tracing): visible in nsys / ncu
+// --nvtx timelines, free otherwise
+namespace spuma {
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+}  // namespace spuma
+#define SPUMA_NVTX(name) spuma::NvtxRange spuma_nvtx_range_(name)
 
 // error plumbing (api.cu)
 namespace spuma {
