@@ -475,6 +475,23 @@ typedef struct {
 } spuma_comm_callbacks;
 spuma_status spuma_set_comm_callbacks(spuma_mesh m, const spuma_comm_callbacks* cb);
 
+/* Peer-memory transport (halo and rank-partial exchanges as direct stores
+ * into the neighbours' device memory over NVLink, no NCCL).  Every rank calls
+ * spuma_peer_export (allocates its mailbox and writes a SPUMA_PEER_BLOB_BYTES description:
+ * CUDA IPC handle, rank, processor patches), the blobs are all-gathered by the caller (any
+ * host transport), and every rank calls spuma_peer_import with the n_ranks blobs in rank
+ * order ([n_ranks][SPUMA_PEER_BLOB_BYTES] bytes).  From then on every collective of the handle
+ * (PCG, PCG-pc, PBiCG, GAMG, assembly halos) runs as device kernels: the halo pack is fused
+ * into the P2P stores, completion is signalled by system-scope release/acquire epoch flags,
+ * and the iteration batches stay CUDA-graph captured.  Ranks may share one GPU (tests).
+ * spuma_peer_check returns SPUMA_ERR_STATE if a poll ever timed out (~20 s).
+ * Errors: INVALID_ARGUMENT (n_ranks > 64, > 32 processor patches, bad or out-of-order blobs),
+ * ADDRESSING (the ranks' processor patches do not pair up), STATE, CUDA. */
+#define SPUMA_PEER_BLOB_BYTES 512
+spuma_status spuma_peer_export(spuma_mesh m, void* blob);
+spuma_status spuma_peer_import(spuma_mesh m, const void* blobs, int n_blobs);
+spuma_status spuma_peer_check(spuma_mesh m);
+
 /* Fill out128 with a fresh ncclUniqueId (rank 0 calls it and broadcasts). */
 spuma_status spuma_nccl_get_unique_id(void* out128);
 

@@ -255,6 +255,14 @@ spuma_status patches_out(spuma_mesh m, double* const* pv, const double* src)
 
 spuma_status halo_exchange(spuma_mesh m, const double* x, double* xr, cudaStream_t s)
 {
+    if (m->peer) {  // pack fused into the peer stores (peer.cu)
+        if (m->px.n_patches == 0) return SPUMA_OK;
+        PeerXfer d = m->px;
+        for (int p = 0; p < d.n_patches; ++p) d.off[p] = m->cb_offsets[p], d.count[p] = m->cb_counts[p];
+        launch_peer_exchange(s, d, x, m->d_if_cell, xr, m->pst);
+        m->stats.kernel_launches += 2;
+        return SPUMA_OK;
+    }
     if (m->n_ranks == 1) return SPUMA_OK;
     if (m->external_comm) {
         if (!m->cb.exchange) return set_error(SPUMA_ERR_STATE, "external comm: callbacks not set");
@@ -299,6 +307,11 @@ spuma_status nccl_async_check(spuma_mesh m)
 // all ranks' 4 partials (device, [4]) into out ([4 * n_ranks], rank order) on stream s
 spuma_status allgather4(spuma_mesh m, const double* in, double* out, cudaStream_t s)
 {
+    if (m->peer) {
+        launch_peer_allgather4(s, m->pg, in, out, m->pst);
+        m->stats.kernel_launches += 1;
+        return SPUMA_OK;
+    }
     if (m->external_comm) {
         if (!m->cb.allgather) return set_error(SPUMA_ERR_STATE, "external comm: callbacks not set");
         SPUMA_CUDA(cudaMemcpyAsync(m->h_part, in, 4 * sizeof(double), cudaMemcpyDeviceToHost, s));
@@ -332,6 +345,14 @@ spuma_status exchange_counts(spuma_mesh m, const std::vector<int>& counts, const
     int n = 0;
     std::vector<int> offsets(counts.size());
     for (size_t p = 0; p < counts.size(); ++p) offsets[p] = n, n += counts[p];
+    if (m->peer) {  // each patch's data lands in the receiver's level-0 region of that patch
+        if (m->px.n_patches == 0) return SPUMA_OK;
+        PeerXfer d = m->px;
+        for (int p = 0; p < d.n_patches; ++p) d.off[p] = offsets[p], d.count[p] = counts[p];
+        launch_peer_exchange(s, d, send, nullptr, recv, m->pst);
+        m->stats.kernel_launches += 2;
+        return SPUMA_OK;
+    }
     if (m->external_comm) {
         if (!m->cb.exchange) return set_error(SPUMA_ERR_STATE, "external comm: callbacks not set");
         std::vector<double> hs(n + 1), hr(n + 1);
@@ -556,7 +577,7 @@ bool host_allgather4(void* ctx, const double* in, double* out)
     double* d = nullptr;
     if (cudaMalloc(reinterpret_cast<void**>(&d), sizeof(double) * 4 * (m->n_ranks + 1)) != cudaSuccess) return false;
     bool ok = cudaMemcpy(d, in, 4 * sizeof(double), cudaMemcpyHostToDevice) == cudaSuccess &&
-              ncclAllGather(d, d + 4, 4, ncclDouble, m->comm, m->stream) == ncclSuccess &&
+              allgather4(m, d, d + 4, m->stream) == SPUMA_OK &&
               cudaMemcpyAsync(out, d + 4, 4 * sizeof(double) * m->n_ranks, cudaMemcpyDeviceToHost, m->stream) ==
                   cudaSuccess &&
               cudaStreamSynchronize(m->stream) == cudaSuccess;
@@ -1176,6 +1197,10 @@ void spuma_free(spuma_mesh m)
     if (m->h_recv) cudaFreeHost(m->h_recv);
     if (m->h_part) cudaFreeHost(m->h_part);
     if (m->h_scal) cudaFreeHost(m->h_scal);
+    for (void* p : m->peer_mapped)
+        if (p) cudaIpcCloseMemHandle(p);
+    if (m->d_mail) cudaFree(m->d_mail);
+    if (m->pst.ctr) cudaFree(m->pst.ctr);
     if (m->comm) ncclCommDestroy(m->comm);
     if (m->comm_stream) cudaStreamDestroy(m->comm_stream);
     if (m->ev_fork) cudaEventDestroy(m->ev_fork);
@@ -1979,6 +2004,138 @@ spuma_status spuma_set_option(spuma_mesh m, int option, int value)
         return SPUMA_OK;
     default: return set_error(SPUMA_ERR_INVALID_ARGUMENT, "unknown option");
     }
+}
+
+// ---------------------------------------------------------------------------
+// peer-memory transport (peer.cu): blob = {IPC handle of the mailbox, rank, n_ranks, n_iface,
+// processor patches (peer, offset, count)}; import maps every other rank's mailbox
+// ---------------------------------------------------------------------------
+namespace {
+struct PeerBlob {
+    cudaIpcMemHandle_t handle;
+    int32_t magic, rank, n_ranks, n_iface, n_patches;
+    int32_t peer[kMaxPeerPatches], offset[kMaxPeerPatches], count[kMaxPeerPatches];
+};
+static_assert(sizeof(PeerBlob) <= SPUMA_PEER_BLOB_BYTES, "peer blob too large");
+constexpr int32_t kPeerMagic = 0x53504d41;  // "SPMA"
+
+// mailbox layout (8-byte units): halo [2][n_iface] | partials [2][n_ranks][4] |
+// halo flags [2][n_ranks] | partial flags [2][n_ranks]
+inline size_t mail_units(int n_iface, int P) { return 2 * (size_t)n_iface + 12 * (size_t)P; }
+}  // namespace
+
+spuma_status spuma_peer_export(spuma_mesh m, void* blob)
+{
+    SPUMA_NVTX("spuma_peer_export");
+    if (!m || !blob) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (m->n_ranks < 2) return set_error(SPUMA_ERR_STATE, "peer transport needs n_ranks > 1");
+    if (m->n_ranks > kMaxPeerRanks || (int)m->cb_peers.size() > kMaxPeerPatches)
+        return set_error(SPUMA_ERR_INVALID_ARGUMENT, "too many ranks or processor patches for the peer transport");
+    if (!m->d_mail) {
+        m->mail_units = mail_units(m->n_iface, m->n_ranks);
+        SPUMA_CUDA(cudaMalloc(reinterpret_cast<void**>(&m->d_mail), sizeof(double) * m->mail_units));
+        SPUMA_CUDA(cudaMemset(m->d_mail, 0, sizeof(double) * m->mail_units));
+        SPUMA_CUDA(cudaMalloc(reinterpret_cast<void**>(&m->pst.ctr), 64));
+        SPUMA_CUDA(cudaMemset(m->pst.ctr, 0, 64));
+        m->pst.ticket = reinterpret_cast<unsigned*>(m->pst.ctr + 2);
+        m->pst.err = reinterpret_cast<int*>(m->pst.ctr + 3);
+        SPUMA_CUDA(cudaDeviceSynchronize());
+    }
+    PeerBlob b{};
+    SPUMA_CUDA(cudaIpcGetMemHandle(&b.handle, m->d_mail));
+    b.magic = kPeerMagic;
+    b.rank = m->rank;
+    b.n_ranks = m->n_ranks;
+    b.n_iface = m->n_iface;
+    b.n_patches = (int)m->cb_peers.size();
+    for (int p = 0; p < b.n_patches; ++p) b.peer[p] = m->cb_peers[p], b.offset[p] = m->cb_offsets[p], b.count[p] = m->cb_counts[p];
+    std::memset(blob, 0, SPUMA_PEER_BLOB_BYTES);
+    std::memcpy(blob, &b, sizeof b);
+    return SPUMA_OK;
+}
+
+spuma_status spuma_peer_import(spuma_mesh m, const void* blobs, int n_blobs)
+{
+    SPUMA_NVTX("spuma_peer_import");
+    if (!m || !blobs) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (!m->d_mail) return set_error(SPUMA_ERR_STATE, "spuma_peer_export first");
+    if (n_blobs != m->n_ranks) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "one blob per rank (rank order)");
+    const int P = m->n_ranks;
+    std::vector<PeerBlob> B(P);
+    for (int r = 0; r < P; ++r) {
+        std::memcpy(&B[r], static_cast<const char*>(blobs) + (size_t)r * SPUMA_PEER_BLOB_BYTES, sizeof(PeerBlob));
+        if (B[r].magic != kPeerMagic || B[r].rank != r || B[r].n_ranks != P)
+            return set_error(SPUMA_ERR_INVALID_ARGUMENT, "peer blob " + std::to_string(r) + " invalid or out of order");
+    }
+    std::vector<double*> base(P, nullptr);
+    for (int r = 0; r < P; ++r) {
+        if (r == m->rank) {
+            base[r] = m->d_mail;
+            continue;
+        }
+        void* p = nullptr;
+        SPUMA_CUDA(cudaIpcOpenMemHandle(&p, B[r].handle, cudaIpcMemLazyEnablePeerAccess));
+        m->peer_mapped.push_back(p);
+        base[r] = static_cast<double*>(p);
+    }
+    auto halo = [&](int r, int par) { return base[r] + (size_t)par * B[r].n_iface; };
+    auto part = [&](int r, int par) { return base[r] + 2 * (size_t)B[r].n_iface + (size_t)par * 4 * P; };
+    auto hflag = [&](int r, int par) {
+        return reinterpret_cast<unsigned long long*>(base[r] + 2 * (size_t)B[r].n_iface + 8 * (size_t)P) + par * P;
+    };
+    auto pflag = [&](int r, int par) {
+        return reinterpret_cast<unsigned long long*>(base[r] + 2 * (size_t)B[r].n_iface + 10 * (size_t)P) + par * P;
+    };
+    PeerXfer& d = m->px;
+    d = PeerXfer{};
+    d.n_patches = (int)m->cb_peers.size();
+    std::vector<int> used(P, 0);  // k-th patch of mine to rank q <-> k-th patch of q to me
+    for (int p = 0; p < d.n_patches; ++p) {
+        const int q = m->cb_peers[p];
+        if (q < 0 || q >= P || q == m->rank) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "bad processor patch peer");
+        int k = used[q]++, j = -1;
+        for (int t = 0; t < B[q].n_patches; ++t)
+            if (B[q].peer[t] == m->rank && k-- == 0) {
+                j = t;
+                break;
+            }
+        if (j < 0 || B[q].count[j] != m->cb_counts[p])
+            return set_error(SPUMA_ERR_ADDRESSING, "processor patches of ranks " + std::to_string(m->rank) + " and " +
+                                                       std::to_string(q) + " do not match");
+        for (int par = 0; par < 2; ++par) {
+            d.dst[p][par] = halo(q, par) + B[q].offset[j];
+            d.dst_flag[p][par] = hflag(q, par) + m->rank;
+            d.src[p][par] = halo(m->rank, par) + m->cb_offsets[p];
+            d.src_flag[p][par] = hflag(m->rank, par) + q;
+        }
+    }
+    PeerGather& g = m->pg;
+    g = PeerGather{};
+    g.n_ranks = P;
+    g.rank = m->rank;
+    for (int r = 0; r < P; ++r)
+        for (int par = 0; par < 2; ++par) {
+            g.part[r][par] = part(r, par);
+            g.flag[r][par] = pflag(r, par);
+        }
+    for (int par = 0; par < 2; ++par) {
+        g.my_part[par] = part(m->rank, par);
+        g.my_flag[par] = pflag(m->rank, par);
+    }
+    m->peer = true;
+    m->external_comm = false;  // graph-capturable from now on
+    destroy_graphs(m);
+    return SPUMA_OK;
+}
+
+spuma_status spuma_peer_check(spuma_mesh m)
+{
+    if (!m) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "mesh is NULL");
+    if (!m->peer) return SPUMA_OK;
+    int e = 0;
+    SPUMA_CUDA(cudaMemcpy(&e, m->pst.err, sizeof e, cudaMemcpyDeviceToHost));
+    if (e) return set_error(SPUMA_ERR_STATE, "peer transport: a neighbour did not answer within the poll limit");
+    return SPUMA_OK;
 }
 
 spuma_status spuma_set_comm_callbacks(spuma_mesh m, const spuma_comm_callbacks* cb)

@@ -9,7 +9,6 @@ namespace spuma {
 // helpers
 // ---------------------------------------------------------------------------
 
-// Sum NV values over the CTA; the result is valid in thread 0.
 // Grid-stride index sequence of this thread over [0, n): ascending, or descending when rev
 // (consecutive kernels that alternate the direction start on the lines the previous one
 // touched last, which are still in L2).  The same indices either way; only the order (and
@@ -24,6 +23,7 @@ struct GridStride {
     __device__ __forceinline__ int at(int j) const { return i0 + (rev ? cnt - 1 - j : j) * st; }
 };
 
+// Sum NV values over the CTA; the result is valid in thread 0.
 template <int NV>
 __device__ __forceinline__ void cta_sum(double (&v)[NV])
 {

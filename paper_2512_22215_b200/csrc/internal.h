@@ -101,6 +101,30 @@ struct GLevel {
     int ncif;                     // next level's interface faces
 };
 
+// Peer-memory transport (peer.cu): kernel-parameter descriptors of one exchange / all-gather
+constexpr int kMaxPeerPatches = 32;
+constexpr int kMaxPeerRanks = 64;
+struct PeerXfer {
+    int n_patches;
+    int off[kMaxPeerPatches], count[kMaxPeerPatches];           // this exchange: local offsets / counts
+    double* dst[kMaxPeerPatches][2];                              // receiver's region for my patch (parity)
+    unsigned long long* dst_flag[kMaxPeerPatches][2];             // receiver's flag slot for me (parity)
+    const double* src[kMaxPeerPatches][2];                        // my region written by patch p's peer
+    const unsigned long long* src_flag[kMaxPeerPatches][2];       // my flag slot for patch p's peer
+};
+struct PeerGather {
+    int n_ranks, rank;
+    double* part[kMaxPeerRanks][2];               // rank t's partials block [n_ranks][4] (parity)
+    unsigned long long* flag[kMaxPeerRanks][2];   // rank t's partial flags [n_ranks] (parity)
+    const double* my_part[2];
+    const unsigned long long* my_flag[2];
+};
+struct PeerState {
+    unsigned long long* ctr;  // [2] exchange / all-gather epochs (device)
+    unsigned* ticket;
+    int* err;                 // set on a poll timeout
+};
+
 struct Patch {
     int kind, n_faces, offset;   // offset into the concatenated boundary arrays
     int neighbour_rank;          // processor
@@ -126,6 +150,14 @@ struct spuma_mesh_s {
     double *h_send = nullptr, *h_recv = nullptr, *h_part = nullptr;  // pinned (external comm)
     std::vector<int> cb_peers, cb_offsets, cb_counts;
     std::vector<int> h_if_cell;          // [n_iface] local cell of each processor face, (patch, face) order
+    // peer-memory transport (spuma_peer_export / spuma_peer_import; peer.cu)
+    bool peer = false;
+    double* d_mail = nullptr;            // this rank's mailbox (IPC-exported)
+    size_t mail_units = 0;
+    std::vector<void*> peer_mapped;      // opened IPC mappings (to close)
+    spuma::PeerXfer px{};                // level-0 exchange descriptor (off/count per call)
+    spuma::PeerGather pg{};
+    spuma::PeerState pst{};
 
     std::vector<spuma::Patch> patches;
     // host copies of the derived addressing (internal numbering) for diagnostics
@@ -373,5 +405,9 @@ void launch_gamg_gs2_res(cudaStream_t s, const GLevel& L, const DevPtrs* P, cons
 void launch_gamg_gs2_upd(cudaStream_t s, const GLevel& L, const DevPtrs* P, const double* xin, const double* xc,
                          const double* alpha, const double* r, const double* zin, double* out, bool skip_lower,
                          bool last, bool psi_acc);
+// peer-memory transport (peer.cu)
+void launch_peer_exchange(cudaStream_t s, const PeerXfer& d, const double* x, const int* idx, double* recv,
+                          const PeerState& st);
+void launch_peer_allgather4(cudaStream_t s, const PeerGather& g, const double* in, double* out, const PeerState& st);
 extern bool g_use_pdl;  // programmatic dependent launch of the hot-loop kernels (process-wide)
 }  // namespace spuma

@@ -32,6 +32,7 @@ OPT_GAMG_TAIL_CELLS = 4
 OPT_FUSE_DIRECTION = 5
 OPT_ALT_SWEEP = 6
 OPT_ELL_STENCIL = 7
+PEER_BLOB_BYTES = 512  # SPUMA_PEER_BLOB_BYTES
 AMUL_VARIANTS = (0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10)
 
 _vp, _ci, _cd, _lab = ctypes.c_void_p, ctypes.c_int, ctypes.c_double, ctypes.c_int32
@@ -153,6 +154,10 @@ def lib():
         L.spuma_nccl_get_unique_id.argtypes = [_vp]
         if hasattr(L, "spuma_set_comm_callbacks"):  # absent only in older A/B builds
             L.spuma_set_comm_callbacks.argtypes = [_vp, ctypes.POINTER(CommCallbacks)]
+        if hasattr(L, "spuma_peer_export"):
+            L.spuma_peer_export.argtypes = [_vp, _vp]
+            L.spuma_peer_import.argtypes = [_vp, _vp, _ci]
+            L.spuma_peer_check.argtypes = [_vp]
         if hasattr(L, "spuma_gamg_solve"):
             L.spuma_gamg_default_params.argtypes = [ctypes.POINTER(GamgParams)]
             L.spuma_gamg_default_params.restype = None
@@ -179,7 +184,8 @@ def lib():
                      "spuma_mesh_get_addressing", "spuma_mesh_get_geometry", "spuma_get_stats",
                      "spuma_reset_stats", "spuma_set_timing", "spuma_set_batch", "spuma_nccl_get_unique_id",
                      "spuma_set_option", "spuma_set_comm_callbacks", "spuma_surface_integrate",
-                     "spuma_face_flux", "spuma_laplacian_correction"):
+                     "spuma_face_flux", "spuma_laplacian_correction", "spuma_peer_export", "spuma_peer_import",
+                     "spuma_peer_check"):
             if hasattr(L, name):
                 getattr(L, name).restype = _ci
         if L.spuma_abi_version() != ABI_VERSION:
@@ -339,6 +345,30 @@ class Mesh:
         _check(lib().spuma_gamg_solve(self._h, d, u, f, s, p, ctypes.byref(ctl),
                                       None if params is None else ctypes.byref(params), ctypes.byref(perf)))
         return perf.as_dict()
+
+    def peer_export(self) -> bytes:
+        """spuma_peer_export: this rank's peer-transport blob (CUDA IPC handle + patches)."""
+        buf = ctypes.create_string_buffer(PEER_BLOB_BYTES)
+        _check(lib().spuma_peer_export(self._h, buf))
+        return buf.raw
+
+    def peer_import(self, blobs) -> None:
+        """spuma_peer_import: every rank's blob, rank order."""
+        data = b"".join(bytes(b) for b in blobs)
+        buf = ctypes.create_string_buffer(data, len(data))
+        _check(lib().spuma_peer_import(self._h, buf, len(blobs)))
+
+    def enable_peer_transport(self) -> None:
+        """Switch this handle's collectives to the peer-memory transport: the blobs are
+        all-gathered over the default torch.distributed process group (host plumbing only)."""
+        import torch.distributed as dist
+        mine = self.peer_export()
+        allb = [None] * dist.get_world_size()
+        dist.all_gather_object(allb, mine)
+        self.peer_import(allb)
+
+    def peer_check(self) -> None:
+        _check(lib().spuma_peer_check(self._h))
 
     def gamg_hierarchy(self, params: Optional[GamgParams] = None, with_ftc: bool = True) -> dict:
         """spuma_gamg_get_hierarchy: level sizes and (internal-numbering) fine-to-coarse maps."""
