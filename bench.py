@@ -135,7 +135,7 @@ def load_traffic(workload):
 
 
 # ---------------------------------------------------------------------------- workload
-def build_workload(n, rank, world):
+def build_workload(n, rank, world, cdev="cuda"):
     """C3: one n^3 block per rank of the global (n px, n py, n pz) cube (px,py,pz) = 1/2x1x1/2x2x1/2x2x2."""
     import gen
     wl = f"C3 cube {n}^3 per GPU (weak), gamma=1, tol 1e-6"
@@ -149,7 +149,7 @@ def build_workload(n, rank, world):
     m = gen.weak_block(n, nproc, rank)
     # b = V (2U - 1) keyed by global cell id, minus the GLOBAL mean (all-reduced)
     b = m.V * (2.0 * gen.uniform(gen.SEED_RHS, 0, m.gid) - 1.0)
-    t = torch.tensor([b.sum(), float(m.n_cells)], dtype=torch.float64, device="cuda")
+    t = torch.tensor([b.sum(), float(m.n_cells)], dtype=torch.float64, device=cdev)
     dist.all_reduce(t)
     b = b - float(t[0] / t[1])
     ref = 0 if rank == 0 else -1  # global cell 0 lives on rank 0, local cell 0
@@ -207,20 +207,52 @@ def run_gpu(args, rank, world, local_rank):
     import torch
     import paper_2512_22215_b200 as P
 
+    # SPUMA_BENCH_SHARE_GPU=1 (testing only): every rank on cuda:0, host plumbing over gloo -- runs the
+    # whole N > 1 code path (peer transport) on a one-GPU box; not a scaling measurement
+    share = os.environ.get("SPUMA_BENCH_SHARE_GPU") == "1"
+    if share:
+        local_rank = 0
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
+    cdev = torch.device("cpu") if share else dev  # device of the host-plumbing collectives
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
-    mesh, b, ref, cfg = build_workload(args.n, rank, world)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+    mesh, b, ref, cfg = build_workload(args.n, rank, world, cdev)
     N, F = mesh.n_cells, mesh.n_faces
     stream = torch.cuda.current_stream()
     uid = None
-    if world > 1:
+    transport = "none (1 rank)"
+    h = None
+    if world > 1 and args.transport == "peer":
+        # device-side transport over peer memory (CUDA IPC over NVLink): halo stores and
+        # rank-partial all-gathers inside the kernels; NCCL if any rank cannot map its peers
+        h = P.Mesh.from_mesh(mesh, stream=stream.cuda_stream, rank=rank, n_ranks=world)
+        err = ""
+        try:
+            h.enable_peer_transport()
+        except Exception as e:  # noqa: BLE001
+            err = str(e).splitlines()[0][:120]
+        flag = torch.tensor([1.0 if err else 0.0], device=cdev)
+        torch.distributed.all_reduce(flag)
+        if flag.item() == 0.0:
+            transport = "peer (CUDA IPC / NVLink, in-kernel halo + all-gather)"
+        else:
+            torch.distributed.barrier()
+            h.free()
+            h = None
+            transport = f"nccl (peer transport unavailable: {err or 'on another rank'})"
+    if world > 1 and h is None:
         obj = [P.nccl_get_unique_id() if rank == 0 else None]
         torch.distributed.broadcast_object_list(obj, src=0)
         uid = obj[0]
-    h = P.Mesh.from_mesh(mesh, stream=stream.cuda_stream, rank=rank, n_ranks=world, nccl_unique_id=uid)
+        if not transport.startswith("nccl"):
+            transport = "nccl (send/recv halo, all-gather of rank partials)"
+    if h is None:
+        h = P.Mesh.from_mesh(mesh, stream=stream.cuda_stream, rank=rank, n_ranks=world, nccl_unique_id=uid)
     h.set_batch(args.batch)
     if args.amul_variant is not None:
         h.set_option(P.spuma.OPT_AMUL_VARIANT, args.amul_variant)
@@ -261,7 +293,7 @@ def run_gpu(args, rank, world, local_rank):
     clk = clocks.stop()
     t = e0.elapsed_time(e1) / 1000.0
     if world > 1:
-        tt = torch.tensor([t], dtype=torch.float64, device=dev)
+        tt = torch.tensor([t], dtype=torch.float64, device=cdev)
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         t = float(tt.item())
     st = h.get_stats()
@@ -307,7 +339,7 @@ def run_gpu(args, rank, world, local_rank):
         wall = time.perf_counter() - w0
         te = max(e0.elapsed_time(e1) / 1000.0, wall)
         if world > 1:
-            tt = torch.tensor([te], dtype=torch.float64, device=dev)
+            tt = torch.tensor([te], dtype=torch.float64, device=cdev)
             torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
             te = float(tt.item())
         eit = sum(p["n_iterations"] for p in eperfs)
@@ -325,7 +357,7 @@ def run_gpu(args, rank, world, local_rank):
         # how many oracle cores one B200 is worth on this workload
         cpu["coe_cores_per_gpu"] = value / cpu["value"]
     traffic = load_traffic(cfg["workload"])
-    cfg.update({"global_cells": n_global, "faces_per_gpu": F, "parallelism": f"dd{world}",
+    cfg.update({"global_cells": n_global, "faces_per_gpu": F, "parallelism": f"dd{world}", "transport": transport,
                 "iterations_per_step": iters / max(len(perfs), 1), "l2": "inputs larger than L2 (no flush)",
                 "batch_iterations": st["batch_iterations"], "grid": st["blocks_per_grid"],
                 "effective_iteration_GBps": eff_gbs,
@@ -360,6 +392,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-kernel-timing", action="store_true")
+    ap.add_argument("--transport", default="peer", choices=["peer", "nccl"],
+                    help="N > 1: device-side peer-memory transport (default) or NCCL")
     ap.add_argument("--amul-variant", type=int, default=None, help="A/B only (default: the library's)")
     ap.add_argument("--alt-sweep", type=int, default=None, help="A/B only (default: the library's)")
     args = ap.parse_args()
