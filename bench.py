@@ -385,7 +385,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="spuma", choices=["spuma", "reference"])
-    ap.add_argument("--n", type=int, default=200, help="cube edge per GPU (C3: 200)")
+    ap.add_argument("--edge", "--n", dest="n", type=int, default=200, help="cube edge per GPU (C3: 200)")
     ap.add_argument("--batch", type=int, default=16)
     ap.add_argument("--cpu-iters", type=int, default=150)
     ap.add_argument("--ref-iters", type=int, default=20)
