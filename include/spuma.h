@@ -420,7 +420,8 @@ spuma_status spuma_set_batch(spuma_mesh m, int iterations);
  * side (one / two rows per thread), 8/9 ELL with a per-solve owner-slot ordered
  * coefficient copy (no row extents streamed; one / two rows per thread), 10 (default) the
  * ELL rows of 8 software-pipelined (the next row's slot loads issued before the current
- * row's gathers).
+ * row's gathers), 11 the ELL rows with the first-level loads streamed by a per-warp
+ * cp.async.bulk ring into shared memory (measured slower; A/B only).
  * Errors: INVALID_ARGUMENT. */
 typedef enum {
     SPUMA_OPT_AMUL_VARIANT = 0,

@@ -663,4 +663,93 @@ __device__ double amul_tma(const MeshArgs& a, const double* __restrict__ diag, c
 }
 
 }  // namespace tma
+
+// ---------------------------------------------------------------------------- variant 11 (bulk ring)
+// The ELL rows of variant 8 with the first dependent level moved into a per-warp ring of
+// cp.async.bulk copies: each warp owns kD shared-memory stages; lane 0 issues the next chunks'
+// slot indices, owner-side coefficients, diag and x (2 KB per 32-cell chunk, one mbarrier per
+// stage with expect_tx) kD chunks ahead, so ~kD chunks of streamed bytes are in flight per warp
+// while the lanes run the second-level gathers of the current chunk from L2.  Same slots,
+// same order: bitwise the variant-8 rows.
+namespace ring {
+
+constexpr int kD = 6;              // stages per warp
+constexpr int kStageBytes = 2048;  // widths <= 3: 128 wn + 128 wo + 256 wo + 256 (diag) + 256 (x)
+constexpr int kWarps = kThreads / 32;
+constexpr int kSmem = kWarps * kD * kStageBytes + kWarps * kD * 8;
+
+template <int IFM, bool DOT>
+__device__ __forceinline__ double amul_ring(const MeshArgs& a, const double* __restrict__ diag,
+                                            const double* __restrict__ upper, const double* __restrict__ iface,
+                                            const double* __restrict__ x, const double* __restrict__ xr,
+                                            double* __restrict__ y, int rev)
+{
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int wn = a.ell_wn, wo = a.ell_wo;
+    double acc = 0.0;
+    if (wn > 3 || wo > 3) {  // not an ELL mesh
+        amul_ell_pipelined<IFM>(a, diag, upper, iface, x, xr, y, acc, DOT, rev);
+        return acc;
+    }
+    unsigned char* wbase = smem + (size_t)warp * kD * kStageBytes;
+    unsigned long long* bar = reinterpret_cast<unsigned long long*>(smem + kWarps * kD * kStageBytes) + warp * kD;
+    const int nchunks = (a.N + 31) >> 5, nfull = a.N >> 5;  // chunks < nfull hold 32 cells
+    const int wid = blockIdx.x * kWarps + warp, wst = gridDim.x * kWarps;
+    const int cnt = wid < nchunks ? (nchunks - 1 - wid) / wst + 1 : 0;
+    const uint32_t bn = 128u * wn, bo = 128u * wo, bu = 256u * wo;
+    const uint32_t offO = bn, offU = bn + bo, offD = bn + bo + bu, offX = offD + 256u;
+    auto chunk = [&](int j) { return wid + (rev ? cnt - 1 - j : j) * wst; };
+    auto issue = [&](int j) {  // lane 0: stage j's copies into slot j % kD
+        const int k = chunk(j);
+        if (k >= nfull) return;
+        unsigned char* st = wbase + (size_t)(j % kD) * kStageBytes;
+        unsigned long long* b = &bar[j % kD];
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the lanes' reads of the slot first
+        tma::bar_arrive_tx(b, bn + bo + bu + 512u);
+        if (bn) tma::bulk_g2s(st, a.sell_n + (size_t)32 * wn * k, bn, b);
+        if (bo) {
+            tma::bulk_g2s(st + offO, a.sell_o + (size_t)32 * wo * k, bo, b);
+            tma::bulk_g2s(st + offU, a.upper_s + (size_t)32 * wo * k, bu, b);
+        }
+        tma::bulk_g2s(st + offD, diag + (size_t)32 * k, 256u, b);
+        tma::bulk_g2s(st + offX, x + (size_t)32 * k, 256u, b);
+    };
+    if (lane == 0) {
+        for (int s = 0; s < kD; ++s) tma::bar_init(&bar[s], 1);
+        tma::bar_fence_init();
+        for (int j = 0; j < kD && j < cnt; ++j) issue(j);
+    }
+    __syncwarp();
+    uint32_t phase = 0;  // bit s: the parity slot s completes next
+    for (int j = 0; j < cnt; ++j) {
+        const int k = chunk(j), s = j % kD;
+        EllL1 L;
+        if (k < nfull) {
+            const unsigned char* st = wbase + (size_t)s * kStageBytes;
+            tma::bar_wait(&bar[s], (phase >> s) & 1u);
+            phase ^= 1u << s;
+            const unsigned* sn = reinterpret_cast<const unsigned*>(st);
+            const int* so = reinterpret_cast<const int*>(st + offO);
+            const double* su = reinterpret_cast<const double*>(st + offU);
+            L.c = 32 * k + lane;
+            L.dg = reinterpret_cast<const double*>(st + offD)[lane];
+            L.xc = reinterpret_cast<const double*>(st + offX)[lane];
+#pragma unroll
+            for (int jj = 0; jj < 3; ++jj) {
+                L.pk[jj] = jj < wn ? sn[32 * jj + lane] : 0xFFFFFFFFu;
+                L.nb[jj] = jj < wo ? so[32 * jj + lane] : -1;
+                L.uo[jj] = jj < wo ? su[32 * jj + lane] : 0.0;
+            }
+        } else {  // the partial last chunk: plain loads (its slot was never filled)
+            ell_load1(a, 32 * k + lane, wn, wo, diag, a.upper_s, x, L);
+        }
+        __syncwarp();
+        if (lane == 0 && j + kD < cnt) issue(j + kD);
+        ell_finish<IFM>(a, L, wo, a.upper_s, iface, x, xr, y, acc, DOT);
+    }
+    return acc;
+}
+
+}  // namespace ring
 }  // namespace spuma

@@ -401,7 +401,7 @@ spuma_status enqueue_iteration(spuma_mesh m, cudaStream_t s, std::vector<cudaEve
     // alternating sweeps (slot parity): C asc, A desc, B asc | C desc, A asc, B desc | ...
     const bool odd = m->alt_sweep && (slot & 1);
     const bool alt = m->alt_sweep;
-    const bool overlap = !fin && m->n_iface > 0 && rv >= 6 && rv <= 10;
+    const bool overlap = !fin && m->n_iface > 0 && rv >= 6 && rv <= 11;
     if (fin && m->defer_psi && m->fuse_direction && rv == 8 && fused_direction_ok(a)) {
         // direction formed inside the Amul gather (one pass less per iteration)
         if (ev) record(m, *ev, slot * 6 + 0, s);
@@ -1998,7 +1998,7 @@ spuma_status spuma_set_option(spuma_mesh m, int option, int value)
         m->small_max_cells = value;
         return SPUMA_OK;
     case SPUMA_OPT_AMUL_VARIANT:
-        if (value < 0 || value > 10) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "amul variant must be 0..10");
+        if (value < 0 || value > 11) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "amul variant must be 0..11");
         if (value != m->amul_variant) destroy_graphs(m);
         m->amul_variant = value;
         return SPUMA_OK;

@@ -292,7 +292,7 @@ __global__ void __launch_bounds__(kThreads)
 template <int V>
 constexpr int amul_min_ctas()
 {
-    return V == 4 ? 8 : (V == 3 ? 4 : ((V == 5 || V == 7 || V == 9) ? 3 : ((V == 6 || V == 8) ? 5 : (V == 10 ? 4 : 6))));
+    return V == 4 ? 8 : (V == 3 ? 4 : ((V == 5 || V == 7 || V == 9) ? 3 : ((V == 6 || V == 8) ? 5 : (V == 10 ? 4 : (V == 11 ? 2 : 6)))));
 }
 
 template <int V, int IFM = 0>
@@ -328,6 +328,8 @@ __global__ void __launch_bounds__(V == 3 ? tma::kBlock : kThreads, amul_min_ctas
     } else if constexpr (V == 10) {
         double acc = 0.0;
         amul_ell_pipelined<IFM>(a, diag, upper, iface, x, xr, y, acc, false, 0);
+    } else if constexpr (V == 11) {
+        ring::amul_ring<IFM, false>(a, diag, upper, iface, x, xr, y, 0);
     } else {
         for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < a.N; c += gridDim.x * blockDim.x)
             y[c] = V == 2 ? amul_row_unrolled(a, c, diag, upper, iface, x, xr)
@@ -474,6 +476,8 @@ __global__ void __launch_bounds__(V == 3 ? tma::kBlock : kThreads, amul_min_ctas
         double acc = 0.0;
         amul_ell_pipelined<IFM>(a, p.diag, p.upper, p.iface, w.pA, w.xr, w.wA, acc, true, rev);
         v[0] = acc;
+    } else if constexpr (V == 11) {
+        v[0] = ring::amul_ring<IFM, true>(a, p.diag, p.upper, p.iface, w.pA, w.xr, w.wA, rev);
     } else {
         for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < a.N; c += gridDim.x * blockDim.x) {
             const double y = V == 2 ? amul_row_unrolled(a, c, p.diag, p.upper, p.iface, w.pA, w.xr)
@@ -949,6 +953,22 @@ static void launch_hot(void (*kernel)(KArgs...), int grid, int block, cudaStream
     cudaLaunchKernelEx(&cfg, kernel, args...);
 }
 
+template <typename... KArgs, typename... Args>
+static void launch_hot_smem(void (*kernel)(KArgs...), int grid, int smem, cudaStream_t s, Args... args)
+{
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = g_use_pdl ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 static int g_sms = 0;
 
 static int sms()
@@ -978,6 +998,21 @@ static int grid_for(K kernel, long long work, int per_thread = 1, int threads_pe
     return (int)(g < 1 ? 1 : g);
 }
 
+// variant 11: dynamic shared memory ring (ring::kSmem per CTA)
+template <class K>
+static int ring_grid(K kernel, int N)
+{
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ring::kSmem);
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kThreads, ring::kSmem);
+    if (occ <= 0) occ = 1;
+    const long long chunks = ((long long)N + 31) / 32;
+    long long need = (chunks + ring::kWarps - 1) / ring::kWarps;
+    long long cap = (long long)occ * sms();
+    long long g = need < cap ? need : cap;
+    return (int)(g < 1 ? 1 : g);
+}
+
 int occupancy_grid(int N, int* grid_faces, int F)
 {
     // the largest grid any reduction kernel uses (sizes the partials buffer)
@@ -1001,6 +1036,9 @@ int occupancy_grid(int N, int* grid_faces, int F)
     g = std::max(g, grid_for(k_amul_dot<7, 2>, N, 2));
     g = std::max(g, grid_for(k_amul_dot<8, 2>, N));
     g = std::max(g, grid_for(k_amul_dot<9, 2>, N, 2));
+    g = std::max(g, ring_grid(k_amul_dot<11>, N));
+    g = std::max(g, ring_grid(k_amul_dot<11, 1>, N));
+    g = std::max(g, ring_grid(k_amul_dot<11, 2>, N));
     g = std::max(g, grid_for(k_amul_dot<10>, N));
     g = std::max(g, grid_for(k_amul_dot<10, 1>, N));
     g = std::max(g, grid_for(k_amul_dot<10, 2>, N));
@@ -1055,7 +1093,7 @@ void launch_amul(cudaStream_t s, int variant, const MeshArgs& a, const double* d
                  int sell_wo)
 {
     if (a.N <= 0) return;
-    if (variant == 10 && !a.upper_s) variant = 6;
+    if ((variant == 10 || variant == 11) && !a.upper_s) variant = 6;
     if ((variant == 8 || variant == 9) && !a.upper_s) variant -= 2;
     if ((variant == 6 || variant == 7) && !a.sell_n) variant = 5;
     const tma::Bounds bd{a.F, x_len, a.N, sell_wn, sell_wo};
@@ -1088,6 +1126,10 @@ void launch_amul(cudaStream_t s, int variant, const MeshArgs& a, const double* d
         if (a.ifMask) k_amul<10, 1><<<grid_for(k_amul<10, 1>, a.N), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd);
         else k_amul<10><<<grid_for(k_amul<10>, a.N), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd);
         break;
+    case 11:
+        if (a.ifMask) k_amul<11, 1><<<ring_grid(k_amul<11, 1>, a.N), kThreads, ring::kSmem, s>>>(a, diag, upper, iface, x, xr, y, bd);
+        else k_amul<11><<<ring_grid(k_amul<11>, a.N), kThreads, ring::kSmem, s>>>(a, diag, upper, iface, x, xr, y, bd);
+        break;
     default: k_amul<0><<<grid_for(k_amul<0>, a.N), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd); break;
     }
 }
@@ -1102,7 +1144,7 @@ __global__ void k_ell_coeffs(MeshArgs a, const double* __restrict__ upper, doubl
     }
 }
 
-bool amul_uses_ell(int variant) { return variant == 8 || variant == 9 || variant == 10; }
+bool amul_uses_ell(int variant) { return variant >= 8 && variant <= 11; }
 
 void launch_ell_coeffs(cudaStream_t s, const MeshArgs& a, const double* upper, double* upper_s)
 {
@@ -1147,7 +1189,7 @@ void launch_direction(cudaStream_t s, int grid, const MeshArgs& a, const Workspa
 
 int resolve_amul_variant(int variant, const MeshArgs& a)
 {
-    if (variant == 10 && !a.upper_s) variant = 6;
+    if ((variant == 10 || variant == 11) && !a.upper_s) variant = 6;
     if ((variant == 8 || variant == 9) && !a.upper_s) variant -= 2;  // no uniform-width layout: SELL
     if ((variant == 6 || variant == 7) && !a.sell_n) variant = 5;    // layout not encodable on this mesh
     return variant;
@@ -1165,6 +1207,7 @@ void launch_amul_dot(cudaStream_t s, int variant, const MeshArgs& a, const Works
         case 8: launch_hot(k_amul_dot<8, 2>, grid_for(k_amul_dot<8, 2>, a.N), kThreads, s, a, w, f, sell_wn, sell_wo, r); return;
         case 9: launch_hot(k_amul_dot<9, 2>, grid_for(k_amul_dot<9, 2>, a.N, 2), kThreads, s, a, w, f, sell_wn, sell_wo, r); return;
         case 10: launch_hot(k_amul_dot<10, 2>, grid_for(k_amul_dot<10, 2>, a.N), kThreads, s, a, w, f, sell_wn, sell_wo, r); return;
+        case 11: launch_hot_smem(k_amul_dot<11, 2>, ring_grid(k_amul_dot<11, 2>, a.N), ring::kSmem, s, a, w, f, sell_wn, sell_wo, r); return;
         default: break;  // other variants add the interface terms inline (halo must precede them)
         }
     }
@@ -1195,6 +1238,10 @@ void launch_amul_dot(cudaStream_t s, int variant, const MeshArgs& a, const Works
     case 10:
         if (a.ifMask) launch_hot(k_amul_dot<10, 1>, grid_for(k_amul_dot<10, 1>, a.N), kThreads, s, a, w, f, sell_wn, sell_wo, r);
         else launch_hot(k_amul_dot<10>, grid_for(k_amul_dot<10>, a.N), kThreads, s, a, w, f, sell_wn, sell_wo, r);
+        break;
+    case 11:
+        if (a.ifMask) launch_hot_smem(k_amul_dot<11, 1>, ring_grid(k_amul_dot<11, 1>, a.N), ring::kSmem, s, a, w, f, sell_wn, sell_wo, r);
+        else launch_hot_smem(k_amul_dot<11>, ring_grid(k_amul_dot<11>, a.N), ring::kSmem, s, a, w, f, sell_wn, sell_wo, r);
         break;
     default: launch_hot(k_amul_dot<0>, grid_for(k_amul_dot<0>, a.N), kThreads, s, a, w, f, sell_wn, sell_wo, r); break;
     }

@@ -33,7 +33,7 @@ OPT_FUSE_DIRECTION = 5
 OPT_ALT_SWEEP = 6
 OPT_ELL_STENCIL = 7
 PEER_BLOB_BYTES = 512  # SPUMA_PEER_BLOB_BYTES
-AMUL_VARIANTS = (0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10)
+AMUL_VARIANTS = (0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11)
 
 _vp, _ci, _cd, _lab = ctypes.c_void_p, ctypes.c_int, ctypes.c_double, ctypes.c_int32
 
