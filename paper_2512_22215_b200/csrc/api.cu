@@ -701,6 +701,13 @@ spuma_status gamg_ensure(spuma_mesh m, const spuma_gamg_params& gp)
                 L.a.ell_wn = sh.uniform_wn;
                 L.a.ell_wo = sh.uniform_wo;
                 L.ell = 1;
+            } else if (h.F > 0) {  // generic rows: a losort-ordered coefficient copy (one dependent load less)
+                std::vector<int> pos(h.F);
+                for (int k = 0; k < h.F; ++k) pos[h.losort[k]] = k;
+                int* lp;
+                SPUMA_TRY(gupload(G, &lp, pos, s));
+                SPUMA_TRY(galloc(G, &L.upperLo, h.F));
+                L.losortPos = lp;
             }
         }
         SPUMA_TRY(galloc(G, &L.x, n));

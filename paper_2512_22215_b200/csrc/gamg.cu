@@ -16,14 +16,20 @@
 namespace spuma {
 namespace {
 
-// row of A applied to an implicit vector x(j), in the oracle's order (Q10, no interfaces)
+// row of A applied to an implicit vector x(j), in the oracle's order (Q10, no interfaces).
+// ul: the coefficients in losort order (coarse levels, written by k_gamg_agg) -- a stream
+// instead of the upper[losort[k]] gather; nullptr: gather.
 template <class X>
 __device__ __forceinline__ double row_ax(const MeshArgs& a, int c, const double* __restrict__ diag,
-                                         const double* __restrict__ upper, const X& x)
+                                         const double* __restrict__ upper, const X& x,
+                                         const double* __restrict__ ul = nullptr)
 {
     double s = diag[c] * x(c);
     const int k1 = a.losortStart[c + 1];
-    for (int k = a.losortStart[c]; k < k1; ++k) s = s + upper[a.losort[k]] * x(a.ownerLo[k]);
+    if (ul)
+        for (int k = a.losortStart[c]; k < k1; ++k) s = s + ul[k] * x(a.ownerLo[k]);
+    else
+        for (int k = a.losortStart[c]; k < k1; ++k) s = s + upper[a.losort[k]] * x(a.ownerLo[k]);
     const int f1 = a.ownerStart[c + 1];
     for (int f = a.ownerStart[c]; f < f1; ++f) s = s + upper[f] * x(a.neighbour[f]);
     return s;
@@ -82,7 +88,7 @@ __device__ __forceinline__ double rowA(const GLevel& L, int c, const double* __r
 {
     double s;
     if constexpr (ELL) s = row_ax_ell(L.a, c, d, x);
-    else s = row_ax(L.a, c, d, u, x);
+    else s = row_ax(L.a, c, d, u, x, L.upperLo);
     return add_if<IF>(L, ic, c, s);
 }
 
@@ -154,6 +160,7 @@ __global__ void __launch_bounds__(kThreads) k_gamg_agg(GLevel F, GLevel C, const
         double u = 0.0;
         for (int k = F.cfStart[e]; k < F.cfStart[e + 1]; ++k) u = u + fu[F.cfList[k]];
         C.upper[e] = u;
+        if (C.upperLo) C.upperLo[C.losortPos[e]] = u;  // losort-ordered copy (generic rows)
         if (C.ell) {  // owner-slot copy for the ELL rows of the coarse level
             const int c = C.a.owner[e];
             const_cast<double*>(C.a.upper_s)[(size_t)32 * C.a.ell_wo * (c >> 5) + 32 * (e - C.a.ownerStart[c]) + (c & 31)] = u;
@@ -177,7 +184,7 @@ __global__ void __launch_bounds__(kThreads) k_gamg_restrict(GLevel F, GLevel C, 
             const int i = F.cList[k];
             double r = F.b[i];
             if (x) {
-                r = r - add_if<IF>(F, level_iface(F, P), i, row_ax(F.a, i, fd, fu, XPlain{x}));
+                r = r - add_if<IF>(F, level_iface(F, P), i, row_ax(F.a, i, fd, fu, XPlain{x}, F.upperLo));
                 F.r[i] = r;
             }
             s = s + r;
@@ -479,7 +486,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_gamg_tail(const GLevel* __res
         double v[2] = {0.0, 0.0};
         for (int c = tid; c < L.a.N; c += kSmallThreads) {  // scale + p/q (Q25, Q29)
             const double ci = X(c);
-            const double aci = L.ell ? row_ax_ell(L.a, c, d, X) : row_ax(L.a, c, d, u, X);
+            const double aci = L.ell ? row_ax_ell(L.a, c, d, X) : row_ax(L.a, c, d, u, X, L.upperLo);
             const double ri = L.b[c];
             const double rd = 1.0 / d[c];
             L.p[c] = ci - omega * (rd * aci);
@@ -498,7 +505,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_gamg_tail(const GLevel* __res
             const double x1 = Y(c);
             double xn = x1;
             if (n_post >= 2)
-                xn = x1 + omega * ((1.0 / d[c]) * (L.b[c] - (L.ell ? row_ax_ell(L.a, c, d, Y) : row_ax(L.a, c, d, u, Y))));
+                xn = x1 + omega * ((1.0 / d[c]) * (L.b[c] - (L.ell ? row_ax_ell(L.a, c, d, Y) : row_ax(L.a, c, d, u, Y, L.upperLo))));
             L.x[c] = xn;
         }
         __syncthreads();
@@ -507,7 +514,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_gamg_tail(const GLevel* __res
         for (int i = 2; i < n_post; ++i) {  // further plain sweeps
             for (int c = tid; c < L.a.N; c += kSmallThreads) {
                 const XPlain Z{xin};
-                const double y = L.ell ? row_ax_ell(L.a, c, d, Z) : row_ax(L.a, c, d, u, Z);
+                const double y = L.ell ? row_ax_ell(L.a, c, d, Z) : row_ax(L.a, c, d, u, Z, L.upperLo);
                 xout[c] = xin[c] + omega * ((1.0 / d[c]) * (L.b[c] - y));
             }
             __syncthreads();

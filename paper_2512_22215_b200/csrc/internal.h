@@ -91,6 +91,8 @@ struct GLevel {
     int nc, ncf;                  // next level's size
     int grid;                     // CTAs of this level's cell kernels (fixed: deterministic reductions)
     int ell;                      // 1: rows over the ELL layout (a.sell_*, a.upper_s; level 0 of a uniform mesh)
+    double* upperLo;              // coarse generic levels: coefficients in losort order (nullptr: gather)
+    const int* losortPos;         //   face -> its losort position (k_gamg_agg writes upperLo through it)
     // processor interfaces (n_ranks > 1, readings Q36-Q38): a.ifStart / a.ifIdx per cell
     const double* iface;          // [n_if] coefficients (nullptr on level 0: DevPtrs::iface)
     double* xr;                   // [n_if] the neighbours' values of the vector a row kernel gathers
