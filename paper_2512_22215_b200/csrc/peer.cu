@@ -141,7 +141,9 @@ void launch_peer_exchange(cudaStream_t s, const PeerXfer& d, const double* x, co
     int grid = (total + kThreads - 1) / kThreads;
     grid = grid < 1 ? 1 : (grid > 592 ? 592 : grid);
     k_peer_send<<<grid, kThreads, 0, s>>>(d, x, idx, st);
-    k_peer_recv<<<grid, kThreads, 0, s>>>(d, recv, st);
+    // the receiver polls: few CTAs, so that while it waits (on the comm stream, overlapped with
+    // the interior Amul) it does not hold the SM slots the Amul runs in
+    k_peer_recv<<<grid < 32 ? grid : 32, kThreads, 0, s>>>(d, recv, st);
 }
 
 void launch_peer_allgather4(cudaStream_t s, const PeerGather& g, const double* in, double* out, const PeerState& st)
