@@ -258,6 +258,10 @@ def run_gpu(args, rank, world, local_rank):
         h.set_option(P.spuma.OPT_AMUL_VARIANT, args.amul_variant)
     if args.alt_sweep is not None:
         h.set_option(P.spuma.OPT_ALT_SWEEP, args.alt_sweep)
+    if args.defer_psi is not None:
+        h.set_option(P.spuma.OPT_DEFER_PSI, args.defer_psi)
+    if args.l2_persist is not None:
+        h.set_option(P.spuma.OPT_L2_PERSIST, args.l2_persist)
     f64 = dict(dtype=torch.float64, device=dev)
     diag, upper = torch.empty(N, **f64), torch.empty(F, **f64)
     b_dev = torch.as_tensor(b, **f64)
@@ -396,6 +400,8 @@ def main():
                     help="N > 1: device-side peer-memory transport (default) or NCCL")
     ap.add_argument("--amul-variant", type=int, default=None, help="A/B only (default: the library's)")
     ap.add_argument("--alt-sweep", type=int, default=None, help="A/B only (default: the library's)")
+    ap.add_argument("--defer-psi", type=int, default=None, help="A/B only (default: the library's)")
+    ap.add_argument("--l2-persist", type=int, default=None, help="A/B only (default: the library's)")
     args = ap.parse_args()
     rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
     if args.impl == "reference":

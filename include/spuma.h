@@ -454,7 +454,10 @@ typedef enum {
      * of 6 explicit 32-bit slot indices (~19 B/cell less; bitwise the same rows).  0 = explicit
      * slots everywhere (default: same-box A/B at 200^3 measured no gain -- the row gather is
      * bound by its two dependent load levels, not by the bytes), 1 = on */
-    SPUMA_OPT_ELL_STENCIL = 7
+    SPUMA_OPT_ELL_STENCIL = 7,
+    /* PCG hot loop: an L2 access-policy window (persisting) over the direction vector pA,
+     * captured into the iteration graphs; 0 = none (default), 1 = on */
+    SPUMA_OPT_L2_PERSIST = 8
 } spuma_option;
 spuma_status spuma_set_option(spuma_mesh m, int option, int value);
 

@@ -460,6 +460,28 @@ void destroy_graphs(spuma_mesh m)
     }
 }
 
+// SPUMA_OPT_L2_PERSIST: an L2 access-policy window over the direction vector pA (the one vector
+// the Amul gathers and three kernels touch), captured into the kernel nodes; 0 = no window
+spuma_status l2_window(spuma_mesh m)
+{
+    cudaStreamAttrValue v{};
+    if (m->l2_persist && m->N > 0) {
+        int dev = 0, maxp = 0, maxw = 0;
+        SPUMA_CUDA(cudaGetDevice(&dev));
+        SPUMA_CUDA(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev));
+        SPUMA_CUDA(cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, dev));
+        const size_t win = std::min((size_t)maxw, sizeof(double) * (size_t)m->N);
+        SPUMA_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min((size_t)maxp, win)));
+        v.accessPolicyWindow.base_ptr = m->ws.pA;
+        v.accessPolicyWindow.num_bytes = win;
+        v.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)maxp / (double)win);
+        v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    }
+    SPUMA_CUDA(cudaStreamSetAttribute(m->stream, cudaStreamAttributeAccessPolicyWindow, &v));
+    return SPUMA_OK;
+}
+
 spuma_status build_graphs(spuma_mesh m)
 {
     if (m->gexec[0] && m->gexec_timed == m->timing && m->gexec_batch == batch_eff(m)) return SPUMA_OK;
@@ -473,6 +495,7 @@ spuma_status build_graphs(spuma_mesh m)
             ev = &m->tev[g];
         }
         cudaGraph_t graph = nullptr;
+        SPUMA_TRY(l2_window(m));
         SPUMA_CUDA(cudaStreamBeginCapture(m->stream, cudaStreamCaptureModeThreadLocal));
         spuma_status st = SPUMA_OK;
         // timing samples the first iteration of every batch (6 event nodes per batch keep the
@@ -1976,6 +1999,11 @@ spuma_status spuma_set_option(spuma_mesh m, int option, int value)
         if (value < 0 || value > 1) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "ell_stencil is 0 or 1");
         if (m->ell_stencil != (value != 0)) destroy_graphs(m);
         m->ell_stencil = value != 0;
+        return SPUMA_OK;
+    case SPUMA_OPT_L2_PERSIST:
+        if (value < 0 || value > 1) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "l2_persist is 0 or 1");
+        if (m->l2_persist != (value != 0)) destroy_graphs(m);
+        m->l2_persist = value != 0;
         return SPUMA_OK;
     case SPUMA_OPT_ALT_SWEEP:
         if (value < 0 || value > 1) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "alt_sweep is 0 or 1");

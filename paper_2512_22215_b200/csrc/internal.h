@@ -220,6 +220,7 @@ struct spuma_mesh_s {
     bool defer_psi = true;  // psi += alpha pA applied every second iteration (same rounding, fewer bytes)  // ELL + coefficient copy (falls back to 6 -> 5 when the mesh is not uniform)
     bool timing = false;
     int fuse_direction = 0;      // 0: k_direction + k_amul_dot (default: faster); 1: fused, rD read; 2: fused, 1/diag inline
+    bool l2_persist = false;     // L2 access-policy window over pA (SPUMA_OPT_L2_PERSIST)
     bool alt_sweep = true;       // alternate the sweep direction of consecutive hot-loop kernels (L2 reuse)
     int gamg_tail_cells = 1024;  // GAMG: levels from the first one at or below this size run in one CTA (0: off)
     cudaGraphExec_t gexec[2] = {nullptr, nullptr};
