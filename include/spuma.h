@@ -325,6 +325,17 @@ spuma_status spuma_host_gamg_hierarchy(int n_cells, int n_faces, const spuma_lab
                                        const spuma_label* neighbour, const spuma_scalar* face_weights,
                                        int n_coarsest, int max_levels, int max_out, int* n_levels,
                                        int* level_cells, int* level_faces, spuma_label* ftc);
+/* The decomposed GAMG hierarchy (Q36, Q37) of n_ranks sub-domains, built by the library's host code
+ * with an in-process transport (one thread per rank standing in for the collectives).  Per rank r:
+ * lduAddressing owner[r] / neighbour[r] [n_faces[r]], face_weights[r], its n_patches[r]
+ * processor patches (patch_peer[r][p], patch_count[r][p]) and if_cell[r] (their face cells,
+ * patch order).  Out: *n_levels; level_cells[64 r + l], level_ifaces[64 r + l] (may be NULL). */
+spuma_status spuma_host_gamg_hierarchy_dd(int n_ranks, const int* n_cells, const int* n_faces,
+                                          const spuma_label* const* owner, const spuma_label* const* neighbour,
+                                          const spuma_scalar* const* face_weights, const int* n_patches,
+                                          const int* const* patch_peer, const int* const* patch_count,
+                                          const spuma_label* const* if_cell, int n_coarsest, int max_levels,
+                                          int* n_levels, int* level_cells, int* level_ifaces);
 spuma_status spuma_host_level_schedule(int n_cells, int n_faces, const spuma_label* owner,
                                        const spuma_label* neighbour, spuma_label* order_f, spuma_label* order_b,
                                        int* depth_f, int* depth_b);

@@ -1,7 +1,12 @@
 // api.cu -- the C-ABI of libspuma (include/spuma.h): mesh handle, assembly,
 // PCG orchestration (graph-captured iteration batches), NCCL halo exchange.
 #include <algorithm>
+#include <condition_variable>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <thread>
+#include <tuple>
 #include <string>
 #include <vector>
 
@@ -2658,6 +2663,137 @@ spuma_status spuma_host_gamg_hierarchy(int n_cells, int n_faces, const spuma_lab
         if (ftc && l + 1 < (int)H.size()) {  // concatenated fine-to-coarse maps of every level but the coarsest
             std::memcpy(ftc + off, H[l].ftc.data(), sizeof(int) * H[l].ftc.size());
             off += H[l].ftc.size();
+        }
+    }
+    return SPUMA_OK;
+}
+
+namespace {
+// in-process transport of spuma_host_gamg_hierarchy_dd: one thread per rank, a shared gather
+// array and a mailbox per (source, destination, k-th patch between them), barrier-separated
+struct SimComm {
+    int P = 0;
+    std::mutex mu;
+    std::condition_variable cv;
+    int arrived = 0;
+    long long gen = 0;
+    std::vector<double> gather;
+    std::map<std::tuple<int, int, int>, std::vector<double>> box;
+    void barrier()
+    {
+        std::unique_lock<std::mutex> lk(mu);
+        const long long g = gen;
+        if (++arrived == P) {
+            arrived = 0;
+            ++gen;
+            cv.notify_all();
+        } else {
+            cv.wait(lk, [&] { return gen != g; });
+        }
+    }
+};
+struct SimRank {
+    SimComm* sc;
+    int rank;
+    std::vector<int> peers;
+};
+bool sim_allgather4(void* ctx, const double* in, double* out)
+{
+    SimRank* r = static_cast<SimRank*>(ctx);
+    {
+        std::lock_guard<std::mutex> lk(r->sc->mu);
+        std::copy(in, in + 4, r->sc->gather.begin() + 4 * r->rank);
+    }
+    r->sc->barrier();
+    {
+        std::lock_guard<std::mutex> lk(r->sc->mu);
+        std::copy(r->sc->gather.begin(), r->sc->gather.end(), out);
+    }
+    r->sc->barrier();
+    return true;
+}
+bool sim_exchange(void* ctx, const std::vector<int>& counts, const std::vector<double>& send, std::vector<double>& recv)
+{
+    SimRank* r = static_cast<SimRank*>(ctx);
+    std::map<int, int> kth;
+    {
+        std::lock_guard<std::mutex> lk(r->sc->mu);
+        int off = 0;
+        for (size_t p = 0; p < counts.size(); ++p) {
+            const int q = r->peers[p], k = kth[q]++;
+            r->sc->box[std::make_tuple(r->rank, q, k)] =
+                std::vector<double>(send.begin() + off, send.begin() + off + counts[p]);
+            off += counts[p];
+        }
+    }
+    r->sc->barrier();
+    kth.clear();
+    {
+        std::lock_guard<std::mutex> lk(r->sc->mu);
+        recv.assign(send.size(), 0.0);
+        int off = 0;
+        for (size_t p = 0; p < counts.size(); ++p) {
+            const int q = r->peers[p], k = kth[q]++;
+            const std::vector<double>& v = r->sc->box[std::make_tuple(q, r->rank, k)];
+            if ((int)v.size() != counts[p]) return false;
+            std::copy(v.begin(), v.end(), recv.begin() + off);
+            off += counts[p];
+        }
+    }
+    r->sc->barrier();
+    return true;
+}
+}  // namespace
+
+spuma_status spuma_host_gamg_hierarchy_dd(int n_ranks, const int* n_cells, const int* n_faces,
+                                          const spuma_label* const* owner, const spuma_label* const* neighbour,
+                                          const spuma_scalar* const* face_weights, const int* n_patches,
+                                          const int* const* patch_peer, const int* const* patch_count,
+                                          const spuma_label* const* if_cell, int n_coarsest, int max_levels,
+                                          int* n_levels, int* level_cells, int* level_ifaces)
+{
+    if (n_ranks < 1 || !n_cells || !n_faces || !owner || !neighbour || !face_weights || !n_patches || !n_levels ||
+        max_levels < 1)
+        return set_error(SPUMA_ERR_INVALID_ARGUMENT, "NULL argument / n_ranks < 1 / max_levels < 1");
+    SimComm sc;
+    sc.P = n_ranks;
+    sc.gather.assign(4 * (size_t)n_ranks, 0.0);
+    std::vector<SimRank> ranks(n_ranks);
+    std::vector<std::vector<GamgHostLevel>> H(n_ranks);
+    std::vector<spuma_status> st(n_ranks, SPUMA_OK);
+    std::vector<std::string> err(n_ranks);
+    auto work = [&](int r) {
+        std::vector<int> o, nb, os, ls, lo, olo;
+        st[r] = host_addressing(n_cells[r], n_faces[r], owner[r], neighbour[r], o, nb, os, ls, lo, olo);
+        if (st[r] != SPUMA_OK) err[r] = spuma_last_error();
+        std::vector<double> w(face_weights[r], face_weights[r] + n_faces[r]);
+        std::vector<int> counts(patch_count[r], patch_count[r] + n_patches[r]);
+        int n_if = 0;
+        for (int c : counts) n_if += c;
+        std::vector<int> ic(if_cell[r], if_cell[r] + n_if);
+        ranks[r] = SimRank{&sc, r, std::vector<int>(patch_peer[r], patch_peer[r] + n_patches[r])};
+        GamgComm comm;
+        comm.n_ranks = n_ranks;
+        comm.allgather4 = sim_allgather4;
+        comm.exchange = sim_exchange;
+        comm.ctx = &ranks[r];
+        bool ok = true;
+        H[r] = gamg_hierarchy_dd(n_cells[r], n_faces[r], o, nb, os, ls, lo, olo, w, ic, counts, n_coarsest, max_levels,
+                                 comm, &ok);
+        if (!ok && st[r] == SPUMA_OK) st[r] = SPUMA_ERR_NCCL;
+    };
+    // every rank must run (the collectives are lockstep), so validation errors are reported after
+    std::vector<std::thread> th;
+    for (int r = 0; r < n_ranks; ++r) th.emplace_back(work, r);
+    for (auto& t : th) t.join();
+    for (int r = 0; r < n_ranks; ++r)
+        if (st[r] != SPUMA_OK) return set_error(st[r], "rank " + std::to_string(r) + ": " + err[r]);
+    *n_levels = (int)H[0].size();
+    for (int r = 0; r < n_ranks; ++r) {
+        if ((int)H[r].size() != *n_levels) return set_error(SPUMA_ERR_STATE, "ranks disagree on the level count");
+        for (int l = 0; l < (int)H[r].size() && l < 64; ++l) {
+            if (level_cells) level_cells[64 * r + l] = H[r][l].n;
+            if (level_ifaces) level_ifaces[64 * r + l] = (int)H[r][l].if_cell.size();
         }
     }
     return SPUMA_OK;

@@ -174,6 +174,8 @@ def lib():
             L.spuma_amul_asym.argtypes = [_vp] * 6 + [_ci]
             L.spuma_ldu_to_csr.argtypes = [_vp] * 4
             L.spuma_csr_values.argtypes = [_vp] * 5
+        if hasattr(L, "spuma_host_gamg_hierarchy_dd"):
+            L.spuma_host_gamg_hierarchy_dd.argtypes = [_ci] + [_vp] * 9 + [_ci, _ci, _vp, _vp, _vp]
         if hasattr(L, "spuma_host_rcm"):
             L.spuma_host_rcm.argtypes = [_ci, _ci, _vp, _vp, _vp]
             L.spuma_host_gamg_hierarchy.argtypes = [_ci, _ci, _vp, _vp, _vp, _ci, _ci, _ci, _vp, _vp, _vp, _vp]
@@ -604,6 +606,48 @@ def host_gamg_hierarchy(n_cells: int, owner, neighbour, face_weights, n_coarsest
         maps.append(ftc[off:off + cells[k]].copy())
         off += int(cells[k])
     return {"levels": n, "cells": cells[:n].tolist(), "faces": faces[:n].tolist(), "ftc": maps}
+
+
+def host_gamg_hierarchy_dd(meshes, n_coarsest=10, max_levels=50) -> dict:
+    """spuma_host_gamg_hierarchy_dd: the decomposed hierarchy (Q36, Q37) libspuma builds for the
+    sub-meshes (duck-typed: n_cells, owner, neighbour, magSf, patches with kind / n_faces /
+    face_cells / neighbour_rank), one thread per rank standing in for the collectives."""
+    P = len(meshes)
+    keep = []
+
+    def arr(a, dt):
+        x = np.ascontiguousarray(a, dt)
+        if x.size == 0:
+            x = np.zeros(1, dt)
+        keep.append(x)
+        return x.ctypes.data
+
+    def tab(ptrs):
+        t = (ctypes.c_void_p * P)(*ptrs)
+        keep.append(t)
+        return ctypes.addressof(t)
+
+    ncell = np.array([m.n_cells for m in meshes], np.int32)
+    nface = np.array([len(m.owner) for m in meshes], np.int32)
+    owners, nbrs, ws, peers, counts, ifc, npat = [], [], [], [], [], [], []
+    for m in meshes:
+        pp = [p for p in m.patches if p.kind == PROCESSOR and p.n_faces > 0]
+        owners.append(arr(m.owner, np.int32))
+        nbrs.append(arr(m.neighbour, np.int32))
+        ws.append(arr(m.magSf, np.float64))
+        peers.append(arr([p.neighbour_rank for p in pp], np.int32))
+        counts.append(arr([p.n_faces for p in pp], np.int32))
+        ifc.append(arr(np.concatenate([p.face_cells for p in pp]) if pp else [], np.int32))
+        npat.append(len(pp))
+    npat = np.array(npat, np.int32)
+    nl = ctypes.c_int(0)
+    cells, ifs = np.zeros(64 * P, np.int32), np.zeros(64 * P, np.int32)
+    _check(lib().spuma_host_gamg_hierarchy_dd(P, ncell.ctypes.data, nface.ctypes.data, tab(owners), tab(nbrs), tab(ws),
+                                              npat.ctypes.data, tab(peers), tab(counts), tab(ifc), n_coarsest,
+                                              max_levels, ctypes.addressof(nl), cells.ctypes.data, ifs.ctypes.data))
+    n = nl.value
+    return {"levels": n, "level_cells": [cells[64 * r:64 * r + n].tolist() for r in range(P)],
+            "level_ifaces": [ifs[64 * r:64 * r + n].tolist() for r in range(P)]}
 
 
 def host_level_schedule(n_cells: int, owner, neighbour):

@@ -65,3 +65,27 @@ def test_host_functions_reject_bad_addressing():
         S.host_rcm(3, np.array([1], np.int32), np.array([0], np.int32))  # owner > neighbour
     with pytest.raises(S.SpumaError):
         S.host_ldu_to_csr(2, np.array([0, 0], np.int32), np.array([1, 1], np.int32)[::-1].copy() * 5)
+
+
+def _dd_case(P, how, n=9):
+    from test_oracle_decomposed import _decomposed_case
+    m = gen.permute(gen.perturbed(n, 0.2), seed=4)
+    part = gen.rcb_parts(m, P) if how == "rcb" else gen.block_parts(m, (P, 1, 1))
+    return _decomposed_case(m, part, gen.gamma_lognormal(m), gen.rhs(m), ref=0)
+
+
+@pytest.mark.parametrize("params", [dict(), dict(n_coarsest=3), dict(max_levels=3)])
+@pytest.mark.parametrize("P,how", [(2, "block"), (3, "rcb"), (4, "rcb"), (8, "rcb")])
+def test_host_gamg_hierarchy_dd_matches_oracle(P, how, params):
+    """The decomposed hierarchy (Q36 global stop rule, Q37 coarse interfaces by first
+    occurrence) of libspuma's host code -- run with one thread per rank for the collectives --
+    has bitwise the decomposed oracle's per-rank level sizes and interface-face counts."""
+    subs, systems = _dd_case(P, how)
+    nc, ml = params.get("n_coarsest", 10), params.get("max_levels", 50)
+    hh = S.host_gamg_hierarchy_dd(subs, nc, ml)
+    _, po = O.gamg_decomposed(subs, systems, None, O.controls(0.0, 0.0, 0, 0),
+                              O.gamg_params(n_coarsest_cells=nc, max_levels=ml))
+    assert hh["levels"] == po["levels"]
+    assert hh["level_cells"] == po["level_cells"]
+    assert hh["level_ifaces"] == po["level_ifaces"]
+    assert hh["levels"] >= (3 if ml > 3 else ml)
