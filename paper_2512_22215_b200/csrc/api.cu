@@ -2099,6 +2099,7 @@ spuma_status spuma_peer_import(spuma_mesh m, const void* blobs, int n_blobs)
     SPUMA_NVTX("spuma_peer_import");
     if (!m || !blobs) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "NULL argument");
     if (!m->d_mail) return set_error(SPUMA_ERR_STATE, "spuma_peer_export first");
+    if (m->peer) return set_error(SPUMA_ERR_STATE, "peer transport already imported on this handle");
     if (n_blobs != m->n_ranks) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "one blob per rank (rank order)");
     const int P = m->n_ranks;
     std::vector<PeerBlob> B(P);
