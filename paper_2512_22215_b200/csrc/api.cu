@@ -380,9 +380,19 @@ spuma_status exchange_counts(spuma_mesh m, const std::vector<int>& counts, const
     return SPUMA_OK;
 }
 
+// timing event of a captured batch, recorded on a LEAF branch (timing stream): the event node
+// depends on the work captured on s so far, nothing on s depends on it, so the programmatic
+// (PDL) edges between the timed kernels are the untimed ones (an event node in line would
+// serialise the next kernel's launch behind it).  "Before kernel k" = "after kernel k - 1".
 void record(spuma_mesh m, std::vector<cudaEvent_t>& ev, int idx, cudaStream_t s)
 {
-    cudaEventRecordWithFlags(ev[idx], s, cudaEventRecordExternal);
+    if (!m->tstream) {  // outside a timed capture (not expected): in line
+        cudaEventRecordWithFlags(ev[idx], s, cudaEventRecordExternal);
+        return;
+    }
+    cudaEventRecord(m->tfork, s);
+    cudaStreamWaitEvent(m->tstream, m->tfork, 0);
+    cudaEventRecordWithFlags(ev[idx], m->tstream, cudaEventRecordExternal);
 }
 
 // one PCG iteration (A11, A7h, A7-A8, A9-A10) on stream s.  P > 1 with processor faces
@@ -501,12 +511,20 @@ spuma_status build_graphs(spuma_mesh m)
         }
         cudaGraph_t graph = nullptr;
         SPUMA_TRY(l2_window(m));
+        if (m->timing && !m->tstream) {
+            SPUMA_CUDA(cudaStreamCreateWithFlags(&m->tstream, cudaStreamNonBlocking));
+            SPUMA_CUDA(cudaEventCreateWithFlags(&m->tfork, cudaEventDisableTiming));
+        }
         SPUMA_CUDA(cudaStreamBeginCapture(m->stream, cudaStreamCaptureModeThreadLocal));
         spuma_status st = SPUMA_OK;
-        // timing samples the first iteration of every batch (6 event nodes per batch keep the
-        // capture's launch gaps unperturbed; ~100 samples per 1600-iteration solve)
+        // timing samples the first iteration of every batch (6 event nodes per batch on a leaf
+        // branch; ~100 samples per 1600-iteration solve)
         for (int k = 0; k < batch_eff(m) && st == SPUMA_OK; ++k)
             st = enqueue_iteration(m, m->stream, k == 0 ? ev : nullptr, k);
+        if (m->timing) {  // the timing branch rejoins the origin stream at the end of the batch
+            cudaEventRecord(m->tfork, m->tstream);
+            cudaStreamWaitEvent(m->stream, m->tfork, 0);
+        }
         cudaError_t e = cudaStreamEndCapture(m->stream, &graph);
         if (st != SPUMA_OK) {
             if (graph) cudaGraphDestroy(graph);
@@ -1239,6 +1257,8 @@ void spuma_free(spuma_mesh m)
     if (m->comm) ncclCommDestroy(m->comm);
     if (m->comm_stream) cudaStreamDestroy(m->comm_stream);
     if (m->ev_fork) cudaEventDestroy(m->ev_fork);
+    if (m->tfork) cudaEventDestroy(m->tfork);
+    if (m->tstream) cudaStreamDestroy(m->tstream);
     if (m->ev_join) cudaEventDestroy(m->ev_join);
     if (m->own_stream && m->stream) cudaStreamDestroy(m->stream);
     delete m;

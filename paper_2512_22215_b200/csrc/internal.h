@@ -201,6 +201,8 @@ struct spuma_mesh_s {
     int* d_ifRows = nullptr;          // cells with processor faces, ascending
     int n_ifRows = 0;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;  // halo / interior overlap
+    cudaStream_t tstream = nullptr;   // leaf branch of the timing event nodes (captured batches)
+    cudaEvent_t tfork = nullptr;
     double* d_sendbuf = nullptr;     // [n_iface] packed x for the neighbours
     // staging (renumbering / host pointers), allocated on first use
     double *d_cell_a = nullptr, *d_cell_b = nullptr, *d_cell_c = nullptr, *d_cell_d = nullptr,
