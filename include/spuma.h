@@ -468,7 +468,11 @@ typedef enum {
     SPUMA_OPT_ELL_STENCIL = 7,
     /* PCG hot loop: an L2 access-policy window (persisting) over the direction vector pA,
      * captured into the iteration graphs; 0 = none (default), 1 = on */
-    SPUMA_OPT_L2_PERSIST = 8
+    SPUMA_OPT_L2_PERSIST = 8,
+    /* GAMG: the coarse levels without uniform widths run their rows over a per-level CSR copy of
+     * the off-diagonal coefficients (row_ax order; bitwise the same rows); 1 = on (default),
+     * 0 = the losort-addressed rows.  Rebuilds the hierarchy at the next solve. */
+    SPUMA_OPT_GAMG_CSR = 9
 } spuma_option;
 spuma_status spuma_set_option(spuma_mesh m, int option, int value);
 

@@ -747,6 +747,32 @@ spuma_status gamg_ensure(spuma_mesh m, const spuma_gamg_params& gp)
                 L.a.ell_wn = sh.uniform_wn;
                 L.a.ell_wo = sh.uniform_wo;
                 L.ell = 1;
+            } else if (h.F > 0 && m->gamg_csr) {
+                // generic rows as CSR runs (row_ax order: neighbour side in losort order, then owner
+                // side); k_gamg_agg writes both entries of every coarse face
+                std::vector<int> rp(n + 1, 0), col(2 * (size_t)h.F), pu(h.F), pl(h.F);
+                int k = 0;
+                for (int c = 0; c < n; ++c) {
+                    for (int q = h.losortStart[c]; q < h.losortStart[c + 1]; ++q) {
+                        col[k] = h.ownerLo[q];
+                        pl[h.losort[q]] = k++;
+                    }
+                    for (int f = h.ownerStart[c]; f < h.ownerStart[c + 1]; ++f) {
+                        col[k] = h.neighbour[f];
+                        pu[f] = k++;
+                    }
+                    rp[c + 1] = k;
+                }
+                int *crp, *ccol, *cpu, *cpl;
+                SPUMA_TRY(gupload(G, &crp, rp, s));
+                SPUMA_TRY(gupload(G, &ccol, col, s));
+                SPUMA_TRY(gupload(G, &cpu, pu, s));
+                SPUMA_TRY(gupload(G, &cpl, pl, s));
+                SPUMA_TRY(galloc(G, &L.cval, 2 * (size_t)h.F));
+                L.crp = crp;
+                L.ccol = ccol;
+                L.cposU = cpu;
+                L.cposL = cpl;
             } else if (h.F > 0) {  // generic rows: a losort-ordered coefficient copy (one dependent load less)
                 std::vector<int> pos(h.F);
                 for (int k = 0; k < h.F; ++k) pos[h.losort[k]] = k;
@@ -2029,6 +2055,11 @@ spuma_status spuma_set_option(spuma_mesh m, int option, int value)
         if (value < 0 || value > 1) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "l2_persist is 0 or 1");
         if (m->l2_persist != (value != 0)) destroy_graphs(m);
         m->l2_persist = value != 0;
+        return SPUMA_OK;
+    case SPUMA_OPT_GAMG_CSR:
+        if (value < 0 || value > 1) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "gamg_csr is 0 or 1");
+        if (m->gamg_csr != (value != 0)) gamg_release(m);  // the hierarchy is rebuilt at the next solve
+        m->gamg_csr = value != 0;
         return SPUMA_OK;
     case SPUMA_OPT_ALT_SWEEP:
         if (value < 0 || value > 1) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "alt_sweep is 0 or 1");

@@ -67,6 +67,18 @@ __device__ __forceinline__ double row_ax_ell(const MeshArgs& a, int c, const dou
     return s;
 }
 
+// The same row over a per-level CSR copy of the off-diagonal coefficients (coarse generic levels):
+// row c's neighbour-side faces in losort order, then its owner-side faces in face order -- the
+// order of row_ax -- as one contiguous (column, value) run; values written by k_gamg_agg.
+template <class X>
+__device__ __forceinline__ double row_ax_csr(const GLevel& L, int c, const double* __restrict__ diag, const X& x)
+{
+    double s = diag[c] * x(c);
+    const int k1 = L.crp[c + 1];
+    for (int k = L.crp[c]; k < k1; ++k) s = s + L.cval[k] * x(L.ccol[k]);
+    return s;
+}
+
 // + the processor-interface terms of row c in (patch, face) order (Q10), reading the halo xr
 // of the same implicit vector (packed by the neighbours before this kernel)
 template <bool IF>
@@ -82,12 +94,13 @@ __device__ __forceinline__ double add_if(const GLevel& L, const double* __restri
     return s;
 }
 
-template <bool ELL, bool IF = false, class X>
+template <int LAY, bool IF = false, class X>
 __device__ __forceinline__ double rowA(const GLevel& L, int c, const double* __restrict__ d,
                                        const double* __restrict__ u, const double* __restrict__ ic, const X& x)
 {
     double s;
-    if constexpr (ELL) s = row_ax_ell(L.a, c, d, x);
+    if constexpr (LAY == 1) s = row_ax_ell(L.a, c, d, x);
+    else if constexpr (LAY == 2) s = row_ax_csr(L, c, d, x);
     else s = row_ax(L.a, c, d, u, x, L.upperLo);
     return add_if<IF>(L, ic, c, s);
 }
@@ -161,6 +174,10 @@ __global__ void __launch_bounds__(kThreads) k_gamg_agg(GLevel F, GLevel C, const
         for (int k = F.cfStart[e]; k < F.cfStart[e + 1]; ++k) u = u + fu[F.cfList[k]];
         C.upper[e] = u;
         if (C.upperLo) C.upperLo[C.losortPos[e]] = u;  // losort-ordered copy (generic rows)
+        if (C.cval) {                                  // CSR rows: both entries of the face
+            C.cval[C.cposU[e]] = u;
+            C.cval[C.cposL[e]] = u;
+        }
         if (C.ell) {  // owner-slot copy for the ELL rows of the coarse level
             const int c = C.a.owner[e];
             const_cast<double*>(C.a.upper_s)[(size_t)32 * C.a.ell_wo * (c >> 5) + 32 * (e - C.a.ownerStart[c]) + (c & 31)] = u;
@@ -184,7 +201,7 @@ __global__ void __launch_bounds__(kThreads) k_gamg_restrict(GLevel F, GLevel C, 
             const int i = F.cList[k];
             double r = F.b[i];
             if (x) {
-                r = r - add_if<IF>(F, level_iface(F, P), i, row_ax(F.a, i, fd, fu, XPlain{x}, F.upperLo));
+                r = r - add_if<IF>(F, level_iface(F, P), i, (F.cval ? row_ax_csr(F, i, fd, XPlain{x}) : row_ax(F.a, i, fd, fu, XPlain{x}, F.upperLo)));
                 F.r[i] = r;
             }
             s = s + r;
@@ -196,7 +213,7 @@ __global__ void __launch_bounds__(kThreads) k_gamg_restrict(GLevel F, GLevel C, 
 
 // Richardson sweep (Q24): xout = x + omega (rD (b - A x)), x = xin or (xin + alpha xc[ftc])
 // when xc is given (the prolonged correction of the first post-sweep); psi_acc: psi += xout.
-template <bool ELL, bool IF>
+template <int ELL, bool IF>
 __global__ void __launch_bounds__(kThreads) k_gamg_smooth(GLevel L, const DevPtrs* __restrict__ P,
                                                           const double* __restrict__ xin, double* __restrict__ xout,
                                                           double omega, const double* __restrict__ xc,
@@ -234,7 +251,7 @@ __global__ void __launch_bounds__(kThreads) k_gamg_smooth(GLevel L, const DevPtr
 //   x1 = x' + omega rD (r - alpha Ac) = alpha p + q,
 //   p = c - omega rD Ac,  q = x + omega rD r       (x = pre-smoothed correction or 0)
 // and k_gamg_post needs two direct loads per neighbour instead of a gather of its own.
-template <bool ELL, bool IF>
+template <int ELL, bool IF>
 __global__ void __launch_bounds__(kThreads) k_gamg_scale(GLevel L, const DevPtrs* __restrict__ P,
                                                          const double* __restrict__ x, const double* __restrict__ xc,
                                                          const double* __restrict__ r, double omega, int pq,
@@ -300,7 +317,7 @@ struct XPQ {  // x1(j) = alpha p_j + q_j
 
 // Post-sweeps 1 (+2) after k_gamg_scale: x1 = alpha p + q; two: x2 = x1 + omega rD (b - A x1)
 // in one gather with x1 formed at the neighbours.  psi_acc: psi += result.
-template <bool ELL, bool IF>
+template <int ELL, bool IF>
 __global__ void __launch_bounds__(kThreads) k_gamg_post(GLevel L, const DevPtrs* __restrict__ P,
                                                         const double* __restrict__ alpha, double omega,
                                                         double* __restrict__ out, int two, int psi_acc)
@@ -323,7 +340,7 @@ __global__ void __launch_bounds__(kThreads) k_gamg_post(GLevel L, const DevPtrs*
 
 // Two-stage Gauss-Seidel (Q30), stage 1: r = b - A x' with x' = xin (+ alpha xc[ftc] when xc
 // is given: the prolonged correction folded into the first post-sweep; xin nullptr: zero).
-template <bool ELL, bool IF>
+template <int ELL, bool IF>
 __global__ void __launch_bounds__(kThreads) k_gamg_gs2_res(GLevel L, const DevPtrs* __restrict__ P,
                                                            const double* __restrict__ xin,
                                                            const double* __restrict__ xc,
@@ -384,7 +401,7 @@ __global__ void __launch_bounds__(kThreads) k_gamg_gs2_upd(GLevel L, const DevPt
 }
 
 // end of a GAMG iteration (Q28): rA = source - A psi, final residual, n++, convergence, done
-template <bool ELL, bool IF>
+template <int ELL, bool IF>
 __global__ void __launch_bounds__(kThreads) k_gamg_residual(GLevel L, Workspace w, double* rank_part)
 {
     pdl_wait();  // predecessor complete and visible (PDL launch)
@@ -486,7 +503,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_gamg_tail(const GLevel* __res
         double v[2] = {0.0, 0.0};
         for (int c = tid; c < L.a.N; c += kSmallThreads) {  // scale + p/q (Q25, Q29)
             const double ci = X(c);
-            const double aci = L.ell ? row_ax_ell(L.a, c, d, X) : row_ax(L.a, c, d, u, X, L.upperLo);
+            const double aci = L.ell ? row_ax_ell(L.a, c, d, X) : (L.cval ? row_ax_csr(L, c, d, X) : row_ax(L.a, c, d, u, X, L.upperLo));
             const double ri = L.b[c];
             const double rd = 1.0 / d[c];
             L.p[c] = ci - omega * (rd * aci);
@@ -505,7 +522,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_gamg_tail(const GLevel* __res
             const double x1 = Y(c);
             double xn = x1;
             if (n_post >= 2)
-                xn = x1 + omega * ((1.0 / d[c]) * (L.b[c] - (L.ell ? row_ax_ell(L.a, c, d, Y) : row_ax(L.a, c, d, u, Y, L.upperLo))));
+                xn = x1 + omega * ((1.0 / d[c]) * (L.b[c] - (L.ell ? row_ax_ell(L.a, c, d, Y) : (L.cval ? row_ax_csr(L, c, d, Y) : row_ax(L.a, c, d, u, Y, L.upperLo)))));
             L.x[c] = xn;
         }
         __syncthreads();
@@ -514,7 +531,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_gamg_tail(const GLevel* __res
         for (int i = 2; i < n_post; ++i) {  // further plain sweeps
             for (int c = tid; c < L.a.N; c += kSmallThreads) {
                 const XPlain Z{xin};
-                const double y = L.ell ? row_ax_ell(L.a, c, d, Z) : row_ax(L.a, c, d, u, Z, L.upperLo);
+                const double y = L.ell ? row_ax_ell(L.a, c, d, Z) : (L.cval ? row_ax_csr(L, c, d, Z) : row_ax(L.a, c, d, u, Z, L.upperLo));
                 xout[c] = xin[c] + omega * ((1.0 / d[c]) * (L.b[c] - y));
             }
             __syncthreads();
@@ -558,7 +575,7 @@ int gamg_grid(int n)
         int dev = 0, sms = 148, occ = 4;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gamg_smooth<false, false>, kThreads, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gamg_smooth<0, false>, kThreads, 0);
         g_gamg_max_grid = sms * (occ > 0 ? occ : 1);
     }
     const int g = (n + kThreads - 1) / kThreads;
@@ -574,12 +591,16 @@ void launch_gamg_agg(cudaStream_t s, const GLevel& fine, const GLevel& coarse, c
 #define GAMG_DISPATCH(K, L, ...)                                                  \
     do {                                                                          \
         const bool if_ = (L).a.ifStart != nullptr;                                \
-        if ((L).ell) {                                                            \
-            if (if_) glaunch(K<true, true>, (L).grid, s, __VA_ARGS__);            \
-            else glaunch(K<true, false>, (L).grid, s, __VA_ARGS__);               \
+        const int lay_ = (L).ell ? 1 : ((L).cval ? 2 : 0);                        \
+        if (lay_ == 1) {                                                          \
+            if (if_) glaunch(K<1, true>, (L).grid, s, __VA_ARGS__);               \
+            else glaunch(K<1, false>, (L).grid, s, __VA_ARGS__);                  \
+        } else if (lay_ == 2) {                                                   \
+            if (if_) glaunch(K<2, true>, (L).grid, s, __VA_ARGS__);               \
+            else glaunch(K<2, false>, (L).grid, s, __VA_ARGS__);                  \
         } else {                                                                  \
-            if (if_) glaunch(K<false, true>, (L).grid, s, __VA_ARGS__);           \
-            else glaunch(K<false, false>, (L).grid, s, __VA_ARGS__);              \
+            if (if_) glaunch(K<0, true>, (L).grid, s, __VA_ARGS__);               \
+            else glaunch(K<0, false>, (L).grid, s, __VA_ARGS__);                  \
         }                                                                         \
     } while (0)
 

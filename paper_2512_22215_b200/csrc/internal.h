@@ -93,6 +93,9 @@ struct GLevel {
     int ell;                      // 1: rows over the ELL layout (a.sell_*, a.upper_s; level 0 of a uniform mesh)
     double* upperLo;              // coarse generic levels: coefficients in losort order (nullptr: gather)
     const int* losortPos;         //   face -> its losort position (k_gamg_agg writes upperLo through it)
+    const int *crp, *ccol;        // coarse generic levels: CSR rows of the off-diagonal entries (row_ax order)
+    double* cval;                 //   their values (k_gamg_agg), nullptr: no CSR copy
+    const int *cposU, *cposL;     //   face -> its positions in the owner / neighbour row
     // processor interfaces (n_ranks > 1, readings Q36-Q38): a.ifStart / a.ifIdx per cell
     const double* iface;          // [n_if] coefficients (nullptr on level 0: DevPtrs::iface)
     double* xr;                   // [n_if] the neighbours' values of the vector a row kernel gathers
@@ -222,6 +225,7 @@ struct spuma_mesh_s {
     bool defer_psi = true;  // psi += alpha pA applied every second iteration (same rounding, fewer bytes)  // ELL + coefficient copy (falls back to 6 -> 5 when the mesh is not uniform)
     bool timing = false;
     int fuse_direction = 0;      // 0: k_direction + k_amul_dot (default: faster); 1: fused, rD read; 2: fused, 1/diag inline
+    bool gamg_csr = true;        // GAMG coarse generic levels as CSR runs (SPUMA_OPT_GAMG_CSR)
     bool l2_persist = false;     // L2 access-policy window over pA (SPUMA_OPT_L2_PERSIST)
     bool alt_sweep = true;       // alternate the sweep direction of consecutive hot-loop kernels (L2 reuse)
     int gamg_tail_cells = 1024;  // GAMG: levels from the first one at or below this size run in one CTA (0: off)
