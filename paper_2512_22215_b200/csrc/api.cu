@@ -711,6 +711,31 @@ spuma_status gamg_ensure(spuma_mesh m, const spuma_gamg_params& gp)
             L.b = m->ws.rA;
             L.ell = (m->d_upper_s && m->d_sell_n && m->sell_wn >= 0 && m->sell_wn <= 3 && m->sell_wo >= 0 &&
                      m->sell_wo <= 3) ? 1 : 0;
+            if (!L.ell && m->gamg_csr && m->F > 0) {  // irregular fine mesh: CSR rows, values per solve
+                std::vector<int> rp(n + 1, 0), col(2 * (size_t)m->F), pu(m->F), pl(m->F);
+                int k = 0;
+                for (int c = 0; c < n; ++c) {
+                    for (int q = m->h_losortStart[c]; q < m->h_losortStart[c + 1]; ++q) {
+                        col[k] = m->h_owner[m->h_losort[q]];
+                        pl[m->h_losort[q]] = k++;
+                    }
+                    for (int f = m->h_ownerStart[c]; f < m->h_ownerStart[c + 1]; ++f) {
+                        col[k] = m->h_neighbour[f];
+                        pu[f] = k++;
+                    }
+                    rp[c + 1] = k;
+                }
+                int *crp, *ccol, *cpu, *cpl;
+                SPUMA_TRY(gupload(G, &crp, rp, s));
+                SPUMA_TRY(gupload(G, &ccol, col, s));
+                SPUMA_TRY(gupload(G, &cpu, pu, s));
+                SPUMA_TRY(gupload(G, &cpl, pl, s));
+                SPUMA_TRY(galloc(G, &L.cval, 2 * (size_t)m->F));
+                L.crp = crp;
+                L.ccol = ccol;
+                L.cposU = cpu;
+                L.cposL = cpl;
+            }
         } else {
             L.a = MeshArgs{};
             L.a.N = n;
@@ -2311,6 +2336,10 @@ spuma_status spuma_gamg_solve(spuma_mesh m, const spuma_scalar* diag, const spum
                           Lc.b ? Lc.b : m->ws.rA, Lc.x};
     SPUMA_CUDA(cudaMemcpyAsync(G->cws.ptrs, G->h_cptrs, sizeof(DevPtrs), cudaMemcpyHostToDevice, s));
     // per-solve: Galerkin coarse matrices (Q27), outer scalars, coarsest PCG controls, A6 setup
+    if (G->lv[0].cval) {  // level 0 over CSR runs: this call's coefficients into them
+        launch_gamg_csr_values(s, G->lv[0], P.upper, m->F);
+        m->stats.kernel_launches += 1;
+    }
     for (int l = 0; l + 1 < nl; ++l) launch_gamg_agg(s, G->lv[l], G->lv[l + 1], m->ws.ptrs);
     if (G->lv[0].ell) {  // level 0 rows over ELL: this call's coefficients in owner-slot order
         launch_ell_coeffs(s, G->lv[0].a, P.upper, m->d_upper_s);

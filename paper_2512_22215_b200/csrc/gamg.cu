@@ -582,6 +582,22 @@ int gamg_grid(int n)
     return g < 1 ? 1 : (g > g_gamg_max_grid ? g_gamg_max_grid : g);
 }
 
+namespace {
+__global__ void __launch_bounds__(kThreads) k_gamg_csr_values(GLevel L, const double* __restrict__ upper, int F)
+{
+    for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < F; f += gridDim.x * blockDim.x) {
+        const double u = upper[f];
+        L.cval[L.cposU[f]] = u;
+        L.cval[L.cposL[f]] = u;
+    }
+}
+}  // namespace
+
+void launch_gamg_csr_values(cudaStream_t s, const GLevel& L, const double* upper, int F)
+{
+    k_gamg_csr_values<<<gamg_grid(F), kThreads, 0, s>>>(L, upper, F);
+}
+
 void launch_gamg_agg(cudaStream_t s, const GLevel& fine, const GLevel& coarse, const DevPtrs* P)
 {
     k_gamg_agg<<<gamg_grid(fine.nc > fine.ncf ? fine.nc : fine.ncf), kThreads, 0, s>>>(fine, coarse, P);

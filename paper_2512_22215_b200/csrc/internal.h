@@ -387,6 +387,7 @@ void launch_amul_asym(cudaStream_t s, const MeshArgs& a, const double* diag, con
 // GAMG (gamg.cu).  P = the handle's DevPtrs (level 0's matrix, source, psi).
 int gamg_grid(int n);
 void launch_gamg_agg(cudaStream_t s, const GLevel& fine, const GLevel& coarse, const DevPtrs* P);
+void launch_gamg_csr_values(cudaStream_t s, const GLevel& L, const double* upper, int F);  // level-0 CSR values
 void launch_gamg_restrict(cudaStream_t s, const GLevel& fine, const GLevel& coarse, const DevPtrs* P,
                           const double* x, double* zero_x = nullptr);  // x nullptr: the level's x is zero
 void launch_gamg_smooth(cudaStream_t s, const GLevel& L, const DevPtrs* P, const double* xin, double* xout,

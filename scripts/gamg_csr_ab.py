@@ -13,9 +13,10 @@ import gen  # noqa: E402
 import paper_2512_22215_b200 as P  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 200
-m = gen.cube(n)
+perm = len(sys.argv) > 2 and sys.argv[2] == "perm"  # perturbed + permuted, RCM-renumbered (irregular level 0)
+m = gen.permute(gen.perturbed(n, 0.15), seed=2) if perm else gen.cube(n)
 f64 = dict(dtype=torch.float64, device="cuda")
-h = P.Mesh.from_mesh(m, stream=torch.cuda.current_stream().cuda_stream)
+h = P.Mesh.from_mesh(m, renumber=perm, stream=torch.cuda.current_stream().cuda_stream)
 diag, upper = torch.empty(m.n_cells, **f64), torch.empty(m.n_faces, **f64)
 src = torch.as_tensor(gen.rhs(m), **f64)
 h.assemble_laplacian(None, None, 0, 0.0, diag, upper, src, None)
@@ -37,6 +38,6 @@ for rnd in range(2):
             t = e0.elapsed_time(e1)
             best = t if best is None else min(best, t)
         out[csr] = psi.clone()
-        print(json.dumps({"n": n, "round": rnd, "gamg_csr": csr, "cycles": perf["n_iterations"],
+        print(json.dumps({"n": n, "mesh": "perturbed+permuted, RCM" if perm else "cube", "round": rnd, "gamg_csr": csr, "cycles": perf["n_iterations"],
                           "ms": best, "ms_per_cycle": best / perf["n_iterations"]}), flush=True)
 print(json.dumps({"bitwise_same": bool(torch.equal(out[0], out[1]))}))
