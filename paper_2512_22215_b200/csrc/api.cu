@@ -1115,6 +1115,7 @@ struct PcState {
     double *wT = nullptr, *rT = nullptr, *pT = nullptr, *part = nullptr;
     double *u_in = nullptr, *l_in = nullptr, *u_int = nullptr, *l_int = nullptr;
     int* csr_map = nullptr;  // device copy of the CSR map
+    double *fco = nullptr, *bco = nullptr, *fcoT = nullptr, *bcoT = nullptr;  // aDILU pass coefficients (per solve)
     double *iface_t = nullptr, *xrT = nullptr;  // PBiCG: Tmul interface coefficients (staging), pT halo
     int nnz = 0;
 };
@@ -1126,7 +1127,8 @@ void pc_release(spuma_mesh m)
     PcState* P = m->pc;
     if (!P) return;
     void* ptrs[] = {P->order_f, P->order_b, P->flag, P->counter, P->raw, P->rD, P->t1, P->t2, P->wT, P->rT,
-                    P->pT, P->part, P->u_in, P->l_in, P->u_int, P->l_int, P->csr_map, P->iface_t, P->xrT};
+                    P->pT, P->part, P->u_in, P->l_in, P->u_int, P->l_int, P->csr_map, P->iface_t, P->xrT,
+                    P->fco, P->bco, P->fcoT, P->bcoT};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     delete P;
@@ -1150,6 +1152,7 @@ spuma_status pc_ensure(spuma_mesh m)
     SPUMA_TRY(dalloc(&P->flag, N + 1));
     SPUMA_TRY(dalloc(&P->counter, 1));
     for (double** b : {&P->raw, &P->rD, &P->t1, &P->t2, &P->wT, &P->rT, &P->pT}) SPUMA_TRY(dalloc(b, N));
+    for (double** b : {&P->fco, &P->bco, &P->fcoT, &P->bcoT}) SPUMA_TRY(dalloc(b, m->F));
     SPUMA_TRY(dalloc(&P->part, (size_t)kMaxPartials * pc_grid(N)));
     SPUMA_CUDA(cudaStreamSynchronize(s));
     return SPUMA_OK;
@@ -1214,6 +1217,8 @@ void pc_setup(spuma_mesh m, const spuma_preconditioner& pc, const double* d, con
     }
     launch_ilu_factor(m->stream, a, P->order_f, d, u, pc.kind == SPUMA_PC_DIC ? u : l, P->raw, P->rD, P->flag,
                       P->counter, P->width_f);
+    if (pc.kind == SPUMA_PC_ADILU && P->fco)
+        launch_adilu_coefs(m->stream, a, P->rD, u, l, P->fco, P->bco, P->fcoT, P->bcoT);
 }
 
 void pc_apply(spuma_mesh m, const spuma_preconditioner& pc, const double* u, const double* l, const double* r,
@@ -1221,9 +1226,11 @@ void pc_apply(spuma_mesh m, const spuma_preconditioner& pc, const double* u, con
 {
     PcState* P = m->pc;
     const int k = pc.kind == SPUMA_PC_DIAGONAL ? 0 : (pc.kind == SPUMA_PC_ADILU ? pc.n_sweeps : -1);
+    const bool pre = pc.kind == SPUMA_PC_ADILU && P->fco;
     launch_ilu_precondition(m->stream, mesh_args(m), P->order_f, P->order_b, P->rD, u,
                             pc.kind == SPUMA_PC_DIC ? u : l, r, w, P->t1, P->t2, P->flag, P->counter, k, transpose,
-                            scal, P->width_f, P->width_b);
+                            scal, P->width_f, P->width_b, pre ? (transpose ? P->fcoT : P->fco) : nullptr,
+                            pre ? (transpose ? P->bcoT : P->bco) : nullptr);
 }
 
 // the sweeps' deadlock guard (flag[N], precond.cu): read and clear after a solve

@@ -361,7 +361,11 @@ void launch_ilu_factor(cudaStream_t s, const MeshArgs& a, const int* order, cons
 void launch_ilu_precondition(cudaStream_t s, const MeshArgs& a, const int* order_f, const int* order_b,
                              const double* rD, const double* upper, const double* lower, const double* r, double* w,
                              double* t1, double* t2, int* flag, unsigned* counter, int k, bool transpose,
-                             const DevScal* scal, int width_f = 1 << 30, int width_b = 1 << 30);
+                             const DevScal* scal, int width_f = 1 << 30, int width_b = 1 << 30,
+                             const double* fpre = nullptr, const double* bpre = nullptr);
+// aDILU pass coefficients rD*lower / rD*upper in pass order, for M^-1 (fco, bco) and M^-T (fcoT, bcoT)
+void launch_adilu_coefs(cudaStream_t s, const MeshArgs& a, const double* rD, const double* upper,
+                        const double* lower, double* fco, double* bco, double* fcoT, double* bcoT);
 void launch_pc_dot(cudaStream_t s, int N, const double* w, const double* r, double* part, DevScal* scal,
                    bool fin = true);
 void launch_pc_direction(cudaStream_t s, int N, const double* wA, double* pA, const double* wT, double* pT,

@@ -224,6 +224,50 @@ __global__ void __launch_bounds__(kThreads) k_adilu_pass(MeshArgs a, int backwar
     }
 }
 
+// aDILU with the pass coefficients rD[c]*coef[f] formed once per solve in the pass's row order
+// (forward: losort order, contiguous per row -- no face indirection; backward: face order):
+// fco/bco for M^-1, fcoT/bcoT for M^-T (lower/upper swapped).  (rD*coef)*prev is the pass's own
+// rounding, so the passes below are bitwise k_adilu_pass.
+__global__ void __launch_bounds__(kThreads) k_adilu_coefs(MeshArgs a, const double* __restrict__ rD,
+                                                          const double* __restrict__ up,
+                                                          const double* __restrict__ lo, double* __restrict__ fco,
+                                                          double* __restrict__ bco, double* __restrict__ fcoT,
+                                                          double* __restrict__ bcoT)
+{
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < a.N; c += gridDim.x * blockDim.x) {
+        const double rd = rD[c];
+        for (int k = a.losortStart[c]; k < a.losortStart[c + 1]; ++k) {
+            const int f = a.losort[k];
+            fco[k] = rd * lo[f];
+            fcoT[k] = rd * up[f];
+        }
+        for (int f = a.ownerStart[c]; f < a.ownerStart[c + 1]; ++f) {
+            bco[f] = rd * up[f];
+            bcoT[f] = rd * lo[f];
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) k_adilu_pass_pre(MeshArgs a, int backward, const double* __restrict__ pre,
+                                                             const double* __restrict__ rD,
+                                                             const double* __restrict__ r,
+                                                             const double* __restrict__ y0,
+                                                             const double* __restrict__ prev,
+                                                             double* __restrict__ out, const DevScal* scal)
+{
+    if (scal && scal->done) return;
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < a.N; c += gridDim.x * blockDim.x) {
+        double t = y0 ? y0[c] : rD[c] * r[c];
+        if (!backward) {
+            const int k1 = a.losortStart[c + 1];
+            for (int k = a.losortStart[c]; k < k1; ++k) t = t - pre[k] * prev[a.ownerLo[k]];
+        } else {
+            for (int f = a.ownerStart[c + 1] - 1; f >= a.ownerStart[c]; --f) t = t - pre[f] * prev[a.neighbour[f]];
+        }
+        out[c] = t;
+    }
+}
+
 // w = rD r (diagonal preconditioner; also aDILU with k = 0)
 __global__ void k_pc_diag(int N, const double* __restrict__ rD, const double* __restrict__ r, double* __restrict__ w,
                           const DevScal* scal)
@@ -453,7 +497,7 @@ void launch_ilu_factor(cudaStream_t s, const MeshArgs& a, const int* order, cons
 void launch_ilu_precondition(cudaStream_t s, const MeshArgs& a, const int* order_f, const int* order_b,
                              const double* rD, const double* upper, const double* lower, const double* r, double* w,
                              double* t1, double* t2, int* flag, unsigned* counter, int k, bool transpose,
-                             const DevScal* scal, int width_f, int width_b)
+                             const DevScal* scal, int width_f, int width_b, const double* fpre, const double* bpre)
 {
     const double* lo = transpose ? upper : lower;
     const double* up = transpose ? lower : upper;
@@ -477,7 +521,8 @@ void launch_ilu_precondition(cudaStream_t s, const MeshArgs& a, const int* order
     double* prev = t1;
     for (int it = 0; it < k; ++it) {
         double* out = prev == t1 ? t2 : t1;
-        k_adilu_pass<<<cell_grid(a.N), kThreads, 0, s>>>(a, 0, rD, lo, r, nullptr, prev, out, scal);
+        if (fpre) k_adilu_pass_pre<<<cell_grid(a.N), kThreads, 0, s>>>(a, 0, fpre, rD, r, nullptr, prev, out, scal);
+        else k_adilu_pass<<<cell_grid(a.N), kThreads, 0, s>>>(a, 0, rD, lo, r, nullptr, prev, out, scal);
         prev = out;
     }
     // backward passes from w_0 = y (kept in Y): out_i alternates Z / w so that out_k = w
@@ -486,9 +531,17 @@ void launch_ilu_precondition(cudaStream_t s, const MeshArgs& a, const int* order
     const double* bprev = Y;
     for (int it = 0; it < k; ++it) {
         double* out = ((k - 1 - it) & 1) ? Z : w;
-        k_adilu_pass<<<cell_grid(a.N), kThreads, 0, s>>>(a, 1, rD, up, r, Y, bprev, out, scal);
+        if (bpre) k_adilu_pass_pre<<<cell_grid(a.N), kThreads, 0, s>>>(a, 1, bpre, rD, r, Y, bprev, out, scal);
+        else k_adilu_pass<<<cell_grid(a.N), kThreads, 0, s>>>(a, 1, rD, up, r, Y, bprev, out, scal);
         bprev = out;
     }
+}
+
+void launch_adilu_coefs(cudaStream_t s, const MeshArgs& a, const double* rD, const double* upper,
+                        const double* lower, double* fco, double* bco, double* fcoT, double* bcoT)
+{
+    if (a.N <= 0) return;
+    k_adilu_coefs<<<cell_grid(a.N), kThreads, 0, s>>>(a, rD, upper, lower, fco, bco, fcoT, bcoT);
 }
 
 void launch_recip(cudaStream_t s, int N, const double* in, double* out)
