@@ -381,11 +381,26 @@ __global__ void __launch_bounds__(kThreads) k_gamg_gs2_upd(GLevel L, const DevPt
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < L.a.N; c += gridDim.x * blockDim.x) {
         double t = r[c];
         if (!skip_lower) {
-            const int k1 = L.a.losortStart[c + 1];
-            for (int k = L.a.losortStart[c]; k < k1; ++k) {
-                const int j = L.a.ownerLo[k];
-                const double zj = zin ? zin[j] : (1.0 / d[j]) * r[j];
-                t = t - u[L.a.losort[k]] * zj;
+            const int k0 = L.a.losortStart[c], k1 = L.a.losortStart[c + 1];
+            if (L.cval) {  // the lower part = the first k1 - k0 entries of the row's CSR run
+                const int q0 = L.crp[c];
+                for (int k = 0; k < k1 - k0; ++k) {
+                    const int j = L.ccol[q0 + k];
+                    const double zj = zin ? zin[j] : (1.0 / d[j]) * r[j];
+                    t = t - L.cval[q0 + k] * zj;
+                }
+            } else if (L.upperLo) {
+                for (int k = k0; k < k1; ++k) {
+                    const int j = L.a.ownerLo[k];
+                    const double zj = zin ? zin[j] : (1.0 / d[j]) * r[j];
+                    t = t - L.upperLo[k] * zj;
+                }
+            } else {
+                for (int k = k0; k < k1; ++k) {
+                    const int j = L.a.ownerLo[k];
+                    const double zj = zin ? zin[j] : (1.0 / d[j]) * r[j];
+                    t = t - u[L.a.losort[k]] * zj;
+                }
             }
         }
         const double z = (1.0 / d[c]) * t;
