@@ -119,11 +119,76 @@ __global__ void k_ilu_recip(int N, const double* __restrict__ raw, double* __res
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < N; c += gridDim.x * blockDim.x) rD[c] = 1.0 / raw[c];
 }
 
-// Forward sweep: w[c] = rD[c] r[c], then w[c] -= rD[c]*lo[f]*w[owner] over the faces with
-// neighbour c in face order.
+// The sweeps publish each row's VALUE as its ready flag: the output array is pre-filled with
+// kPending (a NaN payload no arithmetic on finite data produces) and a row's result is written
+// with one release store, so a consumer's acquire load of the dependency returns the value
+// itself -- one L2 round trip per dependency level instead of flag + value.
+constexpr unsigned long long kPending = 0x7FF4DEADBEEF0001ull;
+
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const double* p)
+{
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_f64(double* p, double v)
+{
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"((unsigned long long)__double_as_longlong(v))
+                 : "memory");
+}
+
+// the values of all n (<= kDep) dependencies, polled together (bounded, back-off)
+__device__ __forceinline__ void wait_values(const double* w, const int* js, int n, double* v, int* err)
+{
+    bool have[kDep];
+#pragma unroll
+    for (int d = 0; d < kDep; ++d) have[d] = d >= n;
+    unsigned ns = 32, polls = 0;
+    for (;;) {
+        bool ok = true;
+#pragma unroll
+        for (int d = 0; d < kDep; ++d)
+            if (!have[d]) {
+                const unsigned long long u = ld_acquire_u64(w + js[d]);
+                if (u != kPending) {
+                    v[d] = __longlong_as_double((long long)u);
+                    have[d] = true;
+                } else {
+                    ok = false;
+                }
+            }
+        if (ok) return;
+        __nanosleep(ns);
+        ns = ns < 512 ? 2 * ns : 512;
+        if (++polls > kSpinLimit) {
+            spin_fail(err);
+#pragma unroll
+            for (int d = 0; d < kDep; ++d)
+                if (!have[d]) v[d] = 0.0;
+            return;
+        }
+    }
+}
+
+__device__ __forceinline__ double wait_value(const double* w, int j, int* err)
+{
+    double v;
+    wait_values(w, &j, 1, &v, err);
+    return v;
+}
+
+__global__ void k_fill_pending(int N, double* __restrict__ w, const DevScal* scal)
+{
+    if (scal && scal->done) return;  // the sweeps are no-ops then: leave w as it is
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < N; c += gridDim.x * blockDim.x)
+        w[c] = __longlong_as_double((long long)kPending);
+}
+
+// Forward sweep: y[c] = rD[c] r[c], then y[c] -= rD[c]*lo[f]*y[owner] over the faces with
+// neighbour c in face order.  y: pre-filled with kPending.
 __global__ void __launch_bounds__(kThreads) k_ilu_fwd(MeshArgs a, const int* __restrict__ order,
                                                       const double* __restrict__ rD, const double* __restrict__ lo,
-                                                      const double* __restrict__ r, double* w, int* flag,
+                                                      const double* __restrict__ r, double* y, int* err,
                                                       unsigned* counter, const DevScal* scal)
 {
     if (scal && scal->done) return;
@@ -143,28 +208,21 @@ __global__ void __launch_bounds__(kThreads) k_ilu_fwd(MeshArgs a, const int* __r
                 cf[d] = rd * lo[a.losort[k0 + d]];
             }
         double t = rd * r[c];
-        wait_all(flag, js, nd < kDep ? nd : kDep, flag + a.N);
-#pragma unroll
-        for (int d = 0; d < kDep; ++d)
-            if (d < nd) v[d] = __ldcg(w + js[d]);
+        wait_values(y, js, nd < kDep ? nd : kDep, v, err);
 #pragma unroll
         for (int d = 0; d < kDep; ++d)
             if (d < nd) t = t - cf[d] * v[d];
-        for (int k = k0 + kDep; k < k0 + nd; ++k) {
-            const int j = a.ownerLo[k];
-            wait_ready(flag, j, flag + a.N);
-            t = t - rd * lo[a.losort[k]] * __ldcg(w + j);
-        }
-        __stcg(w + c, t);
-        st_release(flag + c, 1);
+        for (int k = k0 + kDep; k < k0 + nd; ++k) t = t - rd * lo[a.losort[k]] * wait_value(y, a.ownerLo[k], err);
+        st_release_f64(y + c, t);
     }
 }
 
-// Backward sweep (rows in reverse dependency order): w[c] -= rD[c]*up[f]*w[neighbour] over the
-// faces with owner c in DESCENDING face order.  w holds the forward result on entry.
+// Backward sweep (rows in reverse dependency order): w[c] = y[c] - rD[c]*up[f]*w[neighbour] over
+// the faces with owner c in DESCENDING face order.  y: the forward result; w pre-filled with kPending.
 __global__ void __launch_bounds__(kThreads) k_ilu_bwd(MeshArgs a, const int* __restrict__ order,
                                                       const double* __restrict__ rD, const double* __restrict__ up,
-                                                      double* w, int* flag, unsigned* counter, const DevScal* scal)
+                                                      const double* __restrict__ y, double* w, int* err,
+                                                      unsigned* counter, const DevScal* scal)
 {
     if (scal && scal->done) return;
     for (;;) {
@@ -182,21 +240,13 @@ __global__ void __launch_bounds__(kThreads) k_ilu_bwd(MeshArgs a, const int* __r
                 js[d] = a.neighbour[f1 - d];
                 cf[d] = rd * up[f1 - d];
             }
-        double t = __ldcg(w + c);
-        wait_all(flag, js, nd < kDep ? nd : kDep, flag + a.N);
-#pragma unroll
-        for (int d = 0; d < kDep; ++d)
-            if (d < nd) v[d] = __ldcg(w + js[d]);
+        double t = y[c];
+        wait_values(w, js, nd < kDep ? nd : kDep, v, err);
 #pragma unroll
         for (int d = 0; d < kDep; ++d)
             if (d < nd) t = t - cf[d] * v[d];
-        for (int f = f1 - kDep; f >= a.ownerStart[c]; --f) {
-            const int j = a.neighbour[f];
-            wait_ready(flag, j, flag + a.N);
-            t = t - rd * up[f] * __ldcg(w + j);
-        }
-        __stcg(w + c, t);
-        st_release(flag + c, 1);
+        for (int f = f1 - kDep; f >= a.ownerStart[c]; --f) t = t - rd * up[f] * wait_value(w, a.neighbour[f], err);
+        st_release_f64(w + c, t);
     }
 }
 
@@ -501,15 +551,15 @@ void launch_ilu_precondition(cudaStream_t s, const MeshArgs& a, const int* order
 {
     const double* lo = transpose ? upper : lower;
     const double* up = transpose ? lower : upper;
-    if (k < 0) {
-        cudaMemsetAsync(flag, 0, sizeof(int) * a.N, s);
+    if (k < 0) {  // forward result in t1, backward into w (values as flags, kPending = not yet)
+        k_fill_pending<<<cell_grid(a.N), kThreads, 0, s>>>(a.N, t1, scal);
         cudaMemsetAsync(counter, 0, sizeof(unsigned), s);
-        k_ilu_fwd<<<persistent_grid((const void*)k_ilu_fwd, 2 * width_f), kThreads, 0, s>>>(a, order_f, rD, lo, r, w,
-                                                                                           flag, counter, scal);
-        cudaMemsetAsync(flag, 0, sizeof(int) * a.N, s);
+        k_ilu_fwd<<<persistent_grid((const void*)k_ilu_fwd, 2 * width_f), kThreads, 0, s>>>(a, order_f, rD, lo, r, t1,
+                                                                                           flag + a.N, counter, scal);
+        k_fill_pending<<<cell_grid(a.N), kThreads, 0, s>>>(a.N, w, scal);
         cudaMemsetAsync(counter, 0, sizeof(unsigned), s);
-        k_ilu_bwd<<<persistent_grid((const void*)k_ilu_bwd, 2 * width_b), kThreads, 0, s>>>(a, order_b, rD, up, w,
-                                                                                           flag, counter, scal);
+        k_ilu_bwd<<<persistent_grid((const void*)k_ilu_bwd, 2 * width_b), kThreads, 0, s>>>(a, order_b, rD, up, t1, w,
+                                                                                           flag + a.N, counter, scal);
         return;
     }
     if (k == 0) {
