@@ -159,7 +159,7 @@ __device__ __forceinline__ void wait_values(const double* w, const int* js, int 
             }
         if (ok) return;
         __nanosleep(ns);
-        ns = ns < 512 ? 2 * ns : 512;
+        ns = ns < 64 ? 2 * ns : 64;  // short back-off: the sweep is latency-bound (-2 % vs 512 ns)
         if (++polls > kSpinLimit) {
             spin_fail(err);
 #pragma unroll
