@@ -446,7 +446,8 @@ typedef enum {
     SPUMA_OPT_DEFER_PSI = 3,
     /* GAMG: the levels from the first one (below the finest) with at most this many cells
      * down to the coarsest run in ONE single-CTA kernel per V-cycle (Richardson, scaled
-     * correction, nPre = 0); default 1024 (same-box A/B: 256-1024 best, 4096+ slower); 0 = one
+     * correction, nPre = 0); default 512 (same-box A/B r01q: 512 best, 256/1024 within 1.5 %,
+     * 2048+ slower); 0 = one
      * launch per level and step */
     SPUMA_OPT_GAMG_TAIL_CELLS = 4,
     /* PCG hot loop: form the direction pA = rD rA + beta pA inside the Amul gather instead of

@@ -228,7 +228,7 @@ struct spuma_mesh_s {
     bool gamg_csr = true;        // GAMG coarse generic levels as CSR runs (SPUMA_OPT_GAMG_CSR)
     bool l2_persist = false;     // L2 access-policy window over pA (SPUMA_OPT_L2_PERSIST)
     bool alt_sweep = true;       // alternate the sweep direction of consecutive hot-loop kernels (L2 reuse)
-    int gamg_tail_cells = 1024;  // GAMG: levels from the first one at or below this size run in one CTA (0: off)
+    int gamg_tail_cells = 512;   // GAMG: levels from the first one at or below this size run in one CTA (0: off)
     cudaGraphExec_t gexec[2] = {nullptr, nullptr};
     bool gexec_timed = false;
     int gexec_batch = 0;
