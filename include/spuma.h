@@ -115,7 +115,9 @@ typedef struct {
     const spuma_patch_desc* patches; /* [n_patches], boundary coefficients applied in this order    */
     int renumber;                    /* 0: keep caller numbering; 1: reverse Cuthill-McKee inside   */
     int pointers_on_device;          /* 0: arrays above are host memory; 1: device memory           */
-    void* cuda_stream;               /* cudaStream_t to order work on; NULL: handle makes its own   */
+    void* cuda_stream;               /* cudaStream_t to order work on; NULL: handle makes its own
+                                        BLOCKING stream (ordered with the legacy default stream, so
+                                        e.g. torch fills on the default stream precede each call)   */
     int rank, n_ranks;               /* n_ranks == 1: no communication                              */
     const void* nccl_unique_id;      /* 128-byte ncclUniqueId from rank 0 (n_ranks > 1)             */
 } spuma_mesh_desc;
@@ -473,7 +475,11 @@ typedef enum {
     /* GAMG: the coarse levels without uniform widths run their rows over a per-level CSR copy of
      * the off-diagonal coefficients (row_ax order; bitwise the same rows); 1 = on (default),
      * 0 = the losort-addressed rows.  Rebuilds the hierarchy at the next solve. */
-    SPUMA_OPT_GAMG_CSR = 9
+    SPUMA_OPT_GAMG_CSR = 9,
+    /* peer transport: how long a kernel polls for a neighbour's flag before it gives up, in
+     * milliseconds (approximate: SM clocks at 2 GHz); default 20000.  The call that saw the
+     * timeout returns SPUMA_ERR_STATE. */
+    SPUMA_OPT_PEER_POLL_MS = 10
 } spuma_option;
 spuma_status spuma_set_option(spuma_mesh m, int option, int value);
 

@@ -98,6 +98,27 @@ MeshArgs mesh_args(const spuma_mesh m)
     return a;
 }
 
+static bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+// the loop runs while (n < max_iter && !converged) || n < min_iter (reading Q3): min_iter may
+// exceed max_iter, so the host-side termination guards are bounded by the larger of the two
+static int iter_bound(const spuma_solver_controls* c) { return std::max(c->max_iter, c->min_iter); }
+
+// Peer transport (peer.cu): a poll that exceeds its limit sets the handle's error word and the
+// kernels then skip the stale exchange -- every collective call reads (and clears) that word
+// after its work, so such a call returns SPUMA_ERR_STATE instead of SPUMA_OK with wrong results.
+spuma_status peer_guard(spuma_mesh m)
+{
+    if (!m->peer || !m->pst.err) return SPUMA_OK;
+    int e = 0;
+    SPUMA_CUDA(cudaMemcpyAsync(&e, m->pst.err, sizeof e, cudaMemcpyDeviceToHost, m->stream));
+    SPUMA_CUDA(cudaStreamSynchronize(m->stream));
+    if (!e) return SPUMA_OK;
+    SPUMA_CUDA(cudaMemsetAsync(m->pst.err, 0, sizeof(int), m->stream));
+    SPUMA_CUDA(cudaStreamSynchronize(m->stream));
+    return set_error(SPUMA_ERR_STATE, "peer transport: a neighbour did not answer within the poll limit");
+}
+
 enum CellRole { R_GAMMA = 0, R_DIAG, R_SOURCE, R_PSI, R_X, R_Y, R_COUNT };
 
 double** cell_buf(spuma_mesh m, int role)
@@ -107,17 +128,19 @@ double** cell_buf(spuma_mesh m, int role)
 }
 
 // caller cell array -> device array in internal numbering
+// (the vector kernels access cell arrays as double2: a caller device array that is only 8-byte
+// aligned -- e.g. a torch slice at an odd offset -- is staged through the handle's buffer)
 spuma_status cells_in(spuma_mesh m, const double* p, int role, const double** out)
 {
     const bool dev = is_device_ptr(p);
-    if (!m->renumber && dev) {
+    if (!m->renumber && dev && aligned16(p)) {
         *out = p;
         return SPUMA_OK;
     }
     double** buf = cell_buf(m, role);
     if (!*buf) SPUMA_TRY(dalloc(buf, m->N));
     if (!m->renumber) {
-        SPUMA_CUDA(cudaMemcpyAsync(*buf, p, sizeof(double) * m->N, cudaMemcpyHostToDevice, m->stream));
+        SPUMA_CUDA(cudaMemcpyAsync(*buf, p, sizeof(double) * m->N, cudaMemcpyDefault, m->stream));
     } else {
         const double* src = p;
         if (!dev) {
@@ -477,10 +500,15 @@ void destroy_graphs(spuma_mesh m)
 
 // SPUMA_OPT_L2_PERSIST: an L2 access-policy window over the direction vector pA (the one vector
 // the Amul gathers and three kernels touch), captured into the kernel nodes; 0 = no window
-spuma_status l2_window(spuma_mesh m)
+// The window is set on the stream only for the duration of the capture (the kernel nodes keep
+// it); the stream's previous policy -- it may be the caller's stream -- is restored afterwards.
+spuma_status l2_window(spuma_mesh m, cudaStreamAttrValue* saved)
 {
     cudaStreamAttrValue v{};
-    if (m->l2_persist && m->N > 0) {
+    if (!m->l2_persist || m->N == 0) return SPUMA_OK;
+    SPUMA_CUDA(cudaStreamGetAttribute(m->stream, cudaStreamAttributeAccessPolicyWindow, saved));
+    m->l2_limit_set = true;
+    {
         int dev = 0, maxp = 0, maxw = 0;
         SPUMA_CUDA(cudaGetDevice(&dev));
         SPUMA_CUDA(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev));
@@ -497,6 +525,16 @@ spuma_status l2_window(spuma_mesh m)
     return SPUMA_OK;
 }
 
+// undo SPUMA_OPT_L2_PERSIST's device-wide state: the persisting-L2 limit and the lines
+// already marked persisting
+void l2_reset(spuma_mesh m)
+{
+    if (!m->l2_limit_set) return;
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
+    cudaCtxResetPersistingL2Cache();
+    m->l2_limit_set = false;
+}
+
 spuma_status build_graphs(spuma_mesh m)
 {
     if (m->gexec[0] && m->gexec_timed == m->timing && m->gexec_batch == batch_eff(m)) return SPUMA_OK;
@@ -510,7 +548,8 @@ spuma_status build_graphs(spuma_mesh m)
             ev = &m->tev[g];
         }
         cudaGraph_t graph = nullptr;
-        SPUMA_TRY(l2_window(m));
+        cudaStreamAttrValue saved{};
+        SPUMA_TRY(l2_window(m, &saved));
         if (m->timing && !m->tstream) {
             SPUMA_CUDA(cudaStreamCreateWithFlags(&m->tstream, cudaStreamNonBlocking));
             SPUMA_CUDA(cudaEventCreateWithFlags(&m->tfork, cudaEventDisableTiming));
@@ -526,6 +565,7 @@ spuma_status build_graphs(spuma_mesh m)
             cudaStreamWaitEvent(m->stream, m->tfork, 0);
         }
         cudaError_t e = cudaStreamEndCapture(m->stream, &graph);
+        if (m->l2_persist && m->N > 0) cudaStreamSetAttribute(m->stream, cudaStreamAttributeAccessPolicyWindow, &saved);
         if (st != SPUMA_OK) {
             if (graph) cudaGraphDestroy(graph);
             return st;
@@ -1287,6 +1327,7 @@ void spuma_free(spuma_mesh m)
     destroy_graphs(m);
     gamg_release(m);
     pc_release(m);
+    l2_reset(m);
     for (int i = 0; i < 2; ++i) {
         if (m->batch_done[i]) cudaEventDestroy(m->batch_done[i]);
         if (m->asm_ev[i]) cudaEventDestroy(m->asm_ev[i]);
@@ -1331,7 +1372,9 @@ static spuma_status mesh_create_impl(const spuma_mesh_desc* d, spuma_mesh m)
     if (d->cuda_stream) {
         m->stream = static_cast<cudaStream_t>(d->cuda_stream);
     } else {
-        SPUMA_CUDA(cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking));
+        // blocking (cudaStreamDefault): a caller that filled psi / zeroed y on the legacy default
+        // stream (torch's default) is ordered before the handle's work without an explicit sync
+        SPUMA_CUDA(cudaStreamCreateWithFlags(&m->stream, cudaStreamDefault));
         m->own_stream = true;
     }
     m->N = N;
@@ -1669,7 +1712,7 @@ spuma_status spuma_assemble_laplacian(spuma_mesh m, const spuma_scalar* gamma, c
     SPUMA_TRY(cells_in(m, source, R_SOURCE, &src_in));
     double* src_i = const_cast<double*>(src_in);
     double* diag_i = diag;
-    if (m->renumber || !is_device_ptr(diag)) {
+    if (m->renumber || !is_device_ptr(diag) || !aligned16(diag)) {
         if (!m->d_cell_b) SPUMA_TRY(dalloc(&m->d_cell_b, m->N));
         diag_i = m->d_cell_b;
     }
@@ -1708,7 +1751,7 @@ spuma_status spuma_assemble_laplacian(spuma_mesh m, const spuma_scalar* gamma, c
         m->stats.phase_ms[3] += ms;
         m->stats.phase_count[3] += 1;
     }
-    return SPUMA_OK;
+    return peer_guard(m);
 }
 
 spuma_status spuma_amul(spuma_mesh m, const spuma_scalar* diag, const spuma_scalar* upper,
@@ -1726,7 +1769,7 @@ spuma_status spuma_amul(spuma_mesh m, const spuma_scalar* diag, const spuma_scal
     SPUMA_TRY(cells_in(m, x, R_X, &x_i));
     if (m->n_iface) SPUMA_TRY(iface_in(m, iface_coeffs, &if_i));
     double* y_i = y;
-    if (m->renumber || !is_device_ptr(y)) {
+    if (m->renumber || !is_device_ptr(y) || !aligned16(y)) {
         if (!m->d_cell_t) SPUMA_TRY(dalloc(&m->d_cell_t, m->N));
         y_i = m->d_cell_t;
     }
@@ -1741,7 +1784,7 @@ spuma_status spuma_amul(spuma_mesh m, const spuma_scalar* diag, const spuma_scal
     SPUMA_TRY(cells_out(m, y, y_i));
     SPUMA_CUDA(cudaStreamSynchronize(s));
     SPUMA_CUDA(cudaGetLastError());
-    return SPUMA_OK;
+    return peer_guard(m);
 }
 
 spuma_status spuma_pcg_solve(spuma_mesh m, const spuma_scalar* diag, const spuma_scalar* upper,
@@ -1812,7 +1855,7 @@ spuma_status spuma_pcg_solve(spuma_mesh m, const spuma_scalar* diag, const spuma
             SPUMA_TRY(enqueue_iteration(m, s, nullptr, it));
             SPUMA_CUDA(cudaMemcpyAsync(&m->h_scal[0], m->ws.scal, sizeof(DevScal), cudaMemcpyDeviceToHost, s));
             SPUMA_CUDA(cudaStreamSynchronize(s));
-            if (++it > ctl->max_iter + 1) return set_error(SPUMA_ERR_STATE, "PCG loop did not terminate");
+            if (++it > iter_bound(ctl) + 1) return set_error(SPUMA_ERR_STATE, "PCG loop did not terminate");
         }
     } else {
     // ---- A7-A11 in captured batches, ping-pong; host reads the scalars once per batch
@@ -1840,8 +1883,10 @@ spuma_status spuma_pcg_solve(spuma_mesh m, const spuma_scalar* diag, const spuma
             SPUMA_TRY(nccl_async_check(m));
         }
         ++b;
-        if (b > 2 + (ctl->max_iter + m->gexec_batch - 1) / m->gexec_batch + 1)
+        if (b > 2 + (iter_bound(ctl) + m->gexec_batch - 1) / m->gexec_batch + 1) {
+            cudaStreamSynchronize(s);
             return set_error(SPUMA_ERR_STATE, "PCG batch loop did not terminate");
+        }
     }
     SPUMA_CUDA(cudaStreamSynchronize(s));
     if (m->timing && b > 0) SPUMA_TRY(account_timing(m, (b - 1) & 1, m->h_scal[(b - 1) & 1].n - prev_n));
@@ -1864,7 +1909,7 @@ spuma_status spuma_pcg_solve(spuma_mesh m, const spuma_scalar* diag, const spuma
     m->stats.iterations += fs.n;
     SPUMA_TRY(cells_out(m, psi, P.psi));
     SPUMA_CUDA(cudaStreamSynchronize(s));
-    return SPUMA_OK;
+    return peer_guard(m);
 }
 
 spuma_status spuma_surface_integrate(spuma_mesh m, const spuma_scalar* phi, const spuma_scalar* const* patch_phi,
@@ -1880,7 +1925,7 @@ spuma_status spuma_surface_integrate(spuma_mesh m, const spuma_scalar* phi, cons
     const double* V_i = nullptr;
     SPUMA_TRY(cells_in(m, V, R_X, &V_i));
     double* out_i = out;
-    if (m->renumber || !is_device_ptr(out)) {
+    if (m->renumber || !is_device_ptr(out) || !aligned16(out)) {
         if (!m->d_cell_t) SPUMA_TRY(dalloc(&m->d_cell_t, m->N));
         out_i = m->d_cell_t;
     }
@@ -1889,7 +1934,7 @@ spuma_status spuma_surface_integrate(spuma_mesh m, const spuma_scalar* phi, cons
     SPUMA_TRY(cells_out(m, out, out_i));
     SPUMA_CUDA(cudaStreamSynchronize(s));
     SPUMA_CUDA(cudaGetLastError());
-    return SPUMA_OK;
+    return peer_guard(m);
 }
 
 spuma_status spuma_face_flux(spuma_mesh m, const spuma_scalar* gamma, const spuma_scalar* const* patch_value,
@@ -1941,7 +1986,7 @@ spuma_status spuma_face_flux(spuma_mesh m, const spuma_scalar* gamma, const spum
     if (patch_phi) SPUMA_TRY(patches_out(m, patch_phi, m->d_bphi));
     SPUMA_CUDA(cudaStreamSynchronize(s));
     SPUMA_CUDA(cudaGetLastError());
-    return SPUMA_OK;
+    return peer_guard(m);
 }
 
 spuma_status spuma_laplacian_correction(spuma_mesh m, const spuma_scalar* gamma,
@@ -1964,10 +2009,10 @@ spuma_status spuma_laplacian_correction(spuma_mesh m, const spuma_scalar* gamma,
     double* src_i = const_cast<double*>(src_in);
     // V: its own staging buffer (the other cell roles are in use)
     const double* V_i = V;
-    if (m->renumber || !is_device_ptr(V)) {
+    if (m->renumber || !is_device_ptr(V) || !aligned16(V)) {
         if (!m->d_cell_v) SPUMA_TRY(dalloc(&m->d_cell_v, m->N));
         if (!m->renumber) {
-            SPUMA_CUDA(cudaMemcpyAsync(m->d_cell_v, V, sizeof(double) * m->N, cudaMemcpyHostToDevice, s));
+            SPUMA_CUDA(cudaMemcpyAsync(m->d_cell_v, V, sizeof(double) * m->N, cudaMemcpyDefault, s));
         } else {
             const double* src = V;
             if (!is_device_ptr(V)) {
@@ -2008,7 +2053,7 @@ spuma_status spuma_laplacian_correction(spuma_mesh m, const spuma_scalar* gamma,
     SPUMA_TRY(patches_out(m, patch_corr_flux, m->d_bcflux));
     SPUMA_CUDA(cudaStreamSynchronize(s));
     SPUMA_CUDA(cudaGetLastError());
-    return SPUMA_OK;
+    return peer_guard(m);
 }
 
 spuma_status spuma_mesh_get_addressing(spuma_mesh m, spuma_label* perm, spuma_label* owner, spuma_label* neighbour,
@@ -2087,11 +2132,18 @@ spuma_status spuma_set_option(spuma_mesh m, int option, int value)
         if (value < 0 || value > 1) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "l2_persist is 0 or 1");
         if (m->l2_persist != (value != 0)) destroy_graphs(m);
         m->l2_persist = value != 0;
+        if (!m->l2_persist) l2_reset(m);
         return SPUMA_OK;
     case SPUMA_OPT_GAMG_CSR:
         if (value < 0 || value > 1) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "gamg_csr is 0 or 1");
         if (m->gamg_csr != (value != 0)) gamg_release(m);  // the hierarchy is rebuilt at the next solve
         m->gamg_csr = value != 0;
+        return SPUMA_OK;
+    case SPUMA_OPT_PEER_POLL_MS:
+        if (value < 1) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "peer_poll_ms must be >= 1");
+        m->pst.poll_cycles = (long long)value * 2'000'000LL;
+        destroy_graphs(m);  // the captured kernels (PCG batches, GAMG cycles) hold the old limit
+        gamg_release(m);
         return SPUMA_OK;
     case SPUMA_OPT_ALT_SWEEP:
         if (value < 0 || value > 1) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "alt_sweep is 0 or 1");
@@ -2398,7 +2450,7 @@ spuma_status spuma_gamg_solve(spuma_mesh m, const spuma_scalar* diag, const spum
         }
         SPUMA_CUDA(cudaMemcpyAsync(&m->h_scal[0], m->ws.scal, sizeof(DevScal), cudaMemcpyDeviceToHost, s));
         SPUMA_CUDA(cudaStreamSynchronize(s));
-        if (++cycles > ctl->max_iter + 1) return set_error(SPUMA_ERR_STATE, "GAMG loop did not terminate");
+        if (++cycles > iter_bound(ctl) + 1) return set_error(SPUMA_ERR_STATE, "GAMG loop did not terminate");
     }
     SPUMA_CUDA(cudaGetLastError());
     m->stats.kernel_launches += (uint64_t)cycles * (uint64_t)G->launches_per_cycle;
@@ -2412,7 +2464,7 @@ spuma_status spuma_gamg_solve(spuma_mesh m, const spuma_scalar* diag, const spum
     m->stats.iterations += fs.n;
     SPUMA_TRY(cells_out(m, psi, P.psi));
     SPUMA_CUDA(cudaStreamSynchronize(s));
-    return SPUMA_OK;
+    return peer_guard(m);
 }
 
 spuma_status spuma_gamg_get_hierarchy(spuma_mesh m, const spuma_gamg_params* params, int max_levels,
@@ -2505,7 +2557,7 @@ spuma_status spuma_pcg_solve_pc(spuma_mesh m, const spuma_scalar* diag, const sp
         SPUMA_CUDA(cudaMemcpyAsync(&m->h_scal[0], w.scal, sizeof(DevScal), cudaMemcpyDeviceToHost, s));
         SPUMA_CUDA(cudaStreamSynchronize(s));
         it += per_check;
-        if (it > ctl->max_iter + 16) return set_error(SPUMA_ERR_STATE, "PCG loop did not terminate");
+        if (it > iter_bound(ctl) + 16) return set_error(SPUMA_ERR_STATE, "PCG loop did not terminate");
     }
     SPUMA_CUDA(cudaGetLastError());
     SPUMA_TRY(pc_guard(m));
@@ -2519,7 +2571,7 @@ spuma_status spuma_pcg_solve_pc(spuma_mesh m, const spuma_scalar* diag, const sp
     m->stats.iterations += fs.n;
     SPUMA_TRY(cells_out(m, psi, Pp.psi));
     SPUMA_CUDA(cudaStreamSynchronize(s));
-    return SPUMA_OK;
+    return peer_guard(m);
 }
 
 spuma_status spuma_pbicg_solve(spuma_mesh m, const spuma_scalar* diag, const spuma_scalar* upper,
@@ -2597,7 +2649,7 @@ spuma_status spuma_pbicg_solve(spuma_mesh m, const spuma_scalar* diag, const spu
         SPUMA_CUDA(cudaMemcpyAsync(&m->h_scal[0], w.scal, sizeof(DevScal), cudaMemcpyDeviceToHost, s));
         SPUMA_CUDA(cudaStreamSynchronize(s));
         it += per_check;
-        if (it > ctl->max_iter + 16) return set_error(SPUMA_ERR_STATE, "PBiCG loop did not terminate");
+        if (it > iter_bound(ctl) + 16) return set_error(SPUMA_ERR_STATE, "PBiCG loop did not terminate");
     }
     SPUMA_CUDA(cudaGetLastError());
     SPUMA_TRY(pc_guard(m));
@@ -2611,7 +2663,7 @@ spuma_status spuma_pbicg_solve(spuma_mesh m, const spuma_scalar* diag, const spu
     m->stats.iterations += fs.n;
     SPUMA_TRY(cells_out(m, psi, psi_i));
     SPUMA_CUDA(cudaStreamSynchronize(s));
-    return SPUMA_OK;
+    return peer_guard(m);
 }
 
 spuma_status spuma_precondition(spuma_mesh m, const spuma_scalar* diag, const spuma_scalar* upper,

@@ -128,6 +128,7 @@ struct PeerState {
     unsigned long long* ctr;  // [2] exchange / all-gather epochs (device)
     unsigned* ticket;
     int* err;                 // set on a poll timeout
+    long long poll_cycles = 40'000'000'000LL;  // poll limit, SM clocks (~20 s at 2 GHz; SPUMA_OPT_PEER_POLL_MS)
 };
 
 struct Patch {
@@ -227,6 +228,7 @@ struct spuma_mesh_s {
     int fuse_direction = 0;      // 0: k_direction + k_amul_dot (default: faster); 1: fused, rD read; 2: fused, 1/diag inline
     bool gamg_csr = true;        // GAMG coarse generic levels as CSR runs (SPUMA_OPT_GAMG_CSR)
     bool l2_persist = false;     // L2 access-policy window over pA (SPUMA_OPT_L2_PERSIST)
+    bool l2_limit_set = false;   // the persisting-L2 limit was raised (reset on option off / free)
     bool alt_sweep = true;       // alternate the sweep direction of consecutive hot-loop kernels (L2 reuse)
     int gamg_tail_cells = 512;   // GAMG: levels from the first one at or below this size run in one CTA (0: off)
     cudaGraphExec_t gexec[2] = {nullptr, nullptr};

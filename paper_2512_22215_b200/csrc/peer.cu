@@ -16,8 +16,9 @@
 // Epochs: each rank counts its exchanges on the device (all ranks run the same sequence), so
 // the kernels are graph-capturable.  Two mailbox halves (epoch parity) make reuse safe: a rank
 // can only be one exchange ahead of a neighbour that has not yet consumed (it needs that
-// neighbour's next message first).  A poll that exceeds ~20 s sets the handle's error word
-// (the host turns it into SPUMA_ERR_STATE) instead of hanging the GPU.
+// neighbour's next message first).  A poll that exceeds its limit (~20 s by default,
+// SPUMA_OPT_PEER_POLL_MS) sets the handle's error word instead of hanging the GPU; every
+// collective call reads and clears it afterwards (api.cu peer_guard -> SPUMA_ERR_STATE).
 #include "internal.h"
 
 namespace spuma {
@@ -35,16 +36,14 @@ __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned l
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-constexpr long long kPollCycles = 40'000'000'000LL;  // ~20 s at 2 GHz
-
 // wait until *f >= e (thread-local poll); false on timeout (error word set)
-__device__ bool wait_flag(const unsigned long long* f, unsigned long long e, int* err)
+__device__ bool wait_flag(const unsigned long long* f, unsigned long long e, int* err, long long limit)
 {
     const long long t0 = clock64();
     unsigned ns = 32;
     while (ld_acquire_sys(f) < e) {
         if (*reinterpret_cast<volatile int*>(err)) return false;  // an earlier exchange already failed
-        if (clock64() - t0 > kPollCycles) {
+        if (clock64() - t0 > limit) {
             atomicExch(err, 1);
             return false;
         }
@@ -90,7 +89,7 @@ __global__ void __launch_bounds__(kThreads) k_peer_recv(PeerXfer d, double* __re
     if (threadIdx.x == 0) {
         ok = 1;
         for (int p = 0; p < d.n_patches && ok; ++p)
-            if (!wait_flag(d.src_flag[p][par], e, st.err)) ok = 0;
+            if (!wait_flag(d.src_flag[p][par], e, st.err, st.poll_cycles)) ok = 0;
     }
     __syncthreads();
     if (!ok) return;
@@ -123,7 +122,7 @@ __global__ void k_peer_allgather4(PeerGather g, const double* __restrict__ in, d
         st_release_sys(g.flag[t][par] + g.rank, e);
     }
     __syncthreads();
-    if (t < g.n_ranks && !wait_flag(g.my_flag[par] + t, e, st.err)) ok = 0;
+    if (t < g.n_ranks && !wait_flag(g.my_flag[par] + t, e, st.err, st.poll_cycles)) ok = 0;
     __syncthreads();
     if (ok && t < g.n_ranks)
 #pragma unroll
