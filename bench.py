@@ -60,10 +60,18 @@ def peaks():
     return 6650.0, "fallback"
 
 
-def algorithmic_bytes(N, F):
+def algorithmic_bytes(N, F, lattice_k=0):
     """SURVEY §8(d): per PCG iteration, fused minimum. Phase A (Amul + dot): 24 B/cell + 16 B/face;
-    B (update + dots): 56 B/cell; C (direction): 32 B/cell."""
-    return {"A": 24 * N + 16 * F, "B": 56 * N, "C": 32 * N, "iter": 112 * N + 16 * F}
+    B (update + dots): 56 B/cell; C (direction): 32 B/cell.
+
+    On a lattice numbering the Amul runs over K <= 3 coefficient slots per row and no index
+    arrays (variant 12): phase A is then 24 B/cell (diag, pA, wA) + 8 K B/cell
+    (the owner-side slots; the neighbour-side slots and the pA gathers are L2 hits, counted
+    once) -- the bytes that layout must move."""
+    a = 24 * N + 8 * lattice_k * N if lattice_k else 24 * N + 16 * F
+    return {"A": a, "B": 56 * N, "C": 32 * N, "iter": a + 88 * N, "A_survey": 24 * N + 16 * F,
+            "iter_survey": 112 * N + 16 * F, "A_layout": "lattice slots (K = %d)" % lattice_k if lattice_k
+            else "ELL rows (indices + coefficients per face)"}
 
 
 class ClockSampler:
@@ -120,14 +128,16 @@ class ClockSampler:
                 "samples": len(mhz)}
 
 
-def load_traffic(workload):
+def load_traffic(workload, variant):
+    """ncu DRAM bytes per launch of the dominant kernel (profiles/ncu_traffic.json), if that capture
+    is of this workload and of the Amul variant this run uses."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(p):
         return None
     try:
         with open(p) as f:
             j = json.load(f)
-        if j.get("workload") == workload:
+        if j.get("workload") == workload and f"k_amul_dot<{variant}," in j.get("kernel", ""):
             return j.get("amul_dram_bytes_per_launch")
     except (OSError, ValueError):
         pass
@@ -305,7 +315,8 @@ def run_gpu(args, rank, world, local_rank):
     iters = sum(p["n_iterations"] for p in perfs)
     n_global = N * world
     value = n_global * iters / t
-    nb = algorithmic_bytes(N, F)
+    lat_k = len(P.spuma.host_lattice_offsets(N, mesh.owner, mesh.neighbour)) if st["amul_variant"] in (12, 13) else 0
+    nb = algorithmic_bytes(N, F, lat_k)
     peak, peak_kind = peaks()
     amul_ms = st["phase_ms"][1] / max(st["phase_count"][1], 1)
     achieved = nb["A"] / (amul_ms / 1e3) / 1e9 if amul_ms > 0 else None
@@ -360,13 +371,15 @@ def run_gpu(args, rank, world, local_rank):
         # the paper's coefficient of equivalence (Eq. 1) in its single-core form:
         # how many oracle cores one B200 is worth on this workload
         cpu["coe_cores_per_gpu"] = value / cpu["value"]
-    traffic = load_traffic(cfg["workload"])
+    traffic = load_traffic(cfg["workload"], st["amul_variant"])
     cfg.update({"global_cells": n_global, "faces_per_gpu": F, "parallelism": f"dd{world}", "transport": transport,
                 "iterations_per_step": iters / max(len(perfs), 1), "l2": "inputs larger than L2 (no flush)",
                 "batch_iterations": st["batch_iterations"], "grid": st["blocks_per_grid"],
                 "effective_iteration_GBps": eff_gbs,
-                "effective_iteration_note": "SURVEY 8(d) bytes 112N+16F per iteration x iterations / whole step time "
-                                            "(deferred psi updates move ~8 B/cell less than this algorithmic count)",
+                "effective_iteration_note": "algorithmic bytes per iteration of the layout run (lattice slots: "
+                                            "136N; ELL: SURVEY 8(d) 112N+16F) x iterations / whole step time "
+                                            "(deferred psi updates move ~8 B/cell less than this count)",
+                "amul_variant": st["amul_variant"],
                 "effective_iteration_frac_of_peak": (eff_gbs / peak) if eff_gbs else None,
                 "effective_iteration_frac_of_8TBps": (eff_gbs / 8000.0) if eff_gbs else None,
                 "phase_avg_ms": phase_avg, "algorithmic_bytes": nb})
@@ -375,7 +388,8 @@ def run_gpu(args, rank, world, local_rank):
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg,
            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                         "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                        "kernel": "k_amul_dot (A7 Amul + wA.pA)", "peak_source": f"{peak_kind} hbm_gbs",
+                        "kernel": f"k_amul_dot<{st['amul_variant']}> (A7 Amul + wA.pA, {nb['A_layout']})",
+                        "peak_source": f"{peak_kind} hbm_gbs",
                         "bytes_per_launch": nb["A"], "avg_launch_ms": amul_ms},
            "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": st["kernel_launches"],
            "solver": {"n_iterations": [p["n_iterations"] for p in perfs],

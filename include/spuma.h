@@ -323,6 +323,11 @@ spuma_status spuma_csr_values(spuma_mesh m, const spuma_scalar* diag, const spum
  * coarsest, concatenated (sum of level_cells[0 .. n_levels-2] entries).  order_*: [n_cells]. */
 spuma_status spuma_host_rcm(int n_cells, int n_faces, const spuma_label* owner, const spuma_label* neighbour,
                             spuma_label* perm);
+/* The lattice test of Amul variant 12: *n_offsets = K if every internal face's
+ * column offset neighbour - owner takes one of K <= 3 values with no repeated (owner, neighbour)
+ * pair (offsets[0..K-1] ascending), else 0.  Errors: ADDRESSING for an invalid lduAddressing. */
+spuma_status spuma_host_lattice_offsets(int n_cells, int n_faces, const spuma_label* owner,
+                                        const spuma_label* neighbour, int* n_offsets, int* offsets);
 spuma_status spuma_host_gamg_hierarchy(int n_cells, int n_faces, const spuma_label* owner,
                                        const spuma_label* neighbour, const spuma_scalar* face_weights,
                                        int n_coarsest, int max_levels, int max_out, int* n_levels,
@@ -416,6 +421,8 @@ typedef struct {
     double phase_ms[4];
     uint64_t phase_count[4];
     int blocks_per_grid, threads_per_block, batch_iterations;
+    int amul_variant;                /* the A7 layout the hot loop runs on this mesh (after fallbacks:
+                                        12 lattice slots -> 10 ELL -> 6 SELL -> 5 per-row)          */
 } spuma_stats;
 
 spuma_status spuma_get_stats(spuma_mesh m, spuma_stats* out);
@@ -434,7 +441,10 @@ spuma_status spuma_set_batch(spuma_mesh m, int iterations);
  * coefficient copy (no row extents streamed; one / two rows per thread), 10 (default) the
  * ELL rows of 8 software-pipelined (the next row's slot loads issued before the current
  * row's gathers), 11 the ELL rows with the first-level loads streamed by a per-warp
- * cp.async.bulk ring into shared memory (measured slower; A/B only).
+ * cp.async.bulk ring into shared memory (measured slower; A/B only), 12 (default) lattice
+ * slots: on a structured numbering (every face offset neighbour - owner one of <= 3 values,
+ * spuma_host_lattice_offsets) the rows need no index arrays and every load of a row is
+ * independent (falls back to 10 on other meshes), 13 the same with two rows per thread.
  * Errors: INVALID_ARGUMENT. */
 typedef enum {
     SPUMA_OPT_AMUL_VARIANT = 0,

@@ -463,6 +463,82 @@ __device__ __forceinline__ void amul_ell_pipelined(const MeshArgs& a, const doub
     }
 }
 
+// ---------------------------------------------------------------------------- variant 12 (lattice slots)
+// A structured numbering (host.h lattice_offsets: every face's column offset is one of K <= 3
+// values D[t], e.g. {1, n, n^2} for an n^3 block) needs no index arrays: slot t of row c is the
+// face (c, c + D[t]) with its coefficient at upper_d[t S + c] (kLatAbsent where the row has no
+// such face), and the neighbour-side face (c - D[t], c) is slot t of row c - D[t].  Every
+// address of a row is therefore a function of c alone -- diag[c], x[c], the K owner-side slots
+// (streamed), the K neighbour-side slots and the 2K x values (32-cell windows of the warp, L2
+// hits) are all issued at once: ONE dependent level instead of the ELL rows' two, and
+// 24 + 8K DRAM bytes per cell instead of 24 + 16 per face.  Same order as the oracle (reading
+// Q10): diag x, the neighbour side by ascending owner (t = K-1 .. 0), the owner side by
+// ascending neighbour (t = 0 .. K-1) -- bitwise the rows of every other variant.
+__device__ __forceinline__ bool lat_present(double u)
+{
+    return (unsigned long long)__double_as_longlong(u) != kLatAbsent;
+}
+
+template <int R, int IFM>
+__device__ __forceinline__ void amul_lattice(const MeshArgs& a, const double* __restrict__ diag,
+                                             const double* __restrict__ iface, const double* __restrict__ x,
+                                             const double* __restrict__ xr, double* __restrict__ y, double& acc,
+                                             bool dot, int rev)
+{
+    const int N = a.N, K = a.lat_K;
+    const long long S = a.lat_S;
+    const double* __restrict__ ud = a.upper_d;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nw = gridDim.x * (blockDim.x >> 5), wid = blockIdx.x * (blockDim.x >> 5) + warp;
+    const int nch = (N + 32 * R - 1) / (32 * R);
+    const int cnt = wid < nch ? (nch - 1 - wid) / nw + 1 : 0;
+    for (int j = 0; j < cnt; ++j) {
+        const int ch = wid + (rev ? cnt - 1 - j : j) * nw;
+        int c[R];
+        double dg[R], xc[R], uo[R][3], xo[R][3], un[R][3], xn[R][3];
+        bool on[R][3];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            c[r] = ch * 32 * R + 32 * r + lane;
+            const int cc = min(c[r], N - 1);
+            dg[r] = __ldg(diag + cc);
+            xc[r] = __ldg(x + cc);
+#pragma unroll
+            for (int t = 0; t < 3; ++t) {
+                if (t < K) {
+                    const int D = a.lat_D[t];
+                    const int o = cc - D;
+                    on[r][t] = o >= 0;
+                    const int oc = o >= 0 ? o : cc;
+                    uo[r][t] = __ldg(ud + t * S + cc);
+                    xo[r][t] = __ldg(x + min(cc + D, N - 1));
+                    un[r][t] = __ldg(ud + t * S + oc);
+                    xn[r][t] = __ldg(x + oc);
+                } else {
+                    on[r][t] = false;
+                    uo[r][t] = __longlong_as_double((long long)kLatAbsent);
+                    xo[r][t] = un[r][t] = xn[r][t] = 0.0;
+                }
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            double s = dg[r] * xc[r];
+#pragma unroll
+            for (int t = 2; t >= 0; --t)
+                if (on[r][t] && lat_present(un[r][t])) s = s + un[r][t] * xn[r][t];
+#pragma unroll
+            for (int t = 0; t < 3; ++t)
+                if (lat_present(uo[r][t])) s = s + uo[r][t] * xo[r][t];
+            if (c[r] < N) {
+                if constexpr (IFM == 1) s = add_iface(a, c[r], s, iface, xr);
+                y[c[r]] = s;
+                if (dot && (IFM != 2 || !is_iface_row(a, c[r]))) acc += s * xc[r];
+            }
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------- variant 3 (TMA)
 namespace tma {
 

@@ -95,6 +95,10 @@ MeshArgs mesh_args(const spuma_mesh m)
     a.upper_s = m->d_upper_s;
     a.cmeta = m->ell_stencil ? m->d_cmeta : nullptr;
     a.clane = m->ell_stencil ? m->d_clane : nullptr;
+    a.lat_K = m->d_upper_d ? m->lat_K : 0;
+    for (int t = 0; t < 3; ++t) a.lat_D[t] = m->lat_D[t];
+    a.lat_S = m->lat_S;
+    a.upper_d = m->d_upper_d;
     return a;
 }
 
@@ -422,6 +426,20 @@ void record(spuma_mesh m, std::vector<cudaEvent_t>& ev, int idx, cudaStream_t s)
 // and an ELL/SELL Amul: the halo (pack + NCCL send/recv on the comm stream) overlaps
 // the Amul of every row, whose interface rows are finished by k_iface_rows once the
 // halo has arrived (SURVEY §8(e) "overlapped with the interior Amul").
+// the per-call coefficient copy the selected Amul layout reads (ELL owner-slot order, or the
+// lattice slots of variant 12)
+void prepare_amul_coeffs(spuma_mesh m, cudaStream_t s, const MeshArgs& a, const double* upper)
+{
+    const int rv = resolve_amul_variant(m->amul_variant, a);
+    if (rv == 12 || rv == 13) {
+        launch_lattice_coeffs(s, a, upper);
+        m->stats.kernel_launches += 1;
+    } else if (amul_uses_ell(rv) && m->d_upper_s) {
+        launch_ell_coeffs(s, a, upper, m->d_upper_s);
+        m->stats.kernel_launches += 1;
+    }
+}
+
 spuma_status enqueue_iteration(spuma_mesh m, cudaStream_t s, std::vector<cudaEvent_t>* ev, int slot)
 {
     const MeshArgs a = mesh_args(m);
@@ -439,7 +457,7 @@ spuma_status enqueue_iteration(spuma_mesh m, cudaStream_t s, std::vector<cudaEve
     // alternating sweeps (slot parity): C asc, A desc, B asc | C desc, A asc, B desc | ...
     const bool odd = m->alt_sweep && (slot & 1);
     const bool alt = m->alt_sweep;
-    const bool overlap = !fin && m->n_iface > 0 && rv >= 6 && rv <= 11;
+    const bool overlap = !fin && m->n_iface > 0 && rv >= 6 && rv <= 13;
     if (fin && m->defer_psi && m->fuse_direction && rv == 8 && fused_direction_ok(a)) {
         // direction formed inside the Amul gather (one pass less per iteration)
         if (ev) record(m, *ev, slot * 6 + 0, s);
@@ -1332,7 +1350,7 @@ void spuma_free(spuma_mesh m)
         if (m->batch_done[i]) cudaEventDestroy(m->batch_done[i]);
         if (m->asm_ev[i]) cudaEventDestroy(m->asm_ev[i]);
     }
-    void* dptrs[] = {m->d_sell_meta, m->d_sell_n, m->d_sell_o, m->d_upper_s, m->d_cmeta, m->d_clane,
+    void* dptrs[] = {m->d_sell_meta, m->d_sell_n, m->d_sell_o, m->d_upper_s, m->d_cmeta, m->d_clane, m->d_upper_d,
                      m->d_owner, m->d_neighbour, m->d_ownerStart, m->d_losortStart, m->d_losort, m->d_ownerLo,
                      m->d_perm, m->d_face_map, m->d_delta, m->d_weights, m->d_magSf, m->d_bkind, m->d_bcell,
                      m->d_bproc, m->d_bmagSf, m->d_bdelta, m->d_bweight, m->d_bvalue, m->d_bgamma_r,
@@ -1541,6 +1559,17 @@ static spuma_status mesh_create_impl(const spuma_mesh_desc* d, spuma_mesh m)
             SPUMA_TRY(upload(&m->d_sell_meta, sell.meta, s));
             SPUMA_TRY(upload(&m->d_sell_n, sell.nslot, s));
             SPUMA_TRY(upload(&m->d_sell_o, sell.oslot, s));
+        }
+    }
+    {  // lattice slots (variant 12): absent slots are filled once here, present ones per solve
+        int D[3] = {0, 0, 0};
+        const int K = F > 0 ? lattice_offsets(N, F, owner.data(), neighbour.data(), D) : 0;
+        if (K > 0) {
+            m->lat_K = K;
+            for (int t = 0; t < 3; ++t) m->lat_D[t] = D[t];
+            m->lat_S = ((long long)N + 31) / 32 * 32;
+            SPUMA_TRY(dalloc(&m->d_upper_d, (size_t)(K * m->lat_S)));
+            launch_fill_u64(s, (long long)K * m->lat_S, m->d_upper_d, kLatAbsent);
         }
     }
     if (m->renumber) {
@@ -1774,10 +1803,7 @@ spuma_status spuma_amul(spuma_mesh m, const spuma_scalar* diag, const spuma_scal
         y_i = m->d_cell_t;
     }
     SPUMA_TRY(halo_exchange(m, x_i, m->ws.xr, s));
-    if (amul_uses_ell(m->amul_variant) && m->d_upper_s) {
-        launch_ell_coeffs(s, mesh_args(m), u_i, m->d_upper_s);
-        m->stats.kernel_launches += 1;
-    }
+    prepare_amul_coeffs(m, s, mesh_args(m), u_i);
     launch_amul(s, m->amul_variant, mesh_args(m), d_i, u_i, if_i, x_i, m->ws.xr, y_i,
                 (x_i == x) ? (long long)m->N : (long long)m->N + kPad, m->sell_wn, m->sell_wo);
     m->stats.kernel_launches += 1;
@@ -1835,10 +1861,7 @@ spuma_status spuma_pcg_solve(spuma_mesh m, const spuma_scalar* diag, const spuma
     // ---- A6 setup
     spuma::NvtxRange nvtx_loop("A6 setup + A7-A11 loop");
     const MeshArgs a = mesh_args(m);
-    if (amul_uses_ell(m->amul_variant) && m->d_upper_s) {
-        launch_ell_coeffs(s, a, P.upper, m->d_upper_s);
-        m->stats.kernel_launches += 1;
-    }
+    prepare_amul_coeffs(m, s, a, P.upper);
     const bool fin = m->n_ranks == 1;
     SPUMA_TRY(halo_exchange(m, P.psi, m->ws.xr, s));
     launch_setup1(s, m->grid, a, m->ws, fin);
@@ -2093,6 +2116,7 @@ spuma_status spuma_get_stats(spuma_mesh m, spuma_stats* out)
     if (!m || !out) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "NULL argument");
     m->stats.timing_enabled = m->timing;
     m->stats.batch_iterations = m->batch;
+    m->stats.amul_variant = resolve_amul_variant(m->amul_variant, mesh_args(m));
     *out = m->stats;
     return SPUMA_OK;
 }
@@ -2173,7 +2197,7 @@ spuma_status spuma_set_option(spuma_mesh m, int option, int value)
         m->small_max_cells = value;
         return SPUMA_OK;
     case SPUMA_OPT_AMUL_VARIANT:
-        if (value < 0 || value > 11) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "amul variant must be 0..11");
+        if (value < 0 || value > 13) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "amul variant must be 0..13");
         if (value != m->amul_variant) destroy_graphs(m);
         m->amul_variant = value;
         return SPUMA_OK;
@@ -2525,7 +2549,7 @@ spuma_status spuma_pcg_solve_pc(spuma_mesh m, const spuma_scalar* diag, const sp
     launch_scal_init(s, m->ws, *ctl, m->n_ranks);
     const MeshArgs a = mesh_args(m);
     const bool fin = m->n_ranks == 1;
-    if (amul_uses_ell(m->amul_variant) && m->d_upper_s) launch_ell_coeffs(s, a, Pp.upper, m->d_upper_s);
+    prepare_amul_coeffs(m, s, a, Pp.upper);
     SPUMA_TRY(halo_exchange(m, Pp.psi, m->ws.xr, s));
     launch_setup1(s, m->grid, a, m->ws, fin);
     if (!fin) SPUMA_TRY(reduce_finalize(m, 1, s));
@@ -2778,6 +2802,18 @@ spuma_status spuma_host_rcm(int n_cells, int n_faces, const spuma_label* owner, 
     if (!perm) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "perm is NULL");
     const std::vector<int> p = rcm_permutation(n_cells, n_faces, owner, neighbour);
     std::memcpy(perm, p.data(), sizeof(int) * p.size());
+    return SPUMA_OK;
+}
+
+spuma_status spuma_host_lattice_offsets(int n_cells, int n_faces, const spuma_label* owner,
+                                        const spuma_label* neighbour, int* n_offsets, int* offsets)
+{
+    std::vector<int> o, nb, os, ls, lo, olo;
+    SPUMA_TRY(host_addressing(n_cells, n_faces, owner, neighbour, o, nb, os, ls, lo, olo));
+    if (!n_offsets || !offsets) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "NULL output");
+    int D[3] = {0, 0, 0};
+    *n_offsets = n_faces > 0 ? lattice_offsets(n_cells, n_faces, owner, neighbour, D) : 0;
+    for (int t = 0; t < 3; ++t) offsets[t] = t < *n_offsets ? D[t] : 0;
     return SPUMA_OK;
 }
 

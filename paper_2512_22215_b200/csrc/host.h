@@ -40,6 +40,13 @@ EllStencil build_ell_stencil(int N, const std::vector<int>& ownerStart, const st
                              const std::vector<int>& losort, const std::vector<int>& ownerLo,
                              const std::vector<int>& neighbour);
 
+// Lattice slots (Amul variant 12): if every internal face's column offset
+// d = neighbour - owner takes one of at most 3 values and no owner has two faces with the same
+// offset (a structured numbering, e.g. an n^3 block: d in {1, n, n^2}), return their number K and
+// the offsets D[0] < ... < D[K-1]; otherwise 0.  Face f then lives in slot t (D[t] = d) of its
+// owner row, and the rows of the Amul need no index arrays at all.
+int lattice_offsets(int N, int F, const int* owner, const int* neighbour, int D[3]);
+
 // per-cell lists of the items i with keep[i], in input order
 void cell_lists(int N, const std::vector<int>& cell_of, const std::vector<char>& keep, std::vector<int>& start,
                 std::vector<int>& items);

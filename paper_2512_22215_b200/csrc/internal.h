@@ -62,7 +62,17 @@ struct MeshArgs {
     const double* upper_s;   // owner-slot ordered coefficient copy (variants 8/9), refreshed per call
     const int* cmeta;        // chunk-stencil compression of the ELL rows (variant 8; host.h build_ell_stencil)
     const unsigned* clane;   //   or nullptr
+    // lattice slots (variant 12; host.h lattice_offsets): slot t of row c holds the coefficient of
+    // the face (c, c + lat_D[t]) at upper_d[t * lat_S + c], kLatAbsent where there is no such face
+    int lat_K;               // 0: the numbering is not a lattice (variant 12 unavailable)
+    int lat_D[3];            // column offsets, ascending
+    long long lat_S;         // slot stride (elements)
+    const double* upper_d;   // [lat_K * lat_S], refreshed per solve / Amul call (k_lattice_coeffs)
 };
+
+// absent lattice slot: a NaN with a payload the assembly never produces (a caller upper array
+// holding exactly this bit pattern would be read as "no face")
+constexpr unsigned long long kLatAbsent = 0x7FF4A5A5C3C3A5A5ull;
 
 struct Workspace {
     double *wA, *rA, *pA, *rD, *sumA;
@@ -180,6 +190,10 @@ struct spuma_mesh_s {
     int* d_cmeta = nullptr;          // chunk-stencil ELL compression (uniform layout only)
     unsigned* d_clane = nullptr;
     bool ell_stencil = false;        // use it (SPUMA_OPT_ELL_STENCIL; measured neutral -> off)
+    int lat_K = 0;                   // lattice slots (variant 12): offsets, stride, coefficient copy
+    int lat_D[3] = {0, 0, 0};
+    long long lat_S = 0;
+    double* d_upper_d = nullptr;
     unsigned* d_sell_n = nullptr;
     int* d_sell_o = nullptr;
     // device: geometry
@@ -222,7 +236,7 @@ struct spuma_mesh_s {
     // captured iteration batches (ping-pong) and timing events
     int batch = 16;
     int small_max_cells = 8192;  // single-CTA solve at or below this many cells (1 rank)
-    int amul_variant = 10;  // ELL rows, software-pipelined (falls back to 6 -> 5 off uniform meshes)
+    int amul_variant = 12;  // lattice slots (falls back to 10 -> 6 -> 5 off lattice / uniform meshes)
     bool defer_psi = true;  // psi += alpha pA applied every second iteration (same rounding, fewer bytes)  // ELL + coefficient copy (falls back to 6 -> 5 when the mesh is not uniform)
     bool timing = false;
     int fuse_direction = 0;      // 0: k_direction + k_amul_dot (default: faster); 1: fused, rD read; 2: fused, 1/diag inline
@@ -302,6 +316,8 @@ void launch_amul(cudaStream_t s, int variant, const MeshArgs& a, const double* d
 void launch_gather(cudaStream_t s, int n, const int* idx, const double* in, double* out);   // out[i] = in[idx[i]]
 void launch_ell_coeffs(cudaStream_t s, const MeshArgs& a, const double* upper, double* upper_s);
 bool amul_uses_ell(int variant);
+void launch_lattice_coeffs(cudaStream_t s, const MeshArgs& a, const double* upper);  // variant 12 slots
+void launch_fill_u64(cudaStream_t s, long long n, double* p, unsigned long long v);
 void launch_scatter(cudaStream_t s, int n, const int* idx, const double* in, double* out);  // out[idx[i]] = in[i]
 void launch_pack(cudaStream_t s, int n, const int* cell, const double* x, double* out);     // out[i] = x[cell[i]]
 

@@ -292,7 +292,7 @@ __global__ void __launch_bounds__(kThreads)
 template <int V>
 constexpr int amul_min_ctas()
 {
-    return V == 4 ? 8 : (V == 3 ? 4 : ((V == 5 || V == 7 || V == 9) ? 3 : ((V == 6 || V == 8) ? 5 : (V == 10 ? 4 : (V == 11 ? 2 : 6)))));
+    return V == 4 ? 8 : (V == 3 ? 4 : ((V == 5 || V == 7 || V == 9) ? 3 : ((V == 6 || V == 8) ? 5 : (V == 10 ? 4 : (V == 11 ? 2 : (V == 12 ? 4 : (V == 13 ? 3 : 6)))))));
 }
 
 template <int V, int IFM = 0>
@@ -330,6 +330,9 @@ __global__ void __launch_bounds__(V == 3 ? tma::kBlock : kThreads, amul_min_ctas
         amul_ell_pipelined<IFM>(a, diag, upper, iface, x, xr, y, acc, false, 0);
     } else if constexpr (V == 11) {
         ring::amul_ring<IFM, false>(a, diag, upper, iface, x, xr, y, 0);
+    } else if constexpr (V == 12 || V == 13) {
+        double acc = 0.0;
+        amul_lattice<V == 13 ? 2 : 1, IFM>(a, diag, iface, x, xr, y, acc, false, 0);
     } else {
         for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < a.N; c += gridDim.x * blockDim.x)
             y[c] = V == 2 ? amul_row_unrolled(a, c, diag, upper, iface, x, xr)
@@ -478,6 +481,10 @@ __global__ void __launch_bounds__(V == 3 ? tma::kBlock : kThreads, amul_min_ctas
         v[0] = acc;
     } else if constexpr (V == 11) {
         v[0] = ring::amul_ring<IFM, true>(a, p.diag, p.upper, p.iface, w.pA, w.xr, w.wA, rev);
+    } else if constexpr (V == 12 || V == 13) {
+        double acc = 0.0;
+        amul_lattice<V == 13 ? 2 : 1, IFM>(a, p.diag, p.iface, w.pA, w.xr, w.wA, acc, true, rev);
+        v[0] = acc;
     } else {
         for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < a.N; c += gridDim.x * blockDim.x) {
             const double y = V == 2 ? amul_row_unrolled(a, c, p.diag, p.upper, p.iface, w.pA, w.xr)
@@ -1042,6 +1049,12 @@ int occupancy_grid(int N, int* grid_faces, int F)
     g = std::max(g, grid_for(k_amul_dot<10>, N));
     g = std::max(g, grid_for(k_amul_dot<10, 1>, N));
     g = std::max(g, grid_for(k_amul_dot<10, 2>, N));
+    g = std::max(g, grid_for(k_amul_dot<12>, N));
+    g = std::max(g, grid_for(k_amul_dot<12, 1>, N));
+    g = std::max(g, grid_for(k_amul_dot<12, 2>, N));
+    g = std::max(g, grid_for(k_amul_dot<13>, N, 2));
+    g = std::max(g, grid_for(k_amul_dot<13, 1>, N, 2));
+    g = std::max(g, grid_for(k_amul_dot<13, 2>, N, 2));
     g = std::max(g, grid_for(k_iface_rows, N));
     g = std::max(g, grid_for(k_update, N, 2));
     if (grid_faces) *grid_faces = grid_for(k_face_coeffs, F);
@@ -1093,11 +1106,17 @@ void launch_amul(cudaStream_t s, int variant, const MeshArgs& a, const double* d
                  int sell_wo)
 {
     if (a.N <= 0) return;
-    if ((variant == 10 || variant == 11) && !a.upper_s) variant = 6;
-    if ((variant == 8 || variant == 9) && !a.upper_s) variant -= 2;
-    if ((variant == 6 || variant == 7) && !a.sell_n) variant = 5;
+    variant = resolve_amul_variant(variant, a);
     const tma::Bounds bd{a.F, x_len, a.N, sell_wn, sell_wo};
     switch (variant) {
+    case 12:
+        if (a.ifMask) k_amul<12, 1><<<grid_for(k_amul<12, 1>, a.N), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd);
+        else k_amul<12><<<grid_for(k_amul<12>, a.N), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd);
+        break;
+    case 13:
+        if (a.ifMask) k_amul<13, 1><<<grid_for(k_amul<13, 1>, a.N, 2), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd);
+        else k_amul<13><<<grid_for(k_amul<13>, a.N, 2), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd);
+        break;
     case 1: k_amul<1><<<grid_for(k_amul<1>, a.N), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd); break;
     case 2: k_amul<2><<<grid_for(k_amul<2>, a.N), kThreads, 0, s>>>(a, diag, upper, iface, x, xr, y, bd); break;
     case 3:
@@ -1146,6 +1165,35 @@ __global__ void k_ell_coeffs(MeshArgs a, const double* __restrict__ upper, doubl
 
 bool amul_uses_ell(int variant) { return variant >= 8 && variant <= 11; }
 
+// lattice slot coefficient copy for variant 12 (once per solve / Amul call): face f is slot t of
+// its owner row, D[t] = neighbour - owner (absent slots keep kLatAbsent from mesh_create)
+__global__ void k_lattice_coeffs(MeshArgs a, const double* __restrict__ upper, double* __restrict__ ud)
+{
+    for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < a.F; f += gridDim.x * blockDim.x) {
+        const int o = __ldg(a.owner + f), d = __ldg(a.neighbour + f) - o;
+        const int t = d == a.lat_D[0] ? 0 : (d == a.lat_D[1] ? 1 : 2);
+        ud[t * a.lat_S + o] = __ldg(upper + f);
+    }
+}
+
+void launch_lattice_coeffs(cudaStream_t s, const MeshArgs& a, const double* upper)
+{
+    if (a.F <= 0 || !a.upper_d) return;
+    k_lattice_coeffs<<<grid_for(k_lattice_coeffs, a.F), kThreads, 0, s>>>(a, upper, const_cast<double*>(a.upper_d));
+}
+
+__global__ void k_fill_u64(long long n, unsigned long long* __restrict__ p, unsigned long long v)
+{
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        p[i] = v;
+}
+
+void launch_fill_u64(cudaStream_t s, long long n, double* p, unsigned long long v)
+{
+    if (n <= 0) return;
+    k_fill_u64<<<grid_for(k_fill_u64, n), kThreads, 0, s>>>(n, reinterpret_cast<unsigned long long*>(p), v);
+}
+
 void launch_ell_coeffs(cudaStream_t s, const MeshArgs& a, const double* upper, double* upper_s)
 {
     if (a.F <= 0 || !upper_s) return;
@@ -1189,6 +1237,7 @@ void launch_direction(cudaStream_t s, int grid, const MeshArgs& a, const Workspa
 
 int resolve_amul_variant(int variant, const MeshArgs& a)
 {
+    if ((variant == 12 || variant == 13) && !(a.upper_d && a.lat_K > 0)) variant = 10;  // not a lattice numbering
     if ((variant == 10 || variant == 11) && !a.upper_s) variant = 6;
     if ((variant == 8 || variant == 9) && !a.upper_s) variant -= 2;  // no uniform-width layout: SELL
     if ((variant == 6 || variant == 7) && !a.sell_n) variant = 5;    // layout not encodable on this mesh
@@ -1207,6 +1256,8 @@ void launch_amul_dot(cudaStream_t s, int variant, const MeshArgs& a, const Works
         case 8: launch_hot(k_amul_dot<8, 2>, grid_for(k_amul_dot<8, 2>, a.N), kThreads, s, a, w, f, sell_wn, sell_wo, r); return;
         case 9: launch_hot(k_amul_dot<9, 2>, grid_for(k_amul_dot<9, 2>, a.N, 2), kThreads, s, a, w, f, sell_wn, sell_wo, r); return;
         case 10: launch_hot(k_amul_dot<10, 2>, grid_for(k_amul_dot<10, 2>, a.N), kThreads, s, a, w, f, sell_wn, sell_wo, r); return;
+        case 12: launch_hot(k_amul_dot<12, 2>, grid_for(k_amul_dot<12, 2>, a.N), kThreads, s, a, w, f, sell_wn, sell_wo, r); return;
+        case 13: launch_hot(k_amul_dot<13, 2>, grid_for(k_amul_dot<13, 2>, a.N, 2), kThreads, s, a, w, f, sell_wn, sell_wo, r); return;
         case 11: launch_hot_smem(k_amul_dot<11, 2>, ring_grid(k_amul_dot<11, 2>, a.N), ring::kSmem, s, a, w, f, sell_wn, sell_wo, r); return;
         default: break;  // other variants add the interface terms inline (halo must precede them)
         }
@@ -1238,6 +1289,14 @@ void launch_amul_dot(cudaStream_t s, int variant, const MeshArgs& a, const Works
     case 10:
         if (a.ifMask) launch_hot(k_amul_dot<10, 1>, grid_for(k_amul_dot<10, 1>, a.N), kThreads, s, a, w, f, sell_wn, sell_wo, r);
         else launch_hot(k_amul_dot<10>, grid_for(k_amul_dot<10>, a.N), kThreads, s, a, w, f, sell_wn, sell_wo, r);
+        break;
+    case 12:
+        if (a.ifMask) launch_hot(k_amul_dot<12, 1>, grid_for(k_amul_dot<12, 1>, a.N), kThreads, s, a, w, f, sell_wn, sell_wo, r);
+        else launch_hot(k_amul_dot<12>, grid_for(k_amul_dot<12>, a.N), kThreads, s, a, w, f, sell_wn, sell_wo, r);
+        break;
+    case 13:
+        if (a.ifMask) launch_hot(k_amul_dot<13, 1>, grid_for(k_amul_dot<13, 1>, a.N, 2), kThreads, s, a, w, f, sell_wn, sell_wo, r);
+        else launch_hot(k_amul_dot<13>, grid_for(k_amul_dot<13>, a.N, 2), kThreads, s, a, w, f, sell_wn, sell_wo, r);
         break;
     case 11:
         if (a.ifMask) launch_hot_smem(k_amul_dot<11, 1>, ring_grid(k_amul_dot<11, 1>, a.N), ring::kSmem, s, a, w, f, sell_wn, sell_wo, r);

@@ -304,4 +304,24 @@ void ldu_to_csr_host(int N, int F, const std::vector<int>& owner, const std::vec
     }
 }
 
+int lattice_offsets(int N, int F, const int* owner, const int* neighbour, int D[3])
+{
+    int K = 0;
+    for (int f = 0; f < F; ++f) {
+        const int d = neighbour[f] - owner[f];
+        int t = 0;
+        while (t < K && D[t] != d) ++t;
+        if (t == K) {
+            if (K == 3) return 0;
+            D[K++] = d;
+        }
+    }
+    std::sort(D, D + K);
+    // faces are sorted by (owner, neighbour): a repeated offset within one owner is adjacent
+    for (int f = 1; f < F; ++f)
+        if (owner[f] == owner[f - 1] && neighbour[f] == neighbour[f - 1]) return 0;
+    (void)N;
+    return K;
+}
+
 }  // namespace spuma

@@ -36,7 +36,7 @@ OPT_L2_PERSIST = 8
 OPT_GAMG_CSR = 9
 OPT_PEER_POLL_MS = 10
 PEER_BLOB_BYTES = 512  # SPUMA_PEER_BLOB_BYTES
-AMUL_VARIANTS = (0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11)
+AMUL_VARIANTS = (0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13)
 
 _vp, _ci, _cd, _lab = ctypes.c_void_p, ctypes.c_int, ctypes.c_double, ctypes.c_int32
 
@@ -115,7 +115,8 @@ class CommCallbacks(ctypes.Structure):
 class Stats(ctypes.Structure):
     _fields_ = [("kernel_launches", ctypes.c_uint64), ("solves", ctypes.c_uint64), ("iterations", ctypes.c_uint64),
                 ("timing_enabled", _ci), ("phase_ms", _cd * 4), ("phase_count", ctypes.c_uint64 * 4),
-                ("blocks_per_grid", _ci), ("threads_per_block", _ci), ("batch_iterations", _ci)]
+                ("blocks_per_grid", _ci), ("threads_per_block", _ci), ("batch_iterations", _ci),
+                ("amul_variant", _ci)]
 
     def as_dict(self):
         d = {k: getattr(self, k) for k, _ in self._fields_}
@@ -183,6 +184,8 @@ def lib():
             L.spuma_host_gamg_hierarchy.argtypes = [_ci, _ci, _vp, _vp, _vp, _ci, _ci, _ci, _vp, _vp, _vp, _vp]
             L.spuma_host_level_schedule.argtypes = [_ci, _ci, _vp, _vp, _vp, _vp, _vp, _vp]
             L.spuma_host_ldu_to_csr.argtypes = [_ci, _ci] + [_vp] * 5
+        if hasattr(L, "spuma_host_lattice_offsets"):
+            L.spuma_host_lattice_offsets.argtypes = [_ci, _ci, _vp, _vp, _vp, _vp]
         L.spuma_last_error.restype = ctypes.c_char_p
         L.spuma_abi_version.restype = _ci
         for name in ("spuma_mesh_create", "spuma_assemble_laplacian", "spuma_pcg_solve", "spuma_amul",
@@ -587,6 +590,17 @@ def host_rcm(n_cells: int, owner, neighbour) -> np.ndarray:
     perm = np.zeros(max(n_cells, 1), np.int32)
     _check(lib().spuma_host_rcm(n_cells, o.shape[0], o.ctypes.data, nb.ctypes.data, perm.ctypes.data))
     return perm[:n_cells]
+
+
+def host_lattice_offsets(n_cells: int, owner, neighbour) -> list:
+    """spuma_host_lattice_offsets: the column offsets of Amul variant 12's lattice slots ([] if the
+    numbering is not a lattice)."""
+    o, nb = _addr(owner, neighbour)
+    k = ctypes.c_int(0)
+    d = np.zeros(3, np.int32)
+    _check(lib().spuma_host_lattice_offsets(n_cells, o.shape[0], o.ctypes.data, nb.ctypes.data,
+                                            ctypes.addressof(k), d.ctypes.data))
+    return d[:k.value].tolist()
 
 
 def host_gamg_hierarchy(n_cells: int, owner, neighbour, face_weights, n_coarsest=10, max_levels=50) -> dict:

@@ -36,7 +36,8 @@ def test_own_stream_is_ordered_after_default_stream_work():
     diag, upper, src, _ = gpu_assemble(h, m, None, 0, 0.0, b)
     psi_ref = torch.zeros(m.n_cells, **F64)
     ref = h.pcg_solve(diag, upper, None, src, psi_ref, 1e-8, 0.0, 5000, 0)
-    x0 = dev(np.linspace(-1.0, 1.0, m.n_cells))
+    x0h = np.linspace(-1.0, 1.0, m.n_cells)
+    x0 = dev(x0h)
     for _ in range(3):
         psi = torch.full((m.n_cells,), 123.0, **F64)
         torch.cuda.synchronize()
@@ -51,7 +52,7 @@ def test_own_stream_is_ordered_after_default_stream_work():
         x.copy_(x0)
         h.amul(diag, upper, None, x, y)
         torch.cuda.synchronize()
-        assert np.array_equal(y.cpu().numpy(), O.amul(m, diag.cpu().numpy(), upper.cpu().numpy(), x0))
+        assert np.array_equal(y.cpu().numpy(), O.amul(m, diag.cpu().numpy(), upper.cpu().numpy(), x0h))
     h.free()
 
 

@@ -89,3 +89,38 @@ def test_host_gamg_hierarchy_dd_matches_oracle(P, how, params):
     assert hh["level_cells"] == po["level_cells"]
     assert hh["level_ifaces"] == po["level_ifaces"]
     assert hh["levels"] >= (3 if ml > 3 else ml)
+
+
+def _offsets_by_definition(m):
+    """The lattice test written out: the distinct column offsets of the faces (at most 3) and no
+    repeated (owner, neighbour) pair."""
+    d = sorted(set((m.neighbour - m.owner).tolist()))
+    pairs = set(zip(m.owner.tolist(), m.neighbour.tolist()))
+    return d if (0 < len(d) <= 3 and len(pairs) == m.n_faces) else []
+
+
+@pytest.mark.parametrize("name,make,expect", [
+    ("cube5", lambda: gen.cube(5), [1, 5, 25]),
+    ("cube200-like box", lambda: gen.box(7, 3, 2), [1, 7, 21]),
+    ("cavity2d", lambda: gen.cavity2d(20), [1, 20]),
+    ("chain", lambda: gen.box(9, 1, 1), [1]),
+    ("perturbed", lambda: gen.perturbed(6, 0.3), [1, 6, 36]),
+    ("weak block (rank 1 of 2x2x1)", lambda: gen.weak_block(6, (2, 2, 1), 1), [1, 6, 36]),
+    ("permuted", lambda: gen.permute(gen.cube(5), seed=2), []),
+])
+def test_host_lattice_offsets(name, make, expect):
+    """Amul variant 12 runs exactly on the meshes whose faces take <= 3 column offsets."""
+    m = make()
+    got = S.host_lattice_offsets(m.n_cells, m.owner, m.neighbour)
+    assert got == expect == _offsets_by_definition(m)
+
+
+def test_host_lattice_offsets_rejects_repeated_pairs_and_four_offsets():
+    # two faces between cells 0 and 1 (legal lduAddressing, not a lattice)
+    o, nb = np.array([0, 0, 1], np.int32), np.array([1, 1, 2], np.int32)
+    assert S.host_lattice_offsets(3, o, nb) == []
+    # offsets {1, 2, 3, 4}
+    o, nb = np.array([0, 0, 0, 0], np.int32), np.array([1, 2, 3, 4], np.int32)
+    assert S.host_lattice_offsets(5, o, nb) == []
+    assert S.host_lattice_offsets(5, o[:3], nb[:3]) == [1, 2, 3]
+    assert S.host_lattice_offsets(1, np.zeros(0, np.int32), np.zeros(0, np.int32)) == []
