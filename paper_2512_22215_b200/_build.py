@@ -47,24 +47,26 @@ def stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
+def build(force: bool = False, verbose: bool = False, defines=(), out: str = None) -> str:
+    """defines / out: an A/B build with -D<define> into another path (loaded via SPUMA_LIBRARY)."""
+    if out is None and not force and not stale():
         return SO
     nvcc = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
     inc, lib = nccl_dirs()
     libname = os.path.basename(sorted(glob.glob(os.path.join(lib, "libnccl.so*")))[0])
-    tmp = SO + f".tmp{os.getpid()}"
+    dst = out or SO
+    tmp = dst + f".tmp{os.getpid()}"
     cmd = [nvcc, *ARCH, "-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-shared",
            "-Xcompiler", "-fPIC,-ffp-contract=off,-O2", "-Xptxas", "-v" if verbose else "-O3",
-           "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", inc,
+           *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", inc,
            *sources(), "-o", tmp, "-L", lib, f"-l:{libname}", "-Xlinker", f"-rpath,{lib}", "-lcudart_static"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + " ".join(cmd) + "\n" + r.stdout + r.stderr)
     if verbose:
         print(r.stdout + r.stderr)
-    os.replace(tmp, SO)
-    return SO
+    os.replace(tmp, dst)
+    return dst
 
 
 if __name__ == "__main__":
