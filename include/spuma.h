@@ -454,7 +454,10 @@ typedef enum {
     /* programmatic dependent launch of the hot-loop kernels (1 = on, default; process-wide) */
     SPUMA_OPT_PDL = 2,
     /* apply psi += alpha pA for two iterations at once (psi = (psi + a1 p1) + a2 p2: the same
-     * roundings, fewer bytes); 1 = on (default), 0 = every iteration */
+     * roundings, fewer bytes): 0 = every iteration, 1 = the pairs in the update pass (which then
+     * reads both directions), 2 = the pairs in the direction pass of every even iteration, where
+     * the previous direction is read anyway and the one before is the value being overwritten
+     * (default: 4 B/cell per iteration fewer than 1) */
     SPUMA_OPT_DEFER_PSI = 3,
     /* GAMG: the levels from the first one (below the finest) with at most this many cells
      * down to the coarsest run in ONE single-CTA kernel per V-cycle (Richardson, scaled

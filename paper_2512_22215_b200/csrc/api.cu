@@ -458,7 +458,10 @@ spuma_status enqueue_iteration(spuma_mesh m, cudaStream_t s, std::vector<cudaEve
     const bool odd = m->alt_sweep && (slot & 1);
     const bool alt = m->alt_sweep;
     const bool overlap = !fin && m->n_iface > 0 && rv >= 6 && rv <= 13;
-    if (fin && m->defer_psi && m->fuse_direction && rv == 8 && fused_direction_ok(a)) {
+    // SPUMA_OPT_DEFER_PSI = 2: the pairs are applied by the direction of every even iteration
+    const bool psi_in_dir = m->defer_psi == 2;
+    if (psi_in_dir) psi_mode = 1;
+    if (fin && m->defer_psi == 1 && m->fuse_direction && rv == 8 && fused_direction_ok(a)) {
         // direction formed inside the Amul gather (one pass less per iteration)
         if (ev) record(m, *ev, slot * 6 + 0, s);
         if (ev) record(m, *ev, slot * 6 + 1, s);
@@ -472,7 +475,7 @@ spuma_status enqueue_iteration(spuma_mesh m, cudaStream_t s, std::vector<cudaEve
         return SPUMA_OK;
     }
     if (ev) record(m, *ev, slot * 6 + 0, s);
-    launch_direction(s, m->grid, a, ws, odd);
+    launch_direction(s, m->grid, a, ws, odd, psi_in_dir && !(slot & 1));
     if (ev) record(m, *ev, slot * 6 + 1, s);
     if (overlap) {
         if (!m->external_comm) {
@@ -1917,8 +1920,12 @@ spuma_status spuma_pcg_solve(spuma_mesh m, const spuma_scalar* diag, const spuma
     }
     DevScal fs;
     SPUMA_CUDA(cudaMemcpy(&fs, m->ws.scal, sizeof(DevScal), cudaMemcpyDeviceToHost));
-    if (m->defer_psi && (fs.n & 1)) {  // the last iteration's psi update is still pending
+    if (m->defer_psi == 1 && (fs.n & 1)) {  // the last iteration's psi update is still pending
         launch_psi_flush(s, m->N, m->ws);
+        m->stats.kernel_launches += 1;
+        SPUMA_CUDA(cudaStreamSynchronize(s));
+    } else if (m->defer_psi == 2 && fs.n > fs.psi_done) {  // the last one or two updates are pending
+        launch_psi_flush2(s, m->N, m->ws, fs.n, fs.n - fs.psi_done);
         m->stats.kernel_launches += 1;
         SPUMA_CUDA(cudaStreamSynchronize(s));
     }
@@ -2179,8 +2186,9 @@ spuma_status spuma_set_option(spuma_mesh m, int option, int value)
         m->gamg_tail_cells = value;  // the captured V-cycle is re-captured at the next solve
         return SPUMA_OK;
     case SPUMA_OPT_DEFER_PSI:
-        if (m->defer_psi != (value != 0)) destroy_graphs(m);
-        m->defer_psi = value != 0;
+        if (value < 0 || value > 2) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "defer_psi is 0, 1 or 2");
+        if (m->defer_psi != value) destroy_graphs(m);
+        m->defer_psi = value;
         return SPUMA_OK;
     case SPUMA_OPT_PDL:
         if (g_use_pdl != (value != 0)) {

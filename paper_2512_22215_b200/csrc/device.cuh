@@ -164,6 +164,7 @@ static __device__ void finalize(DevScal* s, int stage, const double* g)
         s->wArAold = s->wArA;
         s->wArA = g[0];
         s->beta = s->wArA / s->wArAold;
+        s->alpha_prev2 = s->alpha_prev;
         s->alpha_prev = s->alpha;  // a deferred psi update of this iteration uses it
         break;
     }

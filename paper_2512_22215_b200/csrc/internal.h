@@ -22,11 +22,13 @@ constexpr int kPhases = 4;         // timing phases (spuma_stats.phase_ms)
 // (last CTA of a reduction kernel, or the 1-CTA finalise kernel when P > 1).
 struct DevScal {
     double wArA, wArAold, wApA, alpha, beta, alpha_prev;
+    double alpha_prev2;    // alpha of the iteration before alpha_prev (psi updates in the direction)
     double normFactor, init, fin, xbar;
     double tol, rel_tol;
     double rank_part[4];   // this rank's partial sums of the current reduction (P > 1)
     int n, done, singular, converged;
-    int max_iter, min_iter, n_ranks, pad;
+    int max_iter, min_iter, n_ranks;
+    int psi_done;          // psi updates applied so far (SPUMA_OPT_DEFER_PSI = 2: by k_direction)
     unsigned int ticket[8];
 };
 
@@ -237,7 +239,7 @@ struct spuma_mesh_s {
     int batch = 16;
     int small_max_cells = 8192;  // single-CTA solve at or below this many cells (1 rank)
     int amul_variant = 12;  // lattice slots (falls back to 10 -> 6 -> 5 off lattice / uniform meshes)
-    bool defer_psi = true;  // psi += alpha pA applied every second iteration (same rounding, fewer bytes)  // ELL + coefficient copy (falls back to 6 -> 5 when the mesh is not uniform)
+    int defer_psi = 2;      // 0: psi += alpha pA every iteration; 1: pairs in k_update; 2: pairs in k_direction  // psi += alpha pA applied every second iteration (same rounding, fewer bytes)  // ELL + coefficient copy (falls back to 6 -> 5 when the mesh is not uniform)
     bool timing = false;
     int fuse_direction = 0;      // 0: k_direction + k_amul_dot (default: faster); 1: fused, rD read; 2: fused, 1/diag inline
     bool gamg_csr = true;        // GAMG coarse generic levels as CSR runs (SPUMA_OPT_GAMG_CSR)
@@ -324,7 +326,10 @@ void launch_pack(cudaStream_t s, int n, const int* cell, const double* x, double
 // PCG (A6-A12). `fin` = true when this rank finalises itself (P == 1).
 void launch_setup1(cudaStream_t s, int grid, const MeshArgs& a, const Workspace& w, bool fin);
 void launch_setup2(cudaStream_t s, int grid, const MeshArgs& a, const Workspace& w, bool fin);
-void launch_direction(cudaStream_t s, int grid, const MeshArgs& a, const Workspace& w, bool reverse = false);
+// psi_pair (SPUMA_OPT_DEFER_PSI = 2, even iterations k >= 2): also psi = (psi + alpha_{k-2} p_{k-2}) +
+// alpha_{k-1} p_{k-1}, p_{k-2} being the buffer the new direction overwrites
+void launch_direction(cudaStream_t s, int grid, const MeshArgs& a, const Workspace& w, bool reverse = false,
+                      bool psi_pair = false);
 void launch_amul_dot(cudaStream_t s, int variant, const MeshArgs& a, const Workspace& w, bool fin, int sell_wn,
                      int sell_wo, bool deferred = false, bool reverse = false);
 // reverse: the kernel sweeps its cells in descending order (alternating sweep directions between
@@ -363,6 +368,9 @@ void launch_update(cudaStream_t s, int grid, const MeshArgs& a, const Workspace&
                    bool reverse = false);
 // psi_mode: 0 psi += alpha pA; 1 defer (psi untouched); 2 psi = (psi + alpha_prev pA_prev) + alpha pA
 void launch_psi_flush(cudaStream_t s, int N, const Workspace& w);
+// SPUMA_OPT_DEFER_PSI = 2: the pending updates j = n - pending .. n - 1 (pending <= 2), p_j in pA if
+// j is even, else pA2; alpha_{n-1} = alpha_prev, alpha_{n-2} = alpha_prev2
+void launch_psi_flush2(cudaStream_t s, int N, const Workspace& w, int n, int pending);
 // A11+A7+A8 in one kernel (ELL, single rank, deferred psi): see kernels.cu
 bool fused_direction_ok(const MeshArgs& a);
 void launch_amul_dot_dir(cudaStream_t s, const MeshArgs& a, const Workspace& w, bool inline_rd);  // psi += alpha_prev pA (pending update)

@@ -400,17 +400,24 @@ __global__ void __launch_bounds__(kThreads) k_setup2(MeshArgs a, Workspace w, in
 // ---------------------------------------------------------------------------
 
 // A11 pA = rD rA + beta pA  (n == 0: pA = rD rA)
-__global__ void __launch_bounds__(kThreads) k_direction(int N, Workspace w, int rev)
+// psi_pair (deferred psi updates in the direction, SPUMA_OPT_DEFER_PSI = 2; even k >= 2): the
+// pair (k-2, k-1) -- psi = (psi + alpha_{k-2} p_{k-2}) + alpha_{k-1} p_{k-1}, the two roundings of
+// two separate updates, so the iterates are bitwise unchanged -- applied here, where p_{k-1}
+// (pA_prev) is read anyway and p_{k-2} is the value of pA this pass overwrites (read first).
+__global__ void __launch_bounds__(kThreads) k_direction(int N, Workspace w, int rev, int psi_pair)
 {
     pdl_wait();
     if (w.scal->done) return;
-    const bool first = w.scal->n == 0;
-    const double beta = w.scal->beta;
+    const int n = w.scal->n;
+    const bool first = n == 0;
+    const bool psi = psi_pair && n >= 2;
+    const double beta = w.scal->beta, a1 = w.scal->alpha_prev, a2 = w.scal->alpha_prev2;
     const int np = N >> 1;
     const double2* __restrict__ rD2 = reinterpret_cast<const double2*>(w.rD);
     const double2* __restrict__ rA2 = reinterpret_cast<const double2*>(w.rA);
     const double2* pprev = reinterpret_cast<const double2*>(w.pA_prev);  // may alias pA (in place)
     double2* pA2 = reinterpret_cast<double2*>(w.pA);
+    double2* psi2 = psi ? reinterpret_cast<double2*>(w.ptrs->psi) : nullptr;
     const GridStride gs(np, rev);
     for (int j = 0; j < gs.cnt; ++j) {
         const int i = gs.at(j);
@@ -421,6 +428,15 @@ __global__ void __launch_bounds__(kThreads) k_direction(int N, Workspace w, int 
             q.y = d.y * r.y;
         } else {
             const double2 p = pprev[i];
+            if (psi) {
+                double2 x = psi2[i];
+                const double2 o = pA2[i];  // p_{k-2}
+                x.x = x.x + a2 * o.x;
+                x.y = x.y + a2 * o.y;
+                x.x = x.x + a1 * p.x;
+                x.y = x.y + a1 * p.y;
+                psi2[i] = x;
+            }
             q.x = d.x * r.x + beta * p.x;
             q.y = d.y * r.y + beta * p.y;
         }
@@ -428,8 +444,13 @@ __global__ void __launch_bounds__(kThreads) k_direction(int N, Workspace w, int 
     }
     if ((N & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
         const int c = N - 1;
+        if (psi) {
+            double* ps = w.ptrs->psi;
+            ps[c] = (ps[c] + a2 * w.pA[c]) + a1 * w.pA_prev[c];
+        }
         w.pA[c] = first ? w.rD[c] * w.rA[c] : w.rD[c] * w.rA[c] + beta * w.pA_prev[c];
     }
+    if (psi && blockIdx.x == 0 && threadIdx.x == 0) w.scal->psi_done = n;
     pdl_trigger();
 }
 
@@ -925,7 +946,8 @@ __global__ void k_scal_init(DevScal* s, double tol, double rel_tol, int max_iter
     s->done = 0;
     s->singular = 0;
     s->converged = 0;
-    s->alpha = s->beta = 0.0;
+    s->alpha = s->beta = s->alpha_prev = s->alpha_prev2 = 0.0;
+    s->psi_done = 0;
     for (int i = 0; i < 4; ++i) s->rank_part[i] = 0.0;
 }
 
@@ -1229,10 +1251,10 @@ void launch_setup2(cudaStream_t s, int grid, const MeshArgs& a, const Workspace&
     k_setup2<<<grid_for(k_setup2, a.N), kThreads, 0, s>>>(a, w, fin ? 1 : 0);
 }
 
-void launch_direction(cudaStream_t s, int grid, const MeshArgs& a, const Workspace& w, bool reverse)
+void launch_direction(cudaStream_t s, int grid, const MeshArgs& a, const Workspace& w, bool reverse, bool psi_pair)
 {
     (void)grid;
-    launch_hot(k_direction, grid_for(k_direction, a.N, 2), kThreads, s, a.N, w, reverse ? 1 : 0);
+    launch_hot(k_direction, grid_for(k_direction, a.N, 2), kThreads, s, a.N, w, reverse ? 1 : 0, psi_pair ? 1 : 0);
 }
 
 int resolve_amul_variant(int variant, const MeshArgs& a)
@@ -1332,6 +1354,25 @@ __global__ void k_psi_flush(int N, Workspace w)
     const double a = w.scal->alpha_prev;
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < N; c += gridDim.x * blockDim.x)
         p.psi[c] = p.psi[c] + a * w.pA[c];
+}
+
+__global__ void k_psi_flush2(int N, Workspace w, int n, int pending)
+{
+    const DevPtrs p = *w.ptrs;
+    const double a1 = w.scal->alpha_prev, a2 = w.scal->alpha_prev2;
+    const double* p1 = ((n - 1) & 1) ? w.pA2 : w.pA;  // p_{n-1}
+    const double* p2 = ((n - 2) & 1) ? w.pA2 : w.pA;  // p_{n-2}
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < N; c += gridDim.x * blockDim.x) {
+        double x = p.psi[c];
+        if (pending == 2) x = x + a2 * p2[c];
+        p.psi[c] = x + a1 * p1[c];
+    }
+}
+
+void launch_psi_flush2(cudaStream_t s, int N, const Workspace& w, int n, int pending)
+{
+    if (N <= 0 || pending <= 0) return;
+    k_psi_flush2<<<grid_for(k_psi_flush2, N), kThreads, 0, s>>>(N, w, n, pending);
 }
 
 void launch_psi_flush(cudaStream_t s, int N, const Workspace& w)

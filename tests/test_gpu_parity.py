@@ -454,13 +454,31 @@ def test_deferred_psi_updates_are_bitwise_neutral(iters):
     g, b = gen.gamma_lognormal(m), gen.rhs(m)
     ctl = (1e-8, 0.0, 5000, 0) if iters is None else (0.0, 0.0, iters, iters)
     out = []
-    for defer in (0, 1):
+    for defer in (0, 1, 2):  # every iteration / pairs in the update / pairs in the direction
         h = P.Mesh.from_mesh(m)
         h.set_option(P.spuma.OPT_SMALL_SOLVE_MAX_CELLS, 0)
         h.set_option(P.spuma.OPT_DEFER_PSI, defer)
         out.append(gpu_solve_case(m, g, b, 0, ctl, handle=h)[:2])
+    for k in (1, 2):
+        assert out[0][1] == out[k][1]
+        assert np.array_equal(out[0][0].view(np.uint64), out[k][0].view(np.uint64)), k
+
+
+@pytest.mark.parametrize("iters", [1, 2, 3, 4, 17])
+def test_deferred_psi_in_direction_lattice_and_psi0(iters):
+    """SPUMA_OPT_DEFER_PSI = 2 on the lattice hot loop with a non-zero psi0: every pending-update
+    count of the final flush (0, 1, 2) gives bitwise the psi of per-iteration updates."""
+    m = gen.cube(24)
+    g, b = gen.gamma_lognormal(m), gen.rhs(m)
+    psi0 = np.cos(np.arange(m.n_cells) * 0.01)
+    out = []
+    for defer in (0, 2):
+        h = P.Mesh.from_mesh(m)
+        h.set_option(P.spuma.OPT_DEFER_PSI, defer)
+        out.append(gpu_solve_case(m, g, b, 0, (0.0, 0.0, iters, iters), psi0=psi0, handle=h)[:2])
+        h.free()
     assert out[0][1] == out[1][1]
-    assert np.array_equal(out[0][0], out[1][0])
+    assert np.array_equal(out[0][0].view(np.uint64), out[1][0].view(np.uint64))
 
 
 @pytest.mark.parametrize("mode", [1, 2])
