@@ -556,6 +556,8 @@ void l2_reset(spuma_mesh m)
     m->l2_limit_set = false;
 }
 
+constexpr int kTimedSlots = 2;  // iterations per batch carrying timing events (spuma_set_timing)
+
 spuma_status build_graphs(spuma_mesh m)
 {
     if (m->gexec[0] && m->gexec_timed == m->timing && m->gexec_batch == batch_eff(m)) return SPUMA_OK;
@@ -564,7 +566,7 @@ spuma_status build_graphs(spuma_mesh m)
     for (int g = 0; g < 2; ++g) {
         std::vector<cudaEvent_t>* ev = nullptr;
         if (m->timing) {
-            m->tev[g].resize(6);
+            m->tev[g].resize(6 * kTimedSlots);
             for (auto& e : m->tev[g]) SPUMA_CUDA(cudaEventCreate(&e));
             ev = &m->tev[g];
         }
@@ -577,10 +579,11 @@ spuma_status build_graphs(spuma_mesh m)
         }
         SPUMA_CUDA(cudaStreamBeginCapture(m->stream, cudaStreamCaptureModeThreadLocal));
         spuma_status st = SPUMA_OK;
-        // timing samples the first iteration of every batch (6 event nodes per batch on a leaf
-        // branch; ~100 samples per 1600-iteration solve)
+        // timing samples the first two iterations of every batch -- one even, one odd, so both
+        // halves of the deferred-psi pattern are in the averages (6 event nodes per timed
+        // iteration on a leaf branch; ~200 samples per 1600-iteration solve)
         for (int k = 0; k < batch_eff(m) && st == SPUMA_OK; ++k)
-            st = enqueue_iteration(m, m->stream, k == 0 ? ev : nullptr, k);
+            st = enqueue_iteration(m, m->stream, k < kTimedSlots ? ev : nullptr, k);
         if (m->timing) {  // the timing branch rejoins the origin stream at the end of the batch
             cudaEventRecord(m->tfork, m->tstream);
             cudaStreamWaitEvent(m->stream, m->tfork, 0);
@@ -602,17 +605,17 @@ spuma_status build_graphs(spuma_mesh m)
     return SPUMA_OK;
 }
 
-// a batch whose first iteration ran (executed > 0) contributes one sample per phase
+// every timed iteration of a batch that ran (slot < executed) contributes one sample per phase
 spuma_status account_timing(spuma_mesh m, int g, int executed)
 {
-    if (executed <= 0) return SPUMA_OK;
     static const int from[3] = {0, 2, 4};
-    for (int ph = 0; ph < 3; ++ph) {
-        float ms = 0.f;
-        SPUMA_CUDA(cudaEventElapsedTime(&ms, m->tev[g][from[ph]], m->tev[g][from[ph] + 1]));
-        m->stats.phase_ms[ph] += ms;
-        m->stats.phase_count[ph] += 1;
-    }
+    for (int k = 0; k < kTimedSlots && k < executed && 6 * k + 5 < (int)m->tev[g].size(); ++k)
+        for (int ph = 0; ph < 3; ++ph) {
+            float ms = 0.f;
+            SPUMA_CUDA(cudaEventElapsedTime(&ms, m->tev[g][6 * k + from[ph]], m->tev[g][6 * k + from[ph] + 1]));
+            m->stats.phase_ms[ph] += ms;
+            m->stats.phase_count[ph] += 1;
+        }
     return SPUMA_OK;
 }
 

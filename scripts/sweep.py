@@ -7,7 +7,8 @@
   C5  oversubscription sweep: cube n^3, n = 100/126/159/200/252/318 (1M..32M cells)
 
 For each: cells*iter/s of the solve (CUDA events around spuma_pcg_solve), effective GB/s of
-the iteration (SURVEY §8(d) bytes 112N + 16F per iteration), the Amul's achieved GB/s from
+the iteration (the algorithmic bytes of the layout run: SURVEY §8(d) 112N + 16F per iteration,
+or 136N on a lattice numbering with K = 3), the Amul's achieved GB/s from
 libspuma's per-launch events, fraction of MEASURED_PEAKS hbm_gbs.  One JSON line per case.
 usage: python scripts/sweep.py [C1] [C2] [C4] [C5] [--c5 100,126,...]
 """
@@ -60,7 +61,11 @@ def run_case(name, mesh, gamma, b, ref=0, renumber=False, ctl=(1e-6, 0.0, 5000, 
     st = h.get_stats()
     perf, t_asm, t_sol = min(runs, key=lambda r: r[2])
     n_it = perf["n_iterations"]
-    B_it = 112 * N + 16 * F
+    # algorithmic bytes of the layout the hot loop ran: lattice slots 24N + 8KN per
+    # Amul, else SURVEY §8(d) 24N + 16F; the iteration adds 88N (update 56N + direction 32N)
+    K = len(P.spuma.host_lattice_offsets(N, mesh.owner, mesh.neighbour)) if st["amul_variant"] in (12, 13) else 0
+    B_A = 24 * N + 8 * K * N if K else 24 * N + 16 * F
+    B_it = B_A + 88 * N
     amul_ms = st["phase_ms"][1] / max(st["phase_count"][1], 1)
     out = {"case": name, "cells": N, "faces": F, "renumber": renumber, "iterations": n_it,
            "converged": perf["converged"], "final_residual": perf["final_residual"],
@@ -69,8 +74,9 @@ def run_case(name, mesh, gamma, b, ref=0, renumber=False, ctl=(1e-6, 0.0, 5000, 
            "iteration_GBps_incl_setup": B_it * n_it / t_sol / 1e9,
            "iteration_frac_of_measured_peak": B_it * n_it / t_sol / 1e9 / PEAK,
            "amul_us": 1e3 * amul_ms,
-           "amul_alg_GBps": (24 * N + 16 * F) / (amul_ms / 1e3) / 1e9 if amul_ms else None,
-           "amul_frac_of_measured_peak": (24 * N + 16 * F) / (amul_ms / 1e3) / 1e9 / PEAK if amul_ms else None,
+           "amul_variant": st["amul_variant"], "amul_bytes": B_A, "iteration_bytes": B_it,
+           "amul_alg_GBps": B_A / (amul_ms / 1e3) / 1e9 if amul_ms else None,
+           "amul_frac_of_measured_peak": B_A / (amul_ms / 1e3) / 1e9 / PEAK if amul_ms else None,
            "assembly_alg_GBps": (56 * F + 24 * N) / t_asm / 1e9,
            "peak_GBps": PEAK}
     if extra:
