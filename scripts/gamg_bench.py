@@ -50,6 +50,9 @@ def run(name, m, gamma, tol, rel_tol=0.0, reps=3, params=None):
     if os.environ.get("GAMG_TAIL") is not None:  # A/B: single-CTA tail threshold (0 = off)
         h.set_option(P.spuma.OPT_GAMG_TAIL_CELLS, int(os.environ["GAMG_TAIL"]))
         name += f" [tail {os.environ['GAMG_TAIL']}]"
+    if os.environ.get("AMUL_VARIANT") is not None:  # A/B: the layout of the level-0 rows (12 lattice, 10 ELL)
+        h.set_option(P.spuma.OPT_AMUL_VARIANT, int(os.environ["AMUL_VARIANT"]))
+        name += f" [amul variant {os.environ['AMUL_VARIANT']}]"
     if os.environ.get("GAMG_PDL") == "0":  # A/B: plain launches
         h.set_option(P.spuma.OPT_PDL, 0)
         name += " [PDL off]"
