@@ -775,8 +775,6 @@ spuma_status gamg_ensure(spuma_mesh m, const spuma_gamg_params& gp)
             L.b = m->ws.rA;
             L.ell = (m->d_upper_s && m->d_sell_n && m->sell_wn >= 0 && m->sell_wn <= 3 && m->sell_wo >= 0 &&
                      m->sell_wo <= 3) ? 1 : 0;
-            // a lattice numbering: level-0 rows over the lattice slots (the hot Amul's layout)
-            L.lat = (m->d_upper_d && m->lat_K > 0 && (m->amul_variant == 12 || m->amul_variant == 13)) ? 1 : 0;
             if (!L.ell && m->gamg_csr && m->F > 0) {  // irregular fine mesh: CSR rows, values per solve
                 std::vector<int> rp(n + 1, 0), col(2 * (size_t)m->F), pu(m->F), pl(m->F);
                 int k = 0;
@@ -2211,10 +2209,7 @@ spuma_status spuma_set_option(spuma_mesh m, int option, int value)
         return SPUMA_OK;
     case SPUMA_OPT_AMUL_VARIANT:
         if (value < 0 || value > 13) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "amul variant must be 0..13");
-        if (value != m->amul_variant) {
-            destroy_graphs(m);
-            gamg_release(m);  // GAMG's level-0 rows follow the layout (rebuilt at the next solve)
-        }
+        if (value != m->amul_variant) destroy_graphs(m);
         m->amul_variant = value;
         return SPUMA_OK;
     default: return set_error(SPUMA_ERR_INVALID_ARGUMENT, "unknown option");
@@ -2440,10 +2435,7 @@ spuma_status spuma_gamg_solve(spuma_mesh m, const spuma_scalar* diag, const spum
         m->stats.kernel_launches += 1;
     }
     for (int l = 0; l + 1 < nl; ++l) launch_gamg_agg(s, G->lv[l], G->lv[l + 1], m->ws.ptrs);
-    if (G->lv[0].lat) {  // level 0 rows over the lattice slots: this call's coefficients into them
-        launch_lattice_coeffs(s, G->lv[0].a, P.upper);
-        m->stats.kernel_launches += 1;
-    } else if (G->lv[0].ell) {  // level 0 rows over ELL: this call's coefficients in owner-slot order
+    if (G->lv[0].ell) {  // level 0 rows over ELL: this call's coefficients in owner-slot order
         launch_ell_coeffs(s, G->lv[0].a, P.upper, m->d_upper_s);
         m->stats.kernel_launches += 1;
     }

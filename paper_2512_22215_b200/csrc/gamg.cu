@@ -67,42 +67,6 @@ __device__ __forceinline__ double row_ax_ell(const MeshArgs& a, int c, const dou
     return s;
 }
 
-// The same row over the lattice slots of a structured numbering (level 0; kernels.cu variant 12,
-// DESIGN.md §5): slot t of row c = face (c, c + D[t]) at upper_d[t S + c], the neighbour-side face
-// (c - D[t], c) = slot t of row c - D[t]; absent slots (NaN sentinel) skipped.  Same order as
-// row_ax (neighbour side by ascending owner, then owner side by ascending neighbour): bitwise.
-template <class X>
-__device__ __forceinline__ double row_ax_lat(const MeshArgs& a, int c, const double* __restrict__ diag, const X& x)
-{
-    const int N = a.N, K = a.lat_K;
-    const long long S = a.lat_S;
-    double un[3], uo[3], xn[3], xo[3];
-    bool on[3];
-#pragma unroll
-    for (int t = 0; t < 3; ++t) {
-        if (t < K) {
-            const int D = a.lat_D[t], o = c - D;
-            on[t] = o >= 0;
-            un[t] = __ldg(a.upper_d + t * S + (o >= 0 ? o : c));
-            uo[t] = __ldg(a.upper_d + t * S + c);
-            xn[t] = x(o >= 0 ? o : c);
-            xo[t] = x(min(c + D, N - 1));
-        } else {
-            on[t] = false;
-            uo[t] = __longlong_as_double((long long)kLatAbsent);
-            un[t] = xn[t] = xo[t] = 0.0;
-        }
-    }
-    double s = diag[c] * x(c);
-#pragma unroll
-    for (int t = 2; t >= 0; --t)
-        if (on[t] && (unsigned long long)__double_as_longlong(un[t]) != kLatAbsent) s = s + un[t] * xn[t];
-#pragma unroll
-    for (int t = 0; t < 3; ++t)
-        if ((unsigned long long)__double_as_longlong(uo[t]) != kLatAbsent) s = s + uo[t] * xo[t];
-    return s;
-}
-
 // The same row over a per-level CSR copy of the off-diagonal coefficients (coarse generic levels):
 // row c's neighbour-side faces in losort order, then its owner-side faces in face order -- the
 // order of row_ax -- as one contiguous (column, value) run; values written by k_gamg_agg.
@@ -135,8 +99,7 @@ __device__ __forceinline__ double rowA(const GLevel& L, int c, const double* __r
                                        const double* __restrict__ u, const double* __restrict__ ic, const X& x)
 {
     double s;
-    if constexpr (LAY == 3) s = row_ax_lat(L.a, c, d, x);
-    else if constexpr (LAY == 1) s = row_ax_ell(L.a, c, d, x);
+    if constexpr (LAY == 1) s = row_ax_ell(L.a, c, d, x);
     else if constexpr (LAY == 2) s = row_ax_csr(L, c, d, x);
     else s = row_ax(L.a, c, d, u, x, L.upperLo);
     return add_if<IF>(L, ic, c, s);
@@ -659,11 +622,8 @@ void launch_gamg_agg(cudaStream_t s, const GLevel& fine, const GLevel& coarse, c
 #define GAMG_DISPATCH(K, L, ...)                                                  \
     do {                                                                          \
         const bool if_ = (L).a.ifStart != nullptr;                                \
-        const int lay_ = (L).lat ? 3 : ((L).ell ? 1 : ((L).cval ? 2 : 0));        \
-        if (lay_ == 3) {                                                          \
-            if (if_) glaunch(K<3, true>, (L).grid, s, __VA_ARGS__);               \
-            else glaunch(K<3, false>, (L).grid, s, __VA_ARGS__);                  \
-        } else if (lay_ == 1) {                                                   \
+        const int lay_ = (L).ell ? 1 : ((L).cval ? 2 : 0);                        \
+        if (lay_ == 1) {                                                          \
             if (if_) glaunch(K<1, true>, (L).grid, s, __VA_ARGS__);               \
             else glaunch(K<1, false>, (L).grid, s, __VA_ARGS__);                  \
         } else if (lay_ == 2) {                                                   \

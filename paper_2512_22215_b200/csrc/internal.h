@@ -103,7 +103,6 @@ struct GLevel {
     int nc, ncf;                  // next level's size
     int grid;                     // CTAs of this level's cell kernels (fixed: deterministic reductions)
     int ell;                      // 1: rows over the ELL layout (a.sell_*, a.upper_s; level 0 of a uniform mesh)
-    int lat;                      // 1: level-0 rows over the lattice slots (a.upper_d, Amul variant 12's layout)
     double* upperLo;              // coarse generic levels: coefficients in losort order (nullptr: gather)
     const int* losortPos;         //   face -> its losort position (k_gamg_agg writes upperLo through it)
     const int *crp, *ccol;        // coarse generic levels: CSR rows of the off-diagonal entries (row_ax order)

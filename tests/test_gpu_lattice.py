@@ -125,32 +125,3 @@ def test_lattice_pcg_full_size_8M_fixed_iterations():
     assert err <= 1e-9, err
     h.free()
 
-
-@pytest.mark.parametrize("name,make", [("cube24", lambda: gen.cube(24)), ("fixed-value-perturbed20", lambda: _fixed_value_cube(20))])
-def test_gamg_level0_lattice_rows_bitwise_ell_rows(name, make):
-    """GAMG's level-0 kernels (smoother, scale, restriction) over the lattice slots give bitwise
-    the V-cycles of the ELL rows (same row values, same reduction shapes), and match the oracle."""
-    m = make()
-    g, b = gen.gamma_lognormal(m), gen.rhs(m)
-    has_fixed = any(p.value is not None for p in m.patches)
-    ref = -1 if has_fixed else 0
-    res = []
-    for variant in (12, 10):
-        h = P.Mesh.from_mesh(m)
-        h.set_option(P.spuma.OPT_AMUL_VARIANT, variant)
-        psi, perf = gpu_gamg(h, m, g, b, ref, (1e-9, 0.0, 200, 0))
-        res.append((psi, perf))
-        h.free()
-    assert res[0][1] == res[1][1]
-    assert np.array_equal(res[0][0].view(np.uint64), res[1][0].view(np.uint64))
-    s = O.assemble(m, g, ref, 0.0, b)
-    _, po = O.gamg(m, s, None, O.controls(1e-9, 0.0, 200, 0))
-    assert abs(res[0][1]["n_iterations"] - po["n_iterations"]) <= 2, (res[0][1], po)
-
-
-def gpu_gamg(h, m, g, b, ref, ctl):
-    from gpu_helpers import gpu_assemble
-    diag, upper, src, _ = gpu_assemble(h, m, g, ref, 0.0, b)
-    psi = torch.zeros(m.n_cells, **F64)
-    perf = h.gamg_solve(diag, upper, None, src, psi, *ctl)
-    return psi.cpu().numpy(), perf
