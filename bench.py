@@ -187,6 +187,39 @@ def cpu_baseline(n, iters):
                       f"(minIter = maxIter = {iters}), single thread, {t:.1f} s"}
 
 
+def _throughput_worker(a):
+    n_local, iters, core = a
+    try:
+        os.sched_setaffinity(0, {core})
+    except (AttributeError, OSError):
+        pass
+    v, t = oracle_sample(n_local, iters)
+    return n_local ** 3, iters, t
+
+
+def cpu_throughput(n, iters, gpu_value=None):
+    """The cpu_baseline leg in host-throughput mode: C concurrent single-threaded
+    oracle processes (C = the host cores), each on an independent cube of ~n^3/C cells -- the
+    partition an MPI CPU run of the workload would use -- each running assembly + setup + `iters`
+    PCG iterations; the aggregate cells*iter/s and the paper's COE analogue (Eq. 1)."""
+    from multiprocessing import get_context
+    import oracle
+    oracle.build()
+    cores = sorted(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else list(range(os.cpu_count()))
+    C = len(cores)
+    n_local = max(2, round((n ** 3 / C) ** (1 / 3)))
+    with get_context("spawn").Pool(C) as pool:
+        res = pool.map(_throughput_worker, [(n_local, iters, cores[i]) for i in range(C)])
+    agg = sum(c * k / t for c, k, t in res)
+    out = {"mode": "oracle throughput", "kind": "oracle", "cores": C, "processes": C,
+           "cells_per_process": n_local ** 3, "iterations": iters, "value": agg, "unit": UNIT,
+           "per_core": agg / C, "seconds": max(t for _, _, t in res)}
+    if gpu_value:
+        out["coe_cores_per_gpu"] = gpu_value / (agg / C)
+        out["gpu_over_all_host_cores"] = gpu_value / agg
+    return out
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
@@ -416,7 +449,14 @@ def main():
     ap.add_argument("--alt-sweep", type=int, default=None, help="A/B only (default: the library's)")
     ap.add_argument("--defer-psi", type=int, default=None, help="A/B only (default: the library's)")
     ap.add_argument("--l2-persist", type=int, default=None, help="A/B only (default: the library's)")
+    ap.add_argument("--cpu-throughput", action="store_true",
+                    help="only the cpu_baseline leg in host-throughput mode (every host core), one JSON line")
+    ap.add_argument("--gpu-value", type=float, default=None, help="--cpu-throughput: GPU value for the COE analogue")
+    ap.add_argument("--throughput-iters", type=int, default=40, help="--cpu-throughput: PCG iterations per process")
     args = ap.parse_args()
+    if args.cpu_throughput:
+        print(json.dumps(cpu_throughput(args.n, args.throughput_iters, args.gpu_value)), flush=True)
+        return
     rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
     if args.impl == "reference":
         run_reference(args, rank, world)

@@ -492,7 +492,11 @@ typedef enum {
     /* peer transport: how long a kernel polls for a neighbour's flag before it gives up, in
      * milliseconds (approximate: SM clocks at 2 GHz); default 20000.  The call that saw the
      * timeout returns SPUMA_ERR_STATE. */
-    SPUMA_OPT_PEER_POLL_MS = 10
+    SPUMA_OPT_PEER_POLL_MS = 10,
+    /* the single-CTA small solve (SPUMA_OPT_SMALL_SOLVE_MAX_CELLS) with the matrix, addressing,
+     * vectors and scalars staged in shared memory when they fit (about 1700 cells of a 3-D hex
+     * mesh); 1 = on (default), 0 = global memory.  Bitwise the same iterates. */
+    SPUMA_OPT_SMALL_SMEM = 11
 } spuma_option;
 spuma_status spuma_set_option(spuma_mesh m, int option, int value);
 

@@ -1845,7 +1845,7 @@ spuma_status spuma_pcg_solve(spuma_mesh m, const spuma_scalar* diag, const spuma
 
     // ---- small meshes: the whole solve in one single-CTA launch (latency path)
     if (m->n_ranks == 1 && m->N <= m->small_max_cells && !m->timing) {
-        launch_pcg_single(s, mesh_args(m), m->ws);
+        if (!(m->small_smem && launch_pcg_single_smem(s, mesh_args(m), m->ws))) launch_pcg_single(s, mesh_args(m), m->ws);
         m->stats.kernel_launches += 2;
         DevScal fs;
         SPUMA_CUDA(cudaMemcpyAsync(m->h_scal, m->ws.scal, sizeof(DevScal), cudaMemcpyDeviceToHost, s));
@@ -2202,6 +2202,10 @@ spuma_status spuma_set_option(spuma_mesh m, int option, int value)
             }
         }
         g_use_pdl = value != 0;
+        return SPUMA_OK;
+    case SPUMA_OPT_SMALL_SMEM:
+        if (value < 0 || value > 1) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "small_smem is 0 or 1");
+        m->small_smem = value != 0;
         return SPUMA_OK;
     case SPUMA_OPT_SMALL_SOLVE_MAX_CELLS:
         if (value < 0) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "small-solve threshold must be >= 0");

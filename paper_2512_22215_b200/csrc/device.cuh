@@ -200,15 +200,15 @@ __device__ __forceinline__ void cta_sum_1024(double (&v)[NV])
     __syncthreads();
 }
 
-// The whole PCG solve (A6-A12) by one CTA of kSmallThreads threads (small meshes, GAMG coarsest level).
-static __device__ void pcg_single_body(const MeshArgs& a, const Workspace& w)
+// The whole PCG solve (A6-A12) by one CTA of up to kSmallThreads threads (small meshes, GAMG coarsest
+// level); rows strided by the block size (the small-solve launchers size it to the mesh).
+// p / sc / w's vectors / a's addressing may live in global or shared memory (k_pcg_single_smem).
+static __device__ void pcg_single_body(const MeshArgs& a, const Workspace& w, const DevPtrs& p, DevScal* sc)
 {
-    const DevPtrs p = *w.ptrs;
-    DevScal* sc = w.scal;
     const int N = a.N, t = threadIdx.x;
     {  // A6: wA = A psi, sumA, gAverage(psi)
         double v[2] = {0.0, 0.0};
-        for (int c = t; c < N; c += kSmallThreads) {
+        for (int c = t; c < N; c += (int)blockDim.x) {
             double rs;
             w.wA[c] = amul_row(a, c, p.diag, p.upper, p.iface, p.psi, w.xr, &rs);
             w.sumA[c] = rs;
@@ -222,7 +222,7 @@ static __device__ void pcg_single_body(const MeshArgs& a, const Workspace& w)
     {  // A6: residual, normFactor, rD, first wArA
         const double xbar = sc->xbar;
         double v[3] = {0.0, 0.0, 0.0};
-        for (int c = t; c < N; c += kSmallThreads) {
+        for (int c = t; c < N; c += (int)blockDim.x) {
             const double b = p.source[c], wa = w.wA[c];
             const double r = b - wa;
             const double xref = w.sumA[c] * xbar;
@@ -240,11 +240,11 @@ static __device__ void pcg_single_body(const MeshArgs& a, const Workspace& w)
     while (!sc->done) {
         const bool first = sc->n == 0;
         const double beta = sc->beta;
-        for (int c = t; c < N; c += kSmallThreads)  // A11
+        for (int c = t; c < N; c += (int)blockDim.x)  // A11
             w.pA[c] = first ? w.rD[c] * w.rA[c] : w.rD[c] * w.rA[c] + beta * w.pA[c];
         __syncthreads();
         double v[2] = {0.0, 0.0};
-        for (int c = t; c < N; c += kSmallThreads) {  // A7
+        for (int c = t; c < N; c += (int)blockDim.x) {  // A7
             const double y = amul_row(a, c, p.diag, p.upper, p.iface, w.pA, w.xr, nullptr);
             w.wA[c] = y;
             v[0] += y * w.pA[c];
@@ -255,7 +255,7 @@ static __device__ void pcg_single_body(const MeshArgs& a, const Workspace& w)
         if (sc->done) break;
         const double alpha = sc->alpha;
         v[0] = v[1] = 0.0;
-        for (int c = t; c < N; c += kSmallThreads) {  // A9
+        for (int c = t; c < N; c += (int)blockDim.x) {  // A9
             p.psi[c] = p.psi[c] + alpha * w.pA[c];
             const double r = w.rA[c] - alpha * w.wA[c];
             w.rA[c] = r;
@@ -268,4 +268,12 @@ static __device__ void pcg_single_body(const MeshArgs& a, const Workspace& w)
     }
 }
 
+}  // namespace spuma
+
+namespace spuma {
+static __device__ void pcg_single_body(const MeshArgs& a, const Workspace& w)
+{
+    const DevPtrs p = *w.ptrs;
+    pcg_single_body(a, w, p, w.scal);
+}
 }  // namespace spuma

@@ -238,6 +238,7 @@ struct spuma_mesh_s {
     // captured iteration batches (ping-pong) and timing events
     int batch = 16;
     int small_max_cells = 8192;  // single-CTA solve at or below this many cells (1 rank)
+    bool small_smem = true;      // ... staged in shared memory when it fits (SPUMA_OPT_SMALL_SMEM)
     int amul_variant = 12;  // lattice slots (falls back to 10 -> 6 -> 5 off lattice / uniform meshes)
     int defer_psi = 2;      // 0: psi += alpha pA every iteration; 1: pairs in k_update; 2: pairs in k_direction  // psi += alpha pA applied every second iteration (same rounding, fewer bytes)  // ELL + coefficient copy (falls back to 6 -> 5 when the mesh is not uniform)
     bool timing = false;
@@ -378,6 +379,8 @@ void launch_amul_dot_dir(cudaStream_t s, const MeshArgs& a, const Workspace& w, 
 void launch_finalize(cudaStream_t s, int stage, const double* gathered, int n_ranks, const Workspace& w);
 void launch_scal_init(cudaStream_t s, const Workspace& w, const spuma_solver_controls& c, int n_ranks);
 void launch_pcg_single(cudaStream_t s, const MeshArgs& a, const Workspace& w);  // whole solve, 1 CTA
+// the same with everything in shared memory; false (nothing launched) if the mesh does not fit
+bool launch_pcg_single_smem(cudaStream_t s, const MeshArgs& a, const Workspace& w);
 int occupancy_grid(int N, int* grid_faces, int F);
 // preconditioned solvers (precond.cu)
 int pc_grid(int n);

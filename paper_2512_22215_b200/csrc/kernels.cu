@@ -663,9 +663,104 @@ __global__ void __launch_bounds__(kThreads) k_update(int N, Workspace w, int fin
 
 __global__ void __launch_bounds__(kSmallThreads) k_pcg_single(MeshArgs a, Workspace w) { pcg_single_body(a, w); }
 
+// threads of the single-CTA solves: one per cell up to kSmallThreads (fewer warps at the CTA barriers
+// of a small mesh); both launchers use the same count, so their reductions have the same shape
+static int small_threads(int N) { return N >= kSmallThreads ? kSmallThreads : (N < 32 ? 32 : (N + 31) / 32 * 32); }
+
 void launch_pcg_single(cudaStream_t s, const MeshArgs& a, const Workspace& w)
 {
-    k_pcg_single<<<1, kSmallThreads, 0, s>>>(a, w);
+    k_pcg_single<<<1, small_threads(a.N), 0, s>>>(a, w);
+}
+
+// The single-CTA solve with everything in shared memory (BASELINE config 1, the 400-cell cavity:
+// a latency problem).  The matrix (diag, upper), source, psi, the row addressing and the PCG
+// vectors and scalars are staged into shared memory once, the whole solve runs there (every
+// gather an SMEM load, every finalisation an SMEM store), and psi / the scalars are written back
+// at the end.  The same row order and the same reduction tree as k_pcg_single: bitwise the same
+// iterates.  Layout: doubles diag, upper, source, psi, wA, rA, rD, pA, sumA, then the DevScal,
+// then ints ownerStart, losortStart [N+1], losort, ownerLo, neighbour [F].
+size_t pcg_single_smem_bytes(int N, int F)
+{
+    const size_t dbl = sizeof(double) * (8 * (size_t)N + (size_t)F) + sizeof(DevScal);
+    return ((dbl + 15) & ~(size_t)15) + sizeof(int) * (2 * ((size_t)N + 1) + 3 * (size_t)F);
+}
+
+__global__ void __launch_bounds__(kSmallThreads) k_pcg_single_smem(MeshArgs a, Workspace w)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int N = a.N, F = a.F, t = threadIdx.x;
+    double* d = reinterpret_cast<double*>(smem);
+    double* up = d + N;
+    double* src = up + F;
+    double* psi = src + N;
+    Workspace ws = w;
+    ws.wA = psi + N;
+    ws.rA = ws.wA + N;
+    ws.rD = ws.rA + N;
+    ws.pA = ws.rD + N;
+    ws.sumA = ws.pA + N;
+    DevScal* sc = reinterpret_cast<DevScal*>(ws.sumA + N);
+    const size_t dbl = sizeof(double) * (8 * (size_t)N + (size_t)F) + sizeof(DevScal);
+    int* os = reinterpret_cast<int*>(smem + ((dbl + 15) & ~(size_t)15));
+    int* ls = os + N + 1;
+    int* lo = ls + N + 1;
+    int* ol = lo + F;
+    int* nb = ol + F;
+    const DevPtrs g = *w.ptrs;
+    for (int i = t; i < N; i += blockDim.x) {
+        d[i] = g.diag[i];
+        src[i] = g.source[i];
+        psi[i] = g.psi[i];
+    }
+    for (int i = t; i < F; i += blockDim.x) {
+        up[i] = g.upper[i];
+        lo[i] = a.losort[i];
+        ol[i] = a.ownerLo[i];
+        nb[i] = a.neighbour[i];
+    }
+    for (int i = t; i <= N; i += blockDim.x) {
+        os[i] = a.ownerStart[i];
+        ls[i] = a.losortStart[i];
+    }
+    if (t == 0) *sc = *w.scal;
+    __syncthreads();
+    MeshArgs as = a;
+    as.ownerStart = os;
+    as.losortStart = ls;
+    as.losort = lo;
+    as.ownerLo = ol;
+    as.neighbour = nb;
+    as.ifStart = nullptr;
+    as.ifIdx = nullptr;
+    as.ifMask = nullptr;
+    const DevPtrs ps{d, up, nullptr, src, psi};
+    pcg_single_body(as, ws, ps, sc);
+    __syncthreads();
+    for (int i = t; i < N; i += blockDim.x) g.psi[i] = psi[i];
+    if (t == 0) *w.scal = *sc;
+}
+
+bool launch_pcg_single_smem(cudaStream_t s, const MeshArgs& a, const Workspace& w)
+{
+    const size_t bytes = pcg_single_smem_bytes(a.N, a.F);
+    static int max_dyn = -1;  // opt-in shared memory per block minus the kernel's static shared memory
+    if (max_dyn < 0) {
+        int dev = 0, optin = 0;
+        cudaFuncAttributes fa{};
+        if (cudaGetDevice(&dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess ||
+            cudaFuncGetAttributes(&fa, k_pcg_single_smem) != cudaSuccess ||
+            cudaFuncSetAttribute(k_pcg_single_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 optin - (int)fa.sharedSizeBytes) != cudaSuccess) {
+            cudaGetLastError();  // not sticky: fall back to the global-memory kernel
+            max_dyn = 0;
+        } else {
+            max_dyn = optin - (int)fa.sharedSizeBytes;
+        }
+    }
+    if (a.ifStart || bytes > (size_t)max_dyn) return false;
+    k_pcg_single_smem<<<1, small_threads(a.N), bytes, s>>>(a, w);
+    return true;
 }
 
 // ---------------------------------------------------------------------------

@@ -7,7 +7,7 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smok
 timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
 timeout 600 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
 GPUV=$(python -c "import json; print(json.load(open('gpurun_out/bench.json'))['value'])" 2>/dev/null)
-timeout 600 python scripts/cpu_throughput.py --n 200 --iters 40 --gpu ${GPUV:-4e10} > gpurun_out/cpu_throughput.json 2>&1
+timeout 600 python bench.py --cpu-throughput --gpu-value ${GPUV:-5e10} > gpurun_out/cpu_throughput.json 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv \
     python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_amul_dot -s 30 -c 2 -o gpurun_out/prof_amul \

@@ -182,3 +182,24 @@ def test_peer_poll_timeout_returns_error_state():
                 p.terminate()
     bad = {r: m for r, m in out.items() if m != "ok"}
     assert not bad and len(out) == 2, bad or out
+
+
+@pytest.mark.parametrize("name,make", [("cavity20", lambda: gen.cavity2d(20)), ("cube11", lambda: gen.cube(11)),
+                                       ("perm-perturbed9", lambda: gen.permute(gen.perturbed(9, 0.3), seed=4)),
+                                       ("cube14-too-big", lambda: gen.cube(14))])
+def test_small_solve_shared_memory_is_bitwise_global(name, make):
+    """SPUMA_OPT_SMALL_SMEM: the single-CTA solve with everything staged in shared memory gives
+    bitwise the iterates of the global-memory single-CTA solve (meshes that do not fit fall back)."""
+    m = make()
+    g, b = gen.gamma_lognormal(m), gen.rhs(m)
+    out = []
+    for smem in (0, 1):
+        h = P.Mesh.from_mesh(m)
+        h.set_option(P.spuma.OPT_SMALL_SMEM, smem)
+        diag, upper, src, _ = gpu_assemble(h, m, g, 0, 0.0, b)
+        psi = torch.zeros(m.n_cells, **F64)
+        perf = h.pcg_solve(diag, upper, None, src, psi, 1e-8, 0.0, 5000, 0)
+        out.append((psi.cpu().numpy(), perf))
+        h.free()
+    assert out[0][1] == out[1][1]
+    assert np.array_equal(out[0][0].view(np.uint64), out[1][0].view(np.uint64))

@@ -1,9 +1,9 @@
 """Mutation sanity check for the oracle pins: each plausible mistake (dropped term, wrong sign,
 wrong index, transposed operand) injected into oracle.c must fail at least one -m "not gpu" test.
-Restores oracle.c at the end.  Run: python scripts/oracle_mutation_check.py"""
+Restores oracle.c at the end.  Run: python tests/tools/oracle_mutation_check.py"""
 import subprocess, sys
 import os
-os.chdir(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+os.chdir(os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 src = open('oracle/oracle.c').read()
 muts = [
  ("diag[neighbour[f]] -= upper[f];", "/*dropped*/"),
