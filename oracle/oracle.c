@@ -34,7 +34,9 @@
  * decomposition invariance, A-norm monotonicity.
  * Parity unpinned: the normFactor formula (Q1) and the convergence/loop
  * semantics (Q2, Q3) are pinned only by special cases (init residual = 1 for
- * psi0 = 0; exact start; minIter), not by any number the paper prints -- the
+ * psi0 = 0, and for a constant psi0 on Neumann and Dirichlet matrices -- the
+ * latter separating the xRef = sumA mean(psi) term from the reference-free
+ * readings; exact start; minIter), not by any number the paper prints -- the
  * paper prints no PCG iteration count, residual or matrix value for this path.
  */
 #include <math.h>

@@ -161,6 +161,29 @@ def test_normfactor_for_constant_start_on_neumann_matrix():
     assert perf["initial_residual"] == 1.0
 
 
+def test_normfactor_reference_term_for_constant_start_on_dirichlet_matrix():
+    """Q1's xRef = sumA * mean(psi) term: with fixedValue walls the row sums are not zero, and for
+    psi0 = c (constant) A psi0 = c sumA, so |A psi - xRef| vanishes and the initial residual is
+    sum|b - c sumA| / sum|b - c sumA| = 1 whatever b is.  With b close to c sumA a normalisation
+    without the reference term (SPEC S:395's sum(|b - A xbar| + |A xbar|), or sum(|A psi| + |b|))
+    gives a value far below 1."""
+    m = dirichlet_box(5, 4, 3)
+    g = gen.gamma_lognormal(m)
+    s0 = O.assemble(m, g, -1, source=np.zeros(m.n_cells))
+    A = dense_ldu(m.n_cells, m.owner, m.neighbour, s0.diag, s0.upper)
+    rowsum = A.sum(axis=1)
+    assert np.count_nonzero(np.abs(rowsum) > 1e-3) >= m.n_cells // 2  # the wall rows: sumA != 0
+    c = 7.0
+    b = c * rowsum + 1e-3 * np.linspace(-1.0, 2.0, m.n_cells)
+    s = O.assemble(m, g, -1, source=b)
+    _, perf = O.pcg(m, s, np.full(m.n_cells, c), O.controls(1e-12, 0.0, 1, 1))
+    assert perf["initial_residual"] == pytest.approx(1.0, rel=1e-9)
+    # the alternative reading, written out with the dense matrix, is far from 1 on this case
+    Ap = A @ np.full(m.n_cells, c)
+    alt = np.abs(s.source - Ap).sum() / (np.abs(Ap).sum() + np.abs(s.source).sum())
+    assert alt < 1e-2
+
+
 # --------------------------------------------------------------- P9 A-norm monotonicity
 def test_p9_error_a_norm_non_increasing():
     m = small_random_mesh(seed=7)
