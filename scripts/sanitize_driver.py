@@ -1,8 +1,9 @@
 #!/usr/bin/env python
 """Small-mesh driver of every libspuma device path, run under compute-sanitizer (memcheck,
 racecheck, synccheck, initcheck) by scripts/gpu_sanitize.sh (race detection /
-sanitizers).  Exercises: mesh creation (natural + RCM), assembly with gamma, all Amul variants,
-PCG (single-CTA path and the captured-batch path), the pEqn steps (surfaceIntegrate, flux,
+sanitizers).  Exercises: mesh creation (natural + RCM), assembly with gamma, all Amul variants
+(incl. the lattice slots), PCG (single-CTA path in shared and global memory, the captured-batch
+path with the lattice / ELL rows and every psi deferral mode), the pEqn steps (surfaceIntegrate, flux,
 non-orthogonal correction), GAMG (Richardson + two-stage Gauss-Seidel), PCG with DIC / DILU /
 aDILU, PBiCG, LDU -> CSR values.  Prints one line per step; exits non-zero on any error."""
 import os
@@ -40,13 +41,17 @@ for mname, mesh, ren in (("perturbed8", gen.perturbed(8, 0.2), False), ("permute
         h.set_option(S.OPT_AMUL_VARIANT, v)
         y = torch.zeros(N, **f64)
         h.amul(diag, upper, None, x, y)
-    h.set_option(S.OPT_AMUL_VARIANT, 10)
     step(f"{mname} amul variants")
-    for thr in (8192, 0):
+    for thr, smem in ((8192, 1), (8192, 0), (0, 1)):
         h.set_option(S.OPT_SMALL_SOLVE_MAX_CELLS, thr)
-        psi = torch.zeros(N, **f64)
-        h.pcg_solve(diag, upper, None, src.clone(), psi, 1e-8, 0.0, 2000, 0)
-    step(f"{mname} pcg (single-CTA + batches)")
+        h.set_option(S.OPT_SMALL_SMEM, smem)
+        for variant, defer in ((12, 2), (10, 1), (10, 0)):  # lattice rows + psi pairs in the direction, ...
+            h.set_option(S.OPT_AMUL_VARIANT, variant)
+            h.set_option(S.OPT_DEFER_PSI, defer)
+            psi = torch.zeros(N, **f64)
+            h.pcg_solve(diag, upper, None, src.clone(), psi, 1e-8, 0.0, 2000, 0)
+    h.set_option(S.OPT_SMALL_SOLVE_MAX_CELLS, 8192)
+    step(f"{mname} pcg (single-CTA in shared / global memory + batches; lattice / ELL rows; psi deferral modes)")
     V = d(mesh.V)
     out = torch.zeros(N, **f64)
     phi = d(np.sin(np.arange(F) * 0.1))
