@@ -361,6 +361,11 @@ spuma_status allgather4(spuma_mesh m, const double* in, double* out, cudaStream_
 spuma_status reduce_finalize_ws(spuma_mesh m, const Workspace& w, int stage, cudaStream_t s)
 {
     double* gathered = w.part;  // free after the reduction kernel finished
+    if (m->peer) {  // the all-gather kernel finalises too
+        launch_peer_allgather4(s, m->pg, w.scal->rank_part, gathered, m->pst, stage, &w);
+        m->stats.kernel_launches += 1;
+        return SPUMA_OK;
+    }
     SPUMA_TRY(allgather4(m, w.scal->rank_part, gathered, s));
     launch_finalize(s, stage, gathered, m->n_ranks, w);
     m->stats.kernel_launches += 1;
@@ -1316,10 +1321,21 @@ uint64_t pc_launches(const spuma_preconditioner& pc)
     return 2;
 }
 
+// our kernels per captured iteration: direction, Amul, update; with ranks: the two reduction
+// finalisations (k_finalize after NCCL's all-gather, or the fused peer all-gather + finalise), the
+// halo (fused pack + P2P send and the receive, or the NCCL pack kernel) and the interface rows
+// finished after the overlapped halo (ELL / lattice rows)
 uint64_t launches_per_iteration(spuma_mesh m)
 {
     uint64_t k = 3;
-    if (m->n_ranks > 1) k += 2 + (m->n_iface ? 1 : 0);
+    if (m->n_ranks > 1) {
+        k += 2;
+        if (m->n_iface) {
+            k += m->peer ? (m->px.n_patches ? 2 : 0) : 1;
+            const int rv = resolve_amul_variant(m->amul_variant, mesh_args(m));
+            if (rv >= 6 && rv <= 13) k += 1;
+        }
+    }
     return k;
 }
 

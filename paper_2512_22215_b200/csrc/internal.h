@@ -451,6 +451,8 @@ void launch_gamg_gs2_upd(cudaStream_t s, const GLevel& L, const DevPtrs* P, cons
 // peer-memory transport (peer.cu)
 void launch_peer_exchange(cudaStream_t s, const PeerXfer& d, const double* x, const int* idx, double* recv,
                           const PeerState& st);
-void launch_peer_allgather4(cudaStream_t s, const PeerGather& g, const double* in, double* out, const PeerState& st);
+// stage > 0 with w: also finalise the PCG scalars of w from the gathered block (k_finalize's sums)
+void launch_peer_allgather4(cudaStream_t s, const PeerGather& g, const double* in, double* out, const PeerState& st,
+                            int stage = 0, const Workspace* w = nullptr);
 extern bool g_use_pdl;  // programmatic dependent launch of the hot-loop kernels (process-wide)
 }  // namespace spuma

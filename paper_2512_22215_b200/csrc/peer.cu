@@ -20,6 +20,7 @@
 // SPUMA_OPT_PEER_POLL_MS) sets the handle's error word instead of hanging the GPU; every
 // collective call reads and clears it afterwards (api.cu peer_guard -> SPUMA_ERR_STATE).
 #include "internal.h"
+#include "device.cuh"
 
 namespace spuma {
 namespace {
@@ -101,8 +102,11 @@ __global__ void __launch_bounds__(kThreads) k_peer_recv(PeerXfer d, double* __re
 }
 
 // all-gather of 4 doubles per rank (one CTA): publish to every rank, wait for every rank,
-// copy the rank-ordered block out
-__global__ void k_peer_allgather4(PeerGather g, const double* __restrict__ in, double* __restrict__ out, PeerState st)
+// copy the rank-ordered block out; stage > 0: then finalise the PCG scalars from it exactly as
+// k_finalize does (rank-order sums, finalize(stage)) -- one launch instead of two per reduction.
+// A timed-out gather (error word set) stops the loop (done) instead of finalising stale values.
+__global__ void k_peer_allgather4(PeerGather g, const double* __restrict__ in, double* __restrict__ out, PeerState st,
+                                  int stage, Workspace w)
 {
     __shared__ unsigned long long se;
     __shared__ int ok;
@@ -128,6 +132,19 @@ __global__ void k_peer_allgather4(PeerGather g, const double* __restrict__ in, d
 #pragma unroll
         for (int k = 0; k < 4; ++k) out[4 * t + k] = g.my_part[par][4 * t + k];
     if (t == 0) st.ctr[1] = e;
+    if (stage > 0) {
+        __syncthreads();
+        if (t == 0) {
+            if (!ok) {
+                w.scal->done = 1;
+            } else if (!(stage >= 3 && w.scal->done)) {
+                double v[4] = {0.0, 0.0, 0.0, 0.0};
+                for (int r = 0; r < g.n_ranks; ++r)
+                    for (int i = 0; i < 4; ++i) v[i] += out[4 * r + i];
+                finalize(w.scal, stage, v);
+            }
+        }
+    }
 }
 
 }  // namespace
@@ -145,9 +162,10 @@ void launch_peer_exchange(cudaStream_t s, const PeerXfer& d, const double* x, co
     k_peer_recv<<<grid < 32 ? grid : 32, kThreads, 0, s>>>(d, recv, st);
 }
 
-void launch_peer_allgather4(cudaStream_t s, const PeerGather& g, const double* in, double* out, const PeerState& st)
+void launch_peer_allgather4(cudaStream_t s, const PeerGather& g, const double* in, double* out, const PeerState& st,
+                            int stage, const Workspace* w)
 {
-    k_peer_allgather4<<<1, 32 * ((g.n_ranks + 31) / 32), 0, s>>>(g, in, out, st);
+    k_peer_allgather4<<<1, 32 * ((g.n_ranks + 31) / 32), 0, s>>>(g, in, out, st, w ? stage : 0, w ? *w : Workspace{});
 }
 
 }  // namespace spuma
