@@ -496,7 +496,12 @@ typedef enum {
     /* the single-CTA small solve (SPUMA_OPT_SMALL_SOLVE_MAX_CELLS) with the matrix, addressing,
      * vectors and scalars staged in shared memory when they fit (about 1700 cells of a 3-D hex
      * mesh); 1 = on (default), 0 = global memory.  Bitwise the same iterates. */
-    SPUMA_OPT_SMALL_SMEM = 11
+    SPUMA_OPT_SMALL_SMEM = 11,
+    /* peer transport, PCG loop: the halo stores fused into the direction kernel and the receive
+     * into the interface rows, the rank-partial all-gather + finalisation into the reductions'
+     * last CTA (4 kernels per iteration instead of 7); 1 = on (default), 0 = separate kernels.
+     * Bitwise the same iterates. */
+    SPUMA_OPT_PEER_FUSED = 12
 } spuma_option;
 spuma_status spuma_set_option(spuma_mesh m, int option, int value);
 

@@ -479,6 +479,25 @@ spuma_status enqueue_iteration(spuma_mesh m, cudaStream_t s, std::vector<cudaEve
         m->stats.kernel_launches += 2;
         return SPUMA_OK;
     }
+    if (overlap && m->peer && m->peer_fused && m->px.n_patches > 0) {
+        // peer transport, fused: four kernels per iteration -- the direction stores the interface
+        // values into the neighbours' mailboxes; the Amul's interior rows overlap the transfer;
+        // the interface rows wait for the neighbours' flags, read their mailbox and all-gather the
+        // rank partials of wA.pA (alpha); the update all-gathers its own (beta, convergence)
+        ws.pst = m->pst;
+        if (ev) record(m, *ev, slot * 6 + 0, s);
+        launch_direction(s, m->grid, a, ws, odd, psi_in_dir && !(slot & 1), true);
+        if (ev) record(m, *ev, slot * 6 + 1, s);
+        if (ev) record(m, *ev, slot * 6 + 2, s);
+        launch_amul_dot(s, m->amul_variant, a, ws, false, m->sell_wn, m->sell_wo, true);
+        launch_iface_rows(s, a, ws, m->d_ifRows, m->n_ifRows, true);
+        if (ev) record(m, *ev, slot * 6 + 3, s);
+        if (ev) record(m, *ev, slot * 6 + 4, s);
+        launch_update(s, m->grid, a, ws, 2, psi_mode, odd);
+        if (ev) record(m, *ev, slot * 6 + 5, s);
+        m->stats.kernel_launches += 4;
+        return SPUMA_OK;
+    }
     if (ev) record(m, *ev, slot * 6 + 0, s);
     launch_direction(s, m->grid, a, ws, odd, psi_in_dir && !(slot & 1));
     if (ev) record(m, *ev, slot * 6 + 1, s);
@@ -1329,11 +1348,13 @@ uint64_t launches_per_iteration(spuma_mesh m)
 {
     uint64_t k = 3;
     if (m->n_ranks > 1) {
+        const int rv = resolve_amul_variant(m->amul_variant, mesh_args(m));
+        const bool overlap = m->n_iface && rv >= 6 && rv <= 13;
+        if (overlap && m->peer && m->peer_fused && m->px.n_patches > 0) return 4;  // fused peer loop
         k += 2;
         if (m->n_iface) {
             k += m->peer ? (m->px.n_patches ? 2 : 0) : 1;
-            const int rv = resolve_amul_variant(m->amul_variant, mesh_args(m));
-            if (rv >= 6 && rv <= 13) k += 1;
+            if (overlap) k += 1;
         }
     }
     return k;
@@ -1393,6 +1414,9 @@ void spuma_free(spuma_mesh m)
         if (p) cudaIpcCloseMemHandle(p);
     if (m->d_mail) cudaFree(m->d_mail);
     if (m->pst.ctr) cudaFree(m->pst.ctr);
+    if (m->d_px) cudaFree(m->d_px);
+    if (m->d_pg) cudaFree(m->d_pg);
+    if (m->d_if_patch) cudaFree(m->d_if_patch);
     if (m->comm) ncclCommDestroy(m->comm);
     if (m->comm_stream) cudaStreamDestroy(m->comm_stream);
     if (m->ev_fork) cudaEventDestroy(m->ev_fork);
@@ -2219,6 +2243,11 @@ spuma_status spuma_set_option(spuma_mesh m, int option, int value)
         }
         g_use_pdl = value != 0;
         return SPUMA_OK;
+    case SPUMA_OPT_PEER_FUSED:
+        if (value < 0 || value > 1) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "peer_fused is 0 or 1");
+        if (m->peer_fused != (value != 0)) destroy_graphs(m);
+        m->peer_fused = value != 0;
+        return SPUMA_OK;
     case SPUMA_OPT_SMALL_SMEM:
         if (value < 0 || value > 1) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "small_smem is 0 or 1");
         m->small_smem = value != 0;
@@ -2352,6 +2381,25 @@ spuma_status spuma_peer_import(spuma_mesh m, const void* blobs, int n_blobs)
     for (int par = 0; par < 2; ++par) {
         g.my_part[par] = part(m->rank, par);
         g.my_flag[par] = pflag(m->rank, par);
+    }
+    // device copies for the fused PCG loop (halo inside k_direction / k_iface_rows, all-gather
+    // inside the reductions' last CTA): the level-0 exchange and the gather descriptors, and the
+    // processor patch of every interface face
+    {
+        PeerXfer x = d;
+        for (int p = 0; p < x.n_patches; ++p) x.off[p] = m->cb_offsets[p], x.count[p] = m->cb_counts[p];
+        std::vector<int> ifp(std::max(m->n_iface, 1), 0);
+        for (int p = 0; p < x.n_patches; ++p)
+            for (int i = 0; i < x.count[p]; ++i) ifp[x.off[p] + i] = p;
+        SPUMA_CUDA(cudaMalloc(reinterpret_cast<void**>(&m->d_px), sizeof(PeerXfer)));
+        SPUMA_CUDA(cudaMalloc(reinterpret_cast<void**>(&m->d_pg), sizeof(PeerGather)));
+        SPUMA_CUDA(cudaMemcpy(m->d_px, &x, sizeof(PeerXfer), cudaMemcpyHostToDevice));
+        SPUMA_CUDA(cudaMemcpy(m->d_pg, &g, sizeof(PeerGather), cudaMemcpyHostToDevice));
+        SPUMA_TRY(upload(&m->d_if_patch, ifp, m->stream));
+        SPUMA_CUDA(cudaStreamSynchronize(m->stream));
+        m->ws.px = m->d_px;
+        m->ws.pg = m->d_pg;
+        m->ws.if_patch = m->d_if_patch;
     }
     m->peer = true;
     m->external_comm = false;  // graph-capturable from now on

@@ -175,6 +175,87 @@ static __device__ void finalize(DevScal* s, int stage, const double* g)
     }
 }
 
+// ---------------------------------------------------------------------------
+// peer-memory transport primitives (peer.cu, and the PCG loop's fused halo / all-gather)
+// ---------------------------------------------------------------------------
+static __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p)
+{
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+static __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v)
+{
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// wait until *f >= e (thread-local poll); false on timeout (error word set)
+static __device__ bool wait_flag(const unsigned long long* f, unsigned long long e, int* err, long long limit)
+{
+    const long long t0 = clock64();
+    unsigned ns = 32;
+    while (ld_acquire_sys(f) < e) {
+        if (*reinterpret_cast<volatile int*>(err)) return false;  // an earlier exchange already failed
+        if (clock64() - t0 > limit) {
+            atomicExch(err, 1);
+            return false;
+        }
+        __nanosleep(ns);
+        ns = ns < 4096 ? 2 * ns : ns;
+    }
+    return true;
+}
+
+// The rank-partial all-gather of the peer transport, then the PCG finalisation: publish this
+// rank's 4 partials (in) into every rank's mailbox slot + flag, wait for every rank's flag, copy
+// the rank-ordered block to out, and (stage > 0) finalise the scalars from it in rank order --
+// the sums of k_finalize, so every rank takes bitwise the same decisions.  Called by every
+// thread of ONE CTA (blockDim >= n_ranks): k_peer_allgather4, or the last CTA of a reduction
+// kernel of the fused PCG loop (compute and collective in one kernel).  A timed-out gather stops
+// the loop (done) instead of finalising stale values.
+static __device__ void peer_gather_finalize(const PeerGather& g, const PeerState& st, const double* in,
+                                            double* out, int stage, DevScal* sc)
+{
+    __shared__ unsigned long long se;
+    __shared__ int ok;
+    if (threadIdx.x == 0) {
+        se = st.ctr[1] + 1;
+        ok = 1;
+    }
+    __syncthreads();
+    const unsigned long long e = se;
+    const int par = (int)(e & 1ull);
+    const int t = threadIdx.x;
+    if (t < g.n_ranks) {
+        double* dst = g.part[t][par] + 4 * g.rank;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) dst[k] = in[k];
+        __threadfence_system();
+        st_release_sys(g.flag[t][par] + g.rank, e);
+    }
+    __syncthreads();
+    if (t < g.n_ranks && !wait_flag(g.my_flag[par] + t, e, st.err, st.poll_cycles)) ok = 0;
+    __syncthreads();
+    if (ok && t < g.n_ranks)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) out[4 * t + k] = g.my_part[par][4 * t + k];
+    if (t == 0) st.ctr[1] = e;
+    if (stage > 0) {
+        __syncthreads();
+        if (t == 0) {
+            if (!ok) {
+                sc->done = 1;
+            } else if (!(stage >= 3 && sc->done)) {
+                double v[4] = {0.0, 0.0, 0.0, 0.0};
+                for (int r = 0; r < g.n_ranks; ++r)
+                    for (int i = 0; i < 4; ++i) v[i] += out[4 * r + i];
+                finalize(sc, stage, v);
+            }
+        }
+    }
+}
+
 template <int NV>
 __device__ __forceinline__ void cta_sum_1024(double (&v)[NV])
 {

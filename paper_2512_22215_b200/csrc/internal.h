@@ -76,6 +76,31 @@ struct MeshArgs {
 // holding exactly this bit pattern would be read as "no face")
 constexpr unsigned long long kLatAbsent = 0x7FF4A5A5C3C3A5A5ull;
 
+// Peer-memory transport (peer.cu): kernel-parameter descriptors of one exchange / all-gather
+constexpr int kMaxPeerPatches = 32;
+constexpr int kMaxPeerRanks = 64;
+struct PeerXfer {
+    int n_patches;
+    int off[kMaxPeerPatches], count[kMaxPeerPatches];           // this exchange: local offsets / counts
+    double* dst[kMaxPeerPatches][2];                              // receiver's region for my patch (parity)
+    unsigned long long* dst_flag[kMaxPeerPatches][2];             // receiver's flag slot for me (parity)
+    const double* src[kMaxPeerPatches][2];                        // my region written by patch p's peer
+    const unsigned long long* src_flag[kMaxPeerPatches][2];       // my flag slot for patch p's peer
+};
+struct PeerGather {
+    int n_ranks, rank;
+    double* part[kMaxPeerRanks][2];               // rank t's partials block [n_ranks][4] (parity)
+    unsigned long long* flag[kMaxPeerRanks][2];   // rank t's partial flags [n_ranks] (parity)
+    const double* my_part[2];
+    const unsigned long long* my_flag[2];
+};
+struct PeerState {
+    unsigned long long* ctr;  // [2] exchange / all-gather epochs (device)
+    unsigned* ticket;
+    int* err;                 // set on a poll timeout
+    long long poll_cycles = 40'000'000'000LL;  // poll limit, SM clocks (~20 s at 2 GHz; SPUMA_OPT_PEER_POLL_MS)
+};
+
 struct Workspace {
     double *wA, *rA, *pA, *rD, *sumA;
     double* pA_prev;   // direction of the previous iteration (== pA unless psi updates are deferred)
@@ -84,6 +109,13 @@ struct Workspace {
     double* part;      // [kMaxPartials * grid] per-CTA partials
     DevScal* scal;
     DevPtrs* ptrs;
+    // the peer transport's fused PCG loop (SPUMA_OPT_PEER_FUSED): the halo stores inside the
+    // direction kernel and the receive inside the interface rows, the rank-partial all-gather
+    // and finalisation inside the reductions' last CTA; nullptr without the peer transport
+    const PeerXfer* px;      // device copy of the level-0 exchange descriptor
+    const PeerGather* pg;    // device copy of the all-gather descriptor
+    const int* if_patch;     // [n_iface] processor patch (px order) of each interface face
+    PeerState pst;
 };
 
 // One GAMG level on the device, captured by value.  Level 0 reads its
@@ -118,30 +150,6 @@ struct GLevel {
     int ncif;                     // next level's interface faces
 };
 
-// Peer-memory transport (peer.cu): kernel-parameter descriptors of one exchange / all-gather
-constexpr int kMaxPeerPatches = 32;
-constexpr int kMaxPeerRanks = 64;
-struct PeerXfer {
-    int n_patches;
-    int off[kMaxPeerPatches], count[kMaxPeerPatches];           // this exchange: local offsets / counts
-    double* dst[kMaxPeerPatches][2];                              // receiver's region for my patch (parity)
-    unsigned long long* dst_flag[kMaxPeerPatches][2];             // receiver's flag slot for me (parity)
-    const double* src[kMaxPeerPatches][2];                        // my region written by patch p's peer
-    const unsigned long long* src_flag[kMaxPeerPatches][2];       // my flag slot for patch p's peer
-};
-struct PeerGather {
-    int n_ranks, rank;
-    double* part[kMaxPeerRanks][2];               // rank t's partials block [n_ranks][4] (parity)
-    unsigned long long* flag[kMaxPeerRanks][2];   // rank t's partial flags [n_ranks] (parity)
-    const double* my_part[2];
-    const unsigned long long* my_flag[2];
-};
-struct PeerState {
-    unsigned long long* ctr;  // [2] exchange / all-gather epochs (device)
-    unsigned* ticket;
-    int* err;                 // set on a poll timeout
-    long long poll_cycles = 40'000'000'000LL;  // poll limit, SM clocks (~20 s at 2 GHz; SPUMA_OPT_PEER_POLL_MS)
-};
 
 struct Patch {
     int kind, n_faces, offset;   // offset into the concatenated boundary arrays
@@ -171,6 +179,9 @@ struct spuma_mesh_s {
     // peer-memory transport (spuma_peer_export / spuma_peer_import; peer.cu)
     bool peer = false;
     double* d_mail = nullptr;            // this rank's mailbox (IPC-exported)
+    spuma::PeerXfer* d_px = nullptr;     // device copies for the fused PCG loop (Workspace::px, pg)
+    spuma::PeerGather* d_pg = nullptr;
+    int* d_if_patch = nullptr;
     size_t mail_units = 0;
     std::vector<void*> peer_mapped;      // opened IPC mappings (to close)
     spuma::PeerXfer px{};                // level-0 exchange descriptor (off/count per call)
@@ -239,6 +250,7 @@ struct spuma_mesh_s {
     int batch = 16;
     int small_max_cells = 8192;  // single-CTA solve at or below this many cells (1 rank)
     bool small_smem = true;      // ... staged in shared memory when it fits (SPUMA_OPT_SMALL_SMEM)
+    bool peer_fused = true;      // peer transport: halo + all-gather fused into the PCG loop's kernels
     int amul_variant = 12;  // lattice slots (falls back to 10 -> 6 -> 5 off lattice / uniform meshes)
     int defer_psi = 2;      // 0: psi += alpha pA every iteration; 1: pairs in k_update; 2: pairs in k_direction  // psi += alpha pA applied every second iteration (same rounding, fewer bytes)  // ELL + coefficient copy (falls back to 6 -> 5 when the mesh is not uniform)
     bool timing = false;
@@ -330,13 +342,15 @@ void launch_setup2(cudaStream_t s, int grid, const MeshArgs& a, const Workspace&
 // psi_pair (SPUMA_OPT_DEFER_PSI = 2, even iterations k >= 2): also psi = (psi + alpha_{k-2} p_{k-2}) +
 // alpha_{k-1} p_{k-1}, p_{k-2} being the buffer the new direction overwrites
 void launch_direction(cudaStream_t s, int grid, const MeshArgs& a, const Workspace& w, bool reverse = false,
-                      bool psi_pair = false);
+                      bool psi_pair = false, bool halo = false);
 void launch_amul_dot(cudaStream_t s, int variant, const MeshArgs& a, const Workspace& w, bool fin, int sell_wn,
                      int sell_wo, bool deferred = false, bool reverse = false);
 // reverse: the kernel sweeps its cells in descending order (alternating sweep directions between
 // consecutive kernels lets each one start on the lines its predecessor left in L2)
 int resolve_amul_variant(int variant, const MeshArgs& a);  // variant actually run on this mesh
-void launch_iface_rows(cudaStream_t s, const MeshArgs& a, const Workspace& w, const int* rows, int n_rows);
+// peer: the halo's receive (flags + mailbox reads) and the stage-3 all-gather + finalisation fused in
+void launch_iface_rows(cudaStream_t s, const MeshArgs& a, const Workspace& w, const int* rows, int n_rows,
+                       bool peer = false);
 void launch_surface_integrate(cudaStream_t s, const MeshArgs& a, const double* phi, const int* bStart,
                               const int* bFace, const double* bphi, const double* V, double* out);
 void launch_face_flux(cudaStream_t s, int F, const int* owner, const int* neighbour, const double* upper,
@@ -365,7 +379,8 @@ void launch_add(cudaStream_t s, int n, const double* in, double* out);
 void launch_scatter_signed(cudaStream_t s, int n, const int* idx, const signed char* flip, const double* in,
                            double* out);
 constexpr int kPad = 8;  // padding elements on internal arrays (16-byte TMA windows may overrun by <= 3)
-void launch_update(cudaStream_t s, int grid, const MeshArgs& a, const Workspace& w, bool fin, int psi_mode = 0,
+// fin: 1 finalise (one rank); 0 leave the rank partials; 2 the peer all-gather + finalisation in the last CTA
+void launch_update(cudaStream_t s, int grid, const MeshArgs& a, const Workspace& w, int fin, int psi_mode = 0,
                    bool reverse = false);
 // psi_mode: 0 psi += alpha pA; 1 defer (psi untouched); 2 psi = (psi + alpha_prev pA_prev) + alpha pA
 void launch_psi_flush(cudaStream_t s, int N, const Workspace& w);

@@ -404,10 +404,42 @@ __global__ void __launch_bounds__(kThreads) k_setup2(MeshArgs a, Workspace w, in
 // pair (k-2, k-1) -- psi = (psi + alpha_{k-2} p_{k-2}) + alpha_{k-1} p_{k-1}, the two roundings of
 // two separate updates, so the iterates are bitwise unchanged -- applied here, where p_{k-1}
 // (pA_prev) is read anyway and p_{k-2} is the value of pA this pass overwrites (read first).
-__global__ void __launch_bounds__(kThreads) k_direction(int N, Workspace w, int rev, int psi_pair)
+// halo (peer transport, SPUMA_OPT_PEER_FUSED): every interface cell's new direction value is stored
+// straight into the neighbours' mailboxes by the thread that computed it (compute and send in one
+// kernel); the last CTA publishes the exchange's epoch (the protocol of k_peer_send, peer.cu).
+__device__ __forceinline__ void halo_store(const MeshArgs& a, const Workspace& w, int par, int c, double v)
+{
+    if (!((__ldg(a.ifMask + (c >> 5)) >> (c & 31)) & 1u)) return;
+    const int j1 = a.ifStart[c + 1];
+    for (int j = a.ifStart[c]; j < j1; ++j) {
+        const int q = a.ifIdx[j], p = w.if_patch[q];
+        w.px->dst[p][par][q - w.px->off[p]] = v;
+    }
+}
+
+__device__ __forceinline__ void halo_publish(const Workspace& w, unsigned long long e)
+{
+    __threadfence_system();  // this thread's peer stores before the ticket
+    __syncthreads();
+    __shared__ bool last;
+    if (threadIdx.x == 0) last = atomicAdd(w.pst.ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+        __threadfence_system();
+        const int par = (int)(e & 1ull);
+        for (int p = 0; p < w.px->n_patches; ++p) st_release_sys(w.px->dst_flag[p][par], e);
+        w.pst.ctr[0] = e;
+        *w.pst.ticket = 0u;
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) k_direction(MeshArgs a, Workspace w, int rev, int psi_pair, int halo)
 {
     pdl_wait();
     if (w.scal->done) return;
+    const int N = a.N;
+    const unsigned long long he = halo ? w.pst.ctr[0] + 1 : 0;  // this exchange's epoch
+    const int hpar = (int)(he & 1ull);
     const int n = w.scal->n;
     const bool first = n == 0;
     const bool psi = psi_pair && n >= 2;
@@ -441,6 +473,10 @@ __global__ void __launch_bounds__(kThreads) k_direction(int N, Workspace w, int 
             q.y = d.y * r.y + beta * p.y;
         }
         pA2[i] = q;
+        if (halo) {
+            halo_store(a, w, hpar, 2 * i, q.x);
+            halo_store(a, w, hpar, 2 * i + 1, q.y);
+        }
     }
     if ((N & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
         const int c = N - 1;
@@ -448,10 +484,13 @@ __global__ void __launch_bounds__(kThreads) k_direction(int N, Workspace w, int 
             double* ps = w.ptrs->psi;
             ps[c] = (ps[c] + a2 * w.pA[c]) + a1 * w.pA_prev[c];
         }
-        w.pA[c] = first ? w.rD[c] * w.rA[c] : w.rD[c] * w.rA[c] + beta * w.pA_prev[c];
+        const double v = first ? w.rD[c] * w.rA[c] : w.rD[c] * w.rA[c] + beta * w.pA_prev[c];
+        w.pA[c] = v;
+        if (halo) halo_store(a, w, hpar, c, v);
     }
     if (psi && blockIdx.x == 0 && threadIdx.x == 0) w.scal->psi_done = n;
     pdl_trigger();
+    if (halo) halo_publish(w, he);
 }
 
 // A7 + A8: wA = A pA, partial wA.pA -> alpha
@@ -646,9 +685,15 @@ __global__ void __launch_bounds__(kThreads) k_update(int N, Workspace w, int fin
         v[1] += fabs(r);
     }
     pdl_trigger();
-    if (grid_sum<2>(v, w.part, &w.scal->ticket[3]) && threadIdx.x == 0) {
-        if (fin) finalize(w.scal, 4, v);
-        else w.scal->rank_part[0] = v[0], w.scal->rank_part[1] = v[1];
+    if (grid_sum<2>(v, w.part, &w.scal->ticket[3])) {  // true in every thread of the last CTA
+        if (threadIdx.x == 0) {
+            if (fin == 1) finalize(w.scal, 4, v);
+            else w.scal->rank_part[0] = v[0], w.scal->rank_part[1] = v[1];
+        }
+        if (fin == 2) {  // the peer all-gather of the rank partials and the finalisation, here
+            __syncthreads();
+            peer_gather_finalize(*w.pg, w.pst, w.scal->rank_part, w.part, 4, w.scal);
+        }
     }
 }
 
@@ -999,11 +1044,27 @@ __global__ void k_add(int n, const double* __restrict__ in, double* __restrict__
 // (ascending).  wA[c] already holds the internal-face sum; add the interface terms
 // in (patch, face) order (bitwise the one-pass row, Q10) and the rows' share of
 // wA.pA, then complete this rank's partial: rank_part[0] = interior + interface rows.
+// peer (SPUMA_OPT_PEER_FUSED): the halo's receive is fused in -- each CTA waits for the neighbours'
+// epoch flags of the exchange k_direction published, then reads the remote values straight from
+// its mailbox -- and the last CTA runs the rank-partial all-gather + finalisation (stage 3).
 __global__ void __launch_bounds__(kThreads) k_iface_rows(MeshArgs a, Workspace w, const int* __restrict__ rows,
-                                                         int n_rows)
+                                                         int n_rows, int peer)
 {
     if (w.scal->done) return;
     const DevPtrs p = *w.ptrs;
+    int par = 0;
+    if (peer) {
+        __shared__ int ok;
+        const unsigned long long e = w.pst.ctr[0];  // set by this rank's k_direction of the same exchange
+        par = (int)(e & 1ull);
+        if (threadIdx.x == 0) {
+            ok = 1;
+            for (int q = 0; q < w.px->n_patches && ok; ++q)
+                if (!wait_flag(w.px->src_flag[q][par], e, w.pst.err, w.pst.poll_cycles)) ok = 0;
+        }
+        __syncthreads();
+        if (!ok) n_rows = 0;  // timed out: the error word is set, the gather below stops the loop
+    }
     double v[1] = {0.0};
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_rows; i += gridDim.x * blockDim.x) {
         const int c = rows[i];
@@ -1011,13 +1072,25 @@ __global__ void __launch_bounds__(kThreads) k_iface_rows(MeshArgs a, Workspace w
         const int j1 = a.ifStart[c + 1];
         for (int j = a.ifStart[c]; j < j1; ++j) {
             const int q = a.ifIdx[j];
-            y = y + p.iface[q] * w.xr[q];
+            double xr;
+            if (peer) {
+                const int pp = w.if_patch[q];
+                xr = __ldcg(w.px->src[pp][par] + (q - w.px->off[pp]));
+            } else {
+                xr = w.xr[q];
+            }
+            y = y + p.iface[q] * xr;
         }
         w.wA[c] = y;
         v[0] += y * w.pA[c];
     }
-    if (grid_sum<1>(v, w.part, &w.scal->ticket[4]) && threadIdx.x == 0)
-        w.scal->rank_part[0] = w.scal->rank_part[0] + v[0];
+    if (grid_sum<1>(v, w.part, &w.scal->ticket[4])) {
+        if (threadIdx.x == 0) w.scal->rank_part[0] = w.scal->rank_part[0] + v[0];
+        if (peer) {
+            __syncthreads();
+            peer_gather_finalize(*w.pg, w.pst, w.scal->rank_part, w.part, 3, w.scal);
+        }
+    }
 }
 
 // P > 1: global sums of the gathered rank partials in rank order, then finalise
@@ -1346,10 +1419,12 @@ void launch_setup2(cudaStream_t s, int grid, const MeshArgs& a, const Workspace&
     k_setup2<<<grid_for(k_setup2, a.N), kThreads, 0, s>>>(a, w, fin ? 1 : 0);
 }
 
-void launch_direction(cudaStream_t s, int grid, const MeshArgs& a, const Workspace& w, bool reverse, bool psi_pair)
+void launch_direction(cudaStream_t s, int grid, const MeshArgs& a, const Workspace& w, bool reverse, bool psi_pair,
+                      bool halo)
 {
     (void)grid;
-    launch_hot(k_direction, grid_for(k_direction, a.N, 2), kThreads, s, a.N, w, reverse ? 1 : 0, psi_pair ? 1 : 0);
+    launch_hot(k_direction, grid_for(k_direction, a.N, 2), kThreads, s, a, w, reverse ? 1 : 0, psi_pair ? 1 : 0,
+               halo ? 1 : 0);
 }
 
 int resolve_amul_variant(int variant, const MeshArgs& a)
@@ -1435,11 +1510,11 @@ void launch_amul_dot_dir(cudaStream_t s, const MeshArgs& a, const Workspace& w, 
     else launch_hot(k_amul_dot_dir<false>, g, kThreads, s, a, w);
 }
 
-void launch_update(cudaStream_t s, int grid, const MeshArgs& a, const Workspace& w, bool fin, int psi_mode,
+void launch_update(cudaStream_t s, int grid, const MeshArgs& a, const Workspace& w, int fin, int psi_mode,
                    bool reverse)
 {
     (void)grid;
-    launch_hot(k_update, grid_for(k_update, a.N, 2), kThreads, s, a.N, w, fin ? 1 : 0, psi_mode, reverse ? 1 : 0);
+    launch_hot(k_update, grid_for(k_update, a.N, 2), kThreads, s, a.N, w, fin, psi_mode, reverse ? 1 : 0);
 }
 
 // the pending half of a deferred pair when the loop stopped after an even-indexed iteration
@@ -1564,10 +1639,11 @@ void launch_add(cudaStream_t s, int n, const double* in, double* out)
     k_add<<<grid_for(k_add, n), kThreads, 0, s>>>(n, in, out);
 }
 
-void launch_iface_rows(cudaStream_t s, const MeshArgs& a, const Workspace& w, const int* rows, int n_rows)
+void launch_iface_rows(cudaStream_t s, const MeshArgs& a, const Workspace& w, const int* rows, int n_rows, bool peer)
 {
-    if (n_rows <= 0) return;
-    k_iface_rows<<<grid_for(k_iface_rows, n_rows), kThreads, 0, s>>>(a, w, rows, n_rows);
+    if (n_rows <= 0 && !peer) return;
+    const int g = n_rows > 0 ? grid_for(k_iface_rows, n_rows) : 1;  // peer: the gather runs even without rows
+    k_iface_rows<<<g, kThreads, 0, s>>>(a, w, rows, n_rows, peer ? 1 : 0);
 }
 
 void launch_finalize(cudaStream_t s, int stage, const double* gathered, int n_ranks, const Workspace& w)

@@ -25,35 +25,6 @@
 namespace spuma {
 namespace {
 
-__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p)
-{
-    unsigned long long v;
-    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-
-__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v)
-{
-    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-
-// wait until *f >= e (thread-local poll); false on timeout (error word set)
-__device__ bool wait_flag(const unsigned long long* f, unsigned long long e, int* err, long long limit)
-{
-    const long long t0 = clock64();
-    unsigned ns = 32;
-    while (ld_acquire_sys(f) < e) {
-        if (*reinterpret_cast<volatile int*>(err)) return false;  // an earlier exchange already failed
-        if (clock64() - t0 > limit) {
-            atomicExch(err, 1);
-            return false;
-        }
-        __nanosleep(ns);
-        ns = ns < 4096 ? 2 * ns : ns;
-    }
-    return true;
-}
-
 // fused pack + send: dst[p][par][i] = (idx ? x[idx[off_p + i]] : x[off_p + i]) for every
 // patch p, then the epoch into each receiver's flag slot (last CTA)
 __global__ void __launch_bounds__(kThreads) k_peer_send(PeerXfer d, const double* __restrict__ x,
@@ -101,50 +72,11 @@ __global__ void __launch_bounds__(kThreads) k_peer_recv(PeerXfer d, double* __re
     }
 }
 
-// all-gather of 4 doubles per rank (one CTA): publish to every rank, wait for every rank,
-// copy the rank-ordered block out; stage > 0: then finalise the PCG scalars from it exactly as
-// k_finalize does (rank-order sums, finalize(stage)) -- one launch instead of two per reduction.
-// A timed-out gather (error word set) stops the loop (done) instead of finalising stale values.
+// all-gather of 4 doubles per rank (one CTA) and, stage > 0, the finalisation (device.cuh)
 __global__ void k_peer_allgather4(PeerGather g, const double* __restrict__ in, double* __restrict__ out, PeerState st,
                                   int stage, Workspace w)
 {
-    __shared__ unsigned long long se;
-    __shared__ int ok;
-    if (threadIdx.x == 0) {
-        se = st.ctr[1] + 1;
-        ok = 1;
-    }
-    __syncthreads();
-    const unsigned long long e = se;
-    const int par = (int)(e & 1ull);
-    const int t = threadIdx.x;
-    if (t < g.n_ranks) {
-        double* dst = g.part[t][par] + 4 * g.rank;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) dst[k] = in[k];
-        __threadfence_system();
-        st_release_sys(g.flag[t][par] + g.rank, e);
-    }
-    __syncthreads();
-    if (t < g.n_ranks && !wait_flag(g.my_flag[par] + t, e, st.err, st.poll_cycles)) ok = 0;
-    __syncthreads();
-    if (ok && t < g.n_ranks)
-#pragma unroll
-        for (int k = 0; k < 4; ++k) out[4 * t + k] = g.my_part[par][4 * t + k];
-    if (t == 0) st.ctr[1] = e;
-    if (stage > 0) {
-        __syncthreads();
-        if (t == 0) {
-            if (!ok) {
-                w.scal->done = 1;
-            } else if (!(stage >= 3 && w.scal->done)) {
-                double v[4] = {0.0, 0.0, 0.0, 0.0};
-                for (int r = 0; r < g.n_ranks; ++r)
-                    for (int i = 0; i < 4; ++i) v[i] += out[4 * r + i];
-                finalize(w.scal, stage, v);
-            }
-        }
-    }
+    peer_gather_finalize(g, st, in, out, stage, w.scal);
 }
 
 }  // namespace

@@ -36,6 +36,7 @@ OPT_L2_PERSIST = 8
 OPT_GAMG_CSR = 9
 OPT_PEER_POLL_MS = 10
 OPT_SMALL_SMEM = 11
+OPT_PEER_FUSED = 12
 PEER_BLOB_BYTES = 512  # SPUMA_PEER_BLOB_BYTES
 AMUL_VARIANTS = (0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13)
 

@@ -5,7 +5,8 @@ acquire epoch flags) -- the code path that runs over NVLink between GPUs, no NCC
 callbacks, iteration batches captured in CUDA graphs.
 
 Checked: the decomposed PCG against the decomposed oracle (Q11 protocol) and bitwise against the
-host-callback transport (same kernels, same reduction order -> same bits); the decomposed GAMG
+host-callback transport (same kernels, same reduction order -> same bits) and against the peer
+transport with separate transport kernels (SPUMA_OPT_PEER_FUSED = 0); the decomposed GAMG
 and PCG-DIC against their decomposed oracles; no poll ever timed out."""
 import os
 
@@ -69,6 +70,13 @@ def _worker(rank, P, how, port, results):
         psi_c = torch.zeros(me.n_cells, **f64)
         pc = hc.pcg_solve(diag, upper, iface, src, psi_c, 1e-9, 0.0, 3000, 0)
         assert pc == pf and torch.equal(psi, psi_c)
+        # the fused loop (halo in the direction / interface-row kernels, all-gather in the
+        # reductions' last CTA) vs separate transport kernels: bitwise the same
+        h.set_option(S.spuma.OPT_PEER_FUSED, 0)
+        psi_s = torch.zeros(me.n_cells, **f64)
+        ps_ = h.pcg_solve(diag, upper, iface, src, psi_s, 1e-9, 0.0, 3000, 0)
+        h.set_option(S.spuma.OPT_PEER_FUSED, 1)
+        assert ps_ == pf and torch.equal(psi_s, psi)
         n = min(pf["n_iterations"], po["n_iterations"])
         psi.zero_()
         h.pcg_solve(diag, upper, iface, src, psi, 0.0, 0.0, n, n)
