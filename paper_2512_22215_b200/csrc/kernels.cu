@@ -407,19 +407,22 @@ __global__ void __launch_bounds__(kThreads) k_setup2(MeshArgs a, Workspace w, in
 // halo (peer transport, SPUMA_OPT_PEER_FUSED): every interface cell's new direction value is stored
 // straight into the neighbours' mailboxes by the thread that computed it (compute and send in one
 // kernel); the last CTA publishes the exchange's epoch (the protocol of k_peer_send, peer.cu).
-__device__ __forceinline__ void halo_store(const MeshArgs& a, const Workspace& w, int par, int c, double v)
+__device__ __forceinline__ bool halo_store(const MeshArgs& a, const Workspace& w, int par, int c, double v)
 {
-    if (!((__ldg(a.ifMask + (c >> 5)) >> (c & 31)) & 1u)) return;
+    if (!((__ldg(a.ifMask + (c >> 5)) >> (c & 31)) & 1u)) return false;
     const int j1 = a.ifStart[c + 1];
     for (int j = a.ifStart[c]; j < j1; ++j) {
         const int q = a.ifIdx[j], p = w.if_patch[q];
         w.px->dst[p][par][q - w.px->off[p]] = v;
     }
+    return true;
 }
 
-__device__ __forceinline__ void halo_publish(const Workspace& w, unsigned long long e)
+// sent: this thread stored into a peer's mailbox (only those threads need the system-scope fence
+// before their CTA's ticket; the last CTA fences again before it publishes the flags)
+__device__ __forceinline__ void halo_publish(const Workspace& w, unsigned long long e, bool sent)
 {
-    __threadfence_system();  // this thread's peer stores before the ticket
+    if (sent) __threadfence_system();
     __syncthreads();
     __shared__ bool last;
     if (threadIdx.x == 0) last = atomicAdd(w.pst.ticket, 1u) == gridDim.x - 1;
@@ -440,6 +443,7 @@ __global__ void __launch_bounds__(kThreads) k_direction(MeshArgs a, Workspace w,
     const int N = a.N;
     const unsigned long long he = halo ? w.pst.ctr[0] + 1 : 0;  // this exchange's epoch
     const int hpar = (int)(he & 1ull);
+    bool sent = false;
     const int n = w.scal->n;
     const bool first = n == 0;
     const bool psi = psi_pair && n >= 2;
@@ -474,8 +478,8 @@ __global__ void __launch_bounds__(kThreads) k_direction(MeshArgs a, Workspace w,
         }
         pA2[i] = q;
         if (halo) {
-            halo_store(a, w, hpar, 2 * i, q.x);
-            halo_store(a, w, hpar, 2 * i + 1, q.y);
+            sent |= halo_store(a, w, hpar, 2 * i, q.x);
+            sent |= halo_store(a, w, hpar, 2 * i + 1, q.y);
         }
     }
     if ((N & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
@@ -486,11 +490,11 @@ __global__ void __launch_bounds__(kThreads) k_direction(MeshArgs a, Workspace w,
         }
         const double v = first ? w.rD[c] * w.rA[c] : w.rD[c] * w.rA[c] + beta * w.pA_prev[c];
         w.pA[c] = v;
-        if (halo) halo_store(a, w, hpar, c, v);
+        if (halo) sent |= halo_store(a, w, hpar, c, v);
     }
     if (psi && blockIdx.x == 0 && threadIdx.x == 0) w.scal->psi_done = n;
     pdl_trigger();
-    if (halo) halo_publish(w, he);
+    if (halo) halo_publish(w, he, sent);
 }
 
 // A7 + A8: wA = A pA, partial wA.pA -> alpha
