@@ -482,8 +482,8 @@ typedef enum {
      * slots everywhere (default: same-box A/B at 200^3 measured no gain -- the row gather is
      * bound by its two dependent load levels, not by the bytes), 1 = on */
     SPUMA_OPT_ELL_STENCIL = 7,
-    /* PCG hot loop: an L2 access-policy window (persisting) over the direction vector pA,
-     * captured into the iteration graphs; 0 = none (default), 1 = on */
+    /* PCG hot loop: an L2 access-policy window (persisting hits) captured into the iteration
+     * graphs over one workspace vector: 0 = none (default), 1 = pA, 2 = rA, 3 = rD, 4 = wA */
     SPUMA_OPT_L2_PERSIST = 8,
     /* GAMG: the coarse levels without uniform widths run their rows over a per-level CSR copy of
      * the off-diagonal coefficients (row_ax order; bitwise the same rows); 1 = on (default),

@@ -560,7 +560,8 @@ spuma_status l2_window(spuma_mesh m, cudaStreamAttrValue* saved)
         SPUMA_CUDA(cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, dev));
         const size_t win = std::min((size_t)maxw, sizeof(double) * (size_t)m->N);
         SPUMA_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min((size_t)maxp, win)));
-        v.accessPolicyWindow.base_ptr = m->ws.pA;
+        double* const target[5] = {nullptr, m->ws.pA, m->ws.rA, m->ws.rD, m->ws.wA};
+        v.accessPolicyWindow.base_ptr = target[m->l2_persist];
         v.accessPolicyWindow.num_bytes = win;
         v.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)maxp / (double)win);
         v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
@@ -2203,9 +2204,9 @@ spuma_status spuma_set_option(spuma_mesh m, int option, int value)
         m->ell_stencil = value != 0;
         return SPUMA_OK;
     case SPUMA_OPT_L2_PERSIST:
-        if (value < 0 || value > 1) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "l2_persist is 0 or 1");
-        if (m->l2_persist != (value != 0)) destroy_graphs(m);
-        m->l2_persist = value != 0;
+        if (value < 0 || value > 4) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "l2_persist is 0..4");
+        if (m->l2_persist != value) destroy_graphs(m);
+        m->l2_persist = value;
         if (!m->l2_persist) l2_reset(m);
         return SPUMA_OK;
     case SPUMA_OPT_GAMG_CSR:

@@ -293,8 +293,10 @@ def test_timing_and_stats():
     _, perf, _, _ = gpu_solve_case(m, None, gen.rhs(m), 0, handle=h)
     st = h.get_stats()
     assert st["kernel_launches"] > 3 * perf["n_iterations"]
-    # one timing sample per executed batch (the batch's first iteration)
-    assert st["phase_count"][1] == -(-perf["n_iterations"] // st["batch_iterations"]) and st["phase_ms"][1] > 0
+    # timing samples of the first two iterations (one even, one odd) of every executed batch
+    n, B = perf["n_iterations"], st["batch_iterations"]
+    expect = (n // B) * min(2, B) + min(2, n % B)
+    assert st["phase_count"][1] == expect and st["phase_ms"][1] > 0
     assert st["phase_count"][3] == 1
 
 
