@@ -483,7 +483,10 @@ typedef enum {
      * bound by its two dependent load levels, not by the bytes), 1 = on */
     SPUMA_OPT_ELL_STENCIL = 7,
     /* PCG hot loop: an L2 access-policy window (persisting hits) captured into the iteration
-     * graphs over one workspace vector: 0 = none (default), 1 = pA, 2 = rA, 3 = rD, 4 = wA */
+     * graphs over one workspace vector: 0 = none, 1 = pA, 2 = rA (default), 3 = rD, 4 = wA.
+     * Sets the device-wide persisting-L2 limit while the handle lives (reset by spuma_free or
+     * by setting 0).  Same-box A/B at 200^3: 161 us per iteration without a window, 150.5 with
+     * rA or pA (profiles/r02n_l2_target_ab.log). */
     SPUMA_OPT_L2_PERSIST = 8,
     /* GAMG: the coarse levels without uniform widths run their rows over a per-level CSR copy of
      * the off-diagonal coefficients (row_ax order; bitwise the same rows); 1 = on (default),

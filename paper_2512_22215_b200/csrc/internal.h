@@ -256,7 +256,7 @@ struct spuma_mesh_s {
     bool timing = false;
     int fuse_direction = 0;      // 0: k_direction + k_amul_dot (default: faster); 1: fused, rD read; 2: fused, 1/diag inline
     bool gamg_csr = true;        // GAMG coarse generic levels as CSR runs (SPUMA_OPT_GAMG_CSR)
-    int l2_persist = 0;          // L2 access-policy window (SPUMA_OPT_L2_PERSIST): 0 none, 1 pA, 2 rA, 3 rD, 4 wA
+    int l2_persist = 2;          // L2 access-policy window (SPUMA_OPT_L2_PERSIST): 0 none, 1 pA, 2 rA (default), 3 rD, 4 wA
     bool l2_limit_set = false;   // the persisting-L2 limit was raised (reset on option off / free)
     bool alt_sweep = true;       // alternate the sweep direction of consecutive hot-loop kernels (L2 reuse)
     int gamg_tail_cells = 512;   // GAMG: levels from the first one at or below this size run in one CTA (0: off)
