@@ -60,6 +60,20 @@ def peaks():
     return 6650.0, "fallback"
 
 
+def loop_bytes(N, lattice_k, resident_frac):
+    """Bytes per iteration the persistent loop (SPUMA_OPT_PERSISTENT) must move through
+    HBM, per phase: C direction rD + pA_prev + pA (24 B/cell) + the psi pair every second iteration
+    (psi read + write + p_{n-2}: 12 B/cell on average) + rA where it is not on chip (8 B/cell);
+    A Amul as the lattice layout (24 + 8K B/cell); B update wA + rD (16 B/cell) + rA read and write
+    where it is not on chip (16 B/cell).  rA held in tensor / shared memory costs nothing per
+    iteration (loaded once and written back once per solve: 16 B/cell per launch)."""
+    off = 1.0 - resident_frac
+    c = (24 + 12 + 8 * off) * N
+    a = (24 + 8 * lattice_k) * N
+    b = (16 + 16 * off) * N
+    return {"C": c, "A": a, "B": b, "iter": a + b + c, "per_launch_fixed": 16 * N * resident_frac}
+
+
 def algorithmic_bytes(N, F, lattice_k=0):
     """SURVEY §8(d): per PCG iteration, fused minimum. Phase A (Amul + dot): 24 B/cell + 16 B/face;
     B (update + dots): 56 B/cell; C (direction): 32 B/cell.
@@ -128,17 +142,18 @@ class ClockSampler:
                 "samples": len(mhz)}
 
 
-def load_traffic(workload, variant):
+def load_traffic(workload, kernel):
     """ncu DRAM bytes per launch of the dominant kernel (profiles/ncu_traffic.json), if that capture
-    is of this workload and of the Amul variant this run uses."""
+    is of this workload and of the kernel this run's roofline names."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(p):
         return None
     try:
         with open(p) as f:
             j = json.load(f)
-        if j.get("workload") == workload and f"k_amul_dot<{variant}," in j.get("kernel", ""):
-            return j.get("amul_dram_bytes_per_launch")
+        for e in j.get("kernels", [j]):
+            if e.get("workload", j.get("workload")) == workload and kernel in e.get("kernel", ""):
+                return e.get("dram_bytes_per_launch", e.get("amul_dram_bytes_per_launch"))
     except (OSError, ValueError):
         pass
     return None
@@ -305,6 +320,10 @@ def run_gpu(args, rank, world, local_rank):
         h.set_option(P.spuma.OPT_DEFER_PSI, args.defer_psi)
     if args.l2_persist is not None:
         h.set_option(P.spuma.OPT_L2_PERSIST, args.l2_persist)
+    if args.persistent is not None:
+        h.set_option(P.spuma.OPT_PERSISTENT, args.persistent)
+    if args.loop_l2 is not None:
+        h.set_option(P.spuma.OPT_LOOP_L2, args.loop_l2)
     f64 = dict(dtype=torch.float64, device=dev)
     diag, upper = torch.empty(N, **f64), torch.empty(F, **f64)
     b_dev = torch.as_tensor(b, **f64)
@@ -345,6 +364,16 @@ def run_gpu(args, rank, world, local_rank):
         t = float(tt.item())
     st = h.get_stats()
     h.set_timing(False)
+    if st["loop_mode"]:  # per-phase profile of the persistent loop: one more (untimed) step
+        h.reset_stats()
+        h.set_option(P.spuma.OPT_LOOP_PROFILE, 1)
+        step()
+        torch.cuda.synchronize()
+        prof = h.get_stats()
+        h.set_option(P.spuma.OPT_LOOP_PROFILE, 0)
+        perfs.pop()
+        for k in ("loop_work_ms", "loop_wait_ms", "loop_work_max_ms"):
+            st[k] = [v * len(perfs) for v in prof[k]]  # per timed step: scaled to the timed steps
     iters = sum(p["n_iterations"] for p in perfs)
     n_global = N * world
     value = n_global * iters / t
@@ -355,6 +384,28 @@ def run_gpu(args, rank, world, local_rank):
     achieved = nb["A"] / (amul_ms / 1e3) / 1e9 if amul_ms > 0 else None
     phase_avg = {k: (st["phase_ms"][i] / st["phase_count"][i] if st["phase_count"][i] else None)
                  for i, k in enumerate(("direction", "amul_dot", "update", "assembly"))}
+    loop = None
+    if st["loop_mode"]:
+        # the persistent loop ran: ONE launch per solve is the dominant kernel (CUDA events on the
+        # launching stream around each launch); its bytes per launch = iterations x loop bytes
+        T = 1024
+        need = -(-(-(-(N // 2) // T)) // max(st["loop_grid"], 1))
+        frac = min(1.0, (st["loop_tmem_pairs"] + st["loop_smem_pairs"]) / need) if need else 1.0
+        lb = loop_bytes(N, lat_k, frac)
+        launches = max(st["loop_count"], 1)
+        loop_ms = st["loop_ms"] / launches
+        it_per_launch = iters / launches
+        bytes_launch = lb["iter"] * it_per_launch + lb["per_launch_fixed"]
+        achieved = bytes_launch / (loop_ms / 1e3) / 1e9 if loop_ms > 0 else None
+        itn = max(iters, 1)
+        loop = {"mode": st["loop_mode"], "grid": st["loop_grid"], "threads": T,
+                "rA_pairs_tmem": st["loop_tmem_pairs"], "rA_pairs_smem": st["loop_smem_pairs"],
+                "rA_resident_frac": frac, "bytes_per_iter": lb, "avg_launch_ms": loop_ms,
+                "us_per_iter": loop_ms * 1e3 / it_per_launch if it_per_launch else None,
+                "phase_work_us": [v * 1e3 / itn for v in st["loop_work_ms"]],
+                "phase_barrier_wait_us": [v * 1e3 / itn for v in st["loop_wait_ms"]],
+                "phase_order": ["C direction", "A Amul + dot", "B update + dots"],
+                "bytes_per_launch": bytes_launch}
     # whole-step effective bandwidth: algorithmic iteration bytes x iterations / step time
     # (assembly and setup included in the time, so this under-states the loop)
     eff_gbs = nb["iter"] * iters / t / 1e9 if t > 0 else None
@@ -406,7 +457,7 @@ def run_gpu(args, rank, world, local_rank):
         # the paper's coefficient of equivalence (Eq. 1) in its single-core form:
         # how many oracle cores one B200 is worth on this workload
         cpu["coe_cores_per_gpu"] = value / cpu["value"]
-    traffic = load_traffic(cfg["workload"], st["amul_variant"])
+    traffic = load_traffic(cfg["workload"], "k_pcg_loop" if loop else f"k_amul_dot<{st['amul_variant']},")
     cfg.update({"global_cells": n_global, "faces_per_gpu": F, "parallelism": f"dd{world}", "transport": transport,
                 "iterations_per_step": iters / max(len(perfs), 1), "l2": "inputs larger than L2 (no flush)",
                 "batch_iterations": st["batch_iterations"], "grid": st["blocks_per_grid"],
@@ -417,15 +468,22 @@ def run_gpu(args, rank, world, local_rank):
                 "amul_variant": st["amul_variant"],
                 "effective_iteration_frac_of_peak": (eff_gbs / peak) if eff_gbs else None,
                 "effective_iteration_frac_of_8TBps": (eff_gbs / 8000.0) if eff_gbs else None,
-                "phase_avg_ms": phase_avg, "algorithmic_bytes": nb})
+                "phase_avg_ms": phase_avg, "algorithmic_bytes": nb, "persistent_loop": loop})
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": 1000 * t / args.steps, "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg,
-           "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                        "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                        "kernel": f"k_amul_dot<{st['amul_variant']}> (A7 Amul + wA.pA, {nb['A_layout']})",
-                        "peak_source": f"{peak_kind} hbm_gbs",
-                        "bytes_per_launch": nb["A"], "avg_launch_ms": amul_ms},
+           "roofline": ({"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                         "kernel": "k_pcg_loop (persistent: every A7-A11 iteration of a solve in one launch, "
+                                   "rA on chip; bytes = iterations x loop bytes per iteration)",
+                         "peak_source": f"{peak_kind} hbm_gbs",
+                         "bytes_per_launch": loop["bytes_per_launch"], "avg_launch_ms": loop["avg_launch_ms"]}
+                        if loop else
+                        {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                         "kernel": f"k_amul_dot<{st['amul_variant']}> (A7 Amul + wA.pA, {nb['A_layout']})",
+                         "peak_source": f"{peak_kind} hbm_gbs",
+                         "bytes_per_launch": nb["A"], "avg_launch_ms": amul_ms}),
            "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": st["kernel_launches"],
            "solver": {"n_iterations": [p["n_iterations"] for p in perfs],
                       "final_residual": perfs[-1]["final_residual"] if perfs else None}}
@@ -451,6 +509,8 @@ def main():
     ap.add_argument("--alt-sweep", type=int, default=None, help="A/B only (default: the library's)")
     ap.add_argument("--defer-psi", type=int, default=None, help="A/B only (default: the library's)")
     ap.add_argument("--l2-persist", type=int, default=None, help="A/B only (default: the library's)")
+    ap.add_argument("--persistent", type=int, default=None, help="A/B only (default: the library's)")
+    ap.add_argument("--loop-l2", type=int, default=None, help="A/B only (default: the library's)")
     ap.add_argument("--cpu-throughput", action="store_true",
                     help="only the cpu_baseline leg in host-throughput mode (every host core), one JSON line")
     ap.add_argument("--gpu-value", type=float, default=None, help="--cpu-throughput: GPU value for the COE analogue")

@@ -423,6 +423,16 @@ typedef struct {
     int blocks_per_grid, threads_per_block, batch_iterations;
     int amul_variant;                /* the A7 layout the hot loop runs on this mesh (after fallbacks:
                                         12 lattice slots -> 10 ELL -> 6 SELL -> 5 per-row)          */
+    /* persistent loop (SPUMA_OPT_PERSISTENT) of the last spuma_pcg_solve: the mode it ran (0: the
+       captured graph batches), its CTAs (one per SM), the rA pairs per thread held in tensor /
+       shared memory, and with timing on the device time of its launches (CUDA events) */
+    int loop_mode, loop_grid, loop_tmem_pairs, loop_smem_pairs;
+    double loop_ms;
+    uint64_t loop_count;
+    /* with SPUMA_OPT_LOOP_PROFILE: per phase (0 direction, 1 Amul, 2 update) the time from the previous grid
+       barrier's release to a CTA's arrival at the next (work) and from arrival to release (wait),
+       summed over the iterations, mean over the CTAs; work_max: the slowest CTA's */
+    double loop_work_ms[3], loop_wait_ms[3], loop_work_max_ms[3];
 } spuma_stats;
 
 spuma_status spuma_get_stats(spuma_mesh m, spuma_stats* out);
@@ -504,7 +514,24 @@ typedef enum {
      * into the interface rows, the rank-partial all-gather + finalisation into the reductions'
      * last CTA (4 kernels per iteration instead of 7); 1 = on (default), 0 = separate kernels.
      * Bitwise the same iterates. */
-    SPUMA_OPT_PEER_FUSED = 12
+    SPUMA_OPT_PEER_FUSED = 12,
+    /* single-rank PCG on a lattice numbering (Amul variant 12, deferred psi pairs): run every
+     * iteration of a solve in ONE cooperative launch of one 1024-thread CTA per SM, three grid
+     * barriers per iteration, each CTA finalising the scalars itself; the residual rA stays on
+     * the SM: 0 = off (captured graph batches), 1 = persistent, rA in HBM, 2 = rA in shared
+     * memory (the rest in HBM), 3 = rA in tensor memory + shared memory (default; ~8.8M cells
+     * fully on chip on 148 SMs).  Same element arithmetic as the graph path; the dot products
+     * are summed in another fixed shape (iterates equal to rounding, deterministic). */
+    SPUMA_OPT_PERSISTENT = 13,
+    /* the persistent loop's L2 access-policy window (persisting hits), targets as
+     * SPUMA_OPT_L2_PERSIST: 0 = none, 1 = pA, 2 = rA, 3 = rD, 4 = wA (default).  Same-box A/B at
+     * 200^3 (profiles/r02r_loop_ab.txt): 149.0 / 143.5 / 146.6 / 143.5 us per iteration for
+     * none / pA / rD / wA; the graph batches with their rA window 153.2 us. */
+    SPUMA_OPT_LOOP_L2 = 14,
+    /* the persistent loop records, per CTA and phase, the time from one grid barrier's release to
+     * its arrival at the next (work) and the wait there (globaltimer; spuma_stats.loop_work_ms /
+     * loop_wait_ms / loop_work_max_ms); 0 = off (default), 1 = on */
+    SPUMA_OPT_LOOP_PROFILE = 15
 } spuma_option;
 spuma_status spuma_set_option(spuma_mesh m, int option, int value);
 

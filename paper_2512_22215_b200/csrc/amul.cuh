@@ -481,7 +481,25 @@ __device__ __forceinline__ bool lat_present(double u)
 
 // one 32R-row chunk of the lattice rows (an interior-chunk version without the range clamps was
 // measured 0.3 % slower and removed, profiles/r02_lattice_ab.md)
-template <int R, int IFM, int KT>
+// x loads of the lattice rows: the read-only path, or (NC = false, the persistent loop of loop.cu,
+// where x is rewritten between grid barriers inside one launch) plain coherent loads
+#ifndef SPUMA_LOOP_XLD
+#define SPUMA_LOOP_XLD 0  // A/B of the persistent loop's coherent loads: 0 ld.global, 1 ld.global.cg (L2 only)
+#endif
+template <bool NC>
+__device__ __forceinline__ double ldx(const double* p)
+{
+    if constexpr (NC) return __ldg(p);
+    double v;
+#if SPUMA_LOOP_XLD == 1
+    asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(p));
+#else
+    asm volatile("ld.global.f64 %0, [%1];" : "=d"(v) : "l"(p));  // volatile: stays behind the barriers
+#endif
+    return v;
+}
+
+template <int R, int IFM, int KT, bool NC = true>
 __device__ __forceinline__ void lat_chunk(const MeshArgs& a, int K, int ch, const double* __restrict__ diag,
                                           const double* const (&ud)[3], const double* __restrict__ iface,
                                           const double* __restrict__ x, const double* __restrict__ xr,
@@ -496,7 +514,7 @@ __device__ __forceinline__ void lat_chunk(const MeshArgs& a, int K, int ch, cons
         c[r] = ch * 32 * R + 32 * r + lane;
         const int cc = min(c[r], N - 1);
         dg[r] = __ldg(diag + cc);
-        xc[r] = __ldg(x + cc);
+        xc[r] = ldx<NC>(x + cc);
 #pragma unroll
         for (int t = 0; t < 3; ++t) {
             if (t < K) {
@@ -505,9 +523,9 @@ __device__ __forceinline__ void lat_chunk(const MeshArgs& a, int K, int ch, cons
                 on[r][t] = o >= 0;
                 const int oc = o >= 0 ? o : cc;
                 uo[r][t] = __ldg(ud[t] + cc);
-                xo[r][t] = __ldg(x + min(cc + D, N - 1));
+                xo[r][t] = ldx<NC>(x + min(cc + D, N - 1));
                 un[r][t] = __ldg(ud[t] + oc);
-                xn[r][t] = __ldg(x + oc);
+                xn[r][t] = ldx<NC>(x + oc);
             } else {
                 on[r][t] = false;
                 uo[r][t] = __longlong_as_double((long long)kLatAbsent);

@@ -543,8 +543,33 @@ void destroy_graphs(spuma_mesh m)
     }
 }
 
-// SPUMA_OPT_L2_PERSIST: an L2 access-policy window over the direction vector pA (the one vector
-// the Amul gathers and three kernels touch), captured into the kernel nodes; 0 = no window
+// An L2 access-policy window (persisting hits, streaming misses) over one workspace vector
+// (1 pA, 2 rA, 3 rD, 4 wA), with the device-wide persisting-L2 limit raised to cover it.  The lines
+// another target left persisting are released first (they would hold the set-aside otherwise).
+spuma_status l2_policy(spuma_mesh m, int target, cudaAccessPolicyWindow* out)
+{
+    int dev = 0, maxp = 0, maxw = 0;
+    SPUMA_CUDA(cudaGetDevice(&dev));
+    SPUMA_CUDA(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev));
+    SPUMA_CUDA(cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, dev));
+    const size_t win = std::min((size_t)maxw, sizeof(double) * (size_t)m->N);
+    SPUMA_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min((size_t)maxp, win)));
+    m->l2_limit_set = true;
+    double* const tg[5] = {nullptr, m->ws.pA, m->ws.rA, m->ws.rD, m->ws.wA};
+    if (m->l2_lines != tg[target]) {
+        SPUMA_CUDA(cudaCtxResetPersistingL2Cache());
+        m->l2_lines = tg[target];
+    }
+    *out = cudaAccessPolicyWindow{};
+    out->base_ptr = tg[target];
+    out->num_bytes = win;
+    out->hitRatio = (float)std::min(1.0, (double)maxp / (double)win);
+    out->hitProp = cudaAccessPropertyPersisting;
+    out->missProp = cudaAccessPropertyStreaming;
+    return SPUMA_OK;
+}
+
+// SPUMA_OPT_L2_PERSIST: the window captured into the iteration graphs' kernel nodes; 0 = none.
 // The window is set on the stream only for the duration of the capture (the kernel nodes keep
 // it); the stream's previous policy -- it may be the caller's stream -- is restored afterwards.
 spuma_status l2_window(spuma_mesh m, cudaStreamAttrValue* saved)
@@ -552,21 +577,7 @@ spuma_status l2_window(spuma_mesh m, cudaStreamAttrValue* saved)
     cudaStreamAttrValue v{};
     if (!m->l2_persist || m->N == 0) return SPUMA_OK;
     SPUMA_CUDA(cudaStreamGetAttribute(m->stream, cudaStreamAttributeAccessPolicyWindow, saved));
-    m->l2_limit_set = true;
-    {
-        int dev = 0, maxp = 0, maxw = 0;
-        SPUMA_CUDA(cudaGetDevice(&dev));
-        SPUMA_CUDA(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev));
-        SPUMA_CUDA(cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, dev));
-        const size_t win = std::min((size_t)maxw, sizeof(double) * (size_t)m->N);
-        SPUMA_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min((size_t)maxp, win)));
-        double* const target[5] = {nullptr, m->ws.pA, m->ws.rA, m->ws.rD, m->ws.wA};
-        v.accessPolicyWindow.base_ptr = target[m->l2_persist];
-        v.accessPolicyWindow.num_bytes = win;
-        v.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)maxp / (double)win);
-        v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-        v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-    }
+    SPUMA_TRY(l2_policy(m, m->l2_persist, &v.accessPolicyWindow));
     SPUMA_CUDA(cudaStreamSetAttribute(m->stream, cudaStreamAttributeAccessPolicyWindow, &v));
     return SPUMA_OK;
 }
@@ -578,6 +589,7 @@ void l2_reset(spuma_mesh m)
     if (!m->l2_limit_set) return;
     cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
     cudaCtxResetPersistingL2Cache();
+    m->l2_lines = nullptr;
     m->l2_limit_set = false;
 }
 
@@ -674,6 +686,100 @@ struct GamgState {
 };
 
 namespace {
+
+// SPUMA_OPT_PERSISTENT: can this solve run as one cooperative launch (loop.cu)?
+bool loop_eligible(spuma_mesh m, const MeshArgs& a)
+{
+    return m->persistent > 0 && m->n_ranks == 1 && !m->external_comm && m->defer_psi == 2 && m->N > 0 &&
+           (resolve_amul_variant(m->amul_variant, a) == 12 || resolve_amul_variant(m->amul_variant, a) == 13) &&
+           (a.lat_K == 3 || a.lat_K == 2 || a.lat_K == 1);
+}
+
+// A7-A11 of the whole solve in one cooperative launch after the A6 setup; *ran = false when the
+// device cannot host it (the caller then runs the graph batches)
+spuma_status run_pcg_loop(spuma_mesh m, cudaStream_t s, const MeshArgs& a, bool* ran)
+{
+    *ran = false;
+    const int T = loop_threads();
+    if (!m->loop_grid) {
+        int dev = 0, sms = 0;
+        SPUMA_CUDA(cudaGetDevice(&dev));
+        SPUMA_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        SPUMA_TRY(dalloc(&m->d_loop_bar, 2));
+        SPUMA_TRY(dalloc(&m->d_loop_part, (size_t)3 * sms));
+        for (int i = 0; i < 2; ++i) SPUMA_CUDA(cudaEventCreate(&m->loop_ev[i]));
+        m->loop_grid = sms;
+    }
+    const int G = m->loop_grid;
+    // rA pairs per thread: the CTA's tiles of T pairs, grid-strided
+    const long long np = m->N / 2, ntile = (np + T - 1) / T;
+    const int need = (int)((ntile + G - 1) / G);
+    int tp = m->persistent >= 3 ? std::min(need, loop_tmem_pairs()) : 0;
+    const int sp_cap = (200 * 1024) / (T * (int)sizeof(double2));  // <= 200 KB of shared memory
+    int sp = m->persistent >= 2 ? std::min(need - tp, sp_cap) : 0;
+    size_t smem = (size_t)sp * T * sizeof(double2);
+    if (loop_occupancy(a.lat_K, smem) < 1) {
+        if (loop_occupancy(a.lat_K, 0) < 1) return SPUMA_OK;  // cannot run here: graph batches
+        sp = 0;
+        smem = 0;
+    }
+    LoopArgs L{};
+    L.bar = m->d_loop_bar;
+    L.tmem_pairs = tp;
+    L.smem_pairs = sp;
+    L.alt = m->alt_sweep ? 1 : 0;
+    L.spin_limit = 4'000'000'000LL;  // ~2 s at 2 GHz per barrier: only a bug waits that long
+    Workspace w = m->ws;
+    w.part = m->d_loop_part;
+    if (m->loop_profile) {
+        if (!m->d_loop_prof) SPUMA_TRY(dalloc(&m->d_loop_prof, (size_t)8 * G));
+        SPUMA_CUDA(cudaMemsetAsync(m->d_loop_prof, 0, sizeof(unsigned long long) * 8 * G, s));
+        L.prof = m->d_loop_prof;
+    }
+    SPUMA_CUDA(cudaMemsetAsync(m->d_loop_bar, 0, 2 * sizeof(unsigned long long), s));
+    if (m->timing) SPUMA_CUDA(cudaEventRecord(m->loop_ev[0], s));
+    cudaAccessPolicyWindow win{};
+    if (m->loop_l2) {
+        SPUMA_TRY(l2_policy(m, m->loop_l2, &win));
+    } else if (m->l2_lines) {  // lines a graph window left persisting would hold the set-aside
+        SPUMA_CUDA(cudaCtxResetPersistingL2Cache());
+        m->l2_lines = nullptr;
+    }
+    SPUMA_CUDA(launch_pcg_loop(s, G, smem, a, w, L, m->loop_l2 ? &win : nullptr));
+    if (m->timing) SPUMA_CUDA(cudaEventRecord(m->loop_ev[1], s));
+    m->stats.kernel_launches += 1;
+    unsigned long long abort_word = 0;
+    SPUMA_CUDA(cudaMemcpyAsync(&abort_word, m->d_loop_bar + 1, sizeof(abort_word), cudaMemcpyDeviceToHost, s));
+    SPUMA_CUDA(cudaStreamSynchronize(s));
+    if (m->timing) {
+        float ms = 0.f;
+        SPUMA_CUDA(cudaEventElapsedTime(&ms, m->loop_ev[0], m->loop_ev[1]));
+        m->stats.loop_ms += ms;
+        m->stats.loop_count += 1;
+    }
+    if (m->loop_profile) {
+        std::vector<unsigned long long> pr((size_t)8 * G);
+        SPUMA_CUDA(cudaMemcpy(pr.data(), m->d_loop_prof, sizeof(unsigned long long) * pr.size(), cudaMemcpyDeviceToHost));
+        for (int ph = 0; ph < 3; ++ph) {
+            double wsum = 0, tsum = 0, wmax = 0;
+            for (int bb = 0; bb < G; ++bb) {
+                wsum += (double)pr[(size_t)bb * 8 + 2 * ph];
+                tsum += (double)pr[(size_t)bb * 8 + 2 * ph + 1];
+                wmax = std::max(wmax, (double)pr[(size_t)bb * 8 + 2 * ph]);
+            }
+            m->stats.loop_work_ms[ph] += wsum / G * 1e-6;
+            m->stats.loop_wait_ms[ph] += tsum / G * 1e-6;
+            m->stats.loop_work_max_ms[ph] += wmax * 1e-6;
+        }
+    }
+    m->stats.loop_mode = m->persistent;
+    m->stats.loop_grid = G;
+    m->stats.loop_tmem_pairs = tp;
+    m->stats.loop_smem_pairs = sp;
+    if (abort_word) return set_error(SPUMA_ERR_STATE, "persistent PCG loop: grid barrier timed out");
+    *ran = true;
+    return SPUMA_OK;
+}
 
 void gamg_release(spuma_mesh m)
 {
@@ -1424,6 +1530,11 @@ void spuma_free(spuma_mesh m)
     if (m->tfork) cudaEventDestroy(m->tfork);
     if (m->tstream) cudaStreamDestroy(m->tstream);
     if (m->ev_join) cudaEventDestroy(m->ev_join);
+    if (m->d_loop_bar) cudaFree(m->d_loop_bar);
+    if (m->d_loop_part) cudaFree(m->d_loop_part);
+    if (m->d_loop_prof) cudaFree(m->d_loop_prof);
+    for (int i = 0; i < 2; ++i)
+        if (m->loop_ev[i]) cudaEventDestroy(m->loop_ev[i]);
     if (m->own_stream && m->stream) cudaStreamDestroy(m->stream);
     delete m;
 }
@@ -1917,7 +2028,12 @@ spuma_status spuma_pcg_solve(spuma_mesh m, const spuma_scalar* diag, const spuma
     if (!fin) SPUMA_TRY(reduce_finalize(m, 2, s));
     m->stats.kernel_launches += 3;
 
-    if (m->external_comm) {  // host callbacks cannot be captured: iterate with direct launches
+    bool looped = false;
+    m->stats.loop_mode = 0;
+    if (loop_eligible(m, a)) SPUMA_TRY(run_pcg_loop(m, s, a, &looped));
+    if (looped) {
+        // the whole loop ran in one launch (scalars in ws.scal)
+    } else if (m->external_comm) {  // host callbacks cannot be captured: iterate with direct launches
         SPUMA_CUDA(cudaMemcpyAsync(&m->h_scal[0], m->ws.scal, sizeof(DevScal), cudaMemcpyDeviceToHost, s));
         SPUMA_CUDA(cudaStreamSynchronize(s));
         int it = 0;
@@ -1930,6 +2046,11 @@ spuma_status spuma_pcg_solve(spuma_mesh m, const spuma_scalar* diag, const spuma
     } else {
     // ---- A7-A11 in captured batches, ping-pong; host reads the scalars once per batch
     SPUMA_TRY(build_graphs(m));
+    {  // the graphs' window makes its target's lines persisting; release another target's first
+        double* const tg[5] = {nullptr, m->ws.pA, m->ws.rA, m->ws.rD, m->ws.wA};
+        if (m->l2_lines && m->l2_lines != tg[m->l2_persist]) SPUMA_CUDA(cudaCtxResetPersistingL2Cache());
+        m->l2_lines = tg[m->l2_persist];
+    }
     SPUMA_CUDA(cudaMemcpyAsync(&m->h_scal[1], m->ws.scal, sizeof(DevScal), cudaMemcpyDeviceToHost, s));
     SPUMA_CUDA(cudaStreamSynchronize(s));
     uint64_t launched_batches = 0;
@@ -2243,6 +2364,18 @@ spuma_status spuma_set_option(spuma_mesh m, int option, int value)
             }
         }
         g_use_pdl = value != 0;
+        return SPUMA_OK;
+    case SPUMA_OPT_LOOP_PROFILE:
+        if (value < 0 || value > 1) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "loop_profile is 0 or 1");
+        m->loop_profile = value != 0;
+        return SPUMA_OK;
+    case SPUMA_OPT_LOOP_L2:
+        if (value < 0 || value > 4) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "loop_l2 is 0..4");
+        m->loop_l2 = value;
+        return SPUMA_OK;
+    case SPUMA_OPT_PERSISTENT:
+        if (value < 0 || value > 3) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "persistent is 0..3");
+        m->persistent = value;
         return SPUMA_OK;
     case SPUMA_OPT_PEER_FUSED:
         if (value < 0 || value > 1) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "peer_fused is 0 or 1");

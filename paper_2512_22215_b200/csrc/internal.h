@@ -118,6 +118,16 @@ struct Workspace {
     PeerState pst;
 };
 
+// The persistent PCG loop (loop.cu, SPUMA_OPT_PERSISTENT)
+struct LoopArgs {
+    unsigned long long* bar;  // [0] grid-barrier arrivals (zeroed before every launch), [1] abort word
+    int tmem_pairs;           // rA pairs per thread held in tensor memory (0: no TMEM)
+    int smem_pairs;           // ... then in shared memory (the rest in HBM)
+    int alt;                  // alternating sweep directions (SPUMA_OPT_ALT_SWEEP)
+    long long spin_limit;     // clock64 cycles a grid barrier waits before it aborts the loop
+    unsigned long long* prof; // [8 * grid] per-CTA phase work / barrier-wait ns (nullptr: off)
+};
+
 // One GAMG level on the device, captured by value.  Level 0 reads its
 // matrix, source and psi through DevPtrs (per-call pointers); its b is Workspace::rA.
 struct GLevel {
@@ -258,8 +268,19 @@ struct spuma_mesh_s {
     bool gamg_csr = true;        // GAMG coarse generic levels as CSR runs (SPUMA_OPT_GAMG_CSR)
     int l2_persist = 2;          // L2 access-policy window (SPUMA_OPT_L2_PERSIST): 0 none, 1 pA, 2 rA (default), 3 rD, 4 wA
     bool l2_limit_set = false;   // the persisting-L2 limit was raised (reset on option off / free)
+    const double* l2_lines = nullptr;  // the vector whose L2 lines the last window made persisting
     bool alt_sweep = true;       // alternate the sweep direction of consecutive hot-loop kernels (L2 reuse)
     int gamg_tail_cells = 512;   // GAMG: levels from the first one at or below this size run in one CTA (0: off)
+    // persistent PCG loop (loop.cu, SPUMA_OPT_PERSISTENT): 0 off, 1 rA in HBM, 2 + shared memory,
+    // 3 + tensor memory (default)
+    int persistent = 3;
+    bool loop_profile = false;   // per-phase work / barrier-wait profile of the loop (SPUMA_OPT_LOOP_PROFILE)
+    int loop_l2 = 4;             // L2 window of the persistent loop (SPUMA_OPT_LOOP_L2, targets as l2_persist): wA
+    unsigned long long* d_loop_bar = nullptr;  // [2] barrier arrivals, abort word
+    double* d_loop_part = nullptr;             // [3 * SMs] CTA partials
+    unsigned long long* d_loop_prof = nullptr; // [8 * SMs] phase work / wait ns (timing on)
+    int loop_grid = 0;                         // SMs (one CTA each), 0 until first use
+    cudaEvent_t loop_ev[2] = {nullptr, nullptr};  // timing of the launch (spuma_set_timing)
     cudaGraphExec_t gexec[2] = {nullptr, nullptr};
     bool gexec_timed = false;
     int gexec_batch = 0;
@@ -387,6 +408,12 @@ void launch_psi_flush(cudaStream_t s, int N, const Workspace& w);
 // SPUMA_OPT_DEFER_PSI = 2: the pending updates j = n - pending .. n - 1 (pending <= 2), p_j in pA if
 // j is even, else pA2; alpha_{n-1} = alpha_prev, alpha_{n-2} = alpha_prev2
 void launch_psi_flush2(cudaStream_t s, int N, const Workspace& w, int n, int pending);
+// loop.cu: the persistent PCG loop (one cooperative launch per solve)
+int loop_threads();
+int loop_tmem_pairs();
+int loop_occupancy(int K, size_t smem);
+cudaError_t launch_pcg_loop(cudaStream_t s, int grid, size_t smem, const MeshArgs& a, const Workspace& w,
+                            const LoopArgs& L, const cudaAccessPolicyWindow* win);
 // A11+A7+A8 in one kernel (ELL, single rank, deferred psi): see kernels.cu
 bool fused_direction_ok(const MeshArgs& a);
 void launch_amul_dot_dir(cudaStream_t s, const MeshArgs& a, const Workspace& w, bool inline_rd);  // psi += alpha_prev pA (pending update)

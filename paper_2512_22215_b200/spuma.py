@@ -37,6 +37,9 @@ OPT_GAMG_CSR = 9
 OPT_PEER_POLL_MS = 10
 OPT_SMALL_SMEM = 11
 OPT_PEER_FUSED = 12
+OPT_PERSISTENT = 13
+OPT_LOOP_L2 = 14
+OPT_LOOP_PROFILE = 15
 PEER_BLOB_BYTES = 512  # SPUMA_PEER_BLOB_BYTES
 AMUL_VARIANTS = (0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13)
 
@@ -118,12 +121,16 @@ class Stats(ctypes.Structure):
     _fields_ = [("kernel_launches", ctypes.c_uint64), ("solves", ctypes.c_uint64), ("iterations", ctypes.c_uint64),
                 ("timing_enabled", _ci), ("phase_ms", _cd * 4), ("phase_count", ctypes.c_uint64 * 4),
                 ("blocks_per_grid", _ci), ("threads_per_block", _ci), ("batch_iterations", _ci),
-                ("amul_variant", _ci)]
+                ("amul_variant", _ci), ("loop_mode", _ci), ("loop_grid", _ci), ("loop_tmem_pairs", _ci),
+                ("loop_smem_pairs", _ci), ("loop_ms", _cd), ("loop_count", ctypes.c_uint64),
+                ("loop_work_ms", _cd * 3), ("loop_wait_ms", _cd * 3), ("loop_work_max_ms", _cd * 3)]
 
     def as_dict(self):
         d = {k: getattr(self, k) for k, _ in self._fields_}
         d["phase_ms"] = list(self.phase_ms)
         d["phase_count"] = list(self.phase_count)
+        for k in ("loop_work_ms", "loop_wait_ms", "loop_work_max_ms"):
+            d[k] = list(getattr(self, k))
         return d
 
 

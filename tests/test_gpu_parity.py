@@ -289,6 +289,7 @@ def test_pcg_deterministic_and_host_pointers():
 def test_timing_and_stats():
     m = gen.cube(20)
     h = P.Mesh.from_mesh(m)
+    h.set_option(P.spuma.OPT_PERSISTENT, 0)  # the captured graph batches (the loop: test_gpu_persistent)
     h.set_timing(True)
     _, perf, _, _ = gpu_solve_case(m, None, gen.rhs(m), 0, handle=h)
     st = h.get_stats()
@@ -476,6 +477,7 @@ def test_deferred_psi_in_direction_lattice_and_psi0(iters):
     out = []
     for defer in (0, 2):
         h = P.Mesh.from_mesh(m)
+        h.set_option(P.spuma.OPT_PERSISTENT, 0)  # graph batches on both sides (same reduction shape)
         h.set_option(P.spuma.OPT_DEFER_PSI, defer)
         out.append(gpu_solve_case(m, g, b, 0, (0.0, 0.0, iters, iters), psi0=psi0, handle=h)[:2])
         h.free()
