@@ -14,8 +14,10 @@ setup + A7-A11 iterations to convergence + A12).  value = global cells *
 PCG iterations / step time (max over ranks).  Inputs (8M cells, ~1.3 GB per
 iteration) are far larger than the 126 MB L2, so no L2 flush is needed.
 
-Also reported: roofline of the dominant kernel (the Amul, A7), timed live
-with CUDA events over the timed region; e2e through the C-ABI with host
+Also reported: roofline of the dominant kernel (the persistent PCG loop
+k_pcg_loop -- every A7-A11 iteration of a solve in one launch -- or, with the
+graph batches, the Amul k_amul_dot), timed live with CUDA events over the
+timed region; e2e through the C-ABI with host
 buffers; clocks under load; our kernel launch count; and the CPU oracle
 (cpu_baseline) on a bounded sample of the same workload.
 

@@ -373,6 +373,22 @@ __device__ __forceinline__ void amul_rows_ell(const MeshArgs& a, int c, int wn, 
     }
 }
 
+#ifndef SPUMA_LOOP_XLD
+#define SPUMA_LOOP_XLD 0  // A/B of the persistent loop's coherent loads: 0 ld.global, 1 ld.global.cg (L2 only)
+#endif
+template <bool NC>
+__device__ __forceinline__ double ldx(const double* p)
+{
+    if constexpr (NC) return __ldg(p);
+    double v;
+#if SPUMA_LOOP_XLD == 1
+    asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(p));
+#else
+    asm volatile("ld.global.f64 %0, [%1];" : "=d"(v) : "l"(p));  // volatile: stays behind the barriers
+#endif
+    return v;
+}
+
 // Variant 10: the ELL rows of variant 8 software-pipelined across the grid-stride loop -- the
 // first-level loads of the thread's NEXT row (diag, x, the six slots, the owner-side
 // coefficients) are issued before the second-level gathers of the current row, so two rows'
@@ -386,13 +402,14 @@ struct EllL1 {
     double uo[3];
 };
 
+template <bool NC = true>
 __device__ __forceinline__ void ell_load1(const MeshArgs& a, int c, int wn, int wo, const double* __restrict__ diag,
                                           const double* __restrict__ upper_s, const double* __restrict__ x, EllL1& L)
 {
     L.c = c;
     const int cc = min(c, a.N - 1), k = cc >> 5, l = c & 31;
     L.dg = __ldg(diag + cc);
-    L.xc = __ldg(x + cc);
+    L.xc = ldx<NC>(x + cc);
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
         L.pk[j] = j < wn ? __ldg(a.sell_n + (size_t)32 * wn * k + 32 * j + l) : 0xFFFFFFFFu;
@@ -401,7 +418,7 @@ __device__ __forceinline__ void ell_load1(const MeshArgs& a, int c, int wn, int 
     }
 }
 
-template <int IFM>
+template <int IFM, bool NC = true>
 __device__ __forceinline__ void ell_finish(const MeshArgs& a, const EllL1& L, int wo, const double* __restrict__ upper_s,
                                            const double* __restrict__ iface, const double* __restrict__ x,
                                            const double* __restrict__ xr, double* __restrict__ y, double& acc, bool dot)
@@ -414,8 +431,8 @@ __device__ __forceinline__ void ell_finish(const MeshArgs& a, const EllL1& L, in
         const int col = vn ? (int)(L.pk[j] >> 5) : cc;
         const int pos = (int)(L.pk[j] & 31u);
         un[j] = vn ? __ldg(upper_s + (size_t)32 * wo * (col >> 5) + 32 * pos + (col & 31)) : 0.0;
-        xn[j] = __ldg(x + col);
-        xo[j] = __ldg(x + (L.nb[j] >= 0 ? L.nb[j] : cc));
+        xn[j] = ldx<NC>(x + col);
+        xo[j] = ldx<NC>(x + (L.nb[j] >= 0 ? L.nb[j] : cc));
     }
     double s = L.dg * L.xc;
 #pragma unroll
@@ -483,22 +500,6 @@ __device__ __forceinline__ bool lat_present(double u)
 // measured 0.3 % slower and removed, profiles/r02_lattice_ab.md)
 // x loads of the lattice rows: the read-only path, or (NC = false, the persistent loop of loop.cu,
 // where x is rewritten between grid barriers inside one launch) plain coherent loads
-#ifndef SPUMA_LOOP_XLD
-#define SPUMA_LOOP_XLD 0  // A/B of the persistent loop's coherent loads: 0 ld.global, 1 ld.global.cg (L2 only)
-#endif
-template <bool NC>
-__device__ __forceinline__ double ldx(const double* p)
-{
-    if constexpr (NC) return __ldg(p);
-    double v;
-#if SPUMA_LOOP_XLD == 1
-    asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(p));
-#else
-    asm volatile("ld.global.f64 %0, [%1];" : "=d"(v) : "l"(p));  // volatile: stays behind the barriers
-#endif
-    return v;
-}
-
 template <int R, int IFM, int KT, bool NC = true>
 __device__ __forceinline__ void lat_chunk(const MeshArgs& a, int K, int ch, const double* __restrict__ diag,
                                           const double* const (&ud)[3], const double* __restrict__ iface,

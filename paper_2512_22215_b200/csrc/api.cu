@@ -546,13 +546,24 @@ void destroy_graphs(spuma_mesh m)
 // An L2 access-policy window (persisting hits, streaming misses) over one workspace vector
 // (1 pA, 2 rA, 3 rD, 4 wA), with the device-wide persisting-L2 limit raised to cover it.  The lines
 // another target left persisting are released first (they would hold the set-aside otherwise).
-spuma_status l2_policy(spuma_mesh m, int target, cudaAccessPolicyWindow* out)
+// *use = false when the vector does not fit the persisting set-aside (a partly persisting window
+// over a larger vector thrashes: 252^3 graph batches 314 -> 379 us per iteration, C4 64M 1525 ->
+// 2378 us, profiles/r02x2_*): no window then.
+spuma_status l2_policy(spuma_mesh m, int target, cudaAccessPolicyWindow* out, bool* use)
 {
     int dev = 0, maxp = 0, maxw = 0;
     SPUMA_CUDA(cudaGetDevice(&dev));
     SPUMA_CUDA(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev));
     SPUMA_CUDA(cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, dev));
     const size_t win = std::min((size_t)maxw, sizeof(double) * (size_t)m->N);
+    *use = win <= (size_t)maxp && sizeof(double) * (size_t)m->N <= (size_t)maxw;
+    if (!*use) {
+        if (m->l2_lines) {
+            SPUMA_CUDA(cudaCtxResetPersistingL2Cache());
+            m->l2_lines = nullptr;
+        }
+        return SPUMA_OK;
+    }
     SPUMA_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min((size_t)maxp, win)));
     m->l2_limit_set = true;
     double* const tg[5] = {nullptr, m->ws.pA, m->ws.rA, m->ws.rD, m->ws.wA};
@@ -577,7 +588,9 @@ spuma_status l2_window(spuma_mesh m, cudaStreamAttrValue* saved)
     cudaStreamAttrValue v{};
     if (!m->l2_persist || m->N == 0) return SPUMA_OK;
     SPUMA_CUDA(cudaStreamGetAttribute(m->stream, cudaStreamAttributeAccessPolicyWindow, saved));
-    SPUMA_TRY(l2_policy(m, m->l2_persist, &v.accessPolicyWindow));
+    bool use = false;
+    SPUMA_TRY(l2_policy(m, m->l2_persist, &v.accessPolicyWindow, &use));
+    if (!use) v.accessPolicyWindow = cudaAccessPolicyWindow{};  // num_bytes 0: no window on the captured nodes
     SPUMA_CUDA(cudaStreamSetAttribute(m->stream, cudaStreamAttributeAccessPolicyWindow, &v));
     return SPUMA_OK;
 }
@@ -688,18 +701,24 @@ struct GamgState {
 namespace {
 
 // SPUMA_OPT_PERSISTENT: can this solve run as one cooperative launch (loop.cu)?
-bool loop_eligible(spuma_mesh m, const MeshArgs& a)
+// layout of the loop's Amul: 1 lattice slots, 2 ELL rows, 0 = not eligible
+int loop_layout(spuma_mesh m, const MeshArgs& a)
 {
-    return m->persistent > 0 && m->n_ranks == 1 && !m->external_comm && m->defer_psi == 2 && m->N > 0 &&
-           (resolve_amul_variant(m->amul_variant, a) == 12 || resolve_amul_variant(m->amul_variant, a) == 13) &&
-           (a.lat_K == 3 || a.lat_K == 2 || a.lat_K == 1);
+    if (!(m->persistent > 0 && m->n_ranks == 1 && !m->external_comm && m->defer_psi == 2 && m->N > 0)) return 0;
+    const int rv = resolve_amul_variant(m->amul_variant, a);
+    if ((rv == 12 || rv == 13) && a.lat_K >= 1 && a.lat_K <= 3) return 1;
+    if ((rv == 8 || rv == 10) && a.upper_s && !m->ell_stencil && a.ell_wn >= 0 && a.ell_wn <= 3 && a.ell_wo >= 0 &&
+        a.ell_wo <= 3)
+        return 2;
+    return 0;
 }
 
 // A7-A11 of the whole solve in one cooperative launch after the A6 setup; *ran = false when the
 // device cannot host it (the caller then runs the graph batches)
-spuma_status run_pcg_loop(spuma_mesh m, cudaStream_t s, const MeshArgs& a, bool* ran)
+spuma_status run_pcg_loop(spuma_mesh m, cudaStream_t s, const MeshArgs& a, int layout, bool* ran)
 {
     *ran = false;
+    const int kkey = layout == 2 ? 0 : a.lat_K;  // loop_fn key: lattice K, 0 = ELL rows
     const int T = loop_threads();
     if (!m->loop_grid) {
         int dev = 0, sms = 0;
@@ -718,8 +737,8 @@ spuma_status run_pcg_loop(spuma_mesh m, cudaStream_t s, const MeshArgs& a, bool*
     const int sp_cap = (200 * 1024) / (T * (int)sizeof(double2));  // <= 200 KB of shared memory
     int sp = m->persistent >= 2 ? std::min(need - tp, sp_cap) : 0;
     size_t smem = (size_t)sp * T * sizeof(double2);
-    if (loop_occupancy(a.lat_K, smem) < 1) {
-        if (loop_occupancy(a.lat_K, 0) < 1) return SPUMA_OK;  // cannot run here: graph batches
+    if (loop_occupancy(kkey, smem) < 1) {
+        if (loop_occupancy(kkey, 0) < 1) return SPUMA_OK;  // cannot run here: graph batches
         sp = 0;
         smem = 0;
     }
@@ -739,13 +758,21 @@ spuma_status run_pcg_loop(spuma_mesh m, cudaStream_t s, const MeshArgs& a, bool*
     SPUMA_CUDA(cudaMemsetAsync(m->d_loop_bar, 0, 2 * sizeof(unsigned long long), s));
     if (m->timing) SPUMA_CUDA(cudaEventRecord(m->loop_ev[0], s));
     cudaAccessPolicyWindow win{};
+    bool use_win = false;
     if (m->loop_l2) {
-        SPUMA_TRY(l2_policy(m, m->loop_l2, &win));
+        SPUMA_TRY(l2_policy(m, m->loop_l2, &win, &use_win));
     } else if (m->l2_lines) {  // lines a graph window left persisting would hold the set-aside
         SPUMA_CUDA(cudaCtxResetPersistingL2Cache());
         m->l2_lines = nullptr;
     }
-    SPUMA_CUDA(launch_pcg_loop(s, G, smem, a, w, L, m->loop_l2 ? &win : nullptr));
+    {
+        const cudaError_t e = launch_pcg_loop(s, G, smem, a, w, L, use_win ? &win : nullptr, layout == 2);
+        if (e == cudaErrorCooperativeLaunchTooLarge) {  // SMs taken (e.g. MPS limits): graph batches instead
+            cudaGetLastError();
+            return SPUMA_OK;
+        }
+        SPUMA_CUDA(e);
+    }
     if (m->timing) SPUMA_CUDA(cudaEventRecord(m->loop_ev[1], s));
     m->stats.kernel_launches += 1;
     unsigned long long abort_word = 0;
@@ -2030,7 +2057,7 @@ spuma_status spuma_pcg_solve(spuma_mesh m, const spuma_scalar* diag, const spuma
 
     bool looped = false;
     m->stats.loop_mode = 0;
-    if (loop_eligible(m, a)) SPUMA_TRY(run_pcg_loop(m, s, a, &looped));
+    if (const int lay = loop_layout(m, a)) SPUMA_TRY(run_pcg_loop(m, s, a, lay, &looped));
     if (looped) {
         // the whole loop ran in one launch (scalars in ws.scal)
     } else if (m->external_comm) {  // host callbacks cannot be captured: iterate with direct launches
@@ -2046,10 +2073,12 @@ spuma_status spuma_pcg_solve(spuma_mesh m, const spuma_scalar* diag, const spuma
     } else {
     // ---- A7-A11 in captured batches, ping-pong; host reads the scalars once per batch
     SPUMA_TRY(build_graphs(m));
-    {  // the graphs' window makes its target's lines persisting; release another target's first
+    if (m->l2_persist) {  // the graphs' window makes its target's lines persisting; release another target's first
         double* const tg[5] = {nullptr, m->ws.pA, m->ws.rA, m->ws.rD, m->ws.wA};
-        if (m->l2_lines && m->l2_lines != tg[m->l2_persist]) SPUMA_CUDA(cudaCtxResetPersistingL2Cache());
-        m->l2_lines = tg[m->l2_persist];
+        cudaAccessPolicyWindow unused{};
+        bool use = false;
+        SPUMA_TRY(l2_policy(m, m->l2_persist, &unused, &use));  // also releases stale lines when no window
+        if (use) m->l2_lines = tg[m->l2_persist];
     }
     SPUMA_CUDA(cudaMemcpyAsync(&m->h_scal[1], m->ws.scal, sizeof(DevScal), cudaMemcpyDeviceToHost, s));
     SPUMA_CUDA(cudaStreamSynchronize(s));

@@ -69,6 +69,12 @@ __device__ __forceinline__ void tm_st(uint32_t addr, double2 v)
 
 __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
+#ifndef SPUMA_LOOP_ELL_PIPE
+#define SPUMA_LOOP_ELL_PIPE 0  // A/B: the ELL rows software-pipelined (variant 10; spills at 64 registers)
+#endif
+#ifndef SPUMA_LOOP_POLL
+#define SPUMA_LOOP_POLL 0  // A/B: 0 acquire poll, 1 relaxed poll + fence, 2 acquire poll with 32 ns back-off
+#endif
 #ifndef SPUMA_LOOP_BAR
 #define SPUMA_LOOP_BAR 1  // A/B: 0 fence + atomicAdd + acquire poll + fence, 1 red.release + acquire poll
 #endif
@@ -139,8 +145,19 @@ __device__ __forceinline__ bool grid_bar(const LoopArgs& L, unsigned long long t
         unsigned spins = 0;
         for (;;) {
             unsigned long long v;
+#if SPUMA_LOOP_POLL == 1
+            asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(L.bar) : "memory");
+            if (v >= target) {
+                asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                break;
+            }
+#else
             asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(L.bar) : "memory");
             if (v >= target) break;
+#if SPUMA_LOOP_POLL == 2
+            __nanosleep(32);
+#endif
+#endif
             if ((++spins & 63u) == 0u &&
                 (*reinterpret_cast<volatile unsigned long long*>(L.bar + 1) || clock64() - t0 > L.spin_limit)) {
                 atomicExch(L.bar + 1, 1ull);
@@ -207,7 +224,10 @@ __device__ __forceinline__ void grid_sums(const double* part, int off, double (&
     }
 }
 
-template <int KT>
+// KT: the lattice offset count at compile time (0: a.lat_K at run time); ELL: the Amul runs over
+// the ELL rows of variant 10 (uniform slot widths <= 3, per-solve coefficient copy upper_s) on a
+// mesh that is not a lattice numbering (C2 / C4 renumbered by RCM)
+template <int KT, bool ELL>
 __global__ void __launch_bounds__(kT, 1) k_pcg_loop(MeshArgs a, Workspace w, LoopArgs L)
 {
     extern __shared__ double2 rs[];
@@ -271,21 +291,25 @@ __global__ void __launch_bounds__(kT, 1) k_pcg_loop(MeshArgs a, Workspace w, Loo
             const bool psi = n >= 2 && !(n & 1);
             const double beta = S.beta, a1 = S.alpha_prev, a2 = S.alpha_prev2;
             // one tile ahead: the next tile's rD / pA_prev loads are in flight while this one computes
-            double2 dn = make_double2(0.0, 0.0), pn = dn;
+            // (rA pairs kept in HBM -- meshes beyond the on-chip capacity -- are loaded here too)
+            double2 dn = make_double2(0.0, 0.0), pn = dn, rn = dn;
+            const int kon = R.tp + R.sp;
             auto pf = [&](int j) {
-                const int i = (b + (odd ? nk - 1 - j : j) * G) * kT + t;
+                const int kk = odd ? nk - 1 - j : j;
+                const int i = (b + kk * G) * kT + t;
                 if (i < np) {
                     dn = __ldg(rD2 + i);
                     if (!first) pn = ld2(pp2 + i);
+                    if (kk >= kon) rn = R.g[i];
                 }
             };
             if (nk > 0) pf(0);
             for (int j = 0; j < nk; ++j) {
                 const int k = odd ? nk - 1 - j : j;
                 const int i = (b + k * G) * kT + t;
-                const double2 d = dn, p = pn;
+                const double2 d = dn, p = pn, rh = rn;
                 if (j + 1 < nk) pf(j + 1);
-                const double2 r = R.load(k, i < np ? i : 0);
+                const double2 r = k < kon ? R.load(k, 0) : rh;
                 if (i < np) {
                     double2 q;
                     if (first) {
@@ -324,9 +348,28 @@ __global__ void __launch_bounds__(kT, 1) k_pcg_loop(MeshArgs a, Workspace w, Loo
             const int nch = (N + 31) / 32;
             const int cnt = wid < nch ? (nch - 1 - wid) / nw + 1 : 0;
             double acc = 0.0;
-            for (int j = 0; j < cnt; ++j) {
-                const int ch = wid + (rev ? cnt - 1 - j : j) * nw;
-                lat_chunk<1, 0, KT, false>(a, K, ch, P.diag, ud, nullptr, pc, nullptr, w.wA, acc, true);
+            if constexpr (ELL && SPUMA_LOOP_ELL_PIPE) {  // variant 10's rows (next row's first-level loads ahead)
+                const int wn = a.ell_wn, wo = a.ell_wo, lane = t & 31;
+                EllL1 cur, nxt;
+                if (cnt > 0) ell_load1<false>(a, (wid + (rev ? cnt - 1 : 0) * nw) * 32 + lane, wn, wo, P.diag, a.upper_s, pc, cur);
+                for (int j = 0; j < cnt; ++j) {
+                    if (j + 1 < cnt)
+                        ell_load1<false>(a, (wid + (rev ? cnt - 2 - j : j + 1) * nw) * 32 + lane, wn, wo, P.diag, a.upper_s, pc, nxt);
+                    ell_finish<0, false>(a, cur, wo, a.upper_s, nullptr, pc, nullptr, w.wA, acc, true);
+                    cur = nxt;
+                }
+            } else if constexpr (ELL) {  // variant 8's rows: one row's loads at a time (64 registers)
+                const int wn = a.ell_wn, wo = a.ell_wo, lane = t & 31;
+                for (int j = 0; j < cnt; ++j) {
+                    EllL1 cur;
+                    ell_load1<false>(a, (wid + (rev ? cnt - 1 - j : j) * nw) * 32 + lane, wn, wo, P.diag, a.upper_s, pc, cur);
+                    ell_finish<0, false>(a, cur, wo, a.upper_s, nullptr, pc, nullptr, w.wA, acc, true);
+                }
+            } else {
+                for (int j = 0; j < cnt; ++j) {
+                    const int ch = wid + (rev ? cnt - 1 - j : j) * nw;
+                    lat_chunk<1, 0, KT, false>(a, K, ch, P.diag, ud, nullptr, pc, nullptr, w.wA, acc, true);
+                }
             }
             double v[1] = {acc};
             cta_reduce<1>(v, sh);
@@ -347,21 +390,24 @@ __global__ void __launch_bounds__(kT, 1) k_pcg_loop(MeshArgs a, Workspace w, Loo
             const double alpha = S.alpha;
             const double2* wA2 = reinterpret_cast<const double2*>(w.wA);
             double v[2] = {0.0, 0.0};
-            double2 wn = make_double2(0.0, 0.0), dn = wn;
+            double2 wn = make_double2(0.0, 0.0), dn = wn, rn = wn;
+            const int kon = R.tp + R.sp;
             auto pf = [&](int j) {
-                const int i = (b + (odd ? nk - 1 - j : j) * G) * kT + t;
+                const int kk = odd ? nk - 1 - j : j;
+                const int i = (b + kk * G) * kT + t;
                 if (i < np) {
                     wn = ld2(wA2 + i);
                     dn = __ldg(rD2 + i);
+                    if (kk >= kon) rn = R.g[i];
                 }
             };
             if (nk > 0) pf(0);
             for (int j = 0; j < nk; ++j) {
                 const int k = odd ? nk - 1 - j : j;
                 const int i = (b + k * G) * kT + t;
-                const double2 ww = wn, d = dn;
+                const double2 ww = wn, d = dn, rh = rn;
                 if (j + 1 < nk) pf(j + 1);
-                double2 r = R.load(k, i < np ? i : 0);
+                double2 r = k < kon ? R.load(k, 0) : rh;
                 if (i < np) {
                     r.x = r.x - alpha * ww.x;
                     r.y = r.y - alpha * ww.y;
@@ -422,7 +468,12 @@ __global__ void __launch_bounds__(kT, 1) k_pcg_loop(MeshArgs a, Workspace w, Loo
 int loop_threads() { return ploop::kT; }
 int loop_tmem_pairs() { return ploop::kTmemPairs; }
 
-static void* loop_fn(int K) { return K == 3 ? (void*)ploop::k_pcg_loop<3> : (void*)ploop::k_pcg_loop<0>; }
+// K: the lattice offset count, 0 = the ELL rows
+static void* loop_fn(int K)
+{
+    return K == 3 ? (void*)ploop::k_pcg_loop<3, false>
+                  : (K > 0 ? (void*)ploop::k_pcg_loop<0, false> : (void*)ploop::k_pcg_loop<0, true>);
+}
 
 // CTAs per SM the loop kernel reaches with `smem` bytes of dynamic shared memory (0: it
 // cannot run, e.g. the shared-memory request is too large)
@@ -442,7 +493,7 @@ int loop_occupancy(int K, size_t smem)
 }
 
 cudaError_t launch_pcg_loop(cudaStream_t s, int grid, size_t smem, const MeshArgs& a, const Workspace& w,
-                            const LoopArgs& L, const cudaAccessPolicyWindow* win)
+                            const LoopArgs& L, const cudaAccessPolicyWindow* win, bool ell)
 {
     MeshArgs aa = a;
     Workspace ww = w;
@@ -464,7 +515,7 @@ cudaError_t launch_pcg_loop(cudaStream_t s, int grid, size_t smem, const MeshArg
     cfg.stream = s;
     cfg.attrs = attr;
     cfg.numAttrs = na;
-    return cudaLaunchKernelExC(&cfg, loop_fn(a.lat_K), args);
+    return cudaLaunchKernelExC(&cfg, loop_fn(ell ? 0 : a.lat_K), args);
 }
 
 }  // namespace spuma

@@ -30,9 +30,21 @@ PEAK = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if 
 f64 = dict(dtype=torch.float64, device="cuda")
 
 
+MODES = [None]  # --modes=0,3: every case once per SPUMA_OPT_PERSISTENT value (None: the library default)
+
+
 def run_case(name, mesh, gamma, b, ref=0, renumber=False, ctl=(1e-6, 0.0, 5000, 0), reps=3, extra=None):
+    out = None
+    for mode in MODES:
+        out = run_case1(name, mesh, gamma, b, ref, renumber, ctl, reps, dict(extra or {}), mode)
+    return out
+
+
+def run_case1(name, mesh, gamma, b, ref, renumber, ctl, reps, extra, mode):
     t0 = time.perf_counter()
     h = P.Mesh.from_mesh(mesh, renumber=renumber, stream=torch.cuda.current_stream().cuda_stream)
+    if mode is not None:
+        h.set_option(P.spuma.OPT_PERSISTENT, mode)
     t_create = time.perf_counter() - t0
     N, F = mesh.n_cells, mesh.n_faces
     diag, upper = torch.empty(N, **f64), torch.empty(F, **f64)
@@ -79,8 +91,20 @@ def run_case(name, mesh, gamma, b, ref=0, renumber=False, ctl=(1e-6, 0.0, 5000, 
            "amul_frac_of_measured_peak": B_A / (amul_ms / 1e3) / 1e9 / PEAK if amul_ms else None,
            "assembly_alg_GBps": (56 * F + 24 * N) / t_asm / 1e9,
            "peak_GBps": PEAK}
-    if extra:
-        out.update(extra)
+    if st["loop_mode"]:  # the persistent loop ran: its own time and bytes (bench.py loop_bytes)
+        import bench
+        T = 1024
+        need = -(-(-(-(N // 2) // T)) // max(st["loop_grid"], 1))
+        frac = min(1.0, (st["loop_tmem_pairs"] + st["loop_smem_pairs"]) / need) if need else 1.0
+        lb = bench.loop_bytes(N, K, frac) if K else None
+        loop_ms = st["loop_ms"] / max(st["loop_count"], 1)
+        out.update({"loop_mode": st["loop_mode"], "loop_us_per_iter": 1e3 * loop_ms / max(n_it, 1),
+                    "loop_rA_resident_frac": frac, "loop_bytes_per_iter": lb["iter"] if lb else None,
+                    "loop_GBps": lb["iter"] * n_it / (loop_ms / 1e3) / 1e9 if lb and loop_ms else None})
+    else:
+        out["loop_mode"] = 0
+    out["persistent_option"] = mode
+    out.update(extra)
     print(json.dumps(out), flush=True)
     h.free()
     return out
@@ -131,6 +155,8 @@ if __name__ == "__main__":
     for a in args:
         if a.startswith("--c5="):
             ns = [int(x) for x in a.split("=")[1].split(",")]
+        if a.startswith("--modes="):
+            MODES[:] = [int(x) for x in a.split("=")[1].split(",")]
     todo = [a for a in args if not a.startswith("--")] or ["C1", "C2", "C5", "C4"]
     for t in todo:
         {"C1": c1, "C2": c2, "C4": c4, "C5": lambda: c5(ns)}[t]()

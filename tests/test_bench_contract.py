@@ -35,3 +35,26 @@ def test_algorithmic_bytes_are_survey_8d():
     assert nb["iter"] == nb["A"] + nb["B"] + nb["C"] == 1_278_080_000
     peak, kind = bench.peaks()
     assert peak > 1000 and isinstance(kind, str)
+
+
+def test_loop_bytes_count_the_on_chip_residual_once():
+    """The persistent loop's bytes per iteration: 100 B/cell on a K = 3 lattice with
+    rA fully on chip (C 36 = rD + pA_prev + pA + half of the psi pair's 24; A 48; B 16 = wA + rD);
+    every pair of rA left in HBM adds its 24 B (read + write in the update, read in the direction)."""
+    import bench
+    N = 8_000_000
+    full = bench.loop_bytes(N, 3, 1.0)
+    assert full["C"] == 36 * N and full["A"] == 48 * N and full["B"] == 16 * N and full["iter"] == 100 * N
+    assert full["per_launch_fixed"] == 16 * N  # rA loaded once and written back once per launch
+    none = bench.loop_bytes(N, 3, 0.0)
+    assert none["iter"] == 124 * N  # = the graph batches' 124 B/cell with the psi pairs in the direction
+    half = bench.loop_bytes(N, 3, 0.5)
+    assert half["iter"] == 112 * N
+
+
+def test_traffic_lookup_names_the_kernel():
+    import bench
+    w = "C3 cube 200^3 per GPU (weak), gamma=1, tol 1e-6"
+    t = bench.load_traffic(w, "k_pcg_loop")
+    assert t is None or t > 1e11  # one launch = the whole solve
+    assert bench.load_traffic("another workload", "k_pcg_loop") is None

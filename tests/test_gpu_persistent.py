@@ -39,8 +39,8 @@ def _solve(h, diag, upper, src, ctl, mode, loop_l2=None, psi0=None):
     return psi.cpu().numpy(), perf, h.get_stats()
 
 
-def _assembled(m, gamma=None, ref=0):
-    h = P.Mesh.from_mesh(m)
+def _assembled(m, gamma=None, ref=0, renumber=False):
+    h = P.Mesh.from_mesh(m, renumber=renumber)
     h.set_option(OPT.OPT_SMALL_SOLVE_MAX_CELLS, 0)  # small meshes through the big-mesh path too
     diag, upper = torch.empty(m.n_cells, **F64), torch.empty(m.n_faces, **F64)
     src = torch.as_tensor(gen.rhs(m), **F64)
@@ -209,3 +209,42 @@ def test_psi_pairs_and_final_flush_with_psi0(iters):
     assert out[0][1]["n_iterations"] == out[1][1]["n_iterations"] == iters
     d = np.abs(out[0][0] - out[1][0]).max() / np.abs(out[0][0]).max()
     assert d <= 1e-13, d
+
+
+ELL_MESHES = [("cube30-permuted-rcm", lambda: gen.permute(gen.cube(30), seed=3)),
+              ("perturbed24-permuted-rcm", lambda: gen.permute(gen.perturbed(24, 0.2), seed=5)),
+              ("box-odd-permuted-rcm", lambda: gen.permute(gen.box(29, 23, 17), seed=7))]
+
+
+@pytest.mark.parametrize("name,make", ELL_MESHES, ids=[c[0] for c in ELL_MESHES])
+def test_ell_rows_loop(name, make):
+    """Meshes that are not lattice numberings (C2 / C4: permuted, renumbered by RCM): the loop's
+    Amul runs over the ELL rows (variant 10's slots) -- modes bitwise equal, the graph batches
+    within 1e-12 at the same count, the oracle within the north_star bar (Q11)."""
+    m = make()
+    h, diag, upper, src = _assembled(m, renumber=True)
+    assert h.get_stats()["amul_variant"] == 10
+    ctl = (1e-8, 0.0, 5000, 0)
+    psi0, p0, _ = _solve(h, diag, upper, src, ctl, 0)
+    outs = []
+    for mode in (1, 3):
+        psi, p, s = _solve(h, diag, upper, src, ctl, mode)
+        assert s["loop_mode"] == mode, s
+        assert p["n_iterations"] == p0["n_iterations"], (p, p0)
+        assert np.linalg.norm(psi - psi0) / np.linalg.norm(psi0) <= 1e-12
+        outs.append(psi)
+    assert np.array_equal(_bits(outs[0]), _bits(outs[1]))
+    h.free()
+    # oracle (caller numbering; the handle renumbers internally)
+    g, b = gen.gamma_lognormal(m), gen.rhs(m)
+    hh = P.Mesh.from_mesh(m, renumber=True)
+    hh.set_option(OPT.OPT_SMALL_SOLVE_MAX_CELLS, 0)
+    psi_g, pg, _, _ = gpu_solve_case(m, g, b, 0, ctl, renumber=True, handle=hh)
+    assert hh.get_stats()["loop_mode"] == 3
+    psi_o, po, _ = O.solve_case(m, g, b, 0, 0.0, O.controls(*ctl))
+    assert pg["converged"] and abs(pg["n_iterations"] - po["n_iterations"]) <= 2, (pg, po)
+    n = min(pg["n_iterations"], po["n_iterations"])
+    psi_g, _, _, _ = gpu_solve_case(m, g, b, 0, (0.0, 0.0, n, n), renumber=True, handle=hh)
+    psi_o, _, _ = O.solve_case(m, g, b, 0, 0.0, O.controls(0.0, 0.0, n, n))
+    assert np.linalg.norm(psi_g - psi_o) / np.linalg.norm(psi_o) <= 1e-9
+    hh.free()
