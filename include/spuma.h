@@ -504,7 +504,7 @@ typedef enum {
     SPUMA_OPT_GAMG_CSR = 9,
     /* peer transport: how long a kernel polls for a neighbour's flag before it gives up, in
      * milliseconds (approximate: SM clocks at 2 GHz); default 20000.  The call that saw the
-     * timeout returns SPUMA_ERR_STATE. */
+     * timeout returns SPUMA_ERR_STATE.  Also the persistent loop's grid-barrier limit. */
     SPUMA_OPT_PEER_POLL_MS = 10,
     /* the single-CTA small solve (SPUMA_OPT_SMALL_SOLVE_MAX_CELLS) with the matrix, addressing,
      * vectors and scalars staged in shared memory when they fit (about 1700 cells of a 3-D hex
@@ -515,13 +515,17 @@ typedef enum {
      * last CTA (4 kernels per iteration instead of 7); 1 = on (default), 0 = separate kernels.
      * Bitwise the same iterates. */
     SPUMA_OPT_PEER_FUSED = 12,
-    /* single-rank PCG on a lattice numbering (Amul variant 12, deferred psi pairs): run every
+    /* single-rank PCG (lattice or ELL layout, deferred psi pairs in the direction): run every
      * iteration of a solve in ONE cooperative launch of one 1024-thread CTA per SM, three grid
      * barriers per iteration, each CTA finalising the scalars itself; the residual rA stays on
      * the SM: 0 = off (captured graph batches), 1 = persistent, rA in HBM, 2 = rA in shared
      * memory (the rest in HBM), 3 = rA in tensor memory + shared memory (default; ~8.8M cells
-     * fully on chip on 148 SMs).  Same element arithmetic as the graph path; the dot products
-     * are summed in another fixed shape (iterates equal to rounding, deterministic). */
+     * fully on chip on 148 SMs).  Modes 2 and 3 fall back to the graph batches when less than
+     * half of rA fits on chip (meshes above ~17M cells), and any mode when the cooperative launch
+     * does not fit the device.  The Amul runs over the lattice slots (variant 12) or, on other
+     * meshes, over the ELL rows (variant 8/10 layout).  Same element arithmetic as the graph
+     * path; the dot products are summed in another fixed shape (iterates equal to rounding,
+     * deterministic). */
     SPUMA_OPT_PERSISTENT = 13,
     /* the persistent loop's L2 access-policy window (persisting hits), targets as
      * SPUMA_OPT_L2_PERSIST: 0 = none, 1 = pA, 2 = rA, 3 = rD, 4 = wA (default).  Same-box A/B at

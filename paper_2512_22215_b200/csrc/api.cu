@@ -736,6 +736,9 @@ spuma_status run_pcg_loop(spuma_mesh m, cudaStream_t s, const MeshArgs& a, int l
     int tp = m->persistent >= 3 ? std::min(need, loop_tmem_pairs()) : 0;
     const int sp_cap = (200 * 1024) / (T * (int)sizeof(double2));  // <= 200 KB of shared memory
     int sp = m->persistent >= 2 ? std::min(need - tp, sp_cap) : 0;
+    // less than half of rA on chip: the graph batches are as fast or faster (C4 64M cells, 13 % on
+    // chip: 1695 vs 1571 us per iteration; 252^3, 52 %: loop 312 vs 321 us, profiles/r02y_*)
+    if (m->persistent >= 2 && 2 * (tp + sp) < need) return SPUMA_OK;
     size_t smem = (size_t)sp * T * sizeof(double2);
     if (loop_occupancy(kkey, smem) < 1) {
         if (loop_occupancy(kkey, 0) < 1) return SPUMA_OK;  // cannot run here: graph batches
@@ -747,7 +750,7 @@ spuma_status run_pcg_loop(spuma_mesh m, cudaStream_t s, const MeshArgs& a, int l
     L.tmem_pairs = tp;
     L.smem_pairs = sp;
     L.alt = m->alt_sweep ? 1 : 0;
-    L.spin_limit = 4'000'000'000LL;  // ~2 s at 2 GHz per barrier: only a bug waits that long
+    L.spin_limit = m->pst.poll_cycles;  // SPUMA_OPT_PEER_POLL_MS (default ~20 s): only a bug waits that long
     Workspace w = m->ws;
     w.part = m->d_loop_part;
     if (m->loop_profile) {

@@ -69,12 +69,6 @@ __device__ __forceinline__ void tm_st(uint32_t addr, double2 v)
 
 __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
-#ifndef SPUMA_LOOP_ELL_PIPE
-#define SPUMA_LOOP_ELL_PIPE 0  // A/B: the ELL rows software-pipelined (variant 10; spills at 64 registers)
-#endif
-#ifndef SPUMA_LOOP_POLL
-#define SPUMA_LOOP_POLL 0  // A/B: 0 acquire poll, 1 relaxed poll + fence, 2 acquire poll with 32 ns back-off
-#endif
 #ifndef SPUMA_LOOP_BAR
 #define SPUMA_LOOP_BAR 1  // A/B: 0 fence + atomicAdd + acquire poll + fence, 1 red.release + acquire poll
 #endif
@@ -145,19 +139,8 @@ __device__ __forceinline__ bool grid_bar(const LoopArgs& L, unsigned long long t
         unsigned spins = 0;
         for (;;) {
             unsigned long long v;
-#if SPUMA_LOOP_POLL == 1
-            asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(L.bar) : "memory");
-            if (v >= target) {
-                asm volatile("fence.acq_rel.gpu;" ::: "memory");
-                break;
-            }
-#else
             asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(L.bar) : "memory");
             if (v >= target) break;
-#if SPUMA_LOOP_POLL == 2
-            __nanosleep(32);
-#endif
-#endif
             if ((++spins & 63u) == 0u &&
                 (*reinterpret_cast<volatile unsigned long long*>(L.bar + 1) || clock64() - t0 > L.spin_limit)) {
                 atomicExch(L.bar + 1, 1ull);
@@ -348,17 +331,9 @@ __global__ void __launch_bounds__(kT, 1) k_pcg_loop(MeshArgs a, Workspace w, Loo
             const int nch = (N + 31) / 32;
             const int cnt = wid < nch ? (nch - 1 - wid) / nw + 1 : 0;
             double acc = 0.0;
-            if constexpr (ELL && SPUMA_LOOP_ELL_PIPE) {  // variant 10's rows (next row's first-level loads ahead)
-                const int wn = a.ell_wn, wo = a.ell_wo, lane = t & 31;
-                EllL1 cur, nxt;
-                if (cnt > 0) ell_load1<false>(a, (wid + (rev ? cnt - 1 : 0) * nw) * 32 + lane, wn, wo, P.diag, a.upper_s, pc, cur);
-                for (int j = 0; j < cnt; ++j) {
-                    if (j + 1 < cnt)
-                        ell_load1<false>(a, (wid + (rev ? cnt - 2 - j : j + 1) * nw) * 32 + lane, wn, wo, P.diag, a.upper_s, pc, nxt);
-                    ell_finish<0, false>(a, cur, wo, a.upper_s, nullptr, pc, nullptr, w.wA, acc, true);
-                    cur = nxt;
-                }
-            } else if constexpr (ELL) {  // variant 8's rows: one row's loads at a time (64 registers)
+            if constexpr (ELL) {  // variant 8's rows: one row's loads at a time (64 registers; the
+                                  // software-pipelined rows of variant 10 spill here: 249 vs 189 us per
+                                  // iteration at 8M cells, profiles/r02aa_*)
                 const int wn = a.ell_wn, wo = a.ell_wo, lane = t & 31;
                 for (int j = 0; j < cnt; ++j) {
                     EllL1 cur;

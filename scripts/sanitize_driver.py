@@ -50,8 +50,21 @@ for mname, mesh, ren in (("perturbed8", gen.perturbed(8, 0.2), False), ("permute
             h.set_option(S.OPT_DEFER_PSI, defer)
             psi = torch.zeros(N, **f64)
             h.pcg_solve(diag, upper, None, src.clone(), psi, 1e-8, 0.0, 2000, 0)
+    # the persistent loop (one cooperative launch per solve; TMEM / shared-memory / HBM residency of
+    # rA) on both Amul layouts; generous barrier limit (the tools slow every kernel down)
+    h.set_option(S.OPT_SMALL_SOLVE_MAX_CELLS, 0)
+    h.set_option(S.OPT_DEFER_PSI, 2)
+    h.set_option(S.OPT_PEER_POLL_MS, 600000)
+    for variant in (12, 10):
+        h.set_option(S.OPT_AMUL_VARIANT, variant)
+        for mode in (1, 2, 3):
+            h.set_option(S.OPT_PERSISTENT, mode)
+            psi = torch.zeros(N, **f64)
+            h.pcg_solve(diag, upper, None, src.clone(), psi, 1e-8, 0.0, 2000, 0)
+    h.set_option(S.OPT_PERSISTENT, 3)
     h.set_option(S.OPT_SMALL_SOLVE_MAX_CELLS, 8192)
-    step(f"{mname} pcg (single-CTA in shared / global memory + batches; lattice / ELL rows; psi deferral modes)")
+    step(f"{mname} pcg (single-CTA in shared / global memory + batches; lattice / ELL rows; psi deferral modes; "
+         f"persistent loop modes 1-3)")
     V = d(mesh.V)
     out = torch.zeros(N, **f64)
     phi = d(np.sin(np.arange(F) * 0.1))
