@@ -153,6 +153,22 @@ __device__ __forceinline__ void amul_rows2(const MeshArgs& a, int c, int e, cons
     }
 }
 
+#ifndef SPUMA_LOOP_XLD
+#define SPUMA_LOOP_XLD 0  // A/B of the persistent loop's coherent loads: 0 ld.global, 1 ld.global.cg (L2 only)
+#endif
+template <bool NC>
+__device__ __forceinline__ double ldx(const double* p)
+{
+    if constexpr (NC) return __ldg(p);
+    double v;
+#if SPUMA_LOOP_XLD == 1
+    asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(p));
+#else
+    asm volatile("ld.global.f64 %0, [%1];" : "=d"(v) : "l"(p));  // volatile: stays behind the barriers
+#endif
+    return v;
+}
+
 // ---------------------------------------------------------------------------- variants 6, 7 (SELL-C)
 // Rows read from the SELL-C slots (host.h build_sell): the neighbour side is one packed
 // int32 per entry (owner column << 5 | position of the face in the owner's range), so
@@ -164,7 +180,20 @@ __device__ __forceinline__ void amul_rows2(const MeshArgs& a, int c, int e, cons
 // IFM (interface mode): 0 no processor faces, 1 add the interface terms inline,
 // 2 deferred -- interface rows keep only their internal-face sum (finished later by
 // k_iface_rows once the halo has arrived) and are left out of this kernel's dot.
-template <int R, int IFM = 0>
+// y_c = (A x)_c by the generic row gather (amul_row's order, reading Q10) with coherent x loads:
+// the wide-row fallback of the persistent loop's SELL rows (x rewritten inside the launch)
+__device__ __forceinline__ double amul_row_coherent(const MeshArgs& a, int c, const double* __restrict__ diag,
+                                                    const double* __restrict__ upper, const double* x)
+{
+    double s = diag[c] * ldx<false>(x + c);
+    const int k1 = a.losortStart[c + 1];
+    for (int k = a.losortStart[c]; k < k1; ++k) s = s + upper[a.losort[k]] * ldx<false>(x + a.ownerLo[k]);
+    const int f1 = a.ownerStart[c + 1];
+    for (int f = a.ownerStart[c]; f < f1; ++f) s = s + upper[f] * ldx<false>(x + a.neighbour[f]);
+    return s;
+}
+
+template <int R, int IFM = 0, bool NC = true>
 __device__ __forceinline__ void amul_rows_sell(const MeshArgs& a, int c, int wn_u, int wo_u,
                                                const double* __restrict__ diag, const double* __restrict__ upper,
                                                const double* __restrict__ iface, const double* __restrict__ x,
@@ -192,13 +221,15 @@ __device__ __forceinline__ void amul_rows_sell(const MeshArgs& a, int c, int wn_
         ok = ok && wn[r] <= W && wo[r] <= W;
         osc[r] = __ldg(a.ownerStart + cc[r]);
         dg[r] = __ldg(diag + cc[r]);
-        xc[r] = __ldg(x + cc[r]);
+        xc[r] = ldx<NC>(x + cc[r]);
     }
     if (!ok) {
 #pragma unroll
         for (int r = 0; r < R; ++r)
             if (c + 32 * r < a.N) {
-                const double v = amul_row(a, cc[r], diag, upper, iface, x, xr, nullptr, IFM != 2);
+                double v;
+                if constexpr (NC) v = amul_row(a, cc[r], diag, upper, iface, x, xr, nullptr, IFM != 2);
+                else v = amul_row_coherent(a, cc[r], diag, upper, x);  // (single rank: no interfaces)
                 y[cc[r]] = v;
                 if (dot && (IFM != 2 || !is_iface_row(a, cc[r]))) acc += v * xc[r];
             }
@@ -222,8 +253,8 @@ __device__ __forceinline__ void amul_rows_sell(const MeshArgs& a, int c, int wn_
             const bool vn = pk[r][j] != 0xFFFFFFFFu, vo = nb[r][j] >= 0;
             const int col = vn ? (int)(pk[r][j] >> 5) : cc[r];
             oc[r][j] = vn ? __ldg(a.ownerStart + col) : 0;
-            xn[r][j] = __ldg(x + col);
-            xo[r][j] = __ldg(x + (vo ? nb[r][j] : cc[r]));
+            xn[r][j] = ldx<NC>(x + col);
+            xo[r][j] = ldx<NC>(x + (vo ? nb[r][j] : cc[r]));
             uo[r][j] = vo ? __ldg(upper + osc[r] + j) : 0.0;
         }
     double un[R][W];
@@ -371,22 +402,6 @@ __device__ __forceinline__ void amul_rows_ell(const MeshArgs& a, int c, int wn, 
             if (dot && (IFM != 2 || !is_iface_row(a, cc[r]))) acc += s * xc[r];
         }
     }
-}
-
-#ifndef SPUMA_LOOP_XLD
-#define SPUMA_LOOP_XLD 0  // A/B of the persistent loop's coherent loads: 0 ld.global, 1 ld.global.cg (L2 only)
-#endif
-template <bool NC>
-__device__ __forceinline__ double ldx(const double* p)
-{
-    if constexpr (NC) return __ldg(p);
-    double v;
-#if SPUMA_LOOP_XLD == 1
-    asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(p));
-#else
-    asm volatile("ld.global.f64 %0, [%1];" : "=d"(v) : "l"(p));  // volatile: stays behind the barriers
-#endif
-    return v;
 }
 
 // Variant 10: the ELL rows of variant 8 software-pipelined across the grid-stride loop -- the

@@ -701,7 +701,7 @@ struct GamgState {
 namespace {
 
 // SPUMA_OPT_PERSISTENT: can this solve run as one cooperative launch (loop.cu)?
-// layout of the loop's Amul: 1 lattice slots, 2 ELL rows, 0 = not eligible
+// layout of the loop's Amul: 1 lattice slots, 2 ELL rows, 3 SELL-C rows, 0 = not eligible
 int loop_layout(spuma_mesh m, const MeshArgs& a)
 {
     if (!(m->persistent > 0 && m->n_ranks == 1 && !m->external_comm && m->defer_psi == 2 && m->N > 0)) return 0;
@@ -710,6 +710,7 @@ int loop_layout(spuma_mesh m, const MeshArgs& a)
     if ((rv == 8 || rv == 10) && a.upper_s && !m->ell_stencil && a.ell_wn >= 0 && a.ell_wn <= 3 && a.ell_wo >= 0 &&
         a.ell_wo <= 3)
         return 2;
+    if (rv == 6 && a.sell_n) return 3;
     return 0;
 }
 
@@ -718,7 +719,7 @@ int loop_layout(spuma_mesh m, const MeshArgs& a)
 spuma_status run_pcg_loop(spuma_mesh m, cudaStream_t s, const MeshArgs& a, int layout, bool* ran)
 {
     *ran = false;
-    const int kkey = layout == 2 ? 0 : a.lat_K;  // loop_fn key: lattice K, 0 = ELL rows
+    const int kkey = layout == 3 ? -1 : (layout == 2 ? 0 : a.lat_K);  // loop_fn key: lattice K, 0 ELL, -1 SELL
     const int T = loop_threads();
     if (!m->loop_grid) {
         int dev = 0, sms = 0;
@@ -769,7 +770,7 @@ spuma_status run_pcg_loop(spuma_mesh m, cudaStream_t s, const MeshArgs& a, int l
         m->l2_lines = nullptr;
     }
     {
-        const cudaError_t e = launch_pcg_loop(s, G, smem, a, w, L, use_win ? &win : nullptr, layout == 2);
+        const cudaError_t e = launch_pcg_loop(s, G, smem, a, w, L, use_win ? &win : nullptr, layout);
         if (e == cudaErrorCooperativeLaunchTooLarge) {  // SMs taken (e.g. MPS limits): graph batches instead
             cudaGetLastError();
             return SPUMA_OK;

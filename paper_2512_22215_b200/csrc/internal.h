@@ -413,7 +413,7 @@ int loop_threads();
 int loop_tmem_pairs();
 int loop_occupancy(int K, size_t smem);
 cudaError_t launch_pcg_loop(cudaStream_t s, int grid, size_t smem, const MeshArgs& a, const Workspace& w,
-                            const LoopArgs& L, const cudaAccessPolicyWindow* win, bool ell);
+                            const LoopArgs& L, const cudaAccessPolicyWindow* win, int layout);  // 1 lattice, 2 ELL, 3 SELL
 // A11+A7+A8 in one kernel (ELL, single rank, deferred psi): see kernels.cu
 bool fused_direction_ok(const MeshArgs& a);
 void launch_amul_dot_dir(cudaStream_t s, const MeshArgs& a, const Workspace& w, bool inline_rd);  // psi += alpha_prev pA (pending update)

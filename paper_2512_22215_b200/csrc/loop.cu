@@ -210,7 +210,8 @@ __device__ __forceinline__ void grid_sums(const double* part, int off, double (&
 // KT: the lattice offset count at compile time (0: a.lat_K at run time); ELL: the Amul runs over
 // the ELL rows of variant 10 (uniform slot widths <= 3, per-solve coefficient copy upper_s) on a
 // mesh that is not a lattice numbering (C2 / C4 renumbered by RCM)
-template <int KT, bool ELL>
+// LAY: 0 lattice slots, 1 ELL rows, 2 SELL-C rows (variant 6: a permuted mesh as given, C2)
+template <int KT, int LAY>
 __global__ void __launch_bounds__(kT, 1) k_pcg_loop(MeshArgs a, Workspace w, LoopArgs L)
 {
     extern __shared__ double2 rs[];
@@ -331,7 +332,12 @@ __global__ void __launch_bounds__(kT, 1) k_pcg_loop(MeshArgs a, Workspace w, Loo
             const int nch = (N + 31) / 32;
             const int cnt = wid < nch ? (nch - 1 - wid) / nw + 1 : 0;
             double acc = 0.0;
-            if constexpr (ELL) {  // variant 8's rows: one row's loads at a time (64 registers; the
+            if constexpr (LAY == 2) {  // variant 6's SELL-C rows (per-chunk widths, wide-row fallback)
+                const int lane = t & 31;
+                for (int j = 0; j < cnt; ++j)
+                    amul_rows_sell<1, 0, false>(a, (wid + (rev ? cnt - 1 - j : j) * nw) * 32 + lane, a.ell_wn, a.ell_wo,
+                                                P.diag, P.upper, nullptr, pc, nullptr, w.wA, acc, true);
+            } else if constexpr (LAY == 1) {  // variant 8's rows: one row's loads at a time (64 registers; the
                                   // software-pipelined rows of variant 10 spill here: 249 vs 189 us per
                                   // iteration at 8M cells, profiles/r02aa_*)
                 const int wn = a.ell_wn, wo = a.ell_wo, lane = t & 31;
@@ -443,11 +449,12 @@ __global__ void __launch_bounds__(kT, 1) k_pcg_loop(MeshArgs a, Workspace w, Loo
 int loop_threads() { return ploop::kT; }
 int loop_tmem_pairs() { return ploop::kTmemPairs; }
 
-// K: the lattice offset count, 0 = the ELL rows
+// K: the lattice offset count, 0 = the ELL rows, -1 = the SELL-C rows
 static void* loop_fn(int K)
 {
-    return K == 3 ? (void*)ploop::k_pcg_loop<3, false>
-                  : (K > 0 ? (void*)ploop::k_pcg_loop<0, false> : (void*)ploop::k_pcg_loop<0, true>);
+    if (K == 3) return (void*)ploop::k_pcg_loop<3, 0>;
+    if (K > 0) return (void*)ploop::k_pcg_loop<0, 0>;
+    return K == 0 ? (void*)ploop::k_pcg_loop<0, 1> : (void*)ploop::k_pcg_loop<0, 2>;
 }
 
 // CTAs per SM the loop kernel reaches with `smem` bytes of dynamic shared memory (0: it
@@ -468,7 +475,7 @@ int loop_occupancy(int K, size_t smem)
 }
 
 cudaError_t launch_pcg_loop(cudaStream_t s, int grid, size_t smem, const MeshArgs& a, const Workspace& w,
-                            const LoopArgs& L, const cudaAccessPolicyWindow* win, bool ell)
+                            const LoopArgs& L, const cudaAccessPolicyWindow* win, int layout)
 {
     MeshArgs aa = a;
     Workspace ww = w;
@@ -490,7 +497,7 @@ cudaError_t launch_pcg_loop(cudaStream_t s, int grid, size_t smem, const MeshArg
     cfg.stream = s;
     cfg.attrs = attr;
     cfg.numAttrs = na;
-    return cudaLaunchKernelExC(&cfg, loop_fn(ell ? 0 : a.lat_K), args);
+    return cudaLaunchKernelExC(&cfg, loop_fn(layout == 1 ? a.lat_K : (layout == 2 ? 0 : -1)), args);
 }
 
 }  // namespace spuma

@@ -211,19 +211,21 @@ def test_psi_pairs_and_final_flush_with_psi0(iters):
     assert d <= 1e-13, d
 
 
-ELL_MESHES = [("cube30-permuted-rcm", lambda: gen.permute(gen.cube(30), seed=3)),
-              ("perturbed24-permuted-rcm", lambda: gen.permute(gen.perturbed(24, 0.2), seed=5)),
-              ("box-odd-permuted-rcm", lambda: gen.permute(gen.box(29, 23, 17), seed=7))]
+ELL_MESHES = [("cube30-permuted-rcm", lambda: gen.permute(gen.cube(30), seed=3), True, 10),
+              ("perturbed24-permuted-rcm", lambda: gen.permute(gen.perturbed(24, 0.2), seed=5), True, 10),
+              ("box-odd-permuted-rcm", lambda: gen.permute(gen.box(29, 23, 17), seed=7), True, 10),
+              ("cube30-permuted-as-given", lambda: gen.permute(gen.cube(30), seed=3), False, 6),
+              ("box-odd-permuted-as-given", lambda: gen.permute(gen.box(29, 23, 17), seed=7), False, 6)]
 
 
-@pytest.mark.parametrize("name,make", ELL_MESHES, ids=[c[0] for c in ELL_MESHES])
-def test_ell_rows_loop(name, make):
-    """Meshes that are not lattice numberings (C2 / C4: permuted, renumbered by RCM): the loop's
-    Amul runs over the ELL rows (variant 10's slots) -- modes bitwise equal, the graph batches
+@pytest.mark.parametrize("name,make,renumber,variant", ELL_MESHES, ids=[c[0] for c in ELL_MESHES])
+def test_ell_rows_loop(name, make, renumber, variant):
+    """Meshes that are not lattice numberings (C2 / C4: permuted; renumbered by RCM -> the ELL rows
+    of variant 10, as given -> the SELL-C rows of variant 6): modes bitwise equal, the graph batches
     within 1e-12 at the same count, the oracle within the north_star bar (Q11)."""
     m = make()
-    h, diag, upper, src = _assembled(m, renumber=True)
-    assert h.get_stats()["amul_variant"] == 10
+    h, diag, upper, src = _assembled(m, renumber=renumber)
+    assert h.get_stats()["amul_variant"] == variant
     ctl = (1e-8, 0.0, 5000, 0)
     psi0, p0, _ = _solve(h, diag, upper, src, ctl, 0)
     outs = []
@@ -237,14 +239,14 @@ def test_ell_rows_loop(name, make):
     h.free()
     # oracle (caller numbering; the handle renumbers internally)
     g, b = gen.gamma_lognormal(m), gen.rhs(m)
-    hh = P.Mesh.from_mesh(m, renumber=True)
+    hh = P.Mesh.from_mesh(m, renumber=renumber)
     hh.set_option(OPT.OPT_SMALL_SOLVE_MAX_CELLS, 0)
-    psi_g, pg, _, _ = gpu_solve_case(m, g, b, 0, ctl, renumber=True, handle=hh)
+    psi_g, pg, _, _ = gpu_solve_case(m, g, b, 0, ctl, renumber=renumber, handle=hh)
     assert hh.get_stats()["loop_mode"] == 3
     psi_o, po, _ = O.solve_case(m, g, b, 0, 0.0, O.controls(*ctl))
     assert pg["converged"] and abs(pg["n_iterations"] - po["n_iterations"]) <= 2, (pg, po)
     n = min(pg["n_iterations"], po["n_iterations"])
-    psi_g, _, _, _ = gpu_solve_case(m, g, b, 0, (0.0, 0.0, n, n), renumber=True, handle=hh)
+    psi_g, _, _, _ = gpu_solve_case(m, g, b, 0, (0.0, 0.0, n, n), renumber=renumber, handle=hh)
     psi_o, _, _ = O.solve_case(m, g, b, 0, 0.0, O.controls(0.0, 0.0, n, n))
     assert np.linalg.norm(psi_g - psi_o) / np.linalg.norm(psi_o) <= 1e-9
     hh.free()
