@@ -10,6 +10,8 @@ import sys
 
 import pytest
 
+from conftest import shared_gpu_ranks  # noqa: E402
+
 pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
@@ -22,6 +24,7 @@ def _port():
     return p
 
 
+@shared_gpu_ranks
 @pytest.mark.parametrize("world", [2])
 def test_bench_n_ranks_peer_transport_on_one_gpu(world):
     env = dict(os.environ, SPUMA_BENCH_SHARE_GPU="1")

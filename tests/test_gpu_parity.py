@@ -460,6 +460,7 @@ def test_deferred_psi_updates_are_bitwise_neutral(iters):
     for defer in (0, 1, 2):  # every iteration / pairs in the update / pairs in the direction
         h = P.Mesh.from_mesh(m)
         h.set_option(P.spuma.OPT_SMALL_SOLVE_MAX_CELLS, 0)
+        h.set_option(P.spuma.OPT_PERSISTENT, 0)  # graph batches on all three (same reduction shape)
         h.set_option(P.spuma.OPT_DEFER_PSI, defer)
         out.append(gpu_solve_case(m, g, b, 0, ctl, handle=h)[:2])
     for k in (1, 2):

@@ -13,6 +13,8 @@ import os
 import numpy as np
 import pytest
 
+from conftest import shared_gpu_ranks  # noqa: E402
+
 from test_gpu_multirank import _callbacks, _case, _port
 
 pytestmark = pytest.mark.gpu
@@ -114,6 +116,7 @@ def _worker(rank, P, how, port, results):
             dist.destroy_process_group()
 
 
+@shared_gpu_ranks
 @pytest.mark.parametrize("P,how", [(2, "block"), (3, "rcb"), (4, "rcb"), (2, "lattice")])
 def test_peer_transport_matches_oracle_and_callbacks(P, how):
     ctx = mp.get_context("spawn")

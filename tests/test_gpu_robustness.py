@@ -14,6 +14,8 @@ import os
 import numpy as np
 import pytest
 
+from conftest import shared_gpu_ranks  # noqa: E402
+
 pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 
@@ -158,6 +160,7 @@ def _peer_timeout_worker(rank, port, results):
             dist.destroy_process_group()
 
 
+@shared_gpu_ranks
 def test_peer_poll_timeout_returns_error_state():
     import torch.multiprocessing as mp
 
