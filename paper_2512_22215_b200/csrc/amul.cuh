@@ -566,61 +566,6 @@ __device__ __forceinline__ void lat_chunk(const MeshArgs& a, int K, int ch, cons
     }
 }
 
-// The lattice rows software-pipelined (the persistent loop's Amul phase, SPUMA_LOOP_LAT_PIPE): the
-// NEXT chunk's streamed loads (diag and the K own slots: DRAM) are issued before the CURRENT chunk's
-// x windows and neighbour-side slots (mostly L2 hits), so two chunks' streams are in flight per
-// warp within 64 registers.  Same operations, same order as lat_chunk: bitwise the same rows.
-struct LatOwn {
-    double dg, uo[3];
-};
-
-template <int KT, bool NC>
-__device__ __forceinline__ void lat_own(const MeshArgs& a, int K, int ch, const double* __restrict__ diag,
-                                        const double* const (&ud)[3], const double* __restrict__ x, LatOwn& o)
-{
-    const int N = a.N, cc = min(ch * 32 + (int)(threadIdx.x & 31), N - 1);
-    o.dg = __ldg(diag + cc);
-#pragma unroll
-    for (int t = 0; t < 3; ++t)
-        o.uo[t] = t < (KT ? KT : K) ? __ldg(ud[t] + cc) : __longlong_as_double((long long)kLatAbsent);
-}
-
-template <int KT, bool NC>
-__device__ __forceinline__ void lat_fin(const MeshArgs& a, int K, int ch, const double* const (&ud)[3],
-                                        const double* __restrict__ x, const LatOwn& o, double* __restrict__ y,
-                                        double& acc)
-{
-    const int N = a.N, c = ch * 32 + (int)(threadIdx.x & 31), cc = min(c, N - 1);
-    double un[3], xn[3], xo[3];
-    bool on[3];
-    const double xc = ldx<NC>(x + cc);
-#pragma unroll
-    for (int t = 0; t < 3; ++t) {
-        if (t < (KT ? KT : K)) {
-            const int oo = cc - a.lat_D[t];
-            on[t] = oo >= 0;
-            const int oc = oo >= 0 ? oo : cc;
-            xo[t] = ldx<NC>(x + min(cc + a.lat_D[t], N - 1));
-            un[t] = __ldg(ud[t] + oc);
-            xn[t] = ldx<NC>(x + oc);
-        } else {
-            on[t] = false;
-            un[t] = xn[t] = xo[t] = 0.0;
-        }
-    }
-    double s = o.dg * xc;
-#pragma unroll
-    for (int t = 2; t >= 0; --t)
-        if (on[t] && lat_present(un[t])) s = s + un[t] * xn[t];
-#pragma unroll
-    for (int t = 0; t < 3; ++t)
-        if (lat_present(o.uo[t])) s = s + o.uo[t] * xo[t];
-    if (c < N) {
-        y[c] = s;
-        acc += s * xc;
-    }
-}
-
 template <int R, int IFM, int KT = 0>  // KT: the offset count at compile time (0: a.lat_K at run time)
 __device__ __forceinline__ void amul_lattice_k(const MeshArgs& a, const double* __restrict__ diag,
                                                const double* __restrict__ iface, const double* __restrict__ x,

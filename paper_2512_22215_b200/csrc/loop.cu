@@ -69,12 +69,6 @@ __device__ __forceinline__ void tm_st(uint32_t addr, double2 v)
 
 __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
-#ifndef SPUMA_LOOP_LAT_PIPE
-#define SPUMA_LOOP_LAT_PIPE 0  // A/B: the lattice rows software-pipelined (next chunk's own-side loads ahead)
-#endif
-#ifndef SPUMA_LOOP_RD_INLINE
-#define SPUMA_LOOP_RD_INLINE 0  // A/B: 1 / diag formed in the update and the direction instead of reading rD
-#endif
 #ifndef SPUMA_LOOP_BAR
 #define SPUMA_LOOP_BAR 1  // A/B: 0 fence + atomicAdd + acquire poll + fence, 1 red.release + acquire poll
 #endif
@@ -260,17 +254,6 @@ __global__ void __launch_bounds__(kT, 1) k_pcg_loop(MeshArgs a, Workspace w, Loo
 
     const double* __restrict__ rD = w.rD;
     const double2* __restrict__ rD2 = reinterpret_cast<const double2*>(w.rD);
-#if SPUMA_LOOP_RD_INLINE
-    // rD = 1 / diag formed where it is used (IEEE division: bitwise the stored rD of k_setup2), so all
-    // three phases stream the same array and each phase finds the previous phase's last lines in L2
-    // (the prefetch loads diag; the division happens where the value is used)
-    const double2* __restrict__ dg2 = reinterpret_cast<const double2*>(w.ptrs->diag);
-    auto ldrd = [&](int i) { return __ldg(dg2 + i); };
-    auto tord = [](double2 g) { return make_double2(1.0 / g.x, 1.0 / g.y); };
-#else
-    auto ldrd = [&](int i) { return __ldg(rD2 + i); };
-    auto tord = [](double2 g) { return g; };
-#endif
     const DevPtrs P = *w.ptrs;
     double2* psi2 = reinterpret_cast<double2*>(P.psi);
     const double* const ud[3] = {a.upper_d, a.upper_d + a.lat_S, a.upper_d + 2 * a.lat_S};
@@ -299,7 +282,7 @@ __global__ void __launch_bounds__(kT, 1) k_pcg_loop(MeshArgs a, Workspace w, Loo
                 const int kk = odd ? nk - 1 - j : j;
                 const int i = (b + kk * G) * kT + t;
                 if (i < np) {
-                    dn = ldrd(i);
+                    dn = __ldg(rD2 + i);
                     if (!first) pn = ld2(pp2 + i);
                     if (kk >= kon) rn = R.g[i];
                 }
@@ -308,7 +291,7 @@ __global__ void __launch_bounds__(kT, 1) k_pcg_loop(MeshArgs a, Workspace w, Loo
             for (int j = 0; j < nk; ++j) {
                 const int k = odd ? nk - 1 - j : j;
                 const int i = (b + k * G) * kT + t;
-                const double2 d = tord(dn), p = pn, rh = rn;
+                const double2 d = dn, p = pn, rh = rn;
                 if (j + 1 < nk) pf(j + 1);
                 const double2 r = k < kon ? R.load(k, 0) : rh;
                 if (i < np) {
@@ -364,20 +347,10 @@ __global__ void __launch_bounds__(kT, 1) k_pcg_loop(MeshArgs a, Workspace w, Loo
                     ell_finish<0, false>(a, cur, wo, a.upper_s, nullptr, pc, nullptr, w.wA, acc, true);
                 }
             } else {
-#if SPUMA_LOOP_LAT_PIPE
-                LatOwn cur, nxt;
-                if (cnt > 0) lat_own<KT, false>(a, K, wid + (rev ? cnt - 1 : 0) * nw, P.diag, ud, pc, cur);
-                for (int j = 0; j < cnt; ++j) {
-                    if (j + 1 < cnt) lat_own<KT, false>(a, K, wid + (rev ? cnt - 2 - j : j + 1) * nw, P.diag, ud, pc, nxt);
-                    lat_fin<KT, false>(a, K, wid + (rev ? cnt - 1 - j : j) * nw, ud, pc, cur, w.wA, acc);
-                    cur = nxt;
-                }
-#else
                 for (int j = 0; j < cnt; ++j) {
                     const int ch = wid + (rev ? cnt - 1 - j : j) * nw;
                     lat_chunk<1, 0, KT, false>(a, K, ch, P.diag, ud, nullptr, pc, nullptr, w.wA, acc, true);
                 }
-#endif
             }
             double v[1] = {acc};
             cta_reduce<1>(v, sh);
@@ -405,7 +378,7 @@ __global__ void __launch_bounds__(kT, 1) k_pcg_loop(MeshArgs a, Workspace w, Loo
                 const int i = (b + kk * G) * kT + t;
                 if (i < np) {
                     wn = ld2(wA2 + i);
-                    dn = ldrd(i);
+                    dn = __ldg(rD2 + i);
                     if (kk >= kon) rn = R.g[i];
                 }
             };
@@ -413,7 +386,7 @@ __global__ void __launch_bounds__(kT, 1) k_pcg_loop(MeshArgs a, Workspace w, Loo
             for (int j = 0; j < nk; ++j) {
                 const int k = odd ? nk - 1 - j : j;
                 const int i = (b + k * G) * kT + t;
-                const double2 ww = wn, d = tord(dn), rh = rn;
+                const double2 ww = wn, d = dn, rh = rn;
                 if (j + 1 < nk) pf(j + 1);
                 double2 r = k < kon ? R.load(k, 0) : rh;
                 if (i < np) {
