@@ -69,6 +69,9 @@ __device__ __forceinline__ void tm_st(uint32_t addr, double2 v)
 
 __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
+#ifndef SPUMA_LOOP_PSI_PF
+#define SPUMA_LOOP_PSI_PF 1  // A/B: the psi pair's loads (psi, p_{n-2}) prefetched one tile ahead too
+#endif
 #ifndef SPUMA_LOOP_BAR
 #define SPUMA_LOOP_BAR 1  // A/B: 0 fence + atomicAdd + acquire poll + fence, 1 red.release + acquire poll
 #endif
@@ -277,6 +280,9 @@ __global__ void __launch_bounds__(kT, 1) k_pcg_loop(MeshArgs a, Workspace w, Loo
             // one tile ahead: the next tile's rD / pA_prev loads are in flight while this one computes
             // (rA pairs kept in HBM -- meshes beyond the on-chip capacity -- are loaded here too)
             double2 dn = make_double2(0.0, 0.0), pn = dn, rn = dn;
+#if SPUMA_LOOP_PSI_PF
+            double2 xn = dn, on = dn;  // psi and p_{n-2} of the next tile (psi iterations)
+#endif
             const int kon = R.tp + R.sp;
             auto pf = [&](int j) {
                 const int kk = odd ? nk - 1 - j : j;
@@ -284,6 +290,12 @@ __global__ void __launch_bounds__(kT, 1) k_pcg_loop(MeshArgs a, Workspace w, Loo
                 if (i < np) {
                     dn = __ldg(rD2 + i);
                     if (!first) pn = ld2(pp2 + i);
+#if SPUMA_LOOP_PSI_PF
+                    if (psi) {
+                        xn = psi2[i];
+                        on = ld2(pc2 + i);
+                    }
+#endif
                     if (kk >= kon) rn = R.g[i];
                 }
             };
@@ -292,6 +304,9 @@ __global__ void __launch_bounds__(kT, 1) k_pcg_loop(MeshArgs a, Workspace w, Loo
                 const int k = odd ? nk - 1 - j : j;
                 const int i = (b + k * G) * kT + t;
                 const double2 d = dn, p = pn, rh = rn;
+#if SPUMA_LOOP_PSI_PF
+                const double2 xc = xn, oc = on;
+#endif
                 if (j + 1 < nk) pf(j + 1);
                 const double2 r = k < kon ? R.load(k, 0) : rh;
                 if (i < np) {
@@ -301,8 +316,13 @@ __global__ void __launch_bounds__(kT, 1) k_pcg_loop(MeshArgs a, Workspace w, Loo
                         q.y = d.y * r.y;
                     } else {
                         if (psi) {
+#if SPUMA_LOOP_PSI_PF
+                            double2 x = xc;
+                            const double2 o = oc;  // p_{n-2}
+#else
                             double2 x = psi2[i];
                             const double2 o = pc2[i];  // p_{n-2}
+#endif
                             x.x = x.x + a2 * o.x;
                             x.y = x.y + a2 * o.y;
                             x.x = x.x + a1 * p.x;
@@ -371,9 +391,8 @@ __global__ void __launch_bounds__(kT, 1) k_pcg_loop(MeshArgs a, Workspace w, Loo
             const double alpha = S.alpha;
             const double2* wA2 = reinterpret_cast<const double2*>(w.wA);
             double v[2] = {0.0, 0.0};
-            double2 wn = make_double2(0.0, 0.0), dn = wn, rn = wn;
             const int kon = R.tp + R.sp;
-            auto pf = [&](int j) {
+            auto pf = [&](int j, double2& wn, double2& dn, double2& rn) {
                 const int kk = odd ? nk - 1 - j : j;
                 const int i = (b + kk * G) * kT + t;
                 if (i < np) {
@@ -382,12 +401,9 @@ __global__ void __launch_bounds__(kT, 1) k_pcg_loop(MeshArgs a, Workspace w, Loo
                     if (kk >= kon) rn = R.g[i];
                 }
             };
-            if (nk > 0) pf(0);
-            for (int j = 0; j < nk; ++j) {
+            auto body = [&](int j, double2 ww, double2 d, double2 rh) {
                 const int k = odd ? nk - 1 - j : j;
                 const int i = (b + k * G) * kT + t;
-                const double2 ww = wn, d = dn, rh = rn;
-                if (j + 1 < nk) pf(j + 1);
                 double2 r = k < kon ? R.load(k, 0) : rh;
                 if (i < np) {
                     r.x = r.x - alpha * ww.x;
@@ -397,7 +413,14 @@ __global__ void __launch_bounds__(kT, 1) k_pcg_loop(MeshArgs a, Workspace w, Loo
                     v[1] += fabs(r.x);
                     v[1] += fabs(r.y);
                 }
-                if (k < R.tp + R.sp || i < np) R.store(k, i, r);  // on-chip: every lane (TMEM stores are warp-collective)
+                if (k < kon || i < np) R.store(k, i, r);  // on-chip: every lane (TMEM stores are warp-collective)
+            };
+            double2 wn = make_double2(0.0, 0.0), dn = wn, rn = wn;
+            if (nk > 0) pf(0, wn, dn, rn);
+            for (int j = 0; j < nk; ++j) {
+                const double2 ww = wn, d = dn, rh = rn;
+                if (j + 1 < nk) pf(j + 1, wn, dn, rn);
+                body(j, ww, d, rh);
             }
             if ((N & 1) && b == 0 && t == 0) {
                 const int c = N - 1;
