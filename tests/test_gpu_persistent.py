@@ -250,3 +250,38 @@ def test_ell_rows_loop(name, make, renumber, variant):
     psi_o, _, _ = O.solve_case(m, g, b, 0, 0.0, O.controls(0.0, 0.0, n, n))
     assert np.linalg.norm(psi_g - psi_o) / np.linalg.norm(psi_o) <= 1e-9
     hh.free()
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 64, 65])
+def test_tiny_chains_through_the_loop(n):
+    """A few cells through the big-mesh path (small-solve threshold 0): the loop's odd-cell and
+    empty-tile paths (N = 1: no pair at all) against the graph batches and the oracle."""
+    m = gen.box(n, 1, 1)
+    h, diag, upper, src = _assembled(m)
+    ctl = (1e-12, 0.0, 200, 0)
+    psi0, p0, _ = _solve(h, diag, upper, src, ctl, 0)
+    psi, p, s = _solve(h, diag, upper, src, ctl, 3)
+    if s["amul_variant"] in (6, 8, 10, 12, 13):  # a layout the loop runs (no faces at all: per-row fallback)
+        assert s["loop_mode"] == 3, s
+    assert p["n_iterations"] == p0["n_iterations"] and p["converged"] == p0["converged"]
+    scale = max(np.abs(psi0).max(), 1e-300)
+    assert np.abs(psi - psi0).max() / scale <= 1e-12
+    g, b = None, gen.rhs(m)
+    psi_o, po, _ = O.solve_case(m, g, b, 0, 0.0, O.controls(*ctl))
+    assert abs(p["n_iterations"] - po["n_iterations"]) <= 2
+    h.free()
+
+
+@pytest.mark.parametrize("alt", [0, 1])
+def test_loop_sweep_direction_option(alt):
+    """SPUMA_OPT_ALT_SWEEP reaches the loop (alternating tile / chunk order): same iteration count
+    and psi within 1e-12 of the graph batches either way."""
+    m = gen.cube(40)
+    h, diag, upper, src = _assembled(m)
+    h.set_option(OPT.OPT_ALT_SWEEP, alt)
+    ctl = (1e-8, 0.0, 5000, 0)
+    psi0, p0, _ = _solve(h, diag, upper, src, ctl, 0)
+    psi, p, s = _solve(h, diag, upper, src, ctl, 3)
+    assert s["loop_mode"] == 3 and p["n_iterations"] == p0["n_iterations"]
+    assert np.linalg.norm(psi - psi0) / np.linalg.norm(psi0) <= 1e-12
+    h.free()
