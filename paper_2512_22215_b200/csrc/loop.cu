@@ -15,10 +15,14 @@
 // copy of the scalars (DevScal in shared memory), so all CTAs take the same decisions
 // without a second barrier; CTA 0 writes the scalars back at the end.
 //
-// Element arithmetic is that of k_direction / k_amul_dot<12> / k_update (same operations in
-// the same order, deferred psi pairs in the direction, SPUMA_OPT_DEFER_PSI = 2): the rows of
-// A are bitwise those of every other variant; the dot products are summed in another (fixed)
-// shape, so iterates agree with the graph path to rounding (deterministic run to run).
+// The Amul phase runs over the lattice slots (variant 12) on structured numberings, else over
+// the ELL rows (variant 8's layout) or the SELL-C rows (variant 6; a permuted mesh as given).
+// Element arithmetic is that of k_direction / k_amul_dot / k_update (same operations in the
+// same order, deferred psi pairs in the direction, SPUMA_OPT_DEFER_PSI = 2): the rows of A are
+// bitwise those of every other variant; the dot products are summed in another (fixed) shape,
+// so iterates agree with the graph path to rounding (deterministic run to run).  The host
+// (api.cu run_pcg_loop) falls back to the graph batches below half residency and when the
+// cooperative launch does not fit.
 #include <cstdint>
 
 #include "internal.h"
