@@ -23,6 +23,9 @@ m = gen.cube(n)
 f64 = dict(dtype=torch.float64, device="cuda")
 st = torch.cuda.current_stream()
 h = P.Mesh.from_mesh(m, stream=st.cuda_stream)
+for kv in filter(None, os.environ.get("SPUMA_AB_OPTS", "").split(",")):  # extra option=value pairs (A/B)
+    k, v = kv.split("=")
+    h.set_option(int(k), int(v))
 diag, upper, src = torch.empty(m.n_cells, **f64), torch.empty(m.n_faces, **f64), torch.as_tensor(gen.rhs(m), **f64)
 h.assemble_laplacian(None, None, 0, 0.0, diag, upper, src, None)
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
