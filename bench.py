@@ -390,7 +390,7 @@ def run_gpu(args, rank, world, local_rank):
     if st["loop_mode"]:
         # the persistent loop ran: ONE launch per solve is the dominant kernel (CUDA events on the
         # launching stream around each launch); its bytes per launch = iterations x loop bytes
-        T = 1024
+        T = st["loop_threads"]
         need = -(-(-(-(N // 2) // T)) // max(st["loop_grid"], 1))
         frac = min(1.0, (st["loop_tmem_pairs"] + st["loop_smem_pairs"]) / need) if need else 1.0
         lb = loop_bytes(N, lat_k, frac)

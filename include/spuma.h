@@ -433,6 +433,7 @@ typedef struct {
        barrier's release to a CTA's arrival at the next (work) and from arrival to release (wait),
        summed over the iterations, mean over the CTAs; work_max: the slowest CTA's */
     double loop_work_ms[3], loop_wait_ms[3], loop_work_max_ms[3];
+    int loop_threads;                /* threads per CTA of the persistent loop (its tile width in cell pairs) */
 } spuma_stats;
 
 spuma_status spuma_get_stats(spuma_mesh m, spuma_stats* out);
@@ -516,10 +517,10 @@ typedef enum {
      * Bitwise the same iterates. */
     SPUMA_OPT_PEER_FUSED = 12,
     /* single-rank PCG (lattice or ELL layout, deferred psi pairs in the direction): run every
-     * iteration of a solve in ONE cooperative launch of one 1024-thread CTA per SM, three grid
+     * iteration of a solve in ONE cooperative launch of one 896-thread CTA per SM, three grid
      * barriers per iteration, each CTA finalising the scalars itself; the residual rA stays on
      * the SM: 0 = off (captured graph batches), 1 = persistent, rA in HBM, 2 = rA in shared
-     * memory (the rest in HBM), 3 = rA in tensor memory + shared memory (default; ~8.8M cells
+     * memory (the rest in HBM), 3 = rA in tensor memory + shared memory (default; ~8.5M cells
      * fully on chip on 148 SMs).  Modes 2 and 3 fall back to the graph batches when less than
      * half of rA fits on chip (meshes above ~17M cells), and any mode when the cooperative launch
      * does not fit the device.  The Amul runs over the lattice slots (variant 12) or, on other

@@ -804,6 +804,7 @@ spuma_status run_pcg_loop(spuma_mesh m, cudaStream_t s, const MeshArgs& a, int l
         }
     }
     m->stats.loop_mode = m->persistent;
+    m->stats.loop_threads = T;
     m->stats.loop_grid = G;
     m->stats.loop_tmem_pairs = tp;
     m->stats.loop_smem_pairs = sp;

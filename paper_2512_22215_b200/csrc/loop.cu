@@ -1,6 +1,6 @@
 // loop.cu -- the persistent PCG loop (SPUMA_OPT_PERSISTENT): A7-A11 of every iteration of one
 // solve (P:506-523 the PCG iteration, P:616 the per-kernel synchronisation the
-// paper's profile is dominated by) in ONE cooperative launch of one 1024-thread CTA per SM.
+// paper's profile is dominated by) in ONE cooperative launch of one 896-thread CTA per SM.
 //
 // Why: the hot loop is HBM-bound (124 B/cell per iteration over three kernels).  A kernel
 // boundary forgets everything a CTA held; a persistent CTA does not.  Each CTA owns a fixed
@@ -8,7 +8,7 @@
 // update and read again by the direction, 24 B/cell per iteration -- never leaves the SM:
 // the first pairs of every thread live in tensor memory (TMEM, 512 columns x 128 lanes x
 // 32 bit per SM, tcgen05.ld / tcgen05.st; the tensor cores themselves stay idle), the next
-// ones in shared memory, any rest in HBM (meshes above ~8.8M cells on a 148-SM B200).
+// ones in shared memory, any rest in HBM (meshes above ~8.5M cells on a 148-SM B200).
 // Per iteration: direction (C) -> grid barrier -> Amul + wA.pA (A) -> grid barrier ->
 // alpha -> update + (rD rA).rA, |rA| (B) -> grid barrier -> beta / convergence.  Every CTA
 // sums the CTA partials in the same fixed order and runs the same finalisation on its own
@@ -33,13 +33,13 @@ namespace spuma {
 namespace ploop {
 
 #ifndef SPUMA_LOOP_THREADS
-#define SPUMA_LOOP_THREADS 1024
+#define SPUMA_LOOP_THREADS 896  // same box: 135.0 (896, 72 registers) / 135.7 (1024, 64) / 141.8 (768, 80) us
 #endif
-constexpr int kT = SPUMA_LOOP_THREADS;           // threads per CTA (one CTA per SM; 1024: 64 registers)
+constexpr int kT = SPUMA_LOOP_THREADS;           // threads per CTA (one CTA per SM)
 constexpr int kWarps = kT / 32;
 constexpr int kGroups = kWarps / 4;              // warps sharing one TMEM lane quarter
 constexpr int kTmemCols = 512;
-constexpr int kColsPerThread = kTmemCols / kGroups / 4 * 4;  // 1024 threads: 64 columns = 16 double2
+constexpr int kColsPerThread = kTmemCols / kGroups / 4 * 4;  // 896 threads: 72 columns = 18 double2
 constexpr int kTmemPairs = kColsPerThread / 4;
 static_assert(kT % 128 == 0, "whole TMEM lane quarters");
 

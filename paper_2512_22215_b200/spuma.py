@@ -123,7 +123,8 @@ class Stats(ctypes.Structure):
                 ("blocks_per_grid", _ci), ("threads_per_block", _ci), ("batch_iterations", _ci),
                 ("amul_variant", _ci), ("loop_mode", _ci), ("loop_grid", _ci), ("loop_tmem_pairs", _ci),
                 ("loop_smem_pairs", _ci), ("loop_ms", _cd), ("loop_count", ctypes.c_uint64),
-                ("loop_work_ms", _cd * 3), ("loop_wait_ms", _cd * 3), ("loop_work_max_ms", _cd * 3)]
+                ("loop_work_ms", _cd * 3), ("loop_wait_ms", _cd * 3), ("loop_work_max_ms", _cd * 3),
+                ("loop_threads", _ci)]
 
     def as_dict(self):
         d = {k: getattr(self, k) for k, _ in self._fields_}

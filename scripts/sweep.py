@@ -93,7 +93,7 @@ def run_case1(name, mesh, gamma, b, ref, renumber, ctl, reps, extra, mode):
            "peak_GBps": PEAK}
     if st["loop_mode"]:  # the persistent loop ran: its own time and bytes (bench.py loop_bytes)
         import bench
-        T = 1024
+        T = st["loop_threads"]
         need = -(-(-(-(N // 2) // T)) // max(st["loop_grid"], 1))
         frac = min(1.0, (st["loop_tmem_pairs"] + st["loop_smem_pairs"]) / need) if need else 1.0
         lb = bench.loop_bytes(N, K, frac) if K else None

@@ -126,7 +126,7 @@ def test_partial_residency_beyond_on_chip_capacity():
         psi, p, s = _solve(h, diag, upper, src, ctl, mode)
         assert p["n_iterations"] == 20 and s["loop_mode"] == mode
         if mode == 3:
-            T = 1024
+            T = s["loop_threads"]
             need = -(-(-(-(m.n_cells // 2) // T)) // s["loop_grid"])
             assert s["loop_tmem_pairs"] + s["loop_smem_pairs"] < need  # some pairs in HBM
             assert s["loop_tmem_pairs"] > 0 and s["loop_smem_pairs"] > 0
