@@ -460,7 +460,8 @@ spuma_status spuma_set_batch(spuma_mesh m, int iterations);
 typedef enum {
     SPUMA_OPT_AMUL_VARIANT = 0,
     /* meshes with at most this many cells (single rank) are solved by one single-CTA
-     * kernel launch (latency path, BASELINE config 1); default 8192; 0 disables */
+     * kernel launch (latency path, BASELINE config 1); default 8192; 0 disables.  Above 3072
+     * cells the persistent loop takes precedence where it can run (SPUMA_OPT_PERSISTENT). */
     SPUMA_OPT_SMALL_SOLVE_MAX_CELLS = 1,
     /* programmatic dependent launch of the hot-loop kernels (1 = on, default; process-wide) */
     SPUMA_OPT_PDL = 2,

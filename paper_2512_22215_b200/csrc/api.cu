@@ -2027,8 +2027,12 @@ spuma_status spuma_pcg_solve(spuma_mesh m, const spuma_scalar* diag, const spuma
     SPUMA_CUDA(cudaMemcpyAsync(m->ws.ptrs, m->h_ptrs, sizeof(DevPtrs), cudaMemcpyHostToDevice, s));
     launch_scal_init(s, m->ws, *ctl, m->n_ranks);
 
-    // ---- small meshes: the whole solve in one single-CTA launch (latency path)
-    if (m->n_ranks == 1 && m->N <= m->small_max_cells && !m->timing) {
+    // ---- small meshes: the whole solve in one single-CTA launch (latency path) -- up to 3072 cells
+    // when the persistent loop could run instead (it takes ~10-11 us per iteration at any small size;
+    // one CTA 9.4 us at 2197 cells, 12.2 at 4096, 22.1 at 8000: profiles/r02ar_small_threshold_ab.jsonl)
+    constexpr int kLoopBeatsSmallCells = 3072;
+    if (m->n_ranks == 1 && m->N <= m->small_max_cells && !m->timing &&
+        (m->N <= kLoopBeatsSmallCells || !loop_layout(m, mesh_args(m)))) {
         if (!(m->small_smem && launch_pcg_single_smem(s, mesh_args(m), m->ws))) launch_pcg_single(s, mesh_args(m), m->ws);
         m->stats.kernel_launches += 2;
         DevScal fs;
