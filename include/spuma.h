@@ -537,7 +537,10 @@ typedef enum {
     /* the persistent loop records, per CTA and phase, the time from one grid barrier's release to
      * its arrival at the next (work) and the wait there (globaltimer; spuma_stats.loop_work_ms /
      * loop_wait_ms / loop_work_max_ms); 0 = off (default), 1 = on */
-    SPUMA_OPT_LOOP_PROFILE = 15
+    SPUMA_OPT_LOOP_PROFILE = 15,
+    /* CTAs of the persistent loop: 0 = automatic (default: 32 per started 16384 cells, at most
+     * one per SM), else at most this many */
+    SPUMA_OPT_LOOP_GRID = 16
 } spuma_option;
 spuma_status spuma_set_option(spuma_mesh m, int option, int value);
 

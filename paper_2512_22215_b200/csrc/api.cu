@@ -730,7 +730,11 @@ spuma_status run_pcg_loop(spuma_mesh m, cudaStream_t s, const MeshArgs& a, int l
         for (int i = 0; i < 2; ++i) SPUMA_CUDA(cudaEventCreate(&m->loop_ev[i]));
         m->loop_grid = sms;
     }
-    const int G = m->loop_grid;
+    // CTAs (SPUMA_OPT_LOOP_GRID): explicit, or 32 per started 16384 cells up to one per SM -- a
+    // few thousand cells run faster on fewer CTAs (8000 cells: 9.0 us per iteration on 32 CTAs,
+    // 11.0 on 148; 64000: 148 best; profiles/r02at_loop_grid_ab.jsonl)
+    const int G_auto = (int)std::min<long long>(m->loop_grid, 32LL * (((long long)m->N + 16383) / 16384));
+    const int G = m->loop_ctas > 0 ? std::min(m->loop_ctas, m->loop_grid) : std::max(1, G_auto);
     // rA pairs per thread: the CTA's tiles of T pairs, grid-strided
     const long long np = m->N / 2, ntile = (np + T - 1) / T;
     const int need = (int)((ntile + G - 1) / G);
@@ -755,7 +759,7 @@ spuma_status run_pcg_loop(spuma_mesh m, cudaStream_t s, const MeshArgs& a, int l
     Workspace w = m->ws;
     w.part = m->d_loop_part;
     if (m->loop_profile) {
-        if (!m->d_loop_prof) SPUMA_TRY(dalloc(&m->d_loop_prof, (size_t)8 * G));
+        if (!m->d_loop_prof) SPUMA_TRY(dalloc(&m->d_loop_prof, (size_t)8 * m->loop_grid));  // G <= SMs
         SPUMA_CUDA(cudaMemsetAsync(m->d_loop_prof, 0, sizeof(unsigned long long) * 8 * G, s));
         L.prof = m->d_loop_prof;
     }
@@ -2406,6 +2410,10 @@ spuma_status spuma_set_option(spuma_mesh m, int option, int value)
     case SPUMA_OPT_LOOP_PROFILE:
         if (value < 0 || value > 1) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "loop_profile is 0 or 1");
         m->loop_profile = value != 0;
+        return SPUMA_OK;
+    case SPUMA_OPT_LOOP_GRID:
+        if (value < 0) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "loop grid must be >= 0");
+        m->loop_ctas = value;
         return SPUMA_OK;
     case SPUMA_OPT_LOOP_L2:
         if (value < 0 || value > 4) return set_error(SPUMA_ERR_INVALID_ARGUMENT, "loop_l2 is 0..4");

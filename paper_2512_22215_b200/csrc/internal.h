@@ -275,6 +275,7 @@ struct spuma_mesh_s {
     // 3 + tensor memory (default)
     int persistent = 3;
     bool loop_profile = false;   // per-phase work / barrier-wait profile of the loop (SPUMA_OPT_LOOP_PROFILE)
+    int loop_ctas = 0;           // CTAs of the persistent loop (SPUMA_OPT_LOOP_GRID; 0 = one per SM)
     int loop_l2 = 4;             // L2 window of the persistent loop (SPUMA_OPT_LOOP_L2, targets as l2_persist): wA
     unsigned long long* d_loop_bar = nullptr;  // [2] barrier arrivals, abort word
     double* d_loop_part = nullptr;             // [3 * SMs] CTA partials

@@ -40,6 +40,7 @@ OPT_PEER_FUSED = 12
 OPT_PERSISTENT = 13
 OPT_LOOP_L2 = 14
 OPT_LOOP_PROFILE = 15
+OPT_LOOP_GRID = 16
 PEER_BLOB_BYTES = 512  # SPUMA_PEER_BLOB_BYTES
 AMUL_VARIANTS = (0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13)
 
