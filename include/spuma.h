@@ -521,7 +521,7 @@ typedef enum {
      * iteration of a solve in ONE cooperative launch of one 896-thread CTA per SM, three grid
      * barriers per iteration, each CTA finalising the scalars itself; the residual rA stays on
      * the SM: 0 = off (captured graph batches), 1 = persistent, rA in HBM, 2 = rA in shared
-     * memory (the rest in HBM), 3 = rA in tensor memory + shared memory (default; ~8.5M cells
+     * memory (the rest in HBM), 3 = rA in tensor memory + shared memory (default; ~8.2M cells
      * fully on chip on 148 SMs).  Modes 2 and 3 fall back to the graph batches when less than
      * half of rA fits on chip (meshes above ~17M cells), and any mode when the cooperative launch
      * does not fit the device.  The Amul runs over the lattice slots (variant 12) or, on other

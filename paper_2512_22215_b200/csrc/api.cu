@@ -739,7 +739,9 @@ spuma_status run_pcg_loop(spuma_mesh m, cudaStream_t s, const MeshArgs& a, int l
     const long long np = m->N / 2, ntile = (np + T - 1) / T;
     const int need = (int)((ntile + G - 1) / G);
     int tp = m->persistent >= 3 ? std::min(need, loop_tmem_pairs()) : 0;
-    const int sp_cap = (200 * 1024) / (T * (int)sizeof(double2));  // <= 200 KB of shared memory
+    // <= 186 KB of shared memory: the rest of the SM's 256 KB stays L1 for the Amul's pA windows
+    // (896 threads with 14 pairs = 201 KB: 252^3 413 vs 303 us per iteration, profiles/r02av_*)
+    const int sp_cap = (186 * 1024) / (T * (int)sizeof(double2));
     int sp = m->persistent >= 2 ? std::min(need - tp, sp_cap) : 0;
     // less than half of rA on chip: the graph batches are as fast or faster (C4 64M cells, 13 % on
     // chip: 1695 vs 1571 us per iteration; 252^3, 52 %: loop 312 vs 321 us, profiles/r02y_*)

@@ -8,7 +8,7 @@
 // update and read again by the direction, 24 B/cell per iteration -- never leaves the SM:
 // the first pairs of every thread live in tensor memory (TMEM, 512 columns x 128 lanes x
 // 32 bit per SM, tcgen05.ld / tcgen05.st; the tensor cores themselves stay idle), the next
-// ones in shared memory, any rest in HBM (meshes above ~8.5M cells on a 148-SM B200).
+// ones in shared memory, any rest in HBM (meshes above ~8.2M cells on a 148-SM B200).
 // Per iteration: direction (C) -> grid barrier -> Amul + wA.pA (A) -> grid barrier ->
 // alpha -> update + (rD rA).rA, |rA| (B) -> grid barrier -> beta / convergence.  Every CTA
 // sums the CTA partials in the same fixed order and runs the same finalisation on its own
