@@ -285,3 +285,19 @@ def test_loop_sweep_direction_option(alt):
     assert s["loop_mode"] == 3 and p["n_iterations"] == p0["n_iterations"]
     assert np.linalg.norm(psi - psi0) / np.linalg.norm(psi0) <= 1e-12
     h.free()
+
+
+@pytest.mark.parametrize("ctas", [1, 2, 7, 32, 0])
+def test_loop_grid_option(ctas):
+    """SPUMA_OPT_LOOP_GRID: the loop on 1..32 CTAs (0 = automatic) -- the same element arithmetic,
+    another partial-sum shape: the graph batches' iteration count and psi within 1e-12."""
+    m = gen.cube(24)
+    h, diag, upper, src = _assembled(m)
+    ctl = (1e-8, 0.0, 5000, 0)
+    psi0, p0, _ = _solve(h, diag, upper, src, ctl, 0)
+    h.set_option(OPT.OPT_LOOP_GRID, ctas)
+    psi, p, s = _solve(h, diag, upper, src, ctl, 3)
+    assert s["loop_mode"] == 3 and (ctas == 0 or s["loop_grid"] == ctas), s
+    assert p["n_iterations"] == p0["n_iterations"]
+    assert np.linalg.norm(psi - psi0) / np.linalg.norm(psi0) <= 1e-12
+    h.free()
