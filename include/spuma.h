@@ -517,7 +517,7 @@ typedef enum {
      * last CTA (4 kernels per iteration instead of 7); 1 = on (default), 0 = separate kernels.
      * Bitwise the same iterates. */
     SPUMA_OPT_PEER_FUSED = 12,
-    /* single-rank PCG (lattice or ELL layout, deferred psi pairs in the direction): run every
+    /* single-rank PCG (lattice, ELL or SELL-C layout, deferred psi pairs in the direction): run every
      * iteration of a solve in ONE cooperative launch of one 896-thread CTA per SM, three grid
      * barriers per iteration, each CTA finalising the scalars itself; the residual rA stays on
      * the SM: 0 = off (captured graph batches), 1 = persistent, rA in HBM, 2 = rA in shared
@@ -525,7 +525,9 @@ typedef enum {
      * fully on chip on 148 SMs).  Modes 2 and 3 fall back to the graph batches when less than
      * half of rA fits on chip (meshes above ~17M cells), and any mode when the cooperative launch
      * does not fit the device.  The Amul runs over the lattice slots (variant 12) or, on other
-     * meshes, over the ELL rows (variant 8/10 layout).  Same element arithmetic as the graph
+     * meshes, over the ELL rows (variant 8/10 layout) or the SELL-C rows (variant 6).  Above
+     * SPUMA_OPT_SMALL_SOLVE_MAX_CELLS's 3072-cell cut it also replaces the single-CTA solve.  Same
+     * element arithmetic as the graph
      * path; the dot products are summed in another fixed shape (iterates equal to rounding,
      * deterministic). */
     SPUMA_OPT_PERSISTENT = 13,
