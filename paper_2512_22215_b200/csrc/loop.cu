@@ -419,12 +419,23 @@ __global__ void __launch_bounds__(kT, 1) k_pcg_loop(MeshArgs a, Workspace w, Loo
                 }
                 if (k < kon || i < np) R.store(k, i, r);  // on-chip: every lane (TMEM stores are warp-collective)
             };
-            double2 wn = make_double2(0.0, 0.0), dn = wn, rn = wn;
-            if (nk > 0) pf(0, wn, dn, rn);
-            for (int j = 0; j < nk; ++j) {
-                const double2 ww = wn, d = dn, rh = rn;
-                if (j + 1 < nk) pf(j + 1, wn, dn, rn);
-                body(j, ww, d, rh);
+            // two tiles ahead: slots 0 / 1 hold the loads of tiles j and j + 1 while tile j - 1
+            // computes (896 threads: 134.4 vs 135.0 us per iteration for one ahead, same box,
+            // profiles/r02bi_*; at 1024 threads / 64 registers it had not paid, r02ah_*)
+            double2 w0 = make_double2(0.0, 0.0), d0 = w0, r0 = w0, w1 = w0, d1 = w0, r1 = w0;
+            if (nk > 0) pf(0, w0, d0, r0);
+            if (nk > 1) pf(1, w1, d1, r1);
+            for (int j = 0; j < nk; j += 2) {
+                {
+                    const double2 ww = w0, d = d0, rh = r0;
+                    if (j + 2 < nk) pf(j + 2, w0, d0, r0);
+                    body(j, ww, d, rh);
+                }
+                if (j + 1 < nk) {
+                    const double2 ww = w1, d = d1, rh = r1;
+                    if (j + 3 < nk) pf(j + 3, w1, d1, r1);
+                    body(j + 1, ww, d, rh);
+                }
             }
             if ((N & 1) && b == 0 && t == 0) {
                 const int c = N - 1;
