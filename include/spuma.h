@@ -532,9 +532,9 @@ typedef enum {
      * deterministic). */
     SPUMA_OPT_PERSISTENT = 13,
     /* the persistent loop's L2 access-policy window (persisting hits), targets as
-     * SPUMA_OPT_L2_PERSIST: 0 = none, 1 = pA, 2 = rA, 3 = rD, 4 = wA (default).  Same-box A/B at
-     * 200^3 (profiles/r02r_loop_ab.txt): 149.0 / 143.5 / 146.6 / 143.5 us per iteration for
-     * none / pA / rD / wA; the graph batches with their rA window 153.2 us. */
+     * SPUMA_OPT_L2_PERSIST: 0 = none, 1 = pA (default), 2 = rA, 3 = rD, 4 = wA.  Same-box A/B at
+     * 200^3 with the final loop (profiles/r02bk_*, r02bl_*): 155.7 / 137.0 / 142.4 / 138.3 us per
+     * iteration for none / pA / rD / wA (pA also ahead at 126^3 and 159^3). */
     SPUMA_OPT_LOOP_L2 = 14,
     /* the persistent loop records, per CTA and phase, the time from one grid barrier's release to
      * its arrival at the next (work) and the wait there (globaltimer; spuma_stats.loop_work_ms /

@@ -276,7 +276,7 @@ struct spuma_mesh_s {
     int persistent = 3;
     bool loop_profile = false;   // per-phase work / barrier-wait profile of the loop (SPUMA_OPT_LOOP_PROFILE)
     int loop_ctas = 0;           // CTAs of the persistent loop (SPUMA_OPT_LOOP_GRID; 0 = one per SM)
-    int loop_l2 = 4;             // L2 window of the persistent loop (SPUMA_OPT_LOOP_L2, targets as l2_persist): wA
+    int loop_l2 = 1;             // L2 window of the persistent loop (SPUMA_OPT_LOOP_L2, targets as l2_persist): pA
     unsigned long long* d_loop_bar = nullptr;  // [2] barrier arrivals, abort word
     double* d_loop_part = nullptr;             // [3 * SMs] CTA partials
     unsigned long long* d_loop_prof = nullptr; // [8 * SMs] phase work / wait ns (timing on)
